@@ -1,0 +1,332 @@
+"""Benchmark: OFRR top-k eigenpairs, time-to-tolerance on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3]
+
+Workload (default, every N): BASELINE configs[1] / SURVEY.md 8 "C2": synthetic dense
+symmetric 16384 x 16384 with geometric spectrum (rho = 0.1^(1/(k-top+1))), top-32
+eigenpairs, k = 64, bf16 basis (tensor-core policy: bf16 storage, fp32 products/sums),
+fp64 Grams and pencil, hess-l + ofrr, tolerance 1e-2 on the FP64 relative residual
+(the bf16 tolerance of SURVEY.md 8(d)).  One step = one complete solve from X0 until the
+leading `top` residuals are below tol.  A is generated on the device (K8) and is HBM
+resident before the timed region (512 MiB > 126 MB L2, so no L2 flush is needed).
+
+N > 1 (torchrun): A is row-partitioned, each rank generates its own rows; time is the
+max over ranks; the problem size is fixed ("strong" scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 20240901
+CONFIGS = {
+    "c2": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-2,
+               name="synthetic dense symmetric 16384x16384, geometric spectrum, top-32, k=64, "
+                    "bf16 basis / fp64 Gram (BASELINE configs[1])"),
+    "c3": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-2,
+               name="synthetic dense symmetric 65536x65536, geometric spectrum, top-64, k=128, "
+                    "bf16 basis / fp64 Gram (BASELINE configs[2], bf16 rung)"),
+}
+MAX_OUTER = 60
+# A passes per C2 solve measured on the B200 (used by the reference arm, which never
+# touches a GPU, to extrapolate its per-pass time to a full solve)
+C2_PASSES_TO_TOL = 10
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------
+# reference arm / CPU baseline: the reference's compiled gemm_mixed (oracle/_ref) on the
+# host cores, a bounded row sample of the same A pass, extrapolated to a full solve
+# ------------------------------------------------------------------------------------
+def cpu_reference_pass_time(cfg, target_s: float = 5.0, threads: int = 0):
+    """Seconds for one C2 A pass (n x n bf16-valued A times n x k X) by the reference's
+    compiled kernel (oracle/_ref, built from /root/reference's own _kernels.pyx), measured
+    on a row sample spread over all host cores and scaled to n rows."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from concurrent.futures import ThreadPoolExecutor
+    kind = "reference"
+    try:
+        import build_ref
+        kern = build_ref.load()
+        gemm = kern.gemm_mixed
+    except Exception:
+        import oracle
+        kind = "port"
+
+        def gemm(a, b, c, acc, out):
+            return oracle.mixed_gemm(a, b, c, acc, out)
+    import oracle
+    n, k = cfg["n"], cfg["k"]
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(SEED)
+    x = oracle.round_to(rng.random((n, k)), oracle.BF16)
+    # calibrate: time a few rows on one core
+    rows_cal = 4
+    a_cal = oracle.round_to(rng.standard_normal((rows_cal, n)) * 1e-3, oracle.BF16)
+    t0 = time.perf_counter()
+    gemm(a_cal, x, 1, 1, 1)
+    per_row = (time.perf_counter() - t0) / rows_cal
+    rows_per_thread = max(1, int(target_s / max(per_row, 1e-9)))
+    a = oracle.round_to(rng.standard_normal((rows_per_thread, n)) * 1e-3, oracle.BF16)
+
+    def work(_):
+        gemm(a, x, 1, 1, 1)   # F32 products (exact for bf16 values), F32 sums
+        return None
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
+    dt = time.perf_counter() - t0
+    rows_done = rows_per_thread * threads
+    pass_s = dt * n / rows_done
+    sample = (f"{rows_done} rows x {n} cols x k={k} of one A pass (gemm_mixed F32/F32, bf16-valued A) on "
+              f"{threads} threads in {dt:.1f} s; per-pass time scaled to n={n} rows")
+    return pass_s, threads, kind, sample
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference's CPU path on the box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per_step = []
+    kind = sample = None
+    threads = 1
+    for i in range(args.warmup + args.steps):
+        pass_s, threads, kind, sample = cpu_reference_pass_time(cfg, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            per_step.append(pass_s * C2_PASSES_TO_TOL)
+    v = float(np.mean(per_step))
+    line = {
+        "impl": "reference", "metric": "OFRR top-k eig time-to-tol", "value": v, "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32 (bf16-valued)",
+        "data": "synthetic", "config": {"workload": cfg["name"], "n": cfg["n"], "top": cfg["top"], "k": cfg["k"],
+                                        "tol": cfg["tol"], "a_passes_per_solve": C2_PASSES_TO_TOL},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": kind,
+                         "sample": sample + f"; x {C2_PASSES_TO_TOL} A passes per solve (94% of the "
+                                            "reference's time is in these passes, SURVEY.md 0.3)"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    import paper_2505_00281_b200 as p
+    from paper_2505_00281_b200 import ops
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = p.Comm.world()
+    n, top, k, tol = cfg["n"], cfg["top"], cfg["k"], cfg["tol"]
+    fmt = p.FpFormat[cfg["fmt"]]
+    lam = p.geometric_spectrum(n, top, k)
+    r0, r1 = comm.row_range(n)
+    A, _ = p.synthetic_symmetric(lam, fmt, seed=SEED, device=dev, row0=r0, rows=r1 - r0)
+    icfg = p.IterConfig(k=k, m=MAX_OUTER, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                        policy=p.TC_BF16 if fmt == p.FpFormat.BF16 else p.POLICY_PRESETS["tc-f16"],
+                        seed=SEED, tol=tol, top=top)
+
+    def solve(stats=None):
+        return p.subspace_iter_eig(A, icfg, stats=stats, comm=comm, n_global=n)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        solve()
+    barrier()
+    # ---- timed region: K solves, CUDA events on the launching stream -------------
+    ops.GEMM_EVENTS = []
+    ops.LAUNCHES[0] = 0
+    stats = p.RunStats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            rs = solve(stats)
+        e1.record()
+        barrier()
+    launches = ops.LAUNCHES[0]
+    ms_total = e0.elapsed_time(e1)
+    gem = ops.GEMM_EVENTS
+    ops.GEMM_EVENTS = None
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    # dominant kernel (K1 block product): algorithmic bytes / average launch duration
+    durs = [a.elapsed_time(b) for a, b, _, _ in gem]
+    nbytes = float(np.mean([nb for _, _, nb, _ in gem]))
+    flops = float(np.mean([fl for _, _, _, fl in gem]))
+    avg_ms = float(np.mean(durs))
+    hbm, bf16_peak, peak_kind = _peaks()
+    achieved = nbytes / (avg_ms * 1e-3) / 1e9
+    gemm_share = float(np.sum(durs)) / ms_total if ms_total > 0 else None
+
+    # ---- e2e: public API with HOST buffers (A from pinned host memory, results back) --
+    e2e = None
+    if world == 1:
+        a_host = A.device_operator(fmt).t[:, :n].to("cpu").pin_memory()
+        del_ok = True
+        times = []
+        h2d = d2h = 0
+        for i in range(max(1, min(3, args.steps)) + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            Ah = p.DenseMatrix(a_host, fmt)               # host buffer in the storage format
+            rsh = p.subspace_iter_eig(Ah, icfg)
+            vals = np.asarray(rsh.values)                 # host result
+            vecs = rsh.vectors.data                       # D2H of the FP64 Ritz vectors
+            torch.cuda.synchronize()
+            if i > 0:
+                times.append(time.perf_counter() - t0)
+            h2d = a_host.numel() * a_host.element_size() + n * k * 8
+            d2h = vals.nbytes + vecs.nbytes + rsh.residuals.nbytes
+            Ah.release_device()
+            del Ah, rsh
+        e2e = {"value": float(np.median(times)), "unit": "s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        pass_s, threads, kind, sample = cpu_reference_pass_time(cfg, target_s=args.ref_seconds)
+        passes = stats.a_passes / args.steps
+        cpu = {"value": pass_s * passes, "unit": "s", "cores": threads, "kind": kind,
+               "sample": sample + f"; x {passes:.0f} A passes per solve (this run's count)"}
+    line = {
+        "metric": "OFRR top-k eig time-to-tol", "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg["name"], "n": n, "top": top, "k": k, "tol": tol,
+                   "outer_iterations_per_solve": stats.iterations and stats.iterations,
+                   "a_passes_per_solve": stats.a_passes / args.steps,
+                   "converged": bool(stats.converged),
+                   "max_residual_top": float(np.max(rs.residuals[:top])),
+                   "parallelism": f"row-partitioned x{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (A = %d MiB per GPU)" % ((r1 - r0) * n * 2 >> 20)},
+        "roofline": {"kernel": "k_gemm_av_tc + k_finalize (K1, A.X block product)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "peak_kind": peak_kind, "traffic": None, "bytes_per_launch": nbytes,
+                     "avg_launch_ms": avg_ms, "launches": len(durs), "share_of_step": gemm_share,
+                     "tflops": flops / (avg_ms * 1e-3) / 1e12, "tflops_peak_bf16": bf16_peak},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--ref-seconds", type=float, default=5.0, help="CPU seconds per reference sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * ofrr_b200.h -- C ABI of libofrr_b200.so, the B200 (sm_100a) OFRR hot path.
+ *
+ * Drop-in boundary for the reference's kernel plugin slot (`ofrr.backend.kernels`,
+ * /root/reference/pkg/src/ofrr/backend.py:14-22) and for the device-resident driver
+ * steps of ofrr/driver.py:84-173.  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *  - Format codes follow ofrr/precision.py:20-25 (F16=0, F32=1, F64=2) and extend them
+ *    with BF16=3, FP8_E4M3=4.
+ *  - "Device" entry points take device pointers and an explicit cudaStream_t (passed as
+ *    void*; NULL = legacy default stream).  They enqueue work and return immediately.
+ *  - Matrices: A is row-major (rows x cols, leading dimension lda in elements); blocks
+ *    X/W/U/Q are column-major (n x k, leading dimension ld >= n), i.e. the reference's
+ *    Fortran order (ofrr/matrix.py:25-31).
+ *  - Every call returns an ofrr status (0 = OK).  Errors map 1:1 onto the reference's
+ *    exceptions (see OFRR_ERR_*); ofrr_last_error() gives the message.
+ *  - The library never frees caller memory.  Workspaces are caller-owned; the
+ *    *_workspace() queries give their sizes in bytes.
+ *  - Thread safety: entry points are re-entrant; concurrent calls must use distinct
+ *    workspaces (the reference's CLI calls drivers from a thread pool,
+ *    ofrr/cli.py:399-401).
+ */
+#ifndef OFRR_B200_H
+#define OFRR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* formats: ofrr/precision.py:20-25 (+ extensions) */
+#define OFRR_F16 0
+#define OFRR_F32 1
+#define OFRR_F64 2
+#define OFRR_BF16 3
+#define OFRR_FP8E4M3 4
+
+/* status codes */
+#define OFRR_OK 0
+#define OFRR_ERR_INVALID 1      /* ValueError (argument validation) */
+#define OFRR_ERR_CUDA 2         /* CUDA runtime failure */
+#define OFRR_ERR_OVERFLOW 3     /* OverflowDiagnostic: ofrr/projection.py:24-25, driver.py:73-75 */
+#define OFRR_ERR_EMPTY_BASIS 4  /* EmptyBasisError: ofrr/basis.py:41-42 */
+#define OFRR_ERR_EMPTY_PENCIL 5 /* EmptyPencilError: ofrr/projection.py:28-29 */
+#define OFRR_ERR_CONVERGENCE 6  /* ConvergenceError: ofrr/smallsolve.py:20-25 */
+#define OFRR_ERR_UNSUPPORTED 7  /* format / shape combination this build does not run */
+
+/* device-side flag bits written by kernels (int32, OR-ed) */
+#define OFRR_FLAG_NONFINITE 1
+#define OFRR_FLAG_NOCONV 2
+#define OFRR_FLAG_INEXACT 4 /* ofrr_transpose_convert: some value was not representable */
+
+int ofrr_abi_version(void);
+const char* ofrr_last_error(void);
+int ofrr_device_sm_count(int device);
+
+/* ---------------------------------------------------------------------------------
+ * K1: block product W = A * X  (or A^T * X when transpose != 0)
+ * Replaces ofrr/matrix.py:242-254 apply_dense -> ofrr/precision.py:122-135 mixed_gemm
+ *          -> ofrr/_kernels.pyx:60-84 gemm_mixed.
+ * A: rows x cols row-major, format a_fmt (BF16/F16: tcgen05 tensor cores, fp32 TMEM
+ *    accumulation; FP8E4M3: tcgen05 kind::f8f6f4; F32/F64: CUDA-core FMA).
+ * X: (transpose ? rows : cols) x k column-major, same format as A.
+ * W: (transpose ? cols : rows) x k column-major, rounded to out_fmt.
+ * colmax (device double[k], may be NULL): max |W[:,j]| after rounding (for the inf-norm
+ *    column scaling, ofrr/precision.py:159-169).  flags (device int, may be NULL):
+ *    OR-ed with OFRR_FLAG_NONFINITE when W has non-finite entries
+ *    (ofrr/driver.py:73-75).  Deterministic: fixed-order split-K reduction.
+ * ------------------------------------------------------------------------------- */
+size_t ofrr_gemm_av_workspace(int64_t rows, int64_t cols, int k, int a_fmt, int transpose);
+int ofrr_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose,
+                 const void* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt,
+                 double* colmax, int* flags, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* K2: X[:,j] <- round_s(round_c(X[:,j] / colmax[j])) for colmax[j] != 0, in place.
+ * Replaces ofrr/precision.py:159-169 scale_columns_inf. */
+int ofrr_scale_columns(void* X, int64_t n, int k, int64_t ldx, int storage, int compute,
+                       const double* colmax, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * K3: Hessenberg (LU with partial pivoting) basis of X (n x k, format `storage`).
+ * Replaces ofrr/basis.py:151-204 hessenberg_basis (layouts "left"/"right" give the
+ * identical update sequence, tests/test_basis.py:92-98).  Arithmetic follows the
+ * reference exactly: axpy in the compute format rounded to storage
+ * (ofrr/precision.py:172-180), pivot = largest |v| over non-pivot rows, lowest index
+ * on ties (ofrr/basis.py:199-204), columns with |pivot| < tol are skipped.
+ * Outputs (device): Q (n x k, kept columns compacted to the front, ldq),
+ * pivots (int64[k], first n_kept valid), kept (int32[k] 0/1), n_kept (int32 scalar).
+ * ------------------------------------------------------------------------------- */
+size_t ofrr_hessenberg_workspace(int64_t n, int k, int storage);
+int ofrr_hessenberg(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute,
+                    double tol, void* Q, int64_t ldq, int64_t* pivots, int* kept, int* n_kept,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * K4: Grams G1 = U^T W and G2 = U^T U (k x k each, column-major fp64 outputs, values
+ * rounded to out_fmt: F32 for F16 storage, F64 otherwise -- ofrr/projection.py:42-53).
+ * Replaces ofrr/projection.py:56-61 _project (x2 in ofrr_eig, :79-80).  W may be NULL
+ * (only G2 is formed) and G2 may be NULL.  Products are exact (storage formats of
+ * <= 24 significant bits multiply exactly in fp64), sums in fp64 with a
+ * fixed-order two-stage reduction.  `k` columns of U, `kw` columns of W.
+ * ------------------------------------------------------------------------------- */
+size_t ofrr_gram_workspace(int64_t n, int k, int kw);
+int ofrr_gram(const void* U, int64_t ldu, const void* W, int64_t ldw, int64_t n, int k, int kw,
+              int storage, int out_fmt, double* G1, double* G2, int* flags, void* workspace,
+              size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * K5: symmetric-definite pencil B y = lambda M y in fp64 (k x k, column-major).
+ * Replaces ofrr/smallsolve.py:64-88 sym_def_gen_eig (with sym_eig :34-49 and the
+ * Jacobi kernel ofrr/_kernels.pyx:105-150): symmetrize, eig(M), keep
+ * mu > k*eps*mu_max, T = D^-1/2 P^T B P D^-1/2, eig(T), y = P D^-1/2 Z, sort
+ * descending (stable) with the largest-|entry|-positive sign rule.
+ * Outputs: values (fp64[k], first *n_out valid), vectors (k x k col-major, first
+ * *n_out columns valid), n_out (device int32), status (device int32:
+ * 0 ok, OFRR_ERR_CONVERGENCE, OFRR_ERR_EMPTY_PENCIL when nothing is retained).
+ * sym_eig alone: ofrr_sym_eig (same sort/sign rules).
+ * ------------------------------------------------------------------------------- */
+size_t ofrr_small_eig_workspace(int k);
+int ofrr_sym_def_gen_eig(const double* B, const double* M, int k, double* values,
+                         double* vectors, int* n_out, int* status, void* workspace,
+                         size_t workspace_bytes, void* stream);
+int ofrr_sym_eig(const double* S, int k, double* values, double* vectors, int* status,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * K6: Ritz recovery  Ut = scale * U * Y[:, :r]  (n x k' times k' x r, fp64 math).
+ * Replaces ofrr/projection.py:86 (u.data @ eig.vectors) and :129-130 (sqrt(2)*U*Y),
+ * fused with ofrr/driver.py:109 round_to(..., mv.storage).
+ * r_dev (device int32, may be NULL -> r_max) gives the number of valid columns.
+ * Outputs (either may be NULL): Ut64 (n x r_max fp64, ldo64), Xout (n x r_max in
+ * x_fmt, ldx; columns >= r are zero-filled), flags |= NONFINITE on Xout.
+ * ------------------------------------------------------------------------------- */
+int ofrr_ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const double* Y,
+                      int ldy, const int* r_dev, int r_max, double scale, double* Ut64,
+                      int64_t ldo64, void* Xout, int64_t ldx, int x_fmt, int* flags,
+                      void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * K7: FP64 residuals  res[j] = || A v_j - lambda_j v_j ||_2 / |lambda_j|  (inf when
+ * lambda_j == 0).  Replaces ofrr/projection.py:136-147 residual_report (eig branch).
+ * A (rows x cols row-major, a_fmt) is promoted to fp64 exactly.  For the SVD branch
+ * (:148-157) call twice: ofrr_residual_pair with (A, V, U) and (A^T, U, V).
+ * ofrr_residual_pair: res[j] = max(res[j], ||op(A) x_j - s_j y_j|| / s_j).
+ * ------------------------------------------------------------------------------- */
+size_t ofrr_residual_workspace(int64_t rows, int r);
+int ofrr_residual_eig(const void* A, int64_t n, int64_t lda, int a_fmt, const double* V,
+                      int64_t ldv, const double* vals, const int* r_dev, int r_max, double* res,
+                      void* workspace, size_t workspace_bytes, void* stream);
+int ofrr_residual_pair(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
+                       int transpose, const double* Xv, int64_t ldx, const double* Yv,
+                       int64_t ldy, const double* vals, const int* r_dev, int r_max,
+                       double* res, int accumulate_max, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * K8: synthetic symmetric matrix A = S C S + Wf Mf^T + Mf Wf^T (FP64, rounded once to
+ * a_fmt, row-major), where C[i,j] = c[i xor j] (n a power of two; Walsh-Hadamard
+ * diagonalisation) or C = diag(c) otherwise.  Row block [row0, row0+rows).
+ * The host computes c, s, Wf, Mf (ofrr_b200/matrix.py); the device evaluates the
+ * elementwise formula in a fixed order, so the oracle reproduces it bit for bit.
+ * ------------------------------------------------------------------------------- */
+int ofrr_generate_sym(int64_t n, int64_t row0, int64_t rows, int hadamard, const double* c,
+                      const double* s, const double* Wf, const double* Mf, int r, void* A,
+                      int64_t lda, int a_fmt, void* stream);
+
+/* utility: round/convert a column-major block between formats (ofrr/precision.py:90-104) */
+int ofrr_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int dst_fmt,
+                 int64_t ld_dst, int64_t n, int64_t k, int* flags, void* stream);
+
+/* utility: dst (row-major rows x cols) <- round(src (column-major rows x cols)); uploads the
+ * reference's F-order operators (ofrr/matrix.py:25-31) into the row-major device layout */
+int ofrr_transpose_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int dst_fmt,
+                           int64_t ld_dst, int64_t rows, int64_t cols, int* flags, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Host-buffer plugin entry points: the exact signatures of the reference's kernel
+ * module (ofrr/_kernels.pyx) so `ofrr.backend.kernels` can bind them.
+ * Host float64 in, host float64 out; copies run inside the call.
+ * ------------------------------------------------------------------------------- */
+/* ofrr/_kernels.pyx:60-84 gemm_mixed(a, b, compute, accumulate, out_fmt): a is m x k
+ * with element strides (ars, acs), b is k x n with (brs, bcs), c is m x n F-order.
+ * The device computes with exact products (tensor cores for 16-bit values) and fp32
+ * (F16/BF16/F32 accumulate) or fp64 accumulation. */
+int ofrr_host_gemm_mixed(const double* a, int64_t ars, int64_t acs, const double* b,
+                         int64_t brs, int64_t bcs, int64_t m, int64_t k, int64_t n, int compute,
+                         int accumulate, int out_fmt, double* c);
+/* ofrr/_kernels.pyx:105-150 jacobi_eig(a, max_sweeps, tol) -> (vals, vecs, sweeps, off)
+ * a: n x n row-major; vals[n]; vecs n x n row-major (vecs[i*n+p] = V[i,p]). */
+int ofrr_host_jacobi_eig(const double* a, int64_t n, int max_sweeps, double tol, double* vals,
+                         double* vecs, int* sweeps, double* off);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OFRR_B200_H */

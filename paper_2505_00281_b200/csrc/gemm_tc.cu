@@ -1,0 +1,354 @@
+// gemm_tc.cu -- K1: W = A * X on the 5th-generation tensor cores (tcgen05 + TMA + TMEM).
+//
+// Replaces the reference's A.V pass: ofrr/matrix.py:242-254 (apply_dense) ->
+// ofrr/precision.py:122-135 (mixed_gemm) -> ofrr/_kernels.pyx:60-84 (gemm_mixed).
+//
+// Shape: A is rows x cols row-major (K-major for the MMA), X is cols x k column-major
+// (K-major B operand), k <= 256.  A is streamed exactly once from HBM; the X panel
+// (n x k, a few MB) is re-read from L2 by every CTA.
+//
+// Design (one CTA per SM, persistent, stream-K):
+//   * tile = 256 rows x BN (BN = k rounded up to 32/64/128/256), two M=128 UMMAs
+//     per K-step share the B (X) tile, halving L2 traffic for X.
+//   * BLOCK_K = 128 bytes (64 bf16/f16, 128 e4m3) so every smem row is one
+//     128B-swizzle atom; 4 UMMAs (32 bytes of K each) per stage.
+//   * the flattened (tile, k-block) iteration space is split evenly over the grid
+//     (stream-K), so all 148 SMs stream A for the whole kernel; each (tile, CTA)
+//     segment is written as an fp32 partial, and k_finalize sums the partials of a
+//     tile in ascending CTA order (deterministic), rounds to the storage format,
+//     and produces the per-column inf-norms for the column scaling (K2).
+//   * warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (+ TMEM owner),
+//     warps 2..5 = epilogue (TMEM -> registers -> fp32 partials, coalesced).
+#include "common.cuh"
+#include <algorithm>
+#include <mutex>
+
+namespace ofrr {
+
+static constexpr int TILE_M = 256;          // rows per tile (2 x UMMA_M=128)
+static constexpr int KBYTES = 128;          // bytes of K per stage (one SW128 atom row)
+static constexpr int A_STAGE = TILE_M * KBYTES;  // 32 KB
+static constexpr int SMEM_BUDGET = 200 * 1024;
+static constexpr int THREADS = 192;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int B_STAGE = BN * KBYTES;
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : (2 * BN);   // power of two for BN in {16..256}
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + 256;
+};
+
+// Instruction descriptor (kind::f16 / kind::f8f6f4): c_format=F32 (bits 4-5), a/b formats
+// (bits 7-9 / 10-12), K-major A and B, N>>3 (bits 17-22), M>>4 (bits 24-28).
+static inline uint32_t make_idesc(int a_fmt, int n) {
+  uint32_t ab = (a_fmt == BF16) ? 1u : 0u;  // F16 = 0, BF16 = 1; E4M3 = 0 for f8f6f4
+  return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+struct Segments {
+  long long it0, it1;
+  int kblocks;
+};
+
+template <int BN, bool FP8K>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_av_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
+                 float* __restrict__ ws, int kblocks, long long total_iters, int max_slots,
+                 uint32_t idesc) {
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long G = gridDim.x;
+  const long long it0 = (long long)blockIdx.x * total_iters / G;
+  const long long it1 = ((long long)blockIdx.x + 1) * total_iters / G;
+  const int t_first = (int)(it0 / kblocks);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_barrier_init();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmX);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      const uint64_t pol_a = policy_evict_first(), pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long it = it0; it < it1; ++it) {
+        const int t = (int)(it / kblocks), kb = (int)(it % kblocks);
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::STAGE;
+        mbar_expect_tx(&full[stage], C::STAGE);
+        const int kcoord = FP8K ? kb * 128 : kb * 64;
+        tma_load_2d(sa, &tmA, kcoord, t * TILE_M, &full[stage], pol_a);
+        tma_load_2d(sa + A_STAGE, &tmX, kcoord, 0, &full[stage], pol_x);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer (single thread) =====
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      long long it = it0;
+      while (it < it1) {
+        const int kb0 = (int)(it % kblocks);
+        const int kb1 = (int)std::min<long long>(kblocks, kb0 + (it1 - it));
+        mbar_wait(tempty, acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE);
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + A_STAGE);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              // +32 B of K per step (>>4 = 2); second M half starts 128 rows (16 KB) later
+              const uint64_t a = da + (uint64_t)(k * 2 + h * (16384 >> 4));
+              const uint64_t b = db + (uint64_t)(k * 2);
+              if (FP8K) mma_f8(tmem + h * BN, a, b, idesc, acc);
+              else mma_f16(tmem + h * BN, a, b, idesc, acc);
+            }
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(tfull);
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5: TMEM -> fp32 partial tiles (column-major 256 x BN) =====
+    const int q = warp & 3;                // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;         // row within the 128-row accumulator
+    uint32_t acc_phase = 0;
+    long long it = it0;
+    while (it < it1) {
+      const int t = (int)(it / kblocks);
+      const int kb0 = (int)(it % kblocks);
+      const int kb1 = (int)std::min<long long>(kblocks, kb0 + (it1 - it));
+      it += kb1 - kb0;
+      mbar_wait(tfull, acc_phase);
+      tc_fence_after();
+      float* dst = ws + ((size_t)blockIdx.x * max_slots + (t - t_first)) * (size_t)(TILE_M * BN);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + h * BN + c0, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) dst[(size_t)(c0 + i) * TILE_M + h * 128 + row] = v[i];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+      acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// Sum the stream-K partials of one 256-row tile in ascending CTA order, round to the
+// output format, write W (column-major) and the per-column inf-norm.
+__device__ __forceinline__ long long seg_begin(long long c, long long T, long long G) { return c * T / G; }
+
+static constexpr int FIN_COLS = 8;   // columns per finalize block
+
+__global__ void __launch_bounds__(256)
+    k_finalize(const float* __restrict__ ws, int BN, int kblocks, long long total_iters, int G,
+               int max_slots, int64_t rows, int k, void* __restrict__ W, int64_t ldw, int out_fmt,
+               double* __restrict__ colmax, int* __restrict__ flags) {
+  __shared__ float smax[8][FIN_COLS];
+  const int t = blockIdx.x;
+  const int j0 = blockIdx.y * FIN_COLS;
+  const int row = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long x0 = (long long)t * kblocks, x1 = x0 + kblocks - 1;
+  // CTA owning iteration x: largest c with seg_begin(c) <= x
+  long long c_lo = x0 * G / total_iters, c_hi = x1 * G / total_iters;
+  while (c_lo + 1 < G && seg_begin(c_lo + 1, total_iters, G) <= x0) ++c_lo;
+  while (c_lo > 0 && seg_begin(c_lo, total_iters, G) > x0) --c_lo;
+  while (c_hi + 1 < G && seg_begin(c_hi + 1, total_iters, G) <= x1) ++c_hi;
+  while (c_hi > 0 && seg_begin(c_hi, total_iters, G) > x1) --c_hi;
+  const int64_t grow = (int64_t)t * TILE_M + row;
+  const bool valid = grow < rows;
+  float s[FIN_COLS];
+#pragma unroll
+  for (int i = 0; i < FIN_COLS; ++i) s[i] = 0.f;
+  for (long long c = c_lo; c <= c_hi; ++c) {
+    const int slot = t - (int)(seg_begin(c, total_iters, G) / kblocks);
+    const float* src = ws + ((size_t)c * max_slots + slot) * (size_t)(TILE_M * BN) + row;
+#pragma unroll
+    for (int i = 0; i < FIN_COLS; ++i)
+      if (j0 + i < k) s[i] += src[(size_t)(j0 + i) * TILE_M];
+  }
+  int bad = 0;
+#pragma unroll
+  for (int i = 0; i < FIN_COLS; ++i) {
+    const int j = j0 + i;
+    float a = 0.f;
+    if (valid && j < k) {
+      const float w = rndf(s[i], out_fmt);
+      st_fmt(W, (int64_t)j * ldw + grow, out_fmt, (double)w);
+      if (!isfinite(w)) bad = 1;
+      a = (w != w) ? INFINITY : fabsf(w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane == 0) smax[warp][i] = a;
+  }
+  __syncthreads();
+  if (colmax && threadIdx.x < FIN_COLS && j0 + threadIdx.x < k) {
+    float a = smax[0][threadIdx.x];
+    for (int w8 = 1; w8 < 8; ++w8) a = fmaxf(a, smax[w8][threadIdx.x]);
+    atomic_max_nonneg(&colmax[j0 + threadIdx.x], (double)a);
+  }
+  if (bad && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t inner, uint64_t outer,
+                        uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) { ofrr_set_error("cuTensorMapEncodeTiled unavailable"); return OFRR_ERR_CUDA; }
+  CUtensorMapDataType dt = a_fmt == BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                         : a_fmt == F16  ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                         : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const int eb = fmt_bytes(a_fmt);
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * (uint64_t)eb};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    ofrr_set_error("cuTensorMapEncodeTiled failed (%d): dims %llu x %llu ld %llu box %u x %u", (int)r,
+                   (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)ld_elems,
+                   box_inner, box_outer);
+    return OFRR_ERR_INVALID;
+  }
+  return OFRR_OK;
+}
+
+static int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : k <= 128 ? 128 : 256; }
+
+struct TcPlan {
+  int bn, m_tiles, kblocks, grid, max_slots;
+  long long total;
+  size_t ws_bytes;
+};
+
+static TcPlan plan_tc(int64_t rows, int64_t cols, int k, int a_fmt) {
+  TcPlan p;
+  p.bn = pick_bn(k);
+  const int kel = (a_fmt == FP8) ? 128 : 64;
+  p.m_tiles = (int)((rows + TILE_M - 1) / TILE_M);
+  p.kblocks = (int)((cols + kel - 1) / kel);
+  p.total = (long long)p.m_tiles * p.kblocks;
+  int sms = ofrr_device_sm_count(-1);
+  if (sms <= 0) sms = 148;
+  p.grid = (int)std::min<long long>(sms, p.total);
+  if (p.grid < 1) p.grid = 1;
+  const long long per = (p.total + p.grid - 1) / p.grid;
+  p.max_slots = (int)((per + p.kblocks - 1) / p.kblocks) + 1;
+  p.ws_bytes = (size_t)p.grid * p.max_slots * TILE_M * p.bn * sizeof(float);
+  return p;
+}
+
+size_t tc_workspace(int64_t rows, int64_t cols, int k, int a_fmt) {
+  return plan_tc(rows, cols, k, a_fmt).ws_bytes;
+}
+
+template <int BN, bool FP8K>
+static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPlan& p, float* ws,
+                        uint32_t idesc, cudaStream_t st) {
+  using C = TcCfg<BN>;
+  auto kern = k_gemm_av_tc<BN, FP8K>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+    attr_done = true;
+  }
+  kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* X,
+               int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags,
+               void* ws, size_t ws_bytes, cudaStream_t st) {
+  TcPlan p = plan_tc(rows, cols, k, a_fmt);
+  if (ws_bytes < p.ws_bytes || ws == nullptr) {
+    ofrr_set_error("gemm_av: workspace too small (%zu < %zu)", ws_bytes, p.ws_bytes);
+    return OFRR_ERR_INVALID;
+  }
+  const bool fp8 = a_fmt == FP8;
+  const uint32_t kel = fp8 ? 128 : 64;
+  CUtensorMap tA, tX;
+  int rc = make_tmap_2d(&tA, A, a_fmt, (uint64_t)cols, (uint64_t)rows, (uint64_t)lda, kel, TILE_M);
+  if (rc) return rc;
+  rc = make_tmap_2d(&tX, X, a_fmt, (uint64_t)cols, (uint64_t)k, (uint64_t)ldx, kel, (uint32_t)p.bn);
+  if (rc) return rc;
+  const uint32_t idesc = make_idesc(a_fmt, p.bn);
+  switch (p.bn) {
+    case 32: rc = fp8 ? launch_tc_bn<32, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<32, false>(tA, tX, p, (float*)ws, idesc, st); break;
+    case 64: rc = fp8 ? launch_tc_bn<64, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<64, false>(tA, tX, p, (float*)ws, idesc, st); break;
+    case 128: rc = fp8 ? launch_tc_bn<128, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<128, false>(tA, tX, p, (float*)ws, idesc, st); break;
+    default: rc = fp8 ? launch_tc_bn<256, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<256, false>(tA, tX, p, (float*)ws, idesc, st); break;
+  }
+  if (rc) return rc;
+  k_finalize<<<dim3(p.m_tiles, (k + FIN_COLS - 1) / FIN_COLS), 256, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
+                                        rows, k, W, ldw, out_fmt, colmax, flags);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+}  // namespace ofrr

@@ -1,0 +1,214 @@
+// hessenberg.cu -- K3: inner-product-free basis by pivot scaling and elimination
+// (LU with partial pivoting of the tall-skinny block X, n x k).
+//
+// Replaces ofrr/basis.py:151-204 (hessenberg_basis, _pivot_row) with the axpy of
+// ofrr/precision.py:172-180.  The elementwise arithmetic is the reference's, op for op
+// (compute-format products / subtractions / divisions, storage rounding), so the
+// pivots, kept mask and Q agree bit for bit with the reference for every policy.
+//
+// One persistent cooperative kernel, one CTA per SM (grid <= #SMs), each CTA owning a
+// contiguous row block.  Per column j there is exactly one grid-wide barrier:
+//   before the barrier every CTA publishes its local pivot candidate for column j
+//   (max |X[i,j]| over its free rows, lowest index on ties) together with that row's
+//   values in columns j..k-1; after the barrier every CTA reduces the candidates in
+//   ascending CTA order (= ascending row order, so ties resolve to the lowest index),
+//   scales column j by the pivot, applies the rank-1 trailing update with the pivot
+//   row taken from the published candidate, and computes its candidate for column j+1
+//   in the same pass.  Candidates are double buffered by step parity.
+#include "common.cuh"
+#include <cooperative_groups.h>
+#include <algorithm>
+
+namespace cg = cooperative_groups;
+
+namespace ofrr {
+
+static constexpr int HT = 256;
+
+struct HessWs {
+  double* cand_val;   // [2][G]
+  long long* cand_idx;  // [2][G]
+  double* cand_row;   // [2][G][k]
+  unsigned char* freerow;  // [n]
+};
+
+__device__ __forceinline__ void block_argmax(double& v, long long& idx, double* sv, long long* si) {
+  // max value; ties -> lowest index; idx < 0 means "no candidate"
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
+  }
+  if (lane == 0) { sv[warp] = v; si[warp] = idx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < HT / 32; ++w) {
+      const double ov = sv[w];
+      const long long oi = si[w];
+      if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
+    }
+    sv[0] = v;
+    si[0] = idx;
+  }
+  __syncthreads();
+  v = sv[0];
+  idx = si[0];
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(HT)
+    k_hessenberg(const T* __restrict__ X, int64_t n, int k, int64_t ldx, T* __restrict__ Xw, int64_t ldw,
+                 int storage, int compute, double tol, T* __restrict__ Q, int64_t ldq,
+                 int64_t* __restrict__ pivots, int* __restrict__ kept, int* __restrict__ n_kept, HessWs ws) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[HT / 32];
+  __shared__ long long si[HT / 32];
+  extern __shared__ double prow[];  // pivot row values, k entries
+
+  const int G = gridDim.x, c = blockIdx.x;
+  const int64_t rows_per = (n + G - 1) / G;
+  const int64_t r0 = std::min<int64_t>(n, (int64_t)c * rows_per);
+  const int64_t r1 = std::min<int64_t>(n, r0 + rows_per);
+  const int64_t nr = r1 - r0;
+
+  // prologue: private copy of my rows, free flags, candidate for column 0
+  for (int j = 0; j < k; ++j)
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Xw[(int64_t)j * ldw + i] = X[(int64_t)j * ldx + i];
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) ws.freerow[i] = 1;
+  __syncthreads();
+
+  auto publish = [&](int j, int buf) {
+    // local argmax of |Xw[i, j]| over my free rows, then publish value/idx/row
+    double v = -1.0;
+    long long idx = -1;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+      if (!ws.freerow[i]) continue;
+      const double a = fabs(to_d(Xw[(int64_t)j * ldw + i]));
+      if (idx < 0 || a > v) { v = a; idx = i; }   // ascending i per thread: keeps lowest on ties
+    }
+    block_argmax(v, idx, sv, si);
+    if (threadIdx.x == 0) {
+      ws.cand_val[buf * G + c] = v;
+      ws.cand_idx[buf * G + c] = idx;
+    }
+    if (idx >= 0)
+      for (int cc = j + threadIdx.x; cc < k; cc += HT)
+        ws.cand_row[((int64_t)buf * G + c) * k + cc] = to_d(Xw[(int64_t)cc * ldw + idx]);
+  };
+
+  publish(0, 0);
+  __threadfence();
+  grid.sync();
+
+  int nk = 0;
+  for (int j = 0; j < k; ++j) {
+    const int buf = j & 1;
+    // reduce the candidates (ascending CTA = ascending rows)
+    double best = -1.0;
+    long long r = -1;
+    int owner = -1;
+    for (int cc = 0; cc < G; ++cc) {
+      const long long oi = ws.cand_idx[buf * G + cc];
+      const double ov = ws.cand_val[buf * G + cc];
+      if (oi >= 0 && (r < 0 || ov > best)) { best = ov; r = oi; owner = cc; }
+    }
+    // ofrr/basis.py:178-180: skip when no free row or |pivot| < tol (NaN pivots skip too)
+    const bool skip = (r < 0) || !(best >= tol);
+    if (!skip) {
+      for (int cc = j + threadIdx.x; cc < k; cc += HT) prow[cc] = ws.cand_row[((int64_t)buf * G + owner) * k + cc];
+      __syncthreads();
+      const double piv = prow[j];
+      // ofrr/basis.py:181-187: v = round_s(round_c(v / piv)); v[r] = 1
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+        const double x = to_d(Xw[(int64_t)j * ldw + i]);
+        const double v = (i == r) ? 1.0 : rnd(c_div(x, piv, compute), storage);
+        Xw[(int64_t)j * ldw + i] = from_d<T>(v);
+        Q[(int64_t)nk * ldq + i] = from_d<T>(v);
+      }
+      if (r >= r0 && r < r1 && threadIdx.x == 0) ws.freerow[r] = 0;
+      if (c == 0 && threadIdx.x == 0) { kept[j] = 1; pivots[nk] = r; }
+      __syncthreads();
+      // ofrr/basis.py:188-190 + precision.py:172-180: a[:,i] = round_s(c(a) - c(c(a[r,i]) * c(v)))
+      const int64_t cols = k - j - 1;
+      const int64_t work = cols * nr;
+      for (int64_t e = threadIdx.x; e < work; e += HT) {
+        const int64_t cc = j + 1 + e / nr;
+        const int64_t i = r0 + e % nr;
+        const double alpha = rnd(prow[cc], compute);
+        const double v = to_d(Xw[(int64_t)j * ldw + i]);
+        const double y = to_d(Xw[cc * ldw + i]);
+        const double t = c_mul(alpha, rnd(v, compute), compute);
+        Xw[cc * ldw + i] = from_d<T>(rnd(c_sub(rnd(y, compute), t, compute), storage));
+      }
+      ++nk;
+      __syncthreads();
+    } else if (c == 0 && threadIdx.x == 0) {
+      kept[j] = 0;
+    }
+    if (j + 1 < k) {
+      publish(j + 1, buf ^ 1);
+      __threadfence();
+      grid.sync();
+    }
+  }
+  if (c == 0 && threadIdx.x == 0) *n_kept = nk;
+}
+
+static int hess_grid(int64_t n) {
+  int sms = ofrr_device_sm_count(-1);
+  if (sms <= 0) sms = 148;
+  int64_t g = (n + 63) / 64;  // at least 64 rows per CTA
+  return (int)std::max<int64_t>(1, std::min<int64_t>(sms, g));
+}
+
+size_t hessenberg_ws(int64_t n, int k, int storage) {
+  const int G = hess_grid(n);
+  size_t b = 0;
+  b += 2 * G * sizeof(double);
+  b += 2 * G * sizeof(long long);
+  b += (size_t)2 * G * k * sizeof(double);
+  b += (size_t)n * fmt_bytes(storage) * k;  // working copy
+  b += n;
+  return b + 2048;
+}
+
+template <typename T>
+static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute, double tol,
+                       void* Q, int64_t ldq, int64_t* pivots, int* kept, int* n_kept, void* ws, cudaStream_t st) {
+  const int G = hess_grid(n);
+  uint8_t* p = (uint8_t*)ws;
+  auto take = [&](size_t bytes) { uint8_t* q = p; p += (bytes + 255) & ~size_t(255); return q; };
+  HessWs h;
+  h.cand_val = (double*)take(2 * G * sizeof(double));
+  h.cand_idx = (long long*)take(2 * G * sizeof(long long));
+  h.cand_row = (double*)take((size_t)2 * G * k * sizeof(double));
+  T* Xw = (T*)take((size_t)n * sizeof(T) * k);
+  h.freerow = (unsigned char*)take(n);
+  const T* Xp = (const T*)X;
+  T* Qp = (T*)Q;
+  int64_t ldw = n;
+  size_t shmem = (size_t)k * sizeof(double);
+  void* args[] = {(void*)&Xp, (void*)&n, (void*)&k, (void*)&ldx, (void*)&Xw, (void*)&ldw, (void*)&storage,
+                  (void*)&compute, (void*)&tol, (void*)&Qp, (void*)&ldq, (void*)&pivots, (void*)&kept,
+                  (void*)&n_kept, (void*)&h};
+  OFRR_CUDA_TRY(cudaMemsetAsync(kept, 0, sizeof(int) * k, st));
+  OFRR_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hessenberg<T>, dim3(G), dim3(HT), args, shmem, st));
+  return OFRR_OK;
+}
+
+int hessenberg(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute, double tol, void* Q,
+               int64_t ldq, int64_t* pivots, int* kept, int* n_kept, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < hessenberg_ws(n, k, storage)) { ofrr_set_error("hessenberg: workspace too small"); return OFRR_ERR_INVALID; }
+  switch (storage) {
+    case F64: return launch_hess<double>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
+    case F32: return launch_hess<float>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
+    case F16: return launch_hess<__half>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
+    case BF16: return launch_hess<__nv_bfloat16>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
+    default: ofrr_set_error("hessenberg: storage format %d unsupported", storage); return OFRR_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace ofrr

@@ -1,0 +1,303 @@
+// simt.cu -- CUDA-core kernels of the OFRR hot path:
+//   * k_gemm_simt: W = op(A) X for F32 / F64 storage (tensor cores have no exact fp32/fp64
+//     path; kind::tf32 is not fp32), and the FP64 residual products (K7);
+//   * k_scale_columns (K2), k_convert.
+#include "common.cuh"
+#include <algorithm>
+
+namespace ofrr {
+
+template <typename T> struct Ld;
+template <> struct Ld<double> { __device__ static double get(const void* p, long i) { return ((const double*)p)[i]; } };
+template <> struct Ld<float> { __device__ static double get(const void* p, long i) { return (double)((const float*)p)[i]; } };
+template <> struct Ld<__half> { __device__ static double get(const void* p, long i) { return (double)__half2float(((const __half*)p)[i]); } };
+template <> struct Ld<__nv_bfloat16> { __device__ static double get(const void* p, long i) { return (double)__bfloat162float(((const __nv_bfloat16*)p)[i]); } };
+template <> struct Ld<__nv_fp8_storage_t> {
+  __device__ static double get(const void* p, long i) {
+    __nv_fp8_e4m3 v; v.__x = ((const __nv_fp8_storage_t*)p)[i]; return (double)float(v);
+  }
+};
+
+// ---------------------------------------------------------------------------------
+// C (m x n) = op(A) (m x K) * B (K x n).  A row-major (rows x cols, lda); op(A) = A or A^T.
+// B column-major (ldb).  Tiles 64 x 64 x 16, 256 threads, 4x4 register blocking.
+// MODE 0: store C rounded to out_fmt (column-major, ldc) + colmax + non-finite flag.
+// MODE 1: residual partials  part[blockIdx.x * n + j] = sum_i (C[i,j] - vals[j] * Y[i,j])^2
+// ---------------------------------------------------------------------------------
+static constexpr int SBM = 64, SBN = 64, SBK = 16;
+
+template <typename TA, typename TB, typename ACC, int MODE>
+__global__ void __launch_bounds__(256)
+    k_gemm_simt(const void* __restrict__ A, int64_t lda, int transpose, int64_t m, int64_t K,
+                const void* __restrict__ B, int64_t ldb, int n, void* __restrict__ C, int64_t ldc,
+                int out_fmt, double* __restrict__ colmax, int* __restrict__ flags,
+                const double* __restrict__ Y, int64_t ldy, const double* __restrict__ vals,
+                const int* __restrict__ r_dev, double* __restrict__ part) {
+  __shared__ ACC As[SBK][SBM + 1];
+  __shared__ ACC Bs[SBK][SBN + 1];
+  __shared__ double cmax[SBN];
+  __shared__ double csum[16][SBN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, each 4 x 4 outputs
+  const int64_t m0 = (int64_t)blockIdx.x * SBM;
+  const int n0 = blockIdx.y * SBN;
+  int nvalid = n;
+  if (MODE == 1 && r_dev) nvalid = min(n, *r_dev);
+  ACC acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = ACC(0);
+
+  for (int64_t k0 = 0; k0 < K; k0 += SBK) {
+    // A tile: 64 rows x 16 k  (1024 elements, 4 per thread)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      int r, kk;
+      if (!transpose) { r = idx >> 4; kk = idx & 15; }   // contiguous along k
+      else { kk = idx >> 6; r = idx & 63; }               // contiguous along m
+      const int64_t gr = m0 + r, gk = k0 + kk;
+      ACC v = ACC(0);
+      if (gr < m && gk < K)
+        v = (ACC)Ld<TA>::get(A, transpose ? gk * lda + gr : gr * lda + gk);
+      As[kk][r] = v;
+    }
+    // B tile: 16 k x 64 cols (column-major: contiguous along k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      const int c = idx >> 4, kk = idx & 15;
+      const int64_t gk = k0 + kk;
+      const int gc = n0 + c;
+      ACC v = ACC(0);
+      if (gk < K && gc < n) v = (ACC)Ld<TB>::get(B, (int64_t)gc * ldb + gk);
+      Bs[kk][c] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SBK; ++kk) {
+      ACC a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+
+  if (MODE == 0) {
+    if (tid < SBN) cmax[tid] = 0.0;
+    __syncthreads();
+    int bad = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = n0 + tx + 16 * j;
+      double lm = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t gr = m0 + ty + 16 * i;
+        if (gr < m && gc < n) {
+          const double w = rnd((double)acc[i][j], out_fmt);
+          st_fmt(C, (int64_t)gc * ldc + gr, out_fmt, w);
+          if (!isfinite(w)) { bad = 1; lm = INFINITY; }
+          else lm = fmax(lm, fabs(w));
+        }
+      }
+      if (gc < n) atomic_max_nonneg(&cmax[tx + 16 * j], lm);
+    }
+    __syncthreads();
+    if (colmax && tid < SBN && n0 + tid < n) atomic_max_nonneg(&colmax[n0 + tid], cmax[tid]);
+    if (bad && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
+  } else {
+    // residual partial sums of squares, fixed order (rows ty, ty+16, ... then over ty)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = n0 + tx + 16 * j;
+      double s = 0.0;
+      if (gc < nvalid) {
+        const double lam = vals[gc];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t gr = m0 + ty + 16 * i;
+          if (gr < m) {
+            const double r = (double)acc[i][j] - lam * Y[(int64_t)gc * ldy + gr];
+            s += r * r;
+          }
+        }
+      }
+      csum[ty][tx + 16 * j] = s;
+    }
+    __syncthreads();
+    if (tid < SBN) {
+      double s = 0.0;
+      for (int y = 0; y < 16; ++y) s += csum[y][tid];
+      if (n0 + tid < n) part[(int64_t)blockIdx.x * n + n0 + tid] = s;
+    }
+  }
+}
+
+// res[j] = sqrt(sum_b part[b, j]) / |vals[j]|  (inf for vals[j] == 0), fixed order.
+__global__ void k_residual_reduce(const double* __restrict__ part, int nblocks, int n,
+                                  const double* __restrict__ vals, const int* __restrict__ r_dev,
+                                  double* __restrict__ res, int accumulate_max) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  // accumulate_max: 0 -> res = ||r|| / |lambda|; 1 -> res = max(res, ||r|| / |lambda|);
+  //                 2 -> res = raw sum of squares (row-partitioned runs all-reduce it first)
+  const int nvalid = r_dev ? min(n, *r_dev) : n;
+  if (j >= nvalid) { if (accumulate_max != 1) res[j] = 0.0; return; }
+  double s = 0.0;
+  for (int b = 0; b < nblocks; ++b) s += part[(int64_t)b * n + j];
+  if (accumulate_max == 2) { res[j] = s; return; }
+  const double lam = vals[j];
+  const double r = lam == 0.0 ? INFINITY : sqrt(s) / fabs(lam);
+  res[j] = accumulate_max ? fmax(res[j], r) : r;
+}
+
+template <typename TA, typename TB, typename ACC, int MODE>
+static int launch_simt(const void* A, int64_t lda, int transpose, int64_t m, int64_t K, const void* B,
+                       int64_t ldb, int n, void* C, int64_t ldc, int out_fmt, double* colmax, int* flags,
+                       const double* Y, int64_t ldy, const double* vals, const int* r_dev, double* part,
+                       cudaStream_t st) {
+  dim3 grid((unsigned)((m + SBM - 1) / SBM), (unsigned)((n + SBN - 1) / SBN));
+  k_gemm_simt<TA, TB, ACC, MODE><<<grid, 256, 0, st>>>(A, lda, transpose, m, K, B, ldb, n, C, ldc, out_fmt,
+                                                       colmax, flags, Y, ldy, vals, r_dev, part);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+int simt_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose,
+                 const void* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax,
+                 int* flags, cudaStream_t st) {
+  const int64_t m = transpose ? cols : rows, K = transpose ? rows : cols;
+  if (a_fmt == F64)
+    return launch_simt<double, double, double, 0>(A, lda, transpose, m, K, X, ldx, k, W, ldw, out_fmt, colmax,
+                                                  flags, nullptr, 0, nullptr, nullptr, nullptr, st);
+  if (a_fmt == F32)
+    return launch_simt<float, float, float, 0>(A, lda, transpose, m, K, X, ldx, k, W, ldw, out_fmt, colmax,
+                                               flags, nullptr, 0, nullptr, nullptr, nullptr, st);
+  ofrr_set_error("simt_gemm_av: format %d not supported on the CUDA-core path", a_fmt);
+  return OFRR_ERR_UNSUPPORTED;
+}
+
+size_t residual_ws(int64_t rows, int r) {
+  return (size_t)((rows + SBM - 1) / SBM) * (size_t)r * sizeof(double);
+}
+
+int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose,
+                  const double* Xv, int64_t ldx, const double* Yv, int64_t ldy, const double* vals,
+                  const int* r_dev, int r_max, double* res, int accumulate_max, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+  const int64_t m = transpose ? cols : rows, K = transpose ? rows : cols;
+  const size_t need = residual_ws(m, r_max);
+  if (!ws || ws_bytes < need) { ofrr_set_error("residual: workspace too small (%zu < %zu)", ws_bytes, need); return OFRR_ERR_INVALID; }
+  double* part = (double*)ws;
+  int rc;
+  switch (a_fmt) {
+    case F64: rc = launch_simt<double, double, double, 1>(A, lda, transpose, m, K, Xv, ldx, r_max, nullptr, 0, 0, nullptr, nullptr, Yv, ldy, vals, r_dev, part, st); break;
+    case F32: rc = launch_simt<float, double, double, 1>(A, lda, transpose, m, K, Xv, ldx, r_max, nullptr, 0, 0, nullptr, nullptr, Yv, ldy, vals, r_dev, part, st); break;
+    case F16: rc = launch_simt<__half, double, double, 1>(A, lda, transpose, m, K, Xv, ldx, r_max, nullptr, 0, 0, nullptr, nullptr, Yv, ldy, vals, r_dev, part, st); break;
+    case BF16: rc = launch_simt<__nv_bfloat16, double, double, 1>(A, lda, transpose, m, K, Xv, ldx, r_max, nullptr, 0, 0, nullptr, nullptr, Yv, ldy, vals, r_dev, part, st); break;
+    default: rc = launch_simt<__nv_fp8_storage_t, double, double, 1>(A, lda, transpose, m, K, Xv, ldx, r_max, nullptr, 0, 0, nullptr, nullptr, Yv, ldy, vals, r_dev, part, st); break;
+  }
+  if (rc) return rc;
+  const int nb = (int)((m + SBM - 1) / SBM);
+  k_residual_reduce<<<(r_max + 127) / 128, 128, 0, st>>>(part, nb, r_max, vals, r_dev, res, accumulate_max);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// K2: X[:,j] <- round_s(round_c(X[:,j] / colmax[j]))   (ofrr/precision.py:159-169)
+// ---------------------------------------------------------------------------------
+__global__ void k_scale_columns(void* __restrict__ X, int64_t n, int k, int64_t ldx, int storage,
+                                int compute, const double* __restrict__ colmax) {
+  const int j = blockIdx.y;
+  const double m = (double)colmax[j];
+  if (m == 0.0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)j * ldx + i;
+    const double x = ld_fmt(X, o, storage);
+    st_fmt(X, o, storage, rnd(c_div(x, m, compute), storage));
+  }
+}
+
+int scale_columns(void* X, int64_t n, int k, int64_t ldx, int storage, int compute, const double* colmax,
+                  cudaStream_t st) {
+  if (k <= 0 || n <= 0) return OFRR_OK;
+  unsigned gx = (unsigned)std::min<int64_t>((n + 255) / 256, 64);
+  k_scale_columns<<<dim3(gx, k), 256, 0, st>>>(X, n, k, ldx, storage, compute, colmax);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+__global__ void k_convert(const void* __restrict__ src, int sf, int64_t lds, void* __restrict__ dst, int df,
+                          int64_t ldd, int64_t n, int64_t k, int* __restrict__ flags) {
+  int bad = 0;
+  const int64_t total = n * k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e - j * n;
+    const double x = ld_fmt(src, j * lds + i, sf);
+    const double v = rnd(x, df);
+    if (!isfinite(v)) bad |= OFRR_FLAG_NONFINITE;
+    if (v != x && x == x) bad |= OFRR_FLAG_INEXACT;
+    st_fmt(dst, j * ldd + i, df, v);
+  }
+  if (bad && flags) atomicOr(flags, bad);
+}
+
+// dst (row-major rows x cols, ldd) <- round(src (column-major rows x cols, lds)): uploads of
+// the reference's F-order float64 operators into the device's row-major storage layout.
+__global__ void k_transpose_convert(const void* __restrict__ src, int sf, int64_t lds, void* __restrict__ dst, int df,
+                                    int64_t ldd, int64_t rows, int64_t cols, int* __restrict__ flags) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + y, r = r0 + threadIdx.x;
+    tile[y][threadIdx.x] = (c < cols && r < rows) ? ld_fmt(src, c * lds + r, sf) : 0.0;
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) {
+      const double x = tile[threadIdx.x][y];
+      const double v = rnd(x, df);
+      if (!isfinite(v)) bad |= OFRR_FLAG_NONFINITE;
+      if (v != x && x == x) bad |= OFRR_FLAG_INEXACT;
+      st_fmt(dst, r * ldd + c, df, v);
+    }
+  }
+  if (bad && flags) atomicOr(flags, bad);
+}
+
+int transpose_convert(const void* src, int sf, int64_t lds, void* dst, int df, int64_t ldd, int64_t rows, int64_t cols,
+                      int* flags, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return OFRR_OK;
+  for (int64_t rb = 0; rb < rows; rb += 32 * 65535) {
+    const int64_t rr = std::min<int64_t>(rows - rb, 32 * 65535);
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rr + 31) / 32));
+    k_transpose_convert<<<grid, dim3(32, 8), 0, st>>>((const uint8_t*)src + rb * fmt_bytes(sf), sf, lds,
+                                                      (uint8_t*)dst + rb * ldd * fmt_bytes(df), df, ldd, rr, cols,
+                                                      flags);
+    OFRR_CHECK_LAUNCH();
+  }
+  return OFRR_OK;
+}
+
+int convert(const void* src, int sf, int64_t lds, void* dst, int df, int64_t ldd, int64_t n, int64_t k,
+            int* flags, cudaStream_t st) {
+  if (n <= 0 || k <= 0) return OFRR_OK;
+  const int64_t total = n * k;
+  unsigned g = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_convert<<<g, 256, 0, st>>>(src, sf, lds, dst, df, ldd, n, k, flags);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+}  // namespace ofrr

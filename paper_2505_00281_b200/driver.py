@@ -1,0 +1,411 @@
+"""Outer iterations of OFRR on the device: subspace iteration for eigenpairs and
+alternating subspace iteration for the partial SVD.
+
+Same entry points, options and results as ofrr/driver.py:40-173
+(``IterConfig``, ``subspace_iter_eig``, ``subspace_iter_svd``), restricted to the
+B200 path's basis/projection pair (hess-l / hess-r + "ofrr"; anything else raises
+ValueError -- there is no CPU fallback).  Extension fields on IterConfig:
+``tol`` / ``top`` turn the fixed ``m`` outer iterations into "stop once the FP64
+residuals of the leading ``top`` pairs are below ``tol``" (``m`` is then the cap);
+their defaults keep the reference's fixed-m behaviour.
+
+Multi-GPU: when torch.distributed is initialised (one process per GPU), A is
+row-partitioned (rank p owns rows [p*rp, (p+1)*rp)); each power step all-gathers the
+n x k block and all-reduces the k column maxima, each projection all-reduces the k x k
+partial Gram U_p^T W_p (fp64).  The Hessenberg basis, the pencil solve and the Ritz
+recovery are redundant on every rank (deterministic, so every rank holds identical
+results).  See DESIGN.md section "Multi-GPU".
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import ops as _ops
+from .basis import BasisMethod, HESSENBERG_METHODS, KRYLOV_METHODS
+from .comm import Comm
+from .errors import ConvergenceError, EmptyBasisError, EmptyPencilError, OverflowDiagnostic
+from .matrix import DenseMatrix
+from .precision import FpFormat, PrecisionPolicy, projection_policy, round_to
+from .projection import POSITIVE_EIG_TOL, RitzSet
+
+
+@dataclass(frozen=True)
+class IterConfig:
+    """ofrr/driver.py:40-62, plus the time-to-tolerance extension (tol, top)."""
+    k: int
+    m: int = 1
+    iter: int = 1
+    restarts: int = 0
+    basis_method: BasisMethod = BasisMethod.MGS_LEFT
+    projection: str = "rr"  # "rr" | "ofrr"
+    policy: PrecisionPolicy = None
+    matvec_policy: Optional[PrecisionPolicy] = None  # defaults to policy
+    seed: int = 0
+    tol: Optional[float] = None   # extension: stop when max residual over `top` < tol
+    top: Optional[int] = None     # extension: number of leading pairs checked
+
+    def __post_init__(self):
+        if self.k < 1 or self.m < 1 or self.iter < 1 or self.restarts < 0:
+            raise ValueError("k, m, iter must be >= 1 and restarts >= 0")
+        if self.projection not in ("rr", "ofrr"):
+            raise ValueError("projection must be 'rr' or 'ofrr'")
+        if self.policy is None:
+            raise ValueError("policy is required")
+        if self.top is not None and not (1 <= self.top <= self.k):
+            raise ValueError("top must be in [1, k]")
+
+    @property
+    def mv_policy(self) -> PrecisionPolicy:
+        return self.matvec_policy or self.policy
+
+
+def _require_ofrr_path(cfg: IterConfig, what: str) -> None:
+    if cfg.basis_method in KRYLOV_METHODS:
+        raise ValueError(f"{what} needs a block basis method")
+    if cfg.basis_method not in HESSENBERG_METHODS or cfg.projection != "ofrr":
+        raise ValueError(
+            f"the B200 path runs basis_method in (hess-l, hess-r) with projection='ofrr'; got "
+            f"{cfg.basis_method.value!r} / {cfg.projection!r} (the Gram-Schmidt / classical RR "
+            "baselines are CPU-reference only)")
+
+
+@dataclass
+class RunStats:
+    """Per-run diagnostics (iterations done, residual history, phase timings)."""
+    iterations: int = 0
+    history: list = field(default_factory=list)   # (iteration, max residual over top)
+    converged: bool = False
+    a_passes: int = 0
+
+
+# status-vector slots (one int32[8] device vector, read once per sync point)
+S_MV_FLAGS, S_NKEPT, S_EIG_STATUS, S_NOUT, S_GRAM_FLAGS, S_RESTART_FLAGS, S_NKEPT2 = 0, 1, 2, 3, 4, 5, 6
+
+
+def _fetch_status(st, comm: Comm):
+    if comm.distributed:
+        comm.all_reduce_max_(st)
+    return st.cpu().numpy()
+
+
+def _raise_for(s, stage: str, eig: bool = True):
+    if s[S_MV_FLAGS] & 1:
+        raise OverflowDiagnostic("non-finite entries after MatVec")
+    if eig:
+        if s[S_GRAM_FLAGS] & 1:
+            raise OverflowDiagnostic("non-finite entries in projected matrix")
+        if s[S_EIG_STATUS] == 6:
+            raise ConvergenceError("Jacobi eigendecomposition did not converge", float("nan"))
+        if s[S_EIG_STATUS] == 5 or s[S_NOUT] == 0:
+            raise EmptyPencilError("mass matrix retained no eigenvalues")
+        if s[S_RESTART_FLAGS] & 1:
+            raise OverflowDiagnostic(f"non-finite entries after {stage}")
+
+
+class EigEngine:
+    """Device state of one subspace_iter_eig run (single GPU or row-partitioned)."""
+
+    def __init__(self, a: DenseMatrix, cfg: IterConfig, comm: Optional[Comm] = None, n_global: Optional[int] = None,
+                 ops=None):
+        self.ops = ops or _ops
+        self.comm = comm or Comm.world()
+        self.cfg = cfg
+        self.pol = cfg.policy
+        self.mv = cfg.mv_policy
+        self.a = a
+        self.n = int(n_global if n_global is not None else a.cols)
+        self.A_mv = a.device_operator(self.mv.storage)
+        self.A_pol = self.A_mv if self.pol.storage == self.mv.storage else a.device_operator(self.pol.storage)
+        self.device = self.A_mv.device
+        self.r0, self.r1 = self.comm.row_range(self.n)
+        if self.comm.distributed and self.A_mv.rows != self.r1 - self.r0:
+            raise ValueError(f"rank {self.comm.rank}: local A has {self.A_mv.rows} rows, expected "
+                             f"{self.r1 - self.r0} (rows {self.r0}..{self.r1} of {self.n})")
+        _, self.proj_out = projection_policy(self.pol)
+        self.stats = RunStats()
+
+    # ---- blocks ---------------------------------------------------------------------
+    def start_block(self):
+        """X0 = PCG64(seed) U(0,1), rounded to the MatVec storage (ofrr/driver.py:97-99)."""
+        rng = np.random.default_rng(self.cfg.seed)
+        x0 = rng.random((self.n, self.cfg.k))
+        return self.ops.block_from_host(round_to(x0, self.mv.storage), self.mv.storage, self.device)
+
+    def power(self, X, st):
+        """cfg.iter MatVecs with inf-norm column scaling (ofrr/driver.py:102-105)."""
+        import torch
+        ops, comm = self.ops, self.comm
+        k = X.k
+        for _ in range(self.cfg.iter):
+            colmax = torch.zeros(k, dtype=torch.float64, device=self.device)
+            W = ops.new_block(self.A_mv.rows, k, self.mv.storage, self.device)
+            ops.gemm_av(self.A_mv, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+            self.stats.a_passes += 1
+            comm.all_reduce_max_(colmax)
+            ops.scale_columns(W, colmax, self.mv.compute)
+            if comm.distributed:
+                Xn = ops.new_block(self.n, k, self.mv.storage, self.device)
+                comm.all_gather_rows(W.t, Xn.t, self.n, k)
+                X = Xn
+            else:
+                X = W
+        return X
+
+    def basis(self, X, st):
+        """Hessenberg basis (K3), redundant on every rank."""
+        h = self.ops.hessenberg(X, self.pol.storage, self.pol.compute, self.pol.drop_tol)
+        st[S_NKEPT:S_NKEPT + 1].copy_(h.n_kept)
+        return h
+
+    def project(self, U, st, want64: bool, top_check: Optional[int] = None):
+        """ofrr_eig (ofrr/projection.py:75-87) + restart block (ofrr/driver.py:109)."""
+        ops, comm = self.ops, self.comm
+        kp = U.k
+        W = ops.new_block(self.A_pol.rows, kp, self.pol.storage, self.device)
+        ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        self.stats.a_passes += 1
+        if comm.distributed:
+            Ul = _row_slice(U, self.r0, self.r1)
+            B, _ = ops.gram(Ul, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], want_m=False)
+            comm.all_reduce_sum_(B)
+            _, M = ops.gram(U, None, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        else:
+            B, M = ops.gram(U, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        eig = ops.sym_def_gen_eig(B, M, kp)
+        st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
+        st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
+        U64, Xn = ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=want64, x_fmt=self.mv.storage,
+                           flags=st[S_RESTART_FLAGS:S_RESTART_FLAGS + 1])
+        res = None
+        if top_check is not None and U64 is not None:
+            res = self.residuals(U64, eig.values, eig.n_out, min(top_check, kp))
+        return eig, U64, Xn, res
+
+    def residuals(self, U64, vals, r_dev, r):
+        """FP64 ||A u - lambda u|| / |lambda| for the first r pairs (K7)."""
+        import torch
+        ops, comm = self.ops, self.comm
+        A = self.a.residual_operator(self.A_mv.fmt) if hasattr(self.a, "residual_operator") else self.A_mv
+        if not comm.distributed:
+            return ops.residual_eig(A, U64, vals, r_dev, r)
+        res = torch.zeros(r, dtype=torch.float64, device=self.device)
+        Yl = _row_slice(U64, self.r0, self.r1)
+        ops.residual_pair(A, False, U64.narrow(r), Yl.narrow(r), vals, r_dev, r, res, accumulate_max=2)
+        comm.all_reduce_sum_(res)
+        return res   # sum of squares; finished on the host (see _finish_residuals)
+
+    def finish_residuals(self, res, vals_np):
+        r = res.cpu().numpy()
+        if self.comm.distributed:
+            lam = vals_np[: len(r)]
+            with np.errstate(divide="ignore"):
+                return np.where(lam == 0.0, np.inf, np.sqrt(r) / np.abs(lam))
+        return r
+
+    # ---- the outer loop -----------------------------------------------------------------
+    def run(self) -> RitzSet:
+        import torch
+        cfg = self.cfg
+        tol, top = cfg.tol, (cfg.top or cfg.k)
+        X = self.start_block()
+        eig = U64 = None
+        kp = r = 0
+        for it in range(cfg.m):
+            st = torch.zeros(8, dtype=torch.int32, device=self.device)
+            X = self.power(X, st)
+            h = self.basis(X, st)
+            s = _fetch_status(st, self.comm)                      # sync 1: MatVec flags, basis width
+            if s[S_MV_FLAGS] & 1:
+                raise OverflowDiagnostic("non-finite entries after MatVec")
+            kp = int(s[S_NKEPT])
+            if kp == 0:
+                raise EmptyBasisError("all columns skipped in Hessenberg process")
+            U = h.Q.narrow(kp)
+            last = it == cfg.m - 1
+            check = tol is not None
+            eig, U64, Xn, res = self.project(U, st, want64=(last or check), top_check=(top if check else None))
+            s = _fetch_status(st, self.comm)                      # sync 2: pencil status, width
+            _raise_for(s, "projection")
+            r = int(s[S_NOUT])
+            X = Xn.narrow(r)
+            self.stats.iterations = it + 1
+            if check:
+                vals_np = eig.values[:r].cpu().numpy()
+                rr = self.finish_residuals(res, vals_np)
+                worst = float(np.max(rr[: min(top, r)])) if r >= top else float("inf")
+                self.stats.history.append((it + 1, worst))
+                if worst < tol:
+                    self.stats.converged = True
+                    break
+            self._last_U = U
+        if U64 is None:  # m iterations without a final FP64 recovery (cannot happen: last=True)
+            raise RuntimeError("internal: no Ritz vectors")
+        vals = eig.values[:r].cpu().numpy()
+        vecs = DenseMatrix.from_block(U64.narrow(r))
+        rs = RitzSet(vals, vecs, "eig")
+        return self.residual_report(rs, U64, eig, r)
+
+    def residual_report(self, rs: RitzSet, U64, eig, r: int) -> RitzSet:
+        """ofrr/driver.py:111 -> ofrr/projection.py:136-147 (FP64, every returned pair)."""
+        from dataclasses import replace
+        res = self.residuals(U64, eig.values, eig.n_out, r)
+        return replace(rs, residuals=self.finish_residuals(res, rs.values)[:r])
+
+
+def _row_slice(B, r0: int, r1: int):
+    """Rows [r0, r1) of a column-major block as a block view (same ld)."""
+    import torch
+    from .ops import DevBlock
+    t = B.t
+    # strided view: row j = column j starting at element r0, same leading dimension
+    view = torch.as_strided(t, (t.shape[0], B.ld - r0), (B.ld, 1), t.storage_offset() + r0)
+    return DevBlock(view, r1 - r0, B.k, B.fmt)
+
+
+def subspace_iter_eig(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats] = None,
+                      comm: Optional[Comm] = None, n_global: Optional[int] = None) -> RitzSet:
+    """Multi-step subspace iteration with the Hessenberg basis and OFRR projection
+    (ofrr/driver.py:84-111), on the device.
+
+    ``a``: the operator (host DenseMatrix uploaded once; or device resident).  In a
+    row-partitioned run ``a`` holds this rank's rows and ``n_global`` the full n."""
+    _require_ofrr_path(cfg, "subspace iteration")
+    n = int(n_global if n_global is not None else a.rows)
+    if cfg.k > n:
+        raise ValueError("k exceeds the operator dimension")
+    eng = EigEngine(a, cfg, comm=comm, n_global=n)
+    rs = eng.run()
+    if stats is not None:
+        stats.__dict__.update(eng.stats.__dict__)
+    return rs
+
+
+# -------------------------------------------------------------------------------------
+# SVD (single GPU)
+# -------------------------------------------------------------------------------------
+class SvdEngine:
+    """Device state of subspace_iter_svd / ofrr_svd (ofrr/driver.py:141-173,
+    ofrr/projection.py:99-133).  A V and A^T U both run K-major on the tensor cores:
+    A^T is kept resident as a second row-major operator."""
+
+    def __init__(self, a: DenseMatrix, pol: PrecisionPolicy, mv: PrecisionPolicy, ops=None):
+        self.ops = ops or _ops
+        self.a, self.pol, self.mv = a, pol, mv
+        self.A_mv = a.device_operator(mv.storage)
+        self.At_mv = a.device_operator_t(mv.storage)
+        self.A_pol = self.A_mv if pol.storage == mv.storage else a.device_operator(pol.storage)
+        self.device = self.A_mv.device
+        _, self.proj_out = projection_policy(pol)
+        self.a_passes = 0
+
+    @classmethod
+    def single(cls, a, pol, mv):
+        return cls(a, pol, mv)
+
+    def matvec(self, op, X, st):
+        import torch
+        colmax = torch.zeros(X.k, dtype=torch.float64, device=self.device)
+        W = self.ops.new_block(op.rows, X.k, self.mv.storage, self.device)
+        self.ops.gemm_av(op, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+        self.a_passes += 1
+        self.ops.scale_columns(W, colmax, self.mv.compute)
+        return W
+
+    def project(self, U, V, want64: bool = True, x_fmt=None):
+        """ofrr_svd on device blocks U (n1 x k1), V (n2 x k2) in policy storage."""
+        import torch
+        ops = self.ops
+        k1, k2 = U.k, V.k
+        kk = k1 + k2
+        st = torch.zeros(8, dtype=torch.int32, device=self.device)
+        W = ops.new_block(self.A_pol.rows, k2, self.pol.storage, self.device)
+        ops.gemm_av(self.A_pol, V, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        self.a_passes += 1
+        G, Mu = ops.gram(U, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        _, Mv = ops.gram(V, None, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        # block pencil (tensors are column-major: row j = column j)
+        Bm = torch.zeros((kk, kk), dtype=torch.float64, device=self.device)
+        Mm = torch.zeros((kk, kk), dtype=torch.float64, device=self.device)
+        Gk = G[:k2, :k1]                 # column j (< k2) of G = U^T W -> row j
+        Bm[k1:, :k1].copy_(Gk)           # columns k1.. of B hold G (rows 0..k1)
+        Bm[:k1, k1:].copy_(Gk.t())       # columns 0..k1 of B hold G^T (rows k1..)
+        Mm[:k1, :k1].copy_((Mu + Mu.t()) / 2.0)
+        Mm[k1:, k1:].copy_((Mv + Mv.t()) / 2.0)
+        eig = ops.sym_def_gen_eig(Bm, Mm, kk)
+        st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
+        st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
+        s = st.cpu().numpy()
+        if s[S_MV_FLAGS] & 1:
+            raise OverflowDiagnostic("non-finite entries after MatVec")
+        if s[S_GRAM_FLAGS] & 1:
+            raise OverflowDiagnostic("non-finite entries in projected matrix")
+        if s[S_EIG_STATUS] == 6:
+            raise ConvergenceError("Jacobi eigendecomposition did not converge", float("nan"))
+        nout = int(s[S_NOUT])
+        if nout == 0:
+            raise EmptyPencilError("mass matrix retained no eigenvalues")
+        vals = eig.values[:nout].cpu().numpy()
+        smax = float(np.max(vals))
+        pos = vals > POSITIVE_EIG_TOL * smax if smax > 0 else vals > 0
+        npos = int(np.count_nonzero(pos))   # a prefix: values are sorted descending
+        sig = vals[:npos]
+        diag = ""
+        if npos < min(k1, k2):
+            diag = f"{npos} positive eigenvalues (pencil admits {min(k1, k2)})"
+        if npos == 0:
+            return RitzSet(sig, DenseMatrix(np.zeros((U.n, 0)), FpFormat.F64), "svd",
+                           right_vectors=DenseMatrix(np.zeros((V.n, 0)), FpFormat.F64), diagnostics=diag), None, None
+        U64, _ = ops.ritz(U, eig.vectors, kk, None, npos, math.sqrt(2.0), want64=True)
+        V64, Vx = ops.ritz(V, eig.vectors, kk, None, npos, math.sqrt(2.0), want64=True,
+                           x_fmt=x_fmt, row_offset=k1, flags=st[S_RESTART_FLAGS:S_RESTART_FLAGS + 1])
+        rs = RitzSet(sig, DenseMatrix.from_block(U64), "svd", right_vectors=DenseMatrix.from_block(V64),
+                     diagnostics=diag)
+        return rs, Vx, st
+
+
+def subspace_iter_svd(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats] = None) -> RitzSet:
+    """Alternating subspace iteration for the SVD (ofrr/driver.py:141-173), on device."""
+    from .projection import residual_report
+    _require_ofrr_path(cfg, "SVD iteration")
+    n1, n2 = a.rows, a.cols
+    if cfg.k > min(n1, n2):
+        raise ValueError("k exceeds min(n1, n2)")
+    pol, mv = cfg.policy, cfg.mv_policy
+    eng = SvdEngine(a, pol, mv)
+    ops = eng.ops
+    rng = np.random.default_rng(cfg.seed)
+    V = ops.block_from_host(round_to(rng.random((n2, cfg.k)), mv.storage), mv.storage, eng.device)
+    rs = None
+    import torch
+    for _ in range(cfg.m):
+        st = torch.zeros(8, dtype=torch.int32, device=eng.device)
+        U = V
+        for _ in range(cfg.iter):
+            U = eng.matvec(eng.A_mv, V, st)
+            V = eng.matvec(eng.At_mv, U, st)
+        hu = ops.hessenberg(U, pol.storage, pol.compute, pol.drop_tol)
+        hv = ops.hessenberg(V, pol.storage, pol.compute, pol.drop_tol)
+        st[S_NKEPT:S_NKEPT + 1].copy_(hu.n_kept)
+        st[S_NKEPT2:S_NKEPT2 + 1].copy_(hv.n_kept)
+        s = st.cpu().numpy()
+        if s[S_MV_FLAGS] & 1:
+            raise OverflowDiagnostic("non-finite entries after MatVec")
+        k1, k2 = int(s[S_NKEPT]), int(s[S_NKEPT2])
+        if k1 == 0 or k2 == 0:
+            raise EmptyBasisError("all columns skipped in Hessenberg process")
+        rs, Vx, st2 = eng.project(hu.Q.narrow(k1), hv.Q.narrow(k2), x_fmt=mv.storage)
+        if Vx is None:
+            raise EmptyPencilError("no positive eigenvalues in the SVD pencil")
+        if int(st2[S_RESTART_FLAGS].item()) & 1:
+            raise OverflowDiagnostic("non-finite entries after projection")
+        V = Vx
+    if stats is not None:
+        stats.iterations = cfg.m
+        stats.a_passes = eng.a_passes
+    return residual_report(a, rs)

@@ -1,0 +1,341 @@
+"""Typed device operations: thin wrappers that pass torch CUDA tensors to the C ABI.
+
+Layout on the device:
+* ``DevOperator``: the operator A, row-major ``rows x cols`` in its storage format,
+  leading dimension padded to 64 elements (TMA needs 16-byte strides).
+* ``DevBlock``: an ``n x k`` block (X, W, U, Q, Ritz vectors) column-major, i.e. the
+  reference's Fortran order (ofrr/matrix.py:25-31), stored as a torch tensor of shape
+  ``(k, ld)`` whose row j is column j; ``ld`` = n padded to 64.
+
+Every function enqueues on the current torch stream and returns without
+synchronising.  Nothing here computes on the host.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .precision import FpFormat
+
+PAD = 64
+
+# launch accounting (bench.py "gpu_launches"): number of libofrr_b200 kernels enqueued
+LAUNCHES = [0]
+# optional per-op CUDA-event timing of the block product (bench.py roofline): when a list
+# is installed here, gemm_av appends (start_event, end_event, bytes) for every call
+GEMM_EVENTS = None
+
+
+def _count(n: int) -> None:
+    LAUNCHES[0] += n
+
+
+def pad_ld(n: int) -> int:
+    return max(PAD, (int(n) + PAD - 1) // PAD * PAD)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+@dataclass
+class DevBlock:
+    """Column-major n x k block in format ``fmt`` (tensor shape (k_alloc, ld))."""
+    t: torch.Tensor
+    n: int
+    k: int
+    fmt: FpFormat
+
+    @property
+    def ld(self) -> int:
+        return self.t.stride(0)
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    @property
+    def device(self):
+        return self.t.device
+
+    def col_view(self, k: Optional[int] = None) -> torch.Tensor:
+        """(k, n) view: row j = column j."""
+        k = self.k if k is None else k
+        return self.t[:k, : self.n]
+
+    def to_numpy_f64(self, k: Optional[int] = None):
+        """Host copy as an F-order float64 n x k array (the reference's layout)."""
+        import numpy as np
+        v = self.col_view(k).to(torch.float64).cpu().numpy()
+        return np.asfortranarray(v.T)
+
+    def narrow(self, k: int) -> "DevBlock":
+        return DevBlock(self.t, self.n, int(k), self.fmt)
+
+
+@dataclass
+class DevOperator:
+    """Row-major rows x cols operator in format ``fmt`` (tensor shape (rows, lda))."""
+    t: torch.Tensor
+    rows: int
+    cols: int
+    fmt: FpFormat
+
+    @property
+    def lda(self) -> int:
+        return self.t.stride(0)
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    @property
+    def device(self):
+        return self.t.device
+
+
+def new_block(n: int, k: int, fmt: FpFormat, device, zero: bool = False) -> DevBlock:
+    fmt = FpFormat(fmt)
+    shape = (max(int(k), 1), pad_ld(n))
+    t = (torch.zeros if zero else torch.empty)(shape, dtype=fmt.torch_dtype, device=device)
+    return DevBlock(t, int(n), int(k), fmt)
+
+
+def new_operator(rows: int, cols: int, fmt: FpFormat, device) -> DevOperator:
+    fmt = FpFormat(fmt)
+    t = torch.empty((int(rows), pad_ld(cols)), dtype=fmt.torch_dtype, device=device)
+    return DevOperator(t, int(rows), int(cols), fmt)
+
+
+def block_from_host(x, fmt: FpFormat, device) -> DevBlock:
+    """Upload a host n x k float64 array (values representable in ``fmt``)."""
+    import numpy as np
+    x = np.asarray(x, dtype=np.float64)
+    n, k = x.shape
+    b = new_block(n, k, FpFormat.F64, device, zero=True)
+    b.t[:k, :n].copy_(torch.from_numpy(np.ascontiguousarray(x.T)))
+    if FpFormat(fmt) == FpFormat.F64:
+        return b
+    out = new_block(n, k, fmt, device, zero=True)
+    convert(b, out)
+    return out
+
+
+def convert(src: DevBlock, dst: DevBlock, flags: Optional[torch.Tensor] = None) -> None:
+    """dst <- round(src) column by column (ofrr/precision.py:90-104)."""
+    L = _lib.load()
+    _lib.check(L.ofrr_convert(src.ptr, int(src.fmt), src.ld, dst.ptr, int(dst.fmt), dst.ld, src.n, src.k,
+                              _p(flags), _stream()), "convert")
+    _count(1)
+
+
+def round_tensor(x: torch.Tensor, fmt: FpFormat) -> torch.Tensor:
+    """Device round_to for a 1-D/2-D CUDA tensor: returns float64 with values in fmt."""
+    x64 = x.to(torch.float64).contiguous()
+    flat = x64.reshape(1, -1) if x64.dim() <= 1 else x64.reshape(-1, x64.shape[-1])
+    rows, cols = flat.shape
+    out = torch.empty_like(flat)
+    tmp = torch.empty((rows, cols), dtype=FpFormat(fmt).torch_dtype, device=x.device)
+    L = _lib.load()
+    # treat each row of `flat` as a column (n = cols, k = rows)
+    _lib.check(L.ofrr_convert(flat.data_ptr(), int(FpFormat.F64), cols, tmp.data_ptr(), int(fmt), cols, cols, rows,
+                              None, _stream()), "round_to")
+    _lib.check(L.ofrr_convert(tmp.data_ptr(), int(fmt), cols, out.data_ptr(), int(FpFormat.F64), cols, cols, rows,
+                              None, _stream()), "round_to")
+    return out.reshape(x.shape)
+
+
+# ---------------------------------------------------------------------------------
+# K1 / K2
+# ---------------------------------------------------------------------------------
+def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat] = None,
+            colmax: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
+            transpose: bool = False) -> None:
+    """W = op(A) X rounded to out_fmt (default W.fmt); colmax[j] = max|W[:,j]|."""
+    L = _lib.load()
+    k = X.k
+    ws_b = L.ofrr_gemm_av_workspace(A.rows, A.cols, k, int(A.fmt), int(transpose))
+    ws = _ws(ws_b, A.device)
+    of = int(W.fmt if out_fmt is None else out_fmt)
+    ev = GEMM_EVENTS
+    if ev is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+    _lib.check(L.ofrr_gemm_av(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), int(transpose), X.ptr, X.ld, k, W.ptr,
+                              W.ld, of, _p(colmax), _p(flags), ws.data_ptr(), ws.numel(), _stream()), "gemm_av")
+    if ev is not None:
+        e1.record()
+        # algorithmic bytes: A once + X once + W once
+        nb = A.rows * A.cols * A.fmt.itemsize + A.cols * k * X.fmt.itemsize + A.rows * k * FpFormat(of).itemsize
+        ev.append((e0, e1, nb, 2.0 * A.rows * A.cols * k))
+    _count(2 if (A.fmt.tensor_core and not transpose) else 1)
+
+
+def scale_columns(X: DevBlock, colmax: torch.Tensor, compute: FpFormat) -> None:
+    L = _lib.load()
+    _lib.check(L.ofrr_scale_columns(X.ptr, X.n, X.k, X.ld, int(X.fmt), int(compute), colmax.data_ptr(), _stream()),
+               "scale_columns")
+    _count(1)
+
+
+# ---------------------------------------------------------------------------------
+# K3
+# ---------------------------------------------------------------------------------
+@dataclass
+class HessOut:
+    Q: DevBlock          # k columns allocated; first n_kept valid
+    pivots: torch.Tensor  # int64[k]
+    kept: torch.Tensor    # int32[k]
+    n_kept: torch.Tensor  # int32[1]
+
+
+def hessenberg(X: DevBlock, storage: FpFormat, compute: FpFormat, tol: float) -> HessOut:
+    L = _lib.load()
+    dev = X.device
+    if FpFormat(storage) != X.fmt:
+        Xs = new_block(X.n, X.k, storage, dev)
+        convert(X, Xs)
+        X = Xs
+    Q = new_block(X.n, X.k, storage, dev)
+    piv = torch.zeros(max(X.k, 1), dtype=torch.int64, device=dev)
+    kept = torch.zeros(max(X.k, 1), dtype=torch.int32, device=dev)
+    nk = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws_b = L.ofrr_hessenberg_workspace(X.n, X.k, int(storage))
+    ws = _ws(ws_b, dev)
+    _lib.check(L.ofrr_hessenberg(X.ptr, X.n, X.k, X.ld, int(storage), int(compute), float(tol), Q.ptr, Q.ld,
+                                 piv.data_ptr(), kept.data_ptr(), nk.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 _stream()), "hessenberg")
+    _count(1)
+    return HessOut(Q, piv, kept, nk)
+
+
+# ---------------------------------------------------------------------------------
+# K4
+# ---------------------------------------------------------------------------------
+def gram(U: DevBlock, W: Optional[DevBlock], out_fmt: FpFormat, flags: Optional[torch.Tensor] = None,
+         want_m: bool = True):
+    """(G1 = U^T W, G2 = U^T U) as fp64 (k x kw) / (k x k) tensors, column-major
+    (returned as torch tensors of shape (kw, k) / (k, k): row j = column j)."""
+    L = _lib.load()
+    dev = U.device
+    k = U.k
+    kw = W.k if W is not None else 0
+    G1 = torch.empty((max(kw, 1), k), dtype=torch.float64, device=dev) if W is not None else None
+    G2 = torch.empty((k, k), dtype=torch.float64, device=dev) if want_m else None
+    ws = _ws(L.ofrr_gram_workspace(U.n, k, kw), dev)
+    if W is not None and W.fmt != U.fmt:
+        raise ValueError("gram: U and W must share a storage format")
+    _lib.check(L.ofrr_gram(U.ptr, U.ld, _p(W.t) if W is not None else None, W.ld if W is not None else 0, U.n, k, kw,
+                           int(U.fmt), int(out_fmt), _p(G1), _p(G2), _p(flags), ws.data_ptr(), ws.numel(),
+                           _stream()), "gram")
+    _count(2)
+    return G1, G2
+
+
+# ---------------------------------------------------------------------------------
+# K5
+# ---------------------------------------------------------------------------------
+@dataclass
+class EigOut:
+    values: torch.Tensor   # fp64[k]
+    vectors: torch.Tensor  # fp64 (k, k): row j = eigenvector j (column-major k x k)
+    n_out: torch.Tensor    # int32[1]
+    status: torch.Tensor   # int32[1]
+
+
+def sym_def_gen_eig(B: torch.Tensor, M: torch.Tensor, k: int) -> EigOut:
+    """B, M: fp64 column-major k x k (torch (k, k) with row j = column j)."""
+    L = _lib.load()
+    dev = B.device
+    vals = torch.zeros(max(k, 1), dtype=torch.float64, device=dev)
+    vecs = torch.zeros((max(k, 1), max(k, 1)), dtype=torch.float64, device=dev)
+    n_out = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _ws(L.ofrr_small_eig_workspace(k), dev)
+    _lib.check(L.ofrr_sym_def_gen_eig(B.data_ptr(), M.data_ptr(), k, vals.data_ptr(), vecs.data_ptr(),
+                                      n_out.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),
+               "sym_def_gen_eig")
+    _count(1)
+    return EigOut(vals, vecs, n_out, status)
+
+
+def sym_eig(S: torch.Tensor, k: int) -> EigOut:
+    L = _lib.load()
+    dev = S.device
+    vals = torch.zeros(max(k, 1), dtype=torch.float64, device=dev)
+    vecs = torch.zeros((max(k, 1), max(k, 1)), dtype=torch.float64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _ws(L.ofrr_small_eig_workspace(k), dev)
+    _lib.check(L.ofrr_sym_eig(S.data_ptr(), k, vals.data_ptr(), vecs.data_ptr(), status.data_ptr(), ws.data_ptr(),
+                              ws.numel(), _stream()), "sym_eig")
+    n_out = torch.full((1,), k, dtype=torch.int32, device=dev)
+    return EigOut(vals, vecs, n_out, status)
+
+
+# ---------------------------------------------------------------------------------
+# K6 / K7
+# ---------------------------------------------------------------------------------
+def ritz(U: DevBlock, Y: torch.Tensor, ldy: int, r_dev: Optional[torch.Tensor], r_max: int, scale: float = 1.0,
+         want64: bool = True, x_fmt: Optional[FpFormat] = None, flags: Optional[torch.Tensor] = None,
+         row_offset: int = 0):
+    """Ut = scale * U Y[:, :r] (fp64 block) and/or X = round(Ut, x_fmt)."""
+    L = _lib.load()
+    dev = U.device
+    U64 = new_block(U.n, r_max, FpFormat.F64, dev) if want64 else None
+    X = new_block(U.n, r_max, x_fmt, dev) if x_fmt is not None else None
+    Yp = Y.data_ptr() + row_offset * 8
+    _lib.check(L.ofrr_ritz_recover(U.ptr, U.ld, int(U.fmt), U.n, U.k, Yp, ldy, _p(r_dev), r_max, float(scale),
+                                   _p(U64.t) if U64 else None, U64.ld if U64 else 0, _p(X.t) if X else None,
+                                   X.ld if X else 0, int(x_fmt) if x_fmt is not None else 0, _p(flags), _stream()),
+               "ritz_recover")
+    _count(1)
+    return U64, X
+
+
+def residual_eig(A: DevOperator, V: DevBlock, vals: torch.Tensor, r_dev: Optional[torch.Tensor], r_max: int):
+    L = _lib.load()
+    res = torch.zeros(max(r_max, 1), dtype=torch.float64, device=A.device)
+    ws = _ws(L.ofrr_residual_workspace(A.rows, r_max), A.device)
+    _lib.check(L.ofrr_residual_eig(A.ptr, A.rows, A.lda, int(A.fmt), V.ptr, V.ld, vals.data_ptr(), _p(r_dev), r_max,
+                                   res.data_ptr(), ws.data_ptr(), ws.numel(), _stream()), "residual_eig")
+    _count(2)
+    return res
+
+
+def residual_pair(A: DevOperator, transpose: bool, Xv: DevBlock, Yv: DevBlock, vals: torch.Tensor,
+                  r_dev: Optional[torch.Tensor], r_max: int, res: torch.Tensor, accumulate_max: bool):
+    L = _lib.load()
+    m = A.cols if transpose else A.rows
+    ws = _ws(L.ofrr_residual_workspace(m, r_max), A.device)
+    _lib.check(L.ofrr_residual_pair(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), int(transpose), Xv.ptr, Xv.ld, Yv.ptr,
+                                    Yv.ld, vals.data_ptr(), _p(r_dev), r_max, res.data_ptr(), int(accumulate_max),
+                                    ws.data_ptr(), ws.numel(), _stream()), "residual_pair")
+    _count(2)
+    return res
+
+
+def generate_sym(A: DevOperator, row0: int, hadamard: bool, c, s, Wf, Mf) -> None:
+    """Evaluate the synthetic symmetric matrix rows [row0, row0 + A.rows) on device."""
+    L = _lib.load()
+    dev = A.device
+    n = A.cols
+    ct = torch.as_tensor(c, dtype=torch.float64).to(dev)
+    st = torch.as_tensor(s, dtype=torch.float64).to(dev)
+    r = Wf.shape[1]
+    Wt = torch.as_tensor(Wf.T.copy(), dtype=torch.float64).to(dev)   # [r][n]
+    Mt = torch.as_tensor(Mf.T.copy(), dtype=torch.float64).to(dev)
+    _lib.check(L.ofrr_generate_sym(n, row0, A.rows, int(hadamard), ct.data_ptr(), st.data_ptr(), Wt.data_ptr(),
+                                   Mt.data_ptr(), r, A.ptr, A.lda, int(A.fmt), _stream()), "generate_sym")
+    torch.cuda.current_stream().synchronize()

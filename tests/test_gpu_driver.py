@@ -1,0 +1,147 @@
+"""End-to-end GPU parity of the OFRR drivers against the reference (golden vectors) and
+the oracle, with the north-star criteria: Ritz values within
+max(10 x the reference's error vs exact, 1e-6 relative), residuals within 2x."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SEED = 20240901
+
+
+def _criteria(vals, res, ref_vals, ref_res, exact, top):
+    """North-star parity: Ritz values within max(10 x the reference's error vs exact,
+    1e-6 relative) and residuals within 2 x the reference's.  "The reference's error"
+    is its error level over the checked pairs (max over the top pairs): with 16-bit
+    storage a single pair's error is a rounding lottery between eps-sized outcomes, so a
+    per-pair 10x bound would test luck, not parity."""
+    ref_err = np.abs(ref_vals[:top] - exact[:top]) / np.abs(exact[:top])
+    err = np.abs(vals[:top] - exact[:top]) / np.abs(exact[:top])
+    assert np.max(err) <= max(10 * np.max(ref_err), 1e-6), (err, ref_err)
+    assert np.max(res[:top]) <= 2 * np.max(ref_res[:top]) + 1e-13, (res[:top], ref_res[:top])
+
+
+@pytest.mark.parametrize("pname", ["full-f64", "full-f32", "tc-f16"])
+@pytest.mark.parametrize("method", ["hess-l", "hess-r"])
+def test_driver_eig_vs_reference_golden(ofrr_gpu, golden, pname, method):
+    """subspace_iter_eig(kernel matrix n=120, k=20, m=3, iter=2) vs the reference's run."""
+    p = ofrr_gpu
+    pol = p.POLICY_PRESETS[pname]
+    key = f"driver_eig/{pname}/{method}"
+    a = p.DenseMatrix(golden[key + "/a"], p.FpFormat.F64)
+    cfg = p.IterConfig(k=20, m=3, iter=2, basis_method=p.BasisMethod(method), projection="ofrr", policy=pol, seed=2)
+    rs = p.subspace_iter_eig(a, cfg)
+    exact = golden["driver_eig/exact"] if pname == "full-f64" else \
+        np.sort(np.linalg.eigvalsh(golden[key + "/a"]))[::-1]
+    _criteria(rs.values, rs.residuals, golden[key + "/vals"], golden[key + "/res"], exact, 6)
+    assert rs.vectors.data.shape == golden[key + "/vecs"].shape
+
+
+def test_driver_eig_deterministic(ofrr_gpu, golden):
+    """tests/test_driver.py:72-79: bitwise determinism of repeated runs."""
+    p = ofrr_gpu
+    a = p.DenseMatrix(golden["driver_eig/tc-f16/hess-l/a"], p.FpFormat.F64)
+    cfg = p.IterConfig(k=8, m=2, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.TC_F16, seed=5)
+    r1 = p.subspace_iter_eig(a, cfg)
+    r2 = p.subspace_iter_eig(a, cfg)
+    np.testing.assert_array_equal(r1.values, r2.values)
+    np.testing.assert_array_equal(r1.vectors.data, r2.vectors.data)
+
+
+@pytest.mark.parametrize("pname", ["full-f64", "full-f32"])
+def test_driver_svd_vs_reference_golden(ofrr_gpu, golden, pname):
+    p = ofrr_gpu
+    key = f"driver_svd/{pname}"
+    a = p.DenseMatrix(golden[key + "/a"], p.FpFormat.F64)
+    cfg = p.IterConfig(k=10, m=6, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.POLICY_PRESETS[pname], seed=9)
+    rs = p.subspace_iter_svd(a, cfg)
+    exact = np.linalg.svd(golden[key + "/a"], compute_uv=False)
+    _criteria(rs.values, rs.residuals, golden[key + "/vals"], golden[key + "/res"], exact, 5)
+
+
+def test_ofrr_eig_known_answers(ofrr_gpu, golden):
+    p = ofrr_gpu
+    # Rayleigh quotient 2.0 for diag(3,1), u=[1,1] (tests/test_projection.py:71-75)
+    rs = p.ofrr_eig(p.DenseMatrix(np.diag([3.0, 1.0]), p.FpFormat.F64),
+                    p.DenseMatrix(np.array([[1.0], [1.0]]), p.FpFormat.F64), p.FULL_F64)
+    assert rs.values[0] == pytest.approx(2.0, abs=1e-14)
+    for pname in ("full-f64", "full-f32"):
+        rs = p.ofrr_eig(p.DenseMatrix(golden[f"ofrreig/{pname}/a"], p.FpFormat.F64),
+                        p.DenseMatrix(golden[f"ofrreig/{pname}/u"], p.POLICY_PRESETS[pname].storage),
+                        p.POLICY_PRESETS[pname])
+        # full-f32: the reference rounds every fp32 product and sum of A.U; the device uses
+        # fp32 FMA in another order -> agreement at the fp32 level
+        rt = 1e-10 if pname == "full-f64" else 2e-5
+        np.testing.assert_allclose(rs.values, golden[f"ofrreig/{pname}/vals"], rtol=rt, atol=rt)
+        np.testing.assert_allclose(rs.vectors.data, golden[f"ofrreig/{pname}/vecs"], rtol=1e3 * rt, atol=1e3 * rt)
+
+
+def test_ofrr_eig_errors(ofrr_gpu):
+    p = ofrr_gpu
+    with pytest.raises(p.EmptyPencilError):       # tests/test_projection.py:96-99
+        p.ofrr_eig(p.DenseMatrix(np.eye(3), p.FpFormat.F64), p.DenseMatrix(np.zeros((3, 2)), p.FpFormat.F64),
+                   p.FULL_F64)
+    with pytest.raises(p.OverflowDiagnostic):      # tests/test_projection.py:101-105
+        p.ofrr_eig(p.DenseMatrix(np.full((2, 2), 6.0e4), p.FpFormat.F64),
+                   p.DenseMatrix(np.full((2, 1), 6.0e4), p.FpFormat.F64), p.NATIVE_F16)
+
+
+def test_ofrr_svd_golden(ofrr_gpu, golden):
+    p = ofrr_gpu
+    rs = p.ofrr_svd(p.DenseMatrix(golden["ofrrsvd/a"], p.FpFormat.F64),
+                    p.DenseMatrix(golden["ofrrsvd/u"], p.FpFormat.F64),
+                    p.DenseMatrix(golden["ofrrsvd/v"], p.FpFormat.F64), p.FULL_F64)
+    np.testing.assert_allclose(rs.values, golden["ofrrsvd/vals"], rtol=1e-10)
+    np.testing.assert_allclose(rs.vectors.data, golden["ofrrsvd/uu"], rtol=1e-7, atol=1e-8)
+    np.testing.assert_allclose(rs.right_vectors.data, golden["ofrrsvd/vv"], rtol=1e-7, atol=1e-8)
+
+
+@pytest.mark.parametrize("fmt", ["tc-bf16", "tc-f16", "full-f32"])
+def test_driver_eig_vs_oracle_geometric(ofrr_gpu, oracle, fmt):
+    """C1/C2-style problem at oracle-feasible size: geometric spectrum, n=1024 (WHT
+    generator), top 10, k 20: same synthetic A, same X0, same policy."""
+    p, o = ofrr_gpu, oracle
+    n, top, k, m = 1024, 10, 20, 5
+    pol = p.POLICY_PRESETS[fmt]
+    lam = p.geometric_spectrum(n, top, k)
+    A, f = p.synthetic_symmetric(lam, pol.storage, seed=SEED)
+    a_host = o.sym_from_factors(n, f.hadamard, f.c, f.s, f.Wf, f.Mf, int(pol.storage))
+    cfg = p.IterConfig(k=k, m=m, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr", policy=pol,
+                       seed=SEED)
+    rs = p.subspace_iter_eig(A, cfg)
+    ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=o.as_pol(pol), seed=SEED)
+    exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+
+
+def test_driver_eig_c1_fp32(ofrr_gpu, oracle):
+    """C1: 2000 x 2000 dense symmetric, geometric spectrum, top 10, k 20, fp32 basis /
+    fp64 projection -- the reference's CPU configuration, run through the oracle."""
+    p, o = ofrr_gpu, oracle
+    n, top, k, m = 2000, 10, 20, 4
+    a_host, lam = o.geometric_symmetric(n, top, k, seed=SEED, fmt=o.F32)
+    cfg = p.IterConfig(k=k, m=m, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.FULL_F32, seed=SEED)
+    rs = p.subspace_iter_eig(p.DenseMatrix(a_host, p.FpFormat.F32), cfg)
+    ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=o.FULL_F32, seed=SEED)
+    exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+
+
+def test_driver_eig_tolerance_stop(ofrr_gpu):
+    """Extension: IterConfig(tol, top) stops at the first outer iteration whose FP64
+    residuals of the top pairs are below tol."""
+    p = ofrr_gpu
+    n, top, k = 4096, 16, 32
+    lam = p.geometric_spectrum(n, top, k)
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    st = p.RunStats()
+    cfg = p.IterConfig(k=k, m=30, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.TC_BF16, seed=SEED, tol=2e-2, top=top)
+    rs = p.subspace_iter_eig(A, cfg, stats=st)
+    assert st.converged and st.iterations < 30
+    assert np.max(rs.residuals[:top]) < 2e-2
+    assert st.history[-1][1] < 2e-2

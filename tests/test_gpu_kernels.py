@@ -1,0 +1,262 @@
+"""GPU parity of every kernel on the OFRR hot path against the CPU oracle (which is
+pinned to the reference by tests/test_oracle_golden.py).  Calls go through the C ABI
+(libofrr_b200.so) via the package's typed ops layer."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+F16, F32, F64, BF16, FP8 = 0, 1, 2, 3, 4
+
+
+def _op(p, a, fmt):
+    """row-major device operator from a host float64 matrix (values representable)."""
+    m = p.DenseMatrix(np.asfortranarray(a), p.FpFormat.F64)
+    return m.device_operator(p.FpFormat(fmt))
+
+
+def _blk(p, x, fmt):
+    from paper_2505_00281_b200 import ops
+    import torch
+    return ops.block_from_host(x, p.FpFormat(fmt), torch.device("cuda"))
+
+
+def _host(b, k=None):
+    return b.to_numpy_f64(k)
+
+
+def _ulp_close(got, ref, fmt_eps, frac=1e-2):
+    """got == ref except for at most `frac` of entries that differ by one storage ulp."""
+    d = np.abs(got - ref)
+    bad = d > 0
+    if not bad.any():
+        return True
+    tol = 2.0 * fmt_eps * np.maximum(np.abs(ref), 1e-30)
+    return bad.mean() <= frac and np.all(d[bad] <= tol[bad])
+
+
+@pytest.mark.parametrize("fmt", [BF16, F16])
+@pytest.mark.parametrize("shape", [(256, 128, 32), (1000, 1000, 20), (517, 777, 64), (2048, 2048, 128),
+                                   (300, 4096, 200), (1, 64, 1), (4000, 512, 256)])
+def test_gemm_tc_fp32_out_vs_fp64(ofrr_gpu, oracle, fmt, shape):
+    """K1 (tcgen05): fp32-accumulated A.X against the exact fp64 product."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rows, cols, k = shape
+    rng = np.random.default_rng(rows * 7 + cols + k)
+    a = o.round_to(rng.standard_normal((rows, cols)), fmt)
+    x = o.round_to(rng.random((cols, k)), fmt)
+    A = _op(p, a, fmt)
+    X = _blk(p, x, fmt)
+    W = ops.new_block(rows, k, p.FpFormat.F32, A.device)
+    colmax = torch.zeros(k, dtype=torch.float64, device=A.device)
+    ops.gemm_av(A, X, W, colmax=colmax)
+    got = _host(W)
+    exact = a @ x
+    bound = 1e-5 * (np.abs(a) @ np.abs(x)) + 1e-30
+    assert np.all(np.abs(got - exact) <= bound), np.max(np.abs(got - exact) / bound)
+    np.testing.assert_array_equal(colmax.cpu().numpy(), np.max(np.abs(got), axis=0))
+
+
+@pytest.mark.parametrize("fmt", [BF16, F16])
+def test_gemm_tc_storage_out_vs_oracle(ofrr_gpu, oracle, fmt):
+    """K1 rounded to the storage format vs the oracle's mixed_gemm (F32 products/sums):
+    equal except for rare one-ulp ties decided by the fp32 summation order."""
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(11)
+    rows, cols, k = 1500, 1300, 48
+    a = o.round_to(rng.standard_normal((rows, cols)), fmt)
+    x = o.round_to(rng.random((cols, k)), fmt)
+    A = _op(p, a, fmt)
+    W = ops.new_block(rows, k, p.FpFormat(fmt), A.device)
+    ops.gemm_av(A, _blk(p, x, fmt), W)
+    ref = o.mixed_gemm(a, x, F32, F32, fmt)
+    got = _host(W)
+    d = np.abs(got - ref)
+    bad = d > 0
+    msg = f"{bad.mean():.2e} of entries differ; max rel {np.max(d / np.maximum(np.abs(ref), 1e-30)):.2e}"
+    # a differing entry is one storage ulp away, or within the fp32 summation-order
+    # error (sums that cancel to near zero)
+    allowed = 2.0 * o.EPS[fmt] * np.abs(ref) + 1e-5 * (np.abs(a) @ np.abs(x))
+    assert bad.mean() <= 1e-2 and np.all(d <= allowed), msg
+
+
+def test_gemm_fp8(ofrr_gpu, oracle):
+    """K1 kind::f8f6f4 (e4m3) vs the exact product."""
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(3)
+    rows, cols, k = 700, 1024, 64
+    a = o.round_to(rng.standard_normal((rows, cols)), FP8)
+    x = o.round_to(rng.random((cols, k)), FP8)
+    A = _op(p, a, FP8)
+    W = ops.new_block(rows, k, p.FpFormat.F32, A.device)
+    ops.gemm_av(A, _blk(p, x, FP8), W)
+    exact = a @ x
+    assert np.all(np.abs(_host(W) - exact) <= 1e-5 * (np.abs(a) @ np.abs(x)) + 1e-30)
+
+
+@pytest.mark.parametrize("fmt", [F32, F64])
+def test_gemm_simt_vs_oracle(ofrr_gpu, oracle, fmt):
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(5)
+    rows, cols, k = 333, 450, 20
+    a = o.round_to(rng.standard_normal((rows, cols)), fmt)
+    x = o.round_to(rng.random((cols, k)), fmt)
+    A = _op(p, a, fmt)
+    W = ops.new_block(rows, k, p.FpFormat(fmt), A.device)
+    ops.gemm_av(A, _blk(p, x, fmt), W)
+    ref = o.mixed_gemm(a, x, fmt, fmt, fmt)
+    tol = 1e-5 if fmt == F32 else 1e-13
+    np.testing.assert_allclose(_host(W), ref, rtol=tol, atol=tol * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("pname,pol", [("tc-bf16", (BF16, F32, F32)), ("tc-f16", (F16, F32, F32)),
+                                       ("native-f16", (F16, F16, F16)), ("full-f32", (F32, F32, F32)),
+                                       ("full-f64", (F64, F64, F64))])
+def test_scale_columns_bitwise(ofrr_gpu, oracle, pname, pol):
+    """K2 reproduces ofrr/precision.py:159-169 bit for bit."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    s, c, a_ = pol
+    rng = np.random.default_rng(9)
+    x = o.round_to(rng.standard_normal((1234, 7)) * 40, s)
+    x[:, 3] = 0.0
+    X = _blk(p, x, s)
+    colmax = torch.tensor(np.max(np.abs(x), axis=0), dtype=torch.float64, device="cuda")
+    ops.scale_columns(X, colmax, p.FpFormat(c))
+    np.testing.assert_array_equal(_host(X), o.scale_columns_inf(x, o.Pol(s, c, a_)))
+
+
+@pytest.mark.parametrize("pol", [(BF16, F32, F32), (F16, F32, F32), (F16, F16, F16), (F16, F16, F32),
+                                 (F32, F32, F32), (F64, F64, F64)])
+@pytest.mark.parametrize("n,k", [(300, 12), (5000, 64), (20000, 40)])
+def test_hessenberg_bitwise(ofrr_gpu, oracle, pol, n, k):
+    """K3 reproduces ofrr/basis.py:151-196 bit for bit: Q, pivots, kept."""
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    s, c, a_ = pol
+    rng = np.random.default_rng(n + k)
+    x = o.round_to(rng.random((n, k)), s)
+    h = ops.hessenberg(_blk(p, x, s), p.FpFormat(s), p.FpFormat(c), o.EPS[s])
+    nk = int(h.n_kept.item())
+    q, piv, kept = o.hessenberg_basis(x, o.Pol(s, c, a_))
+    assert nk == q.shape[1]
+    np.testing.assert_array_equal(h.pivots[:nk].cpu().numpy(), piv)
+    np.testing.assert_array_equal(h.kept[:k].cpu().numpy().astype(bool), kept)
+    np.testing.assert_array_equal(_host(h.Q, nk), q)
+
+
+@pytest.mark.parametrize("case", ["f64_20x6", "f16_25x8", "mh_64x10", "f32_64x10", "tc16_300x12", "dep_6x3",
+                                  "ties_8x3"])
+def test_hessenberg_golden(ofrr_gpu, golden, case):
+    """K3 against the reference's own outputs (tests/golden)."""
+    from paper_2505_00281_b200 import ops
+    p = ofrr_gpu
+    key = f"hess/{case}/left"
+    s, c, _ = (int(v) for v in golden[key + "/policy"])
+    x = golden[key + "/x"]
+    eps = {0: 2.0**-10, 1: 2.0**-23, 2: 2.0**-52}[s]
+    h = ops.hessenberg(_blk(p, x, s), p.FpFormat(s), p.FpFormat(c), eps)
+    nk = int(h.n_kept.item())
+    np.testing.assert_array_equal(_host(h.Q, nk), golden[key + "/q"])
+    np.testing.assert_array_equal(h.pivots[:nk].cpu().numpy(), golden[key + "/pivots"])
+    np.testing.assert_array_equal(h.kept[: x.shape[1]].cpu().numpy().astype(bool), golden[key + "/kept"])
+
+
+@pytest.mark.parametrize("fmt,out", [(BF16, F64), (F16, F32), (F32, F64), (F64, F64)])
+def test_gram_vs_fp64(ofrr_gpu, oracle, fmt, out):
+    """K4: U^T W and U^T U (fp64 sums of exact products), rounded to the projection format."""
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(fmt * 10 + out)
+    n, k = 9000, 70
+    u = o.round_to(rng.standard_normal((n, k)), fmt)
+    w = o.round_to(rng.standard_normal((n, k)), fmt)
+    G1, G2 = ops.gram(_blk(p, u, fmt), _blk(p, w, fmt), p.FpFormat(out))
+    g1 = G1.cpu().numpy().T
+    g2 = G2.cpu().numpy().T
+    tol = 1e-12 if out == F64 else 2e-7
+    np.testing.assert_allclose(g1, o.round_to(u.T @ w, out), rtol=tol, atol=tol * np.abs(u.T @ w).max())
+    np.testing.assert_allclose(g2, o.round_to(u.T @ u, out), rtol=tol, atol=tol * np.abs(u.T @ u).max())
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 12, 40])
+def test_sym_eig_golden(ofrr_gpu, golden, n):
+    """K5 sym_eig vs the reference's Jacobi results (ordering and sign rule included)."""
+    p = ofrr_gpu
+    r = p.sym_eig(golden[f"symeig/{n}/s"])
+    np.testing.assert_allclose(r.values, golden[f"symeig/{n}/vals"], rtol=1e-12, atol=1e-12 * n)
+    np.testing.assert_allclose(r.vectors, golden[f"symeig/{n}/vecs"], atol=1e-9)
+
+
+@pytest.mark.parametrize("n", ["2", "6", "15", "33", "rankdef"])
+def test_gen_eig_golden(ofrr_gpu, golden, n):
+    p = ofrr_gpu
+    r = p.sym_def_gen_eig(golden[f"geneig/{n}/b"], golden[f"geneig/{n}/m"])
+    np.testing.assert_allclose(r.values, golden[f"geneig/{n}/vals"], rtol=1e-10, atol=1e-11)
+    np.testing.assert_allclose(r.vectors, golden[f"geneig/{n}/vecs"], rtol=1e-8, atol=1e-9)
+
+
+@pytest.mark.parametrize("k", [64, 100, 128, 200])
+def test_gen_eig_large_vs_lapack(ofrr_gpu, k):
+    """K5 at the basis widths of the BASELINE configs (k = 64 / 128; 200 / 400 for SVD)."""
+    import scipy.linalg
+    p = ofrr_gpu
+    rng = np.random.default_rng(k)
+    b = rng.standard_normal((k, k))
+    b = (b + b.T) / 2
+    r = rng.standard_normal((k, k))
+    m = r.T @ r + 0.5 * np.eye(k)
+    res = p.sym_def_gen_eig(b, m)
+    ref = np.sort(scipy.linalg.eigh(b, m, eigvals_only=True))[::-1]
+    np.testing.assert_allclose(res.values, ref, atol=1e-9 * np.abs(ref).max())
+    g = res.vectors.T @ m @ res.vectors
+    np.testing.assert_allclose(g, np.eye(k), atol=1e-8)
+
+
+def test_ritz_and_residual(ofrr_gpu, oracle):
+    """K6 (U Y in fp64 + storage rounding) and K7 (FP64 residual) vs numpy."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(1)
+    n, k = 3000, 40
+    u = o.round_to(rng.standard_normal((n, k)), BF16)
+    y = rng.standard_normal((k, k))
+    U = _blk(p, u, BF16)
+    Y = torch.tensor(np.ascontiguousarray(y.T), device="cuda")
+    r_dev = torch.tensor([30], dtype=torch.int32, device="cuda")
+    U64, X = ops.ritz(U, Y, k, r_dev, k, 1.0, want64=True, x_fmt=p.FpFormat.BF16)
+    ut = u @ y[:, :30]
+    np.testing.assert_allclose(_host(U64)[:, :30], ut, rtol=1e-12, atol=1e-12 * np.abs(ut).max())
+    assert not _host(U64)[:, 30:].any()
+    np.testing.assert_array_equal(_host(X)[:, :30], o.round_to(_host(U64)[:, :30], BF16))
+    # residual
+    a = rng.standard_normal((n, n))
+    a = o.round_to((a + a.T) / 2, BF16)
+    A = _op(p, a, BF16)
+    lam = rng.standard_normal(30)
+    res = ops.residual_eig(A, U64, torch.tensor(lam, device="cuda"), None, 30).cpu().numpy()
+    ref = np.linalg.norm(a @ ut - ut * lam[None, :], axis=0) / np.abs(lam)
+    np.testing.assert_allclose(res, ref, rtol=1e-10)
+
+
+@pytest.mark.parametrize("n", [1024, 1000])
+def test_generator_bitwise(ofrr_gpu, oracle, n):
+    """K8 evaluates the synthetic matrix bit for bit like the host formula."""
+    p, o = ofrr_gpu, oracle
+    lam = p.geometric_spectrum(n, 10, 20)
+    for fmt in (F64, BF16):
+        m, f = p.synthetic_symmetric(lam, p.FpFormat(fmt), seed=5)
+        got = m.data
+        ref = o.sym_from_factors(n, f.hadamard, f.c, f.s, f.Wf, f.Mf, fmt)
+        np.testing.assert_array_equal(got, ref)
+    # the spectrum is the prescribed one
+    ev = np.sort(np.linalg.eigvalsh(o.sym_from_factors(n, f.hadamard, f.c, f.s, f.Wf, f.Mf, F64)))[::-1]
+    np.testing.assert_allclose(ev[:50], lam[:50], atol=1e-13)
