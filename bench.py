@@ -32,10 +32,14 @@ sys.path.insert(0, ROOT)
 
 SEED = 20240901
 CONFIGS = {
-    "c2": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-2,
-               name="synthetic dense symmetric 16384x16384, geometric spectrum, top-32, k=64, "
-                    "bf16 basis / fp64 Gram (BASELINE configs[1])"),
-    "c3": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-2,
+    "c2": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-2, policy="full-f32",
+               name="synthetic dense symmetric 16384x16384 (bf16 operator), geometric spectrum, top-32, k=64, "
+                    "bf16 tensor-core products with the basis as 3 bf16 slices (fp32-accurate) / fp64 Gram "
+                    "(BASELINE configs[1])"),
+    "c2-bf16": dict(n=16384, top=32, k=64, fmt="BF16", tol=2e-2, policy="tc-bf16",
+                    name="synthetic dense symmetric 16384x16384, geometric spectrum, top-32, k=64, "
+                         "pure bf16 basis (floor ~1.7e-2) / fp64 Gram"),
+    "c3": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-2, policy="tc-bf16",
                name="synthetic dense symmetric 65536x65536, geometric spectrum, top-64, k=128, "
                     "bf16 basis / fp64 Gram (BASELINE configs[2], bf16 rung)"),
 }
@@ -209,8 +213,7 @@ def run_ours(args, cfg):
     r0, r1 = comm.row_range(n)
     A, _ = p.synthetic_symmetric(lam, fmt, seed=SEED, device=dev, row0=r0, rows=r1 - r0)
     icfg = p.IterConfig(k=k, m=MAX_OUTER, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
-                        policy=p.TC_BF16 if fmt == p.FpFormat.BF16 else p.POLICY_PRESETS["tc-f16"],
-                        seed=SEED, tol=tol, top=top)
+                        policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=tol, top=top)
 
     def solve(stats=None):
         return p.subspace_iter_eig(A, icfg, stats=stats, comm=comm, n_global=n)
@@ -289,7 +292,7 @@ def run_ours(args, cfg):
         "metric": "OFRR top-k eig time-to-tol", "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": cfg["name"], "n": n, "top": top, "k": k, "tol": tol,
+        "config": {"workload": cfg["name"], "n": n, "top": top, "k": k, "tol": tol, "policy": cfg["policy"],
                    "outer_iterations_per_solve": stats.iterations and stats.iterations,
                    "a_passes_per_solve": stats.a_passes / args.steps,
                    "converged": bool(stats.converged),

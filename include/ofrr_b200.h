@@ -76,6 +76,25 @@ int ofrr_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_f
                  double* colmax, int* flags, void* workspace, size_t workspace_bytes,
                  void* stream);
 
+/* K1 with a second output: W2 = the same product rounded to out_fmt2 (e.g. the fp32
+ * accumulator itself, kept for the residual estimate of ofrr_residual_estimate). */
+int ofrr_gemm_av2(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose,
+                  const void* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt,
+                  double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* K1, fp32 block on the bf16 tensor cores: W = A X with A bf16 and X fp32.  X is split into
+ * three bf16 slices [X_hi | X_mid | X_lo] (exact: 3 x 8 bits = the fp32 significand), the
+ * n x 3k product runs in ONE pass over A (3k <= 256), and the slices are summed in fp32 in
+ * the finalize.  This is the device form of the reference's full-f32 policy
+ * (ofrr/precision.py:79) for an operator stored in bf16 -- fp32-accurate products at
+ * bf16 HBM traffic. */
+size_t ofrr_gemm_av_split_workspace(int64_t rows, int64_t cols, int k);
+int ofrr_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
+                       const float* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt,
+                       double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* K2: X[:,j] <- round_s(round_c(X[:,j] / colmax[j])) for colmax[j] != 0, in place.
  * Replaces ofrr/precision.py:159-169 scale_columns_inf. */
 int ofrr_scale_columns(void* X, int64_t n, int k, int64_t ldx, int storage, int compute,
@@ -157,6 +176,16 @@ int ofrr_residual_pair(const void* A, int64_t rows, int64_t cols, int64_t lda, i
                        double* res, int accumulate_max, void* workspace,
                        size_t workspace_bytes, void* stream);
 
+/* K7e: per-iteration residual estimate without another pass over A:
+ *   res[j] = || (W - lambda_j U) y_j ||_2 / |lambda_j|,  W = A U in its accumulation format
+ * (mode 0; mode 2 returns raw sums of squares for a cross-rank all-reduce).  Used only to
+ * decide when to stop; the reported residuals are always the FP64 ones of K7. */
+size_t ofrr_residual_estimate_workspace(int64_t n, int r);
+int ofrr_residual_estimate(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt,
+                           int64_t n, int kp, const double* Y, int ldy, const double* vals,
+                           const int* r_dev, int r_max, double* res, int mode, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------------
  * K8: synthetic symmetric matrix A = S C S + Wf Mf^T + Mf Wf^T (FP64, rounded once to
  * a_fmt, row-major), where C[i,j] = c[i xor j] (n a power of two; Walsh-Hadamard
@@ -167,6 +196,12 @@ int ofrr_residual_pair(const void* A, int64_t rows, int64_t cols, int64_t lda, i
 int ofrr_generate_sym(int64_t n, int64_t row0, int64_t rows, int hadamard, const double* c,
                       const double* s, const double* Wf, const double* Mf, int r, void* A,
                       int64_t lda, int a_fmt, void* stream);
+
+/* Start block X0 = numpy.random.default_rng(seed).random((n, k)) rounded to fmt
+ * (ofrr/driver.py:97-99, ofrr/driver.py:150-152), generated on the device bit for bit from
+ * the PCG64 state (state, inc) that numpy's SeedSequence derives from the seed. */
+int ofrr_start_block_pcg64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                           int64_t n, int k, void* X, int64_t ldx, int fmt, void* stream);
 
 /* utility: round/convert a column-major block between formats (ofrr/precision.py:90-104) */
 int ofrr_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int dst_fmt,

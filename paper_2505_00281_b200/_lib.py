@@ -36,6 +36,14 @@ _SIGS = {
     "ofrr_gemm_av_workspace": ([c_i64, c_i64, c_int, c_int, c_int], c_sz),
     "ofrr_gemm_av": ([c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_int,
                       c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "ofrr_gemm_av2": ([c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_int,
+                       c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_sz, c_vp], c_int),
+    "ofrr_gemm_av_split_workspace": ([c_i64, c_i64, c_int], c_sz),
+    "ofrr_gemm_av_split": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_vp,
+                            c_vp, c_i64, c_int, c_vp, c_sz, c_vp], c_int),
+    "ofrr_residual_estimate_workspace": ([c_i64, c_int], c_sz),
+    "ofrr_residual_estimate": ([c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_i64, c_int, c_vp, c_int, c_vp, c_vp,
+                                c_int, c_vp, c_int, c_vp, c_sz, c_vp], c_int),
     "ofrr_scale_columns": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_vp, c_vp], c_int),
     "ofrr_hessenberg_workspace": ([c_i64, c_int, c_int], c_sz),
     "ofrr_hessenberg": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp,
@@ -55,6 +63,8 @@ _SIGS = {
                             c_int, c_vp, c_int, c_vp, c_sz, c_vp], c_int),
     "ofrr_generate_sym": ([c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_i64, c_int,
                            c_vp], c_int),
+    "ofrr_start_block_pcg64": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, c_i64, c_int,
+                                c_vp, c_i64, c_int, c_vp], c_int),
     "ofrr_convert": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_i64, c_i64, c_vp, c_vp], c_int),
     "ofrr_transpose_convert": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_i64, c_i64, c_vp, c_vp], c_int),
     "ofrr_host_gemm_mixed": ([c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int,

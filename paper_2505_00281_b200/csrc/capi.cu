@@ -10,9 +10,19 @@ namespace ofrr {
 // implemented in the kernel translation units
 size_t tc_workspace(int64_t rows, int64_t cols, int k, int a_fmt);
 int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* X, int64_t ldx, int k,
-               void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes, cudaStream_t st);
+               void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes, cudaStream_t st,
+               void* W2, int64_t ldw2, int out_fmt2, int nsplit);
+size_t split_workspace(int64_t rows, int64_t cols, int k);
+int tc_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, const float* X, int64_t ldx, int k,
+                     void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes,
+                     cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2);
 int simt_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const void* X,
-                 int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, cudaStream_t st);
+                 int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, cudaStream_t st,
+                 void* W2, int64_t ldw2, int out_fmt2);
+size_t resid_est_ws(int64_t n, int r);
+int resid_est(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt, int64_t n, int kp,
+              const double* Y, int ldy, const double* vals, const int* r_dev, int r_max, double* res, int mode,
+              void* ws, size_t ws_bytes, cudaStream_t st);
 size_t residual_ws(int64_t rows, int r);
 int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const double* Xv,
                   int64_t ldx, const double* Yv, int64_t ldy, const double* vals, const int* r_dev, int r_max,
@@ -37,6 +47,8 @@ int ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const
                  cudaStream_t st);
 int generate_sym(int64_t n, int64_t row0, int64_t rows, int hadamard, const double* c, const double* s,
                  const double* Wf, const double* Mf, int r, void* A, int64_t lda, int a_fmt, cudaStream_t st);
+int start_block_pcg64(unsigned long long s_hi, unsigned long long s_lo, unsigned long long i_hi,
+                      unsigned long long i_lo, int64_t n, int k, void* X, int64_t ldx, int fmt, cudaStream_t st);
 }  // namespace ofrr
 
 using namespace ofrr;
@@ -75,18 +87,20 @@ size_t ofrr_gemm_av_workspace(int64_t rows, int64_t cols, int k, int a_fmt, int 
   return 256;
 }
 
-int ofrr_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const void* X,
-                 int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* workspace,
-                 size_t workspace_bytes, void* stream) {
-  if (!valid_fmt(a_fmt) || !valid_fmt(out_fmt) || k < 0 || rows < 0 || cols < 0) {
+int ofrr_gemm_av2(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const void* X,
+                  int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2,
+                  int64_t ldw2, int out_fmt2, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!valid_fmt(a_fmt) || !valid_fmt(out_fmt) || !valid_fmt(out_fmt2) || k < 0 || rows < 0 || cols < 0) {
     ofrr_set_error("gemm_av: invalid arguments");
     return OFRR_ERR_INVALID;
   }
   if (rows == 0 || cols == 0 || k == 0) {
     // empty inner dimension -> zeros (ofrr/_kernels.pyx:70-74)
     const int64_t m = transpose ? cols : rows;
-    if (m > 0 && k > 0 && cols * rows == 0)
+    if (m > 0 && k > 0 && cols * rows == 0) {
       OFRR_CUDA_TRY(cudaMemset2DAsync(W, ldw * fmt_bytes(out_fmt), 0, m * fmt_bytes(out_fmt), k, S(stream)));
+      if (W2) OFRR_CUDA_TRY(cudaMemset2DAsync(W2, ldw2 * fmt_bytes(out_fmt2), 0, m * fmt_bytes(out_fmt2), k, S(stream)));
+    }
     return OFRR_OK;
   }
   if (tc_fmt(a_fmt) && !transpose) {
@@ -96,9 +110,29 @@ int ofrr_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_f
       return OFRR_ERR_INVALID;
     }
     return tc_gemm_av(A, rows, cols, lda, a_fmt, X, ldx, k, W, ldw, out_fmt, colmax, flags, workspace,
-                      workspace_bytes, S(stream));
+                      workspace_bytes, S(stream), W2, ldw2, out_fmt2, 1);
   }
-  return simt_gemm_av(A, rows, cols, lda, a_fmt, transpose, X, ldx, k, W, ldw, out_fmt, colmax, flags, S(stream));
+  return simt_gemm_av(A, rows, cols, lda, a_fmt, transpose, X, ldx, k, W, ldw, out_fmt, colmax, flags, S(stream),
+                      W2, ldw2, out_fmt2);
+}
+
+size_t ofrr_gemm_av_split_workspace(int64_t rows, int64_t cols, int k) { return split_workspace(rows, cols, k); }
+
+int ofrr_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const float* X, int64_t ldx,
+                       int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2,
+                       int out_fmt2, void* workspace, size_t workspace_bytes, void* stream) {
+  if (a_fmt != BF16) { ofrr_set_error("gemm_av_split: A must be bf16"); return OFRR_ERR_UNSUPPORTED; }
+  if (rows <= 0 || cols <= 0 || k <= 0) return OFRR_OK;
+  if ((lda * 2) % 16) { ofrr_set_error("gemm_av_split: lda must be a multiple of 8"); return OFRR_ERR_INVALID; }
+  return tc_gemm_av_split(A, rows, cols, lda, X, ldx, k, W, ldw, out_fmt, colmax, flags, workspace, workspace_bytes,
+                          S(stream), W2, ldw2, out_fmt2);
+}
+
+int ofrr_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const void* X,
+                 int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  return ofrr_gemm_av2(A, rows, cols, lda, a_fmt, transpose, X, ldx, k, W, ldw, out_fmt, colmax, flags, nullptr, 0,
+                       out_fmt, workspace, workspace_bytes, stream);
 }
 
 int ofrr_scale_columns(void* X, int64_t n, int k, int64_t ldx, int storage, int compute, const double* colmax,
@@ -146,6 +180,15 @@ int ofrr_ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, 
 
 size_t ofrr_residual_workspace(int64_t rows, int r) { return residual_ws(rows, r); }
 
+size_t ofrr_residual_estimate_workspace(int64_t n, int r) { return resid_est_ws(n, r); }
+
+int ofrr_residual_estimate(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt, int64_t n,
+                           int kp, const double* Y, int ldy, const double* vals, const int* r_dev, int r_max,
+                           double* res, int mode, void* workspace, size_t workspace_bytes, void* stream) {
+  return resid_est(U, ldu, u_fmt, W, ldw, w_fmt, n, kp, Y, ldy, vals, r_dev, r_max, res, mode, workspace,
+                   workspace_bytes, S(stream));
+}
+
 int ofrr_residual_eig(const void* A, int64_t n, int64_t lda, int a_fmt, const double* V, int64_t ldv,
                       const double* vals, const int* r_dev, int r_max, double* res, void* workspace,
                       size_t workspace_bytes, void* stream) {
@@ -164,6 +207,12 @@ int ofrr_residual_pair(const void* A, int64_t rows, int64_t cols, int64_t lda, i
 int ofrr_generate_sym(int64_t n, int64_t row0, int64_t rows, int hadamard, const double* c, const double* s,
                       const double* Wf, const double* Mf, int r, void* A, int64_t lda, int a_fmt, void* stream) {
   return generate_sym(n, row0, rows, hadamard, c, s, Wf, Mf, r, A, lda, a_fmt, S(stream));
+}
+
+int ofrr_start_block_pcg64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t n, int k,
+                           void* X, int64_t ldx, int fmt, void* stream) {
+  if (!valid_fmt(fmt) || n < 0 || k < 0) { ofrr_set_error("start_block: invalid arguments"); return OFRR_ERR_INVALID; }
+  return start_block_pcg64(state_hi, state_lo, inc_hi, inc_lo, n, k, X, ldx, fmt, S(stream));
 }
 
 int ofrr_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int dst_fmt, int64_t ld_dst, int64_t n,

@@ -185,7 +185,10 @@ static constexpr int FIN_COLS = 8;   // columns per finalize block
 __global__ void __launch_bounds__(256)
     k_finalize(const float* __restrict__ ws, int BN, int kblocks, long long total_iters, int G,
                int max_slots, int64_t rows, int k, void* __restrict__ W, int64_t ldw, int out_fmt,
-               double* __restrict__ colmax, int* __restrict__ flags) {
+               double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
+               int out_fmt2, int nsplit) {
+  // nsplit > 1: the product was taken against [X_hi | X_mid | X_lo] (bf16 slices of an fp32
+  // block, see k_split_bf16); output column j sums tile columns j + s*k, lowest slice first
   __shared__ float smax[8][FIN_COLS];
   const int t = blockIdx.x;
   const int j0 = blockIdx.y * FIN_COLS;
@@ -203,12 +206,14 @@ __global__ void __launch_bounds__(256)
   float s[FIN_COLS];
 #pragma unroll
   for (int i = 0; i < FIN_COLS; ++i) s[i] = 0.f;
-  for (long long c = c_lo; c <= c_hi; ++c) {
-    const int slot = t - (int)(seg_begin(c, total_iters, G) / kblocks);
-    const float* src = ws + ((size_t)c * max_slots + slot) * (size_t)(TILE_M * BN) + row;
+  for (int sl = nsplit - 1; sl >= 0; --sl) {
+    for (long long c = c_lo; c <= c_hi; ++c) {
+      const int slot = t - (int)(seg_begin(c, total_iters, G) / kblocks);
+      const float* src = ws + ((size_t)c * max_slots + slot) * (size_t)(TILE_M * BN) + row + (size_t)sl * k * TILE_M;
 #pragma unroll
-    for (int i = 0; i < FIN_COLS; ++i)
-      if (j0 + i < k) s[i] += src[(size_t)(j0 + i) * TILE_M];
+      for (int i = 0; i < FIN_COLS; ++i)
+        if (j0 + i < k) s[i] += src[(size_t)(j0 + i) * TILE_M];
+    }
   }
   int bad = 0;
 #pragma unroll
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(256)
     if (valid && j < k) {
       const float w = rndf(s[i], out_fmt);
       st_fmt(W, (int64_t)j * ldw + grow, out_fmt, (double)w);
+      if (W2) st_fmt(W2, (int64_t)j * ldw2 + grow, out_fmt2, (double)rndf(s[i], out_fmt2));
       if (!isfinite(w)) bad = 1;
       a = (w != w) ? INFINITY : fabsf(w);
     }
@@ -324,7 +330,7 @@ static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPl
 
 int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* X,
                int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags,
-               void* ws, size_t ws_bytes, cudaStream_t st) {
+               void* ws, size_t ws_bytes, cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2, int nsplit) {
   TcPlan p = plan_tc(rows, cols, k, a_fmt);
   if (ws_bytes < p.ws_bytes || ws == nullptr) {
     ofrr_set_error("gemm_av: workspace too small (%zu < %zu)", ws_bytes, p.ws_bytes);
@@ -345,10 +351,55 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
     default: rc = fp8 ? launch_tc_bn<256, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<256, false>(tA, tX, p, (float*)ws, idesc, st); break;
   }
   if (rc) return rc;
-  k_finalize<<<dim3(p.m_tiles, (k + FIN_COLS - 1) / FIN_COLS), 256, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
-                                        rows, k, W, ldw, out_fmt, colmax, flags);
+  k_finalize<<<dim3(p.m_tiles, (k / nsplit + FIN_COLS - 1) / FIN_COLS), 256, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
+                                        rows, k / nsplit, W, ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
+                                        nsplit);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// fp32 blocks on the bf16 tensor cores: X (n x k fp32, column-major) -> [X_hi|X_mid|X_lo]
+// (n x 3k bf16): x_hi = bf16(x), x_mid = bf16(x - x_hi), x_lo = bf16(x - x_hi - x_mid).  The
+// residues are exact in fp32, so the three slices carry the full 24-bit significand and
+// A (bf16) times each slice is an exact-product, fp32-accumulated tensor-core product.
+// ---------------------------------------------------------------------------------
+__global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n, int k,
+                             __nv_bfloat16* __restrict__ Xs, int64_t lds) {
+  const int j = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = X[(int64_t)j * ldx + i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(h);
+    const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+    const float r2 = r1 - __bfloat162float(m);
+    Xs[(int64_t)j * lds + i] = h;
+    Xs[(int64_t)(k + j) * lds + i] = m;
+    Xs[(int64_t)(2 * k + j) * lds + i] = __float2bfloat16_rn(r2);
+  }
+}
+
+size_t split_workspace(int64_t rows, int64_t cols, int k) {
+  const int64_t lds = (cols + 63) / 64 * 64;
+  return (size_t)3 * k * lds * 2 + 1024 + tc_workspace(rows, cols, 3 * k, BF16);
+}
+
+int tc_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, const float* X, int64_t ldx, int k,
+                     void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes,
+                     cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2) {
+  if (3 * k > 256) {
+    ofrr_set_error("gemm_av: fp32 block on bf16 tensor cores needs 3k <= 256 (k=%d)", k);
+    return OFRR_ERR_UNSUPPORTED;
+  }
+  if (ws_bytes < split_workspace(rows, cols, k)) { ofrr_set_error("gemm_av split: workspace too small"); return OFRR_ERR_INVALID; }
+  const int64_t lds = (cols + 63) / 64 * 64;
+  __nv_bfloat16* Xs = (__nv_bfloat16*)ws;
+  uint8_t* rest = (uint8_t*)ws + (((size_t)3 * k * lds * 2 + 1023) & ~size_t(1023));
+  unsigned gx = (unsigned)std::min<int64_t>((cols + 255) / 256, 64);
+  k_split_bf16<<<dim3(gx, k), 256, 0, st>>>(X, ldx, cols, k, Xs, lds);
+  OFRR_CHECK_LAUNCH();
+  return tc_gemm_av(A, rows, cols, lda, BF16, Xs, lds, 3 * k, W, ldw, out_fmt, colmax, flags, rest,
+                    ws_bytes - (rest - (uint8_t*)ws), st, W2, ldw2, out_fmt2, 3);
 }
 
 }  // namespace ofrr

@@ -60,19 +60,25 @@ __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* 
 
 template <typename T>
 __global__ void __launch_bounds__(HT)
-    k_hessenberg(const T* __restrict__ X, int64_t n, int k, int64_t ldx, T* __restrict__ Xw, int64_t ldw,
+    k_hessenberg(const T* __restrict__ X, int64_t n, int k, int64_t ldx, T* __restrict__ Xg, int64_t ldg,
                  int storage, int compute, double tol, T* __restrict__ Q, int64_t ldq,
-                 int64_t* __restrict__ pivots, int* __restrict__ kept, int* __restrict__ n_kept, HessWs ws) {
+                 int64_t* __restrict__ pivots, int* __restrict__ kept, int* __restrict__ n_kept, HessWs ws,
+                 int in_smem) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sv[HT / 32];
   __shared__ long long si[HT / 32];
-  extern __shared__ double prow[];  // pivot row values, k entries
+  extern __shared__ double dyn[];
+  double* prow = dyn;                                        // pivot row values, k entries
 
   const int G = gridDim.x, c = blockIdx.x;
   const int64_t rows_per = (n + G - 1) / G;
   const int64_t r0 = std::min<int64_t>(n, (int64_t)c * rows_per);
   const int64_t r1 = std::min<int64_t>(n, r0 + rows_per);
   const int64_t nr = r1 - r0;
+  // my working rows: in shared memory when they fit (column-major, ld rows_per), else in
+  // the global workspace.  Xw is indexed with global row numbers.
+  const int64_t ldw = in_smem ? rows_per : ldg;
+  T* Xw = in_smem ? reinterpret_cast<T*>(dyn + k) - r0 : Xg;
 
   // prologue: private copy of my rows, free flags, candidate for column 0
   for (int j = 0; j < k; ++j)
@@ -106,19 +112,37 @@ __global__ void __launch_bounds__(HT)
   int nk = 0;
   for (int j = 0; j < k; ++j) {
     const int buf = j & 1;
-    // reduce the candidates (ascending CTA = ascending rows)
-    double best = -1.0;
-    long long r = -1;
-    int owner = -1;
-    for (int cc = 0; cc < G; ++cc) {
-      const long long oi = ws.cand_idx[buf * G + cc];
-      const double ov = ws.cand_val[buf * G + cc];
-      if (oi >= 0 && (r < 0 || ov > best)) { best = ov; r = oi; owner = cc; }
+    // reduce the candidates: warp 0, lanes strided over CTAs; max value, ties -> lowest row
+    // (CTA row blocks ascend, so the lowest row is the reference's np.argmax choice)
+    __shared__ double s_best;
+    __shared__ long long s_r;
+    __shared__ int s_owner;
+    if (threadIdx.x < 32) {
+      double bv = -1.0;
+      long long bi = -1;
+      int bo = -1;
+      for (int cc = threadIdx.x; cc < G; cc += 32) {
+        const long long oi = __ldcg(&ws.cand_idx[buf * G + cc]);
+        const double ov = __ldcg(&ws.cand_val[buf * G + cc]);
+        if (oi >= 0 && (bi < 0 || ov > bv)) { bv = ov; bi = oi; bo = cc; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
+        if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; bo = oo; }
+      }
+      if (threadIdx.x == 0) { s_best = bv; s_r = bi; s_owner = bo; }
     }
+    __syncthreads();
+    const double best = s_best;
+    const long long r = s_r;
+    const int owner = s_owner;
     // ofrr/basis.py:178-180: skip when no free row or |pivot| < tol (NaN pivots skip too)
     const bool skip = (r < 0) || !(best >= tol);
     if (!skip) {
-      for (int cc = j + threadIdx.x; cc < k; cc += HT) prow[cc] = ws.cand_row[((int64_t)buf * G + owner) * k + cc];
+      for (int cc = j + threadIdx.x; cc < k; cc += HT) prow[cc] = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
       __syncthreads();
       const double piv = prow[j];
       // ofrr/basis.py:181-187: v = round_s(round_c(v / piv)); v[r] = 1
@@ -160,7 +184,7 @@ __global__ void __launch_bounds__(HT)
 static int hess_grid(int64_t n) {
   int sms = ofrr_device_sm_count(-1);
   if (sms <= 0) sms = 148;
-  int64_t g = (n + 63) / 64;  // at least 64 rows per CTA
+  int64_t g = (n + 127) / 128;  // at least 128 rows per CTA
   return (int)std::max<int64_t>(1, std::min<int64_t>(sms, g));
 }
 
@@ -190,10 +214,19 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   const T* Xp = (const T*)X;
   T* Qp = (T*)Q;
   int64_t ldw = n;
-  size_t shmem = (size_t)k * sizeof(double);
+  const int64_t rows_per = (n + G - 1) / G;
+  const size_t tile = (size_t)rows_per * k * sizeof(T);
+  int in_smem = tile <= (size_t)160 * 1024 ? 1 : 0;
+  size_t shmem = (size_t)k * sizeof(double) + (in_smem ? tile + 16 : 0);
+  static bool attr = false;
+  if (!attr) {
+    OFRR_CUDA_TRY(cudaFuncSetAttribute((const void*)k_hessenberg<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+    attr = true;
+  }
   void* args[] = {(void*)&Xp, (void*)&n, (void*)&k, (void*)&ldx, (void*)&Xw, (void*)&ldw, (void*)&storage,
                   (void*)&compute, (void*)&tol, (void*)&Qp, (void*)&ldq, (void*)&pivots, (void*)&kept,
-                  (void*)&n_kept, (void*)&h};
+                  (void*)&n_kept, (void*)&h, (void*)&in_smem};
   OFRR_CUDA_TRY(cudaMemsetAsync(kept, 0, sizeof(int) * k, st));
   OFRR_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hessenberg<T>, dim3(G), dim3(HT), args, shmem, st));
   return OFRR_OK;

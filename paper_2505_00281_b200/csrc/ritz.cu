@@ -81,6 +81,148 @@ int ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const
 }
 
 // ---------------------------------------------------------------------------------
+// K7e: residual estimate for the per-iteration convergence test.
+//   r_j = || (W - lambda_j U) y_j ||_2      with W = A U kept in the accumulation format
+// (fp32 from the tensor cores, fp64 on the fp64 path) -- since A (U y) = (A U) y, this is
+// the Ritz residual up to the accumulation error of W, without another pass over A.
+// Partial sums of squares per 64-row block -> part[block * r_max + j] (fixed order).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_resid_est(const void* __restrict__ U, int64_t ldu, int u_fmt, const void* __restrict__ W, int64_t ldw,
+                int w_fmt, int64_t n, int kp, const double* __restrict__ Y, int ldy, const int* __restrict__ r_dev,
+                int r_max, const double* __restrict__ vals, double* __restrict__ part) {
+  __shared__ double Us[16][65];
+  __shared__ double Ws[16][65];
+  __shared__ double Ys[16][65];
+  __shared__ double csum[16][64];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t m0 = (int64_t)blockIdx.x * 64;
+  const int n0 = blockIdx.y * 64;
+  const int r = r_dev ? min(r_max, *r_dev) : r_max;
+  double au[4][4] = {}, aw[4][4] = {};
+  for (int l0 = 0; l0 < kp; l0 += 16) {
+    for (int e = tid; e < 16 * 64; e += 256) {
+      const int rr = e & 63, ll = e >> 6;
+      const int64_t gi = m0 + rr;
+      const bool ok = gi < n && l0 + ll < kp;
+      Us[ll][rr] = ok ? ld_fmt(U, (int64_t)(l0 + ll) * ldu + gi, u_fmt) : 0.0;
+      Ws[ll][rr] = ok ? ld_fmt(W, (int64_t)(l0 + ll) * ldw + gi, w_fmt) : 0.0;
+      const int gj = n0 + rr;
+      Ys[ll][rr] = (gj < r && l0 + ll < kp) ? Y[(int64_t)gj * ldy + l0 + ll] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ll = 0; ll < 16; ++ll) {
+      double a[4], w[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = Us[ll][ty + 16 * i]; w[i] = Ws[ll][ty + 16 * i]; }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Ys[ll][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { au[i][j] = fma(a[i], b[j], au[i][j]); aw[i][j] = fma(w[i], b[j], aw[i][j]); }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int gj = n0 + tx + 16 * j;
+    double s = 0.0;
+    if (gj < r) {
+      const double lam = vals[gj];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (m0 + ty + 16 * i < n) {
+          const double d = aw[i][j] - lam * au[i][j];
+          s += d * d;
+        }
+    }
+    csum[ty][tx + 16 * j] = s;
+  }
+  __syncthreads();
+  if (tid < 64 && n0 + tid < r_max) {
+    double s = 0.0;
+    for (int y = 0; y < 16; ++y) s += csum[y][tid];
+    part[(int64_t)blockIdx.x * r_max + n0 + tid] = s;
+  }
+}
+
+int residual_reduce(const double* part, int nblocks, int n, const double* vals, const int* r_dev, double* res,
+                    int mode, cudaStream_t st);
+
+size_t resid_est_ws(int64_t n, int r) { return (size_t)((n + 63) / 64) * (size_t)r * sizeof(double); }
+
+int resid_est(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt, int64_t n, int kp,
+              const double* Y, int ldy, const double* vals, const int* r_dev, int r_max, double* res, int mode,
+              void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n <= 0 || r_max <= 0) return OFRR_OK;
+  if (ws_bytes < resid_est_ws(n, r_max)) { ofrr_set_error("residual estimate: workspace too small"); return OFRR_ERR_INVALID; }
+  const int nb = (int)((n + 63) / 64);
+  dim3 grid((unsigned)nb, (unsigned)((r_max + 63) / 64));
+  k_resid_est<<<grid, 256, 0, st>>>(U, ldu, u_fmt, W, ldw, w_fmt, n, kp, Y, ldy, r_dev, r_max, vals, (double*)ws);
+  OFRR_CHECK_LAUNCH();
+  return residual_reduce((double*)ws, nb, r_max, vals, r_dev, res, mode, st);
+}
+
+// ---------------------------------------------------------------------------------
+// Start block X0 = numpy default_rng(seed).random((n, k)) rounded to the storage format
+// (ofrr/driver.py:97-99), generated on the device bit for bit: numpy's PCG64 is a 128-bit
+// LCG (state <- state * M + inc) with the XSL-RR output; random() = (next64 >> 11) * 2^-53,
+// drawn in C order (element [i, j] is draw i*k + j).  Each thread jumps its private copy of
+// the LCG to its first draw (O(log) square-and-multiply, pcg_advance_lcg_128) and walks a
+// contiguous run of draws.
+// ---------------------------------------------------------------------------------
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 lcg_advance(u128 state, u128 delta, u128 mult, u128 plus) {
+  u128 acc_mult = 1, acc_plus = 0;
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_mult *= mult;
+      acc_plus = acc_plus * mult + plus;
+    }
+    plus = (mult + 1) * plus;
+    mult *= mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+__global__ void k_pcg64_block(unsigned long long s_hi, unsigned long long s_lo, unsigned long long i_hi,
+                              unsigned long long i_lo, int64_t n, int k, void* __restrict__ X, int64_t ldx, int fmt,
+                              int per_thread) {
+  const u128 M = ((u128)2549297995355413924ULL << 64) | (u128)4865540595714422341ULL;
+  const u128 inc = ((u128)i_hi << 64) | (u128)i_lo;
+  const int64_t total = n * (int64_t)k;
+  const int64_t d0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * per_thread;
+  if (d0 >= total) return;
+  u128 s = lcg_advance(((u128)s_hi << 64) | (u128)s_lo, (u128)d0, M, inc);
+  const int64_t d1 = d0 + per_thread < total ? d0 + per_thread : total;
+  for (int64_t d = d0; d < d1; ++d) {
+    s = s * M + inc;
+    const unsigned long long hi = (unsigned long long)(s >> 64), lo = (unsigned long long)s;
+    const unsigned rot = (unsigned)(s >> 122);
+    const unsigned long long x = hi ^ lo;
+    const unsigned long long out = (x >> rot) | (x << ((64u - rot) & 63u));
+    const double v = (double)(out >> 11) * (1.0 / 9007199254740992.0);
+    const int64_t i = d / k, j = d - i * k;
+    st_fmt(X, (int64_t)j * ldx + i, fmt, rnd(v, fmt));
+  }
+}
+
+int start_block_pcg64(unsigned long long s_hi, unsigned long long s_lo, unsigned long long i_hi,
+                      unsigned long long i_lo, int64_t n, int k, void* X, int64_t ldx, int fmt, cudaStream_t st) {
+  const int64_t total = n * (int64_t)k;
+  if (total <= 0) return OFRR_OK;
+  const int per = 64;
+  const int64_t threads = (total + per - 1) / per;
+  k_pcg64_block<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(s_hi, s_lo, i_hi, i_lo, n, k, X, ldx, fmt, per);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+// ---------------------------------------------------------------------------------
 // K8: A[i, j] = base(i, j) + sum_s (Wf[i,s] Mf[j,s] + Mf[i,s] Wf[j,s]), FP64 in a fixed
 // order (no FMA contraction), rounded once to a_fmt.  base = s_i s_j c[i ^ j] (Walsh-
 // Hadamard diagonalised) or diag(c).  Rows [row0, row0 + rows) written row-major.

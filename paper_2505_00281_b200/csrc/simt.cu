@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(256)
                 const void* __restrict__ B, int64_t ldb, int n, void* __restrict__ C, int64_t ldc,
                 int out_fmt, double* __restrict__ colmax, int* __restrict__ flags,
                 const double* __restrict__ Y, int64_t ldy, const double* __restrict__ vals,
-                const int* __restrict__ r_dev, double* __restrict__ part) {
+                const int* __restrict__ r_dev, double* __restrict__ part, void* __restrict__ C2, int64_t ldc2,
+                int out_fmt2) {
   __shared__ ACC As[SBK][SBM + 1];
   __shared__ ACC Bs[SBK][SBN + 1];
   __shared__ double cmax[SBN];
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(256)
         if (gr < m && gc < n) {
           const double w = rnd((double)acc[i][j], out_fmt);
           st_fmt(C, (int64_t)gc * ldc + gr, out_fmt, w);
+          if (C2) st_fmt(C2, (int64_t)gc * ldc2 + gr, out_fmt2, rnd((double)acc[i][j], out_fmt2));
           if (!isfinite(w)) { bad = 1; lm = INFINITY; }
           else lm = fmax(lm, fabs(w));
         }
@@ -163,26 +165,33 @@ template <typename TA, typename TB, typename ACC, int MODE>
 static int launch_simt(const void* A, int64_t lda, int transpose, int64_t m, int64_t K, const void* B,
                        int64_t ldb, int n, void* C, int64_t ldc, int out_fmt, double* colmax, int* flags,
                        const double* Y, int64_t ldy, const double* vals, const int* r_dev, double* part,
-                       cudaStream_t st) {
+                       cudaStream_t st, void* C2 = nullptr, int64_t ldc2 = 0, int out_fmt2 = 0) {
   dim3 grid((unsigned)((m + SBM - 1) / SBM), (unsigned)((n + SBN - 1) / SBN));
   k_gemm_simt<TA, TB, ACC, MODE><<<grid, 256, 0, st>>>(A, lda, transpose, m, K, B, ldb, n, C, ldc, out_fmt,
-                                                       colmax, flags, Y, ldy, vals, r_dev, part);
+                                                       colmax, flags, Y, ldy, vals, r_dev, part, C2, ldc2, out_fmt2);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
 
 int simt_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose,
                  const void* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax,
-                 int* flags, cudaStream_t st) {
+                 int* flags, cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2) {
   const int64_t m = transpose ? cols : rows, K = transpose ? rows : cols;
   if (a_fmt == F64)
     return launch_simt<double, double, double, 0>(A, lda, transpose, m, K, X, ldx, k, W, ldw, out_fmt, colmax,
-                                                  flags, nullptr, 0, nullptr, nullptr, nullptr, st);
+                                                  flags, nullptr, 0, nullptr, nullptr, nullptr, st, W2, ldw2, out_fmt2);
   if (a_fmt == F32)
     return launch_simt<float, float, float, 0>(A, lda, transpose, m, K, X, ldx, k, W, ldw, out_fmt, colmax,
-                                               flags, nullptr, 0, nullptr, nullptr, nullptr, st);
+                                               flags, nullptr, 0, nullptr, nullptr, nullptr, st, W2, ldw2, out_fmt2);
   ofrr_set_error("simt_gemm_av: format %d not supported on the CUDA-core path", a_fmt);
   return OFRR_ERR_UNSUPPORTED;
+}
+
+int residual_reduce(const double* part, int nblocks, int n, const double* vals, const int* r_dev, double* res,
+                    int mode, cudaStream_t st) {
+  k_residual_reduce<<<(n + 127) / 128, 128, 0, st>>>(part, nblocks, n, vals, r_dev, res, mode);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
 }
 
 size_t residual_ws(int64_t rows, int r) {

@@ -65,6 +65,20 @@ class IterConfig:
         return self.matvec_policy or self.policy
 
 
+def operator_for(a: DenseMatrix, block_fmt: FpFormat):
+    """The device copy of A that multiplies blocks stored in ``block_fmt``.
+
+    An F32 block against an operator held exactly in bf16 runs on the bf16 tensor cores
+    (the block split into three bf16 slices, ops.gemm_av): fp32-accurate products at bf16
+    HBM traffic, instead of a second fp32 copy of A on the CUDA cores."""
+    block_fmt = FpFormat(block_fmt)
+    if block_fmt == FpFormat.F32 and (a.fmt == FpFormat.BF16 or FpFormat.BF16 in getattr(a, "_dev", {})):
+        op = a.device_operator(FpFormat.BF16)
+        if a.exact_in(FpFormat.BF16):
+            return op
+    return a.device_operator(block_fmt)
+
+
 def _require_ofrr_path(cfg: IterConfig, what: str) -> None:
     if cfg.basis_method in KRYLOV_METHODS:
         raise ValueError(f"{what} needs a block basis method")
@@ -120,8 +134,8 @@ class EigEngine:
         self.mv = cfg.mv_policy
         self.a = a
         self.n = int(n_global if n_global is not None else a.cols)
-        self.A_mv = a.device_operator(self.mv.storage)
-        self.A_pol = self.A_mv if self.pol.storage == self.mv.storage else a.device_operator(self.pol.storage)
+        self.A_mv = operator_for(a, self.mv.storage)
+        self.A_pol = self.A_mv if self.pol.storage == self.mv.storage else operator_for(a, self.pol.storage)
         self.device = self.A_mv.device
         self.r0, self.r1 = self.comm.row_range(self.n)
         if self.comm.distributed and self.A_mv.rows != self.r1 - self.r0:
@@ -133,9 +147,7 @@ class EigEngine:
     # ---- blocks ---------------------------------------------------------------------
     def start_block(self):
         """X0 = PCG64(seed) U(0,1), rounded to the MatVec storage (ofrr/driver.py:97-99)."""
-        rng = np.random.default_rng(self.cfg.seed)
-        x0 = rng.random((self.n, self.cfg.k))
-        return self.ops.block_from_host(round_to(x0, self.mv.storage), self.mv.storage, self.device)
+        return self.ops.start_block(self.cfg.seed, self.n, self.cfg.k, self.mv.storage, self.device)
 
     def power(self, X, st):
         """cfg.iter MatVecs with inf-norm column scaling (ofrr/driver.py:102-105)."""
@@ -164,14 +176,22 @@ class EigEngine:
         return h
 
     def project(self, U, st, want64: bool, top_check: Optional[int] = None):
-        """ofrr_eig (ofrr/projection.py:75-87) + restart block (ofrr/driver.py:109)."""
+        """ofrr_eig (ofrr/projection.py:75-87) + restart block (ofrr/driver.py:109).
+
+        With ``top_check`` the block product also keeps W = A U in its accumulation
+        format (fp32 on the tensor cores) and the residual estimate of the leading
+        pairs is formed from it (K7e) -- no extra pass over A."""
         ops, comm = self.ops, self.comm
         kp = U.k
         W = ops.new_block(self.A_pol.rows, kp, self.pol.storage, self.device)
-        ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        W2 = None
+        if top_check is not None:
+            acc = FpFormat.F64 if self.A_pol.fmt == FpFormat.F64 else FpFormat.F32
+            W2 = ops.new_block(self.A_pol.rows, kp, acc, self.device)
+        ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2)
         self.stats.a_passes += 1
+        Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U
         if comm.distributed:
-            Ul = _row_slice(U, self.r0, self.r1)
             B, _ = ops.gram(Ul, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], want_m=False)
             comm.all_reduce_sum_(B)
             _, M = ops.gram(U, None, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
@@ -182,10 +202,14 @@ class EigEngine:
         st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
         U64, Xn = ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=want64, x_fmt=self.mv.storage,
                            flags=st[S_RESTART_FLAGS:S_RESTART_FLAGS + 1])
-        res = None
-        if top_check is not None and U64 is not None:
-            res = self.residuals(U64, eig.values, eig.n_out, min(top_check, kp))
-        return eig, U64, Xn, res
+        est = None
+        if W2 is not None:
+            t = min(top_check, kp)
+            est = ops.residual_estimate(Ul, W2, eig.vectors, kp, eig.values, eig.n_out, t,
+                                        mode=2 if comm.distributed else 0)
+            if comm.distributed:
+                comm.all_reduce_sum_(est)
+        return eig, U64, Xn, est
 
     def residuals(self, U64, vals, r_dev, r):
         """FP64 ||A u - lambda u|| / |lambda| for the first r pairs (K7)."""
@@ -210,12 +234,18 @@ class EigEngine:
 
     # ---- the outer loop -----------------------------------------------------------------
     def run(self) -> RitzSet:
+        """The outer loop (ofrr/driver.py:101-111).  With cfg.tol the loop stops at the
+        first iteration whose leading `top` residuals pass: the cheap estimate (K7e)
+        nominates, the FP64 residual report (K7) confirms; the returned residuals are
+        always the FP64 ones."""
         import torch
         cfg = self.cfg
         tol, top = cfg.tol, (cfg.top or cfg.k)
+        check = tol is not None
         X = self.start_block()
-        eig = U64 = None
-        kp = r = 0
+        eig = U64 = U = None
+        r = 0
+        rs = None
         for it in range(cfg.m):
             st = torch.zeros(8, dtype=torch.int32, device=self.device)
             X = self.power(X, st)
@@ -228,8 +258,7 @@ class EigEngine:
                 raise EmptyBasisError("all columns skipped in Hessenberg process")
             U = h.Q.narrow(kp)
             last = it == cfg.m - 1
-            check = tol is not None
-            eig, U64, Xn, res = self.project(U, st, want64=(last or check), top_check=(top if check else None))
+            eig, U64, Xn, est = self.project(U, st, want64=last, top_check=(top if check else None))
             s = _fetch_status(st, self.comm)                      # sync 2: pencil status, width
             _raise_for(s, "projection")
             r = int(s[S_NOUT])
@@ -237,18 +266,28 @@ class EigEngine:
             self.stats.iterations = it + 1
             if check:
                 vals_np = eig.values[:r].cpu().numpy()
-                rr = self.finish_residuals(res, vals_np)
-                worst = float(np.max(rr[: min(top, r)])) if r >= top else float("inf")
-                self.stats.history.append((it + 1, worst))
-                if worst < tol:
-                    self.stats.converged = True
-                    break
-            self._last_U = U
-        if U64 is None:  # m iterations without a final FP64 recovery (cannot happen: last=True)
-            raise RuntimeError("internal: no Ritz vectors")
+                e = self.finish_residuals(est, vals_np)
+                worst = float(np.max(e[: min(top, r)])) if r >= top else float("inf")
+                if worst < tol or last:
+                    if U64 is None:
+                        U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
+                    rs = self.report(U64, eig, r)                 # FP64 confirmation
+                    worst = float(np.max(rs.residuals[: min(top, r)])) if r >= top else float("inf")
+                    self.stats.history.append((it + 1, worst))
+                    if worst < tol:
+                        self.stats.converged = True
+                        break
+                else:
+                    self.stats.history.append((it + 1, worst))
+        if rs is None:
+            if U64 is None:
+                U64, _ = self.ops.ritz(U, eig.vectors, U.k, eig.n_out, U.k, 1.0, want64=True)
+            rs = self.report(U64, eig, r)
+        return rs
+
+    def report(self, U64, eig, r: int) -> RitzSet:
         vals = eig.values[:r].cpu().numpy()
-        vecs = DenseMatrix.from_block(U64.narrow(r))
-        rs = RitzSet(vals, vecs, "eig")
+        rs = RitzSet(vals, DenseMatrix.from_block(U64.narrow(r)), "eig")
         return self.residual_report(rs, U64, eig, r)
 
     def residual_report(self, rs: RitzSet, U64, eig, r: int) -> RitzSet:
@@ -379,8 +418,7 @@ def subspace_iter_svd(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats]
     pol, mv = cfg.policy, cfg.mv_policy
     eng = SvdEngine(a, pol, mv)
     ops = eng.ops
-    rng = np.random.default_rng(cfg.seed)
-    V = ops.block_from_host(round_to(rng.random((n2, cfg.k)), mv.storage), mv.storage, eng.device)
+    V = ops.start_block(cfg.seed, n2, cfg.k, mv.storage, eng.device)
     rs = None
     import torch
     for _ in range(cfg.m):

@@ -133,6 +133,22 @@ def block_from_host(x, fmt: FpFormat, device) -> DevBlock:
     return out
 
 
+def start_block(seed: int, n: int, k: int, fmt: FpFormat, device) -> DevBlock:
+    """X0 = numpy default_rng(seed).random((n, k)) rounded to fmt, generated on the device
+    bit for bit (ofrr/driver.py:97-99): numpy derives the PCG64 state from the seed, the
+    device walks the stream."""
+    import numpy as np
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    X = new_block(n, k, fmt, device, zero=True)
+    L = _lib.load()
+    _lib.check(L.ofrr_start_block_pcg64(s >> 64, s & m64, inc >> 64, inc & m64, n, k, X.ptr, X.ld, int(fmt),
+                                        _stream()), "start_block")
+    _count(1)
+    return X
+
+
 def convert(src: DevBlock, dst: DevBlock, flags: Optional[torch.Tensor] = None) -> None:
     """dst <- round(src) column by column (ofrr/precision.py:90-104)."""
     L = _lib.load()
@@ -162,8 +178,9 @@ def round_tensor(x: torch.Tensor, fmt: FpFormat) -> torch.Tensor:
 # ---------------------------------------------------------------------------------
 def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat] = None,
             colmax: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
-            transpose: bool = False) -> None:
-    """W = op(A) X rounded to out_fmt (default W.fmt); colmax[j] = max|W[:,j]|."""
+            transpose: bool = False, W2: Optional[DevBlock] = None) -> None:
+    """W = op(A) X rounded to out_fmt (default W.fmt); colmax[j] = max|W[:,j]|; optionally
+    W2 = the same product in W2.fmt (e.g. the fp32 accumulator)."""
     L = _lib.load()
     k = X.k
     ws_b = L.ofrr_gemm_av_workspace(A.rows, A.cols, k, int(A.fmt), int(transpose))
@@ -173,14 +190,27 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
     if ev is not None:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-    _lib.check(L.ofrr_gemm_av(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), int(transpose), X.ptr, X.ld, k, W.ptr,
-                              W.ld, of, _p(colmax), _p(flags), ws.data_ptr(), ws.numel(), _stream()), "gemm_av")
+    split = A.fmt == FpFormat.BF16 and X.fmt == FpFormat.F32 and not transpose
+    if split:
+        # fp32 block on the bf16 tensor cores (3 bf16 slices, one pass over A)
+        ws = _ws(L.ofrr_gemm_av_split_workspace(A.rows, A.cols, k), A.device)
+        _lib.check(L.ofrr_gemm_av_split(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), X.ptr, X.ld, k, W.ptr, W.ld, of,
+                                        _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
+                                        W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else of,
+                                        ws.data_ptr(), ws.numel(), _stream()), "gemm_av_split")
+    else:
+        if X.fmt != A.fmt:
+            raise ValueError(f"gemm_av: block format {X.fmt.name} with operator format {A.fmt.name}")
+        _lib.check(L.ofrr_gemm_av2(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), int(transpose), X.ptr, X.ld, k,
+                                   W.ptr, W.ld, of, _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
+                                   W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else of,
+                                   ws.data_ptr(), ws.numel(), _stream()), "gemm_av")
     if ev is not None:
         e1.record()
         # algorithmic bytes: A once + X once + W once
         nb = A.rows * A.cols * A.fmt.itemsize + A.cols * k * X.fmt.itemsize + A.rows * k * FpFormat(of).itemsize
         ev.append((e0, e1, nb, 2.0 * A.rows * A.cols * k))
-    _count(2 if (A.fmt.tensor_core and not transpose) else 1)
+    _count(3 if split else 2 if (A.fmt.tensor_core and not transpose) else 1)
 
 
 def scale_columns(X: DevBlock, colmax: torch.Tensor, compute: FpFormat) -> None:
@@ -302,6 +332,19 @@ def ritz(U: DevBlock, Y: torch.Tensor, ldy: int, r_dev: Optional[torch.Tensor], 
                "ritz_recover")
     _count(1)
     return U64, X
+
+
+def residual_estimate(U: DevBlock, W: DevBlock, Y: torch.Tensor, ldy: int, vals: torch.Tensor,
+                      r_dev: Optional[torch.Tensor], r_max: int, mode: int = 0) -> torch.Tensor:
+    """K7e: ||(W - lambda_j U) y_j|| / |lambda_j| (mode 0) or raw sums of squares (mode 2)."""
+    L = _lib.load()
+    res = torch.zeros(max(r_max, 1), dtype=torch.float64, device=U.device)
+    ws = _ws(L.ofrr_residual_estimate_workspace(U.n, r_max), U.device)
+    _lib.check(L.ofrr_residual_estimate(U.ptr, U.ld, int(U.fmt), W.ptr, W.ld, int(W.fmt), U.n, U.k, Y.data_ptr(),
+                                        ldy, vals.data_ptr(), _p(r_dev), r_max, res.data_ptr(), mode, ws.data_ptr(),
+                                        ws.numel(), _stream()), "residual_estimate")
+    _count(2)
+    return res
 
 
 def residual_eig(A: DevOperator, V: DevBlock, vals: torch.Tensor, r_dev: Optional[torch.Tensor], r_max: int):

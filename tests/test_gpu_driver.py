@@ -145,3 +145,20 @@ def test_driver_eig_tolerance_stop(ofrr_gpu):
     assert st.converged and st.iterations < 30
     assert np.max(rs.residuals[:top]) < 2e-2
     assert st.history[-1][1] < 2e-2
+
+
+def test_driver_eig_fp32_basis_on_bf16_operator(ofrr_gpu, oracle):
+    """full-f32 policy on a bf16-stored operator: the fp32 blocks run on the bf16 tensor
+    cores (three-slice split); parity vs the oracle's full-f32 run on the same A."""
+    p, o = ofrr_gpu, oracle
+    n, top, k, m = 1024, 10, 20, 6
+    lam = p.geometric_spectrum(n, top, k)
+    A, f = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    a_host = o.sym_from_factors(n, f.hadamard, f.c, f.s, f.Wf, f.Mf, o.BF16)
+    cfg = p.IterConfig(k=k, m=m, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.FULL_F32, seed=SEED)
+    rs = p.subspace_iter_eig(A, cfg)
+    ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=o.FULL_F32, seed=SEED)
+    exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+    assert np.max(rs.residuals[:top]) < 1e-4

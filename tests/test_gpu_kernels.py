@@ -260,3 +260,36 @@ def test_generator_bitwise(ofrr_gpu, oracle, n):
     # the spectrum is the prescribed one
     ev = np.sort(np.linalg.eigvalsh(o.sym_from_factors(n, f.hadamard, f.c, f.s, f.Wf, f.Mf, F64)))[::-1]
     np.testing.assert_allclose(ev[:50], lam[:50], atol=1e-13)
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048, 64), (1000, 3000, 20), (4096, 1024, 85)])
+def test_gemm_split_fp32_block_vs_fp64(ofrr_gpu, oracle, shape):
+    """K1 split mode: bf16 A times an fp32 block via three bf16 slices is fp32-accurate."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rows, cols, k = shape
+    rng = np.random.default_rng(rows + k)
+    a = o.round_to(rng.standard_normal((rows, cols)), BF16)
+    x = o.round_to(rng.standard_normal((cols, k)), F32)
+    A = _op(p, a, BF16)
+    X = _blk(p, x, F32)
+    W = ops.new_block(rows, k, p.FpFormat.F32, A.device)
+    colmax = torch.zeros(k, dtype=torch.float64, device=A.device)
+    ops.gemm_av(A, X, W, colmax=colmax)
+    got = _host(W)
+    exact = a @ x
+    bound = 2e-6 * (np.abs(a) @ np.abs(x)) + 1e-30
+    assert np.all(np.abs(got - exact) <= bound), np.max(np.abs(got - exact) / bound)
+    np.testing.assert_array_equal(colmax.cpu().numpy(), np.max(np.abs(got), axis=0))
+
+
+@pytest.mark.parametrize("n,k,fmt", [(1000, 20, F64), (16384, 64, BF16), (333, 7, F16), (5000, 33, F32)])
+def test_start_block_matches_numpy(ofrr_gpu, oracle, n, k, fmt):
+    """X0 on the device == numpy default_rng(seed).random((n, k)) rounded (ofrr/driver.py:97-99)."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    for seed in (0, 2, 20240901):
+        X = ops.start_block(seed, n, k, ofrr_gpu.FpFormat(fmt), torch.device("cuda"))
+        ref = oracle.round_to(np.random.default_rng(seed).random((n, k)), fmt)
+        np.testing.assert_array_equal(_host(X), ref)
