@@ -324,3 +324,6 @@ int ofrr_host_jacobi_eig(const double* a, int64_t n, int max_sweeps, double tol,
 }
 
 }  // extern "C"
+
+namespace ofrr { int k5_profile(long long* out); }
+extern "C" int ofrr_debug_k5_profile(long long* out8) { return ofrr::k5_profile(out8); }

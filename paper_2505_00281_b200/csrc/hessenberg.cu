@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -58,10 +59,10 @@ __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* 
   __syncthreads();
 }
 
-template <typename T>
+template <typename T, int compute>
 __global__ void __launch_bounds__(HT)
     k_hessenberg(const T* __restrict__ X, int64_t n, int k, int64_t ldx, T* __restrict__ Xg, int64_t ldg,
-                 int storage, int compute, double tol, T* __restrict__ Q, int64_t ldq,
+                 int storage, int compute_rt, double tol, T* __restrict__ Q, int64_t ldq,
                  int64_t* __restrict__ pivots, int* __restrict__ kept, int* __restrict__ n_kept, HessWs ws,
                  int in_smem) {
   cg::grid_group grid = cg::this_grid();
@@ -156,16 +157,16 @@ __global__ void __launch_bounds__(HT)
       if (c == 0 && threadIdx.x == 0) { kept[j] = 1; pivots[nk] = r; }
       __syncthreads();
       // ofrr/basis.py:188-190 + precision.py:172-180: a[:,i] = round_s(c(a) - c(c(a[r,i]) * c(v)))
-      const int64_t cols = k - j - 1;
-      const int64_t work = cols * nr;
-      for (int64_t e = threadIdx.x; e < work; e += HT) {
-        const int64_t cc = j + 1 + e / nr;
-        const int64_t i = r0 + e % nr;
-        const double alpha = rnd(prow[cc], compute);
-        const double v = to_d(Xw[(int64_t)j * ldw + i]);
-        const double y = to_d(Xw[cc * ldw + i]);
-        const double t = c_mul(alpha, rnd(v, compute), compute);
-        Xw[cc * ldw + i] = from_d<T>(rnd(c_sub(rnd(y, compute), t, compute), storage));
+      for (int cc = j + 1 + threadIdx.x; cc < k; cc += HT) prow[cc] = rnd(prow[cc], compute);   // alpha_c
+      __syncthreads();
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+        const double v = rnd(to_d(Xw[(int64_t)j * ldw + i]), compute);
+        T* yp = Xw + i;
+        for (int cc = j + 1; cc < k; ++cc) {
+          const double y = to_d(yp[(int64_t)cc * ldw]);
+          const double t = c_mul(prow[cc], v, compute);
+          yp[(int64_t)cc * ldw] = from_d<T>(rnd(c_sub(rnd(y, compute), t, compute), storage));
+        }
       }
       ++nk;
       __syncthreads();
@@ -184,7 +185,13 @@ __global__ void __launch_bounds__(HT)
 static int hess_grid(int64_t n) {
   int sms = ofrr_device_sm_count(-1);
   if (sms <= 0) sms = 148;
-  int64_t g = (n + 127) / 128;  // at least 128 rows per CTA
+  static int min_rows = -1;
+  if (min_rows < 0) {
+    const char* e = getenv("OFRR_HESS_MIN_ROWS");   // tuning knob (rows per CTA lower bound)
+    min_rows = e ? atoi(e) : 128;
+    if (min_rows < 32) min_rows = 32;
+  }
+  int64_t g = (n + min_rows - 1) / min_rows;
   return (int)std::max<int64_t>(1, std::min<int64_t>(sms, g));
 }
 
@@ -199,7 +206,7 @@ size_t hessenberg_ws(int64_t n, int k, int storage) {
   return b + 2048;
 }
 
-template <typename T>
+template <typename T, int C>
 static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute, double tol,
                        void* Q, int64_t ldq, int64_t* pivots, int* kept, int* n_kept, void* ws, cudaStream_t st) {
   const int G = hess_grid(n);
@@ -220,7 +227,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   size_t shmem = (size_t)k * sizeof(double) + (in_smem ? tile + 16 : 0);
   static bool attr = false;
   if (!attr) {
-    OFRR_CUDA_TRY(cudaFuncSetAttribute((const void*)k_hessenberg<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    OFRR_CUDA_TRY(cudaFuncSetAttribute((const void*)k_hessenberg<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        200 * 1024));
     attr = true;
   }
@@ -228,20 +235,29 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
                   (void*)&compute, (void*)&tol, (void*)&Qp, (void*)&ldq, (void*)&pivots, (void*)&kept,
                   (void*)&n_kept, (void*)&h, (void*)&in_smem};
   OFRR_CUDA_TRY(cudaMemsetAsync(kept, 0, sizeof(int) * k, st));
-  OFRR_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hessenberg<T>, dim3(G), dim3(HT), args, shmem, st));
+  OFRR_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hessenberg<T, C>, dim3(G), dim3(HT), args, shmem, st));
   return OFRR_OK;
 }
 
 int hessenberg(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute, double tol, void* Q,
                int64_t ldq, int64_t* pivots, int* kept, int* n_kept, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (ws_bytes < hessenberg_ws(n, k, storage)) { ofrr_set_error("hessenberg: workspace too small"); return OFRR_ERR_INVALID; }
-  switch (storage) {
-    case F64: return launch_hess<double>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
-    case F32: return launch_hess<float>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
-    case F16: return launch_hess<__half>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
-    case BF16: return launch_hess<__nv_bfloat16>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st);
-    default: ofrr_set_error("hessenberg: storage format %d unsupported", storage); return OFRR_ERR_UNSUPPORTED;
+#define HESS(T, C) return launch_hess<T, C>(X, n, k, ldx, storage, compute, tol, Q, ldq, pivots, kept, n_kept, ws, st)
+  switch (storage * 8 + compute) {
+    case F64 * 8 + F64: HESS(double, F64);
+    case F32 * 8 + F32: HESS(float, F32);
+    case F32 * 8 + F64: HESS(float, F64);
+    case F16 * 8 + F16: HESS(__half, F16);
+    case F16 * 8 + F32: HESS(__half, F32);
+    case F16 * 8 + F64: HESS(__half, F64);
+    case BF16 * 8 + BF16: HESS(__nv_bfloat16, BF16);
+    case BF16 * 8 + F32: HESS(__nv_bfloat16, F32);
+    case BF16 * 8 + F64: HESS(__nv_bfloat16, F64);
+    default:
+      ofrr_set_error("hessenberg: storage %d / compute %d unsupported", storage, compute);
+      return OFRR_ERR_UNSUPPORTED;
   }
+#undef HESS
 }
 
 }  // namespace ofrr

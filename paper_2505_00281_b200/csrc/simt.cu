@@ -143,6 +143,176 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------------
+// FP64 residual product (K7), tuned: C = A (rows x K, row-major, any storage format,
+// promoted exactly to fp64) * V (K x r, column-major fp64), epilogue
+// part[block, j] = sum_rows (C[i,j] - vals[j] * Y[i,j])^2.
+// CTA tile 128 x 64, BK = 32, 256 threads, 8 x 4 fp64 accumulators per thread,
+// double-buffered shared memory (A staged transposed as fp64 so a warp's A reads are
+// broadcasts), 16-byte global loads.  FP64-FMA bound.
+// ---------------------------------------------------------------------------------
+static constexpr int RBM = 128, RBN = 64, RBK = 32;
+
+// Raw global staging of one k-tile (kept in registers while the previous tile computes):
+// A: thread -> (row tid & 127, k half tid >> 7) : 16 consecutive elements of one row
+// B: thread -> (col tid >> 2, k quarter tid & 3): 8 consecutive fp64 of one column
+template <typename TA>
+struct ResidStage {
+  uint4 araw[2];   // 16 x 16-bit values (vector path)
+  TA a[16];        // scalar path
+  double b[8];
+  bool vec;
+};
+
+template <typename TA>
+__device__ __forceinline__ void resid_fetch(const TA* __restrict__ A, int64_t lda, const double* __restrict__ V,
+                                            int64_t ldv, int64_t m0, int n0, int64_t k0, int64_t m, int64_t K, int n,
+                                            int tid, ResidStage<TA>& st) {
+  const int r = tid & 127, kh = (tid >> 7) * 16;
+  const int64_t gr = m0 + r;
+  st.vec = false;
+  if constexpr (sizeof(TA) == 2) {
+    if (gr < m && k0 + kh + 16 <= K) {
+      const uint4* p = reinterpret_cast<const uint4*>(A + gr * lda + k0 + kh);
+      st.araw[0] = __ldg(p);
+      st.araw[1] = __ldg(p + 1);
+      st.vec = true;
+    }
+  }
+  if (!st.vec) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t gk = k0 + kh + e;
+      st.a[e] = (gr < m && gk < K) ? A[gr * lda + gk] : from_d<TA>(0.0);
+    }
+  }
+  const int c = tid >> 2, kq = (tid & 3) * 8;
+  const int gc = n0 + c;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int64_t gk = k0 + kq + e;
+    st.b[e] = (gc < n && gk < K) ? V[(int64_t)gc * ldv + gk] : 0.0;
+  }
+}
+
+// converts (exactly) to fp64 only here, after the previous tile's math, so the global
+// loads of resid_fetch stay in flight across the compute loop
+template <typename TA>
+__device__ __forceinline__ void resid_store(double (*As)[RBM + 1], double (*Bs)[RBN + 1], int tid,
+                                            const ResidStage<TA>& st) {
+  const int r = tid & 127, kh = (tid >> 7) * 16;
+  if constexpr (sizeof(TA) == 2) {
+    if (st.vec) {
+      const uint32_t w[8] = {st.araw[0].x, st.araw[0].y, st.araw[0].z, st.araw[0].w,
+                             st.araw[1].x, st.araw[1].y, st.araw[1].z, st.araw[1].w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        TA lo, hi;
+        const uint16_t l16 = (uint16_t)(w[e] & 0xffffu), h16 = (uint16_t)(w[e] >> 16);
+        memcpy(&lo, &l16, 2);
+        memcpy(&hi, &h16, 2);
+        As[kh + 2 * e][r] = to_d(lo);        // a warp: 32 consecutive rows
+        As[kh + 2 * e + 1][r] = to_d(hi);
+      }
+    }
+  }
+  if (!st.vec) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) As[kh + e][r] = to_d(st.a[e]);
+  }
+  const int c = tid >> 2, kq = (tid & 3) * 8;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) Bs[kq + e][c] = st.b[e];
+}
+
+template <typename TA>
+__global__ void __launch_bounds__(256, 1)
+    k_resid64(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t K, const double* __restrict__ V, int64_t ldv,
+              int n, const double* __restrict__ Y, int64_t ldy, const double* __restrict__ vals,
+              const int* __restrict__ r_dev, double* __restrict__ part) {
+  extern __shared__ double rsm[];
+  double (*As)[RBM + 1] = reinterpret_cast<double (*)[RBM + 1]>(rsm);                       // [2][RBK][RBM+1]
+  double (*Bs)[RBN + 1] = reinterpret_cast<double (*)[RBN + 1]>(rsm + 2 * RBK * (RBM + 1));  // [2][RBK][RBN+1]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t m0 = (int64_t)blockIdx.x * RBM;
+  const int n0 = blockIdx.y * RBN;
+  const int nvalid = r_dev ? min(n, *r_dev) : n;
+  // thread (ty, tx) owns rows ty + 16 i (i < 8) and columns tx + 16 j (j < 4): smem reads
+  // of a warp are broadcasts (A) or 16 consecutive doubles (B) -- bank-conflict free
+  double acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  const int nk = (int)((K + RBK - 1) / RBK);
+  ResidStage<TA> st;
+  resid_fetch<TA>(A, lda, V, ldv, m0, n0, 0, m, K, n, tid, st);
+  resid_store<TA>(As, Bs, tid, st);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    double (*Ac)[RBM + 1] = As + cur * RBK;
+    double (*Bc)[RBN + 1] = Bs + cur * RBK;
+    const bool more = t + 1 < nk;
+    if (more) resid_fetch<TA>(A, lda, V, ldv, m0, n0, (int64_t)(t + 1) * RBK, m, K, n, tid, st);
+#pragma unroll 8
+    for (int kk = 0; kk < RBK; ++kk) {
+      double a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = Ac[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bc[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    if (more) resid_store<TA>(As + (cur ^ 1) * RBK, Bs + (cur ^ 1) * RBK, tid, st);
+    __syncthreads();
+  }
+  // epilogue: per-column sums of squares over this CTA's rows, fixed order
+  double* csum = rsm;   // reuse: [16][RBN]
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int gc = n0 + tx + 16 * j;
+    double s = 0.0;
+    if (gc < nvalid) {
+      const double lam = vals[gc];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t gr = m0 + ty + 16 * i;
+        if (gr < m) {
+          const double d = acc[i][j] - lam * Y[(int64_t)gc * ldy + gr];
+          s = fma(d, d, s);
+        }
+      }
+    }
+    csum[ty * RBN + tx + 16 * j] = s;
+  }
+  __syncthreads();
+  if (tid < RBN && n0 + tid < n) {
+    double s = 0.0;
+    for (int y = 0; y < 16; ++y) s += csum[y * RBN + tid];
+    part[(int64_t)blockIdx.x * n + n0 + tid] = s;
+  }
+}
+
+template <typename TA>
+static int launch_resid64(const void* A, int64_t lda, int64_t m, int64_t K, const double* V, int64_t ldv, int n,
+                          const double* Y, int64_t ldy, const double* vals, const int* r_dev, double* part,
+                          cudaStream_t st) {
+  const size_t shm = (size_t)2 * RBK * ((RBM + 1) + (RBN + 1)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_resid64<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    attr = true;
+  }
+  dim3 grid((unsigned)((m + RBM - 1) / RBM), (unsigned)((n + RBN - 1) / RBN));
+  k_resid64<TA><<<grid, 256, shm, st>>>((const TA*)A, lda, m, K, V, ldv, n, Y, ldy, vals, r_dev, part);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
 // res[j] = sqrt(sum_b part[b, j]) / |vals[j]|  (inf for vals[j] == 0), fixed order.
 __global__ void k_residual_reduce(const double* __restrict__ part, int nblocks, int n,
                                   const double* __restrict__ vals, const int* __restrict__ r_dev,
@@ -207,6 +377,19 @@ int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
   if (!ws || ws_bytes < need) { ofrr_set_error("residual: workspace too small (%zu < %zu)", ws_bytes, need); return OFRR_ERR_INVALID; }
   double* part = (double*)ws;
   int rc;
+  if (!transpose && a_fmt != FP8) {
+    switch (a_fmt) {
+      case F64: rc = launch_resid64<double>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+      case F32: rc = launch_resid64<float>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+      case F16: rc = launch_resid64<__half>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+      default: rc = launch_resid64<__nv_bfloat16>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+    }
+    if (rc) return rc;
+    const int nb = (int)((m + RBM - 1) / RBM);
+    k_residual_reduce<<<(r_max + 127) / 128, 128, 0, st>>>(part, nb, r_max, vals, r_dev, res, accumulate_max);
+    OFRR_CHECK_LAUNCH();
+    return OFRR_OK;
+  }
   switch (a_fmt) {
     case F64: rc = launch_simt<double, double, double, 1>(A, lda, transpose, m, K, Xv, ldx, r_max, nullptr, 0, 0, nullptr, nullptr, Yv, ldy, vals, r_dev, part, st); break;
     case F32: rc = launch_simt<float, double, double, 1>(A, lda, transpose, m, K, Xv, ldx, r_max, nullptr, 0, 0, nullptr, nullptr, Yv, ldy, vals, r_dev, part, st); break;

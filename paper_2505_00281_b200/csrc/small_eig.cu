@@ -90,6 +90,7 @@ __device__ double jacobi_parallel(double* S, int ld, double* V, int ldv, int k, 
     for (int r = 0; r < m; ++r) {
       // ---- phase A: every warp forms the rotations of its pairs, rotates their rows ----
       // (a warp handles pairs w, w + NW, ...; k <= 2*NW*...: loop)
+      int my_act = 0;
       for (int t = warp; t < np; t += NW) {
         if (lane != 0) continue;
         int a, b;
@@ -113,8 +114,11 @@ __device__ double jacobi_parallel(double* S, int ld, double* V, int ldv, int k, 
           }
         }
         sc.c[t] = c; sc.s[t] = s; sc.p[t] = p; sc.q[t] = q; sc.act[t] = ac;
+        my_act |= ac;
       }
-      __syncthreads();   // every warp has read its a_pp, a_qq, a_pq before any row changes
+      // barrier: every warp has read its a_pp, a_qq, a_pq before any row changes; a round
+      // in which every pair is below the skip threshold does nothing (uniform branch)
+      if (!__syncthreads_or(my_act)) continue;
       for (int t = warp; t < np; t += NW) {
         if (!sc.act[t]) continue;
         const int p = sc.p[t], q = sc.q[t];
@@ -252,6 +256,9 @@ __device__ void tri_inverse_lower(const double* L, int ld, double* X, int ldx, i
 
 struct EigBufs { double *S, *V, *P, *T; };
 
+__device__ long long g_k5prof[8];   // phase timestamps of the last pencil solve (debug)
+int k5_profile(long long* out) { return cudaMemcpyFromSymbol(out, g_k5prof, sizeof(g_k5prof)) == cudaSuccess ? 0 : 2; }
+
 // Every k x k work buffer uses the padded leading dimension L = k | 1 (odd): row walks of a
 // column-major fp64 matrix then hit distinct shared-memory banks.
 __host__ __device__ inline int pad_k(int k) { return (k % 2 == 0) ? k + 1 : k; }
@@ -311,15 +318,18 @@ __global__ void __launch_bounds__(ET, 1)
   }
 
   // ======================= mode 2: the pencil ===========================================
+  if (threadIdx.x == 0) g_k5prof[0] = clock64();
   // ---- fast whitening: Cholesky, certified above the safeguard cutoff ----
   const double mnorm = fro_norm(S, k, L, sc.red);   // ||M||_F >= mu_max
   for (int j = warp; j < k; j += NW)
     for (int i = lane; i < k; i += 32) P[j * L + i] = S[j * L + i];
   __syncthreads();
   bool chol = mnorm > 0.0 && cholesky(P, L, k, sc);
+  if (threadIdx.x == 0) g_k5prof[1] = clock64();
   int kp = k;
   if (chol) {
     tri_inverse_lower(P, L, T, L, k);                // T = L^-1 (= R^-T)
+    if (threadIdx.x == 0) g_k5prof[2] = clock64();
     const double inv2 = fro_norm(T, k, L, sc.red);   // ||R^-1||_F ; mu_min >= 1/||R^-1||_F^2
     chol = (1.0 / (inv2 * inv2)) > 4.0 * (double)k * 2.220446049250313e-16 * mnorm;
   }
@@ -329,6 +339,7 @@ __global__ void __launch_bounds__(ET, 1)
     __syncthreads();
     mm(T, L, false, V, L, false, P, L, k, k, k);     // P <- L^-1 Bs
     mm(P, L, false, T, L, true, V, L, k, k, k);      // V <- (L^-1 Bs) L^-T
+    if (threadIdx.x == 0) g_k5prof[3] = clock64();
   } else {
     // ---- the reference's eigen-whitening (smallsolve.py:75-88) ----
     const double tol = 1e-14 * mnorm;
@@ -363,6 +374,7 @@ __global__ void __launch_bounds__(ET, 1)
       for (int i = lane; i < kp; i += 32) V[j * L + i] = (sc.dis[i] * V[j * L + i]) * sc.dis[j];
     __syncthreads();
   }
+  if (threadIdx.x == 0) g_k5prof[4] = clock64();
   // ---- eig(T), T = (V + V^T)/2 (kp x kp) ----
   for (int j = warp; j < kp; j += NW)
     for (int i = lane; i < kp; i += 32) S[j * L + i] = (V[j * L + i] + V[i * L + j]) / 2.0;
@@ -375,6 +387,7 @@ __global__ void __launch_bounds__(ET, 1)
   }
   for (int i = threadIdx.x; i < kp; i += blockDim.x) tau[i] = S[i * L + i];
   __syncthreads();
+  if (threadIdx.x == 0) g_k5prof[5] = clock64();
   // ---- back-transform y = W Z  (W = L^-T, or P D^-1/2) -> S, then sort + sign ----
   if (chol) {
     mm(T, L, true, V, L, false, S, L, k, kp, k);     // S <- L^-T Z
@@ -391,6 +404,7 @@ __global__ void __launch_bounds__(ET, 1)
     __syncthreads();
   }
   sorted_desc(tau, S, L, k, kp, values, vectors, k, sc);
+  if (threadIdx.x == 0) g_k5prof[6] = clock64();
   if (threadIdx.x == 0) { *status = 0; *n_out = kp; }
 }
 
