@@ -68,10 +68,10 @@ class Comm:
         send = torch.zeros((k, rp), dtype=local.dtype, device=local.device)
         r0, r1 = self.row_range(n)
         send[:, : r1 - r0].copy_(local[:k, : r1 - r0])
-        recv = torch.empty((self.size, k, rp), dtype=local.dtype, device=local.device)
-        # gathered as bytes: every storage format (bf16, fp8, ...) on every backend
+        recv = torch.empty((self.size * k, rp), dtype=local.dtype, device=local.device)
+        # gathered as bytes (every storage format on every backend), rank-major along dim 0
         dist.all_gather_into_tensor(recv.view(torch.uint8), send.view(torch.uint8), group=self.group)
-        # recv[p, j, i] = X[p*rp + i, j]
-        tmp = recv.permute(1, 0, 2).reshape(k, self.size * rp)
+        # recv[p*k + j, i] = X[p*rp + i, j]
+        tmp = recv.view(self.size, k, rp).permute(1, 0, 2).reshape(k, self.size * rp)
         full[:k, :n].copy_(tmp[:, :n])
         return full

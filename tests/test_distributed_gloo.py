@@ -1,0 +1,106 @@
+"""Row-partitioned multi-process OFRR on CPU: world_size 2, gloo.
+
+Each rank owns half the rows of A; the driver's collectives (all-gather of the n x k
+block, all-reduce(max) of the column inf-norms, all-reduce(sum) of the partial Grams and
+residual sums of squares, all-reduce(max) of the status words) run over torch.distributed
+(gloo here, NCCL on the GPU box).  The per-op arithmetic is the test-only oracle backend
+(tests/cpu_ops.py), so the single-process and the 2-rank runs must agree to the rounding
+of the Gram all-reduce.
+"""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+N, TOP, K, M, SEED = 160, 6, 12, 4, 20240901
+
+
+def _problem():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as o
+    a, _ = o.geometric_symmetric(N, TOP, K, seed=SEED, fmt=o.F32)
+    return a
+
+
+def _run(a_rows, n, comm, tol=None):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cpu_ops
+    import paper_2505_00281_b200 as p
+    from paper_2505_00281_b200.driver import EigEngine
+    cfg = p.IterConfig(k=K, m=M, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.FULL_F32, seed=SEED, tol=tol, top=TOP if tol else None)
+    eng = EigEngine(cpu_ops.RowBlock(a_rows, p.FpFormat.F32), cfg, comm=comm, n_global=n, ops=cpu_ops)
+    rs = eng.run()
+    return rs.values, rs.vectors.data if hasattr(rs.vectors, "data") else None, rs.residuals, eng.stats
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, ROOT)
+        from paper_2505_00281_b200.comm import Comm
+        comm = Comm.world()
+        a = _problem()
+        r0, r1 = comm.row_range(N)
+        for tol in (None, 1e-4):
+            vals, _, res, st = _run(a[r0:r1], N, comm, tol=tol)
+            q.put((rank, tol, vals, res, st.iterations, st.a_passes))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_row_partitioned_matches_single_process():
+    sys.path.insert(0, ROOT)
+    from paper_2505_00281_b200.comm import Comm
+    a = _problem()
+    single = {tol: _run(a, N, Comm(), tol=tol) for tol in (None, 1e-4)}
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=180) for _ in range(4)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, tol, vals, res, iters, passes in out:
+        v1, _, r1, st1 = single[tol]
+        assert iters == st1.iterations
+        assert passes == st1.a_passes
+        np.testing.assert_allclose(vals, v1, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(res, r1, rtol=1e-6, atol=1e-12)
+    # both ranks hold identical results (redundant pencil solve is deterministic)
+    by_tol = {}
+    for rank, tol, vals, res, _, _ in out:
+        by_tol.setdefault(tol, []).append(vals)
+    for tol, vs in by_tol.items():
+        np.testing.assert_array_equal(vs[0], vs[1])
+
+
+def test_comm_row_ranges():
+    sys.path.insert(0, ROOT)
+    from paper_2505_00281_b200.comm import Comm
+    for n in (1, 7, 160, 16384):
+        for P in (1, 2, 3, 8):
+            rows = [Comm(r, P).row_range(n) for r in range(P)]
+            assert rows[0][0] == 0 and rows[-1][1] == n
+            assert all(rows[i][1] == rows[i + 1][0] for i in range(P - 1))
