@@ -37,7 +37,9 @@ struct TcCfg {
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : (2 * BN);   // power of two for BN in {16..256}
+  // two accumulators (M halves) of BN fp32 columns; allocation is a power of two >= 32
+  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
+                                   : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + 256;
 };
 
@@ -284,7 +286,8 @@ static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t i
   return OFRR_OK;
 }
 
-static int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : k <= 128 ? 128 : 256; }
+// N of the UMMA = k rounded up to a multiple of 32 (M=128 needs N % 16 == 0, N <= 256)
+static int pick_bn(int k) { return k <= 32 ? 32 : ((k + 31) / 32) * 32; }
 
 struct TcPlan {
   int bn, m_tiles, kblocks, grid, max_slots;
@@ -344,12 +347,13 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
   rc = make_tmap_2d(&tX, X, a_fmt, (uint64_t)cols, (uint64_t)k, (uint64_t)ldx, kel, (uint32_t)p.bn);
   if (rc) return rc;
   const uint32_t idesc = make_idesc(a_fmt, p.bn);
+#define TC_CASE(B) case B: rc = fp8 ? launch_tc_bn<B, true>(tA, tX, p, (float*)ws, idesc, st) \
+                                  : launch_tc_bn<B, false>(tA, tX, p, (float*)ws, idesc, st); break;
   switch (p.bn) {
-    case 32: rc = fp8 ? launch_tc_bn<32, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<32, false>(tA, tX, p, (float*)ws, idesc, st); break;
-    case 64: rc = fp8 ? launch_tc_bn<64, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<64, false>(tA, tX, p, (float*)ws, idesc, st); break;
-    case 128: rc = fp8 ? launch_tc_bn<128, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<128, false>(tA, tX, p, (float*)ws, idesc, st); break;
-    default: rc = fp8 ? launch_tc_bn<256, true>(tA, tX, p, (float*)ws, idesc, st) : launch_tc_bn<256, false>(tA, tX, p, (float*)ws, idesc, st); break;
+    TC_CASE(32) TC_CASE(64) TC_CASE(96) TC_CASE(128) TC_CASE(160) TC_CASE(192) TC_CASE(224)
+    default: TC_CASE(256)
   }
+#undef TC_CASE
   if (rc) return rc;
   k_finalize<<<dim3(p.m_tiles, (k / nsplit + FIN_COLS - 1) / FIN_COLS), 256, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
                                         rows, k / nsplit, W, ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
