@@ -59,58 +59,51 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML, every 2 ms in
+    a background thread; the timed region of a few solves is only tens of ms, too short
+    for `nvidia-smi -lms`)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.sm, self.mx, self.reasons = [], 0.0, set()
+        self._stop = threading.Event()
+        self._ok = False
+
+    def _run(self):
+        import pynvml as nv
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not self._stop.is_set():
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for nm, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(nm)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self._ok = True
+            self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         except Exception:
-            self.proc = None
+            self._ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._ok:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 # ------------------------------------------------------------------------------------
@@ -227,12 +220,15 @@ def run_ours(args, cfg):
         solve()
     barrier()
     # ---- timed region: K solves, CUDA events on the launching stream -------------
-    ops.GEMM_EVENTS = []
+    from paper_2505_00281_b200 import _lib
+    L = _lib.load()
+    ops.GEMM_LOG = []
     ops.LAUNCHES[0] = 0
     stats = p.RunStats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        L.ofrr_prof_gemm_enable(1)
         e0.record()
         for _ in range(args.steps):
             rs = solve(stats)
@@ -240,18 +236,23 @@ def run_ours(args, cfg):
         barrier()
     launches = ops.LAUNCHES[0]
     ms_total = e0.elapsed_time(e1)
-    gem = ops.GEMM_EVENTS
-    ops.GEMM_EVENTS = None
+    log = ops.GEMM_LOG
+    ops.GEMM_LOG = None
+    import ctypes
+    buf = (ctypes.c_float * 4096)()
+    nk = L.ofrr_prof_gemm_read(ctypes.addressof(buf), 4096)
+    L.ofrr_prof_gemm_enable(0)
+    durs = [float(buf[i]) for i in range(max(nk, 0))]
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    # dominant kernel (K1 block product): algorithmic bytes / average launch duration
-    durs = [a.elapsed_time(b) for a, b, _, _ in gem]
-    nbytes = float(np.mean([nb for _, _, nb, _ in gem]))
-    flops = float(np.mean([fl for _, _, _, fl in gem]))
-    avg_ms = float(np.mean(durs))
+    # dominant kernel (K1, k_gemm_av_tc): algorithmic bytes / kernel-only CUDA-event duration
+    nl = min(len(durs), len(log))
+    nbytes = float(np.mean([b for b, _ in log[:nl]])) if nl else float("nan")
+    flops = float(np.mean([f for _, f in log[:nl]])) if nl else float("nan")
+    avg_ms = float(np.mean(durs[:nl])) if nl else float("nan")
     hbm, bf16_peak, peak_kind = _peaks()
     achieved = nbytes / (avg_ms * 1e-3) / 1e9
     gemm_share = float(np.sum(durs)) / ms_total if ms_total > 0 else None
@@ -285,7 +286,7 @@ def run_ours(args, cfg):
     cpu = None
     if world == 1 and not args.no_cpu:
         pass_s, threads, kind, sample = cpu_reference_pass_time(cfg, target_s=args.ref_seconds)
-        passes = stats.a_passes / args.steps
+        passes = stats.a_passes
         cpu = {"value": pass_s * passes, "unit": "s", "cores": threads, "kind": kind,
                "sample": sample + f"; x {passes:.0f} A passes per solve (this run's count)"}
     line = {
@@ -294,16 +295,17 @@ def run_ours(args, cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfg["name"], "n": n, "top": top, "k": k, "tol": tol, "policy": cfg["policy"],
                    "outer_iterations_per_solve": stats.iterations and stats.iterations,
-                   "a_passes_per_solve": stats.a_passes / args.steps,
+                   "a_passes_per_solve": stats.a_passes,
                    "converged": bool(stats.converged),
                    "max_residual_top": float(np.max(rs.residuals[:top])),
                    "parallelism": f"row-partitioned x{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (A = %d MiB per GPU)" % ((r1 - r0) * n * 2 >> 20)},
-        "roofline": {"kernel": "k_gemm_av_tc + k_finalize (K1, A.X block product)", "bound": "hbm",
+        "roofline": {"kernel": "k_gemm_av_tc (K1, A.X block product; kernel-only CUDA events)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_kind": peak_kind, "traffic": None, "bytes_per_launch": nbytes,
                      "avg_launch_ms": avg_ms, "launches": len(durs), "share_of_step": gemm_share,
-                     "tflops": flops / (avg_ms * 1e-3) / 1e12, "tflops_peak_bf16": bf16_peak},
+                     "tflops": flops / (avg_ms * 1e-3) / 1e12, "tflops_peak_bf16": bf16_peak,
+                     "launches_per_solve": nl / args.steps},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -317,7 +319,7 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))

@@ -95,6 +95,12 @@ int ofrr_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, i
                        double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Kernel-only timing of the K1 tensor-core kernel (measurement support): while enabled,
+ * every k_gemm_av_tc launch is bracketed by CUDA events on its stream; read returns the
+ * durations (ms) of the launches since enable. */
+void ofrr_prof_gemm_enable(int on);
+int ofrr_prof_gemm_read(float* ms, int max);
+
 /* K2: X[:,j] <- round_s(round_c(X[:,j] / colmax[j])) for colmax[j] != 0, in place.
  * Replaces ofrr/precision.py:159-169 scale_columns_inf. */
 int ofrr_scale_columns(void* X, int64_t n, int k, int64_t ldx, int storage, int compute,

@@ -44,6 +44,8 @@ _SIGS = {
     "ofrr_residual_estimate_workspace": ([c_i64, c_int], c_sz),
     "ofrr_residual_estimate": ([c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_i64, c_int, c_vp, c_int, c_vp, c_vp,
                                 c_int, c_vp, c_int, c_vp, c_sz, c_vp], c_int),
+    "ofrr_prof_gemm_enable": ([c_int], None),
+    "ofrr_prof_gemm_read": ([c_vp, c_int], c_int),
     "ofrr_scale_columns": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_vp, c_vp], c_int),
     "ofrr_hessenberg_workspace": ([c_i64, c_int, c_int], c_sz),
     "ofrr_hessenberg": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp,

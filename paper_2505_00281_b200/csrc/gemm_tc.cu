@@ -22,6 +22,8 @@
 #include "common.cuh"
 #include <algorithm>
 #include <mutex>
+#include <vector>
+#include <utility>
 
 namespace ofrr {
 
@@ -287,6 +289,42 @@ static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t i
 }
 
 // N of the UMMA = k rounded up to a multiple of 32 (M=128 needs N % 16 == 0, N <= 256)
+// ---- kernel-only timing of k_gemm_av_tc (bench.py roofline): CUDA events recorded on the
+// launching stream immediately around the launch, read back after the timed region ----
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_ev;
+static size_t g_prof_n = 0;
+
+static cudaEvent_t* prof_slot() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_prof_on) return nullptr;
+  if (g_prof_n == g_prof_ev.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return nullptr;
+    g_prof_ev.push_back({a, b});
+  }
+  return &g_prof_ev[g_prof_n++].first;
+}
+
+void prof_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  g_prof_n = 0;
+}
+
+int prof_read(float* ms, int max) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int n = 0;
+  for (size_t i = 0; i < g_prof_n && n < max; ++i) {
+    if (cudaEventSynchronize(g_prof_ev[i].second) != cudaSuccess) return -1;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, g_prof_ev[i].first, g_prof_ev[i].second);
+    ms[n++] = t;
+  }
+  return n;
+}
+
 static int pick_bn(int k) { return k <= 32 ? 32 : ((k + 31) / 32) * 32; }
 
 struct TcPlan {
@@ -326,7 +364,10 @@ static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPl
     OFRR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_done = true;
   }
+  cudaEvent_t* ev = prof_slot();
+  if (ev) cudaEventRecord(ev[0], st);
   kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc);
+  if (ev) cudaEventRecord(ev[1], st);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }

@@ -21,6 +21,7 @@
 //    and the largest-|entry|-positive sign rule (smallsolve.py:52-61).
 #include "common.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace ofrr {
 
@@ -36,6 +37,7 @@ struct EigScratch {
   double vals[MAXK];
   double dis[MAXK];
   int order[MAXK];
+  double td[MAXK], te[MAXK], ttau[MAXK], tlam[MAXK], tq[MAXK];   // tridiagonal solver
   int flag;
 };
 
@@ -257,11 +259,279 @@ __device__ void tri_inverse_lower(const double* L, int ld, double* X, int ldx, i
 struct EigBufs { double *S, *V, *P, *T; };
 
 __device__ long long g_k5prof[8];   // phase timestamps of the last pencil solve (debug)
-int k5_profile(long long* out) { return cudaMemcpyFromSymbol(out, g_k5prof, sizeof(g_k5prof)) == cudaSuccess ? 0 : 2; }
 
 // Every k x k work buffer uses the padded leading dimension L = k | 1 (odd): row walks of a
 // column-major fp64 matrix then hit distinct shared-memory banks.
 __host__ __device__ inline int pad_k(int k) { return (k % 2 == 0) ? k + 1 : k; }
+
+// ---------------------------------------------------------------------------------
+// Symmetric eigensolver with O(k) sequential depth (used for T of the pencil):
+//   1. Householder tridiagonalisation T = Q Tri Q^T (k-2 reflectors, stored in place);
+//   2. eigenvalues of Tri by bisection on Sturm counts, one warp per eigenvalue doing
+//      32-way multisection (~11 rounds to full fp64 precision);
+//   3. eigenvectors of Tri by inverse iteration (LU with partial pivoting of the shifted
+//      tridiagonal), Gram-Schmidt within clusters of close eigenvalues (LAPACK dstein's
+//      1e-3 ||T|| rule), one thread per cluster;
+//   4. back-transformation by the reflectors.
+// Eigenvalues are returned in descending order with their vectors (the sign rule is
+// applied by sorted_desc afterwards).  Returns false if inverse iteration failed to
+// produce a usable vector (the caller falls back to Jacobi).
+// ---------------------------------------------------------------------------------
+struct TriWork {
+  double* d;     // [k]
+  double* e;     // [k]   e[i] couples i and i+1
+  double* tau;   // [k]
+  double* lam;   // [k]   ascending eigenvalues of Tri
+  double* wk;    // [4 * k * k] inverse-iteration scratch (global)
+};
+
+__device__ __forceinline__ int sturm_count(const double* d, const double* e, int k, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0.0) ++cnt;
+  for (int i = 1; i < k; ++i) {
+    q = d[i] - x - (e[i - 1] * e[i - 1]) / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+__device__ long long g_triprof[8];
+
+// Sturm-sequence divide with a cheap reciprocal: the count only needs signs, so an
+// fp32 reciprocal refined by one fp64 Newton step (~1e-14 relative) is plenty.
+__device__ __forceinline__ double fast_div(double a, double b) {
+  const double ab = fabs(b);
+  if (ab > 1e-30 && ab < 1e30) {
+    double r = (double)__frcp_rn((float)b);
+    r = r * fma(-b, r, 2.0);
+    r = r * fma(-b, r, 2.0);
+    return a * r;
+  }
+  return a / b;
+}
+
+__device__ __forceinline__ int sturm_fast(const double* d, const double* e2, int k, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0.0;
+  for (int i = 1; i < k; ++i) {
+    q = (d[i] - x) - fast_div(e2[i - 1], q);
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+__device__ bool sym_eig_tridiag(double* S, int ld, int k, double* vals_desc, double* Z, int ldz, TriWork tw,
+                                EigScratch& sc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red2[2];
+  if (threadIdx.x == 0) g_triprof[0] = clock64();
+  // ---- 1. tridiagonalisation: 3 barriers per reflector ------------------------------
+  for (int j = 0; j + 2 < k; ++j) {
+    if (warp == 0) {
+      double s2 = 0.0;
+      for (int i = j + 1 + lane; i < k; i += 32) s2 += S[j * ld + i] * S[j * ld + i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (lane == 0) { red2[0] = s2; red2[1] = 0.0; }
+    }
+    __syncthreads();                                             // (1)
+    const double norm2 = red2[0];
+    const double x0 = S[j * ld + j + 1];
+    const double alpha = -copysign(sqrt(norm2), x0);
+    const double unorm2 = 2.0 * (norm2 - x0 * alpha);
+    const bool skip = !(unorm2 > 0.0) || norm2 == 0.0;
+    const double tau = skip ? 0.0 : 2.0 / unorm2;
+    const double u0 = x0 - alpha;                                 // u[j+1]; u[i>j+1] = S[j, i]
+    if (!skip) {
+      // p_i = tau * sum_l S[i,l] u_l (i, l > j) -> sc.vals; K partial sums -> red2[1]
+      double kpart = 0.0;
+      for (int i = j + 1 + warp; i < k; i += NW) {
+        double sum = 0.0;
+        for (int l = j + 1 + lane; l < k; l += 32) sum = fma(S[l * ld + i], l == j + 1 ? u0 : S[j * ld + l], sum);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const double pi = tau * sum;
+        if (lane == 0) sc.vals[i] = pi;
+        kpart = fma(i == j + 1 ? u0 : S[j * ld + i], pi, kpart);
+      }
+      if (lane == 0) sc.red[warp] = kpart;                        // fixed-order sum below
+    }
+    __syncthreads();                                             // (2)
+    if (!skip) {
+      double ksum = 0.0;
+      for (int w = 0; w < NW; ++w) ksum += sc.red[w];
+      const double K = 0.5 * tau * ksum;
+      // S_sub -= u q^T + q u^T with q = p - K u
+      for (int l = j + 1 + warp; l < k; l += NW) {
+        const double ul = l == j + 1 ? u0 : S[j * ld + l];
+        const double ql = sc.vals[l] - K * ul;
+        for (int i = j + 1 + lane; i < k; i += 32) {
+          const double ui = i == j + 1 ? u0 : S[j * ld + i];
+          const double qi = sc.vals[i] - K * ui;
+          S[l * ld + i] -= ui * ql + qi * ul;
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      tw.d[j] = S[j * ld + j];
+      tw.e[j] = skip ? x0 : alpha;
+      tw.tau[j] = tau;
+    }
+    __syncthreads();                                             // (3)
+    if (threadIdx.x == 0 && !skip) S[j * ld + j + 1] = u0;       // reflector stored in place
+  }
+  if (threadIdx.x == 0) {
+    if (k >= 2) {
+      tw.d[k - 2] = S[(k - 2) * ld + k - 2];
+      tw.e[k - 2] = S[(k - 2) * ld + k - 1];
+      tw.tau[k - 2] = 0.0;
+    }
+    tw.d[k - 1] = S[(k - 1) * ld + k - 1];
+    tw.e[k - 1] = 0.0;
+    tw.tau[k - 1] = 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) sc.tq[i] = tw.e[i] * tw.e[i];   // e^2
+  __syncthreads();
+  if (threadIdx.x == 0) g_triprof[1] = clock64();
+  // ---- 2. bisection (warp multisection, absolute tolerance ~eps ||T||) ---------------
+  double glo = 0.0, ghi = 0.0;
+  for (int i = 0; i < k; ++i) {
+    const double r = (i > 0 ? fabs(tw.e[i - 1]) : 0.0) + (i + 1 < k ? fabs(tw.e[i]) : 0.0);
+    glo = i == 0 ? tw.d[i] - r : fmin(glo, tw.d[i] - r);
+    ghi = i == 0 ? tw.d[i] + r : fmax(ghi, tw.d[i] + r);
+  }
+  const double tnrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
+  const double pivmin = fmax(tnrm * 2.2250738585072014e-308 / 2.220446049250313e-16, 2.2250738585072014e-308);
+  const double atol = 2.0 * 2.220446049250313e-16 * tnrm;
+  glo -= 2.220446049250313e-16 * tnrm + 2.0 * pivmin;
+  ghi += 2.220446049250313e-16 * tnrm + 2.0 * pivmin;
+  // half-warps: lanes 0-15 and 16-31 each run a 16-way multisection on their own eigenvalue
+  {
+    const int hl = lane & 15, half = lane >> 4;
+    const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+    for (int m = 2 * warp + half; m - half < k; m += 2 * NW) {   // m-th smallest eigenvalue
+      const bool act = m < k;
+      double lo = glo, hi = ghi;
+      for (int it = 0; it < 40; ++it) {
+        const bool more = act && hi - lo > fmax(atol, 4.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi)));
+        if (!__any_sync(0xffffffffu, more)) break;
+        const double x = lo + (hi - lo) * (double)(hl + 1) / 17.0;
+        const int c = more ? sturm_fast(tw.d, sc.tq, k, x, pivmin) : 0;
+        const unsigned above = __ballot_sync(0xffffffffu, more && c > m) & hmask;
+        if (more) {
+          const int f = above ? __ffs(above) - 1 - 16 * half : 16;
+          const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f / 17.0;
+          const double nhi = f == 16 ? hi : lo + (hi - lo) * (double)(f + 1) / 17.0;
+          lo = nlo;
+          hi = nhi;
+        }
+      }
+      if (act && hl == 0) tw.lam[m] = 0.5 * (lo + hi);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) g_triprof[2] = clock64();
+  // ---- 3. eigenvectors by twisted factorisation (one thread per eigenvalue) -----------
+  //   D+_i forward, D-_i backward, gamma_r = D+_r + D-_r - (d_r - lam); twist at argmin |gamma|
+  //   x_r = 1; x_i = -(e_i / D+_i) x_{i+1} (i < r);  x_i = -(e_{i-1} / D-_i) x_{i-1} (i > r)
+  if (threadIdx.x == 0) sc.flag = 1;
+  __syncthreads();
+  double* dminus = tw.wk;                      // [k][k]: dminus[i * k + m] (coalesced over m)
+  for (int m = threadIdx.x; m < k; m += blockDim.x) {
+    const double lam = tw.lam[m];
+    double* z = Z + (size_t)(k - 1 - m) * ldz;   // descending order output column; holds D+ first
+    double q = tw.d[0] - lam;
+    if (fabs(q) < pivmin) q = -pivmin;
+    z[0] = q;
+    for (int i = 1; i < k; ++i) {
+      q = (tw.d[i] - lam) - sc.tq[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      z[i] = q;
+    }
+    q = tw.d[k - 1] - lam;
+    if (fabs(q) < pivmin) q = -pivmin;
+    dminus[(size_t)(k - 1) * k + m] = q;
+    for (int i = k - 2; i >= 0; --i) {
+      q = (tw.d[i] - lam) - sc.tq[i] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      dminus[(size_t)i * k + m] = q;
+    }
+    int r = 0;
+    double best = 1e300;
+    for (int i = 0; i < k; ++i) {
+      const double g = fabs(z[i] + dminus[(size_t)i * k + m] - (tw.d[i] - lam));
+      if (g < best) { best = g; r = i; }
+    }
+    // x below the twist (uses D+ stored in z[i], i < r) -- walk down, overwriting z
+    double xv = 1.0;
+    for (int i = r - 1; i >= 0; --i) {
+      xv = -(tw.e[i] / z[i]) * xv;
+      z[i] = xv;
+    }
+    z[r] = 1.0;
+    xv = 1.0;
+    for (int i = r + 1; i < k; ++i) {
+      xv = -(tw.e[i - 1] / dminus[(size_t)i * k + m]) * xv;
+      z[i] = xv;
+    }
+    double nrm = 0.0;
+    for (int i = 0; i < k; ++i) nrm = fma(z[i], z[i], nrm);
+    nrm = sqrt(nrm);
+    if (!(nrm > 0.0) || !isfinite(nrm)) { sc.flag = 0; continue; }
+    for (int i = 0; i < k; ++i) z[i] /= nrm;
+    vals_desc[k - 1 - m] = lam;
+  }
+  __syncthreads();
+  // clusters of (numerically) coincident eigenvalues: Gram-Schmidt, one thread per cluster
+  const double ctol = 1e-9 * tnrm;
+  for (int m0 = threadIdx.x; m0 < k; m0 += blockDim.x) {
+    if (m0 > 0 && tw.lam[m0] - tw.lam[m0 - 1] <= ctol) continue;
+    int m1 = m0 + 1;
+    while (m1 < k && tw.lam[m1] - tw.lam[m1 - 1] <= ctol) ++m1;
+    for (int m = m0 + 1; m < m1; ++m) {
+      double* z = Z + (size_t)(k - 1 - m) * ldz;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int mm = m0; mm < m; ++mm) {
+          const double* y = Z + (size_t)(k - 1 - mm) * ldz;
+          double dot = 0.0;
+          for (int i = 0; i < k; ++i) dot = fma(y[i], z[i], dot);
+          for (int i = 0; i < k; ++i) z[i] -= dot * y[i];
+        }
+      double nrm = 0.0;
+      for (int i = 0; i < k; ++i) nrm = fma(z[i], z[i], nrm);
+      nrm = sqrt(nrm);
+      if (!(nrm > 1e-8)) { sc.flag = 0; continue; }
+      for (int i = 0; i < k; ++i) z[i] /= nrm;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { g_triprof[3] = clock64(); g_triprof[5] = sc.flag; }
+  if (!sc.flag) return false;
+  // ---- 4. back-transformation: z <- H_0 ... H_{k-3} z ----------------------------------
+  for (int j = k - 3; j >= 0; --j) {
+    const double tau = tw.tau[j];
+    if (tau == 0.0) continue;                 // uniform: tau is shared
+    for (int c = warp; c < k; c += NW) {
+      double* zc = Z + (size_t)c * ldz;
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < k; i += 32) s = fma(S[j * ld + i], zc[i], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      s *= tau;
+      for (int i = j + 1 + lane; i < k; i += 32) zc[i] -= s * S[j * ld + i];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) g_triprof[4] = clock64();
+  return true;
+}
 
 // mode 0: sym_eig(A)      -> values[k], vectors (k x k)            (smallsolve.py:34-49)
 // mode 1: raw jacobi_eig  -> values = diag (unsorted), vectors = V  (_kernels.pyx:105-150)
@@ -271,7 +541,7 @@ __global__ void __launch_bounds__(ET, 1)
     k_small_eig(int mode, const double* __restrict__ A, const double* __restrict__ Mm, int k, double raw_tol,
                 int raw_sweeps, double* __restrict__ values, double* __restrict__ vectors, int* __restrict__ n_out,
                 int* __restrict__ status, double* __restrict__ off_out, int* __restrict__ sweeps_out, EigBufs gb,
-                int nsm) {
+                int nsm, double* __restrict__ wk, int use_tridiag) {
   extern __shared__ double dsm[];
   __shared__ EigScratch sc;
   __shared__ double tau[MAXK];
@@ -379,13 +649,32 @@ __global__ void __launch_bounds__(ET, 1)
   for (int j = warp; j < kp; j += NW)
     for (int i = lane; i < kp; i += 32) S[j * L + i] = (V[j * L + i] + V[i * L + j]) / 2.0;
   __syncthreads();
-  const double nrm = fro_norm(S, kp, L, sc.red), tol = 1e-14 * nrm;
-  const double off = jacobi_parallel(S, L, V, L, kp, tol, JACOBI_MAX_SWEEPS, sc, nullptr);
-  if (off > tol && nrm > 0.0) {
-    if (threadIdx.x == 0) { *status = OFRR_ERR_CONVERGENCE; *n_out = 0; if (off_out) *off_out = off; }
-    return;
+  bool tri_ok = false;
+  if (use_tridiag) {
+    // Householder + bisection + inverse iteration (O(k) sequential depth).  S is consumed,
+    // so a copy goes to the buffer that is free at this point (P after Cholesky whitening,
+    // T after eigen-whitening) for the Jacobi fallback.
+    double* Ssave = chol ? P : T;
+    for (int j = warp; j < kp; j += NW)
+      for (int i = lane; i < kp; i += 32) Ssave[j * L + i] = S[j * L + i];
+    __syncthreads();
+    TriWork tw{sc.td, sc.te, sc.ttau, sc.tlam, wk};
+    tri_ok = sym_eig_tridiag(S, L, kp, tau, V, L, tw, sc);
+    if (!tri_ok) {   // restore and fall back to Jacobi
+      for (int j = warp; j < kp; j += NW)
+        for (int i = lane; i < kp; i += 32) S[j * L + i] = Ssave[j * L + i];
+      __syncthreads();
+    }
   }
-  for (int i = threadIdx.x; i < kp; i += blockDim.x) tau[i] = S[i * L + i];
+  if (!tri_ok) {
+    const double nrm = fro_norm(S, kp, L, sc.red), tol = 1e-14 * nrm;
+    const double off = jacobi_parallel(S, L, V, L, kp, tol, JACOBI_MAX_SWEEPS, sc, nullptr);
+    if (off > tol && nrm > 0.0) {
+      if (threadIdx.x == 0) { *status = OFRR_ERR_CONVERGENCE; *n_out = 0; if (off_out) *off_out = off; }
+      return;
+    }
+    for (int i = threadIdx.x; i < kp; i += blockDim.x) tau[i] = S[i * L + i];
+  }
   __syncthreads();
   if (threadIdx.x == 0) g_k5prof[5] = clock64();
   // ---- back-transform y = W Z  (W = L^-T, or P D^-1/2) -> S, then sort + sign ----
@@ -408,7 +697,7 @@ __global__ void __launch_bounds__(ET, 1)
   if (threadIdx.x == 0) { *status = 0; *n_out = kp; }
 }
 
-size_t small_eig_ws(int k) { return (size_t)4 * k * pad_k(k) * sizeof(double) + 1024; }
+size_t small_eig_ws(int k) { return (size_t)4 * k * pad_k(k) * sizeof(double) + (size_t)5 * k * k * sizeof(double) + 2048; }
 
 int small_eig(int mode, const double* A, const double* M, int k, double raw_tol, int raw_sweeps, double* values,
               double* vectors, int* n_out, int* status, double* off_out, int* sweeps_out, void* ws, size_t ws_bytes,
@@ -419,19 +708,30 @@ int small_eig(int mode, const double* A, const double* M, int k, double raw_tol,
   double* p = (double*)ws;
   const size_t kL = (size_t)k * pad_k(k);
   b.S = p; b.V = p + kL; b.P = p + 2 * kL; b.T = p + 3 * kL;
+  double* wk = p + 4 * kL;
   const size_t one = kL * sizeof(double);
-  const size_t budget = 190 * 1024;
+  const size_t budget = 160 * 1024;
   int nsm = one ? (int)std::min<size_t>(4, budget / one) : 0;
   const size_t shm = (size_t)nsm * one;
   static bool attr = false;
   if (!attr) {
-    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_small_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 190 * 1024));
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_small_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
+  static int tridiag = -1;
+  if (tridiag < 0) {
+    const char* e = getenv("OFRR_EIG_JACOBI");   // 1: force the reference-order Jacobi for eig(T)
+    tridiag = (e && atoi(e) == 1) ? 0 : 1;
+  }
   k_small_eig<<<1, ET, shm, st>>>(mode, A, M, k, raw_tol, raw_sweeps, values, vectors, n_out, status, off_out,
-                                  sweeps_out, b, nsm);
+                                  sweeps_out, b, nsm, wk, tridiag);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
+}
+
+int k5_profile(long long* out) {
+  if (cudaMemcpyFromSymbol(out, g_k5prof, sizeof(g_k5prof)) != cudaSuccess) return 2;
+  return cudaMemcpyFromSymbol(out + 8, g_triprof, sizeof(g_triprof)) == cudaSuccess ? 0 : 2;
 }
 
 }  // namespace ofrr

@@ -25,9 +25,10 @@ PAD = 64
 
 # launch accounting (bench.py "gpu_launches"): number of libofrr_b200 kernels enqueued
 LAUNCHES = [0]
-# optional per-op CUDA-event timing of the block product (bench.py roofline): when a list
-# is installed here, gemm_av appends (start_event, end_event, bytes) for every call
-GEMM_EVENTS = None
+# optional log of the tensor-core block products (bench.py roofline): when a list is
+# installed here, gemm_av appends (algorithmic bytes, flops) of every k_gemm_av_tc launch;
+# the kernel-only durations come from the library (ofrr_prof_gemm_read), in launch order
+GEMM_LOG = None
 
 
 def _count(n: int) -> None:
@@ -186,10 +187,6 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
     ws_b = L.ofrr_gemm_av_workspace(A.rows, A.cols, k, int(A.fmt), int(transpose))
     ws = _ws(ws_b, A.device)
     of = int(W.fmt if out_fmt is None else out_fmt)
-    ev = GEMM_EVENTS
-    if ev is not None:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
     split = A.fmt == FpFormat.BF16 and X.fmt == FpFormat.F32 and not transpose
     if split:
         # fp32 block on the bf16 tensor cores (3 bf16 slices, one pass over A)
@@ -205,11 +202,12 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
                                    W.ptr, W.ld, of, _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
                                    W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else of,
                                    ws.data_ptr(), ws.numel(), _stream()), "gemm_av")
-    if ev is not None:
-        e1.record()
-        # algorithmic bytes: A once + X once + W once
-        nb = A.rows * A.cols * A.fmt.itemsize + A.cols * k * X.fmt.itemsize + A.rows * k * FpFormat(of).itemsize
-        ev.append((e0, e1, nb, 2.0 * A.rows * A.cols * k))
+    if GEMM_LOG is not None and (split or (A.fmt.tensor_core and not transpose)):
+        # algorithmic bytes of the tensor-core kernel: A once + the B operand
+        # once (3 bf16 slices in split mode); W is written by the finalize kernel
+        kb = 3 * k if split else k
+        nb = A.rows * A.cols * A.fmt.itemsize + A.cols * kb * (2 if split else X.fmt.itemsize)
+        GEMM_LOG.append((nb, 2.0 * A.rows * A.cols * kb))
     _count(3 if split else 2 if (A.fmt.tensor_core and not transpose) else 1)
 
 

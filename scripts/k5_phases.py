@@ -13,7 +13,7 @@ for _ in range(2):
     ops.sym_def_gen_eig(B, M, k)
 torch.cuda.synchronize()
 L = _lib.load()
-out = (ctypes.c_longlong * 8)()
+out = (ctypes.c_longlong * 16)()
 L.ofrr_debug_k5_profile.argtypes = [ctypes.c_void_p]
 L.ofrr_debug_k5_profile(ctypes.addressof(out))
 t = list(out)
@@ -22,3 +22,8 @@ for i, nm in enumerate(names):
     if t[i + 1] and t[i]:
         print(f"{nm:24s} {(t[i + 1] - t[i]) / 1965.0:9.1f} us")
 print(f"total {(t[6] - t[0]) / 1965.0:.1f} us")
+tn = ["tridiagonalise", "bisection", "inverse iteration", "back-transform"]
+for i, nm in enumerate(tn):
+    if t[8 + i + 1] and t[8 + i]:
+        print(f"  tri {nm:20s} {(t[8 + i + 1] - t[8 + i]) / 1965.0:9.1f} us")
+print("  tri ok flag", t[13])

@@ -162,3 +162,25 @@ def test_driver_eig_fp32_basis_on_bf16_operator(ofrr_gpu, oracle):
     exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
     _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
     assert np.max(rs.residuals[:top]) < 1e-4
+
+
+@pytest.mark.parametrize("pname", ["tc-bf16", "tc-f16", "full-f32"])
+def test_driver_svd_tensor_core_vs_oracle(ofrr_gpu, oracle, pname):
+    """partial SVD on the tensor-core path (A V and A^T U both K-major: A^T resident):
+    tall low-rank + noise matrix (C4-style, scaled down), vs the oracle on the same A."""
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(SEED)
+    n1, n2, r, k, top, m = 3000, 512, 40, 24, 8, 5
+    g1, _ = np.linalg.qr(rng.standard_normal((n1, r)))
+    g2, _ = np.linalg.qr(rng.standard_normal((n2, r)))
+    sig = 0.8 ** np.arange(r)
+    a = (g1 * sig) @ g2.T + 1e-4 * rng.standard_normal((n1, n2)) / np.sqrt(n2)
+    pol = p.POLICY_PRESETS[pname]
+    store = pol.storage if pol.storage != p.FpFormat.F32 else p.FpFormat.BF16
+    a = o.round_to(a, int(store))
+    cfg = p.IterConfig(k=k, m=m, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr", policy=pol,
+                       seed=SEED)
+    rs = p.subspace_iter_svd(p.DenseMatrix(a, store), cfg)
+    ref = o.subspace_iter_svd(a, k=k, m=m, iters=1, pol=o.as_pol(pol), seed=SEED)
+    exact = np.linalg.svd(a, compute_uv=False)
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
