@@ -424,27 +424,37 @@ __global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n
   }
 }
 
+static constexpr int SPLIT_KC = 85;   // 3 * 85 = 255 <= 256 columns per pass
+
 size_t split_workspace(int64_t rows, int64_t cols, int k) {
+  const int kc = std::min(k, SPLIT_KC);
   const int64_t lds = (cols + 63) / 64 * 64;
-  return (size_t)3 * k * lds * 2 + 1024 + tc_workspace(rows, cols, 3 * k, BF16);
+  return (size_t)3 * kc * lds * 2 + 1024 + tc_workspace(rows, cols, 3 * kc, BF16);
 }
 
+// k <= 85: one pass over A with N = 3k.  k > 85: column chunks of <= 85, one pass each
+// (full fp32 semantics at the price of ceil(k / 85) passes).
 int tc_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, const float* X, int64_t ldx, int k,
                      void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes,
                      cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2) {
-  if (3 * k > 256) {
-    ofrr_set_error("gemm_av: fp32 block on bf16 tensor cores needs 3k <= 256 (k=%d)", k);
-    return OFRR_ERR_UNSUPPORTED;
-  }
   if (ws_bytes < split_workspace(rows, cols, k)) { ofrr_set_error("gemm_av split: workspace too small"); return OFRR_ERR_INVALID; }
   const int64_t lds = (cols + 63) / 64 * 64;
+  const int kcmax = std::min(k, SPLIT_KC);
   __nv_bfloat16* Xs = (__nv_bfloat16*)ws;
-  uint8_t* rest = (uint8_t*)ws + (((size_t)3 * k * lds * 2 + 1023) & ~size_t(1023));
-  unsigned gx = (unsigned)std::min<int64_t>((cols + 255) / 256, 64);
-  k_split_bf16<<<dim3(gx, k), 256, 0, st>>>(X, ldx, cols, k, Xs, lds);
-  OFRR_CHECK_LAUNCH();
-  return tc_gemm_av(A, rows, cols, lda, BF16, Xs, lds, 3 * k, W, ldw, out_fmt, colmax, flags, rest,
-                    ws_bytes - (rest - (uint8_t*)ws), st, W2, ldw2, out_fmt2, 3);
+  uint8_t* rest = (uint8_t*)ws + (((size_t)3 * kcmax * lds * 2 + 1023) & ~size_t(1023));
+  const size_t rest_bytes = ws_bytes - (rest - (uint8_t*)ws);
+  const int ob = fmt_bytes(out_fmt), ob2 = fmt_bytes(out_fmt2);
+  for (int j0 = 0; j0 < k; j0 += SPLIT_KC) {
+    const int kc = std::min(SPLIT_KC, k - j0);
+    unsigned gx = (unsigned)std::min<int64_t>((cols + 255) / 256, 64);
+    k_split_bf16<<<dim3(gx, kc), 256, 0, st>>>(X + (int64_t)j0 * ldx, ldx, cols, kc, Xs, lds);
+    OFRR_CHECK_LAUNCH();
+    const int rc = tc_gemm_av(A, rows, cols, lda, BF16, Xs, lds, 3 * kc, (uint8_t*)W + (size_t)j0 * ldw * ob, ldw,
+                              out_fmt, colmax ? colmax + j0 : nullptr, flags, rest, rest_bytes, st,
+                              W2 ? (uint8_t*)W2 + (size_t)j0 * ldw2 * ob2 : nullptr, ldw2, out_fmt2, 3);
+    if (rc) return rc;
+  }
+  return OFRR_OK;
 }
 
 }  // namespace ofrr

@@ -4,6 +4,7 @@
 //   * k_scale_columns (K2), k_convert.
 #include "common.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace ofrr {
 
@@ -297,6 +298,173 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------
+// FP64 residual product on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64):
+// CTA tile 128 x 64, 8 warps as 4 (rows) x 2 (cols), warp tile 32 x 32 = 4 x 4 DMMA tiles,
+// k-tile 32 staged as As[m][k] / Bs[n][k] (k contiguous, padded to 36: fragment loads
+// are bank-conflict free), register-staged prefetch of the next k-tile.
+// Fragments (PTX m8n8k4 .f64): a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// c[2] = C[lane/4][2*(lane%4) + {0,1}].
+// ---------------------------------------------------------------------------------
+static constexpr int DBM = 128, DBN = 64, DBK = 32, DLK = 36;
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <typename TA>
+__global__ void __launch_bounds__(256, 1)
+    k_resid_dmma(const TA* __restrict__ A, int64_t lda, int64_t m, int64_t K, const double* __restrict__ V,
+                 int64_t ldv, int n, const double* __restrict__ Y, int64_t ldy, const double* __restrict__ vals,
+                 const int* __restrict__ r_dev, double* __restrict__ part) {
+  extern __shared__ double dsh[];
+  double* As = dsh;                        // [2][DBM][DLK]
+  double* Bs = dsh + 2 * DBM * DLK;        // [2][DBN][DLK]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;   // warp tile origin: rows 32*wm, cols 32*wn
+  const int64_t m0 = (int64_t)blockIdx.x * DBM;
+  const int n0 = blockIdx.y * DBN;
+  const int nvalid = r_dev ? min(n, *r_dev) : n;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // staging: A tile 128 x 32 -> thread (row tid/2, 16 k); V tile 64 cols x 32 k -> thread (col tid/4, 8 k)
+  uint4 araw[2];
+  double areg[16], breg[8];
+  bool avec = false;
+  auto fetch = [&](int64_t k0) {
+    const int r = tid >> 1, kh = (tid & 1) * 16;
+    const int64_t gr = m0 + r;
+    avec = false;
+    if constexpr (sizeof(TA) == 2) {
+      if (gr < m && k0 + kh + 16 <= K) {
+        const uint4* pp = reinterpret_cast<const uint4*>(A + gr * lda + k0 + kh);
+        araw[0] = __ldg(pp);
+        araw[1] = __ldg(pp + 1);
+        avec = true;
+      }
+    }
+    if (!avec) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int64_t gk = k0 + kh + e;
+        areg[e] = (gr < m && gk < K) ? to_d(A[gr * lda + gk]) : 0.0;
+      }
+    }
+    const int c = tid >> 2, kq = (tid & 3) * 8;
+    const int gc = n0 + c;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int64_t gk = k0 + kq + e;
+      breg[e] = (gc < n && gk < K) ? V[(int64_t)gc * ldv + gk] : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+    const int r = tid >> 1, kh = (tid & 1) * 16;
+    double* Ab = As + buf * DBM * DLK + r * DLK + kh;
+    if constexpr (sizeof(TA) == 2) {
+      if (avec) {
+        const uint32_t w[8] = {araw[0].x, araw[0].y, araw[0].z, araw[0].w, araw[1].x, araw[1].y, araw[1].z, araw[1].w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          TA lo, hi;
+          const uint16_t l16 = (uint16_t)(w[e] & 0xffffu), h16 = (uint16_t)(w[e] >> 16);
+          memcpy(&lo, &l16, 2);
+          memcpy(&hi, &h16, 2);
+          Ab[2 * e] = to_d(lo);
+          Ab[2 * e + 1] = to_d(hi);
+        }
+      }
+    }
+    if (!avec) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) Ab[e] = areg[e];
+    }
+    const int c = tid >> 2, kq = (tid & 3) * 8;
+    double* Bb = Bs + buf * DBN * DLK + c * DLK + kq;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) Bb[e] = breg[e];
+  };
+  const int nk = (int)((K + DBK - 1) / DBK);
+  fetch(0);
+  store(0);
+  __syncthreads();
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    const bool more = t + 1 < nk;
+    if (more) fetch((int64_t)(t + 1) * DBK);
+    const double* Ab = As + cur * DBM * DLK + (32 * wm + fr) * DLK + fk;
+    const double* Bb = Bs + cur * DBN * DLK + (32 * wn + fr) * DLK + fk;
+#pragma unroll
+    for (int kk = 0; kk < DBK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Ab[i * 8 * DLK + kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bb[j * 8 * DLK + kk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+    if (more) store(cur ^ 1);
+    __syncthreads();
+  }
+  // epilogue: C[row][col] = acc[i][j][e] at row 32 wm + 8 i + lane/4, col 32 wn + 8 j + 2 (lane%4) + e
+  double* csum = dsh;   // [4 (wm)][DBN] partial column sums (reuse smem after the final barrier)
+  for (int e = tid; e < 4 * DBN; e += blockDim.x) csum[e] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int lc = 32 * wn + 8 * j + 2 * (lane & 3) + h;
+      const int gc = n0 + lc;
+      double s = 0.0;
+      if (gc < nvalid) {
+        const double lam = vals[gc];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t gr = m0 + 32 * wm + 8 * i + (lane >> 2);
+          if (gr < m) {
+            const double d = acc[i][j][h] - lam * Y[(int64_t)gc * ldy + gr];
+            s = fma(d, d, s);
+          }
+        }
+      }
+      // reduce over the 8 lanes sharing this column (lane>>2 varies), fixed order
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((lane >> 2) == 0) csum[wm * DBN + lc] = s;
+    }
+  __syncthreads();
+  if (tid < DBN && n0 + tid < n) {
+    const double s = ((csum[tid] + csum[DBN + tid]) + csum[2 * DBN + tid]) + csum[3 * DBN + tid];
+    part[(int64_t)blockIdx.x * n + n0 + tid] = s;
+  }
+}
+
+template <typename TA>
+static int launch_resid_dmma(const void* A, int64_t lda, int64_t m, int64_t K, const double* V, int64_t ldv, int n,
+                             const double* Y, int64_t ldy, const double* vals, const int* r_dev, double* part,
+                             cudaStream_t st) {
+  const size_t shm = (size_t)2 * (DBM + DBN) * DLK * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_resid_dmma<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    attr = true;
+  }
+  dim3 grid((unsigned)((m + DBM - 1) / DBM), (unsigned)((n + DBN - 1) / DBN));
+  k_resid_dmma<TA><<<grid, 256, shm, st>>>((const TA*)A, lda, m, K, V, ldv, n, Y, ldy, vals, r_dev, part);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
 template <typename TA>
 static int launch_resid64(const void* A, int64_t lda, int64_t m, int64_t K, const double* V, int64_t ldv, int n,
                           const double* Y, int64_t ldy, const double* vals, const int* r_dev, double* part,
@@ -378,11 +546,22 @@ int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
   double* part = (double*)ws;
   int rc;
   if (!transpose && a_fmt != FP8) {
-    switch (a_fmt) {
-      case F64: rc = launch_resid64<double>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
-      case F32: rc = launch_resid64<float>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
-      case F16: rc = launch_resid64<__half>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
-      default: rc = launch_resid64<__nv_bfloat16>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+    static int use_simt = -1;
+    if (use_simt < 0) { const char* e = getenv("OFRR_RESID_SIMT"); use_simt = (e && atoi(e) == 1) ? 1 : 0; }
+    if (use_simt) {
+      switch (a_fmt) {
+        case F64: rc = launch_resid64<double>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+        case F32: rc = launch_resid64<float>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+        case F16: rc = launch_resid64<__half>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+        default: rc = launch_resid64<__nv_bfloat16>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+      }
+    } else {
+      switch (a_fmt) {
+        case F64: rc = launch_resid_dmma<double>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+        case F32: rc = launch_resid_dmma<float>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+        case F16: rc = launch_resid_dmma<__half>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+        default: rc = launch_resid_dmma<__nv_bfloat16>(A, lda, m, K, Xv, ldx, r_max, Yv, ldy, vals, r_dev, part, st); break;
+      }
     }
     if (rc) return rc;
     const int nb = (int)((m + RBM - 1) / RBM);
