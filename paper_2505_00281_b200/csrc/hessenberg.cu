@@ -27,6 +27,8 @@ namespace ofrr {
 static constexpr int HT = 256;
 
 struct HessWs {
+  unsigned* bar_count;  // grid barrier arrivals
+  unsigned* bar_gen;    // grid barrier generation
   double* cand_val;   // [2][G]
   long long* cand_idx;  // [2][G]
   double* cand_row;   // [2][G][k]
@@ -65,7 +67,6 @@ __global__ void __launch_bounds__(HT)
                  int storage, int compute_rt, double tol, T* __restrict__ Q, int64_t ldq,
                  int64_t* __restrict__ pivots, int* __restrict__ kept, int* __restrict__ n_kept, HessWs ws,
                  int in_smem) {
-  cg::grid_group grid = cg::this_grid();
   __shared__ double sv[HT / 32];
   __shared__ long long si[HT / 32];
   extern __shared__ double dyn[];
@@ -87,13 +88,42 @@ __global__ void __launch_bounds__(HT)
   for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) ws.freerow[i] = 1;
   __syncthreads();
 
-  auto publish = [&](int j, int buf) {
-    // local argmax of |Xw[i, j]| over my free rows, then publish value/idx/row
+  // split grid barrier: arrive (release) ... independent work ... wait (acquire).  The
+  // counters are zeroed before the launch; all CTAs are co-resident (cooperative launch).
+  unsigned phase = 0;
+  auto arrive = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(ws.bar_count, 1u);
+      if (old == (unsigned)G - 1) {
+        atomicExch(ws.bar_count, 0u);
+        __threadfence();
+        atomicAdd(ws.bar_gen, 1u);
+      }
+    }
+    ++phase;
+  };
+  auto wait = [&]() {
+    if (threadIdx.x == 0) {
+      unsigned g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(ws.bar_gen) : "memory");
+      } while (g < phase);
+    }
+    __syncthreads();
+  };
+
+  // publish my pivot candidate for column jn: max |Xw[i, jn]| over my free rows (lowest
+  // index on ties) and that row's values in columns jn..k-1 *after* the current step's
+  // elimination.  Columns > jn may still be pending (deferred) in Xw: their values for the
+  // candidate row are formed here with exactly the arithmetic of the deferred update.
+  auto publish = [&](int jn, int buf, bool pending, int jp, long long rp) {
     double v = -1.0;
     long long idx = -1;
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
       if (!ws.freerow[i]) continue;
-      const double a = fabs(to_d(Xw[(int64_t)j * ldw + i]));
+      const double a = fabs(to_d(Xw[(int64_t)jn * ldw + i]));
       if (idx < 0 || a > v) { v = a; idx = i; }   // ascending i per thread: keeps lowest on ties
     }
     block_argmax(v, idx, sv, si);
@@ -101,14 +131,21 @@ __global__ void __launch_bounds__(HT)
       ws.cand_val[buf * G + c] = v;
       ws.cand_idx[buf * G + c] = idx;
     }
-    if (idx >= 0)
-      for (int cc = j + threadIdx.x; cc < k; cc += HT)
-        ws.cand_row[((int64_t)buf * G + c) * k + cc] = to_d(Xw[(int64_t)cc * ldw + idx]);
+    if (idx >= 0) {
+      const double vr = pending ? rnd(to_d(Xw[(int64_t)jp * ldw + idx]), compute) : 0.0;
+      for (int cc = jn + threadIdx.x; cc < k; cc += HT) {
+        double y = to_d(Xw[(int64_t)cc * ldw + idx]);
+        if (pending && cc > jn)
+          y = rnd(c_sub(rnd(y, compute), c_mul(prow[cc], vr, compute), compute), storage);
+        ws.cand_row[((int64_t)buf * G + c) * k + cc] = y;
+      }
+    }
+    (void)rp;
   };
 
-  publish(0, 0);
-  __threadfence();
-  grid.sync();
+  publish(0, 0, false, 0, -1);
+  arrive();
+  wait();
 
   int nk = 0;
   for (int j = 0; j < k; ++j) {
@@ -155,28 +192,38 @@ __global__ void __launch_bounds__(HT)
       }
       if (r >= r0 && r < r1 && threadIdx.x == 0) ws.freerow[r] = 0;
       if (c == 0 && threadIdx.x == 0) { kept[j] = 1; pivots[nk] = r; }
+      // alpha_c = round_c(a[r, c]) for the axpys of ofrr/precision.py:172-180
+      for (int cc = j + 1 + threadIdx.x; cc < k; cc += HT) prow[cc] = rnd(prow[cc], compute);
       __syncthreads();
-      // ofrr/basis.py:188-190 + precision.py:172-180: a[:,i] = round_s(c(a) - c(c(a[r,i]) * c(v)))
-      for (int cc = j + 1 + threadIdx.x; cc < k; cc += HT) prow[cc] = rnd(prow[cc], compute);   // alpha_c
-      __syncthreads();
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
-        const double v = rnd(to_d(Xw[(int64_t)j * ldw + i]), compute);
-        T* yp = Xw + i;
-        for (int cc = j + 1; cc < k; ++cc) {
-          const double y = to_d(yp[(int64_t)cc * ldw]);
-          const double t = c_mul(prow[cc], v, compute);
-          yp[(int64_t)cc * ldw] = from_d<T>(rnd(c_sub(rnd(y, compute), t, compute), storage));
+      // ofrr/basis.py:188-190: column j+1 now (the next pivot search needs it) ...
+      if (j + 1 < k) {
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+          const double v = rnd(to_d(Xw[(int64_t)j * ldw + i]), compute);
+          T* yp = Xw + (int64_t)(j + 1) * ldw + i;
+          *yp = from_d<T>(rnd(c_sub(rnd(to_d(*yp), compute), c_mul(prow[j + 1], v, compute), compute), storage));
         }
+        __syncthreads();
+        publish(j + 1, buf ^ 1, true, j, r);
+        arrive();
+        // ... columns j+2.. while the other CTAs catch up (hidden behind the barrier)
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+          const double v = rnd(to_d(Xw[(int64_t)j * ldw + i]), compute);
+          T* yp = Xw + i;
+          for (int cc = j + 2; cc < k; ++cc) {
+            const double y = to_d(yp[(int64_t)cc * ldw]);
+            yp[(int64_t)cc * ldw] = from_d<T>(rnd(c_sub(rnd(y, compute), c_mul(prow[cc], v, compute), compute), storage));
+          }
+        }
+        wait();
       }
       ++nk;
-      __syncthreads();
-    } else if (c == 0 && threadIdx.x == 0) {
-      kept[j] = 0;
-    }
-    if (j + 1 < k) {
-      publish(j + 1, buf ^ 1);
-      __threadfence();
-      grid.sync();
+    } else {
+      if (c == 0 && threadIdx.x == 0) kept[j] = 0;
+      if (j + 1 < k) {
+        publish(j + 1, buf ^ 1, false, 0, -1);
+        arrive();
+        wait();
+      }
     }
   }
   if (c == 0 && threadIdx.x == 0) *n_kept = nk;
@@ -203,7 +250,7 @@ size_t hessenberg_ws(int64_t n, int k, int storage) {
   b += (size_t)2 * G * k * sizeof(double);
   b += (size_t)n * fmt_bytes(storage) * k;  // working copy
   b += n;
-  return b + 2048;
+  return b + 4096;
 }
 
 template <typename T, int C>
@@ -213,6 +260,9 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   uint8_t* p = (uint8_t*)ws;
   auto take = [&](size_t bytes) { uint8_t* q = p; p += (bytes + 255) & ~size_t(255); return q; };
   HessWs h;
+  h.bar_count = (unsigned*)take(256);
+  h.bar_gen = h.bar_count + 32;
+  OFRR_CUDA_TRY(cudaMemsetAsync(h.bar_count, 0, 256, st));
   h.cand_val = (double*)take(2 * G * sizeof(double));
   h.cand_idx = (long long*)take(2 * G * sizeof(long long));
   h.cand_row = (double*)take((size_t)2 * G * k * sizeof(double));
