@@ -7,14 +7,15 @@
 // pivots, kept mask and Q agree bit for bit with the reference for every policy.
 //
 // One persistent cooperative kernel, one CTA per SM (grid <= #SMs), each CTA owning a
-// contiguous row block.  Per column j there is exactly one grid-wide barrier:
-//   before the barrier every CTA publishes its local pivot candidate for column j
-//   (max |X[i,j]| over its free rows, lowest index on ties) together with that row's
-//   values in columns j..k-1; after the barrier every CTA reduces the candidates in
-//   ascending CTA order (= ascending row order, so ties resolve to the lowest index),
-//   scales column j by the pivot, applies the rank-1 trailing update with the pivot
-//   row taken from the published candidate, and computes its candidate for column j+1
-//   in the same pass.  Candidates are double buffered by step parity.
+// contiguous row block (in shared memory when it fits).  Per column j there is exactly
+// one grid-wide barrier, split into arrive and wait:
+//   after the wait every CTA reduces the published candidates in ascending CTA order
+//   (= ascending row order, so ties resolve to the lowest index), scales column j by the
+//   pivot and updates column j+1 only; it then publishes its candidate for column j+1
+//   (max |X[i,j+1]| over its free rows, and that row's values in columns j+1..k-1 with the
+//   pending update applied on the fly) and arrives; the bulk trailing update of columns
+//   j+2..k-1 runs between arrive and wait, hidden behind the slowest CTA's arrival.
+//   Candidates are double buffered by step parity.
 #include "common.cuh"
 #include <cooperative_groups.h>
 #include <algorithm>
@@ -226,6 +227,9 @@ __global__ void __launch_bounds__(HT)
       }
     }
   }
+  // columns nk..k-1 of Q are zero (a caller may project with all k columns speculatively)
+  for (int j = nk; j < k; ++j)
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Q[(int64_t)j * ldq + i] = from_d<T>(0.0);
   if (c == 0 && threadIdx.x == 0) *n_kept = nk;
 }
 
@@ -273,12 +277,14 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   int64_t ldw = n;
   const int64_t rows_per = (n + G - 1) / G;
   const size_t tile = (size_t)rows_per * k * sizeof(T);
-  int in_smem = tile <= (size_t)160 * 1024 ? 1 : 0;
+  // up to the 227 KB opt-in per CTA (one CTA per SM): C3's fp32 rows (443 x 128) fit
+  const size_t smem_max = 226 * 1024;
+  int in_smem = (size_t)k * sizeof(double) + tile + 16 <= smem_max ? 1 : 0;
   size_t shmem = (size_t)k * sizeof(double) + (in_smem ? tile + 16 : 0);
   static bool attr = false;
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute((const void*)k_hessenberg<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024));
+                                       (int)smem_max));
     attr = true;
   }
   void* args[] = {(void*)&Xp, (void*)&n, (void*)&k, (void*)&ldx, (void*)&Xw, (void*)&ldw, (void*)&storage,

@@ -245,33 +245,40 @@ class EigEngine:
         X = self.start_block()
         eig = U64 = U = None
         r = 0
-        rs = None
+        rs = vals = None
         for it in range(cfg.m):
             st = torch.zeros(8, dtype=torch.int32, device=self.device)
             X = self.power(X, st)
             h = self.basis(X, st)
-            s = _fetch_status(st, self.comm)                      # sync 1: MatVec flags, basis width
+            last = it == cfg.m - 1
+            # project speculatively with every column (the basis keeps all k in the common
+            # case; dropped columns of Q are zero): one host sync per outer iteration
+            kp = X.k
+            U = h.Q.narrow(kp)
+            eig, U64, Xn, est = self.project(U, st, want64=last, top_check=(top if check else None))
+            s, vals_all, est_np = self._fetch(st, eig.values, est)  # the iteration's one sync
             if s[S_MV_FLAGS] & 1:
                 raise OverflowDiagnostic("non-finite entries after MatVec")
-            kp = int(s[S_NKEPT])
-            if kp == 0:
+            if s[S_NKEPT] == 0:
                 raise EmptyBasisError("all columns skipped in Hessenberg process")
-            U = h.Q.narrow(kp)
-            last = it == cfg.m - 1
-            eig, U64, Xn, est = self.project(U, st, want64=last, top_check=(top if check else None))
-            s = _fetch_status(st, self.comm)                      # sync 2: pencil status, width
+            if s[S_NKEPT] < kp:                                    # rare: redo with the kept width
+                kp = int(s[S_NKEPT])
+                U = h.Q.narrow(kp)
+                st[S_EIG_STATUS:].zero_()                     # gram/pencil/restart slots
+                eig, U64, Xn, est = self.project(U, st, want64=last, top_check=(top if check else None))
+                s, vals_all, est_np = self._fetch(st, eig.values, est)
             _raise_for(s, "projection")
             r = int(s[S_NOUT])
+            vals = vals_all[:r]
             X = Xn.narrow(r)
             self.stats.iterations = it + 1
             if check:
-                vals_np = eig.values[:r].cpu().numpy()
-                e = self.finish_residuals(est, vals_np)
+                e = self._finish(est_np, vals)
                 worst = float(np.max(e[: min(top, r)])) if r >= top else float("inf")
                 if worst < tol or last:
                     if U64 is None:
                         U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
-                    rs = self.report(U64, eig, r)                 # FP64 confirmation
+                    rs = self.report(U64, eig, r, vals)                 # FP64 confirmation
                     worst = float(np.max(rs.residuals[: min(top, r)])) if r >= top else float("inf")
                     self.stats.history.append((it + 1, worst))
                     if worst < tol:
@@ -282,12 +289,40 @@ class EigEngine:
         if rs is None:
             if U64 is None:
                 U64, _ = self.ops.ritz(U, eig.vectors, U.k, eig.n_out, U.k, 1.0, want64=True)
-            rs = self.report(U64, eig, r)
+            rs = self.report(U64, eig, r, vals)
         return rs
 
-    def report(self, U64, eig, r: int) -> RitzSet:
-        vals = eig.values[:r].cpu().numpy()
-        rs = RitzSet(vals, DenseMatrix.from_block(U64.narrow(r)), "eig")
+    def _fetch(self, st, *vecs):
+        """One device->host read: the status word (max over ranks) and fp64 vectors."""
+        import torch
+        if self.comm.distributed:
+            self.comm.all_reduce_max_(st)
+        parts = [st.to(torch.float64)] + [v.reshape(-1).to(torch.float64) for v in vecs if v is not None]
+        host = torch.cat(parts).cpu().numpy()
+        out = [host[:8].astype(np.int64)]
+        off = 8
+        for v in vecs:
+            if v is None:
+                out.append(None)
+                continue
+            out.append(host[off:off + v.numel()])
+            off += v.numel()
+        return out
+
+    def _finish(self, r, vals_np):
+        """Host finish of residuals read back: relative already (one GPU) or sums of
+        squares (row-partitioned, ||.||^2 all-reduced) -> sqrt / |lambda|."""
+        if self.comm.distributed:
+            lam = vals_np[: len(r)]
+            r = r[: len(lam)]
+            with np.errstate(divide="ignore"):
+                return np.where(lam == 0.0, np.inf, np.sqrt(r) / np.abs(lam))
+        return r
+
+    def report(self, U64, eig, r: int, vals=None) -> RitzSet:
+        if vals is None:
+            vals = eig.values[:r].cpu().numpy()
+        rs = RitzSet(np.array(vals[:r]), DenseMatrix.from_block(U64.narrow(r)), "eig")
         return self.residual_report(rs, U64, eig, r)
 
     def residual_report(self, rs: RitzSet, U64, eig, r: int) -> RitzSet:
