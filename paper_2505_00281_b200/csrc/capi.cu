@@ -327,6 +327,8 @@ int ofrr_host_jacobi_eig(const double* a, int64_t n, int max_sweeps, double tol,
 
 namespace ofrr { int k5_profile(long long* out); }
 extern "C" int ofrr_debug_k5_profile(long long* out8) { return ofrr::k5_profile(out8); }
+namespace ofrr { int hess_profile(unsigned long long* out); }
+extern "C" int ofrr_debug_hess_profile(unsigned long long* out8) { return ofrr::hess_profile(out8); }
 
 namespace ofrr { void prof_enable(int on); int prof_read(float* ms, int max); }
 extern "C" void ofrr_prof_gemm_enable(int on) { ofrr::prof_enable(on); }

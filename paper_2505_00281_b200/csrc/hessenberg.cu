@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 namespace cg = cooperative_groups;
 
@@ -28,8 +29,8 @@ namespace ofrr {
 static constexpr int HT = 256;
 
 struct HessWs {
-  unsigned* bar_count;  // grid barrier arrivals
-  unsigned* bar_gen;    // grid barrier generation
+  unsigned* bar_count;  // grid barrier arrivals (monotonic)
+  unsigned long long* key;  // [k] packed (|pivot| f32 bits, ~row) maxima, non-f64 storage
   double* cand_val;   // [2][G]
   long long* cand_idx;  // [2][G]
   double* cand_row;   // [2][G][k]
@@ -37,7 +38,8 @@ struct HessWs {
 };
 
 __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* sv, long long* si) {
-  // max value; ties -> lowest index; idx < 0 means "no candidate"
+  // max value; ties -> lowest index; idx < 0 means "no candidate".  One barrier: every
+  // thread folds the per-warp results itself (the caller separates consecutive uses).
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -47,31 +49,115 @@ __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* 
   }
   if (lane == 0) { sv[warp] = v; si[warp] = idx; }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < HT / 32; ++w) {
-      const double ov = sv[w];
-      const long long oi = si[w];
-      if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
-    }
-    sv[0] = v;
-    si[0] = idx;
-  }
-  __syncthreads();
   v = sv[0];
   idx = si[0];
-  __syncthreads();
+  for (int w = 1; w < HT / 32; ++w) {
+    const double ov = sv[w];
+    const long long oi = si[w];
+    if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
+  }
 }
 
-template <typename T, int compute>
+// Packed candidate key for storage formats narrower than f64: |x| is exact in f32 and its
+// bit pattern orders like the value (NaN above inf, as np.argmax picks NaN); the low word
+// ~row makes ties resolve to the lowest row.  0 = no candidate.
+__device__ __forceinline__ unsigned long long cand_key(float absval, long long row) {
+  return ((unsigned long long)__float_as_uint(absval) << 32) | (unsigned)(0xFFFFFFFFu - (unsigned)row);
+}
+__device__ __forceinline__ unsigned long long block_max_key(unsigned long long key, unsigned long long* sk) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+    key = ok > key ? ok : key;
+  }
+  if (lane == 0) sk[warp] = key;
+  __syncthreads();
+  key = sk[0];
+  for (int w = 1; w < HT / 32; ++w) key = sk[w] > key ? sk[w] : key;
+  return key;
+}
+
+// ---- compute-format arithmetic in the narrowest native type -------------------------
+// The reference rounds every product / difference / quotient into the compute format and
+// every stored value into the storage format (ofrr/precision.py:172-185).  For compute
+// formats up to F32 one f32 operation (RN, no contraction) followed by a rounding into the
+// compute format is exactly that (f16/bf16 via f32 are exact by the 2p+2 bound); for F64
+// compute the same ops run in f64.  Operands are always representable in the compute
+// format (storage <= compute), so loading them needs no rounding.
+struct f8 { uint8_t x; };    // FP8 e4m3 storage element
+template <int C> struct CT { using type = float; };
+template <> struct CT<F64> { using type = double; };
+
+template <int C> __device__ __forceinline__ float rcf(float x) {
+  if constexpr (C == F16) return __half2float(__float2half_rn(x));
+  else if constexpr (C == BF16) return __bfloat162float(__float2bfloat16_rn(x));
+  else return x;
+}
+template <int C> __device__ __forceinline__ typename CT<C>::type cmul(typename CT<C>::type a, typename CT<C>::type b) {
+  if constexpr (C == F64) return __dmul_rn(a, b); else return rcf<C>(__fmul_rn(a, b));
+}
+template <int C> __device__ __forceinline__ typename CT<C>::type csub(typename CT<C>::type a, typename CT<C>::type b) {
+  if constexpr (C == F64) return __dsub_rn(a, b); else return rcf<C>(__fsub_rn(a, b));
+}
+template <int C> __device__ __forceinline__ typename CT<C>::type cdiv(typename CT<C>::type a, typename CT<C>::type b) {
+  if constexpr (C == F64) return __ddiv_rn(a, b); else return rcf<C>(__fdiv_rn(a, b));
+}
+// element (storage) -> compute type, exact
+template <int C, typename T> __device__ __forceinline__ typename CT<C>::type ld_c(T y) {
+  if constexpr (std::is_same<T, f8>::value) {
+    __nv_fp8_e4m3 v; v.__x = y.x; return (typename CT<C>::type)float(v);
+  } else if constexpr (std::is_same<T, double>::value) {
+    return (typename CT<C>::type)y;   // storage F64 implies compute F64
+  } else if constexpr (std::is_same<T, float>::value) {
+    return (typename CT<C>::type)y;
+  } else if constexpr (std::is_same<T, __half>::value) {
+    return (typename CT<C>::type)__half2float(y);
+  } else {
+    return (typename CT<C>::type)__bfloat162float(y);
+  }
+}
+// compute value -> storage element, rounded into the storage format (common.cuh rnd)
+template <typename T, typename V> __device__ __forceinline__ T st_s(V v) {
+  if constexpr (std::is_same<T, double>::value) return (double)v;
+  else {
+    const float f = std::is_same<V, double>::value ? __double2float_rn((double)v) : (float)v;
+    if constexpr (std::is_same<T, float>::value) return f;
+    else if constexpr (std::is_same<T, __half>::value) return __float2half_rn(f);
+    else if constexpr (std::is_same<T, __nv_bfloat16>::value) return __float2bfloat16_rn(f);
+    else {
+      f8 o;
+      const float r = rnd_fp8f(f);
+      __nv_fp8_e4m3 q(r);
+      if (isinf(r)) q.__x = r > 0 ? 0x7e : 0xfe;
+      o.x = q.__x;
+      return o;
+    }
+  }
+}
+template <typename T> __device__ __forceinline__ double el_d(T y) {
+  if constexpr (std::is_same<T, f8>::value) { __nv_fp8_e4m3 v; v.__x = y.x; return (double)float(v); }
+  else return to_d(y);
+}
+
+__device__ unsigned long long g_hessprof[8];   // debug: CTA 0 per-phase time (ns), last launch
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <typename T, int C>
 __global__ void __launch_bounds__(HT)
     k_hessenberg(const T* __restrict__ X, int64_t n, int k, int64_t ldx, T* __restrict__ Xg, int64_t ldg,
-                 int storage, int compute_rt, double tol, T* __restrict__ Q, int64_t ldq,
-                 int64_t* __restrict__ pivots, int* __restrict__ kept, int* __restrict__ n_kept, HessWs ws,
-                 int in_smem) {
+                 double tol, T* __restrict__ Q, int64_t ldq, int64_t* __restrict__ pivots, int* __restrict__ kept,
+                 int* __restrict__ n_kept, HessWs ws, int in_smem) {
+  using CV = typename CT<C>::type;
   __shared__ double sv[HT / 32];
   __shared__ long long si[HT / 32];
   extern __shared__ double dyn[];
   double* prow = dyn;                                        // pivot row values, k entries
+  CV* pc = reinterpret_cast<CV*>(dyn + k);                   // alpha_c (compute format), k entries
 
   const int G = gridDim.x, c = blockIdx.x;
   const int64_t rows_per = (n + G - 1) / G;
@@ -81,147 +167,228 @@ __global__ void __launch_bounds__(HT)
   // my working rows: in shared memory when they fit (column-major, ld rows_per), else in
   // the global workspace.  Xw is indexed with global row numbers.
   const int64_t ldw = in_smem ? rows_per : ldg;
-  T* Xw = in_smem ? reinterpret_cast<T*>(dyn + k) - r0 : Xg;
+  T* Xw = in_smem ? reinterpret_cast<T*>(dyn + 2 * k) - r0 : Xg;
+  // thread -> (row, column phase) for the trailing updates: two threads per row when the
+  // row block is at most half the CTA
+  const int tpr = (2 * nr <= HT) ? 2 : 1;
+  const int rb = HT / tpr;
+  const int trow = threadIdx.x % rb, tcol = threadIdx.x / rb;
 
-  // prologue: private copy of my rows, free flags, candidate for column 0
+  // prologue: private copy of my rows, free flags
   for (int j = 0; j < k; ++j)
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Xw[(int64_t)j * ldw + i] = X[(int64_t)j * ldx + i];
   for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) ws.freerow[i] = 1;
   __syncthreads();
 
-  // split grid barrier: arrive (release) ... independent work ... wait (acquire).  The
-  // counters are zeroed before the launch; all CTAs are co-resident (cooperative launch).
+  // split grid barrier: arrive (release) ... independent work ... wait (acquire).  One
+  // monotonically increasing arrival counter (zeroed before the launch): barrier number p
+  // is complete once it reaches p * G.  All CTAs are co-resident (cooperative launch).
   unsigned phase = 0;
   auto arrive = [&]() {
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned old = atomicAdd(ws.bar_count, 1u);
-      if (old == (unsigned)G - 1) {
-        atomicExch(ws.bar_count, 0u);
-        __threadfence();
-        atomicAdd(ws.bar_gen, 1u);
-      }
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ws.bar_count) : "memory");
     }
     ++phase;
   };
   auto wait = [&]() {
     if (threadIdx.x == 0) {
+      const unsigned target = phase * (unsigned)G;
       unsigned g;
       do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(ws.bar_gen) : "memory");
-      } while (g < phase);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(ws.bar_count) : "memory");
+      } while (g < target);
     }
     __syncthreads();
   };
 
-  // publish my pivot candidate for column jn: max |Xw[i, jn]| over my free rows (lowest
-  // index on ties) and that row's values in columns jn..k-1 *after* the current step's
-  // elimination.  Columns > jn may still be pending (deferred) in Xw: their values for the
-  // candidate row are formed here with exactly the arithmetic of the deferred update.
-  auto publish = [&](int jn, int buf, bool pending, int jp, long long rp) {
-    double v = -1.0;
-    long long idx = -1;
+  // Pivot candidates.  Narrow storage: one packed key per column (atomicMax over CTAs).
+  // F64 storage: (value, row) per CTA, reduced by every CTA after the barrier.
+  constexpr bool KEYED = !std::is_same<T, double>::value;
+  __shared__ unsigned long long sk[HT / 32];
+  // this thread's candidate over its rows i (free rows only) of column jn
+  auto local_scan = [&](int jn, double& v, long long& idx, unsigned long long& key) {
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
       if (!ws.freerow[i]) continue;
-      const double a = fabs(to_d(Xw[(int64_t)jn * ldw + i]));
-      if (idx < 0 || a > v) { v = a; idx = i; }   // ascending i per thread: keeps lowest on ties
-    }
-    block_argmax(v, idx, sv, si);
-    if (threadIdx.x == 0) {
-      ws.cand_val[buf * G + c] = v;
-      ws.cand_idx[buf * G + c] = idx;
-    }
-    if (idx >= 0) {
-      const double vr = pending ? rnd(to_d(Xw[(int64_t)jp * ldw + idx]), compute) : 0.0;
-      for (int cc = jn + threadIdx.x; cc < k; cc += HT) {
-        double y = to_d(Xw[(int64_t)cc * ldw + idx]);
-        if (pending && cc > jn)
-          y = rnd(c_sub(rnd(y, compute), c_mul(prow[cc], vr, compute), compute), storage);
-        ws.cand_row[((int64_t)buf * G + c) * k + cc] = y;
+      const double a = fabs(el_d(Xw[(int64_t)jn * ldw + i]));
+      if constexpr (KEYED) {
+        const unsigned long long kk = cand_key((float)a, i);
+        key = kk > key ? kk : key;
+      } else {
+        if (idx < 0 || a > v) { v = a; idx = i; }   // ascending i per thread: lowest on ties
       }
     }
-    (void)rp;
+  };
+  // publish the CTA's candidate for column jn and that row's values in columns jn..k-1
+  // *after* the current step's elimination.  Columns > jn may still be pending (deferred)
+  // in Xw: their values for the candidate row are formed here with exactly the arithmetic
+  // of the deferred update.
+  auto publish = [&](int jn, int buf, bool pending, int jp, double v, long long idx, unsigned long long key) {
+    if constexpr (KEYED) {
+      key = block_max_key(key, sk);
+      idx = key ? (long long)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull)) : -1;
+      if (threadIdx.x == 0 && key) atomicMax(&ws.key[jn], key);
+    } else {
+      block_argmax(v, idx, sv, si);
+      if (threadIdx.x == 0) {
+        ws.cand_val[buf * G + c] = v;
+        ws.cand_idx[buf * G + c] = idx;
+      }
+    }
+    if (idx >= 0) {
+      const CV vr = pending ? ld_c<C>(Xw[(int64_t)jp * ldw + idx]) : CV(0);
+      for (int cc = jn + threadIdx.x; cc < k; cc += HT) {
+        T y = Xw[(int64_t)cc * ldw + idx];
+        if (pending && cc > jn) y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(pc[cc], vr)));
+        ws.cand_row[((int64_t)buf * G + c) * k + cc] = el_d(y);
+      }
+    }
   };
 
-  publish(0, 0, false, 0, -1);
+  {
+    double v = -1.0;
+    long long idx = -1;
+    unsigned long long key = 0;
+    local_scan(0, v, idx, key);
+    publish(0, 0, false, 0, v, idx, key);
+  }
   arrive();
   wait();
 
   int nk = 0;
+  unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0}, tp = gtime();
+  auto mark = [&](int ph) {
+    if (c == 0 && threadIdx.x == 0) { const unsigned long long t = gtime(); pacc[ph] += t - tp; tp = t; }
+  };
+  __shared__ double s_best;
+  __shared__ long long s_r;
+  __shared__ int s_owner;
   for (int j = 0; j < k; ++j) {
     const int buf = j & 1;
-    // reduce the candidates: warp 0, lanes strided over CTAs; max value, ties -> lowest row
-    // (CTA row blocks ascend, so the lowest row is the reference's np.argmax choice)
-    __shared__ double s_best;
-    __shared__ long long s_r;
-    __shared__ int s_owner;
-    if (threadIdx.x < 32) {
-      double bv = -1.0;
-      long long bi = -1;
-      int bo = -1;
-      for (int cc = threadIdx.x; cc < G; cc += 32) {
-        const long long oi = __ldcg(&ws.cand_idx[buf * G + cc]);
-        const double ov = __ldcg(&ws.cand_val[buf * G + cc]);
-        if (oi >= 0 && (bi < 0 || ov > bv)) { bv = ov; bi = oi; bo = cc; }
-      }
+    double best;
+    long long r;
+    int owner;
+    if constexpr (KEYED) {
+      // every thread reads the column's winning key (one L2 word)
+      const unsigned long long key = __ldcg(&ws.key[j]);
+      r = key ? (long long)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull)) : -1;
+      best = (double)__uint_as_float((unsigned)(key >> 32));
+      owner = r >= 0 ? (int)(r / rows_per) : 0;
+    } else {
+      // warp 0 reduces the CTAs' candidates; max value, ties -> lowest row (CTA row
+      // blocks ascend, so the lowest row is the reference's np.argmax choice)
+      if (threadIdx.x < 32) {
+        double bv = -1.0;
+        long long bi = -1;
+        int bo = -1;
+        for (int cc = threadIdx.x; cc < G; cc += 32) {
+          const long long oi = __ldcg(&ws.cand_idx[buf * G + cc]);
+          const double ov = __ldcg(&ws.cand_val[buf * G + cc]);
+          if (oi >= 0 && (bi < 0 || ov > bv)) { bv = ov; bi = oi; bo = cc; }
+        }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
-        if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; bo = oo; }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
+          if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; bo = oo; }
+        }
+        if (threadIdx.x == 0) { s_best = bv; s_r = bi; s_owner = bo; }
       }
-      if (threadIdx.x == 0) { s_best = bv; s_r = bi; s_owner = bo; }
+      __syncthreads();
+      best = s_best;
+      r = s_r;
+      owner = s_owner;
     }
-    __syncthreads();
-    const double best = s_best;
-    const long long r = s_r;
-    const int owner = s_owner;
     // ofrr/basis.py:178-180: skip when no free row or |pivot| < tol (NaN pivots skip too)
     const bool skip = (r < 0) || !(best >= tol);
+    mark(0);
     if (!skip) {
-      for (int cc = j + threadIdx.x; cc < k; cc += HT) prow[cc] = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
-      __syncthreads();
-      const double piv = prow[j];
-      // ofrr/basis.py:181-187: v = round_s(round_c(v / piv)); v[r] = 1
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
-        const double x = to_d(Xw[(int64_t)j * ldw + i]);
-        const double v = (i == r) ? 1.0 : rnd(c_div(x, piv, compute), storage);
-        Xw[(int64_t)j * ldw + i] = from_d<T>(v);
-        Q[(int64_t)nk * ldq + i] = from_d<T>(v);
+      // pivot row (values exact in the storage format); alpha_c = round_c(a[r, c]) is the
+      // value itself (storage <= compute)
+      for (int cc = j + threadIdx.x; cc < k; cc += HT) {
+        const double a = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
+        prow[cc] = a;
+        pc[cc] = (CV)a;
       }
       if (r >= r0 && r < r1 && threadIdx.x == 0) ws.freerow[r] = 0;
       if (c == 0 && threadIdx.x == 0) { kept[j] = 1; pivots[nk] = r; }
-      // alpha_c = round_c(a[r, c]) for the axpys of ofrr/precision.py:172-180
-      for (int cc = j + 1 + threadIdx.x; cc < k; cc += HT) prow[cc] = rnd(prow[cc], compute);
       __syncthreads();
-      // ofrr/basis.py:188-190: column j+1 now (the next pivot search needs it) ...
-      if (j + 1 < k) {
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
-          const double v = rnd(to_d(Xw[(int64_t)j * ldw + i]), compute);
+      mark(1);
+      const CV piv = pc[j];
+      const CV a1 = j + 1 < k ? pc[j + 1] : CV(0);
+      // ofrr/basis.py:181-187: v = round_s(round_c(v / piv)); v[r] = 1; then (188-190,
+      // precision.py:172-180) column j+1 at once -- the next pivot search needs it -- and
+      // this thread's candidate for it
+      double cv = -1.0;
+      long long cidx = -1;
+      unsigned long long ckey = 0;
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+        const T v = (i == r) ? st_s<T>(CV(1)) : st_s<T>(cdiv<C>(ld_c<C>(Xw[(int64_t)j * ldw + i]), piv));
+        Xw[(int64_t)j * ldw + i] = v;
+        Q[(int64_t)nk * ldq + i] = v;
+        if (j + 1 < k) {
           T* yp = Xw + (int64_t)(j + 1) * ldw + i;
-          *yp = from_d<T>(rnd(c_sub(rnd(to_d(*yp), compute), c_mul(prow[j + 1], v, compute), compute), storage));
-        }
-        __syncthreads();
-        publish(j + 1, buf ^ 1, true, j, r);
-        arrive();
-        // ... columns j+2.. while the other CTAs catch up (hidden behind the barrier)
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
-          const double v = rnd(to_d(Xw[(int64_t)j * ldw + i]), compute);
-          T* yp = Xw + i;
-          for (int cc = j + 2; cc < k; ++cc) {
-            const double y = to_d(yp[(int64_t)cc * ldw]);
-            yp[(int64_t)cc * ldw] = from_d<T>(rnd(c_sub(rnd(y, compute), c_mul(prow[cc], v, compute), compute), storage));
+          const T y = st_s<T>(csub<C>(ld_c<C>(*yp), cmul<C>(a1, ld_c<C>(v))));
+          *yp = y;
+          if (i != r && ws.freerow[i]) {
+            const double a = fabs(el_d(y));
+            if constexpr (KEYED) {
+              const unsigned long long kk = cand_key((float)a, i);
+              ckey = kk > ckey ? kk : ckey;
+            } else {
+              if (cidx < 0 || a > cv) { cv = a; cidx = i; }
+            }
           }
         }
+      }
+      mark(2);
+      if (j + 1 < k) {
+        publish(j + 1, buf ^ 1, true, j, cv, cidx, ckey);
+        arrive();
+        mark(3);
+        // ... columns j+2.. while the other CTAs catch up (hidden behind the barrier).
+        // Two rows x two columns per iteration, all loads before the stores (ILP).
+        for (int64_t i0 = r0 + trow; i0 < r1; i0 += 2 * rb) {
+          const bool h1 = i0 + rb < r1;
+          const CV v0 = ld_c<C>(Xw[(int64_t)j * ldw + i0]);
+          const CV v1 = h1 ? ld_c<C>(Xw[(int64_t)j * ldw + i0 + rb]) : CV(0);
+          T* p = Xw + (int64_t)(j + 2 + tcol) * ldw + i0;
+          const int64_t st1 = (int64_t)tpr * ldw;
+          int cc = j + 2 + tcol;
+          for (; cc + tpr < k; cc += 2 * tpr, p += 2 * st1) {
+            const CV a0 = pc[cc], a1 = pc[cc + tpr];
+            const CV y00 = ld_c<C>(p[0]), y01 = ld_c<C>(p[st1]);
+            const CV y10 = h1 ? ld_c<C>(p[rb]) : CV(0), y11 = h1 ? ld_c<C>(p[st1 + rb]) : CV(0);
+            p[0] = st_s<T>(csub<C>(y00, cmul<C>(a0, v0)));
+            p[st1] = st_s<T>(csub<C>(y01, cmul<C>(a1, v0)));
+            if (h1) {
+              p[rb] = st_s<T>(csub<C>(y10, cmul<C>(a0, v1)));
+              p[st1 + rb] = st_s<T>(csub<C>(y11, cmul<C>(a1, v1)));
+            }
+          }
+          if (cc < k) {
+            const CV a0 = pc[cc];
+            const CV y00 = ld_c<C>(p[0]);
+            const CV y10 = h1 ? ld_c<C>(p[rb]) : CV(0);
+            p[0] = st_s<T>(csub<C>(y00, cmul<C>(a0, v0)));
+            if (h1) p[rb] = st_s<T>(csub<C>(y10, cmul<C>(a0, v1)));
+          }
+        }
+        __syncthreads();
+        mark(4);
         wait();
+        mark(5);
       }
       ++nk;
     } else {
       if (c == 0 && threadIdx.x == 0) kept[j] = 0;
       if (j + 1 < k) {
-        publish(j + 1, buf ^ 1, false, 0, -1);
+        double v = -1.0;
+        long long idx = -1;
+        unsigned long long key = 0;
+        local_scan(j + 1, v, idx, key);
+        publish(j + 1, buf ^ 1, false, 0, v, idx, key);
         arrive();
         wait();
       }
@@ -229,8 +396,15 @@ __global__ void __launch_bounds__(HT)
   }
   // columns nk..k-1 of Q are zero (a caller may project with all k columns speculatively)
   for (int j = nk; j < k; ++j)
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Q[(int64_t)j * ldq + i] = from_d<T>(0.0);
-  if (c == 0 && threadIdx.x == 0) *n_kept = nk;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Q[(int64_t)j * ldq + i] = st_s<T>(CV(0));
+  if (c == 0 && threadIdx.x == 0) {
+    *n_kept = nk;
+    for (int i = 0; i < 6; ++i) g_hessprof[i] = pacc[i];
+  }
+}
+
+int hess_profile(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_hessprof, sizeof(g_hessprof)) == cudaSuccess ? 0 : 2;
 }
 
 static int hess_grid(int64_t n) {
@@ -248,7 +422,7 @@ static int hess_grid(int64_t n) {
 
 size_t hessenberg_ws(int64_t n, int k, int storage) {
   const int G = hess_grid(n);
-  size_t b = 0;
+  size_t b = 256 + (size_t)k * 8 + 256;
   b += 2 * G * sizeof(double);
   b += 2 * G * sizeof(long long);
   b += (size_t)2 * G * k * sizeof(double);
@@ -265,8 +439,8 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   auto take = [&](size_t bytes) { uint8_t* q = p; p += (bytes + 255) & ~size_t(255); return q; };
   HessWs h;
   h.bar_count = (unsigned*)take(256);
-  h.bar_gen = h.bar_count + 32;
-  OFRR_CUDA_TRY(cudaMemsetAsync(h.bar_count, 0, 256, st));
+  h.key = (unsigned long long*)take((size_t)k * 8);
+  OFRR_CUDA_TRY(cudaMemsetAsync(h.bar_count, 0, 256 + ((size_t)k * 8 + 255) / 256 * 256, st));
   h.cand_val = (double*)take(2 * G * sizeof(double));
   h.cand_idx = (long long*)take(2 * G * sizeof(long long));
   h.cand_row = (double*)take((size_t)2 * G * k * sizeof(double));
@@ -279,17 +453,18 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   const size_t tile = (size_t)rows_per * k * sizeof(T);
   // up to the 227 KB opt-in per CTA (one CTA per SM): C3's fp32 rows (443 x 128) fit
   const size_t smem_max = 226 * 1024;
-  int in_smem = (size_t)k * sizeof(double) + tile + 16 <= smem_max ? 1 : 0;
-  size_t shmem = (size_t)k * sizeof(double) + (in_smem ? tile + 16 : 0);
+  int in_smem = (size_t)2 * k * sizeof(double) + tile + 16 <= smem_max ? 1 : 0;
+  size_t shmem = (size_t)2 * k * sizeof(double) + (in_smem ? tile + 16 : 0);
   static bool attr = false;
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute((const void*)k_hessenberg<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_max));
     attr = true;
   }
-  void* args[] = {(void*)&Xp, (void*)&n, (void*)&k, (void*)&ldx, (void*)&Xw, (void*)&ldw, (void*)&storage,
-                  (void*)&compute, (void*)&tol, (void*)&Qp, (void*)&ldq, (void*)&pivots, (void*)&kept,
-                  (void*)&n_kept, (void*)&h, (void*)&in_smem};
+  (void)storage; (void)compute;
+  void* args[] = {(void*)&Xp, (void*)&n, (void*)&k, (void*)&ldx, (void*)&Xw, (void*)&ldw, (void*)&tol,
+                  (void*)&Qp, (void*)&ldq, (void*)&pivots, (void*)&kept, (void*)&n_kept, (void*)&h,
+                  (void*)&in_smem};
   OFRR_CUDA_TRY(cudaMemsetAsync(kept, 0, sizeof(int) * k, st));
   OFRR_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hessenberg<T, C>, dim3(G), dim3(HT), args, shmem, st));
   return OFRR_OK;
@@ -309,6 +484,10 @@ int hessenberg(const void* X, int64_t n, int k, int64_t ldx, int storage, int co
     case BF16 * 8 + BF16: HESS(__nv_bfloat16, BF16);
     case BF16 * 8 + F32: HESS(__nv_bfloat16, F32);
     case BF16 * 8 + F64: HESS(__nv_bfloat16, F64);
+    case FP8 * 8 + F16: HESS(f8, F16);
+    case FP8 * 8 + BF16: HESS(f8, BF16);
+    case FP8 * 8 + F32: HESS(f8, F32);
+    case FP8 * 8 + F64: HESS(f8, F64);
     default:
       ofrr_set_error("hessenberg: storage %d / compute %d unsupported", storage, compute);
       return OFRR_ERR_UNSUPPORTED;

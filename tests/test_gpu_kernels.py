@@ -134,7 +134,8 @@ def test_scale_columns_bitwise(ofrr_gpu, oracle, pname, pol):
 
 
 @pytest.mark.parametrize("pol", [(BF16, F32, F32), (F16, F32, F32), (F16, F16, F16), (F16, F16, F32),
-                                 (F32, F32, F32), (F64, F64, F64)])
+                                 (F32, F32, F32), (F64, F64, F64), (FP8, F32, F32), (FP8, BF16, F32),
+                                 (F32, F64, F64), (BF16, BF16, F32)])
 @pytest.mark.parametrize("n,k", [(300, 12), (5000, 64), (20000, 40)])
 def test_hessenberg_bitwise(ofrr_gpu, oracle, pol, n, k):
     """K3 reproduces ofrr/basis.py:151-196 bit for bit: Q, pivots, kept."""
