@@ -173,6 +173,11 @@ int ofrr_ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, 
  * ofrr_residual_pair: res[j] = max(res[j], ||op(A) x_j - s_j y_j|| / s_j).
  * ------------------------------------------------------------------------------- */
 size_t ofrr_residual_workspace(int64_t rows, int r);
+/* Workspace of ofrr_residual_eig / ofrr_residual_pair for a rows x cols operator in a_fmt.
+ * For a 16/8-bit operator (not transposed) the FP64-accurate product runs on the int8
+ * tensor cores (Ozaki scheme: six 7-bit digit planes of A and of the vectors, exact int32
+ * level sums); the workspace then holds the digit planes (~6 bytes per entry of A). */
+size_t ofrr_residual_workspace2(int64_t rows, int64_t cols, int r, int a_fmt, int transpose);
 int ofrr_residual_eig(const void* A, int64_t n, int64_t lda, int a_fmt, const double* V,
                       int64_t ldv, const double* vals, const int* r_dev, int r_max, double* res,
                       void* workspace, size_t workspace_bytes, void* stream);

@@ -24,6 +24,7 @@ int resid_est(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw,
               const double* Y, int ldy, const double* vals, const int* r_dev, int r_max, double* res, int mode,
               void* ws, size_t ws_bytes, cudaStream_t st);
 size_t residual_ws(int64_t rows, int r);
+size_t residual_ws2(int64_t rows, int64_t cols, int r, int a_fmt, int transpose);
 int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const double* Xv,
                   int64_t ldx, const double* Yv, int64_t ldy, const double* vals, const int* r_dev, int r_max,
                   double* res, int accumulate_max, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -179,6 +180,9 @@ int ofrr_ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, 
 }
 
 size_t ofrr_residual_workspace(int64_t rows, int r) { return residual_ws(rows, r); }
+size_t ofrr_residual_workspace2(int64_t rows, int64_t cols, int r, int a_fmt, int transpose) {
+  return residual_ws2(rows, cols, r, a_fmt, transpose);
+}
 
 size_t ofrr_residual_estimate_workspace(int64_t n, int r) { return resid_est_ws(n, r); }
 

@@ -288,6 +288,12 @@ static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t i
   return OFRR_OK;
 }
 
+// 2-D uint8 map with 128B swizzle (the int8 digit planes of oz.cu)
+int oz_make_tmap_u8(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                    uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_2d(tm, base, FP8, inner, outer, ld_bytes, box_inner, box_outer);
+}
+
 // N of the UMMA = k rounded up to a multiple of 32 (M=128 needs N % 16 == 0, N <= 256)
 // ---- kernel-only timing of k_gemm_av_tc (bench.py roofline): CUDA events recorded on the
 // launching stream immediately around the launch, read back after the timed region ----

@@ -1,0 +1,605 @@
+// oz.cu -- K7z: FP64-accurate A * V for a 16/8-bit operator on the int8 tensor cores
+// (Ozaki scheme: error-free integer slices, exact int32 accumulation).
+//
+// Replaces the FP64 product inside the reference's residual report
+// (ofrr/projection.py:136-147: A @ v in numpy float64 on to_dense_f64(A)).
+//
+// Representation.  Every row i of A gets a power-of-two scale 2^T_i > max_l |a_il|, every
+// column j of V a scale 2^F_j > max_l |v_lj|.  An entry is written in fixed point on a
+// 42-bit window below its scale and split into six signed 7-bit digits:
+//     a_il = 2^(T_i - 42) * sum_p a^(p)_il 2^(7 (6 - p))        (truncated below 2^(T_i - 42))
+// A bf16/fp16/e4m3 entry is exact unless it is 2^-34 below its row maximum.  Products of
+// digits are exact in int8 x int8 -> int32 (tcgen05.mma kind::i8), and an int32 level sum
+//     D_L = sum_{p + q = L} sum_l a^(p)_il v^(q)_lj,   L = 2..7 (p, q = 1..6, 21 products)
+// cannot overflow while a chunk of K covers at most 16384 terms (6 * 16384 * 127^2 < 2^31).
+// Then  (A V)_ij = 2^(T_i + F_j) * sum_L D_L 2^(-7 L)  up to the dropped levels L > 7 and the
+// truncated tails, i.e. ~2^-40 relative to |A| |V| (FP64 GEMM: ~n 2^-53 worst case); the
+// level sums are combined in fp64.
+//
+// Kernels: k_oz_slices_a (row scales + the six digit planes of A; HBM-bound),
+// k_oz_slices_v (column scales + digits of V), k_oz_gemm (tcgen05 int8, TMA, TMEM int32
+// accumulators for the six levels, stream-K over (row tile, K chunk) with fp64 partials),
+// k_oz_resid (deterministic partial sums -> (A v_j - lambda_j y_j) column sums of squares).
+#include "common.cuh"
+#include <algorithm>
+#include <climits>
+
+namespace ofrr {
+
+static constexpr int OZ_D = 6;            // digits per operand
+static constexpr int OZ_TM = 128;         // rows per tile (UMMA M = 128)
+static constexpr int OZ_KB = 128;         // K per k-block (int8: one 128B swizzle row)
+static constexpr int OZ_THREADS = 192;    // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
+static constexpr int OZ_MAXCHUNK = 128;   // k-blocks per accumulation chunk (16384 terms)
+static constexpr int OZ_BAD = INT_MIN;    // scale marker: the row / column has inf or NaN
+
+template <int BN>
+struct OzCfg {
+  static constexpr int A_BYTES = OZ_TM * OZ_KB;            // one digit plane tile of A, 16 KB
+  static constexpr int V_BYTES = OZ_D * BN * OZ_KB;        // the six digit tiles of V for a k-block
+  static constexpr int A_STAGES_RAW = (200 * 1024 - 2 * V_BYTES) / A_BYTES;
+  static constexpr int A_STAGES = A_STAGES_RAW > 8 ? 8 : A_STAGES_RAW;
+  static constexpr int TMEM_COLS = OZ_D * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = 1024 + 2 * V_BYTES + A_STAGES * A_BYTES + 256;
+};
+
+// idesc for kind::i8: D = S32 (bits 4-5 = 2), A = B = signed 8-bit (bits 7-9, 10-12 = 1),
+// K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+__host__ __device__ inline uint32_t oz_idesc(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_ld16i(uint32_t taddr, int* v) {
+  float f[16];
+  tmem_ld16(taddr, f);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __float_as_int(f[i]);
+}
+
+// scale exponent E with |x| < 2^E for m = max |x| (0 for m == 0, OZ_BAD for inf/NaN)
+__device__ __forceinline__ int oz_scale(double m) {
+  if (!(m <= 1.7976931348623157e308)) return OZ_BAD;
+  if (m == 0.0) return 0;
+  return ilogb(m) + 1;
+}
+// the six signed digits of x on the 42-bit window below 2^E, packed little-endian
+__device__ __forceinline__ void oz_split(double x, int E, uint32_t& lo, uint32_t& hi) {
+  lo = hi = 0;
+  if (E == OZ_BAD || x == 0.0) return;
+  const long long t = (long long)ldexp(fabs(x), 42 - E);   // < 2^42, truncated toward zero
+  const bool neg = x < 0.0;
+#pragma unroll
+  for (int p = 0; p < OZ_D; ++p) {
+    int d = (int)((t >> (7 * (OZ_D - 1 - p))) & 127);
+    if (neg) d = -d;
+    const uint32_t b = (uint32_t)(d & 0xff);
+    if (p < 4) lo |= b << (8 * p); else hi |= b << (8 * (p - 4));
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// A (rows x cols, row-major, 16/8-bit) -> T[rows_pad], planes[6][rows_pad][cols_pad] int8.
+// One CTA per row.  Entries go through their f32 bit pattern (exact for bf16 / f16 /
+// e4m3): value = M 2^(e - 150) with the 24-bit significand M, so the fixed-point word is
+// t = M << (e - 108 - T) (or >> when negative) -- integer ops only.  The row maximum is
+// an integer max over |bits| (positive float patterns order like their values; NaN
+// patterns sort above inf).  Padding rows get zero digits.
+// ---------------------------------------------------------------------------------
+template <int FMT>
+__device__ __forceinline__ float oz_ld_f(const void* A, int64_t i) {
+  if constexpr (FMT == BF16) return __bfloat162float(((const __nv_bfloat16*)A)[i]);
+  else if constexpr (FMT == F16) return __half2float(((const __half*)A)[i]);
+  else { __nv_fp8_e4m3 v; v.__x = ((const __nv_fp8_storage_t*)A)[i]; return float(v); }
+}
+// fixed-point word of x on the 42-bit window below 2^T as (hi 10 bits, lo 32 bits)
+__device__ __forceinline__ void oz_fixed32(uint32_t b, int T, uint32_t& hi, uint32_t& lo) {
+  const int e = (int)(b >> 23);
+  const uint32_t M = (b & 0x7fffffu) | (e ? 0x800000u : 0u);
+  const int sh = (e ? e : 1) - 108 - T;        // t = M 2^sh, sh <= 18
+  const uint32_t s = (uint32_t)max(sh, 0), r = (uint32_t)min(max(-sh, 0), 31);
+  lo = (M << s) >> r;
+  hi = s ? (M >> (32u - s)) : 0u;
+}
+// the six 7-bit digits (most significant first) of four entries, one byte each, signed
+__device__ __forceinline__ void oz_pack4(const float (&x)[4], int T, uint32_t (&w)[OZ_D]) {
+  uint32_t u[OZ_D] = {0, 0, 0, 0, 0, 0}, nm = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t b = __float_as_uint(x[e]);
+    uint32_t hi, lo;
+    oz_fixed32(b & 0x7fffffffu, T, hi, lo);
+    const uint32_t sh8 = 8u * e;
+    u[0] |= ((hi >> 3) & 127u) << sh8;
+    u[1] |= (((hi << 4) | (lo >> 28)) & 127u) << sh8;
+    u[2] |= ((lo >> 21) & 127u) << sh8;
+    u[3] |= ((lo >> 14) & 127u) << sh8;
+    u[4] |= ((lo >> 7) & 127u) << sh8;
+    u[5] |= (lo & 127u) << sh8;
+    nm |= (b >> 31) ? (0xffu << sh8) : 0u;
+  }
+  // bytewise negation of digits <= 127 without inter-byte borrow: (0x80 - d) ^ 0x80
+#pragma unroll
+  for (int p = 0; p < OZ_D; ++p) {
+    const uint32_t ng = (0x80808080u - u[p]) ^ 0x80808080u;
+    w[p] = u[p] ^ ((u[p] ^ ng) & nm);
+  }
+}
+
+// 8 consecutive entries of A as f32 (vector load when aligned and in range)
+template <int FMT>
+__device__ __forceinline__ void oz_ld8(const void* A, int64_t base, int64_t l0, int64_t cols, bool vec, float (&x)[8]) {
+  if (vec && l0 + 8 <= cols) {
+    if constexpr (FMT == FP8) {
+      const uint2 v = *reinterpret_cast<const uint2*>((const uint8_t*)A + base + l0);
+      const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        __nv_fp8_e4m3 q;
+        q.__x = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
+        x[e] = float(q);
+      }
+    } else {
+      const uint4 v = *reinterpret_cast<const uint4*>((const uint16_t*)A + base + l0);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint16_t h = (uint16_t)(w[e >> 1] >> (16 * (e & 1)));
+        if constexpr (FMT == BF16) x[e] = __uint_as_float((uint32_t)h << 16);
+        else x[e] = __half2float(__ushort_as_half(h));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[e] = l0 + e < cols ? oz_ld_f<FMT>(A, base + l0 + e) : 0.0f;
+  }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(256)
+    k_oz_slices_a(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, int* __restrict__ T,
+                  int8_t* __restrict__ planes, int64_t rows_pad, int64_t cols_pad) {
+  const int64_t i = blockIdx.x;
+  __shared__ uint32_t red[8];
+  const size_t plane = (size_t)rows_pad * cols_pad;
+  int8_t* row0 = planes + (size_t)i * cols_pad;
+  if (i >= rows) {
+    for (int64_t l = 4 * (int64_t)threadIdx.x; l < cols_pad; l += 4 * (int64_t)blockDim.x)
+      for (int p = 0; p < OZ_D; ++p) *reinterpret_cast<uint32_t*>(row0 + p * plane + l) = 0u;
+    if (threadIdx.x == 0) T[i] = 0;
+    return;
+  }
+  const int64_t base = i * lda;
+  const int eb = FMT == FP8 ? 1 : 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) + (uintptr_t)(base * eb)) & 15) == 0;
+  uint32_t m = 0;
+  for (int64_t l0 = 8 * (int64_t)threadIdx.x; l0 < cols; l0 += 8 * (int64_t)blockDim.x) {
+    float x[8];
+    oz_ld8<FMT>(A, base, l0, cols, vec, x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t b = __float_as_uint(x[e]) & 0x7fffffffu;
+      m = b > m ? b : m;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint32_t om = __shfl_xor_sync(0xffffffffu, m, o);
+    m = om > m ? om : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = red[0];
+  for (int w = 1; w < 8; ++w) m = red[w] > m ? red[w] : m;
+  const int E = oz_scale((double)__uint_as_float(m));
+  if (threadIdx.x == 0) T[i] = E;
+  // 8 consecutive entries per thread step -> one 64-bit word per plane (cols_pad % 16 == 0)
+  for (int64_t l0 = 8 * (int64_t)threadIdx.x; l0 < cols_pad; l0 += 8 * (int64_t)blockDim.x) {
+    uint32_t w0[OZ_D] = {0, 0, 0, 0, 0, 0}, w1[OZ_D] = {0, 0, 0, 0, 0, 0};
+    if (E != OZ_BAD) {
+      float x[8];
+      oz_ld8<FMT>(A, base, l0, cols, vec, x);
+      const float xa[4] = {x[0], x[1], x[2], x[3]}, xb[4] = {x[4], x[5], x[6], x[7]};
+      oz_pack4(xa, E, w0);
+      oz_pack4(xb, E, w1);
+    }
+#pragma unroll
+    for (int p = 0; p < OZ_D; ++p) *reinterpret_cast<uint2*>(row0 + p * plane + l0) = make_uint2(w0[p], w1[p]);
+  }
+}
+
+// V (cols x n fp64, column j contiguous, ld ldv) -> F[npad], digits[6][npad][cols_pad]
+__global__ void __launch_bounds__(256)
+    k_oz_slices_v(const double* __restrict__ V, int64_t ldv, int64_t cols, int n, int* __restrict__ F,
+                  int8_t* __restrict__ dig, int npad, int64_t cols_pad) {
+  const int j = blockIdx.x;
+  __shared__ double red[8];
+  __shared__ int sE;
+  const size_t plane = (size_t)npad * cols_pad;
+  int8_t* row0 = dig + (size_t)j * cols_pad;
+  if (j >= n) {
+    for (int64_t l = threadIdx.x; l < cols_pad; l += blockDim.x)
+      for (int p = 0; p < OZ_D; ++p) row0[p * plane + l] = 0;
+    if (threadIdx.x == 0) F[j] = 0;
+    return;
+  }
+  const double* v = V + (size_t)j * ldv;
+  double m = 0.0;
+  for (int64_t l = threadIdx.x; l < cols; l += blockDim.x) {
+    const double a = fabs(v[l]);
+    m = (a != a || a > m) ? a : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (om != om || om > m) ? om : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mm = (red[w] != red[w] || red[w] > mm) ? red[w] : mm;
+    sE = oz_scale(mm);
+    F[j] = sE;
+  }
+  __syncthreads();
+  const int E = sE;
+  for (int64_t l0 = 4 * (int64_t)threadIdx.x; l0 < cols_pad; l0 += 4 * (int64_t)blockDim.x) {
+    uint32_t w[OZ_D] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t l = l0 + e;
+      if (l < cols) {
+        uint32_t lo, hi;
+        oz_split(v[l], E, lo, hi);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) w[p] |= ((lo >> (8 * p)) & 0xffu) << (8 * e);
+        w[4] |= (hi & 0xffu) << (8 * e);
+        w[5] |= ((hi >> 8) & 0xffu) << (8 * e);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < OZ_D; ++p) *reinterpret_cast<uint32_t*>(row0 + p * plane + l0) = w[p];
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// The int8 tensor-core product.  Work unit = one k-block of a virtual tile vt = (row tile,
+// K chunk); stream-K splits the units evenly over the grid.  Per unit the V digit tiles
+// (6 x BN x 128 B) are staged once (double-buffered) and the six A digit-plane tiles
+// stream through a ring; digit p of A meets digits q = 1..7-p of V in one or two MMAs that
+// write the contiguous TMEM levels p+q (level L at column (L - 2) BN, int32).
+// ---------------------------------------------------------------------------------
+template <int BN>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
+              double* __restrict__ ws, int kbc, int nchunks, long long total_units, int max_slots,
+              int rows_pad, int npad, int col0) {
+  using C = OzCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* vbuf = smem;                               // [2][V_BYTES]
+  uint8_t* abuf = smem + 2 * C::V_BYTES;              // [A_STAGES][A_BYTES]
+  uint64_t* afull = reinterpret_cast<uint64_t*>(abuf + C::A_STAGES * C::A_BYTES);
+  uint64_t* aempty = afull + C::A_STAGES;
+  uint64_t* vfull = aempty + C::A_STAGES;
+  uint64_t* vempty = vfull + 2;
+  uint64_t* tfull = vempty + 2;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long G = gridDim.x;
+  const long long u0 = (long long)blockIdx.x * total_units / G;
+  const long long u1 = ((long long)blockIdx.x + 1) * total_units / G;
+  const int vt_first = (int)(u0 / kbc);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::A_STAGES; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_barrier_init();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmV);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      const uint64_t pol_a = policy_evict_first(), pol_v = policy_evict_last();
+      int as = 0, vs = 0;
+      uint32_t aph = 0, vph = 0;
+      for (long long u = u0; u < u1; ++u) {
+        const int vt = (int)(u / kbc);
+        const int kb = (vt % nchunks) * kbc + (int)(u % kbc);
+        const int mt = vt / nchunks;
+        mbar_wait(&vempty[vs], vph ^ 1);
+        mbar_expect_tx(&vfull[vs], C::V_BYTES);
+        for (int q = 0; q < OZ_D; ++q)
+          tma_load_2d(vbuf + vs * C::V_BYTES + q * BN * OZ_KB, &tmV, kb * OZ_KB, q * npad + col0, &vfull[vs], pol_v);
+        if (++vs == 2) { vs = 0; vph ^= 1; }
+        for (int p = 0; p < OZ_D; ++p) {
+          mbar_wait(&aempty[as], aph ^ 1);
+          mbar_expect_tx(&afull[as], C::A_BYTES);
+          tma_load_2d(abuf + as * C::A_BYTES, &tmA, kb * OZ_KB, p * rows_pad + mt * OZ_TM, &afull[as], pol_a);
+          if (++as == C::A_STAGES) { as = 0; aph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      int as = 0, vs = 0;
+      uint32_t aph = 0, vph = 0, acc_phase = 0;
+      long long u = u0;
+      while (u < u1) {
+        const int vt = (int)(u / kbc);
+        const long long seg_end = std::min<long long>(u1, (long long)(vt + 1) * kbc);
+        const long long seg_start = u;
+        mbar_wait(tempty, acc_phase ^ 1);
+        tc_fence_after();
+        for (; u < seg_end; ++u) {
+          mbar_wait(&vfull[vs], vph);
+          tc_fence_after();
+          const uint64_t dv = umma_desc_sw128(smem_u32(vbuf + vs * C::V_BYTES));
+          for (int p = 0; p < OZ_D; ++p) {
+            mbar_wait(&afull[as], aph);
+            tc_fence_after();
+            const uint64_t da = umma_desc_sw128(smem_u32(abuf + as * C::A_BYTES));
+            const int nq = OZ_D - p;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              // the segment's first unit, digit 0, k 0 initialises every level
+              const uint32_t acc = (u > seg_start || p > 0 || k > 0) ? 1u : 0u;
+              for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
+                const int ng = std::min(256 / BN, nq - q0);
+                mma_i8(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
+                       dv + (uint64_t)((q0 * BN * OZ_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN), acc);
+              }
+            }
+            tc_commit(&aempty[as]);
+            if (++as == C::A_STAGES) { as = 0; aph ^= 1; }
+          }
+          tc_commit(&vempty[vs]);
+          if (++vs == 2) { vs = 0; vph ^= 1; }
+        }
+        tc_commit(tfull);
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5: TMEM int32 levels -> fp64 partial tile (column-major) =====
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    uint32_t acc_phase = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int vt = (int)(u / kbc);
+      u = std::min<long long>(u1, (long long)(vt + 1) * kbc);
+      mbar_wait(tfull, acc_phase);
+      tc_fence_after();
+      double* dst = ws + ((size_t)blockIdx.x * max_slots + (vt - vt_first)) * (size_t)(OZ_TM * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        double s[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s[i] = 0.0;
+#pragma unroll 1
+        for (int lv = OZ_D - 1; lv >= 0; --lv) {     // lowest weight first
+          int d[16];
+          tmem_ld16i(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(lv * BN + c0), d);
+          const double w = ldexp(1.0, -7 * (lv + 2));
+#pragma unroll
+          for (int i = 0; i < 16; ++i) s[i] = fma((double)d[i], w, s[i]);   // exact product
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dst[(size_t)(c0 + i) * OZ_TM + row] = s[i];
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+      acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+__device__ __forceinline__ long long oz_seg_begin(long long c, long long T, long long G) { return c * T / G; }
+
+// Sum the partials of row tile t over its K chunks and stream-K segments (fixed order),
+// scale to (A V)_ij and form the residual column sums of squares of this tile:
+//   part[t * ldp + j0 + j] = sum_i ((A V)_ij - lambda_j Y_ij)^2
+// (with W: write W = A V (fp64) instead).  One thread per row, 16 columns at a time.
+__global__ void __launch_bounds__(OZ_TM)
+    k_oz_resid(const double* __restrict__ ws, int BN, int kbc, int nchunks, long long total_units, int G,
+               int max_slots, int64_t rows, int ncols, int j0, const int* __restrict__ T, const int* __restrict__ F,
+               const double* __restrict__ vals, const int* __restrict__ r_dev, const double* __restrict__ Y,
+               int64_t ldy, double* __restrict__ part, int ldp, double* __restrict__ W, int64_t ldw) {
+  __shared__ double red[4][16];
+  const int t = blockIdx.x;
+  const int row = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t grow = (int64_t)t * OZ_TM + row;
+  const bool valid = grow < rows;
+  const int Ti = valid ? T[grow] : 0;
+  const int nvalid = r_dev ? min(j0 + ncols, *r_dev) : j0 + ncols;
+  // segments covering the tile's units, per chunk, ascending
+  long long c_lo[16], c_hi[16];
+  for (int ch = 0; ch < nchunks && ch < 16; ++ch) {
+    const long long vt = (long long)t * nchunks + ch;
+    const long long x0 = vt * kbc, x1 = x0 + kbc - 1;
+    long long lo = x0 * G / total_units, hi = x1 * G / total_units;
+    while (lo + 1 < G && oz_seg_begin(lo + 1, total_units, G) <= x0) ++lo;
+    while (lo > 0 && oz_seg_begin(lo, total_units, G) > x0) --lo;
+    while (hi + 1 < G && oz_seg_begin(hi + 1, total_units, G) <= x1) ++hi;
+    while (hi > 0 && oz_seg_begin(hi, total_units, G) > x1) --hi;
+    c_lo[ch] = lo;
+    c_hi[ch] = hi;
+  }
+  for (int jb = 0; jb < ncols; jb += 16) {
+    double s[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s[q] = 0.0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const long long vt = (long long)t * nchunks + ch;
+      for (long long c = c_lo[ch]; c <= c_hi[ch]; ++c) {
+        const int slot = (int)(vt - oz_seg_begin(c, total_units, G) / kbc);
+        const double* src = ws + ((size_t)c * max_slots + slot) * (size_t)(OZ_TM * BN) + row;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (jb + q < ncols) s[q] += src[(size_t)(jb + q) * OZ_TM];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int j = jb + q, gj = j0 + j;
+      double r2 = 0.0;
+      if (valid && j < ncols && gj < nvalid) {
+        const int Fj = F[j];
+        const double av = (Ti == OZ_BAD || Fj == OZ_BAD) ? __longlong_as_double(0x7ff8000000000000ll)
+                                                          : ldexp(s[q], Ti + Fj);
+        if (W) {
+          W[(int64_t)gj * ldw + grow] = av;
+        } else {
+          const double d = av - vals[gj] * Y[(int64_t)gj * ldy + grow];
+          r2 = d * d;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      if (lane == 0) red[warp][q] = r2;
+    }
+    __syncthreads();
+    if (!W && threadIdx.x < 16 && jb + threadIdx.x < ncols)
+      part[(int64_t)t * ldp + j0 + jb + threadIdx.x] =
+          ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled_oz)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int oz_make_tmap_u8(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                    uint32_t box_inner, uint32_t box_outer);   // gemm_tc.cu
+
+struct OzPlan {
+  int bn, npass, m_tiles, kblocks, nchunks, kbc, grid, max_slots;
+  int64_t rows_pad, cols_pad;
+  int npad;
+  long long total;
+  size_t off_T, off_F, off_planes, off_dig, off_ws, off_part, bytes;
+};
+
+static OzPlan oz_plan(int64_t rows, int64_t cols, int r) {
+  OzPlan p;
+  p.bn = r <= 32 ? 32 : 64;
+  p.npass = (r + p.bn - 1) / p.bn;
+  p.npad = p.npass * p.bn;
+  p.rows_pad = (rows + OZ_TM - 1) / OZ_TM * OZ_TM;
+  p.cols_pad = (cols + 15) / 16 * 16;
+  p.m_tiles = (int)(p.rows_pad / OZ_TM);
+  p.kblocks = (int)((cols + OZ_KB - 1) / OZ_KB);
+  p.nchunks = (p.kblocks + OZ_MAXCHUNK - 1) / OZ_MAXCHUNK;
+  p.kbc = (p.kblocks + p.nchunks - 1) / p.nchunks;
+  p.total = (long long)p.m_tiles * p.nchunks * p.kbc;   // work units (k-blocks)
+  int sms = ofrr_device_sm_count(-1);
+  if (sms <= 0) sms = 148;
+  p.grid = (int)std::max<long long>(1, std::min<long long>(sms, p.total));
+  const long long per = (p.total + p.grid - 1) / p.grid;
+  p.max_slots = (int)((per + p.kbc - 1) / p.kbc) + 1;
+  size_t b = 0;
+  auto take = [&](size_t n) { size_t o = b; b += (n + 1023) & ~size_t(1023); return o; };
+  p.off_T = take((size_t)p.rows_pad * 4);
+  p.off_F = take((size_t)p.npad * 4);
+  p.off_planes = take((size_t)OZ_D * p.rows_pad * p.cols_pad);
+  p.off_dig = take((size_t)OZ_D * p.npad * p.cols_pad);
+  p.off_ws = take((size_t)p.grid * p.max_slots * OZ_TM * p.bn * sizeof(double));
+  p.off_part = take((size_t)p.m_tiles * r * sizeof(double));
+  p.bytes = b;
+  return p;
+}
+
+size_t oz_ws(int64_t rows, int64_t cols, int r) { return oz_plan(rows, cols, std::max(r, 1)).bytes; }
+int oz_nblocks(int64_t rows) { return (int)((rows + OZ_TM - 1) / OZ_TM); }
+
+template <int BN>
+static int oz_launch(const CUtensorMap& tA, const CUtensorMap& tV, const OzPlan& p, double* ws, int col0,
+                     cudaStream_t st) {
+  using C = OzCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_oz_gemm<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+    attr = true;
+  }
+  k_oz_gemm<BN><<<p.grid, OZ_THREADS, C::SMEM_BYTES, st>>>(tA, tV, ws, p.kbc, p.nchunks, p.total, p.max_slots,
+                                                           (int)p.rows_pad, p.npad, col0);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+// part[m_tile * r + j] = sum over the tile's rows of ((A V)_ij - vals_j Y_ij)^2, or, with W,
+// W = A V (fp64).  A: rows x cols row-major in a_fmt (F16 / BF16 / FP8); V: cols x r fp64.
+int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const double* V, int64_t ldv,
+               int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, double* W, int64_t ldw,
+               double** part_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (a_fmt != BF16 && a_fmt != F16 && a_fmt != FP8) {
+    ofrr_set_error("ozaki product: A format %d not supported", a_fmt);
+    return OFRR_ERR_UNSUPPORTED;
+  }
+  const OzPlan p = oz_plan(rows, cols, r);
+  if (p.nchunks > 16) { ofrr_set_error("ozaki product: cols=%lld beyond 16 chunks", (long long)cols); return OFRR_ERR_UNSUPPORTED; }
+  if (!ws || ws_bytes < p.bytes) { ofrr_set_error("ozaki product: workspace too small (%zu < %zu)", ws_bytes, p.bytes); return OFRR_ERR_INVALID; }
+  uint8_t* base = (uint8_t*)ws;
+  int* T = (int*)(base + p.off_T);
+  int* F = (int*)(base + p.off_F);
+  int8_t* planes = (int8_t*)(base + p.off_planes);
+  int8_t* dig = (int8_t*)(base + p.off_dig);
+  double* pws = (double*)(base + p.off_ws);
+  double* part = (double*)(base + p.off_part);
+  if (a_fmt == BF16)
+    k_oz_slices_a<BF16><<<(unsigned)p.rows_pad, 256, 0, st>>>(A, rows, cols, lda, T, planes, p.rows_pad, p.cols_pad);
+  else if (a_fmt == F16)
+    k_oz_slices_a<F16><<<(unsigned)p.rows_pad, 256, 0, st>>>(A, rows, cols, lda, T, planes, p.rows_pad, p.cols_pad);
+  else
+    k_oz_slices_a<FP8><<<(unsigned)p.rows_pad, 256, 0, st>>>(A, rows, cols, lda, T, planes, p.rows_pad, p.cols_pad);
+  OFRR_CHECK_LAUNCH();
+  k_oz_slices_v<<<(unsigned)p.npad, 256, 0, st>>>(V, ldv, cols, r, F, dig, p.npad, p.cols_pad);
+  OFRR_CHECK_LAUNCH();
+  CUtensorMap tA, tV;
+  int rc = oz_make_tmap_u8(&tA, planes, (uint64_t)cols, (uint64_t)OZ_D * p.rows_pad, (uint64_t)p.cols_pad, OZ_KB, OZ_TM);
+  if (rc) return rc;
+  rc = oz_make_tmap_u8(&tV, dig, (uint64_t)cols, (uint64_t)OZ_D * p.npad, (uint64_t)p.cols_pad, OZ_KB, (uint32_t)p.bn);
+  if (rc) return rc;
+  for (int ps = 0; ps < p.npass; ++ps) {
+    const int j0 = ps * p.bn;
+    rc = p.bn == 32 ? oz_launch<32>(tA, tV, p, pws, j0, st) : oz_launch<64>(tA, tV, p, pws, j0, st);
+    if (rc) return rc;
+    k_oz_resid<<<p.m_tiles, OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
+                                           std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
+                                           ldw);
+    OFRR_CHECK_LAUNCH();
+  }
+  if (part_out) *part_out = part;
+  return OFRR_OK;
+}
+
+}  // namespace ofrr

@@ -536,11 +536,46 @@ size_t residual_ws(int64_t rows, int r) {
   return (size_t)((rows + SBM - 1) / SBM) * (size_t)r * sizeof(double);
 }
 
+size_t oz_ws(int64_t rows, int64_t cols, int r);
+int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const double* V, int64_t ldv,
+               int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, double* W, int64_t ldw,
+               double** part_out, void* ws, size_t ws_bytes, cudaStream_t st);
+int oz_nblocks(int64_t rows);
+
+// The FP64-accurate residual product runs on the int8 tensor cores (oz.cu) for 16/8-bit
+// operators; OFRR_RESID_DMMA=1 forces the FP64 DMMA kernel (and OFRR_RESID_SIMT=1 the
+// CUDA-core one) for comparison.
+static bool use_ozaki(int a_fmt, int transpose) {
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("OFRR_RESID_DMMA");
+    const char* f = getenv("OFRR_RESID_SIMT");
+    force = ((e && atoi(e) == 1) || (f && atoi(f) == 1)) ? 1 : 0;
+  }
+  return !force && !transpose && (a_fmt == BF16 || a_fmt == F16 || a_fmt == FP8);
+}
+
+size_t residual_ws2(int64_t rows, int64_t cols, int r, int a_fmt, int transpose) {
+  const int64_t m = transpose ? cols : rows;
+  if (use_ozaki(a_fmt, transpose)) return oz_ws(rows, cols, r);
+  return residual_ws(m, r);
+}
+
 int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose,
                   const double* Xv, int64_t ldx, const double* Yv, int64_t ldy, const double* vals,
                   const int* r_dev, int r_max, double* res, int accumulate_max, void* ws, size_t ws_bytes,
                   cudaStream_t st) {
   const int64_t m = transpose ? cols : rows, K = transpose ? rows : cols;
+  if (use_ozaki(a_fmt, transpose)) {
+    double* part = nullptr;
+    const int rc = oz_product(A, rows, cols, lda, a_fmt, Xv, ldx, r_max, vals, r_dev, Yv, ldy, nullptr, 0, &part,
+                              ws, ws_bytes, st);
+    if (rc) return rc;
+    k_residual_reduce<<<(r_max + 127) / 128, 128, 0, st>>>(part, oz_nblocks(m), r_max, vals, r_dev, res,
+                                                           accumulate_max);
+    OFRR_CHECK_LAUNCH();
+    return OFRR_OK;
+  }
   const size_t need = residual_ws(m, r_max);
   if (!ws || ws_bytes < need) { ofrr_set_error("residual: workspace too small (%zu < %zu)", ws_bytes, need); return OFRR_ERR_INVALID; }
   double* part = (double*)ws;

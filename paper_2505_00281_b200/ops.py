@@ -350,7 +350,7 @@ def residual_estimate(U: DevBlock, W: DevBlock, Y: torch.Tensor, ldy: int, vals:
 def residual_eig(A: DevOperator, V: DevBlock, vals: torch.Tensor, r_dev: Optional[torch.Tensor], r_max: int):
     L = _lib.load()
     res = torch.zeros(max(r_max, 1), dtype=torch.float64, device=A.device)
-    ws = _ws(L.ofrr_residual_workspace(A.rows, r_max), A.device)
+    ws = _ws(L.ofrr_residual_workspace2(A.rows, A.cols, r_max, int(A.fmt), 0), A.device)
     _lib.check(L.ofrr_residual_eig(A.ptr, A.rows, A.lda, int(A.fmt), V.ptr, V.ld, vals.data_ptr(), _p(r_dev), r_max,
                                    res.data_ptr(), ws.data_ptr(), ws.numel(), _stream()), "residual_eig")
     _count(2)
@@ -361,7 +361,7 @@ def residual_pair(A: DevOperator, transpose: bool, Xv: DevBlock, Yv: DevBlock, v
                   r_dev: Optional[torch.Tensor], r_max: int, res: torch.Tensor, accumulate_max: bool):
     L = _lib.load()
     m = A.cols if transpose else A.rows
-    ws = _ws(L.ofrr_residual_workspace(m, r_max), A.device)
+    ws = _ws(L.ofrr_residual_workspace2(A.rows, A.cols, r_max, int(A.fmt), int(transpose)), A.device)
     _lib.check(L.ofrr_residual_pair(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), int(transpose), Xv.ptr, Xv.ld, Yv.ptr,
                                     Yv.ld, vals.data_ptr(), _p(r_dev), r_max, res.data_ptr(), int(accumulate_max),
                                     ws.data_ptr(), ws.numel(), _stream()), "residual_pair")

@@ -248,6 +248,54 @@ def test_ritz_and_residual(ofrr_gpu, oracle):
     np.testing.assert_allclose(res, ref, rtol=1e-10)
 
 
+@pytest.mark.parametrize("fmt,rows,cols,r,rv", [(BF16, 300, 20000, 64, 64), (BF16, 1000, 1000, 100, 90),
+                                                (F16, 257, 3001, 7, 7), (FP8, 640, 5000, 33, 20),
+                                                (BF16, 129, 16384, 32, 32)])
+def test_residual_ozaki_vs_fp64(ofrr_gpu, oracle, fmt, rows, cols, r, rv):
+    """K7 on the int8 tensor cores (Ozaki digit planes) vs numpy fp64: ||A x_j - s_j y_j|| /
+    s_j for rectangular A (several K chunks, padded tiles, two column passes, r_dev < r)."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(rows + cols + r)
+    a = o.round_to(rng.standard_normal((rows, cols)) * np.exp(rng.uniform(-3, 3, (rows, 1))), fmt)
+    a = np.where(np.abs(a) > 400, 0.0, a)
+    x = rng.standard_normal((cols, r))
+    y = rng.standard_normal((rows, r))
+    s = np.abs(rng.standard_normal(r)) + 0.1
+    A = _op(p, a, fmt)
+    X = _blk(p, x, F64)
+    Yb = _blk(p, y, F64)
+    res = torch.zeros(r, dtype=torch.float64, device="cuda")
+    r_dev = torch.tensor([rv], dtype=torch.int32, device="cuda")
+    ops.residual_pair(A, False, X, Yb, torch.tensor(s, device="cuda"), r_dev, r, res, accumulate_max=0)
+    ref = np.linalg.norm(a @ x[:, :rv] - y[:, :rv] * s[None, :rv], axis=0) / s[:rv]
+    got = res.cpu().numpy()
+    np.testing.assert_allclose(got[:rv], ref, rtol=1e-11)
+    assert not got[rv:].any()
+
+
+def test_residual_ozaki_tiny_residuals(ofrr_gpu, oracle):
+    """FP64-class accuracy where it matters: exact (fp64 eigh) eigenpairs of a bf16 matrix
+    have residuals ~1e-15; the int8-digit product must not add more than ~1e-12."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(5)
+    n = 1500
+    a = rng.standard_normal((n, n))
+    a = o.round_to((a + a.T) / 2, BF16)
+    w, v = np.linalg.eigh(a)
+    sel = np.argsort(-np.abs(w))[:48]
+    lam, vec = w[sel], v[:, sel]
+    A = _op(p, a, BF16)
+    V = _blk(p, vec, F64)
+    res = ops.residual_eig(A, V, torch.tensor(lam, device="cuda"), None, 48).cpu().numpy()
+    ref = np.linalg.norm(a @ vec - vec * lam[None, :], axis=0) / np.abs(lam)
+    assert np.all(ref < 1e-13)
+    assert np.all(np.abs(res - ref) < 2e-12), np.max(np.abs(res - ref))
+
+
 @pytest.mark.parametrize("n", [1024, 1000])
 def test_generator_bitwise(ofrr_gpu, oracle, n):
     """K8 evaluates the synthetic matrix bit for bit like the host formula."""
