@@ -331,7 +331,8 @@ int ofrr_host_jacobi_eig(const double* a, int64_t n, int max_sweeps, double tol,
 
 namespace ofrr { int k5_profile(long long* out); }
 extern "C" int ofrr_debug_k5_profile(long long* out8) { return ofrr::k5_profile(out8); }
-namespace ofrr { int hess_profile(unsigned long long* out); }
+namespace ofrr { int hess_profile(unsigned long long* out); int pc_profile(unsigned long long* out); }
+extern "C" int ofrr_debug_pencil_profile(unsigned long long* out16) { return ofrr::pc_profile(out16); }
 extern "C" int ofrr_debug_hess_profile(unsigned long long* out8) { return ofrr::hess_profile(out8); }
 
 namespace ofrr { void prof_enable(int on); int prof_read(float* ms, int max); }

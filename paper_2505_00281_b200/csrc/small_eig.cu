@@ -541,7 +541,10 @@ __global__ void __launch_bounds__(ET, 1)
     k_small_eig(int mode, const double* __restrict__ A, const double* __restrict__ Mm, int k, double raw_tol,
                 int raw_sweeps, double* __restrict__ values, double* __restrict__ vectors, int* __restrict__ n_out,
                 int* __restrict__ status, double* __restrict__ off_out, int* __restrict__ sweeps_out, EigBufs gb,
-                int nsm, double* __restrict__ wk, int use_tridiag) {
+                int nsm, double* __restrict__ wk, int use_tridiag, const int* __restrict__ gate) {
+  // gate: the fast pipeline (pencil.cu) ran first; this general kernel only runs when it
+  // raised the gate (certificate not met / breakdown)
+  if (gate && *gate == 0) return;
   extern __shared__ double dsm[];
   __shared__ EigScratch sc;
   __shared__ double tau[MAXK];
@@ -697,7 +700,13 @@ __global__ void __launch_bounds__(ET, 1)
   if (threadIdx.x == 0) { *status = 0; *n_out = kp; }
 }
 
-size_t small_eig_ws(int k) { return (size_t)4 * k * pad_k(k) * sizeof(double) + (size_t)5 * k * k * sizeof(double) + 2048; }
+int pencil_max_k();
+size_t pencil_ws(int k);
+int pencil_eig(const double* B, const double* M, int k, double* values, double* vectors, int* n_out, int* status,
+               void* ws, int* gate, cudaStream_t st);
+
+static size_t legacy_ws(int k) { return (size_t)4 * k * pad_k(k) * sizeof(double) + (size_t)5 * k * k * sizeof(double) + 2048; }
+size_t small_eig_ws(int k) { return legacy_ws(k) + pencil_ws(k) + 1024; }
 
 int small_eig(int mode, const double* A, const double* M, int k, double raw_tol, int raw_sweeps, double* values,
               double* vectors, int* n_out, int* status, double* off_out, int* sweeps_out, void* ws, size_t ws_bytes,
@@ -718,13 +727,22 @@ int small_eig(int mode, const double* A, const double* M, int k, double raw_tol,
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_small_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
-  static int tridiag = -1;
+  static int tridiag = -1, legacy = -1;
   if (tridiag < 0) {
     const char* e = getenv("OFRR_EIG_JACOBI");   // 1: force the reference-order Jacobi for eig(T)
     tridiag = (e && atoi(e) == 1) ? 0 : 1;
+    const char* l = getenv("OFRR_K5_LEGACY");    // 1: single-kernel path only
+    legacy = (l && atoi(l) == 1) ? 1 : 0;
+  }
+  int* gate = nullptr;
+  if (mode == 2 && k >= 1 && k <= pencil_max_k() && !legacy && tridiag) {
+    uint8_t* pw = (uint8_t*)ws + ((legacy_ws(k) + 255) & ~size_t(255));
+    gate = (int*)(pw + ((pencil_ws(k) + 255) & ~size_t(255)));
+    const int rc = pencil_eig(A, M, k, values, vectors, n_out, status, pw, gate, st);
+    if (rc) return rc;
   }
   k_small_eig<<<1, ET, shm, st>>>(mode, A, M, k, raw_tol, raw_sweeps, values, vectors, n_out, status, off_out,
-                                  sweeps_out, b, nsm, wk, tridiag);
+                                  sweeps_out, b, nsm, wk, tridiag, gate);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
