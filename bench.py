@@ -216,12 +216,15 @@ def run_ours(args, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
+    from paper_2505_00281_b200 import _lib
+    L = _lib.load()
+    # warm-up with the kernel timers on, so the CUDA graph of the outer iteration (captured
+    # during the warm-up) carries the K1 timing events the timed region harvests
+    L.ofrr_prof_gemm_enable(1)
     for _ in range(args.warmup):
         solve()
     barrier()
     # ---- timed region: K solves, CUDA events on the launching stream -------------
-    from paper_2505_00281_b200 import _lib
-    L = _lib.load()
     ops.GEMM_LOG = []
     ops.LAUNCHES[0] = 0
     stats = p.RunStats()
@@ -258,25 +261,28 @@ def run_ours(args, cfg):
     gemm_share = float(np.sum(durs)) / ms_total if ms_total > 0 else None
 
     # ---- e2e: public API with HOST buffers (A from pinned host memory, results back) --
+    # Every step copies A host -> device into the caller's operator buffer (DenseMatrix.on_device,
+    # the documented device path; a fixed buffer keeps the captured CUDA graph valid) and
+    # reads the values, FP64 Ritz vectors and residuals back to the host.
     e2e = None
     if world == 1:
         a_host = A.device_operator(fmt).t[:, :n].to("cpu").pin_memory()
-        del_ok = True
+        op = ops.new_operator(n, n, fmt, dev)
         times = []
         h2d = d2h = 0
         for i in range(max(1, min(3, args.steps)) + 1):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            Ah = p.DenseMatrix(a_host, fmt)               # host buffer in the storage format
+            op.t[:, :n].copy_(a_host, non_blocking=True)       # H2D of this step's A
+            Ah = p.DenseMatrix.on_device(op)
             rsh = p.subspace_iter_eig(Ah, icfg)
             vals = np.asarray(rsh.values)                 # host result
             vecs = rsh.vectors.data                       # D2H of the FP64 Ritz vectors
             torch.cuda.synchronize()
             if i > 0:
                 times.append(time.perf_counter() - t0)
-            h2d = a_host.numel() * a_host.element_size() + n * k * 8
+            h2d = a_host.numel() * a_host.element_size()
             d2h = vals.nbytes + vecs.nbytes + rsh.residuals.nbytes
-            Ah.release_device()
             del Ah, rsh
         e2e = {"value": float(np.median(times)), "unit": "s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h)}

@@ -97,9 +97,15 @@ int ofrr_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, i
 
 /* Kernel-only timing of the K1 tensor-core kernel (measurement support): while enabled,
  * every k_gemm_av_tc launch is bracketed by CUDA events on its stream; read returns the
- * durations (ms) of the launches since enable. */
+ * durations (ms) of the launches since enable.  Launches captured into a CUDA graph:
+ * claim (right after the capture) turns the captured event pairs into a group whose
+ * durations collect_group appends after each replay; collect harvests eager launches. */
 void ofrr_prof_gemm_enable(int on);
 int ofrr_prof_gemm_read(float* ms, int max);
+int ofrr_prof_gemm_active(void);
+int ofrr_prof_gemm_collect(void);
+int ofrr_prof_gemm_claim(void);
+int ofrr_prof_gemm_collect_group(int group);
 
 /* K2: X[:,j] <- round_s(round_c(X[:,j] / colmax[j])) for colmax[j] != 0, in place.
  * Replaces ofrr/precision.py:159-169 scale_columns_inf. */

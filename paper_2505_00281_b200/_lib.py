@@ -46,6 +46,10 @@ _SIGS = {
                                 c_int, c_vp, c_int, c_vp, c_sz, c_vp], c_int),
     "ofrr_prof_gemm_enable": ([c_int], None),
     "ofrr_prof_gemm_read": ([c_vp, c_int], c_int),
+    "ofrr_prof_gemm_active": ([], c_int),
+    "ofrr_prof_gemm_collect": ([], c_int),
+    "ofrr_prof_gemm_claim": ([], c_int),
+    "ofrr_prof_gemm_collect_group": ([c_int], c_int),
     "ofrr_scale_columns": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_vp, c_vp], c_int),
     "ofrr_hessenberg_workspace": ([c_i64, c_int, c_int], c_sz),
     "ofrr_hessenberg": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp,

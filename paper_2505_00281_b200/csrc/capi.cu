@@ -335,6 +335,13 @@ namespace ofrr { int hess_profile(unsigned long long* out); int pc_profile(unsig
 extern "C" int ofrr_debug_pencil_profile(unsigned long long* out16) { return ofrr::pc_profile(out16); }
 extern "C" int ofrr_debug_hess_profile(unsigned long long* out8) { return ofrr::hess_profile(out8); }
 
-namespace ofrr { void prof_enable(int on); int prof_read(float* ms, int max); }
+namespace ofrr {
+void prof_enable(int on); int prof_read(float* ms, int max); int prof_active(); int prof_collect();
+int prof_claim(); int prof_collect_group(int g);
+}
 extern "C" void ofrr_prof_gemm_enable(int on) { ofrr::prof_enable(on); }
 extern "C" int ofrr_prof_gemm_read(float* ms, int max) { return ofrr::prof_read(ms, max); }
+extern "C" int ofrr_prof_gemm_active(void) { return ofrr::prof_active(); }
+extern "C" int ofrr_prof_gemm_collect(void) { return ofrr::prof_collect(); }
+extern "C" int ofrr_prof_gemm_claim(void) { return ofrr::prof_claim(); }
+extern "C" int ofrr_prof_gemm_collect_group(int group) { return ofrr::prof_collect_group(group); }

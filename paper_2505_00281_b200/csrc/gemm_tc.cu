@@ -295,39 +295,97 @@ int oz_make_tmap_u8(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t 
 }
 
 // N of the UMMA = k rounded up to a multiple of 32 (M=128 needs N % 16 == 0, N <= 256)
-// ---- kernel-only timing of k_gemm_av_tc (bench.py roofline): CUDA events recorded on the
-// launching stream immediately around the launch, read back after the timed region ----
+// ---- kernel-only timing of k_gemm_av_tc (bench.py roofline): a pair of CUDA events
+// recorded on the launching stream immediately around each launch.  Eager launches take a
+// pair from a free pool and queue it as pending; launches captured into a CUDA graph
+// (pairs still pending when the caller claims them) become a group owned by the graph,
+// re-recorded by every replay and harvested after it.  Durations accumulate in launch
+// order and are read back after the timed region. ----
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_ev;
-static size_t g_prof_n = 0;
+static std::vector<int> g_prof_free, g_prof_pending;
+static std::vector<std::vector<int>> g_prof_groups;
+static std::vector<float> g_prof_acc;
 
 static cudaEvent_t* prof_slot() {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (!g_prof_on) return nullptr;
-  if (g_prof_n == g_prof_ev.size()) {
+  int idx;
+  if (!g_prof_free.empty()) {
+    idx = g_prof_free.back();
+    g_prof_free.pop_back();
+  } else {
     cudaEvent_t a, b;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return nullptr;
     g_prof_ev.push_back({a, b});
+    idx = (int)g_prof_ev.size() - 1;
   }
-  return &g_prof_ev[g_prof_n++].first;
+  g_prof_pending.push_back(idx);
+  return &g_prof_ev[idx].first;
+}
+
+static int prof_harvest(const std::vector<int>& idx) {
+  for (int i : idx) {
+    float t = 0.f;
+    if (cudaEventSynchronize(g_prof_ev[i].second) != cudaSuccess ||
+        cudaEventElapsedTime(&t, g_prof_ev[i].first, g_prof_ev[i].second) != cudaSuccess) {
+      (void)cudaGetLastError();   // timing is best effort: never poison later launch checks
+      return -1;
+    }
+    g_prof_acc.push_back(t);
+  }
+  return 0;
+}
+
+// record a timing event; inside a stream capture as an external event node, so that every
+// replay of the graph records it
+static void prof_record(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ev, st);
 }
 
 void prof_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof_on = on != 0;
-  g_prof_n = 0;
+  g_prof_acc.clear();
+  for (int i : g_prof_pending) g_prof_free.push_back(i);
+  g_prof_pending.clear();
+}
+int prof_active() { return g_prof_on ? 1 : 0; }
+
+// pending (eager) pairs -> accumulated durations; the pairs return to the pool
+int prof_collect() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int rc = prof_harvest(g_prof_pending);
+  for (int i : g_prof_pending) g_prof_free.push_back(i);
+  g_prof_pending.clear();
+  return rc;
+}
+// the pending pairs were captured into a graph: make them a group, return its id
+int prof_claim() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (g_prof_pending.empty()) return -1;
+  g_prof_groups.push_back(g_prof_pending);
+  g_prof_pending.clear();
+  return (int)g_prof_groups.size() - 1;
+}
+// after a replay of the graph owning group g (and a synchronisation)
+int prof_collect_group(int g) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (g < 0 || g >= (int)g_prof_groups.size()) return 0;
+  if (!g_prof_on) return 0;
+  return prof_harvest(g_prof_groups[g]);
 }
 
 int prof_read(float* ms, int max) {
+  if (prof_collect() != 0) return -1;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   int n = 0;
-  for (size_t i = 0; i < g_prof_n && n < max; ++i) {
-    if (cudaEventSynchronize(g_prof_ev[i].second) != cudaSuccess) return -1;
-    float t = 0.f;
-    cudaEventElapsedTime(&t, g_prof_ev[i].first, g_prof_ev[i].second);
-    ms[n++] = t;
-  }
+  for (size_t i = 0; i < g_prof_acc.size() && n < max; ++i) ms[n++] = g_prof_acc[i];
   return n;
 }
 
@@ -371,9 +429,9 @@ static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPl
     attr_done = true;
   }
   cudaEvent_t* ev = prof_slot();
-  if (ev) cudaEventRecord(ev[0], st);
+  if (ev) prof_record(ev[0], st);
   kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc);
-  if (ev) cudaEventRecord(ev[1], st);
+  if (ev) prof_record(ev[1], st);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }

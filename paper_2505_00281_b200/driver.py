@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import math
 import time
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -100,6 +101,31 @@ class RunStats:
 
 # status-vector slots (one int32[8] device vector, read once per sync point)
 S_MV_FLAGS, S_NKEPT, S_EIG_STATUS, S_NOUT, S_GRAM_FLAGS, S_RESTART_FLAGS, S_NKEPT2 = 0, 1, 2, 3, 4, 5, 6
+
+
+# CUDA graphs of the outer iteration, keyed by everything the captured launches depend on
+# (device pointers of A, shapes, formats, policies).  A graph reads A through its pointer,
+# so a new operator at the same address replays correctly.
+_GRAPH_MAX = 8
+_GRAPHS = OrderedDict()
+_WARM = set()
+_NO_GRAPH = set()
+
+
+class _IterGraph:
+    def __init__(self, graph, Xs, outs, rec, prof_group):
+        self.graph, self.Xs, self.outs, self.rec, self.prof_group = graph, Xs, outs, rec, prof_group
+
+
+def _prof_collect(out) -> None:
+    """Harvest K1 kernel timings (bench.py) after the iteration's synchronisation."""
+    from . import _lib
+    L = _lib.load()
+    if L.ofrr_prof_gemm_active():
+        g = out.get("prof_group", -1)
+        if g is not None and g >= 0:
+            L.ofrr_prof_gemm_collect_group(g)
+        L.ofrr_prof_gemm_collect()
 
 
 def _fetch_status(st, comm: Comm):
@@ -238,7 +264,6 @@ class EigEngine:
         first iteration whose leading `top` residuals pass: the cheap estimate (K7e)
         nominates, the FP64 residual report (K7) confirms; the returned residuals are
         always the FP64 ones."""
-        import torch
         cfg = self.cfg
         tol, top = cfg.tol, (cfg.top or cfg.k)
         check = tol is not None
@@ -246,17 +271,20 @@ class EigEngine:
         eig = U64 = U = None
         r = 0
         rs = vals = None
+        use_graph = self._graph_capable()
         for it in range(cfg.m):
-            st = torch.zeros(8, dtype=torch.int32, device=self.device)
-            X = self.power(X, st)
-            h = self.basis(X, st)
             last = it == cfg.m - 1
-            # project speculatively with every column (the basis keeps all k in the common
-            # case; dropped columns of Q are zero): one host sync per outer iteration
-            kp = X.k
-            U = h.Q.narrow(kp)
-            eig, U64, Xn, est = self.project(U, st, want64=last, top_check=(top if check else None))
-            s, vals_all, est_np = self._fetch(st, eig.values, est)  # the iteration's one sync
+            # one iteration: power step(s), Hessenberg basis, projection with every column
+            # (the basis keeps all k in the common case; dropped columns of Q are zero),
+            # residual estimate -- replayed as one CUDA graph when possible.  One host sync.
+            out = self._graph_step(X, check, top) if use_graph and X.k == cfg.k else None
+            if out is None:
+                out = self._body(X, check, top)
+                if use_graph:
+                    _WARM.add(self._graph_key(check, top))
+            st, h, U, eig, Xn, est = out["st"], out["h"], out["U"], out["eig"], out["Xn"], out["est"]
+            kp = U.k
+            s, vals_all, est_np = self._unpack(out, st, eig, est)      # the iteration's one sync
             if s[S_MV_FLAGS] & 1:
                 raise OverflowDiagnostic("non-finite entries after MatVec")
             if s[S_NKEPT] == 0:
@@ -265,19 +293,19 @@ class EigEngine:
                 kp = int(s[S_NKEPT])
                 U = h.Q.narrow(kp)
                 st[S_EIG_STATUS:].zero_()                     # gram/pencil/restart slots
-                eig, U64, Xn, est = self.project(U, st, want64=last, top_check=(top if check else None))
+                eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
                 s, vals_all, est_np = self._fetch(st, eig.values, est)
             _raise_for(s, "projection")
             r = int(s[S_NOUT])
             vals = vals_all[:r]
             X = Xn.narrow(r)
+            U64 = None
             self.stats.iterations = it + 1
             if check:
                 e = self._finish(est_np, vals)
                 worst = float(np.max(e[: min(top, r)])) if r >= top else float("inf")
                 if worst < tol or last:
-                    if U64 is None:
-                        U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
+                    U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
                     rs = self.report(U64, eig, r, vals)                 # FP64 confirmation
                     worst = float(np.max(rs.residuals[: min(top, r)])) if r >= top else float("inf")
                     self.stats.history.append((it + 1, worst))
@@ -287,10 +315,98 @@ class EigEngine:
                 else:
                     self.stats.history.append((it + 1, worst))
         if rs is None:
-            if U64 is None:
-                U64, _ = self.ops.ritz(U, eig.vectors, U.k, eig.n_out, U.k, 1.0, want64=True)
+            U64, _ = self.ops.ritz(U, eig.vectors, U.k, eig.n_out, U.k, 1.0, want64=True)
             rs = self.report(U64, eig, r, vals)
         return rs
+
+    # ---- one outer iteration: eager body, or a replayed CUDA graph of it -----------------
+    def _body(self, X, check: bool, top: int) -> dict:
+        import torch
+        st = torch.zeros(8, dtype=torch.int32, device=self.device)
+        Xp = self.power(X, st)
+        h = self.basis(Xp, st)
+        U = h.Q.narrow(Xp.k)
+        eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
+        out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None)
+        if not self.comm.distributed:
+            parts = [st.to(torch.float64), eig.values.reshape(-1).to(torch.float64)]
+            if est is not None:
+                parts.append(est.reshape(-1).to(torch.float64))
+            out["pack"] = torch.cat(parts)
+        return out
+
+    def _unpack(self, out, st, eig, est):
+        """The iteration's single device->host read (status word, values, estimates)."""
+        if out["pack"] is None:
+            return self._fetch(st, eig.values, est)
+        host = out["pack"].cpu().numpy()
+        _prof_collect(out)
+        k = eig.values.numel()
+        return host[:8].astype(np.int64), host[8:8 + k], (host[8 + k:] if est is not None else None)
+
+    def _graph_capable(self) -> bool:
+        import os
+        return (self.ops is _ops and self.device.type == "cuda" and not self.comm.distributed
+                and os.environ.get("OFRR_CUDA_GRAPHS", "1") != "0")
+
+    def _graph_key(self, check: bool, top: int):
+        A, B = self.A_mv, self.A_pol
+        pol = lambda p: (int(p.storage), int(p.compute), int(p.accumulate), float(p.drop_tol))  # noqa: E731
+        from . import _lib
+        return (A.t.data_ptr(), A.rows, A.cols, A.lda, int(A.fmt), B.t.data_ptr(), B.rows, B.cols, B.lda, int(B.fmt),
+                self.n, self.cfg.k, self.cfg.iter, pol(self.pol), pol(self.mv), check, top, self.device.index,
+                bool(_lib.load().ofrr_prof_gemm_active()))
+
+    def _graph_step(self, X, check: bool, top: int):
+        """Replay the captured iteration (capturing it first once the shapes have run
+        eagerly in this process); None -> run it eagerly."""
+        key = self._graph_key(check, top)
+        g = _GRAPHS.get(key)
+        if g is None:
+            if key not in _WARM or key in _NO_GRAPH:
+                return None
+            g = self._capture(X, check, top, key)
+            if g is None:
+                return None
+        else:
+            _GRAPHS.move_to_end(key)
+        if X.t.data_ptr() != g.Xs.t.data_ptr():
+            g.Xs.t.copy_(X.t)
+        g.graph.replay()
+        g.rec.replayed()
+        self.stats.a_passes += g.a_passes
+        out = dict(g.outs)
+        out["prof_group"] = g.prof_group
+        return out
+
+    def _capture(self, X, check: bool, top: int, key):
+        import torch
+        from . import _lib
+        L = _lib.load()
+        Xs = self.ops.new_block(self.n, self.cfg.k, self.mv.storage, self.device)
+        Xs.t.copy_(X.t)
+        rec = self.ops.Recorder()
+        graph = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize(self.device)
+        passes0 = self.stats.a_passes
+        try:
+            with rec:
+                with torch.cuda.graph(graph):
+                    outs = self._body(Xs, check, top)
+                    Xs.t.copy_(outs["Xn"].t)                       # the next iteration's input
+        except Exception:                                             # capture unsupported: stay eager
+            _NO_GRAPH.add(key)
+            L.ofrr_prof_gemm_collect()
+            return None
+        prof_group = L.ofrr_prof_gemm_claim() if L.ofrr_prof_gemm_active() else -1
+        outs["Xn"] = Xs
+        g = _IterGraph(graph, Xs, outs, rec, prof_group)
+        g.a_passes = self.stats.a_passes - passes0       # passes the captured body makes
+        self.stats.a_passes = passes0                    # counted again by the replay
+        _GRAPHS[key] = g
+        while len(_GRAPHS) > _GRAPH_MAX:
+            _GRAPHS.popitem(last=False)
+        return g
 
     def _fetch(self, st, *vecs):
         """One device->host read: the status word (max over ranks) and fp64 vectors."""

@@ -31,8 +31,44 @@ LAUNCHES = [0]
 GEMM_LOG = None
 
 
+_RECORDER = None   # a Recorder while a CUDA graph is being captured
+
+
+class Recorder:
+    """Launch / GEMM-log accounting of a captured CUDA graph, re-applied on every replay."""
+
+    def __init__(self):
+        self.launches = 0
+        self.gemm = []
+
+    def __enter__(self):
+        global _RECORDER
+        self._prev = _RECORDER
+        _RECORDER = self
+        return self
+
+    def __exit__(self, *exc):
+        global _RECORDER
+        _RECORDER = self._prev
+        return False
+
+    def replayed(self) -> None:
+        LAUNCHES[0] += self.launches
+        if GEMM_LOG is not None:
+            GEMM_LOG.extend(self.gemm)
+
+
 def _count(n: int) -> None:
     LAUNCHES[0] += n
+    if _RECORDER is not None:
+        _RECORDER.launches += n
+
+
+def _log_gemm(entry) -> None:
+    if GEMM_LOG is not None:
+        GEMM_LOG.append(entry)
+    if _RECORDER is not None:
+        _RECORDER.gemm.append(entry)
 
 
 def pad_ld(n: int) -> int:
@@ -202,14 +238,14 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
                                    W.ptr, W.ld, of, _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
                                    W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else of,
                                    ws.data_ptr(), ws.numel(), _stream()), "gemm_av")
-    if GEMM_LOG is not None and (split or (A.fmt.tensor_core and not transpose)):
+    if split or (A.fmt.tensor_core and not transpose):
         # algorithmic bytes of the tensor-core kernel: A once + the B operand
         # once (3 bf16 slices in split mode); W is written by the finalize kernel
         chunks = [min(85, k - j0) for j0 in range(0, k, 85)] if split else [k]   # one launch per chunk
         for kc in chunks:
             kb = 3 * kc if split else kc
             nb = A.rows * A.cols * A.fmt.itemsize + A.cols * kb * (2 if split else X.fmt.itemsize)
-            GEMM_LOG.append((nb, 2.0 * A.rows * A.cols * kb))
+            _log_gemm((nb, 2.0 * A.rows * A.cols * kb))
     _count(3 if split else 2 if (A.fmt.tensor_core and not transpose) else 1)
 
 
@@ -297,7 +333,7 @@ def sym_def_gen_eig(B: torch.Tensor, M: torch.Tensor, k: int) -> EigOut:
     _lib.check(L.ofrr_sym_def_gen_eig(B.data_ptr(), M.data_ptr(), k, vals.data_ptr(), vecs.data_ptr(),
                                       n_out.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),
                "sym_def_gen_eig")
-    _count(1)
+    _count(8 if 1 <= k <= 160 else 1)   # pencil pipeline (7) + the gated general kernel
     return EigOut(vals, vecs, n_out, status)
 
 
@@ -353,7 +389,7 @@ def residual_eig(A: DevOperator, V: DevBlock, vals: torch.Tensor, r_dev: Optiona
     ws = _ws(L.ofrr_residual_workspace2(A.rows, A.cols, r_max, int(A.fmt), 0), A.device)
     _lib.check(L.ofrr_residual_eig(A.ptr, A.rows, A.lda, int(A.fmt), V.ptr, V.ld, vals.data_ptr(), _p(r_dev), r_max,
                                    res.data_ptr(), ws.data_ptr(), ws.numel(), _stream()), "residual_eig")
-    _count(2)
+    _count(5 if A.fmt in (FpFormat.BF16, FpFormat.F16, FpFormat.FP8_E4M3) else 2)
     return res
 
 
