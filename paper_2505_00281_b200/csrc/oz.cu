@@ -5,19 +5,21 @@
 // (ofrr/projection.py:136-147: A @ v in numpy float64 on to_dense_f64(A)).
 //
 // Representation.  Every row i of A gets a power-of-two scale 2^T_i > max_l |a_il|, every
-// column j of V a scale 2^F_j > max_l |v_lj|.  An entry is written in fixed point on a
-// 42-bit window below its scale and split into six signed 7-bit digits:
-//     a_il = 2^(T_i - 42) * sum_p a^(p)_il 2^(7 (6 - p))        (truncated below 2^(T_i - 42))
-// A bf16/fp16/e4m3 entry is exact unless it is 2^-34 below its row maximum.  Products of
-// digits are exact in int8 x int8 -> int32 (tcgen05.mma kind::i8), and an int32 level sum
-//     D_L = sum_{p + q = L} sum_l a^(p)_il v^(q)_lj,   L = 2..7 (p, q = 1..6, 21 products)
-// cannot overflow while a chunk of K covers at most 16384 terms (6 * 16384 * 127^2 < 2^31).
-// Then  (A V)_ij = 2^(T_i + F_j) * sum_L D_L 2^(-7 L)  up to the dropped levels L > 7 and the
-// truncated tails, i.e. ~2^-40 relative to |A| |V| (FP64 GEMM: ~n 2^-53 worst case); the
-// level sums are combined in fp64.
+// column j of V a scale 2^F_j > max_l |v_lj|.  An entry becomes the fixed-point integer
+// t = trunc(a 2^(46 - T_i)), |t| < 2^46, written in balanced base 256: six signed bytes,
+// most significant first,
+//     a_il = 2^(T_i - 46) * sum_P d^(P)_il 256^(5 - P),   d in [-128, 127]
+// (byte P of t + 0x808080808080, minus 128: slicing is an add and byte extraction).  A
+// bf16/fp16/e4m3 entry is exact unless it is 2^-23 below its row maximum.  Digit products
+// are exact in int8 x int8 -> int32 (tcgen05.mma kind::i8), and a level sum
+//     D_L = sum_{P + Q = L} sum_l a^(P)_il v^(Q)_lj,   L = 0..5 (21 products)
+// cannot overflow while a chunk of K covers at most 16384 terms (6 * 128^2 * 16384 < 2^31).
+// Then  (A V)_ij = 2^(T_i + F_j) * sum_L D_L 2^(-8 L - 12)  up to the dropped levels L > 5
+// and the truncated tails, both of random sign: ~2^-46 relative to |A| |V| per term (an
+// FP64 GEMM: ~2^-53); the level sums are combined in fp64.
 //
-// Kernels: k_oz_slices_a (row scales + the six digit planes of A; HBM-bound),
-// k_oz_slices_v (column scales + digits of V), k_oz_gemm (tcgen05 int8, TMA, TMEM int32
+// Kernels: k_oz_slices_a (row scales + the six byte planes of A; HBM-bound),
+// k_oz_slices_v (column scales + bytes of V), k_oz_gemm (tcgen05 int8, TMA, TMEM int32
 // accumulators for the six levels, stream-K over (row tile, K chunk) with fp64 partials),
 // k_oz_resid (deterministic partial sums -> (A v_j - lambda_j y_j) column sums of squares).
 #include "common.cuh"
@@ -43,10 +45,11 @@ struct OzCfg {
   static constexpr int SMEM_BYTES = 1024 + 2 * V_BYTES + A_STAGES * A_BYTES + 256;
 };
 
-// idesc for kind::i8: D = S32 (bits 4-5 = 2), A = B = signed 8-bit (bits 7-9, 10-12 = 1),
-// K-major, N >> 3 at bit 17, M >> 4 at bit 24.
-__host__ __device__ inline uint32_t oz_idesc(int n) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// idesc for kind::i8: D = S32 (bits 4-5 = 2), A / B signed (1) or unsigned (0) 8-bit
+// (bits 7-9 / 10-12), K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+__host__ __device__ inline uint32_t oz_idesc(int n, bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -70,19 +73,44 @@ __device__ __forceinline__ int oz_scale(double m) {
   if (m == 0.0) return 0;
   return ilogb(m) + 1;
 }
-// the six signed digits of x on the 42-bit window below 2^E, packed little-endian
-__device__ __forceinline__ void oz_split(double x, int E, uint32_t& lo, uint32_t& hi) {
-  lo = hi = 0;
-  if (E == OZ_BAD || x == 0.0) return;
-  const long long t = (long long)ldexp(fabs(x), 42 - E);   // < 2^42, truncated toward zero
-  const bool neg = x < 0.0;
-#pragma unroll
-  for (int p = 0; p < OZ_D; ++p) {
-    int d = (int)((t >> (7 * (OZ_D - 1 - p))) & 127);
-    if (neg) d = -d;
-    const uint32_t b = (uint32_t)(d & 0xff);
-    if (p < 4) lo |= b << (8 * p); else hi |= b << (8 * (p - 4));
+// 4 x 4 byte transpose: in[e] holds bytes (b0, b1, b2, b3) of entry e; out[b] holds byte b
+// of entries 0..3 (entry e in byte e)
+__device__ __forceinline__ void oz_t4(const uint32_t (&in)[4], uint32_t (&out)[4]) {
+  const uint32_t a01 = __byte_perm(in[0], in[1], 0x5140), b01 = __byte_perm(in[0], in[1], 0x7362);
+  const uint32_t a23 = __byte_perm(in[2], in[3], 0x5140), b23 = __byte_perm(in[2], in[3], 0x7362);
+  out[0] = __byte_perm(a01, a23, 0x5410);
+  out[1] = __byte_perm(a01, a23, 0x7632);
+  out[2] = __byte_perm(b01, b23, 0x5410);
+  out[3] = __byte_perm(b01, b23, 0x7632);
+}
+// balanced base-256 digit planes (most significant first) of four fixed-point words given
+// as biased (lo, hi) = t + 0x808080808080: digit = byte - 128 = byte ^ 0x80
+__device__ __forceinline__ void oz_planes4(const uint32_t (&lo)[4], const uint32_t (&hi)[4], uint32_t (&w)[OZ_D]) {
+  uint32_t tl[4], th[4];
+  oz_t4(lo, tl);
+  oz_t4(hi, th);
+  w[0] = th[1] ^ 0x80808080u;   // byte 5
+  w[1] = th[0] ^ 0x80808080u;   // byte 4
+  w[2] = tl[3] ^ 0x80808080u;
+  w[3] = tl[2] ^ 0x80808080u;
+  w[4] = tl[1] ^ 0x80808080u;
+  w[5] = tl[0] ^ 0x80808080u;
+}
+__device__ __forceinline__ void oz_bias(uint32_t& lo, uint32_t& hi) {
+  const uint32_t l = lo + 0x80808080u;
+  hi = hi + 0x8080u + (l < lo ? 1u : 0u);
+  lo = l;
+}
+// fp64 x on the 46-bit window below 2^E -> biased two's-complement (lo, hi)
+__device__ __forceinline__ void oz_fixed64(double x, int E, uint32_t& lo, uint32_t& hi) {
+  long long t = 0;
+  if (E != OZ_BAD && x != 0.0) {
+    t = (long long)ldexp(fabs(x), 46 - E);   // < 2^46, truncated toward zero
+    if (x < 0.0) t = -t;
   }
+  lo = (uint32_t)(unsigned long long)t;
+  hi = (uint32_t)((unsigned long long)t >> 32);
+  oz_bias(lo, hi);
 }
 
 // ---------------------------------------------------------------------------------
@@ -99,41 +127,25 @@ __device__ __forceinline__ float oz_ld_f(const void* A, int64_t i) {
   else if constexpr (FMT == F16) return __half2float(((const __half*)A)[i]);
   else { __nv_fp8_e4m3 v; v.__x = ((const __nv_fp8_storage_t*)A)[i]; return float(v); }
 }
-// fixed-point word of x on the 42-bit window below 2^T as (hi 10 bits, lo 32 bits)
-__device__ __forceinline__ void oz_fixed32(uint32_t b, int T, uint32_t& hi, uint32_t& lo) {
-  const int e = (int)(b >> 23);
-  const uint32_t M = (b & 0x7fffffu) | (e ? 0x800000u : 0u);
-  const int sh = (e ? e : 1) - 108 - T;        // t = M 2^sh, sh <= 18
+// f32 bit pattern b (exact value of a bf16 / f16 / e4m3 entry) on the 46-bit window
+// below 2^T -> biased two's-complement (lo, hi): value = M 2^(e - 150), t = M << (e - 104 - T)
+__device__ __forceinline__ void oz_fixed32(uint32_t b, int T, uint32_t& lo, uint32_t& hi) {
+  const uint32_t ab = b & 0x7fffffffu;
+  const int e = (int)(ab >> 23);
+  const uint32_t M = (ab & 0x7fffffu) | (e ? 0x800000u : 0u);
+  const int sh = (e ? e : 1) - 104 - T;                 // <= 22
   const uint32_t s = (uint32_t)max(sh, 0), r = (uint32_t)min(max(-sh, 0), 31);
-  lo = (M << s) >> r;
-  hi = s ? (M >> (32u - s)) : 0u;
-}
-// the six 7-bit digits (most significant first) of four entries, one byte each, signed
-__device__ __forceinline__ void oz_pack4(const float (&x)[4], int T, uint32_t (&w)[OZ_D]) {
-  uint32_t u[OZ_D] = {0, 0, 0, 0, 0, 0}, nm = 0;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const uint32_t b = __float_as_uint(x[e]);
-    uint32_t hi, lo;
-    oz_fixed32(b & 0x7fffffffu, T, hi, lo);
-    const uint32_t sh8 = 8u * e;
-    u[0] |= ((hi >> 3) & 127u) << sh8;
-    u[1] |= (((hi << 4) | (lo >> 28)) & 127u) << sh8;
-    u[2] |= ((lo >> 21) & 127u) << sh8;
-    u[3] |= ((lo >> 14) & 127u) << sh8;
-    u[4] |= ((lo >> 7) & 127u) << sh8;
-    u[5] |= (lo & 127u) << sh8;
-    nm |= (b >> 31) ? (0xffu << sh8) : 0u;
+  uint32_t l = (M << s) >> r;
+  uint32_t h = s ? (M >> (32u - s)) : 0u;
+  if (b >> 31) {                                         // two's-complement negate (lo, hi)
+    h = ~h + (l == 0u ? 1u : 0u);
+    l = 0u - l;
   }
-  // bytewise negation of digits <= 127 without inter-byte borrow: (0x80 - d) ^ 0x80
-#pragma unroll
-  for (int p = 0; p < OZ_D; ++p) {
-    const uint32_t ng = (0x80808080u - u[p]) ^ 0x80808080u;
-    w[p] = u[p] ^ ((u[p] ^ ng) & nm);
-  }
+  lo = l;
+  hi = h;
+  oz_bias(lo, hi);
 }
 
-// 8 consecutive entries of A as f32 (vector load when aligned and in range)
 template <int FMT>
 __device__ __forceinline__ void oz_ld8(const void* A, int64_t base, int64_t l0, int64_t cols, bool vec, float (&x)[8]) {
   if (vec && l0 + 8 <= cols) {
@@ -199,15 +211,37 @@ __global__ void __launch_bounds__(256)
   for (int w = 1; w < 8; ++w) m = red[w] > m ? red[w] : m;
   const int E = oz_scale((double)__uint_as_float(m));
   if (threadIdx.x == 0) T[i] = E;
+  // the scale 2^(46 - E) as an f32 (normal range) -> conversion path; else the bit path
+  const bool fast = E != OZ_BAD && 46 - E <= 127 && 46 - E >= -126;
+  const float sc = fast ? __int_as_float((46 - E + 127) << 23) : 0.0f;
   // 8 consecutive entries per thread step -> one 64-bit word per plane (cols_pad % 16 == 0)
   for (int64_t l0 = 8 * (int64_t)threadIdx.x; l0 < cols_pad; l0 += 8 * (int64_t)blockDim.x) {
     uint32_t w0[OZ_D] = {0, 0, 0, 0, 0, 0}, w1[OZ_D] = {0, 0, 0, 0, 0, 0};
     if (E != OZ_BAD) {
       float x[8];
       oz_ld8<FMT>(A, base, l0, cols, vec, x);
-      const float xa[4] = {x[0], x[1], x[2], x[3]}, xb[4] = {x[4], x[5], x[6], x[7]};
-      oz_pack4(xa, E, w0);
-      oz_pack4(xb, E, w1);
+      uint32_t lo[4], hi[4];
+      if (fast) {
+        // t = trunc(x 2^(46 - E)): exact scaling in f32, one f32 -> s64 conversion
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const long long t = __float2ll_rz(x[4 * h + e] * sc);
+            lo[e] = (uint32_t)(unsigned long long)t;
+            hi[e] = (uint32_t)((unsigned long long)t >> 32);
+            oz_bias(lo[e], hi[e]);
+          }
+          oz_planes4(lo, hi, h ? w1 : w0);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) oz_fixed32(__float_as_uint(x[e]), E, lo[e], hi[e]);
+        oz_planes4(lo, hi, w0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) oz_fixed32(__float_as_uint(x[4 + e]), E, lo[e], hi[e]);
+        oz_planes4(lo, hi, w1);
+      }
     }
 #pragma unroll
     for (int p = 0; p < OZ_D; ++p) *reinterpret_cast<uint2*>(row0 + p * plane + l0) = make_uint2(w0[p], w1[p]);
@@ -250,19 +284,10 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int E = sE;
   for (int64_t l0 = 4 * (int64_t)threadIdx.x; l0 < cols_pad; l0 += 4 * (int64_t)blockDim.x) {
-    uint32_t w[OZ_D] = {0, 0, 0, 0, 0, 0};
+    uint32_t w[OZ_D], lo[4], hi[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t l = l0 + e;
-      if (l < cols) {
-        uint32_t lo, hi;
-        oz_split(v[l], E, lo, hi);
-#pragma unroll
-        for (int p = 0; p < 4; ++p) w[p] |= ((lo >> (8 * p)) & 0xffu) << (8 * e);
-        w[4] |= (hi & 0xffu) << (8 * e);
-        w[5] |= ((hi >> 8) & 0xffu) << (8 * e);
-      }
-    }
+    for (int e = 0; e < 4; ++e) oz_fixed64(l0 + e < cols ? v[l0 + e] : 0.0, E, lo[e], hi[e]);
+    oz_planes4(lo, hi, w);
 #pragma unroll
     for (int p = 0; p < OZ_D; ++p) *reinterpret_cast<uint32_t*>(row0 + p * plane + l0) = w[p];
   }
@@ -360,12 +385,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             const int nq = OZ_D - p;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              // the segment's first unit, digit 0, k 0 initialises every level
+              // the segment's first unit, plane 0, k 0 initialises every level
               const uint32_t acc = (u > seg_start || p > 0 || k > 0) ? 1u : 0u;
               for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
                 const int ng = std::min(256 / BN, nq - q0);
                 mma_i8(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
-                       dv + (uint64_t)((q0 * BN * OZ_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN), acc);
+                       dv + (uint64_t)((q0 * BN * OZ_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN, true, true),
+                       acc);
               }
             }
             tc_commit(&aempty[as]);
@@ -399,7 +425,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         for (int lv = OZ_D - 1; lv >= 0; --lv) {     // lowest weight first
           int d[16];
           tmem_ld16i(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(lv * BN + c0), d);
-          const double w = ldexp(1.0, -7 * (lv + 2));
+          const double w = ldexp(1.0, -8 * lv - 12);
 #pragma unroll
           for (int i = 0; i < 16; ++i) s[i] = fma((double)d[i], w, s[i]);   // exact product
         }
