@@ -42,6 +42,14 @@ CONFIGS = {
     "c3": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-2, policy="full-f32",
                name="synthetic dense symmetric 65536x65536, geometric spectrum, top-64, k=128, "
                     "bf16 operator, fp32-accurate basis on bf16 tensor cores / fp64 Gram (BASELINE configs[2])"),
+    "c2-f64": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-8, policy="full-f64",
+                   name="synthetic dense symmetric 16384x16384 (bf16 operator), geometric spectrum, top-32, k=64, "
+                        "to 1e-8: fp64 basis with FP64-accurate products on the int8 tensor cores (Ozaki "
+                        "digit planes) / fp64 Gram"),
+    "c3-f64": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
+                   name="synthetic dense symmetric 65536x65536 (bf16 operator), geometric spectrum, top-64, "
+                        "k=128, to 1e-8 (the north-star target): fp64 basis, FP64-accurate int8 tensor-core "
+                        "products / fp64 Gram"),
 }
 MAX_OUTER = 60
 # A passes per C2 solve measured on the B200 (used by the reference arm, which never

@@ -455,7 +455,9 @@ __global__ void __launch_bounds__(OZ_TM)
     k_oz_resid(const double* __restrict__ ws, int BN, int kbc, int nchunks, long long total_units, int G,
                int max_slots, int64_t rows, int ncols, int j0, const int* __restrict__ T, const int* __restrict__ F,
                const double* __restrict__ vals, const int* __restrict__ r_dev, const double* __restrict__ Y,
-               int64_t ldy, double* __restrict__ part, int ldp, double* __restrict__ W, int64_t ldw) {
+               int64_t ldy, double* __restrict__ part, int ldp, void* __restrict__ W, int64_t ldw, int out_fmt,
+               double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
+               int out_fmt2) {
   __shared__ double red[4][16];
   const int t = blockIdx.x;
   const int row = threadIdx.x;
@@ -500,20 +502,37 @@ __global__ void __launch_bounds__(OZ_TM)
         const double av = (Ti == OZ_BAD || Fj == OZ_BAD) ? __longlong_as_double(0x7ff8000000000000ll)
                                                           : ldexp(s[q], Ti + Fj);
         if (W) {
-          W[(int64_t)gj * ldw + grow] = av;
+          // the product rounded to the output format; r2 carries |w| for the column max
+          const double w = rnd(av, out_fmt);
+          st_fmt(W, (long)((int64_t)gj * ldw + grow), out_fmt, w);
+          if (W2) st_fmt(W2, (long)((int64_t)gj * ldw2 + grow), out_fmt2, rnd(av, out_fmt2));
+          if (!isfinite(w) && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
+          r2 = (w != w) ? INFINITY : fabs(w);
         } else {
           const double d = av - vals[gj] * Y[(int64_t)gj * ldy + grow];
           r2 = d * d;
         }
       }
+      if (W) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        for (int o = 16; o > 0; o >>= 1) r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+      } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      }
       if (lane == 0) red[warp][q] = r2;
     }
     __syncthreads();
-    if (!W && threadIdx.x < 16 && jb + threadIdx.x < ncols)
-      part[(int64_t)t * ldp + j0 + jb + threadIdx.x] =
-          ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+    if (threadIdx.x < 16 && jb + threadIdx.x < ncols) {
+      const double* rr = &red[0][0];
+      if (W) {
+        const double m = fmax(fmax(rr[threadIdx.x], rr[16 + threadIdx.x]), fmax(rr[32 + threadIdx.x], rr[48 + threadIdx.x]));
+        if (colmax) atomic_max_nonneg(&colmax[j0 + jb + threadIdx.x], m);
+      } else {
+        part[(int64_t)t * ldp + j0 + jb + threadIdx.x] =
+            ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+      }
+    }
     __syncthreads();
   }
 }
@@ -532,11 +551,15 @@ struct OzPlan {
   int64_t rows_pad, cols_pad;
   int npad;
   long long total;
-  size_t off_T, off_F, off_planes, off_dig, off_ws, off_part, bytes;
+  // operator workspace (per A): row scales + digit planes
+  size_t op_T, op_planes, op_bytes;
+  // product workspace (per call): column scales, digits of V, partials, residual partials
+  size_t off_F, off_dig, off_ws, off_part, bytes;
 };
 
 static OzPlan oz_plan(int64_t rows, int64_t cols, int r) {
   OzPlan p;
+  r = std::max(r, 1);
   p.bn = r <= 32 ? 32 : 64;
   p.npass = (r + p.bn - 1) / p.bn;
   p.npad = p.npass * p.bn;
@@ -554,9 +577,11 @@ static OzPlan oz_plan(int64_t rows, int64_t cols, int r) {
   p.max_slots = (int)((per + p.kbc - 1) / p.kbc) + 1;
   size_t b = 0;
   auto take = [&](size_t n) { size_t o = b; b += (n + 1023) & ~size_t(1023); return o; };
-  p.off_T = take((size_t)p.rows_pad * 4);
+  p.op_T = take((size_t)p.rows_pad * 4);
+  p.op_planes = take((size_t)OZ_D * p.rows_pad * p.cols_pad);
+  p.op_bytes = b;
+  b = 0;
   p.off_F = take((size_t)p.npad * 4);
-  p.off_planes = take((size_t)OZ_D * p.rows_pad * p.cols_pad);
   p.off_dig = take((size_t)OZ_D * p.npad * p.cols_pad);
   p.off_ws = take((size_t)p.grid * p.max_slots * OZ_TM * p.bn * sizeof(double));
   p.off_part = take((size_t)p.m_tiles * r * sizeof(double));
@@ -564,7 +589,13 @@ static OzPlan oz_plan(int64_t rows, int64_t cols, int r) {
   return p;
 }
 
-size_t oz_ws(int64_t rows, int64_t cols, int r) { return oz_plan(rows, cols, std::max(r, 1)).bytes; }
+size_t oz_op_ws(int64_t rows, int64_t cols) { return oz_plan(rows, cols, 1).op_bytes; }
+size_t oz_prod_ws(int64_t rows, int64_t cols, int r) { return oz_plan(rows, cols, r).bytes; }
+// one-shot workspace (operator + product) of the residual entry points
+size_t oz_ws(int64_t rows, int64_t cols, int r) {
+  const OzPlan p = oz_plan(rows, cols, r);
+  return ((p.op_bytes + 1023) & ~size_t(1023)) + p.bytes;
+}
 int oz_nblocks(int64_t rows) { return (int)((rows + OZ_TM - 1) / OZ_TM); }
 
 template <int BN>
@@ -582,25 +613,20 @@ static int oz_launch(const CUtensorMap& tA, const CUtensorMap& tV, const OzPlan&
   return OFRR_OK;
 }
 
-// part[m_tile * r + j] = sum over the tile's rows of ((A V)_ij - vals_j Y_ij)^2, or, with W,
-// W = A V (fp64).  A: rows x cols row-major in a_fmt (F16 / BF16 / FP8); V: cols x r fp64.
-int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const double* V, int64_t ldv,
-               int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, double* W, int64_t ldw,
-               double** part_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+// K7z stage 1: the row scales and digit planes of A (rows x cols row-major, F16 / BF16 /
+// FP8) into the operator workspace; reusable for any number of products with this A.
+int oz_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws, size_t op_bytes,
+               cudaStream_t st) {
   if (a_fmt != BF16 && a_fmt != F16 && a_fmt != FP8) {
-    ofrr_set_error("ozaki product: A format %d not supported", a_fmt);
+    ofrr_set_error("ozaki: A format %d not supported (16/8-bit operators)", a_fmt);
     return OFRR_ERR_UNSUPPORTED;
   }
-  const OzPlan p = oz_plan(rows, cols, r);
-  if (p.nchunks > 16) { ofrr_set_error("ozaki product: cols=%lld beyond 16 chunks", (long long)cols); return OFRR_ERR_UNSUPPORTED; }
-  if (!ws || ws_bytes < p.bytes) { ofrr_set_error("ozaki product: workspace too small (%zu < %zu)", ws_bytes, p.bytes); return OFRR_ERR_INVALID; }
-  uint8_t* base = (uint8_t*)ws;
-  int* T = (int*)(base + p.off_T);
-  int* F = (int*)(base + p.off_F);
-  int8_t* planes = (int8_t*)(base + p.off_planes);
-  int8_t* dig = (int8_t*)(base + p.off_dig);
-  double* pws = (double*)(base + p.off_ws);
-  double* part = (double*)(base + p.off_part);
+  const OzPlan p = oz_plan(rows, cols, 1);
+  if (p.nchunks > 16) { ofrr_set_error("ozaki: cols=%lld beyond 16 chunks", (long long)cols); return OFRR_ERR_UNSUPPORTED; }
+  if (!op_ws || op_bytes < p.op_bytes) { ofrr_set_error("ozaki: operator workspace too small (%zu < %zu)", op_bytes, p.op_bytes); return OFRR_ERR_INVALID; }
+  uint8_t* base = (uint8_t*)op_ws;
+  int* T = (int*)(base + p.op_T);
+  int8_t* planes = (int8_t*)(base + p.op_planes);
   if (a_fmt == BF16)
     k_oz_slices_a<BF16><<<(unsigned)p.rows_pad, 256, 0, st>>>(A, rows, cols, lda, T, planes, p.rows_pad, p.cols_pad);
   else if (a_fmt == F16)
@@ -608,6 +634,26 @@ int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
   else
     k_oz_slices_a<FP8><<<(unsigned)p.rows_pad, 256, 0, st>>>(A, rows, cols, lda, T, planes, p.rows_pad, p.cols_pad);
   OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+// K7z stage 2: (A V) with a prepared operator.  Residual mode (W == nullptr):
+// part[m_tile * r + j] = sum over the tile's rows of ((A V)_ij - vals_j Y_ij)^2.  Product
+// mode: W = A V rounded to out_fmt (+ W2 in out_fmt2, colmax |= max |W|, flags on non-finite).
+int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int64_t ldv, int r,
+             const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W, int64_t ldw, int out_fmt,
+             double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2, double** part_out, void* ws,
+             size_t ws_bytes, cudaStream_t st) {
+  const OzPlan p = oz_plan(rows, cols, r);
+  if (!ws || ws_bytes < p.bytes) { ofrr_set_error("ozaki: workspace too small (%zu < %zu)", ws_bytes, p.bytes); return OFRR_ERR_INVALID; }
+  const uint8_t* obase = (const uint8_t*)op_ws;
+  const int* T = (const int*)(obase + p.op_T);
+  const int8_t* planes = (const int8_t*)(obase + p.op_planes);
+  uint8_t* base = (uint8_t*)ws;
+  int* F = (int*)(base + p.off_F);
+  int8_t* dig = (int8_t*)(base + p.off_dig);
+  double* pws = (double*)(base + p.off_ws);
+  double* part = (double*)(base + p.off_part);
   k_oz_slices_v<<<(unsigned)p.npad, 256, 0, st>>>(V, ldv, cols, r, F, dig, p.npad, p.cols_pad);
   OFRR_CHECK_LAUNCH();
   CUtensorMap tA, tV;
@@ -621,11 +667,24 @@ int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
     if (rc) return rc;
     k_oz_resid<<<p.m_tiles, OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
-                                           ldw);
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;
   return OFRR_OK;
+}
+
+// one-shot residual product (prepare + apply in one workspace)
+int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const double* V, int64_t ldv,
+               int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, double* W, int64_t ldw,
+               double** part_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const OzPlan p = oz_plan(rows, cols, r);
+  const size_t opb = (p.op_bytes + 1023) & ~size_t(1023);
+  if (!ws || ws_bytes < opb + p.bytes) { ofrr_set_error("ozaki product: workspace too small (%zu < %zu)", ws_bytes, opb + p.bytes); return OFRR_ERR_INVALID; }
+  int rc = oz_prepare(A, rows, cols, lda, a_fmt, ws, opb, st);
+  if (rc) return rc;
+  return oz_apply(ws, rows, cols, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, F64, nullptr, nullptr, nullptr, 0, F64,
+                  part_out, (uint8_t*)ws + opb, ws_bytes - opb, st);
 }
 
 }  // namespace ofrr

@@ -77,6 +77,14 @@ def operator_for(a: DenseMatrix, block_fmt: FpFormat):
         op = a.device_operator(FpFormat.BF16)
         if a.exact_in(FpFormat.BF16):
             return op
+    if block_fmt == FpFormat.F64:
+        # an fp64 block against an operator held exactly in 16/8 bits: FP64-accurate int8
+        # tensor-core products (ops.ozaki_gemm) -- no fp64 copy of A (4x the bytes)
+        for low in (FpFormat.BF16, FpFormat.F16, FpFormat.FP8_E4M3):
+            if a.fmt == low or low in getattr(a, "_dev", {}):
+                op = a.device_operator(low)
+                if a.exact_in(low):
+                    return op
     return a.device_operator(block_fmt)
 
 
@@ -169,6 +177,21 @@ class EigEngine:
                              f"{self.r1 - self.r0} (rows {self.r0}..{self.r1} of {self.n})")
         _, self.proj_out = projection_policy(self.pol)
         self.stats = RunStats()
+        self._oz = {}           # prepared Ozaki digit planes per operator (this run)
+
+    def _ozaki(self, A):
+        """Prepared int8 digit planes of a 16/8-bit operator (once per run), or None."""
+        if self.ops is not _ops or A.fmt not in _ops.OZAKI_FMTS:
+            return None
+        oz = self._oz.get(id(A))
+        if oz is None:
+            oz = self.ops.OzakiOperator(A)
+            self._oz[id(A)] = oz
+        return oz
+
+    def _block_oz(self, A, X):
+        """The Ozaki operator when an fp64 block meets a 16/8-bit operator."""
+        return self._ozaki(A) if X.fmt == FpFormat.F64 else None
 
     # ---- blocks ---------------------------------------------------------------------
     def start_block(self):
@@ -183,7 +206,8 @@ class EigEngine:
         for _ in range(self.cfg.iter):
             colmax = torch.zeros(k, dtype=torch.float64, device=self.device)
             W = ops.new_block(self.A_mv.rows, k, self.mv.storage, self.device)
-            ops.gemm_av(self.A_mv, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+            ops.gemm_av(self.A_mv, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1],
+                        **({"oz": self._block_oz(self.A_mv, X)} if self.ops is _ops else {}))
             self.stats.a_passes += 1
             comm.all_reduce_max_(colmax)
             ops.scale_columns(W, colmax, self.mv.compute)
@@ -212,9 +236,10 @@ class EigEngine:
         W = ops.new_block(self.A_pol.rows, kp, self.pol.storage, self.device)
         W2 = None
         if top_check is not None:
-            acc = FpFormat.F64 if self.A_pol.fmt == FpFormat.F64 else FpFormat.F32
+            acc = FpFormat.F64 if FpFormat.F64 in (self.A_pol.fmt, U.fmt) else FpFormat.F32
             W2 = ops.new_block(self.A_pol.rows, kp, acc, self.device)
-        ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2)
+        ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2,
+                    **({"oz": self._block_oz(self.A_pol, U)} if self.ops is _ops else {}))
         self.stats.a_passes += 1
         Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U
         if comm.distributed:
@@ -242,11 +267,18 @@ class EigEngine:
         import torch
         ops, comm = self.ops, self.comm
         A = self.a.residual_operator(self.A_mv.fmt) if hasattr(self.a, "residual_operator") else self.A_mv
+        oz = self._ozaki(A)
         if not comm.distributed:
+            if oz is not None:
+                res = torch.zeros(max(r, 1), dtype=torch.float64, device=self.device)
+                return ops.ozaki_residual(oz, U64, U64, vals, r_dev, r, res, 0)
             return ops.residual_eig(A, U64, vals, r_dev, r)
         res = torch.zeros(r, dtype=torch.float64, device=self.device)
         Yl = _row_slice(U64, self.r0, self.r1)
-        ops.residual_pair(A, False, U64.narrow(r), Yl.narrow(r), vals, r_dev, r, res, accumulate_max=2)
+        if oz is not None:
+            ops.ozaki_residual(oz, U64.narrow(r), Yl.narrow(r), vals, r_dev, r, res, 2)
+        else:
+            ops.residual_pair(A, False, U64.narrow(r), Yl.narrow(r), vals, r_dev, r, res, accumulate_max=2)
         comm.all_reduce_sum_(res)
         return res   # sum of squares; finished on the host (see _finish_residuals)
 
@@ -272,6 +304,9 @@ class EigEngine:
         r = 0
         rs = vals = None
         use_graph = self._graph_capable()
+        self._block_oz(self.A_mv, X)                 # FP64 blocks: slice A once per run, eagerly
+        if self.mv.storage != self.pol.storage:
+            self._ozaki(self.A_pol) if self.pol.storage == FpFormat.F64 else None
         for it in range(cfg.m):
             last = it == cfg.m - 1
             # one iteration: power step(s), Hessenberg basis, projection with every column

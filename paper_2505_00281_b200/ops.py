@@ -213,13 +213,81 @@ def round_tensor(x: torch.Tensor, fmt: FpFormat) -> torch.Tensor:
 # ---------------------------------------------------------------------------------
 # K1 / K2
 # ---------------------------------------------------------------------------------
+# ---------------------------------------------------------------------------------
+# K7z: FP64-accurate products with a 16/8-bit operator (int8 tensor cores, Ozaki digits)
+# ---------------------------------------------------------------------------------
+OZAKI_FMTS = (FpFormat.BF16, FpFormat.F16, FpFormat.FP8_E4M3)
+_OZ_BUFFERS = {}   # operator workspace per (A pointer, shape, format): stable addresses
+
+
+class OzakiOperator:
+    """The digit planes of a 16/8-bit operator (ofrr_ozaki_prepare), reusable for every
+    FP64-accurate product with it until A changes; ``refresh`` re-slices A in place."""
+
+    def __init__(self, A: DevOperator):
+        if A.fmt not in OZAKI_FMTS:
+            raise ValueError(f"Ozaki products need a 16/8-bit operator, got {A.fmt.name}")
+        L = _lib.load()
+        self.A = A
+        key = (A.ptr, A.rows, A.cols, A.lda, int(A.fmt), str(A.device))
+        nb = L.ofrr_ozaki_operator_workspace(A.rows, A.cols)
+        ws = _OZ_BUFFERS.get(key)
+        if ws is None or ws.numel() < nb:
+            ws = _ws(nb, A.device)
+            if len(_OZ_BUFFERS) >= 2:
+                _OZ_BUFFERS.pop(next(iter(_OZ_BUFFERS)))
+            _OZ_BUFFERS[key] = ws
+        self.ws = ws
+        self.refresh()
+
+    def refresh(self) -> None:
+        L = _lib.load()
+        A = self.A
+        _lib.check(L.ofrr_ozaki_prepare(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), self.ws.data_ptr(), self.ws.numel(),
+                                        _stream()), "ozaki_prepare")
+        _count(1)
+
+
+def ozaki_gemm(oz: OzakiOperator, X: DevBlock, W: DevBlock, colmax=None, flags=None, W2: Optional[DevBlock] = None):
+    """W = A X for an fp64 block X, FP64-accurate (rounded to W.fmt)."""
+    L = _lib.load()
+    A = oz.A
+    if X.fmt != FpFormat.F64:
+        raise ValueError("ozaki_gemm: the block must be fp64")
+    ws = _ws(L.ofrr_ozaki_workspace(A.rows, A.cols, X.k), A.device)
+    _lib.check(L.ofrr_ozaki_gemm(oz.ws.data_ptr(), A.rows, A.cols, X.ptr, X.ld, X.k, W.ptr, W.ld, int(W.fmt),
+                                 _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
+                                 W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else int(W.fmt),
+                                 ws.data_ptr(), ws.numel(), _stream()), "ozaki_gemm")
+    _count(2 + (X.k + 63) // 64 * 2)
+
+
+def ozaki_residual(oz: OzakiOperator, Xv: DevBlock, Yv: DevBlock, vals: torch.Tensor,
+                   r_dev: Optional[torch.Tensor], r_max: int, res: torch.Tensor, accumulate_max: int = 0):
+    L = _lib.load()
+    A = oz.A
+    ws = _ws(L.ofrr_ozaki_workspace(A.rows, A.cols, r_max), A.device)
+    _lib.check(L.ofrr_ozaki_residual(oz.ws.data_ptr(), A.rows, A.cols, Xv.ptr, Xv.ld, Yv.ptr, Yv.ld, vals.data_ptr(),
+                                     _p(r_dev), r_max, res.data_ptr(), int(accumulate_max), ws.data_ptr(), ws.numel(),
+                                     _stream()), "ozaki_residual")
+    _count(3 + (r_max + 63) // 64 * 2)
+    return res
+
+
 def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat] = None,
             colmax: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
-            transpose: bool = False, W2: Optional[DevBlock] = None) -> None:
+            transpose: bool = False, W2: Optional[DevBlock] = None, oz: Optional[OzakiOperator] = None) -> None:
     """W = op(A) X rounded to out_fmt (default W.fmt); colmax[j] = max|W[:,j]|; optionally
-    W2 = the same product in W2.fmt (e.g. the fp32 accumulator)."""
+    W2 = the same product in W2.fmt (e.g. the fp32 accumulator).  An fp64 block against a
+    16/8-bit operator runs as an FP64-accurate int8 tensor-core product (``oz``: prepared
+    digit planes of A, made on the fly when absent)."""
     L = _lib.load()
     k = X.k
+    if X.fmt == FpFormat.F64 and A.fmt in OZAKI_FMTS and not transpose:
+        if out_fmt is not None and FpFormat(out_fmt) != W.fmt:
+            raise ValueError("gemm_av (fp64 block): out_fmt must be W's format")
+        ozaki_gemm(oz if oz is not None else OzakiOperator(A), X, W, colmax=colmax, flags=flags, W2=W2)
+        return
     ws_b = L.ofrr_gemm_av_workspace(A.rows, A.cols, k, int(A.fmt), int(transpose))
     ws = _ws(ws_b, A.device)
     of = int(W.fmt if out_fmt is None else out_fmt)

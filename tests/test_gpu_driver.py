@@ -164,6 +164,52 @@ def test_driver_eig_fp32_basis_on_bf16_operator(ofrr_gpu, oracle):
     assert np.max(rs.residuals[:top]) < 1e-4
 
 
+def test_driver_eig_fp64_basis_on_bf16_operator(ofrr_gpu, oracle):
+    """full-f64 policy on a bf16-stored operator: the fp64 blocks multiply A on the int8
+    tensor cores (Ozaki digit planes, no fp64 copy of A); parity vs the oracle's full-f64
+    run (FP64 products) on the same A, to 1e-8-class residuals."""
+    import paper_2505_00281_b200.ops as ops
+    p, o = ofrr_gpu, oracle
+    n, top, k, m = 1024, 10, 20, 8
+    lam = p.geometric_spectrum(n, top, k)
+    A, f = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    a_host = o.sym_from_factors(n, f.hadamard, f.c, f.s, f.Wf, f.Mf, o.BF16)
+    cfg = p.IterConfig(k=k, m=m, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.FULL_F64, seed=SEED)
+    before = len(A._dev)
+    rs = p.subspace_iter_eig(A, cfg)
+    assert p.FpFormat.F64 not in A._dev and len(A._dev) == before      # no fp64 copy of A was made
+    ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=o.FULL_F64, seed=SEED)
+    exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+    assert np.max(rs.residuals[:top]) < 1e-8
+    assert ops.OZAKI_FMTS
+
+
+def test_ozaki_gemm_vs_fp64(ofrr_gpu, oracle):
+    """ofrr_ozaki_gemm: W = A X (fp64 X, bf16 A) to ~1e-14 of the FP64 product; column
+    inf-norms and the fp32 second output."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(7)
+    rows, cols, k = 777, 20000, 70
+    a = o.round_to(rng.standard_normal((rows, cols)), 3)
+    x = rng.standard_normal((cols, k))
+    A = p.DenseMatrix(np.asfortranarray(a), p.FpFormat.F64).device_operator(p.FpFormat.BF16)
+    X = ops.block_from_host(x, p.FpFormat.F64, torch.device("cuda"))
+    W = ops.new_block(rows, k, p.FpFormat.F64, torch.device("cuda"))
+    W2 = ops.new_block(rows, k, p.FpFormat.F32, torch.device("cuda"))
+    colmax = torch.zeros(k, dtype=torch.float64, device="cuda")
+    ops.gemm_av(A, X, W, colmax=colmax, W2=W2)
+    ref = a @ x
+    got = W.to_numpy_f64()
+    bound = 1e-13 * (np.abs(a) @ np.abs(x))
+    assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
+    np.testing.assert_array_equal(colmax.cpu().numpy(), np.max(np.abs(got), axis=0))
+    np.testing.assert_array_equal(W2.to_numpy_f64(), o.round_to(got, 1))
+
+
 @pytest.mark.parametrize("pname", ["tc-bf16", "tc-f16", "full-f32"])
 def test_driver_svd_tensor_core_vs_oracle(ofrr_gpu, oracle, pname):
     """partial SVD on the tensor-core path (A V and A^T U both K-major: A^T resident):
