@@ -194,6 +194,35 @@ def run_reference(args, cfg):
 # ------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------
+def _num(x):
+    """JSON-safe float (None for NaN / inf: configs whose products all run through K7z
+    launch no K1 kernel)."""
+    return float(x) if x is not None and np.isfinite(x) else None
+
+
+def profiled_traffic(cfg_name: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the K1 kernel this config
+    runs, from the committed ncu launch list of the same bench command (profiles/); None when
+    there is no capture for this config."""
+    import glob
+    if cfg_name != "c2":
+        return None, None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_launches_c2_bench.txt")))
+    if not files:
+        return None, None
+    best = None
+    for line in open(files[-1]):
+        if "k_gemm_av_tc" in line and "MB/launch" in line:
+            parts = line.split()
+            n = int(parts[0])
+            mb = float(parts[parts.index("MB/launch") - 1])
+            if best is None or n > best[0]:
+                best = (n, mb)
+    if best is None:
+        return None, None
+    return best[1] * 1e6, os.path.relpath(files[-1], ROOT)
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -303,6 +332,7 @@ def run_ours(args, cfg):
         passes = stats.a_passes
         cpu = {"value": pass_s * passes, "unit": "s", "cores": threads, "kind": kind,
                "sample": sample + f"; x {passes:.0f} A passes per solve (this run's count)"}
+    traffic, traffic_src = profiled_traffic(args.config)
     line = {
         "metric": "OFRR top-k eig time-to-tol", "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
@@ -315,10 +345,11 @@ def run_ours(args, cfg):
                    "parallelism": f"row-partitioned x{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (A = %d MiB per GPU)" % ((r1 - r0) * n * 2 >> 20)},
         "roofline": {"kernel": "k_gemm_av_tc (K1, A.X block product; kernel-only CUDA events)", "bound": "hbm",
-                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_kind": peak_kind, "traffic": None, "bytes_per_launch": nbytes,
-                     "avg_launch_ms": avg_ms, "launches": len(durs), "share_of_step": gemm_share,
-                     "tflops": flops / (avg_ms * 1e-3) / 1e12, "tflops_peak_bf16": bf16_peak,
+                     "achieved": _num(achieved), "peak": hbm, "unit": "GB/s", "frac": _num(achieved / hbm),
+                     "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
+                     "bytes_per_launch": _num(nbytes),
+                     "avg_launch_ms": _num(avg_ms), "launches": len(durs), "share_of_step": gemm_share,
+                     "tflops": _num(flops / (avg_ms * 1e-3) / 1e12), "tflops_peak_bf16": bf16_peak,
                      "launches_per_solve": nl / args.steps},
         "cpu_baseline": cpu,
         "e2e": e2e,
