@@ -54,7 +54,7 @@ CONFIGS = {
 MAX_OUTER = 60
 # A passes per C2 solve measured on the B200 (used by the reference arm, which never
 # touches a GPU, to extrapolate its per-pass time to a full solve)
-C2_PASSES_TO_TOL = 10
+C2_PASSES_TO_TOL = 4
 
 
 def _peaks():
