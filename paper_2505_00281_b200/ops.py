@@ -170,13 +170,27 @@ def block_from_host(x, fmt: FpFormat, device) -> DevBlock:
     return out
 
 
+_PCG_STATE = {}
+
+
+def _pcg64_state(seed: int):
+    """numpy's PCG64 (state, increment) for default_rng(seed) (SeedSequence hashing on the
+    host; memoised, it is a pure function of the seed)."""
+    st = _PCG_STATE.get(seed)
+    if st is None:
+        import numpy as np
+        raw = np.random.default_rng(seed).bit_generator.state["state"]
+        st = (int(raw["state"]), int(raw["inc"]))
+        if len(_PCG_STATE) < 64:
+            _PCG_STATE[seed] = st
+    return st
+
+
 def start_block(seed: int, n: int, k: int, fmt: FpFormat, device) -> DevBlock:
     """X0 = numpy default_rng(seed).random((n, k)) rounded to fmt, generated on the device
     bit for bit (ofrr/driver.py:97-99): numpy derives the PCG64 state from the seed, the
     device walks the stream."""
-    import numpy as np
-    st = np.random.default_rng(seed).bit_generator.state["state"]
-    s, inc = int(st["state"]), int(st["inc"])
+    s, inc = _pcg64_state(seed)
     m64 = (1 << 64) - 1
     X = new_block(n, k, fmt, device, zero=True)
     L = _lib.load()
