@@ -187,8 +187,10 @@ size_t ofrr_residual_workspace2(int64_t rows, int64_t cols, int r, int a_fmt, in
 
 /* FP64-accurate products with a 16/8-bit operator on the int8 tensor cores (Ozaki scheme,
  * see ofrr_residual_workspace2), split into a per-operator stage and per-product calls:
- *   prepare   row scales + six balanced base-256 digit planes of A into op_ws
- *             (ofrr_ozaki_operator_workspace bytes; ~6 bytes per entry of A);
+ *   prepare   the row scales of A into op_ws (ofrr_ozaki_operator_workspace bytes); the
+ *             digits of A are made on the fly inside the product kernel (A is read once
+ *             in its own format); OFRR_OZ_PLANES=1 selects the variant that stores six
+ *             balanced base-256 digit planes of A (~6 bytes per entry) instead;
  *   gemm      W = A X for an fp64 block X (cols x k, ldx), W rounded to out_fmt (ldw),
  *             optional W2 in out_fmt2, colmax[j] = max(colmax[j], max_i |W_ij|), flags |=
  *             NONFINITE -- the F64-policy block product of ofrr/_kernels.pyx:60-84 without an
@@ -200,13 +202,14 @@ size_t ofrr_ozaki_operator_workspace(int64_t rows, int64_t cols);
 size_t ofrr_ozaki_workspace(int64_t rows, int64_t cols, int r);
 int ofrr_ozaki_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws,
                        size_t op_bytes, void* stream);
-int ofrr_ozaki_gemm(const void* op_ws, int64_t rows, int64_t cols, const double* X, int64_t ldx, int k,
-                    void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2,
-                    int64_t ldw2, int out_fmt2, void* workspace, size_t workspace_bytes, void* stream);
-int ofrr_ozaki_residual(const void* op_ws, int64_t rows, int64_t cols, const double* Xv, int64_t ldx,
-                        const double* Yv, int64_t ldy, const double* vals, const int* r_dev, int r_max,
-                        double* res, int accumulate_max, void* workspace, size_t workspace_bytes,
-                        void* stream);
+int ofrr_ozaki_gemm(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
+                    const void* op_ws, const double* X, int64_t ldx, int k, void* W, int64_t ldw,
+                    int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
+                    void* workspace, size_t workspace_bytes, void* stream);
+int ofrr_ozaki_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
+                        const void* op_ws, const double* Xv, int64_t ldx, const double* Yv,
+                        int64_t ldy, const double* vals, const int* r_dev, int r_max, double* res,
+                        int accumulate_max, void* workspace, size_t workspace_bytes, void* stream);
 int ofrr_residual_eig(const void* A, int64_t n, int64_t lda, int a_fmt, const double* V,
                       int64_t ldv, const double* vals, const int* r_dev, int r_max, double* res,
                       void* workspace, size_t workspace_bytes, void* stream);

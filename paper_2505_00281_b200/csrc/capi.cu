@@ -25,14 +25,14 @@ int resid_est(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw,
               void* ws, size_t ws_bytes, cudaStream_t st);
 size_t residual_ws(int64_t rows, int r);
 size_t residual_ws2(int64_t rows, int64_t cols, int r, int a_fmt, int transpose);
-size_t oz_op_ws(int64_t rows, int64_t cols);
-size_t oz_prod_ws(int64_t rows, int64_t cols, int r);
-int oz_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws, size_t op_bytes,
-               cudaStream_t st);
-int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int64_t ldv, int r,
-             const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W, int64_t ldw, int out_fmt,
-             double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2, double** part_out, void* ws,
-             size_t ws_bytes, cudaStream_t st);
+size_t ozx_op_ws(int64_t rows, int64_t cols);
+size_t ozx_prod_ws(int64_t rows, int64_t cols, int r);
+int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws, size_t op_bytes,
+                cudaStream_t st);
+int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws, const double* V,
+              int64_t ldv, int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W,
+              int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
+              double** part_out, void* ws, size_t ws_bytes, cudaStream_t st);
 int oz_nblocks(int64_t rows);
 int residual_reduce(const double* part, int nblocks, int n, const double* vals, const int* r_dev, double* res,
                     int mode, cudaStream_t st);
@@ -195,29 +195,31 @@ size_t ofrr_residual_workspace2(int64_t rows, int64_t cols, int r, int a_fmt, in
   return residual_ws2(rows, cols, r, a_fmt, transpose);
 }
 
-size_t ofrr_ozaki_operator_workspace(int64_t rows, int64_t cols) { return oz_op_ws(rows, cols); }
-size_t ofrr_ozaki_workspace(int64_t rows, int64_t cols, int r) { return oz_prod_ws(rows, cols, r); }
+size_t ofrr_ozaki_operator_workspace(int64_t rows, int64_t cols) { return ozx_op_ws(rows, cols); }
+size_t ofrr_ozaki_workspace(int64_t rows, int64_t cols, int r) { return ozx_prod_ws(rows, cols, r); }
 
 int ofrr_ozaki_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws,
                        size_t op_bytes, void* stream) {
   if (rows <= 0 || cols <= 0) { ofrr_set_error("ozaki_prepare: empty operator"); return OFRR_ERR_INVALID; }
-  return oz_prepare(A, rows, cols, lda, a_fmt, op_ws, op_bytes, S(stream));
+  return ozx_prepare(A, rows, cols, lda, a_fmt, op_ws, op_bytes, S(stream));
 }
 
-int ofrr_ozaki_gemm(const void* op_ws, int64_t rows, int64_t cols, const double* X, int64_t ldx, int k, void* W,
-                    int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
-                    void* workspace, size_t workspace_bytes, void* stream) {
+int ofrr_ozaki_gemm(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws,
+                    const double* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax,
+                    int* flags, void* W2, int64_t ldw2, int out_fmt2, void* workspace, size_t workspace_bytes,
+                    void* stream) {
   if (!valid_fmt(out_fmt) || !valid_fmt(out_fmt2) || k <= 0 || !W) { ofrr_set_error("ozaki_gemm: invalid arguments"); return OFRR_ERR_INVALID; }
-  return oz_apply(op_ws, rows, cols, X, ldx, k, nullptr, nullptr, nullptr, 0, W, ldw, out_fmt, colmax, flags, W2,
-                  ldw2, out_fmt2, nullptr, workspace, workspace_bytes, S(stream));
+  return ozx_apply(A, rows, cols, lda, a_fmt, op_ws, X, ldx, k, nullptr, nullptr, nullptr, 0, W, ldw, out_fmt, colmax,
+                   flags, W2, ldw2, out_fmt2, nullptr, workspace, workspace_bytes, S(stream));
 }
 
-int ofrr_ozaki_residual(const void* op_ws, int64_t rows, int64_t cols, const double* Xv, int64_t ldx,
-                        const double* Yv, int64_t ldy, const double* vals, const int* r_dev, int r_max, double* res,
-                        int accumulate_max, void* workspace, size_t workspace_bytes, void* stream) {
+int ofrr_ozaki_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws,
+                        const double* Xv, int64_t ldx, const double* Yv, int64_t ldy, const double* vals,
+                        const int* r_dev, int r_max, double* res, int accumulate_max, void* workspace,
+                        size_t workspace_bytes, void* stream) {
   double* part = nullptr;
-  int rc = oz_apply(op_ws, rows, cols, Xv, ldx, r_max, vals, r_dev, Yv, ldy, nullptr, 0, F64, nullptr, nullptr,
-                    nullptr, 0, F64, &part, workspace, workspace_bytes, S(stream));
+  int rc = ozx_apply(A, rows, cols, lda, a_fmt, op_ws, Xv, ldx, r_max, vals, r_dev, Yv, ldy, nullptr, 0, F64, nullptr,
+                     nullptr, nullptr, 0, F64, &part, workspace, workspace_bytes, S(stream));
   if (rc) return rc;
   return residual_reduce(part, oz_nblocks(rows), r_max, vals, r_dev, res, accumulate_max, S(stream));
 }

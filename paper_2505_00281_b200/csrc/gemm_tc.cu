@@ -265,7 +265,8 @@ static PFN_encodeTiled get_encode() {
 }
 
 static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t inner, uint64_t outer,
-                        uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
+                        uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
+                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) { ofrr_set_error("cuTensorMapEncodeTiled unavailable"); return OFRR_ERR_CUDA; }
   CUtensorMapDataType dt = a_fmt == BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -277,7 +278,7 @@ static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t i
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(tm, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     ofrr_set_error("cuTensorMapEncodeTiled failed (%d): dims %llu x %llu ld %llu box %u x %u", (int)r,
@@ -292,6 +293,11 @@ static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t i
 int oz_make_tmap_u8(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
                     uint32_t box_inner, uint32_t box_outer) {
   return make_tmap_2d(tm, base, FP8, inner, outer, ld_bytes, box_inner, box_outer);
+}
+
+int oz_make_tmap_u8_sw64(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                         uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_2d(tm, base, FP8, inner, outer, ld_bytes, box_inner, box_outer, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 // N of the UMMA = k rounded up to a multiple of 32 (M=128 needs N % 16 == 0, N <= 256)

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 namespace ofrr {
 
@@ -445,6 +446,348 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Row scales of A only (the in-kernel slicing path below converts A on the fly).
+// ---------------------------------------------------------------------------------
+template <int FMT>
+__global__ void __launch_bounds__(256)
+    k_oz_rowscale(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, int* __restrict__ T) {
+  const int64_t i = blockIdx.x;
+  __shared__ uint32_t red[8];
+  if (i >= rows) {
+    if (threadIdx.x == 0) T[i] = 0;
+    return;
+  }
+  const int64_t base = i * lda;
+  const int eb = FMT == FP8 ? 1 : 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) + (uintptr_t)(base * eb)) & 15) == 0;
+  uint32_t m = 0;
+  for (int64_t l0 = 8 * (int64_t)threadIdx.x; l0 < cols; l0 += 8 * (int64_t)blockDim.x) {
+    float x[8];
+    oz_ld8<FMT>(A, base, l0, cols, vec, x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t b = __float_as_uint(x[e]) & 0x7fffffffu;
+      m = b > m ? b : m;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint32_t om = __shfl_xor_sync(0xffffffffu, m, o);
+    m = om > m ? om : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m = red[0];
+    for (int w = 1; w < 8; ++w) m = red[w] > m ? red[w] : m;
+    T[i] = oz_scale((double)__uint_as_float(m));
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// The int8 tensor-core product with the A digits made on the fly (no digit planes in HBM):
+// A is read once in its own format.  64-byte k-blocks (SWIZZLE_64B tiles: a full digit set
+// of one k-block is 6 x 8 KB), 8 converter warps turn the bf16/f16/e4m3 tile into the six
+// balanced base-256 digit tiles in shared memory (triple-buffered) while warp 1 issues the
+// tcgen05 int8 MMAs of the previous k-block and warp 0 streams the V digit tiles by TMA.
+// Same digits and exact integer level sums as k_oz_gemm: identical results.
+// ---------------------------------------------------------------------------------
+static constexpr int OZK_KB = 64;          // K elements (= int8 bytes) per k-block
+static constexpr int OZK_CONV_WARPS = 16;
+static constexpr int OZK_THREADS = 192 + 32 * OZK_CONV_WARPS;
+static constexpr int OZK_MAXCHUNK = 256;   // k-blocks per chunk (16384 terms)
+
+template <int BN>
+struct OzkCfg {
+  static constexpr int A_TILE = OZ_TM * OZK_KB;         // 8 KB per digit plane
+  static constexpr int A_SET = OZ_D * A_TILE;           // 48 KB per k-block
+  static constexpr int V_SET = OZ_D * BN * OZK_KB;      // six V digit tiles per k-block
+  static constexpr int A_STAGES = 3;
+  static constexpr int V_STAGES = 2;
+  static constexpr int TMEM_COLS = OZ_D * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = 1024 + A_STAGES * A_SET + V_STAGES * V_SET + 256;
+};
+
+// UMMA shared-memory descriptor: K-major, 64B swizzle, 8-row groups 512 B apart
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int FMT>
+__device__ __forceinline__ void ozk_load32(const void* A, int64_t off, bool ok_vec, int64_t l0, int64_t cols,
+                                           bool row_ok, uint4 (&raw)[4]) {
+  // 32 consecutive entries (64 B for 16-bit, 32 B for e4m3) of one row, zero outside
+  constexpr int EB = FMT == FP8 ? 1 : 2;
+  constexpr int NV = 32 * EB / 16;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) raw[v] = make_uint4(0, 0, 0, 0);
+  if (!row_ok) return;
+  if (ok_vec && l0 + 32 <= cols) {
+    const uint4* src = reinterpret_cast<const uint4*>((const uint8_t*)A + (off + l0) * EB);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) raw[v] = __ldcs(src + v);
+  } else {
+    uint8_t* dst = reinterpret_cast<uint8_t*>(raw);
+    for (int e = 0; e < 32; ++e) {
+      if (l0 + e < cols) {
+        if (EB == 2) {
+          const uint16_t h = ((const uint16_t*)A)[off + l0 + e];
+          dst[2 * e] = (uint8_t)h;
+          dst[2 * e + 1] = (uint8_t)(h >> 8);
+        } else {
+          dst[e] = ((const uint8_t*)A)[off + l0 + e];
+        }
+      }
+    }
+  }
+}
+template <int FMT>
+__device__ __forceinline__ float ozk_elem(const uint4 (&raw)[4], int e) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(raw);
+  if constexpr (FMT == BF16) {
+    return __uint_as_float(((w[e >> 1] >> (16 * (e & 1))) & 0xffffu) << 16);
+  } else if constexpr (FMT == F16) {
+    return __half2float(__ushort_as_half((uint16_t)(w[e >> 1] >> (16 * (e & 1)))));
+  } else {
+    __nv_fp8_e4m3 q;
+    q.__x = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
+    return float(q);
+  }
+}
+
+template <int FMT, int BN>
+__global__ void __launch_bounds__(OZK_THREADS, 1)
+    k_ozk_gemm(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, const int* __restrict__ Tg,
+               const __grid_constant__ CUtensorMap tmV, double* __restrict__ ws, int kbc, int nchunks,
+               long long total_units, int max_slots, int npad, int col0) {
+  using C = OzkCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* abuf = smem;                                  // [A_STAGES][6][128 x 64 B]
+  uint8_t* vbuf = smem + C::A_STAGES * C::A_SET;         // [V_STAGES][6][BN x 64 B]
+  uint64_t* afull = reinterpret_cast<uint64_t*>(vbuf + C::V_STAGES * C::V_SET);
+  uint64_t* aempty = afull + C::A_STAGES;
+  uint64_t* vfull = aempty + C::A_STAGES;
+  uint64_t* vempty = vfull + C::V_STAGES;
+  uint64_t* tfull = vempty + C::V_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long G = gridDim.x;
+  const long long u0 = (long long)blockIdx.x * total_units / G;
+  const long long u1 = ((long long)blockIdx.x + 1) * total_units / G;
+  const int vt_first = (int)(u0 / kbc);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::A_STAGES; ++s) { mbar_init(&afull[s], OZK_CONV_WARPS); mbar_init(&aempty[s], 1); }
+    for (int s = 0; s < C::V_STAGES; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_barrier_init();
+    prefetch_tmap(&tmV);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer: V digit tiles =====
+      const uint64_t pol_v = policy_evict_last();
+      int vs = 0;
+      uint32_t vph = 0;
+      for (long long u = u0; u < u1; ++u) {
+        const int vt = (int)(u / kbc);
+        const int kb = (vt % nchunks) * kbc + (int)(u % kbc);
+        mbar_wait(&vempty[vs], vph ^ 1);
+        mbar_expect_tx(&vfull[vs], C::V_SET);
+        for (int q = 0; q < OZ_D; ++q)
+          tma_load_2d(vbuf + vs * C::V_SET + q * BN * OZK_KB, &tmV, kb * OZK_KB, q * npad + col0, &vfull[vs], pol_v);
+        if (++vs == C::V_STAGES) { vs = 0; vph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      int as = 0, vs = 0;
+      uint32_t aph = 0, vph = 0, acc_phase = 0;
+      long long u = u0;
+      while (u < u1) {
+        const int vt = (int)(u / kbc);
+        const long long seg_end = std::min<long long>(u1, (long long)(vt + 1) * kbc);
+        const long long seg_start = u;
+        mbar_wait(tempty, acc_phase ^ 1);
+        tc_fence_after();
+        for (; u < seg_end; ++u) {
+          mbar_wait(&vfull[vs], vph);
+          mbar_wait(&afull[as], aph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(abuf + as * C::A_SET);
+          const uint64_t dv = umma_desc_sw64(smem_u32(vbuf + vs * C::V_SET));
+          for (int p = 0; p < OZ_D; ++p) {
+            const uint64_t da = umma_desc_sw64(sa + p * C::A_TILE);
+            const int nq = OZ_D - p;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const uint32_t acc = (u > seg_start || p > 0 || k > 0) ? 1u : 0u;
+              for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
+                const int ng = std::min(256 / BN, nq - q0);
+                mma_i8(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
+                       dv + (uint64_t)((q0 * BN * OZK_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN, true, true),
+                       acc);
+              }
+            }
+          }
+          tc_commit(&aempty[as]);
+          tc_commit(&vempty[vs]);
+          if (++as == C::A_STAGES) { as = 0; aph ^= 1; }
+          if (++vs == C::V_STAGES) { vs = 0; vph ^= 1; }
+        }
+        tc_commit(tfull);
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp < 6) {
+    // ===== epilogue warps 2..5: TMEM int32 levels -> fp64 partial tile (column-major) =====
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    uint32_t acc_phase = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int vt = (int)(u / kbc);
+      u = std::min<long long>(u1, (long long)(vt + 1) * kbc);
+      mbar_wait(tfull, acc_phase);
+      tc_fence_after();
+      double* dst = ws + ((size_t)blockIdx.x * max_slots + (vt - vt_first)) * (size_t)(OZ_TM * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        double s[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s[i] = 0.0;
+#pragma unroll 1
+        for (int lv = OZ_D - 1; lv >= 0; --lv) {
+          int d[16];
+          tmem_ld16i(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(lv * BN + c0), d);
+          const double w = ldexp(1.0, -8 * lv - 12);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) s[i] = fma((double)d[i], w, s[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dst[(size_t)(c0 + i) * OZ_TM + row] = s[i];
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+      acc_phase ^= 1;
+    }
+  } else {
+    // ===== converter warps: A tile (128 rows x 64 entries) -> six digit tiles ===========
+    // thread -> (row, 16-entry quarter of the k-block): one 16-byte chunk per digit plane
+    const int ct = threadIdx.x - 192;        // 0..511
+    const int r = ct >> 2, qt = ct & 3;
+    constexpr int EB = FMT == FP8 ? 1 : 2;
+    int as = 0;
+    uint32_t aph = 0;
+    int cur_vt = -1;
+    int E = 0;
+    float sc = 0.0f;
+    bool fast = false, row_ok = false;
+    uint4 nxt[2];
+    auto fetch = [&](long long u, uint4 (&raw)[2]) {
+      const int vt = (int)(u / kbc);
+      const int kb = (vt % nchunks) * kbc + (int)(u % kbc);
+      const int64_t grow = (int64_t)(vt / nchunks) * OZ_TM + r;
+      raw[0] = raw[1] = make_uint4(0, 0, 0, 0);
+      if (grow >= rows) return;
+      const int64_t o = grow * lda, l0 = (int64_t)kb * OZK_KB + qt * 16;
+      const uint8_t* src = (const uint8_t*)A + (o + l0) * EB;
+      if (l0 + 16 <= cols && ((reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        raw[0] = __ldcs(reinterpret_cast<const uint4*>(src));
+        if (EB == 2) raw[1] = __ldcs(reinterpret_cast<const uint4*>(src) + 1);
+      } else {
+        uint8_t* dst = reinterpret_cast<uint8_t*>(raw);
+        for (int e = 0; e < 16; ++e)
+          if (l0 + e < cols)
+            for (int bb = 0; bb < EB; ++bb) dst[EB * e + bb] = src[EB * e + bb];
+      }
+    };
+    if (u0 < u1) fetch(u0, nxt);
+    for (long long u = u0; u < u1; ++u) {
+      uint4 raw[4];
+      raw[0] = nxt[0];
+      raw[1] = nxt[1];
+      if (u + 1 < u1) fetch(u + 1, nxt);                 // prefetch the next k-block's entries
+      const int vt = (int)(u / kbc);
+      if (vt != cur_vt) {
+        cur_vt = vt;
+        const int64_t grow = (int64_t)(vt / nchunks) * OZ_TM + r;
+        row_ok = grow < rows;
+        E = row_ok ? Tg[grow] : 0;
+        fast = row_ok && E != OZ_BAD && 46 - E <= 127 && 46 - E >= -126;
+        sc = fast ? __int_as_float((46 - E + 127) << 23) : 0.0f;
+      }
+      uint32_t w[OZ_D][4];
+      if (fast) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t lo[4], hi[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const long long t = __float2ll_rz(ozk_elem<FMT>(raw, 4 * g + e) * sc);
+            lo[e] = (uint32_t)(unsigned long long)t;
+            hi[e] = (uint32_t)((unsigned long long)t >> 32);
+            oz_bias(lo[e], hi[e]);
+          }
+          uint32_t pw[OZ_D];
+          oz_planes4(lo, hi, pw);
+#pragma unroll
+          for (int p = 0; p < OZ_D; ++p) w[p][g] = pw[p];
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t lo[4], hi[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (row_ok && E != OZ_BAD) {
+              oz_fixed32(__float_as_uint(ozk_elem<FMT>(raw, 4 * g + e)), E, lo[e], hi[e]);
+            } else {
+              lo[e] = 0x80808080u;
+              hi[e] = 0x8080u;
+            }
+          }
+          uint32_t pw[OZ_D];
+          oz_planes4(lo, hi, pw);
+#pragma unroll
+          for (int p = 0; p < OZ_D; ++p) w[p][g] = pw[p];
+        }
+      }
+      mbar_wait(&aempty[as], aph ^ 1);
+      uint8_t* slot = abuf + as * C::A_SET;
+      const int pos = (r >> 3) * 512 + (r & 7) * 64 + ((qt ^ ((r >> 1) & 3)) << 4);
+#pragma unroll
+      for (int p = 0; p < OZ_D; ++p)
+        *reinterpret_cast<uint4*>(slot + p * C::A_TILE + pos) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[as]);
+      if (++as == C::A_STAGES) { as = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
 __device__ __forceinline__ long long oz_seg_begin(long long c, long long T, long long G) { return c * T / G; }
 
 // Sum the partials of row tile t over its K chunks and stream-K segments (fixed order),
@@ -592,9 +935,10 @@ static OzPlan oz_plan(int64_t rows, int64_t cols, int r) {
 size_t oz_op_ws(int64_t rows, int64_t cols) { return oz_plan(rows, cols, 1).op_bytes; }
 size_t oz_prod_ws(int64_t rows, int64_t cols, int r) { return oz_plan(rows, cols, r).bytes; }
 // one-shot workspace (operator + product) of the residual entry points
+size_t ozx_op_ws(int64_t rows, int64_t cols);
+size_t ozx_prod_ws(int64_t rows, int64_t cols, int r);
 size_t oz_ws(int64_t rows, int64_t cols, int r) {
-  const OzPlan p = oz_plan(rows, cols, r);
-  return ((p.op_bytes + 1023) & ~size_t(1023)) + p.bytes;
+  return ((ozx_op_ws(rows, cols) + 1023) & ~size_t(1023)) + ozx_prod_ws(rows, cols, r);
 }
 int oz_nblocks(int64_t rows) { return (int)((rows + OZ_TM - 1) / OZ_TM); }
 
@@ -674,17 +1018,140 @@ int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int
   return OFRR_OK;
 }
 
+// ---- in-kernel slicing path (default): operator workspace = row scales only ----------
+int oz_make_tmap_u8_sw64(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                         uint32_t box_inner, uint32_t box_outer);   // gemm_tc.cu
+
+static bool oz_use_planes() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("OFRR_OZ_PLANES"); v = (e && atoi(e) == 1) ? 1 : 0; }
+  return v == 1;
+}
+
+struct OzkPlan {
+  int bn, npass, npad, m_tiles, kblocks, nchunks, kbc, grid, max_slots;
+  int64_t rows_pad, cols_pad;
+  long long total;
+  size_t off_F, off_dig, off_ws, off_part, bytes;
+};
+
+static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r) {
+  OzkPlan p;
+  r = std::max(r, 1);
+  p.bn = r <= 32 ? 32 : 64;
+  p.npass = (r + p.bn - 1) / p.bn;
+  p.npad = p.npass * p.bn;
+  p.rows_pad = (rows + OZ_TM - 1) / OZ_TM * OZ_TM;
+  p.cols_pad = (cols + 15) / 16 * 16;
+  p.m_tiles = (int)(p.rows_pad / OZ_TM);
+  p.kblocks = (int)((cols + OZK_KB - 1) / OZK_KB);
+  p.nchunks = (p.kblocks + OZK_MAXCHUNK - 1) / OZK_MAXCHUNK;
+  p.kbc = (p.kblocks + p.nchunks - 1) / p.nchunks;
+  p.total = (long long)p.m_tiles * p.nchunks * p.kbc;
+  int sms = ofrr_device_sm_count(-1);
+  if (sms <= 0) sms = 148;
+  p.grid = (int)std::max<long long>(1, std::min<long long>(sms, p.total));
+  const long long per = (p.total + p.grid - 1) / p.grid;
+  p.max_slots = (int)((per + p.kbc - 1) / p.kbc) + 1;
+  size_t b = 0;
+  auto take = [&](size_t n) { size_t o = b; b += (n + 1023) & ~size_t(1023); return o; };
+  p.off_F = take((size_t)p.npad * 4);
+  p.off_dig = take((size_t)OZ_D * p.npad * p.cols_pad);
+  p.off_ws = take((size_t)p.grid * p.max_slots * OZ_TM * p.bn * sizeof(double));
+  p.off_part = take((size_t)p.m_tiles * r * sizeof(double));
+  p.bytes = b;
+  return p;
+}
+
+template <int FMT, int BN>
+static int ozk_launch(const void* A, int64_t rows, int64_t cols, int64_t lda, const int* T, const CUtensorMap& tV,
+                      const OzkPlan& p, double* ws, int col0, cudaStream_t st) {
+  using C = OzkCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_ozk_gemm<FMT, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+    attr = true;
+  }
+  k_ozk_gemm<FMT, BN><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc, p.nchunks,
+                                                                 p.total, p.max_slots, p.npad, col0);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+size_t ozx_op_ws(int64_t rows, int64_t cols) {
+  return oz_use_planes() ? oz_plan(rows, cols, 1).op_bytes : (size_t)((rows + OZ_TM - 1) / OZ_TM * OZ_TM) * 4 + 1024;
+}
+size_t ozx_prod_ws(int64_t rows, int64_t cols, int r) {
+  return oz_use_planes() ? oz_plan(rows, cols, r).bytes : ozk_plan(rows, cols, r).bytes;
+}
+
+int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws, size_t op_bytes,
+                cudaStream_t st) {
+  if (oz_use_planes()) return oz_prepare(A, rows, cols, lda, a_fmt, op_ws, op_bytes, st);
+  if (a_fmt != BF16 && a_fmt != F16 && a_fmt != FP8) {
+    ofrr_set_error("ozaki: A format %d not supported (16/8-bit operators)", a_fmt);
+    return OFRR_ERR_UNSUPPORTED;
+  }
+  if (!op_ws || op_bytes < ozx_op_ws(rows, cols)) { ofrr_set_error("ozaki: operator workspace too small"); return OFRR_ERR_INVALID; }
+  const unsigned g = (unsigned)((rows + OZ_TM - 1) / OZ_TM * OZ_TM);
+  int* T = (int*)op_ws;
+  if (a_fmt == BF16) k_oz_rowscale<BF16><<<g, 256, 0, st>>>(A, rows, cols, lda, T);
+  else if (a_fmt == F16) k_oz_rowscale<F16><<<g, 256, 0, st>>>(A, rows, cols, lda, T);
+  else k_oz_rowscale<FP8><<<g, 256, 0, st>>>(A, rows, cols, lda, T);
+  OFRR_CHECK_LAUNCH();
+  return OFRR_OK;
+}
+
+int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws, const double* V,
+              int64_t ldv, int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W,
+              int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
+              double** part_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (oz_use_planes())
+    return oz_apply(op_ws, rows, cols, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, out_fmt, colmax, flags, W2, ldw2,
+                    out_fmt2, part_out, ws, ws_bytes, st);
+  const OzkPlan p = ozk_plan(rows, cols, r);
+  if (p.nchunks > 16) { ofrr_set_error("ozaki: cols=%lld beyond 16 chunks", (long long)cols); return OFRR_ERR_UNSUPPORTED; }
+  if (!ws || ws_bytes < p.bytes) { ofrr_set_error("ozaki: workspace too small (%zu < %zu)", ws_bytes, p.bytes); return OFRR_ERR_INVALID; }
+  const int* T = (const int*)op_ws;
+  uint8_t* base = (uint8_t*)ws;
+  int* F = (int*)(base + p.off_F);
+  int8_t* dig = (int8_t*)(base + p.off_dig);
+  double* pws = (double*)(base + p.off_ws);
+  double* part = (double*)(base + p.off_part);
+  k_oz_slices_v<<<(unsigned)p.npad, 256, 0, st>>>(V, ldv, cols, r, F, dig, p.npad, p.cols_pad);
+  OFRR_CHECK_LAUNCH();
+  CUtensorMap tV;
+  int rc = oz_make_tmap_u8_sw64(&tV, dig, (uint64_t)cols, (uint64_t)OZ_D * p.npad, (uint64_t)p.cols_pad, OZK_KB,
+                                (uint32_t)p.bn);
+  if (rc) return rc;
+  for (int ps = 0; ps < p.npass; ++ps) {
+    const int j0 = ps * p.bn;
+#define OZK_CASE(F)                                                                              \
+    rc = p.bn == 32 ? ozk_launch<F, 32>(A, rows, cols, lda, T, tV, p, pws, j0, st)               \
+                    : ozk_launch<F, 64>(A, rows, cols, lda, T, tV, p, pws, j0, st);
+    if (a_fmt == BF16) { OZK_CASE(BF16) } else if (a_fmt == F16) { OZK_CASE(F16) } else { OZK_CASE(FP8) }
+#undef OZK_CASE
+    if (rc) return rc;
+    k_oz_resid<<<p.m_tiles, OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
+                                           std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2);
+    OFRR_CHECK_LAUNCH();
+  }
+  if (part_out) *part_out = part;
+  return OFRR_OK;
+}
+
 // one-shot residual product (prepare + apply in one workspace)
 int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const double* V, int64_t ldv,
                int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, double* W, int64_t ldw,
                double** part_out, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const OzPlan p = oz_plan(rows, cols, r);
-  const size_t opb = (p.op_bytes + 1023) & ~size_t(1023);
-  if (!ws || ws_bytes < opb + p.bytes) { ofrr_set_error("ozaki product: workspace too small (%zu < %zu)", ws_bytes, opb + p.bytes); return OFRR_ERR_INVALID; }
-  int rc = oz_prepare(A, rows, cols, lda, a_fmt, ws, opb, st);
+  const size_t opb = (ozx_op_ws(rows, cols) + 1023) & ~size_t(1023);
+  const size_t pb = ozx_prod_ws(rows, cols, r);
+  if (!ws || ws_bytes < opb + pb) { ofrr_set_error("ozaki product: workspace too small (%zu < %zu)", ws_bytes, opb + pb); return OFRR_ERR_INVALID; }
+  int rc = ozx_prepare(A, rows, cols, lda, a_fmt, ws, opb, st);
   if (rc) return rc;
-  return oz_apply(ws, rows, cols, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, F64, nullptr, nullptr, nullptr, 0, F64,
-                  part_out, (uint8_t*)ws + opb, ws_bytes - opb, st);
+  return ozx_apply(A, rows, cols, lda, a_fmt, ws, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, F64, nullptr, nullptr,
+                   nullptr, 0, F64, part_out, (uint8_t*)ws + opb, ws_bytes - opb, st);
 }
 
 }  // namespace ofrr

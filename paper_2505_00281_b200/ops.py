@@ -269,7 +269,8 @@ def ozaki_gemm(oz: OzakiOperator, X: DevBlock, W: DevBlock, colmax=None, flags=N
     if X.fmt != FpFormat.F64:
         raise ValueError("ozaki_gemm: the block must be fp64")
     ws = _ws(L.ofrr_ozaki_workspace(A.rows, A.cols, X.k), A.device)
-    _lib.check(L.ofrr_ozaki_gemm(oz.ws.data_ptr(), A.rows, A.cols, X.ptr, X.ld, X.k, W.ptr, W.ld, int(W.fmt),
+    _lib.check(L.ofrr_ozaki_gemm(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), oz.ws.data_ptr(), X.ptr, X.ld, X.k, W.ptr,
+                                 W.ld, int(W.fmt),
                                  _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
                                  W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else int(W.fmt),
                                  ws.data_ptr(), ws.numel(), _stream()), "ozaki_gemm")
@@ -281,7 +282,8 @@ def ozaki_residual(oz: OzakiOperator, Xv: DevBlock, Yv: DevBlock, vals: torch.Te
     L = _lib.load()
     A = oz.A
     ws = _ws(L.ofrr_ozaki_workspace(A.rows, A.cols, r_max), A.device)
-    _lib.check(L.ofrr_ozaki_residual(oz.ws.data_ptr(), A.rows, A.cols, Xv.ptr, Xv.ld, Yv.ptr, Yv.ld, vals.data_ptr(),
+    _lib.check(L.ofrr_ozaki_residual(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), oz.ws.data_ptr(), Xv.ptr, Xv.ld, Yv.ptr,
+                                     Yv.ld, vals.data_ptr(),
                                      _p(r_dev), r_max, res.data_ptr(), int(accumulate_max), ws.data_ptr(), ws.numel(),
                                      _stream()), "ozaki_residual")
     _count(3 + (r_max + 63) // 64 * 2)
