@@ -739,10 +739,10 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
           uint32_t lo[4], hi[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const long long t = __float2ll_rz(ozk_elem<FMT>(raw, 4 * g + e) * sc);
-            lo[e] = (uint32_t)(unsigned long long)t;
-            hi[e] = (uint32_t)((unsigned long long)t >> 32);
-            oz_bias(lo[e], hi[e]);
+            const unsigned long long t =
+                (unsigned long long)__float2ll_rz(ozk_elem<FMT>(raw, 4 * g + e) * sc) + 0x808080808080ull;
+            lo[e] = (uint32_t)t;
+            hi[e] = (uint32_t)(t >> 32);
           }
           uint32_t pw[OZ_D];
           oz_planes4(lo, hi, pw);
@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(OZ_TM)
     c_lo[ch] = lo;
     c_hi[ch] = hi;
   }
-  for (int jb = 0; jb < ncols; jb += 16) {
+  for (int jb = 16 * blockIdx.y; jb < ncols; jb += 16 * gridDim.y) {   // 16 columns per y-block
     double s[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) s[q] = 0.0;
@@ -1009,7 +1009,7 @@ int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int
     const int j0 = ps * p.bn;
     rc = p.bn == 32 ? oz_launch<32>(tA, tV, p, pws, j0, st) : oz_launch<64>(tA, tV, p, pws, j0, st);
     if (rc) return rc;
-    k_oz_resid<<<p.m_tiles, OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
+    k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
                                            ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2);
     OFRR_CHECK_LAUNCH();
@@ -1132,7 +1132,7 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     if (a_fmt == BF16) { OZK_CASE(BF16) } else if (a_fmt == F16) { OZK_CASE(F16) } else { OZK_CASE(FP8) }
 #undef OZK_CASE
     if (rc) return rc;
-    k_oz_resid<<<p.m_tiles, OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
+    k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
                                            ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2);
     OFRR_CHECK_LAUNCH();
