@@ -82,6 +82,7 @@ __device__ __forceinline__ double to_d(double x) { return x; }
 __device__ __forceinline__ double to_d(float x) { return (double)x; }
 __device__ __forceinline__ double to_d(__half x) { return (double)__half2float(x); }
 __device__ __forceinline__ double to_d(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
+__device__ __forceinline__ double to_d(__nv_fp8_e4m3 x) { return (double)float(x); }
 template <typename T> __device__ __forceinline__ T from_d(double v);
 template <> __device__ __forceinline__ double from_d<double>(double v) { return v; }
 template <> __device__ __forceinline__ float from_d<float>(double v) { return (float)v; }

@@ -129,6 +129,7 @@ int gram(const void* U, int64_t ldu, const void* W, int64_t ldw, int64_t n, int 
     case F32: return launch_gram<float>(U, ldu, W, ldw, n, k, kw, out_fmt, G1, G2, flags, part, st);
     case F16: return launch_gram<__half>(U, ldu, W, ldw, n, k, kw, out_fmt, G1, G2, flags, part, st);
     case BF16: return launch_gram<__nv_bfloat16>(U, ldu, W, ldw, n, k, kw, out_fmt, G1, G2, flags, part, st);
+    case FP8: return launch_gram<__nv_fp8_e4m3>(U, ldu, W, ldw, n, k, kw, out_fmt, G1, G2, flags, part, st);
     default: ofrr_set_error("gram: storage format %d unsupported", storage); return OFRR_ERR_UNSUPPORTED;
   }
 }

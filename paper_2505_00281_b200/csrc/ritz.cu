@@ -74,6 +74,7 @@ int ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const
     case F32: k_ritz<float><<<grid, 256, 0, st>>>((const float*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
     case F16: k_ritz<__half><<<grid, 256, 0, st>>>((const __half*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
     case BF16: k_ritz<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
+    case FP8: k_ritz<__nv_fp8_e4m3><<<grid, 256, 0, st>>>((const __nv_fp8_e4m3*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
     default: ofrr_set_error("ritz: basis format %d unsupported", u_fmt); return OFRR_ERR_UNSUPPORTED;
   }
   OFRR_CHECK_LAUNCH();

@@ -99,7 +99,7 @@ def test_ofrr_svd_golden(ofrr_gpu, golden):
     np.testing.assert_allclose(rs.right_vectors.data, golden["ofrrsvd/vv"], rtol=1e-7, atol=1e-8)
 
 
-@pytest.mark.parametrize("fmt", ["tc-bf16", "tc-f16", "full-f32"])
+@pytest.mark.parametrize("fmt", ["tc-bf16", "tc-f16", "full-f32", "tc-fp8"])
 def test_driver_eig_vs_oracle_geometric(ofrr_gpu, oracle, fmt):
     """C1/C2-style problem at oracle-feasible size: geometric spectrum, n=1024 (WHT
     generator), top 10, k 20: same synthetic A, same X0, same policy."""
