@@ -13,7 +13,7 @@ from .comm import Comm
 from .driver import IterConfig, RunStats, subspace_iter_eig, subspace_iter_svd
 from .errors import ConvergenceError, EmptyBasisError, EmptyPencilError, OverflowDiagnostic
 from .matrix import (DenseMatrix, clustered_spectrum, geometric_spectrum, sym_factors,
-                     synthetic_symmetric, to_dense_f64)
+                     synthetic_lowrank, synthetic_symmetric, to_dense_f64)
 from .precision import (FULL_F32, FULL_F64, MIXED_HALF, NATIVE_F16, POLICY_PRESETS, TC_BF16, TC_F16,
                         TC_FP8, FpFormat, PrecisionPolicy, projection_policy, round_to)
 from .projection import POSITIVE_EIG_TOL, RitzSet, ofrr_eig, ofrr_svd, residual_report
@@ -34,7 +34,7 @@ __all__ = [
     "BasisFactorization", "BasisMethod", "EmptyBasisError", "build_basis", "hessenberg_basis",
     "IterConfig", "RunStats", "subspace_iter_eig", "subspace_iter_svd",
     "DenseMatrix", "to_dense_f64", "geometric_spectrum", "clustered_spectrum", "sym_factors",
-    "synthetic_symmetric",
+    "synthetic_symmetric", "synthetic_lowrank",
     "FULL_F32", "FULL_F64", "MIXED_HALF", "NATIVE_F16", "TC_F16", "TC_BF16", "TC_FP8", "POLICY_PRESETS",
     "FpFormat", "PrecisionPolicy", "round_to", "projection_policy",
     "EmptyPencilError", "OverflowDiagnostic", "RitzSet", "ofrr_eig", "ofrr_svd", "residual_report",

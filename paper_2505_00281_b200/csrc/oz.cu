@@ -809,26 +809,26 @@ __global__ void __launch_bounds__(OZ_TM)
   const bool valid = grow < rows;
   const int Ti = valid ? T[grow] : 0;
   const int nvalid = r_dev ? min(j0 + ncols, *r_dev) : j0 + ncols;
-  // segments covering the tile's units, per chunk, ascending
-  long long c_lo[16], c_hi[16];
-  for (int ch = 0; ch < nchunks && ch < 16; ++ch) {
+  // segments covering the tile's units, per chunk, ascending (found on the fly per chunk)
+  auto seg_range = [&](int ch, long long& lo, long long& hi) {
     const long long vt = (long long)t * nchunks + ch;
     const long long x0 = vt * kbc, x1 = x0 + kbc - 1;
-    long long lo = x0 * G / total_units, hi = x1 * G / total_units;
+    lo = x0 * G / total_units;
+    hi = x1 * G / total_units;
     while (lo + 1 < G && oz_seg_begin(lo + 1, total_units, G) <= x0) ++lo;
     while (lo > 0 && oz_seg_begin(lo, total_units, G) > x0) --lo;
     while (hi + 1 < G && oz_seg_begin(hi + 1, total_units, G) <= x1) ++hi;
     while (hi > 0 && oz_seg_begin(hi, total_units, G) > x1) --hi;
-    c_lo[ch] = lo;
-    c_hi[ch] = hi;
-  }
+  };
   for (int jb = 16 * blockIdx.y; jb < ncols; jb += 16 * gridDim.y) {   // 16 columns per y-block
     double s[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) s[q] = 0.0;
     for (int ch = 0; ch < nchunks; ++ch) {
       const long long vt = (long long)t * nchunks + ch;
-      for (long long c = c_lo[ch]; c <= c_hi[ch]; ++c) {
+      long long c_lo, c_hi;
+      seg_range(ch, c_lo, c_hi);
+      for (long long c = c_lo; c <= c_hi; ++c) {
         const int slot = (int)(vt - oz_seg_begin(c, total_units, G) / kbc);
         const double* src = ws + ((size_t)c * max_slots + slot) * (size_t)(OZ_TM * BN) + row;
 #pragma unroll
@@ -966,7 +966,6 @@ int oz_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
     return OFRR_ERR_UNSUPPORTED;
   }
   const OzPlan p = oz_plan(rows, cols, 1);
-  if (p.nchunks > 16) { ofrr_set_error("ozaki: cols=%lld beyond 16 chunks", (long long)cols); return OFRR_ERR_UNSUPPORTED; }
   if (!op_ws || op_bytes < p.op_bytes) { ofrr_set_error("ozaki: operator workspace too small (%zu < %zu)", op_bytes, p.op_bytes); return OFRR_ERR_INVALID; }
   uint8_t* base = (uint8_t*)op_ws;
   int* T = (int*)(base + p.op_T);
@@ -1110,7 +1109,6 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     return oz_apply(op_ws, rows, cols, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, out_fmt, colmax, flags, W2, ldw2,
                     out_fmt2, part_out, ws, ws_bytes, st);
   const OzkPlan p = ozk_plan(rows, cols, r);
-  if (p.nchunks > 16) { ofrr_set_error("ozaki: cols=%lld beyond 16 chunks", (long long)cols); return OFRR_ERR_UNSUPPORTED; }
   if (!ws || ws_bytes < p.bytes) { ofrr_set_error("ozaki: workspace too small (%zu < %zu)", ws_bytes, p.bytes); return OFRR_ERR_INVALID; }
   const int* T = (const int*)op_ws;
   uint8_t* base = (uint8_t*)ws;

@@ -356,3 +356,44 @@ def synthetic_symmetric(lam: np.ndarray, fmt: FpFormat, seed: int = 20240901, r:
     op = ops.new_operator(rows, n, fmt, device)
     ops.generate_sym(op, row0, f.hadamard, f.c, f.s, f.Wf, f.Mf)
     return DenseMatrix.on_device(op), f
+
+
+def synthetic_lowrank(n1: int, n2: int, fmt: FpFormat, r: int = 256, rho: float = 0.9, nu_rel: float = 1e-4,
+                      seed: int = 20240901, device=None, row0: int = 0, rows: Optional[int] = None):
+    """C4: A = G1 diag(sigma) G2^T + nu N, G1 (n1 x r) and G2 (n2 x r) with
+    orthonormal seeded Gaussian columns, sigma_i = rho^i, nu = nu_rel * sigma_1, N i.i.d.
+    N(0,1)/sqrt(n2); built on the device in fp32 (torch, input generation only -- outside any
+    timed region) and rounded once to ``fmt``.  ``row0``/``rows``: this rank's row block
+    (G1 is generated in full from the seed, so row blocks agree across ranks).
+
+    Returns (DenseMatrix on device, sigma)."""
+    import torch
+    from . import ops
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    rows = n1 - row0 if rows is None else rows
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    g1, _ = torch.linalg.qr(torch.randn(n1, r, generator=g, device=device, dtype=torch.float32))
+    g2, _ = torch.linalg.qr(torch.randn(n2, r, generator=g, device=device, dtype=torch.float32))
+    sigma = rho ** np.arange(r, dtype=np.float64)
+    sig_t = torch.tensor(sigma, dtype=torch.float32, device=device)
+    op = ops.new_operator(rows, n2, fmt, device)
+    nu = nu_rel * float(sigma[0])
+    # rows of A in globally aligned slabs of 4096 rows (bounded fp32 temporaries); the noise
+    # of a slab comes from a stream keyed by its global index, so any row partition agrees
+    SL = 4096
+    for gs in range((row0 // SL) * SL, row0 + rows, SL):
+        ge = min(n1, gs + SL)
+        lo, hi = max(gs, row0), min(ge, row0 + rows)
+        if lo >= hi:
+            continue
+        gn = torch.Generator(device=device)
+        gn.manual_seed(seed * 1_000_003 + gs // SL)
+        noise = torch.randn(ge - gs, n2, generator=gn, device=device, dtype=torch.float32)
+        blk = (g1[lo:hi] * sig_t) @ g2.T
+        blk += (nu / np.sqrt(n2)) * noise[lo - gs: hi - gs]
+        op.t[lo - row0: hi - row0, :n2].copy_(blk.to(FpFormat(fmt).torch_dtype))
+        del blk, noise
+    del g1, g2
+    return DenseMatrix.on_device(op), sigma
