@@ -46,6 +46,14 @@ CONFIGS = {
                    name="synthetic dense symmetric 16384x16384 (bf16 operator), geometric spectrum, top-32, k=64, "
                         "to 1e-8: fp64 basis with FP64-accurate products on the int8 tensor cores (Ozaki "
                         "digit planes) / fp64 Gram"),
+    "c2-ladder": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-8, policy="full-f64", ladder="full-f32",
+                      name="synthetic dense symmetric 16384x16384 (bf16 operator), geometric spectrum, top-32, "
+                           "k=64, to 1e-8 by a precision ladder: fp32 basis on the bf16 tensor cores until the "
+                           "estimate reaches 1e-3, then fp64 basis with int8 Ozaki products"),
+    "c3-ladder": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64", ladder="full-f32",
+                      name="synthetic dense symmetric 65536x65536 (bf16 operator), geometric spectrum, top-64, "
+                           "k=128, to 1e-8 (north-star target) by a precision ladder: fp32 basis on the bf16 "
+                           "tensor cores, then fp64 basis with int8 Ozaki products"),
     "c3-f64": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
                    name="synthetic dense symmetric 65536x65536 (bf16 operator), geometric spectrum, top-64, "
                         "k=128, to 1e-8 (the north-star target): fp64 basis, FP64-accurate int8 tensor-core "
@@ -243,7 +251,8 @@ def run_ours(args, cfg):
     r0, r1 = comm.row_range(n)
     A, _ = p.synthetic_symmetric(lam, fmt, seed=SEED, device=dev, row0=r0, rows=r1 - r0)
     icfg = p.IterConfig(k=k, m=MAX_OUTER, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
-                        policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=tol, top=top)
+                        policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=tol, top=top,
+                        ladder=p.POLICY_PRESETS[cfg["ladder"]] if cfg.get("ladder") else None)
 
     def solve(stats=None):
         return p.subspace_iter_eig(A, icfg, stats=stats, comm=comm, n_global=n)

@@ -50,6 +50,8 @@ class IterConfig:
     seed: int = 0
     tol: Optional[float] = None   # extension: stop when max residual over `top` < tol
     top: Optional[int] = None     # extension: number of leading pairs checked
+    ladder: Optional[PrecisionPolicy] = None   # extension: cheaper policy run first (see below)
+    ladder_switch: float = 1e-3   # ... until its residual estimate falls below this (or stalls)
 
     def __post_init__(self):
         if self.k < 1 or self.m < 1 or self.iter < 1 or self.restarts < 0:
@@ -60,6 +62,8 @@ class IterConfig:
             raise ValueError("policy is required")
         if self.top is not None and not (1 <= self.top <= self.k):
             raise ValueError("top must be in [1, k]")
+        if self.ladder is not None and self.tol is None:
+            raise ValueError("a precision ladder needs tol (it switches on the residual estimate)")
 
     @property
     def mv_policy(self) -> PrecisionPolicy:
@@ -297,15 +301,24 @@ class EigEngine:
         return r
 
     # ---- the outer loop -----------------------------------------------------------------
-    def run(self) -> RitzSet:
+    def run(self, X0=None, stop_estimate: Optional[float] = None):
         """The outer loop (ofrr/driver.py:101-111).  With cfg.tol the loop stops at the
         first iteration whose leading `top` residuals pass: the cheap estimate (K7e)
         nominates, the FP64 residual report (K7) confirms; the returned residuals are
-        always the FP64 ones."""
+        always the FP64 ones.
+
+        Ladder rung (``stop_estimate``): return the restart block (no report) as soon as
+        the estimate falls below ``stop_estimate`` or stalls; ``X0`` starts from a block."""
         cfg = self.cfg
         tol, top = cfg.tol, (cfg.top or cfg.k)
         check = tol is not None
-        X = self.start_block()
+        if X0 is None:
+            X = self.start_block()
+        elif X0.fmt != self.mv.storage:
+            X = self.ops.new_block(X0.n, X0.k, self.mv.storage, self.device)
+            self.ops.convert(X0, X)                               # exact widening (f32 -> f64)
+        else:
+            X = X0
         eig = U64 = U = None
         r = 0
         rs = vals = None
@@ -350,6 +363,13 @@ class EigEngine:
                 # floor it can stall above a tolerance the FP64 residuals already meet, so a
                 # stalled estimate within 16x of tol is confirmed in FP64 as well
                 stalled = prev_est is not None and worst > 0.5 * prev_est and worst < 16.0 * tol
+                if stop_estimate is not None:
+                    rung_done = worst < stop_estimate or (prev_est is not None and worst > 0.5 * prev_est)
+                    prev_est = worst
+                    self.stats.history.append((it + 1, worst))
+                    if rung_done and not last:
+                        return X                                   # next rung starts from here
+                    continue
                 prev_est = worst
                 if worst < tol or stalled or last:
                     rs = self._final_report(out, U, eig, kp, r, vals, check, top)   # FP64 confirmation
@@ -550,10 +570,28 @@ def subspace_iter_eig(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats]
     n = int(n_global if n_global is not None else a.rows)
     if cfg.k > n:
         raise ValueError("k exceeds the operator dimension")
+    X0 = None
+    hist, iters, passes = [], 0, 0
+    if cfg.ladder is not None:
+        # precision ladder: run the cheaper policy while it makes
+        # progress, then continue from its restart block in cfg.policy
+        from dataclasses import replace as _replace
+        low = _replace(cfg, policy=cfg.ladder, matvec_policy=None, ladder=None)
+        eng0 = EigEngine(a, low, comm=comm, n_global=n)
+        X0 = eng0.run(stop_estimate=cfg.ladder_switch)
+        if isinstance(X0, RitzSet):                                # m exhausted in the low rung
+            if stats is not None:
+                stats.__dict__.update(eng0.stats.__dict__)
+            return X0
+        hist, iters, passes = list(eng0.stats.history), eng0.stats.iterations, eng0.stats.a_passes
+        cfg = _replace(cfg, ladder=None, m=max(1, cfg.m - iters))
     eng = EigEngine(a, cfg, comm=comm, n_global=n)
-    rs = eng.run()
+    rs = eng.run(X0=X0)
     if stats is not None:
         stats.__dict__.update(eng.stats.__dict__)
+        stats.iterations += iters
+        stats.a_passes += passes
+        stats.history = hist + [(it + iters, w) for it, w in eng.stats.history]
     return rs
 
 
