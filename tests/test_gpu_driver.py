@@ -186,6 +186,24 @@ def test_driver_eig_fp64_basis_on_bf16_operator(ofrr_gpu, oracle):
     assert ops.OZAKI_FMTS
 
 
+def test_driver_precision_ladder(ofrr_gpu):
+    """IterConfig.ladder: fp32 basis on the bf16 tensor cores first, then the fp64 rung
+    (int8 Ozaki products) from its restart block, to a 1e-9 FP64 residual."""
+    p = ofrr_gpu
+    n, top, k = 4096, 16, 32
+    lam = p.geometric_spectrum(n, top, k)
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    cfg = p.IterConfig(k=k, m=40, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.FULL_F64, ladder=p.FULL_F32, ladder_switch=1e-3, seed=SEED, tol=1e-9, top=top)
+    st = p.RunStats()
+    rs = p.subspace_iter_eig(A, cfg, stats=st)
+    assert st.converged and np.max(rs.residuals[:top]) < 1e-9
+    assert rs.vectors.data.dtype == np.float64
+    np.testing.assert_allclose(rs.values[:top], lam[:top], rtol=1e-2)   # A is bf16-rounded
+    its = [i for i, _ in st.history]
+    assert its == sorted(its) and st.iterations == its[-1]
+
+
 def test_ozaki_gemm_vs_fp64(ofrr_gpu, oracle):
     """ofrr_ozaki_gemm: W = A X (fp64 X, bf16 A) to ~1e-14 of the FP64 product; column
     inf-norms and the fp32 second output."""

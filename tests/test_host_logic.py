@@ -98,6 +98,8 @@ def test_iterconfig_validation():
         p.IterConfig(k=2)
     with pytest.raises(ValueError):
         p.IterConfig(k=4, policy=p.FULL_F64, top=5)
+    with pytest.raises(ValueError):   # a ladder switches on the residual estimate: needs tol
+        p.IterConfig(k=4, policy=p.FULL_F64, ladder=p.FULL_F32)
     cfg = p.IterConfig(k=2, policy=p.FULL_F64)
     assert cfg.mv_policy is p.FULL_F64 and cfg.m == 1 and cfg.iter == 1 and cfg.seed == 0
     assert cfg.basis_method is p.BasisMethod.MGS_LEFT and cfg.projection == "rr"   # reference defaults
