@@ -241,8 +241,10 @@ __global__ void __launch_bounds__(PT, 1)
   __syncthreads();
   pc_mark(4);
   // ---- 1. Householder tridiagonalisation (reflector j stored in column j, rows > j) ----
-  // two barriers per column: [matvec p = tau S u, per-warp K partials] | [rank-2 update,
-  // the next column's norm by the warp that owns it]
+  // Column-owner layout: warp w owns the trailing columns c = j+1+w, j+1+w+16, ...; the
+  // symmetric matvec p_c = tau S[:, c] . u is a warp dot product over the owner's column,
+  // the rank-2 update touches only the owner's columns.  Two barriers per column.
+  constexpr int RT = (PK_MAX + 31) / 32;                               // rows per lane
   if (warp == 0 && k > 2) {
     double s2 = 0.0;
     for (int i = 1 + lane; i < k; i += 32) s2 = fma(S[i], S[i], s2);
@@ -260,37 +262,30 @@ __global__ void __launch_bounds__(PT, 1)
     const double tj = skip ? 0.0 : 2.0 / unorm2;
     const double u0 = x0 - alpha;                                        // u[j+1]; u[i>j+1] = S[j, i]
     const int j1 = j + 1;
+    // u in registers: lane holds u_i for i = j1 + lane + 32 t
+    double ur[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int i = j1 + lane + 32 * t;
+      ur[t] = i < k ? (i == j1 ? u0 : S[j * ld + i]) : 0.0;
+    }
     if (!skip) {
-      // p_i = tau sum_l S[i, l] u_l: four threads per row i, interleaved l
-      for (int r0 = 0; r0 < k - j1; r0 += PT / 4) {                  // uniform trip count
-        const int i = j1 + r0 + quad;
+      double kpart = 0.0;
+      for (int c = j1 + warp; c < k; c += PNW) {
+        const double* col = S + c * ld;
         double sum = 0.0;
-        if (i < k) {
-          // l = j1 (u = u0) on lane 0 of the quad; l > j1 interleaved over the quad
-          double a0 = ql == 0 ? S[j1 * ld + i] * u0 : 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          int l = j1 + 1 + ql;
-          for (; l + 12 < k; l += 16) {
-            a0 = fma(S[l * ld + i], S[j * ld + l], a0);
-            a1 = fma(S[(l + 4) * ld + i], S[j * ld + l + 4], a1);
-            a2 = fma(S[(l + 8) * ld + i], S[j * ld + l + 8], a2);
-            a3 = fma(S[(l + 12) * ld + i], S[j * ld + l + 12], a3);
-          }
-          for (; l < k; l += 4) a0 = fma(S[l * ld + i], S[j * ld + l], a0);
-          sum = (a0 + a1) + (a2 + a3);
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int i = j1 + lane + 32 * t;
+          if (i < k) sum = fma(col[i], ur[t], sum);
         }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        double kp = 0.0;
-        if (i < k) {
-          const double pi = tj * sum;
-          if (ql == 0) pv[i] = pi;
-          kp = ql == 0 ? (i == j1 ? u0 : S[j * ld + i]) * pi : 0.0;
-        }
-        kp += __shfl_xor_sync(0xffffffffu, kp, 4);
-        kp += __shfl_xor_sync(0xffffffffu, kp, 8);
-        kp += __shfl_xor_sync(0xffffffffu, kp, 16);
-        if (lane == 0) red[warp] = (r0 == 0 ? 0.0 : red[warp]) + kp;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const double pc = tj * sum;
+        if (lane == 0) pv[c] = pc;
+        kpart = fma(c == j1 ? u0 : S[j * ld + c], pc, kpart);
       }
+      if (lane == 0) red[warp] = kpart;
     }
     if (threadIdx.x == 0) {
       dd[j] = S[j * ld + j];
@@ -301,37 +296,30 @@ __global__ void __launch_bounds__(PT, 1)
     if (threadIdx.x == 0 && !skip) S[j * ld + j1] = u0;                 // reflector in place
     if (!skip) {
       double ksum = 0.0;
+#pragma unroll
       for (int w = 0; w < PNW; ++w) ksum += red[w];
       const double K = 0.5 * tj * ksum;
-      constexpr int RT = (PK_MAX + 31) / 32;                             // rows per lane
-      double ur[RT], qr[RT];
+      double qr[RT];
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const int i = j1 + lane + 32 * t;
-        ur[t] = i < k ? (i == j1 ? u0 : S[j * ld + i]) : 0.0;
         qr[t] = i < k ? pv[i] - K * ur[t] : 0.0;
       }
-      for (int l = j1 + warp; l < k; l += PNW) {
-        const double ul = l == j1 ? u0 : S[j * ld + l];
-        const double qlv = pv[l] - K * ul;
-        double* col = S + l * ld;
-        double v[RT];
-#pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int i = j1 + lane + 32 * t;
-          v[t] = i < k ? col[i] : 0.0;
-        }
+      for (int c = j1 + warp; c < k; c += PNW) {
+        const double uc = c == j1 ? u0 : S[j * ld + c];
+        const double qc = pv[c] - K * uc;
+        double* col = S + c * ld;
         double s2 = 0.0;
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
           const int i = j1 + lane + 32 * t;
           if (i < k) {
-            const double nv = v[t] - (ur[t] * qlv + qr[t] * ul);
+            const double nv = col[i] - (ur[t] * qc + qr[t] * uc);
             col[i] = nv;
-            if (i > l) s2 = fma(nv, nv, s2);
+            if (i > c) s2 = fma(nv, nv, s2);
           }
         }
-        if (l == j1) {                                                   // norm of the next column
+        if (c == j1) {                                                   // norm of the next column
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
           if (lane == 0) s_norm2 = s2;
@@ -405,71 +393,39 @@ __global__ void __launch_bounds__(PT, 1)
   __syncthreads();
   pc_mark(6);
   for (int i = threadIdx.x; i < k; i += PT) lam_g[i] = lam[i];
-  if (threadIdx.x == 0 && k >= 2) S[(k - 1) * ld + k - 1] = 1.0;     // the 1 x 1 seed block
-  __syncthreads();
-  // ---- 3. Q = H_0 H_1 ... H_{k-3} formed in place (backward accumulation) -------------
-  // Before step j the block Q[j+2:, j+2:] holds H_{j+1} ... H_{k-3}; step j grows it by
-  // row / column j+1 (identity) and applies H_j from the left.  Reflector j lives in
-  // column j (outside the block).  w is formed without reading the new row / column:
-  //   w_c = tau sum_{i >= j+2} u_i Q[i, c] (c >= j+2),  w_{j+1} = tau u_{j+1}.
-  for (int j = k - 3; j >= 0; --j) {
-    const double tj = tau[j];
-    const int j1 = j + 1;
-    const double u1 = S[j * ld + j1];
-    for (int r0 = 0; r0 < k - j1 - 1; r0 += PT / 4) {                // uniform trip count
-      const int c = j1 + 1 + r0 + quad;
-      double s = 0.0;
-      if (c < k) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int i = j1 + 1 + ql;
-        for (; i + 12 < k; i += 16) {
-          a0 = fma(S[j * ld + i], S[c * ld + i], a0);
-          a1 = fma(S[j * ld + i + 4], S[c * ld + i + 4], a1);
-          a2 = fma(S[j * ld + i + 8], S[c * ld + i + 8], a2);
-          a3 = fma(S[j * ld + i + 12], S[c * ld + i + 12], a3);
-        }
-        for (; i < k; i += 4) a0 = fma(S[j * ld + i], S[c * ld + i], a0);
-        s = (a0 + a1) + (a2 + a3);
+  // ---- 3. Q = H_0 H_1 ... H_{k-3}, one column per warp, straight to global -------------
+  // Column c of Q is H_0 ... H_{k-3} e_c; H_j leaves e_c alone for j >= c, so the warp
+  // starts from v = e_c (registers, lane holds rows lane + 32 t) and applies H_{min(c-1,k-3)}
+  // down to H_0: v -= tau_j (u_j . v) u_j.  The reflectors stay read-only in S: no barrier.
+  for (int c = warp; c < k; c += PNW) {
+    double v[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) v[t] = (lane + 32 * t == c) ? 1.0 : 0.0;
+    for (int j = std::min(c - 1, k - 3); j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const double* uj = S + j * ld;
+      double sum = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int i = lane + 32 * t;
+        if (i > j && i < k) sum = fma(uj[i], v[t], sum);
       }
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (c < k && ql == 0) pv[c] = tj * s;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const double wc = tj * sum;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int i = lane + 32 * t;
+        if (i > j && i < k) v[t] = fma(-uj[i], wc, v[t]);
+      }
     }
-    if (threadIdx.x == 0) pv[j1] = tj * u1;
-    constexpr int RT = (PK_MAX + 31) / 32;
-    double ur[RT];
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
-      const int i = j1 + lane + 32 * t;
-      ur[t] = i < k ? S[j * ld + i] : 0.0;
+      const int i = lane + 32 * t;
+      if (i < k) Qg[(size_t)c * k + i] = v[t];
     }
-    __syncthreads();
-    for (int c = j1 + warp; c < k; c += PNW) {
-      const double wc = pv[c];
-      double* col = S + c * ld;
-      double v[RT];
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int i = j1 + lane + 32 * t;
-        v[t] = (i < k && i != j1 && c != j1) ? col[i] : (i == c ? 1.0 : 0.0);
-      }
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int i = j1 + lane + 32 * t;
-        if (i < k) col[i] = v[t] - ur[t] * wc;
-      }
-    }
-    __syncthreads();
   }
-  // rows / columns 0 (and the k <= 2 cases) of Q
-  for (int i = threadIdx.x; i < k; i += PT) {
-    S[i] = i == 0 ? 1.0 : 0.0;
-    if (i > 0) S[i * ld] = 0.0;
-  }
-  if (k == 2 && threadIdx.x == 0) { S[ld + 1] = 1.0; S[ld] = 0.0; S[1] = 0.0; }
-  __syncthreads();
-  for (int j = warp; j < k; j += PNW)
-    for (int i = lane; i < k; i += 32) Qg[(size_t)j * k + i] = S[j * ld + i];
   __syncthreads();
   pc_mark(7);
   // ---- 4. eigenvectors of the tridiagonal: twisted factorisation, one thread each, into
