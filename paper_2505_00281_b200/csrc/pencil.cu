@@ -245,22 +245,30 @@ __global__ void __launch_bounds__(PT, 1)
   // symmetric matvec p_c = tau S[:, c] . u is a warp dot product over the owner's column,
   // the rank-2 update touches only the owner's columns.  Two barriers per column.
   constexpr int RT = (PK_MAX + 31) / 32;                               // rows per lane
+  // the reflector scalars of the next column are formed by warp 0 as soon as that column is
+  // final (end of the previous step), off the next step's critical path
+  __shared__ double s_alpha, s_tau, s_u0, s_x0;
+  auto reflector = [&](int j, double norm2) {                          // lane 0 of warp 0
+    const double x0 = S[j * ld + j + 1];
+    const double alpha = -copysign(sqrt(norm2), x0);
+    const double unorm2 = 2.0 * (norm2 - x0 * alpha);
+    const bool skip = !(unorm2 > 0.0) || norm2 == 0.0;
+    s_x0 = x0;
+    s_alpha = alpha;
+    s_tau = skip ? 0.0 : 2.0 / unorm2;
+    s_u0 = x0 - alpha;
+  };
   if (warp == 0 && k > 2) {
     double s2 = 0.0;
     for (int i = 1 + lane; i < k; i += 32) s2 = fma(S[i], S[i], s2);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    if (lane == 0) s_norm2 = s2;
+    if (lane == 0) reflector(0, s2);
   }
   __syncthreads();
   for (int j = 0; j + 2 < k; ++j) {
-    const double norm2 = s_norm2;
-    const double x0 = S[j * ld + j + 1];
-    const double alpha = -copysign(sqrt(norm2), x0);
-    const double unorm2 = 2.0 * (norm2 - x0 * alpha);
-    const bool skip = !(unorm2 > 0.0) || norm2 == 0.0;
-    const double tj = skip ? 0.0 : 2.0 / unorm2;
-    const double u0 = x0 - alpha;                                        // u[j+1]; u[i>j+1] = S[j, i]
+    const double tj = s_tau, u0 = s_u0, x0 = s_x0, alpha = s_alpha;
+    const bool skip = tj == 0.0;
     const int j1 = j + 1;
     // u in registers: lane holds u_i for i = j1 + lane + 32 t
     double ur[RT];
@@ -294,11 +302,12 @@ __global__ void __launch_bounds__(PT, 1)
     }
     __syncthreads();                                                     // (A)
     if (threadIdx.x == 0 && !skip) S[j * ld + j1] = u0;                 // reflector in place
+    double s2 = 0.0;
     if (!skip) {
-      double ksum = 0.0;
+      double ks = lane < PNW ? red[lane] : 0.0;                          // fixed-order tree
 #pragma unroll
-      for (int w = 0; w < PNW; ++w) ksum += red[w];
-      const double K = 0.5 * tj * ksum;
+      for (int o = 16; o > 0; o >>= 1) ks += __shfl_xor_sync(0xffffffffu, ks, o);
+      const double K = 0.5 * tj * ks;
       double qr[RT];
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
@@ -309,28 +318,23 @@ __global__ void __launch_bounds__(PT, 1)
         const double uc = c == j1 ? u0 : S[j * ld + c];
         const double qc = pv[c] - K * uc;
         double* col = S + c * ld;
-        double s2 = 0.0;
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
           const int i = j1 + lane + 32 * t;
           if (i < k) {
             const double nv = col[i] - (ur[t] * qc + qr[t] * uc);
             col[i] = nv;
-            if (i > c) s2 = fma(nv, nv, s2);
+            if (c == j1 && i > c) s2 = fma(nv, nv, s2);
           }
-        }
-        if (c == j1) {                                                   // norm of the next column
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-          if (lane == 0) s_norm2 = s2;
         }
       }
     } else if (warp == 0) {
-      double s2 = 0.0;
       for (int i = j1 + 1 + lane; i < k; i += 32) s2 = fma(S[j1 * ld + i], S[j1 * ld + i], s2);
+    }
+    if (warp == 0 && j1 + 2 < k) {                                      // next column's reflector
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      if (lane == 0) s_norm2 = s2;
+      if (lane == 0) reflector(j1, s2);
     }
     __syncthreads();                                                     // (B)
   }
