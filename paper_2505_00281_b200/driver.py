@@ -188,6 +188,15 @@ class EigEngine:
         _, self.proj_out = projection_policy(self.pol)
         self.stats = RunStats()
         self._oz = {}           # prepared Ozaki digit planes per operator (this run)
+        # the FP64 report's operator scales only depend on A: refreshed on a side stream while
+        # the pencil solve occupies one SM (off the critical path), see _body
+        self._res_oz = None
+        if (self.ops is _ops and not self.comm.distributed and FpFormat.F64 not in (self.mv.storage, self.pol.storage)
+                and hasattr(a, "residual_operator")):
+            A_res = a.residual_operator(self.A_mv.fmt)
+            if A_res.fmt in _ops.OZAKI_FMTS:
+                self._res_oz = _ops.OzakiOperator(A_res, prepare=False)
+                self._oz[id(A_res)] = self._res_oz
 
     def _ozaki(self, A):
         """Prepared int8 digit planes of a 16/8-bit operator (once per run), or None."""
@@ -258,6 +267,7 @@ class EigEngine:
             _, M = ops.gram(U, None, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
         else:
             B, M = ops.gram(U, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        side = self._fork_res_scales()
         eig = ops.sym_def_gen_eig(B, M, kp)
         st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
         st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
@@ -270,7 +280,27 @@ class EigEngine:
                                         mode=2 if comm.distributed else 0)
             if comm.distributed:
                 comm.all_reduce_sum_(est)
+        self._join(side)
         return eig, U64, Xn, est
+
+    def _fork_res_scales(self):
+        """Launch the row-scale pass of the FP64 report's operator on a side stream (it
+        overlaps the single-SM pencil solve); returns the stream to join, or None."""
+        if self._res_oz is None:
+            return None
+        import torch
+        main = torch.cuda.current_stream(self.device)
+        side = torch.cuda.Stream(self.device) if not hasattr(self, "_side") else self._side
+        self._side = side
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self._res_oz.refresh()
+        return side
+
+    def _join(self, side) -> None:
+        if side is not None:
+            import torch
+            torch.cuda.current_stream(self.device).wait_stream(side)
 
     def residuals(self, U64, vals, r_dev, r):
         """FP64 ||A u - lambda u|| / |lambda| for the first r pairs (K7)."""

@@ -238,7 +238,7 @@ class OzakiOperator:
     """The digit planes of a 16/8-bit operator (ofrr_ozaki_prepare), reusable for every
     FP64-accurate product with it until A changes; ``refresh`` re-slices A in place."""
 
-    def __init__(self, A: DevOperator):
+    def __init__(self, A: DevOperator, prepare: bool = True):
         if A.fmt not in OZAKI_FMTS:
             raise ValueError(f"Ozaki products need a 16/8-bit operator, got {A.fmt.name}")
         L = _lib.load()
@@ -252,7 +252,8 @@ class OzakiOperator:
                 _OZ_BUFFERS.pop(next(iter(_OZ_BUFFERS)))
             _OZ_BUFFERS[key] = ws
         self.ws = ws
-        self.refresh()
+        if prepare:
+            self.refresh()
 
     def refresh(self) -> None:
         L = _lib.load()
