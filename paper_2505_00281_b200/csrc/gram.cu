@@ -3,88 +3,134 @@
 // Replaces ofrr/projection.py:56-61 (_project) as called from ofrr_eig (:79-80) and
 // ofrr_svd (:109-111).  Tall-skinny reduction over the n rows:
 //   stage 1: grid (row chunks x 64x64 output tiles); each CTA stages a 32-row slab of
-//            U and [W U] in shared memory as fp64 and accumulates 4x4 outputs per thread
-//            with fp64 FMA (storage values have <= 24 significant bits, so every product
-//            is exact in fp64; only the sums round);
+//            U and [W U] in shared memory as fp64 (register-prefetched one slab ahead) and
+//            accumulates with fp64 tensor-core MMA (DMMA m8n8k4; storage values have <= 24
+//            significant bits, so every product is exact in fp64; only the sums round);
 //   stage 2: fixed-order sum of the chunk partials (deterministic), rounding to the
 //            projection output format (ofrr/projection.py:42-53), non-finite check.
 #include "common.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace ofrr {
 
 static constexpr int GT = 64;   // output tile
 static constexpr int GR = 32;   // rows per smem slab
 
+// fp64 tensor-core MMA (DMMA), m8n8k4: A row-major 8x4, B col-major 4x8, C 8x8 fp64.
+// Fragments (lane = 4 g + t): a = A[g][t], b = B[t][g], c = C[g][2t .. 2t+1].
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+static constexpr int GS = GR + 4;   // smem row stride (doubles): conflict-free fragment reads
+
 template <typename T>
 __global__ void __launch_bounds__(256)
     k_gram_partial(const T* __restrict__ U, int64_t ldu, const T* __restrict__ W, int64_t ldw, int64_t n,
                    int k, int kw, int64_t rows_per_chunk, double* __restrict__ part) {
-  // output columns: [0, kw) -> U^T W, [kw, kw + k) -> U^T U
-  __shared__ double Us[GR][GT + 1];
-  __shared__ double Vs[GR][GT + 1];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  // output columns: [0, kw) -> U^T W, [kw, kw + k) -> U^T U.  Slabs are staged column-major
+  // ([column][row], stride GS) as fp64; each warp owns a 16 x 32 block of the 64 x 64 tile
+  // (2 x 4 DMMA tiles) and walks the slab 4 rows per MMA.
+  __shared__ double Us[GT][GS];
+  __shared__ double Vs[GT][GS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
   const int i0 = blockIdx.y * GT;      // rows of the Gram (columns of U)
   const int j0 = blockIdx.z * GT;      // columns of the Gram ([W U])
   const int ncols = kw + k;
   const int64_t rb = (int64_t)blockIdx.x * rows_per_chunk;
   const int64_t re = std::min<int64_t>(n, rb + rows_per_chunk);
-  double acc[4][4] = {};
-  for (int64_t l0 = rb; l0 < re; l0 += GR) {
-    for (int e = tid; e < GR * GT; e += 256) {
+  double acc[2][4][2] = {};
+  // software pipeline: the next slab's 8 + 8 raw elements per thread are loaded into registers
+  // (branch-free, clamped addresses + validity masks, converted only when staged) while the
+  // current slab is multiplied out of shared memory -- all 16 loads are in flight at once
+  constexpr int PER = GR * GT / 256;
+  T pu[PER], pv[PER];
+  unsigned okm = 0;
+  auto fetch = [&](int64_t l0) {
+    okm = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + 256 * q;
       const int c = e / GR, rr = e % GR;   // contiguous along rows (column-major inputs)
       const int64_t l = l0 + rr;
-      double u = 0.0, v = 0.0;
-      if (l < re) {
-        if (i0 + c < k) u = to_d(U[(int64_t)(i0 + c) * ldu + l]);
-        const int jc = j0 + c;
-        if (jc < kw) v = to_d(W[(int64_t)jc * ldw + l]);
-        else if (jc < ncols) v = to_d(U[(int64_t)(jc - kw) * ldu + l]);
-      }
-      Us[rr][c] = u;
-      Vs[rr][c] = v;
+      const bool lin = l < re;
+      const bool uok = lin && i0 + c < k;
+      const int jc = j0 + c;
+      const bool vok = lin && jc < ncols;
+      const T* vp = jc < kw ? W + (int64_t)jc * ldw : U + (int64_t)(jc - kw) * ldu;
+      pu[q] = U[uok ? (int64_t)(i0 + c) * ldu + l : 0];
+      pv[q] = vok ? vp[l] : U[0];
+      okm |= (uok ? 1u : 0u) << q | (vok ? 1u : 0u) << (q + 16);
+    }
+  };
+  if (rb < re) fetch(rb);
+  for (int64_t l0 = rb; l0 < re; l0 += GR) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + 256 * q;
+      Us[e / GR][e % GR] = (okm >> q & 1u) ? to_d(pu[q]) : 0.0;
+      Vs[e / GR][e % GR] = (okm >> (q + 16) & 1u) ? to_d(pv[q]) : 0.0;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int rr = 0; rr < GR; ++rr) {
-      double a[4], b[4];
+    if (l0 + GR < re) fetch(l0 + GR);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = Us[rr][ty + 16 * i];
+    for (int kk = 0; kk < GR; kk += 4) {
+      double a[2], b[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Vs[rr][tx + 16 * j];
+      for (int i = 0; i < 2; ++i) a[i] = Us[wm + 8 * i + g][kk + t];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) b[j] = Vs[wn + 8 * j + g][kk + t];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], a[i], b[j]);
     }
     __syncthreads();
   }
   // partial layout: [chunk][ncols][k] column-major per chunk
   double* dst = part + (int64_t)blockIdx.x * ncols * k;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;
-      if (gi < k && gj < ncols) dst[(int64_t)gj * k + gi] = acc[i][j];
-    }
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gi = i0 + wm + 8 * i + g, gj = j0 + wn + 8 * j + 2 * t + h;
+        if (gi < k && gj < ncols) dst[(int64_t)gj * k + gi] = acc[i][j][h];
+      }
 }
 
-__global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int k, int kw, int out_fmt,
-                              double* __restrict__ G1, double* __restrict__ G2, int* __restrict__ flags) {
+// 32 output elements x 8 chunk lanes per CTA: each lane sums its chunks c = g, g+8, ... in
+// order, then lane 0 adds the 8 lane sums in order -- a fixed summation order (deterministic)
+// with 8x the memory-level parallelism of one thread per element
+__global__ void __launch_bounds__(256) k_gram_reduce(const double* __restrict__ part, int nchunks, int k, int kw,
+                                                     int out_fmt, double* __restrict__ G1, double* __restrict__ G2,
+                                                     int* __restrict__ flags) {
+  __shared__ double red[8][33];
   const int ncols = kw + k;
   const int64_t total = (int64_t)ncols * k;
-  int bad = 0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += part[(int64_t)c * total + e];
-    s = rnd(s, out_fmt);
-    if (!isfinite(s)) bad = 1;
-    const int gj = (int)(e / k), gi = (int)(e % k);
-    if (gj < kw) { if (G1) G1[(int64_t)gj * k + gi] = s; }
-    else if (G2) G2[(int64_t)(gj - kw) * k + gi] = s;
+  const int lx = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lx;
+  double s = 0.0;
+  if (e < total) {
+#pragma unroll 4
+    for (int c = g; c < nchunks; c += 8) s += part[(int64_t)c * total + e];
   }
-  if (bad && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
+  red[g][lx] = s;
+  __syncthreads();
+  if (g != 0 || e >= total) return;
+  s = red[0][lx];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) s += red[j][lx];
+  s = rnd(s, out_fmt);
+  if (!isfinite(s) && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
+  const int gj = (int)(e / k), gi = (int)(e % k);
+  if (gj < kw) { if (G1) G1[(int64_t)gj * k + gi] = s; }
+  else if (G2) G2[(int64_t)(gj - kw) * k + gi] = s;
 }
 
 struct GramPlan { int nchunks; int64_t rows_per; };
@@ -92,8 +138,11 @@ static GramPlan gram_plan(int64_t n, int k, int kw) {
   int sms = ofrr_device_sm_count(-1);
   if (sms <= 0) sms = 148;
   const int tiles = ((k + GT - 1) / GT) * ((kw + k + GT - 1) / GT);
-  int64_t chunks = std::max<int64_t>(1, (2 * sms + tiles - 1) / tiles);
-  chunks = std::min<int64_t>(chunks, (n + GR - 1) / GR);
+  // ~4 CTAs per SM (each has one slab of loads in flight; more CTAs hide the latency),
+  // at least 4 slabs per chunk (the partials are re-read by the reduce)
+  int64_t chunks = std::max<int64_t>(1, (4 * sms + tiles - 1) / tiles);
+  if (const char* e = getenv("OFRR_GRAM_CHUNKS")) chunks = atoi(e);   // tuning override
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n / (4 * GR)));
   int64_t rows_per = (n + chunks - 1) / chunks;
   rows_per = (rows_per + GR - 1) / GR * GR;
   chunks = std::max<int64_t>(1, (n + rows_per - 1) / rows_per);
@@ -113,7 +162,7 @@ static int launch_gram(const void* U, int64_t ldu, const void* W, int64_t ldw, i
   k_gram_partial<T><<<grid, 256, 0, st>>>((const T*)U, ldu, (const T*)W, ldw, n, k, kw, p.rows_per, part);
   OFRR_CHECK_LAUNCH();
   const int64_t total = (int64_t)(kw + k) * k;
-  k_gram_reduce<<<(unsigned)std::min<int64_t>((total + 255) / 256, 1024), 256, 0, st>>>(part, p.nchunks, k, kw, out_fmt,
+  k_gram_reduce<<<(unsigned)((total + 31) / 32), 256, 0, st>>>(part, p.nchunks, k, kw, out_fmt,
                                                                                       G1, G2, flags);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;

@@ -191,6 +191,7 @@ class EigEngine:
         # the FP64 report's operator scales only depend on A: refreshed on a side stream while
         # the pencil solve occupies one SM (off the critical path), see _body
         self._res_oz = None
+        self._refresh_now = True    # first iteration of a run: refresh the report's row scales
         if (self.ops is _ops and not self.comm.distributed and FpFormat.F64 not in (self.mv.storage, self.pol.storage)
                 and hasattr(a, "residual_operator")):
             A_res = a.residual_operator(self.A_mv.fmt)
@@ -285,8 +286,9 @@ class EigEngine:
 
     def _fork_res_scales(self):
         """Launch the row-scale pass of the FP64 report's operator on a side stream (it
-        overlaps the single-SM pencil solve); returns the stream to join, or None."""
-        if self._res_oz is None:
+        overlaps the single-SM pencil solve) -- in the first iteration of a run only (its own
+        CUDA graph); returns the stream to join, or None."""
+        if self._res_oz is None or not self._refresh_now:
             return None
         import torch
         main = torch.cuda.current_stream(self.device)
@@ -359,6 +361,7 @@ class EigEngine:
             self._ozaki(self.A_pol) if self.pol.storage == FpFormat.F64 else None
         for it in range(cfg.m):
             last = it == cfg.m - 1
+            self._refresh_now = it == 0      # A's report scales: once per run (A may change between runs)
             # one iteration: power step(s), Hessenberg basis, projection with every column
             # (the basis keeps all k in the common case; dropped columns of Q are zero),
             # residual estimate -- replayed as one CUDA graph when possible.  One host sync.
@@ -485,7 +488,7 @@ class EigEngine:
         from . import _lib
         return (A.t.data_ptr(), A.rows, A.cols, A.lda, int(A.fmt), B.t.data_ptr(), B.rows, B.cols, B.lda, int(B.fmt),
                 self.n, self.cfg.k, self.cfg.iter, pol(self.pol), pol(self.mv), check, top, self.device.index,
-                bool(_lib.load().ofrr_prof_gemm_active()))
+                bool(_lib.load().ofrr_prof_gemm_active()), self._refresh_now and self._res_oz is not None)
 
     def _graph_step(self, X, check: bool, top: int):
         """Replay the captured iteration (capturing it first once the shapes have run

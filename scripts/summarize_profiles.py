@@ -103,7 +103,8 @@ def launches(name="launches_c2_bench.csv"):
 if __name__ == "__main__":
     launches()
     summarize_rep("k1_c2", "K1 bf16 block k=64 at C2 shape, third launch")
-    summarize_rep("oz_gemm_c2", "K7z int8 digit-plane product, C2 residual r=64")
-    summarize_rep("oz_slices_c2", "K7z digit planes of A, C2")
+    summarize_rep("ozk_gemm_c2", "K7z int8 Ozaki product with in-kernel digit conversion, C2 residual r=64")
+    summarize_rep("oz_rowscale_c2", "K7z row scales of A (one pass over A), C2")
+    summarize_rep("gram_c2", "K4 Gram partials (DMMA), n=16384 k=64 fp32 basis")
     summarize_rep("hess_c2", "K3 Hessenberg basis n=16384 k=64")
     summarize_rep("pc_tri_k64", "K5c tridiagonal eigensolver k=64")
