@@ -7,12 +7,13 @@
 //   k_pc_chol   M = L L^T (right-looking, one barrier per column), X = L^-1 in place
 //               (right-looking forward substitution), certificate 1/||X||_F^2 > 4 k eps ||M||_F
 //   k_pc_gemm   T = X sym(B) X^T  (two launches)
-//   k_pc_tri    T = Q Tri Q^T (Householder), eigenvalues of Tri by multisection on
-//               division-free Sturm sequences (4 lanes per eigenvalue), eigenvectors Z of
-//               Tri by twisted factorisation (+ Gram-Schmidt inside numerically coincident
-//               clusters), Q formed in place from the reflectors
-//   k_pc_gemm   Y = X^T (Q Z)  (two launches)
-//   k_pc_finish descending order + the largest-|entry|-positive sign rule (smallsolve.py:52-61)
+//   k_pc_tri    T = Q Tri Q^T (Householder, one CTA): the tridiagonal and the reflectors
+//   k_pc_eigvec eigenvalues of Tri by multisection on division-free Sturm sequences,
+//               eigenvectors Z of Tri by twisted factorisation, W1 = Q Z by applying the
+//               reflectors -- a few eigenpairs per CTA, spread over the GPU
+//   k_pc_gemm   Y = X^T W1
+//   k_pc_finish descending order + the largest-|entry|-positive sign rule (smallsolve.py:52-61);
+//               numerically coincident eigenvalues raise the gate
 // Any failure (Cholesky breakdown, certificate not met, eigenvector breakdown) raises a gate
 // flag on the device and the general kernel (small_eig.cu: the reference's eig(M)
 // whitening + Jacobi fallback) runs instead; with the gate down it returns at once.
@@ -27,12 +28,13 @@ static constexpr int PK_MAX = 160;        // one k x (k|1) fp64 matrix in shared
 
 __device__ __forceinline__ int pc_ld(int k) { return k | 1; }
 
-__device__ unsigned long long g_pcprof[16];   // debug: phase end times (globaltimer ns)
+__device__ unsigned long long g_pcprof[16];   // debug: phase end times (globaltimer ns | SM clock)
 __device__ __forceinline__ void pc_mark(int i) {
   if (threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     g_pcprof[i] = t;
+    if (i < 6) g_pcprof[10 + i] = clock64();
   }
 }
 int pc_profile(unsigned long long* out) {
@@ -176,8 +178,9 @@ __global__ void __launch_bounds__(256)
 
 // division-free Sturm count (number of eigenvalues of the scaled tridiagonal below x):
 // sign changes of the leading principal minors p_i (three-term recurrence), rescaled by a
-// power of two after every 8 steps.  The product e2 * p_{i-1} and d_i - x are off the
-// dependency chain (one fma per step on it); signs are compared on the raw bits.
+// power of two after every 8 steps (exponent read from the bits: ilogb is a slow library
+// path on the recurrence's critical chain).  The product e2 * p_{i-1} and d_i - x are off
+// the dependency chain (one fma per step on it); signs are compared on the raw bits.
 __device__ __forceinline__ int pc_sturm(const double* __restrict__ d, const double* __restrict__ e2, int k, double x) {
   double p0 = 1.0, p1 = d[0] - x;
   int cnt = (int)((unsigned)__double2hiint(p1) >> 31);
@@ -193,8 +196,13 @@ __device__ __forceinline__ int pc_sturm(const double* __restrict__ d, const doub
       p0 = p1;
       p1 = p2;
     }
-    const int ex = ilogb(p1);
-    if (ex > 256 || ex < -256) { p0 = ldexp(p0, -ex); p1 = ldexp(p1, -ex); }
+    const int ex = ((__double2hiint(p1) >> 20) & 0x7ff) - 1023;      // biased exponent of p1
+    if (ex > 256 || ex < -256) {                                      // (zero/denormal: ex = -1023)
+      const int e = ex < -1000 ? 0 : ex;
+      const double sc = __hiloint2double((1023 - e) << 20, 0);        // 2^-e, exact
+      p0 *= sc;
+      p1 *= sc;
+    }
   }
   for (; i < k; ++i) {
     const double p2 = fma(d[i] - x, p1, -e2[i - 1] * p0);
@@ -206,12 +214,14 @@ __device__ __forceinline__ int pc_sturm(const double* __restrict__ d, const doub
 }
 
 __device__ __forceinline__ double pc_fast_div(double a, double b) {
-  // a / b to ~1 ulp via an f32 reciprocal and two Newton steps (finite, normal b)
+  // a / b to ~1 ulp: MUFU fp64 reciprocal seed and two Newton steps (finite, normal b);
+  // a third of the latency of the IEEE division sequence
   const double ab = fabs(b);
   if (ab > 1e-300 && ab < 1e300) {
-    double r = (double)__frcp_rn((float)b);
-    r = r * fma(-b, r, 2.0);
-    r = r * fma(-b, r, 2.0);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    r = fma(r, fma(-b, r, 1.0), r);
+    r = fma(r, fma(-b, r, 1.0), r);
     return a * r;
   }
   return a / b;
@@ -222,33 +232,37 @@ __device__ __forceinline__ double pc_fast_div(double a, double b) {
 // column c <-> lam[k-1-c], i.e. descending), Q (k x k) with T = Q Tri Q^T.
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(PT, 1)
-    k_pc_tri(const double* __restrict__ Tg, int k, double* __restrict__ lam_g, double* __restrict__ Zg,
-             double* __restrict__ Qg, double* __restrict__ wk, int* __restrict__ gate) {
+    k_pc_tri(const double* __restrict__ Tg, int k, double* __restrict__ tri, double* __restrict__ Rg,
+             int* __restrict__ gate) {
   if (*gate) return;
   extern __shared__ double sm[];
   __shared__ double red[PNW];
-  __shared__ double dd[PK_MAX], ee[PK_MAX], tau[PK_MAX], lam[PK_MAX], e2[PK_MAX], ds[PK_MAX], e2s[PK_MAX];
+  __shared__ double dd[PK_MAX], ee[PK_MAX], tau[PK_MAX];
   __shared__ double pv[PK_MAX];
-  __shared__ double s_norm2;
-  __shared__ int flag;
   const int ld = pc_ld(k);
   double* S = sm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int quad = threadIdx.x >> 2, ql = threadIdx.x & 3;   // 4 threads per row / column
   for (int j = warp; j < k; j += PNW)
     for (int i = lane; i < k; i += 32) S[j * ld + i] = 0.5 * (Tg[(size_t)j * k + i] + Tg[(size_t)i * k + j]);
-  if (threadIdx.x == 0) flag = 1;
   __syncthreads();
   pc_mark(4);
   // ---- 1. Householder tridiagonalisation (reflector j stored in column j, rows > j) ----
-  // Column-owner layout: warp w owns the trailing columns c = j+1+w, j+1+w+16, ...; the
-  // symmetric matvec p_c = tau S[:, c] . u is a warp dot product over the owner's column,
-  // the rank-2 update touches only the owner's columns.  Two barriers per column.
-  constexpr int RT = (PK_MAX + 31) / 32;                               // rows per lane
-  // the reflector scalars of the next column are formed by warp 0 as soon as that column is
-  // final (end of the previous step), off the next step's critical path
+  // Group-per-column layout: the CTA is split into groups of tpc adjacent lanes, group g
+  // owning column g of S (tpc = 8 / 4 / 2 for k <= 64 / 128 / 160, one column per group).
+  // Step j: every group forms p_c = tau S[:, c] . u over its rows (tpc partial sums, an
+  // in-group shuffle tree), the leaders fold u_c p_c into a per-warp partial; barrier (A);
+  // K = tau/2 u.p in fixed order, then the group applies the rank-2 update to its own
+  // column and the group of column j+1 forms the next reflector at once; barrier (B).
+  const int tpc = k <= 64 ? 8 : (k <= 128 ? 4 : 2);
+  const int grp = threadIdx.x / tpc, sub = threadIdx.x % tpc;
+  const unsigned gmask = (tpc == 32 ? 0xffffffffu : (((1u << tpc) - 1u) << (lane & ~(tpc - 1))));
+  // the reflector scalars of the next column: formed by the group that owns that column
   __shared__ double s_alpha, s_tau, s_u0, s_x0;
-  auto reflector = [&](int j, double norm2) {                          // lane 0 of warp 0
+  auto group_sum = [&](double v) {
+    for (int o = tpc >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+    return v;
+  };
+  auto reflector = [&](int j, double norm2) {                          // group j+1... leader
     const double x0 = S[j * ld + j + 1];
     const double alpha = -copysign(sqrt(norm2), x0);
     const double unorm2 = 2.0 * (norm2 - x0 * alpha);
@@ -258,42 +272,38 @@ __global__ void __launch_bounds__(PT, 1)
     s_tau = skip ? 0.0 : 2.0 / unorm2;
     s_u0 = x0 - alpha;
   };
-  if (warp == 0 && k > 2) {
+  if (k > 2 && grp == 0) {
     double s2 = 0.0;
-    for (int i = 1 + lane; i < k; i += 32) s2 = fma(S[i], S[i], s2);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    if (lane == 0) reflector(0, s2);
+    for (int i = 1 + sub; i < k; i += tpc) s2 = fma(S[i], S[i], s2);
+    s2 = group_sum(s2);
+    if (sub == 0) reflector(0, s2);
   }
   __syncthreads();
   for (int j = 0; j + 2 < k; ++j) {
     const double tj = s_tau, u0 = s_u0, x0 = s_x0, alpha = s_alpha;
     const bool skip = tj == 0.0;
     const int j1 = j + 1;
-    // u in registers: lane holds u_i for i = j1 + lane + 32 t
-    double ur[RT];
-#pragma unroll
-    for (int t = 0; t < RT; ++t) {
-      const int i = j1 + lane + 32 * t;
-      ur[t] = i < k ? (i == j1 ? u0 : S[j * ld + i]) : 0.0;
-    }
+    const int c = grp;
+    const bool own = c >= j1 && c < k;
+    const double* uj = S + j * ld;                                     // u_i = uj[i] (i > j1), u0 at j1
+    double pc = 0.0;
     if (!skip) {
-      double kpart = 0.0;
-      for (int c = j1 + warp; c < k; c += PNW) {
+      if (own) {
         const double* col = S + c * ld;
-        double sum = 0.0;
-#pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int i = j1 + lane + 32 * t;
-          if (i < k) sum = fma(col[i], ur[t], sum);
+        double a0 = 0.0, a1 = 0.0;
+        int i = j1 + sub;
+        for (; i + tpc < k; i += 2 * tpc) {
+          a0 = fma(col[i], i == j1 ? u0 : uj[i], a0);
+          a1 = fma(col[i + tpc], uj[i + tpc], a1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        const double pc = tj * sum;
-        if (lane == 0) pv[c] = pc;
-        kpart = fma(c == j1 ? u0 : S[j * ld + c], pc, kpart);
+        if (i < k) a0 = fma(col[i], i == j1 ? u0 : uj[i], a0);
+        pc = tj * group_sum(a0 + a1);
+        if (sub == 0) pv[c] = pc;
       }
-      if (lane == 0) red[warp] = kpart;
+      double kp = (own && sub == 0) ? (c == j1 ? u0 : uj[c]) * pc : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) kp += __shfl_xor_sync(0xffffffffu, kp, o);
+      if (lane == 0) red[warp] = kp;
     }
     if (threadIdx.x == 0) {
       dd[j] = S[j * ld + j];
@@ -301,41 +311,27 @@ __global__ void __launch_bounds__(PT, 1)
       tau[j] = tj;
     }
     __syncthreads();                                                     // (A)
-    if (threadIdx.x == 0 && !skip) S[j * ld + j1] = u0;                 // reflector in place
-    double s2 = 0.0;
-    if (!skip) {
-      double ks = lane < PNW ? red[lane] : 0.0;                          // fixed-order tree
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ks += __shfl_xor_sync(0xffffffffu, ks, o);
+    if (!skip && own) {
+      double ks = 0.0;
+      for (int w = 0; w < PNW; ++w) ks += red[w];                        // fixed order
       const double K = 0.5 * tj * ks;
-      double qr[RT];
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int i = j1 + lane + 32 * t;
-        qr[t] = i < k ? pv[i] - K * ur[t] : 0.0;
+      const double uc = c == j1 ? u0 : uj[c];
+      const double qc = pc - K * uc;
+      double* col = S + c * ld;
+      for (int i = j1 + sub; i < k; i += tpc) {
+        const double ui = i == j1 ? u0 : uj[i];
+        const double qi = pv[i] - K * ui;
+        col[i] = col[i] - (ui * qc + qi * uc);
       }
-      for (int c = j1 + warp; c < k; c += PNW) {
-        const double uc = c == j1 ? u0 : S[j * ld + c];
-        const double qc = pv[c] - K * uc;
-        double* col = S + c * ld;
-#pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int i = j1 + lane + 32 * t;
-          if (i < k) {
-            const double nv = col[i] - (ur[t] * qc + qr[t] * uc);
-            col[i] = nv;
-            if (c == j1 && i > c) s2 = fma(nv, nv, s2);
-          }
-        }
-      }
-    } else if (warp == 0) {
-      for (int i = j1 + 1 + lane; i < k; i += 32) s2 = fma(S[j1 * ld + i], S[j1 * ld + i], s2);
     }
-    if (warp == 0 && j1 + 2 < k) {                                      // next column's reflector
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      if (lane == 0) reflector(j1, s2);
+    if (c == j1 && j1 + 2 < k) {                                         // next column's reflector
+      __syncwarp(gmask);
+      double s2 = 0.0;
+      for (int i = j1 + 1 + sub; i < k; i += tpc) s2 = fma(S[j1 * ld + i], S[j1 * ld + i], s2);
+      s2 = group_sum(s2);
+      if (sub == 0) reflector(j1, s2);
     }
+    if (threadIdx.x == 0 && !skip) S[j * ld + j1] = u0;                 // reflector in place
     __syncthreads();                                                     // (B)
   }
   if (threadIdx.x == 0) {
@@ -350,16 +346,257 @@ __global__ void __launch_bounds__(PT, 1)
   }
   __syncthreads();
   pc_mark(5);
-  // ---- 2. eigenvalues: 4-lane multisection on the power-of-two scaled tridiagonal -------
-  double glo = 0.0, ghi = 0.0;
-  for (int i = 0; i < k; ++i) {
-    const double r = (i > 0 ? fabs(ee[i - 1]) : 0.0) + (i + 1 < k ? fabs(ee[i]) : 0.0);
-    glo = i == 0 ? dd[i] - r : fmin(glo, dd[i] - r);
-    ghi = i == 0 ? dd[i] + r : fmax(ghi, dd[i] + r);
-  }
-  const double tnrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
-  const int sx = ilogb(tnrm);
+  // tridiagonal (d, e, tau) and the reflectors (column j, rows > j) to global for K5d
   for (int i = threadIdx.x; i < k; i += PT) {
+    tri[i] = dd[i];
+    tri[k + i] = ee[i];
+    tri[2 * k + i] = tau[i];
+  }
+  for (int j = warp; j < k; j += PNW)
+    for (int i = lane; i < k; i += 32) Rg[(size_t)j * k + i] = i > j ? S[j * ld + i] : 0.0;
+}
+
+// ---------------------------------------------------------------------------------
+// K5c for k <= 128: the same Householder tridiagonalisation with the matrix held in
+// registers (shared memory bandwidth bounds the in-smem version: every step re-reads and
+// re-writes the trailing matrix in fp64).  Group g of TPC adjacent lanes owns column g;
+// lane `sub` of the group holds the contiguous rows sub*RPT + t (t < RPT).  The step's
+// vectors (reflector u, p = tau S u) live in shared memory padded by two doubles per RPT
+// rows, so the TPC lanes of a group read them as conflict-free 16-byte vectors.
+// Step j: every group forms p_c from its registers, the leaders fold u_c p_c per warp;
+// barrier (A); K (a 16-term tree), the rank-2 update in registers as two fmas per entry
+// (S -= u (q_c - K u_c) + p u_c), the group of column j+1 accumulating the norm of its
+// new column on the way and forming the next reflector at once; barrier (B).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double pc_sum16(const double* r) {
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  double v[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) { const double2 x = r2[w]; v[w] = x.x + x.y; }
+  return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+}
+
+template <int TPC, int RPT>
+__global__ void __launch_bounds__(PT, 1)
+    k_pc_tri_reg(const double* __restrict__ Tg, int k, double* __restrict__ tri, double* __restrict__ Rg,
+                 int* __restrict__ gate) {
+  if (*gate) return;
+  static_assert(PNW == 16, "pc_sum16 folds 16 warp partials");
+  constexpr int RP = RPT + 2;                                     // padded chunk
+  __shared__ __align__(16) double red[2][PNW];
+  __shared__ __align__(16) double uv[2][TPC * RP];               // reflector of the step, by parity
+  __shared__ __align__(16) double pv[TPC * RP];
+  __shared__ double dd[PK_MAX], ee[PK_MAX], tau[PK_MAX];
+  __shared__ double s_tau[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = threadIdx.x / TPC, sub = threadIdx.x % TPC;      // my column, my lane in the group
+  const unsigned gmask = (TPC == 32 ? 0xffffffffu : (((1u << TPC) - 1u) << (lane & ~(TPC - 1))));
+  const int gl0 = lane & ~(TPC - 1);                              // lane of the group's sub 0
+  const int r0 = sub * RPT;                                       // my first row
+  const bool colok = c < k;
+  auto pidx = [](int i) { return i + 2 * (i / RPT); };            // padded index of row i
+  double a[RPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    const int i = r0 + t;
+    a[t] = (colok && i < k) ? 0.5 * (Tg[(size_t)c * k + i] + Tg[(size_t)i * k + c]) : 0.0;
+  }
+  for (int i = threadIdx.x; i < TPC * RP; i += PT) {            // rows >= k stay zero
+    pv[i] = 0.0;
+    uv[0][i] = 0.0;
+    uv[1][i] = 0.0;
+  }
+  __syncthreads();
+  auto group_sum = [&](double v) {
+#pragma unroll
+    for (int o = TPC >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+    return v;
+  };
+  // group of column j (after its update): reflector from rows > j -> uv[buf], tau, d_j, e_j.
+  // s2 = this lane's sum of squares over rows > j + 1.
+  auto make_reflector = [&](int j, int buf, double s2) {
+    double x0 = 0.0, djj = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      if (r0 + t == j + 1) x0 = a[t];
+      if (r0 + t == j) djj = a[t];
+    }
+    s2 = group_sum(s2);
+    x0 = __shfl_sync(gmask, x0, gl0 + (j + 1) / RPT);
+    djj = __shfl_sync(gmask, djj, gl0 + j / RPT);
+    const double norm2 = fma(x0, x0, s2);
+    const double alpha = -copysign(sqrt(norm2), x0);
+    const double unorm2 = 2.0 * (norm2 - x0 * alpha);
+    const bool skip = !(unorm2 > 0.0) || norm2 == 0.0;
+    const double u0 = x0 - alpha;
+    double* ub = uv[buf] + sub * RP;
+#pragma unroll
+    for (int t = 0; t < RPT; t += 2) {
+      const int i = r0 + t;
+      double2 w;
+      w.x = i > j + 1 ? a[t] : (i == j + 1 ? u0 : 0.0);
+      w.y = i + 1 > j + 1 ? a[t + 1] : (i + 1 == j + 1 ? u0 : 0.0);
+      *reinterpret_cast<double2*>(ub + t) = w;
+      if (i < k) Rg[(size_t)j * k + i] = w.x;                       // reflector j for K5d
+      if (i + 1 < k) Rg[(size_t)j * k + i + 1] = w.y;
+    }
+    if (sub == 0) {
+      const double tj = skip ? 0.0 : pc_fast_div(2.0, unorm2);
+      s_tau[buf] = tj;
+      tau[j] = tj;
+      dd[j] = djj;
+      ee[j] = skip ? x0 : alpha;
+    }
+  };
+  pc_mark(4);
+  if (k > 2 && c == 0) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPT; ++t)
+      if (r0 + t > 1 && r0 + t < k) s2 = fma(a[t], a[t], s2);
+    make_reflector(0, 0, s2);
+  }
+  __syncthreads();
+  for (int j = 0; j + 2 < k; ++j) {
+    const int buf = j & 1, j1 = j + 1;
+    const double tj = s_tau[buf];
+    const bool skip = tj == 0.0;
+    const bool own = colok && c >= j1;
+    const double* ub = uv[buf] + sub * RP;
+    double pc = 0.0, uc = 0.0;
+    if (!skip) {
+      if (own) {
+        double s0 = 0.0, s1 = 0.0;                              // u is zero at rows <= j
+#pragma unroll
+        for (int t = 0; t < RPT; t += 2) {
+          const double2 w = *reinterpret_cast<const double2*>(ub + t);
+          s0 = fma(a[t], w.x, s0);
+          s1 = fma(a[t + 1], w.y, s1);
+        }
+        pc = tj * group_sum(s0 + s1);
+        uc = uv[buf][pidx(c)];
+        if (sub == 0) pv[pidx(c)] = pc;
+      }
+      double kp = (own && sub == 0) ? uc * pc : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) kp += __shfl_xor_sync(0xffffffffu, kp, o);
+      if (lane == 0) red[buf][warp] = kp;
+    }
+    __syncthreads();                                                     // (A)
+    double s2 = 0.0;                                                     // column j+1's new norm
+    if (!skip && own) {
+      const double K = 0.5 * tj * pc_sum16(red[buf]);
+      const double qc = fma(-K, uc, pc) - K * uc;                        // q_c - K u_c
+      const double* pb = pv + sub * RP;
+#pragma unroll
+      for (int t = 0; t < RPT; t += 2) {
+        const int i = r0 + t;
+        const double2 w = *reinterpret_cast<const double2*>(ub + t);
+        const double2 q = *reinterpret_cast<const double2*>(pb + t);
+        if (i >= j1) a[t] = fma(-q.x, uc, fma(-w.x, qc, a[t]));
+        if (i + 1 >= j1) a[t + 1] = fma(-q.y, uc, fma(-w.y, qc, a[t + 1]));
+        if (i > j1 + 1) s2 = fma(a[t], a[t], s2);
+        if (i + 1 > j1 + 1) s2 = fma(a[t + 1], a[t + 1], s2);
+      }
+    } else if (c == j1) {
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+        if (r0 + t > j1 + 1) s2 = fma(a[t], a[t], s2);
+    }
+    if (c == j1) {
+      if (j1 + 2 < k) {
+        make_reflector(j1, buf ^ 1, s2);
+      } else if (sub == 0) {                                             // last two: no reflector
+        s_tau[buf ^ 1] = 0.0;
+      }
+    }
+    __syncthreads();                                                     // (B)
+  }
+  // d_{k-2}, e_{k-2}, d_{k-1} from the owners' registers
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    const int i = r0 + t;
+    if (k >= 2 && c == k - 2 && i == k - 2) dd[k - 2] = a[t];
+    if (k >= 2 && c == k - 2 && i == k - 1) ee[k - 2] = a[t];
+    if (c == k - 1 && i == k - 1) dd[k - 1] = a[t];
+  }
+  if (threadIdx.x == 0) {
+    if (k >= 2) tau[k - 2] = 0.0;
+    ee[k - 1] = 0.0;
+    tau[k - 1] = 0.0;
+  }
+  __syncthreads();
+  pc_mark(5);
+  for (int i = threadIdx.x; i < k; i += PT) {
+    tri[i] = dd[i];
+    tri[k + i] = ee[i];
+    tri[2 * k + i] = tau[i];
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// K5d: eigenpairs of the tridiagonal and their back-transformation, EPB eigenvalues per
+// CTA (ascending index m), spread over the GPU:
+//   multisection on division-free Sturm counts, one warp per eigenvalue (32 points per
+//     round: the interval shrinks 33x), on the power-of-two scaled tridiagonal;
+//   twisted factorisation, two lanes per eigenvalue (D+ and D- in parallel, shared memory);
+//   W1[:, k-1-m] = Q z_m = H_0 ... H_{k-3} z_m, one warp per eigenvector, the reflectors
+//     staged in shared memory by cp.async while the multisection runs.
+// Numerically coincident eigenvalues are left to k_pc_finish, which raises the gate (the
+// general kernel then runs); a failed eigenvector raises it here.
+// ---------------------------------------------------------------------------------
+static constexpr int EPT = 256;                       // threads of K5d (8 warps)
+__host__ __device__ constexpr int pc_epb(int k) { return k <= 128 ? 8 : 4; }
+
+__global__ void __launch_bounds__(EPT)
+    k_pc_eigvec(const double* __restrict__ tri, const double* __restrict__ Rg, int k, double* __restrict__ lam_g,
+                double* __restrict__ W1, double* __restrict__ tnrm_g, int* __restrict__ gate) {
+  if (*gate) return;
+  extern __shared__ double sm[];
+  __shared__ double dd[PK_MAX], ee[PK_MAX], tau[PK_MAX], e2[PK_MAX], ds[PK_MAX], e2s[PK_MAX];
+  __shared__ double lam[8];
+  __shared__ double s_lo, s_hi;
+  const int epb = pc_epb(k);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* R = sm;                                        // k x k reflectors (ld k)
+  double* zb = sm + (size_t)k * k;                       // [epb][k]: D+ then z
+  double* dm = zb + (size_t)epb * k;                     // [epb][k]: D-
+  const int m0 = blockIdx.x * epb;
+  // reflectors -> shared memory, asynchronously (needed only by the back-transformation)
+  {
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(R);
+    const int nel = k * k;
+    for (int e = threadIdx.x; e < nel; e += EPT)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + 8u * (unsigned)e), "l"(Rg + e) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < k; i += EPT) {
+    dd[i] = tri[i];
+    ee[i] = tri[k + i];
+    tau[i] = tri[2 * k + i];
+  }
+  __syncthreads();
+  // Gershgorin bounds (fixed order, warp 0)
+  if (warp == 0) {
+    double lo = 1e300, hi = -1e300;
+    for (int i = lane; i < k; i += 32) {
+      const double r = (i > 0 ? fabs(ee[i - 1]) : 0.0) + (i + 1 < k ? fabs(ee[i]) : 0.0);
+      lo = fmin(lo, dd[i] - r);
+      hi = fmax(hi, dd[i] + r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) { s_lo = lo; s_hi = hi; }
+  }
+  __syncthreads();
+  const double glo = s_lo, ghi = s_hi;
+  const double tnrm = fmax(fmax(fabs(glo), fabs(ghi)), 1e-300);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *tnrm_g = tnrm;
+  const int sx = ilogb(tnrm);
+  for (int i = threadIdx.x; i < k; i += EPT) {
     ds[i] = ldexp(dd[i], -sx);
     const double es = ldexp(ee[i], -sx);
     e2s[i] = es * es;
@@ -368,147 +605,145 @@ __global__ void __launch_bounds__(PT, 1)
   __syncthreads();
   const double eps = 2.220446049250313e-16;
   const double pivmin = fmax(tnrm * 2.2250738585072014e-308 / eps, 2.2250738585072014e-308);
-  {
-    const double sn = ldexp(tnrm, -sx);                  // in [1, 2)
-    const double atol = 2.0 * eps * sn;
-    const double lo0 = ldexp(glo, -sx) - (eps * sn + 2.0 * atol), hi0 = ldexp(ghi, -sx) + (eps * sn + 2.0 * atol);
-    const unsigned qshift = (unsigned)(lane & ~3);
-    for (int base = 0; base < k; base += PT / 4) {
-      const int m = base + quad;                        // m-th smallest eigenvalue
-      const bool act = m < k;
-      double lo = lo0, hi = hi0;
+  pc_mark(6);
+  // ---- eigenvalues: one warp per eigenvalue, 32-point multisection ----------------------
+  if (warp < epb) {
+    const int m = m0 + warp;                          // m-th smallest eigenvalue
+    if (m < k) {
+      const double sn = ldexp(tnrm, -sx);              // in [1, 2)
+      const double atol = 2.0 * eps * sn;
+      double lo = ldexp(glo, -sx) - (eps * sn + 2.0 * atol), hi = ldexp(ghi, -sx) + (eps * sn + 2.0 * atol);
+      const double inv33 = 1.0 / 33.0;
       for (int it = 0; it < 64; ++it) {
-        const bool more = act && hi - lo > fmax(atol, 4.0 * eps * fmax(fabs(lo), fabs(hi)));
-        if (!__any_sync(0xffffffffu, more)) break;
-        const double x = lo + (hi - lo) * (double)(ql + 1) * 0.2;
-        const int c = more ? pc_sturm(ds, e2s, k, x) : 0;
-        const unsigned bits = (__ballot_sync(0xffffffffu, more && c > m) >> qshift) & 0xfu;
-        if (more) {
-          const int f = bits ? __ffs(bits) - 1 : 4;
-          const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f * 0.2;
-          const double nhi = f == 4 ? hi : lo + (hi - lo) * (double)(f + 1) * 0.2;
-          lo = nlo;
-          hi = nhi;
-        }
+        if (!(hi - lo > fmax(atol, 4.0 * eps * fmax(fabs(lo), fabs(hi))))) break;   // warp-uniform
+        const double x = lo + (hi - lo) * (double)(lane + 1) * inv33;
+        const int c = pc_sturm(ds, e2s, k, x);
+        const unsigned bits = __ballot_sync(0xffffffffu, c > m);
+        const int f = bits ? __ffs(bits) - 1 : 32;
+        const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f * inv33;
+        const double nhi = f == 32 ? hi : lo + (hi - lo) * (double)(f + 1) * inv33;
+        lo = nlo;
+        hi = nhi;
       }
-      if (act && ql == 0) lam[m] = ldexp(0.5 * (lo + hi), sx);
+      if (lane == 0) {
+        const double l = ldexp(0.5 * (lo + hi), sx);
+        lam[warp] = l;
+        lam_g[m] = l;
+      }
     }
   }
   __syncthreads();
-  pc_mark(6);
-  for (int i = threadIdx.x; i < k; i += PT) lam_g[i] = lam[i];
-  // ---- 3. Q = H_0 H_1 ... H_{k-3}, one column per warp, straight to global -------------
-  // Column c of Q is H_0 ... H_{k-3} e_c; H_j leaves e_c alone for j >= c, so the warp
-  // starts from v = e_c (registers, lane holds rows lane + 32 t) and applies H_{min(c-1,k-3)}
-  // down to H_0: v -= tau_j (u_j . v) u_j.  The reflectors stay read-only in S: no barrier.
-  for (int c = warp; c < k; c += PNW) {
+  pc_mark(7);
+  // ---- eigenvectors of the tridiagonal: twisted factorisation, two lanes per eigenvalue ----
+  if (threadIdx.x < 2 * epb) {
+    const int e = threadIdx.x >> 1, side = threadIdx.x & 1, m = m0 + e;
+    const bool act = m < k;
+    const double lm = act ? lam[e] : 0.0;
+    double* z = zb + (size_t)e * k;
+    double* dmn = dm + (size_t)e * k;
+    if (act) {
+      if (side == 0) {
+        double q = dd[0] - lm;
+        if (fabs(q) < pivmin) q = -pivmin;
+        z[0] = q;
+        for (int i = 1; i < k; ++i) {
+          q = (dd[i] - lm) - pc_fast_div(e2[i - 1], q);
+          if (fabs(q) < pivmin) q = -pivmin;
+          z[i] = q;
+        }
+      } else {
+        double q = dd[k - 1] - lm;
+        if (fabs(q) < pivmin) q = -pivmin;
+        dmn[k - 1] = q;
+        for (int i = k - 2; i >= 0; --i) {
+          q = (dd[i] - lm) - pc_fast_div(e2[i], q);
+          if (fabs(q) < pivmin) q = -pivmin;
+          dmn[i] = q;
+        }
+      }
+    }
+    const unsigned pm = (1u << (2 * epb)) - 1u;
+    __syncwarp(pm);
+    int r = 0;
+    if (act && side == 0) {
+      double best = 1e300;
+      for (int i = 0; i < k; ++i) {
+        const double g = fabs(z[i] + dmn[i] - (dd[i] - lm));
+        if (g < best) { best = g; r = i; }
+      }
+    }
+    r = __shfl_sync(pm, r, threadIdx.x & ~1);
+    __syncwarp(pm);
+    double nrm = 0.0;
+    if (act) {
+      double xv = 1.0;
+      if (side == 0) {
+        for (int i = r - 1; i >= 0; --i) {
+          xv = -pc_fast_div(ee[i], z[i]) * xv;
+          z[i] = xv;
+          nrm = fma(xv, xv, nrm);
+        }
+        z[r] = 1.0;
+        nrm += 1.0;
+      } else {
+        for (int i = r + 1; i < k; ++i) {
+          xv = -pc_fast_div(ee[i - 1], dmn[i]) * xv;
+          z[i] = xv;
+          nrm = fma(xv, xv, nrm);
+        }
+      }
+    }
+    nrm += __shfl_xor_sync(pm, nrm, 1);
+    __syncwarp(pm);
+    if (act) {
+      nrm = sqrt(nrm);
+      if (!(nrm > 0.0) || !isfinite(nrm)) {
+        *gate = 1;
+      } else {
+        const double inv = 1.0 / nrm;
+        if (side == 0) { for (int i = 0; i <= r; ++i) z[i] *= inv; }
+        else { for (int i = r + 1; i < k; ++i) z[i] *= inv; }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  pc_mark(8);
+  // ---- back-transformation: W1[:, k-1-m] = H_0 ... H_{k-3} z, one warp per eigenvector ----
+  constexpr int RT = (PK_MAX + 31) / 32;
+  if (warp < epb && m0 + warp < k) {
+    const double* z = zb + (size_t)warp * k;
     double v[RT];
 #pragma unroll
-    for (int t = 0; t < RT; ++t) v[t] = (lane + 32 * t == c) ? 1.0 : 0.0;
-    for (int j = std::min(c - 1, k - 3); j >= 0; --j) {
+    for (int t = 0; t < RT; ++t) {
+      const int i = lane + 32 * t;
+      v[t] = i < k ? z[i] : 0.0;
+    }
+    for (int j = k - 3; j >= 0; --j) {
       const double tj = tau[j];
       if (tj == 0.0) continue;
-      const double* uj = S + j * ld;
+      const double* uj = R + (size_t)j * k;          // zero at rows <= j
+      double ur[RT];
       double sum = 0.0;
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const int i = lane + 32 * t;
-        if (i > j && i < k) sum = fma(uj[i], v[t], sum);
+        ur[t] = i < k ? uj[i] : 0.0;
+        sum = fma(ur[t], v[t], sum);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       const double wc = tj * sum;
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int i = lane + 32 * t;
-        if (i > j && i < k) v[t] = fma(-uj[i], wc, v[t]);
-      }
+      for (int t = 0; t < RT; ++t) v[t] = fma(-ur[t], wc, v[t]);
     }
+    double* out = W1 + (size_t)(k - 1 - (m0 + warp)) * k;
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
       const int i = lane + 32 * t;
-      if (i < k) Qg[(size_t)c * k + i] = v[t];
+      if (i < k) out[i] = v[t];
     }
   }
-  __syncthreads();
-  pc_mark(7);
-  // ---- 4. eigenvectors of the tridiagonal: twisted factorisation, one thread each, into
-  // the (now free) shared matrix; D- in global scratch -------------------------------------
-  double* dminus = wk;                      // [k][k], dminus[i * k + m]
-  for (int m = threadIdx.x; m < k; m += PT) {
-    const double lm = lam[m];
-    double* z = S + (size_t)(k - 1 - m) * ld;   // descending column order; holds D+ first
-    double q = dd[0] - lm;
-    if (fabs(q) < pivmin) q = -pivmin;
-    z[0] = q;
-    for (int i = 1; i < k; ++i) {
-      q = (dd[i] - lm) - pc_fast_div(e2[i - 1], q);
-      if (fabs(q) < pivmin) q = -pivmin;
-      z[i] = q;
-    }
-    q = dd[k - 1] - lm;
-    if (fabs(q) < pivmin) q = -pivmin;
-    dminus[(size_t)(k - 1) * k + m] = q;
-    for (int i = k - 2; i >= 0; --i) {
-      q = (dd[i] - lm) - pc_fast_div(e2[i], q);
-      if (fabs(q) < pivmin) q = -pivmin;
-      dminus[(size_t)i * k + m] = q;
-    }
-    int r = 0;
-    double best = 1e300;
-    for (int i = 0; i < k; ++i) {
-      const double g = fabs(z[i] + dminus[(size_t)i * k + m] - (dd[i] - lm));
-      if (g < best) { best = g; r = i; }
-    }
-    double xv = 1.0;
-    for (int i = r - 1; i >= 0; --i) {
-      xv = -pc_fast_div(ee[i], z[i]) * xv;
-      z[i] = xv;
-    }
-    z[r] = 1.0;
-    xv = 1.0;
-    for (int i = r + 1; i < k; ++i) {
-      xv = -pc_fast_div(ee[i - 1], dminus[(size_t)i * k + m]) * xv;
-      z[i] = xv;
-    }
-    double nrm = 0.0;
-    for (int i = 0; i < k; ++i) nrm = fma(z[i], z[i], nrm);
-    nrm = sqrt(nrm);
-    if (!(nrm > 0.0) || !isfinite(nrm)) { flag = 0; continue; }
-    const double inv = 1.0 / nrm;
-    for (int i = 0; i < k; ++i) z[i] *= inv;
-  }
-  __syncthreads();
-  pc_mark(8);
-  // numerically coincident clusters: Gram-Schmidt (twice), one thread per cluster
-  const double ctol = 1e-9 * tnrm;
-  for (int m0 = threadIdx.x; m0 < k; m0 += PT) {
-    if (m0 > 0 && lam[m0] - lam[m0 - 1] <= ctol) continue;
-    int m1 = m0 + 1;
-    while (m1 < k && lam[m1] - lam[m1 - 1] <= ctol) ++m1;
-    for (int m = m0 + 1; m < m1; ++m) {
-      double* z = S + (size_t)(k - 1 - m) * ld;
-      for (int pass = 0; pass < 2; ++pass)
-        for (int mm = m0; mm < m; ++mm) {
-          const double* y = S + (size_t)(k - 1 - mm) * ld;
-          double dot = 0.0;
-          for (int i = 0; i < k; ++i) dot = fma(y[i], z[i], dot);
-          for (int i = 0; i < k; ++i) z[i] -= dot * y[i];
-        }
-      double nrm = 0.0;
-      for (int i = 0; i < k; ++i) nrm = fma(z[i], z[i], nrm);
-      nrm = sqrt(nrm);
-      if (!(nrm > 1e-8)) { flag = 0; continue; }
-      for (int i = 0; i < k; ++i) z[i] /= nrm;
-    }
-  }
-  __syncthreads();
-  if (!flag) {
-    if (threadIdx.x == 0) *gate = 1;
-    return;
-  }
-  for (int j = warp; j < k; j += PNW)
-    for (int i = lane; i < k; i += 32) Zg[(size_t)j * k + i] = S[j * ld + i];
   pc_mark(9);
 }
 
@@ -516,13 +751,25 @@ __global__ void __launch_bounds__(PT, 1)
 __global__ void __launch_bounds__(256)
     k_pc_finish(const double* __restrict__ lam, const double* __restrict__ Y, int k, double* __restrict__ values,
                 double* __restrict__ vectors, int* __restrict__ n_out, int* __restrict__ status,
-                const int* __restrict__ gate) {
+                const double* __restrict__ tnrm_g, int* __restrict__ gate) {
   if (*gate) return;
   const int c = blockIdx.x;                  // one column per CTA
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ double sb[8];
   __shared__ int si[8];
   __shared__ int s_neg;
+  // numerically coincident eigenvalues (gap <= 1e-9 of the Gershgorin bound): the twisted
+  // vectors are not orthogonal there -- every CTA sees the same verdict and leaves the
+  // pencil to the general kernel
+  {
+    const double ctol = 1e-9 * *tnrm_g;
+    int clus = 0;
+    for (int m = 1 + threadIdx.x; m < k; m += blockDim.x) clus |= (lam[m] - lam[m - 1] <= ctol) ? 1 : 0;
+    if (__syncthreads_or(clus)) {
+      if (c == 0 && threadIdx.x == 0) *gate = 1;
+      return;
+    }
+  }
   double best = -1.0;
   int bi = 0x7fffffff;
   for (int r = threadIdx.x; r < k; r += blockDim.x) {
@@ -565,19 +812,23 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
   double* X = p;            // L^-1
   double* T1 = p + kk;      // X sym(B)
   double* T = p + 2 * kk;   // T1 X^T
-  double* Z = p + 3 * kk;
-  double* Q = p + 4 * kk;
+  double* R = p + 3 * kk;   // reflectors of the tridiagonalisation
+  double* tri = p + 4 * kk; // d | e | tau | tnrm (3k + 1 <= kk for k >= 4; else T1, dead by then)
   double* W1 = p + 5 * kk;  // Q Z
   double* Y = p + 6 * kk;   // X^T W1
   double* lam = p + 7 * kk;
-  double* dminus = T1;      // scratch of k_pc_tri (T1 is dead by then)
+  if (3 * (size_t)k + 1 > kk) tri = T1;
+  double* tnrm = tri + 3 * k;
   const size_t shm = (size_t)k * (k | 1) * sizeof(double);
+  const size_t shm_e = (kk + 2 * (size_t)pc_epb(k) * k) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)((size_t)PK_MAX * (PK_MAX | 1) * sizeof(double))));
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_tri, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)((size_t)PK_MAX * (PK_MAX | 1) * sizeof(double))));
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_eigvec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(((size_t)PK_MAX * PK_MAX + 2 * pc_epb(PK_MAX) * PK_MAX) * sizeof(double))));
     attr = true;
   }
   const dim3 gg((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
@@ -586,12 +837,15 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
   k_pc_gemm<false, false, true><<<gg, 256, 0, st>>>(X, B, T1, k, gate);
   k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);
   OFRR_CHECK_LAUNCH();
-  k_pc_tri<<<1, PT, shm, st>>>(T, k, lam, Z, Q, dminus, gate);
+  if (k <= 64) k_pc_tri_reg<8, 8><<<1, PT, 0, st>>>(T, k, tri, R, gate);
+  else if (k <= 128) k_pc_tri_reg<4, 32><<<1, PT, 0, st>>>(T, k, tri, R, gate);
+  else k_pc_tri<<<1, PT, shm, st>>>(T, k, tri, R, gate);
   OFRR_CHECK_LAUNCH();
-  k_pc_gemm<false, false, false><<<gg, 256, 0, st>>>(Q, Z, W1, k, gate);
+  k_pc_eigvec<<<(k + pc_epb(k) - 1) / pc_epb(k), EPT, shm_e, st>>>(tri, R, k, lam, W1, tnrm, gate);
+  OFRR_CHECK_LAUNCH();
   k_pc_gemm<true, false, false><<<gg, 256, 0, st>>>(X, W1, Y, k, gate);
   OFRR_CHECK_LAUNCH();
-  k_pc_finish<<<k, 256, 0, st>>>(lam, Y, k, values, vectors, n_out, status, gate);
+  k_pc_finish<<<k, 256, 0, st>>>(lam, Y, k, values, vectors, n_out, status, tnrm, gate);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
