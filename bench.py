@@ -54,6 +54,15 @@ CONFIGS = {
                       name="synthetic dense symmetric 65536x65536 (bf16 operator), geometric spectrum, top-64, "
                            "k=128, to 1e-8 (north-star target) by a precision ladder: fp32 basis on the bf16 "
                            "tensor cores, then fp64 basis with int8 Ozaki products"),
+    "c2-reuse": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-2, policy="full-f32", reuse=True,
+                     name="as c2, with A-pass reuse (IterConfig.reuse_av): the restart block's MatVec is "
+                          "W Y from the projection (one A pass per outer iteration after the first)"),
+    "c3-ladder-reuse": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64", ladder="full-f32",
+                            reuse=True,
+                            name="as c3-ladder (65536^2, top-64, k=128, to 1e-8 by the fp32 -> fp64 ladder), "
+                                 "with A-pass reuse (IterConfig.reuse_av)"),
+    "c3-f64-reuse": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64", reuse=True,
+                         name="as c3-f64 (fp64 basis throughout, to 1e-8), with A-pass reuse (IterConfig.reuse_av)"),
     "c3-f64": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
                    name="synthetic dense symmetric 65536x65536 (bf16 operator), geometric spectrum, top-64, "
                         "k=128, to 1e-8 (the north-star target): fp64 basis, FP64-accurate int8 tensor-core "
@@ -259,7 +268,8 @@ def run_ours(args, cfg):
     A, _ = p.synthetic_symmetric(lam, fmt, seed=SEED, device=dev, row0=r0, rows=r1 - r0)
     icfg = p.IterConfig(k=k, m=MAX_OUTER, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
                         policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=tol, top=top,
-                        ladder=p.POLICY_PRESETS[cfg["ladder"]] if cfg.get("ladder") else None)
+                        ladder=p.POLICY_PRESETS[cfg["ladder"]] if cfg.get("ladder") else None,
+                        reuse_av=bool(cfg.get("reuse", False)))
 
     def solve(stats=None):
         return p.subspace_iter_eig(A, icfg, stats=stats, comm=comm, n_global=n)
@@ -361,6 +371,7 @@ def run_ours(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfg["name"], "n": n, "top": top, "k": k, "tol": tol, "policy": cfg["policy"],
+                   "ladder": cfg.get("ladder"), "reuse_av": bool(cfg.get("reuse", False)),
                    "outer_iterations_per_solve": stats.iterations and stats.iterations,
                    "a_passes_per_solve": stats.a_passes,
                    "converged": bool(stats.converged),

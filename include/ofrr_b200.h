@@ -172,6 +172,17 @@ int ofrr_ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, 
                       void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * A-pass reuse (IterConfig.reuse_av, an extension): the next power step A X with
+ * X = U Y taken from the projection's block product, A X = (A U) Y = W Y.  Replaces the
+ * MatVec of ofrr/driver.py:102-104 that follows the restart of :109.
+ * Xout = round(W Y[:, :r], x_fmt) (columns >= r zero-filled), colmax[j] = max |Xout[:, j]|
+ * (atomic max: zero it first; the input of ofrr_scale_columns), flags |= NONFINITE.
+ * ------------------------------------------------------------------------------- */
+int ofrr_reuse_power(const void* W, int64_t ldw, int w_fmt, int64_t n, int kp, const double* Y,
+                     int ldy, const int* r_dev, int r_max, void* Xout, int64_t ldx, int x_fmt,
+                     double* colmax, int* flags, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * K7: FP64 residuals  res[j] = || A v_j - lambda_j v_j ||_2 / |lambda_j|  (inf when
  * lambda_j == 0).  Replaces ofrr/projection.py:136-147 residual_report (eig branch).
  * A (rows x cols row-major, a_fmt) is promoted to fp64 exactly.  For the SVD branch

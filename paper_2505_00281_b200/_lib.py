@@ -62,6 +62,8 @@ _SIGS = {
     "ofrr_sym_eig": ([c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "ofrr_ritz_recover": ([c_vp, c_i64, c_int, c_i64, c_int, c_vp, c_int, c_vp, c_int, c_dbl, c_vp, c_i64,
                            c_vp, c_i64, c_int, c_vp, c_vp], c_int),
+    "ofrr_reuse_power": ([c_vp, c_i64, c_int, c_i64, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_i64, c_int, c_vp,
+                          c_vp, c_vp], c_int),
     "ofrr_residual_workspace": ([c_i64, c_int], c_sz),
     "ofrr_residual_workspace2": ([c_i64, c_i64, c_int, c_int, c_int], c_sz),
     "ofrr_ozaki_operator_workspace": ([c_i64, c_i64], c_sz),

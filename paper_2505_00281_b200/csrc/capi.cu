@@ -56,7 +56,7 @@ int small_eig(int mode, const double* A, const double* M, int k, double raw_tol,
               cudaStream_t st);
 int ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const double* Y, int ldy, const int* r_dev,
                  int r_max, double scale, double* Ut64, int64_t ldo64, void* Xout, int64_t ldx, int x_fmt, int* flags,
-                 cudaStream_t st);
+                 cudaStream_t st, double* colmax = nullptr);
 int generate_sym(int64_t n, int64_t row0, int64_t rows, int hadamard, const double* c, const double* s,
                  const double* Wf, const double* Mf, int r, void* A, int64_t lda, int a_fmt, cudaStream_t st);
 int start_block_pcg64(unsigned long long s_hi, unsigned long long s_lo, unsigned long long i_hi,
@@ -188,6 +188,14 @@ int ofrr_ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, 
                       int x_fmt, int* flags, void* stream) {
   return ritz_recover(U, ldu, u_fmt, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags,
                       S(stream));
+}
+
+int ofrr_reuse_power(const void* W, int64_t ldw, int w_fmt, int64_t n, int kp, const double* Y, int ldy,
+                     const int* r_dev, int r_max, void* Xout, int64_t ldx, int x_fmt, double* colmax, int* flags,
+                     void* stream) {
+  if (!Xout || !colmax || !valid_fmt(x_fmt)) { ofrr_set_error("reuse_power: invalid arguments"); return OFRR_ERR_INVALID; }
+  return ritz_recover(W, ldw, w_fmt, n, kp, Y, ldy, r_dev, r_max, 1.0, nullptr, 0, Xout, ldx, x_fmt, flags, S(stream),
+                      colmax);
 }
 
 size_t ofrr_residual_workspace(int64_t rows, int r) { return residual_ws(rows, r); }

@@ -13,9 +13,11 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     k_ritz(const T* __restrict__ U, int64_t ldu, int64_t n, int kp, const double* __restrict__ Y, int ldy,
            const int* __restrict__ r_dev, int r_max, double scale, double* __restrict__ Ut64, int64_t ldo64,
-           void* __restrict__ Xout, int64_t ldx, int x_fmt, int* __restrict__ flags) {
+           void* __restrict__ Xout, int64_t ldx, int x_fmt, int* __restrict__ flags,
+           double* __restrict__ colmax) {
   __shared__ double Us[16][65];
   __shared__ double Ys[16][65];
+  __shared__ double cm[64];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t m0 = (int64_t)blockIdx.x * 64;
   const int n0 = blockIdx.y * 64;
@@ -46,6 +48,9 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
   }
   int bad = 0;
+  if (colmax && tid < 64) cm[tid] = 0.0;
+  if (colmax) __syncthreads();
+  double cmax[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -59,22 +64,29 @@ __global__ void __launch_bounds__(256)
         const double xv = rnd(v, x_fmt);
         if (!isfinite(xv)) bad = 1;
         st_fmt(Xout, (int64_t)gj * ldx + gi, x_fmt, xv);
+        cmax[j] = fmax(cmax[j], fabs(xv));
       }
     }
   if (bad && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
+  if (colmax) {                       // column inf-norms of the rounded block (K2's input)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) atomic_max_nonneg(&cm[tx + 16 * j], cmax[j]);
+    __syncthreads();
+    if (tid < 64 && n0 + tid < r_max) atomic_max_nonneg(&colmax[n0 + tid], cm[tid]);
+  }
 }
 
 int ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const double* Y, int ldy, const int* r_dev,
                  int r_max, double scale, double* Ut64, int64_t ldo64, void* Xout, int64_t ldx, int x_fmt, int* flags,
-                 cudaStream_t st) {
+                 cudaStream_t st, double* colmax) {
   if (n <= 0 || r_max <= 0) return OFRR_OK;
   dim3 grid((unsigned)((n + 63) / 64), (unsigned)((r_max + 63) / 64));
   switch (u_fmt) {
-    case F64: k_ritz<double><<<grid, 256, 0, st>>>((const double*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
-    case F32: k_ritz<float><<<grid, 256, 0, st>>>((const float*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
-    case F16: k_ritz<__half><<<grid, 256, 0, st>>>((const __half*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
-    case BF16: k_ritz<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
-    case FP8: k_ritz<__nv_fp8_e4m3><<<grid, 256, 0, st>>>((const __nv_fp8_e4m3*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags); break;
+    case F64: k_ritz<double><<<grid, 256, 0, st>>>((const double*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case F32: k_ritz<float><<<grid, 256, 0, st>>>((const float*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case F16: k_ritz<__half><<<grid, 256, 0, st>>>((const __half*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case BF16: k_ritz<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case FP8: k_ritz<__nv_fp8_e4m3><<<grid, 256, 0, st>>>((const __nv_fp8_e4m3*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
     default: ofrr_set_error("ritz: basis format %d unsupported", u_fmt); return OFRR_ERR_UNSUPPORTED;
   }
   OFRR_CHECK_LAUNCH();

@@ -52,6 +52,8 @@ class IterConfig:
     top: Optional[int] = None     # extension: number of leading pairs checked
     ladder: Optional[PrecisionPolicy] = None   # extension: cheaper policy run first (see below)
     ladder_switch: float = 1e-3   # ... until its residual estimate falls below this (or stalls)
+    reuse_av: bool = False        # extension: next power step from the projection, A U Y = W Y (one
+    #                               A pass per outer iteration instead of iter + 1; see EigEngine)
 
     def __post_init__(self):
         if self.k < 1 or self.m < 1 or self.iter < 1 or self.restarts < 0:
@@ -218,12 +220,12 @@ class EigEngine:
         """X0 = PCG64(seed) U(0,1), rounded to the MatVec storage (ofrr/driver.py:97-99)."""
         return self.ops.start_block(self.cfg.seed, self.n, self.cfg.k, self.mv.storage, self.device)
 
-    def power(self, X, st):
+    def power(self, X, st, steps: Optional[int] = None):
         """cfg.iter MatVecs with inf-norm column scaling (ofrr/driver.py:102-105)."""
         import torch
         ops, comm = self.ops, self.comm
         k = X.k
-        for _ in range(self.cfg.iter):
+        for _ in range(self.cfg.iter if steps is None else steps):
             colmax = torch.zeros(k, dtype=torch.float64, device=self.device)
             W = ops.new_block(self.A_mv.rows, k, self.mv.storage, self.device)
             ops.gemm_av(self.A_mv, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1],
@@ -239,13 +241,34 @@ class EigEngine:
                 X = W
         return X
 
+    def power_from(self, W, eig, kp: int, st):
+        """A-pass reuse (cfg.reuse_av): the restart block is Ut = U Y, so its MatVec is
+        A Ut = (A U) Y = W Y with W the projection's block product (kept in its accumulation
+        format): X = round(W Y) to the MatVec storage, inf-norm scaled (ofrr/driver.py:
+        102-105), then the remaining cfg.iter - 1 MatVecs with A.  Same iterate as the
+        reference's A round(Ut) up to the rounding of Ut and the accumulation error of W."""
+        import torch
+        ops, comm = self.ops, self.comm
+        colmax = torch.zeros(kp, dtype=torch.float64, device=self.device)
+        X = ops.reuse_power(W, eig.vectors, kp, eig.n_out, kp, self.mv.storage, colmax,
+                            flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+        comm.all_reduce_max_(colmax)
+        ops.scale_columns(X, colmax, self.mv.compute)
+        if comm.distributed:
+            Xn = ops.new_block(self.n, kp, self.mv.storage, self.device)
+            comm.all_gather_rows(X.t, Xn.t, self.n, kp)
+            X = Xn
+        if self.cfg.iter > 1:
+            X = self.power(X, st, steps=self.cfg.iter - 1)
+        return X
+
     def basis(self, X, st):
         """Hessenberg basis (K3), redundant on every rank."""
         h = self.ops.hessenberg(X, self.pol.storage, self.pol.compute, self.pol.drop_tol)
         st[S_NKEPT:S_NKEPT + 1].copy_(h.n_kept)
         return h
 
-    def project(self, U, st, want64: bool, top_check: Optional[int] = None):
+    def project(self, U, st, want64: bool, top_check: Optional[int] = None, reuse: bool = False):
         """ofrr_eig (ofrr/projection.py:75-87) + restart block (ofrr/driver.py:109).
 
         With ``top_check`` the block product also keeps W = A U in its accumulation
@@ -255,7 +278,7 @@ class EigEngine:
         kp = U.k
         W = ops.new_block(self.A_pol.rows, kp, self.pol.storage, self.device)
         W2 = None
-        if top_check is not None:
+        if top_check is not None or reuse:
             acc = FpFormat.F64 if FpFormat.F64 in (self.A_pol.fmt, U.fmt) else FpFormat.F32
             W2 = ops.new_block(self.A_pol.rows, kp, acc, self.device)
         ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2,
@@ -275,13 +298,16 @@ class EigEngine:
         U64, Xn = ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=want64, x_fmt=self.mv.storage,
                            flags=st[S_RESTART_FLAGS:S_RESTART_FLAGS + 1])
         est = None
-        if W2 is not None:
+        if W2 is not None and top_check is not None:
             t = min(top_check, kp)
             est = ops.residual_estimate(Ul, W2, eig.vectors, kp, eig.values, eig.n_out, t,
                                         mode=2 if comm.distributed else 0)
             if comm.distributed:
                 comm.all_reduce_sum_(est)
+        Xp = self.power_from(W2, eig, kp, st) if reuse else None
         self._join(side)
+        if reuse:
+            return eig, U64, Xn, est, Xp
         return eig, U64, Xn, est
 
     def _fork_res_scales(self):
@@ -365,11 +391,12 @@ class EigEngine:
             # one iteration: power step(s), Hessenberg basis, projection with every column
             # (the basis keeps all k in the common case; dropped columns of Q are zero),
             # residual estimate -- replayed as one CUDA graph when possible.  One host sync.
-            out = self._graph_step(X, check, top) if use_graph and X.k == cfg.k else None
+            first = it == 0
+            out = self._graph_step(X, check, top, first) if use_graph and X.k == cfg.k else None
             if out is None:
-                out = self._body(X, check, top)
+                out = self._body(X, check, top, first)
                 if use_graph:
-                    _WARM.add(self._graph_key(check, top))
+                    _WARM.add(self._graph_key(check, top, first))
             st, h, U, eig, Xn, est = out["st"], out["h"], out["U"], out["eig"], out["Xn"], out["est"]
             kp = U.k
             s, vals_all, est_np = self._unpack(out, st, eig, est)      # the iteration's one sync
@@ -381,12 +408,17 @@ class EigEngine:
                 kp = int(s[S_NKEPT])
                 U = h.Q.narrow(kp)
                 st[S_EIG_STATUS:].zero_()                     # gram/pencil/restart slots
-                eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
+                res = self.project(U, st, want64=False, top_check=(top if check else None), reuse=cfg.reuse_av)
+                eig, _, Xn, est = res[:4]
+                out = dict(out, Xnext=res[4] if cfg.reuse_av else None)
                 s, vals_all, est_np = self._fetch(st, eig.values, est)
             _raise_for(s, "projection")
             r = int(s[S_NOUT])
             vals = vals_all[:r]
             X = Xn.narrow(r)
+            Xrestart = X                                           # the reference's restart block
+            if cfg.reuse_av:
+                X = out["Xnext"].narrow(r)                         # its MatVec, already made
             U64 = None
             self.stats.iterations = it + 1
             if check:
@@ -401,7 +433,7 @@ class EigEngine:
                     prev_est = worst
                     self.stats.history.append((it + 1, worst))
                     if rung_done and not last:
-                        return X                                   # next rung starts from here
+                        return Xrestart                            # next rung starts from here
                     continue
                 prev_est = worst
                 if worst < tol or stalled or last:
@@ -453,14 +485,21 @@ class EigEngine:
         return g.report
 
     # ---- one outer iteration: eager body, or a replayed CUDA graph of it -----------------
-    def _body(self, X, check: bool, top: int) -> dict:
+    def _body(self, X, check: bool, top: int, first: bool = True) -> dict:
+        """One outer iteration.  With cfg.reuse_av the input of every iteration but the
+        first is already the power-stepped block (the previous projection made it)."""
         import torch
         st = torch.zeros(8, dtype=torch.int32, device=self.device)
-        Xp = self.power(X, st)
+        reuse = self.cfg.reuse_av
+        Xp = self.power(X, st) if (first or not reuse) else X
         h = self.basis(Xp, st)
         U = h.Q.narrow(Xp.k)
-        eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
-        out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None)
+        Xnext = None
+        if reuse:
+            eig, _, Xn, est, Xnext = self.project(U, st, want64=False, top_check=(top if check else None), reuse=True)
+        else:
+            eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
+        out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None, Xnext=Xnext)
         if not self.comm.distributed:
             parts = [st.to(torch.float64), eig.values.reshape(-1).to(torch.float64)]
             if est is not None:
@@ -482,23 +521,26 @@ class EigEngine:
         return (self.ops is _ops and self.device.type == "cuda" and not self.comm.distributed
                 and os.environ.get("OFRR_CUDA_GRAPHS", "1") != "0")
 
-    def _graph_key(self, check: bool, top: int):
+    def _graph_key(self, check: bool, top: int, first: bool = True):
         A, B = self.A_mv, self.A_pol
         pol = lambda p: (int(p.storage), int(p.compute), int(p.accumulate), float(p.drop_tol))  # noqa: E731
         from . import _lib
         return (A.t.data_ptr(), A.rows, A.cols, A.lda, int(A.fmt), B.t.data_ptr(), B.rows, B.cols, B.lda, int(B.fmt),
                 self.n, self.cfg.k, self.cfg.iter, pol(self.pol), pol(self.mv), check, top, self.device.index,
-                bool(_lib.load().ofrr_prof_gemm_active()), self._refresh_now and self._res_oz is not None)
+                bool(_lib.load().ofrr_prof_gemm_active()), self._refresh_now and self._res_oz is not None,
+                self.cfg.reuse_av, first or not self.cfg.reuse_av,
+                # Ozaki workspaces the captured kernels read (made outside the capture)
+                tuple(sorted(oz.ws.data_ptr() for oz in self._oz.values())))
 
-    def _graph_step(self, X, check: bool, top: int):
+    def _graph_step(self, X, check: bool, top: int, first: bool = True):
         """Replay the captured iteration (capturing it first once the shapes have run
         eagerly in this process); None -> run it eagerly."""
-        key = self._graph_key(check, top)
+        key = self._graph_key(check, top, first)
         g = _GRAPHS.get(key)
         if g is None:
             if key not in _WARM or key in _NO_GRAPH:
                 return None
-            g = self._capture(X, check, top, key)
+            g = self._capture(X, check, top, key, first)
             if g is None:
                 return None
         else:
@@ -513,7 +555,7 @@ class EigEngine:
         out["graph"] = g
         return out
 
-    def _capture(self, X, check: bool, top: int, key):
+    def _capture(self, X, check: bool, top: int, key, first: bool = True):
         import torch
         from . import _lib
         L = _lib.load()
@@ -526,15 +568,21 @@ class EigEngine:
         try:
             with rec:
                 with torch.cuda.graph(graph):
-                    outs = self._body(Xs, check, top)
-                    Xs.t.copy_(outs["Xn"].t)                       # the next iteration's input
+                    outs = self._body(Xs, check, top, first)
+                    nxt = outs["Xnext"] if self.cfg.reuse_av else outs["Xn"]
+                    if first and self.cfg.reuse_av:
+                        pass                                       # input: the start block
+                    else:
+                        Xs.t.copy_(nxt.t)                          # the next iteration's input
         except Exception:                                             # capture unsupported: stay eager
             _NO_GRAPH.add(key)
             L.ofrr_prof_gemm_collect()
             return None
         prof_group = L.ofrr_prof_gemm_claim() if L.ofrr_prof_gemm_active() else -1
-        outs["Xn"] = Xs
+        if not (first and self.cfg.reuse_av):
+            outs["Xnext" if self.cfg.reuse_av else "Xn"] = Xs
         g = _IterGraph(graph, Xs, outs, rec, prof_group)
+        g.keep = [oz.ws for oz in self._oz.values()]     # buffers captured by reference
         g.a_passes = self.stats.a_passes - passes0       # passes the captured body makes
         self.stats.a_passes = passes0                    # counted again by the replay
         _GRAPHS[key] = g

@@ -455,6 +455,18 @@ def ritz(U: DevBlock, Y: torch.Tensor, ldy: int, r_dev: Optional[torch.Tensor], 
     return U64, X
 
 
+def reuse_power(W: DevBlock, Y: torch.Tensor, ldy: int, r_dev: Optional[torch.Tensor], r_max: int,
+                x_fmt: FpFormat, colmax: torch.Tensor, flags: Optional[torch.Tensor] = None) -> DevBlock:
+    """The next power step from the projection (A-pass reuse): X = round(W Y, x_fmt) with
+    W = A U, so X = A (U Y); colmax gets the column inf-norms of X (zeroed by the caller)."""
+    L = _lib.load()
+    X = new_block(W.n, r_max, x_fmt, W.device)
+    _lib.check(L.ofrr_reuse_power(W.ptr, W.ld, int(W.fmt), W.n, W.k, Y.data_ptr(), ldy, _p(r_dev), r_max, _p(X.t),
+                                  X.ld, int(x_fmt), colmax.data_ptr(), _p(flags), _stream()), "reuse_power")
+    _count(1)
+    return X
+
+
 def residual_estimate(U: DevBlock, W: DevBlock, Y: torch.Tensor, ldy: int, vals: torch.Tensor,
                       r_dev: Optional[torch.Tensor], r_max: int, mode: int = 0) -> torch.Tensor:
     """K7e: ||(W - lambda_j U) y_j|| / |lambda_j| (mode 0) or raw sums of squares (mode 2)."""

@@ -19,7 +19,9 @@ n, top, k = cfg["n"], cfg["top"], cfg["k"]
 lam = p.geometric_spectrum(n, top, k)
 A, _ = p.synthetic_symmetric(lam, p.FpFormat[cfg["fmt"]], seed=bench.SEED, device=dev)
 icfg = p.IterConfig(k=k, m=bench.MAX_OUTER, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
-                    policy=p.POLICY_PRESETS[cfg["policy"]], seed=bench.SEED, tol=cfg["tol"], top=top)
+                    policy=p.POLICY_PRESETS[cfg["policy"]], seed=bench.SEED, tol=cfg["tol"], top=top,
+                    ladder=p.POLICY_PRESETS[cfg["ladder"]] if cfg.get("ladder") else None,
+                    reuse_av=bool(cfg.get("reuse", False)))
 for _ in range(3):
     p.subspace_iter_eig(A, icfg)
 torch.cuda.synchronize()

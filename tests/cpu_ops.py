@@ -137,6 +137,12 @@ def ritz(U, Y, ldy, r_dev, r_max, scale=1.0, want64=True, x_fmt=None, flags=None
     return U64, X
 
 
+def reuse_power(W, Y, ldy, r_dev, r_max, x_fmt, colmax, flags=None):
+    _, X = ritz(W, Y, ldy, r_dev, r_max, want64=False, x_fmt=x_fmt)
+    colmax.copy_(torch.maximum(colmax, torch.from_numpy(np.max(np.abs(_np(X)), axis=0))))
+    return X
+
+
 def residual_estimate(U, W, Y, ldy, vals, r_dev, r_max, mode=0):
     r = min(r_max, int(r_dev.item()) if r_dev is not None else r_max)
     y = Y.numpy().T[: U.k, :r]

@@ -28,7 +28,10 @@ def _problem():
     return a
 
 
-def _run(a_rows, n, comm, tol=None):
+CASES = ((None, False), (1e-4, False), (None, True), (1e-4, True))   # (tol, reuse_av)
+
+
+def _run(a_rows, n, comm, tol=None, reuse=False):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -36,7 +39,7 @@ def _run(a_rows, n, comm, tol=None):
     import paper_2505_00281_b200 as p
     from paper_2505_00281_b200.driver import EigEngine
     cfg = p.IterConfig(k=K, m=M, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
-                       policy=p.FULL_F32, seed=SEED, tol=tol, top=TOP if tol else None)
+                       policy=p.FULL_F32, seed=SEED, tol=tol, top=TOP if tol else None, reuse_av=reuse)
     eng = EigEngine(cpu_ops.RowBlock(a_rows, p.FpFormat.F32), cfg, comm=comm, n_global=n, ops=cpu_ops)
     rs = eng.run()
     return rs.values, rs.vectors.data if hasattr(rs.vectors, "data") else None, rs.residuals, eng.stats
@@ -52,9 +55,9 @@ def _worker(rank, world, port, q):
         comm = Comm.world()
         a = _problem()
         r0, r1 = comm.row_range(N)
-        for tol in (None, 1e-4):
-            vals, _, res, st = _run(a[r0:r1], N, comm, tol=tol)
-            q.put((rank, tol, vals, res, st.iterations, st.a_passes))
+        for tol, reuse in CASES:
+            vals, _, res, st = _run(a[r0:r1], N, comm, tol=tol, reuse=reuse)
+            q.put((rank, (tol, reuse), vals, res, st.iterations, st.a_passes))
     finally:
         dist.destroy_process_group()
 
@@ -71,14 +74,14 @@ def test_row_partitioned_matches_single_process():
     sys.path.insert(0, ROOT)
     from paper_2505_00281_b200.comm import Comm
     a = _problem()
-    single = {tol: _run(a, N, Comm(), tol=tol) for tol in (None, 1e-4)}
+    single = {(tol, reuse): _run(a, N, Comm(), tol=tol, reuse=reuse) for tol, reuse in CASES}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for pr in procs:
         pr.start()
-    out = [q.get(timeout=180) for _ in range(4)]
+    out = [q.get(timeout=180) for _ in range(2 * len(CASES))]
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
@@ -94,6 +97,20 @@ def test_row_partitioned_matches_single_process():
         by_tol.setdefault(tol, []).append(vals)
     for tol, vs in by_tol.items():
         np.testing.assert_array_equal(vs[0], vs[1])
+
+
+def test_reuse_av_single_process():
+    """A-pass reuse (IterConfig.reuse_av): the next MatVec comes from the projection's
+    W = A U (A U Y = W Y), one A pass per outer iteration after the first instead of
+    iter + 1; same Ritz values as the reference's schedule to its precision."""
+    sys.path.insert(0, ROOT)
+    from paper_2505_00281_b200.comm import Comm
+    a = _problem()
+    v0, _, r0, st0 = _run(a, N, Comm(), tol=None, reuse=False)
+    v1, _, r1, st1 = _run(a, N, Comm(), tol=None, reuse=True)
+    assert st0.a_passes == 2 * M and st1.a_passes == M + 1
+    np.testing.assert_allclose(v1[:TOP], v0[:TOP], rtol=1e-5)
+    assert np.all(r1[:TOP] <= 2 * r0[:TOP] + 1e-6)
 
 
 def test_comm_row_ranges():

@@ -248,3 +248,49 @@ def test_driver_svd_tensor_core_vs_oracle(ofrr_gpu, oracle, pname):
     ref = o.subspace_iter_svd(a, k=k, m=m, iters=1, pol=o.as_pol(pol), seed=SEED)
     exact = np.linalg.svd(a, compute_uv=False)
     _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pname", ["tc-bf16", "full-f32", "full-f64"])
+def test_driver_reuse_av_vs_oracle(ofrr_gpu, oracle, pname):
+    """IterConfig.reuse_av: the MatVec of the restart block comes from the projection's
+    W = A U (A U Y = W Y, ofrr_reuse_power) -- one A pass per outer iteration after the
+    first.  Parity with the oracle's reference schedule (north-star criteria) and the pass
+    count."""
+    p, o = ofrr_gpu, oracle
+    n, top, k, m = 1024, 10, 20, 8
+    lam = p.geometric_spectrum(n, top, k)
+    A, f = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    a_host = o.sym_from_factors(n, f.hadamard, f.c, f.s, f.Wf, f.Mf, o.BF16)
+    pol = p.POLICY_PRESETS[pname]
+    opol = {"tc-bf16": o.TC_BF16, "full-f32": o.FULL_F32, "full-f64": o.FULL_F64}[pname]
+    cfg = p.IterConfig(k=k, m=m, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=pol, seed=SEED, reuse_av=True)
+    st = p.RunStats()
+    rs = p.subspace_iter_eig(A, cfg, stats=st)
+    assert st.a_passes == m + 1
+    ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=opol, seed=SEED)
+    exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+    if pname == "full-f64":
+        assert np.max(rs.residuals[:top]) < 1e-8
+
+
+@pytest.mark.gpu
+def test_driver_reuse_av_ladder_to_tol(ofrr_gpu):
+    """reuse_av with the precision ladder and a time-to-tolerance stop (the C3 north-star
+    configuration at reduced n): converges to the FP64 tolerance with fewer A passes."""
+    p = ofrr_gpu
+    n, top, k = 4096, 16, 32
+    lam = p.geometric_spectrum(n, top, k)
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    res = {}
+    for reuse in (False, True):
+        cfg = p.IterConfig(k=k, m=40, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                           policy=p.FULL_F64, ladder=p.FULL_F32, seed=SEED, tol=1e-9, top=top, reuse_av=reuse)
+        st = p.RunStats()
+        rs = p.subspace_iter_eig(A, cfg, stats=st)
+        assert st.converged and np.max(rs.residuals[:top]) < 1e-9
+        res[reuse] = (rs, st)
+    np.testing.assert_allclose(res[True][0].values[:top], res[False][0].values[:top], rtol=1e-12)
+    assert res[True][1].a_passes < res[False][1].a_passes
