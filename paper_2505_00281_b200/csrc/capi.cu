@@ -382,6 +382,8 @@ extern "C" int ofrr_debug_k5_profile(long long* out8) { return ofrr::k5_profile(
 namespace ofrr { int hess_profile(unsigned long long* out); int pc_profile(unsigned long long* out); }
 extern "C" int ofrr_debug_pencil_profile(unsigned long long* out16) { return ofrr::pc_profile(out16); }
 extern "C" int ofrr_debug_hess_profile(unsigned long long* out8) { return ofrr::hess_profile(out8); }
+namespace ofrr { int hess_mode(int force_global, int pb); }
+extern "C" int ofrr_debug_hess_mode(int force_global, int pb) { return ofrr::hess_mode(force_global, pb); }
 
 namespace ofrr {
 void prof_enable(int on); int prof_read(float* ms, int max); int prof_active(); int prof_collect();

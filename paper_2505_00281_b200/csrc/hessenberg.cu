@@ -151,13 +151,19 @@ template <typename T, int C>
 __global__ void __launch_bounds__(HT)
     k_hessenberg(const T* __restrict__ X, int64_t n, int k, int64_t ldx, T* __restrict__ Xg, int64_t ldg,
                  double tol, T* __restrict__ Q, int64_t ldq, int64_t* __restrict__ pivots, int* __restrict__ kept,
-                 int* __restrict__ n_kept, HessWs ws, int in_smem) {
+                 int* __restrict__ n_kept, HessWs ws, int in_smem, int pb) {
   using CV = typename CT<C>::type;
   __shared__ double sv[HT / 32];
   __shared__ long long si[HT / 32];
   extern __shared__ double dyn[];
   double* prow = dyn;                                        // pivot row values, k entries
   CV* pc = reinterpret_cast<CV*>(dyn + k);                   // alpha_c (compute format), k entries
+  // panel mode (pb > 1): the pivot rows of the panel's kept steps (compute format, k each)
+  // and their column indices; columns beyond the panel take those steps in one blocked
+  // update at the panel's end (each element read and written once per panel)
+  CV* PR = reinterpret_cast<CV*>(dyn + 2 * k);
+  __shared__ int s_pl[32];                                   // kept steps of the panel
+  __shared__ int s_npl;
 
   const int G = gridDim.x, c = blockIdx.x;
   const int64_t rows_per = (n + G - 1) / G;
@@ -167,7 +173,22 @@ __global__ void __launch_bounds__(HT)
   // my working rows: in shared memory when they fit (column-major, ld rows_per), else in
   // the global workspace.  Xw is indexed with global row numbers.
   const int64_t ldw = in_smem ? rows_per : ldg;
-  T* Xw = in_smem ? reinterpret_cast<T*>(dyn + 2 * k) - r0 : Xg;
+  const size_t pr_dbl = pb > 1 ? ((size_t)pb * k * sizeof(CV) + 7) / 8 : 0;   // PR, in doubles
+  T* Xw = in_smem ? reinterpret_cast<T*>(dyn + 2 * k + pr_dbl) - r0 : Xg;
+  // rows in global memory + panels: the current panel's columns are cached in shared
+  // memory (col(cc) is a row-indexed pointer to column cc wherever it lives)
+  const bool pwc = !in_smem && pb > 1;
+  T* Pw = reinterpret_cast<T*>(dyn + 2 * k + pr_dbl);
+  int cp0 = -1;
+  auto col = [&](int cc) -> T* {
+    return (pwc && cc >= cp0 && cc < cp0 + pb) ? Pw + (int64_t)(cc - cp0) * nr - r0 : Xw + (int64_t)cc * ldw;
+  };
+  auto load_panel = [&](int q0) {   // global -> shared memory (caller syncs before and after)
+    const int qe = min(k, q0 + pb);
+    for (int cc = q0; cc < qe; ++cc)
+      for (int64_t i = threadIdx.x; i < nr; i += HT) Pw[(int64_t)(cc - q0) * nr + i] = Xw[(int64_t)cc * ldw + r0 + i];
+    cp0 = q0;
+  };
   // thread -> (row, column phase) for the trailing updates: two threads per row when the
   // row block is at most half the CTA
   const int tpr = (2 * nr <= HT) ? 2 : 1;
@@ -179,6 +200,10 @@ __global__ void __launch_bounds__(HT)
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Xw[(int64_t)j * ldw + i] = X[(int64_t)j * ldx + i];
   for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) ws.freerow[i] = 1;
   __syncthreads();
+  if (pwc) {
+    load_panel(0);
+    __syncthreads();
+  }
 
   // split grid barrier: arrive (release) ... independent work ... wait (acquire).  One
   // monotonically increasing arrival counter (zeroed before the launch): barrier number p
@@ -210,7 +235,7 @@ __global__ void __launch_bounds__(HT)
   auto local_scan = [&](int jn, double& v, long long& idx, unsigned long long& key) {
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
       if (!ws.freerow[i]) continue;
-      const double a = fabs(el_d(Xw[(int64_t)jn * ldw + i]));
+      const double a = fabs(el_d(col(jn)[i]));
       if constexpr (KEYED) {
         const unsigned long long kk = cand_key((float)a, i);
         key = kk > key ? kk : key;
@@ -223,7 +248,9 @@ __global__ void __launch_bounds__(HT)
   // *after* the current step's elimination.  Columns > jn may still be pending (deferred)
   // in Xw: their values for the candidate row are formed here with exactly the arithmetic
   // of the deferred update.
-  auto publish = [&](int jn, int buf, bool pending, int jp, double v, long long idx, unsigned long long key) {
+  // pending beyond the panel: columns >= pe still owe the panel's kept steps s_pl[0..npl)
+  auto publish = [&](int jn, int buf, bool pending, int jp, double v, long long idx, unsigned long long key,
+                     int pe, int npl) {
     if constexpr (KEYED) {
       key = block_max_key(key, sk);
       idx = key ? (long long)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull)) : -1;
@@ -236,21 +263,59 @@ __global__ void __launch_bounds__(HT)
       }
     }
     if (idx >= 0) {
-      const CV vr = pending ? ld_c<C>(Xw[(int64_t)jp * ldw + idx]) : CV(0);
+      const CV vr = pending ? ld_c<C>(col(jp)[idx]) : CV(0);
       for (int cc = jn + threadIdx.x; cc < k; cc += HT) {
-        T y = Xw[(int64_t)cc * ldw + idx];
-        if (pending && cc > jn) y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(pc[cc], vr)));
+        T y = col(cc)[idx];
+        if (cc < pe) {
+          if (pending && cc > jn) y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(pc[cc], vr)));
+        } else {
+          for (int q = 0; q < npl; ++q)    // the panel's kept steps, in order (bitwise the blocked update)
+            y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(PR[(size_t)q * k + cc], ld_c<C>(col(s_pl[q])[idx]))));
+        }
         ws.cand_row[((int64_t)buf * G + c) * k + cc] = el_d(y);
       }
     }
   };
+  // panel end: columns >= pe take the panel's kept steps, element by element in step order
+  auto blocked_update = [&](int pe, int npl) {
+    if (npl == 0 || pe >= k) return;
+    // thread per row: the row's npl multipliers in registers, the pivot rows broadcast
+    // from shared memory, each trailing element read and written once (coalesced)
+    constexpr int QMAX = 32;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+      CV mult[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) mult[q] = q < npl ? ld_c<C>(col(s_pl[q])[i]) : CV(0);
+      // columns >= pe live in global memory; eight at a time, every load issued before the
+      // stores (the stores could alias the next loads otherwise, serialising the latency)
+      constexpr int CB = 8;
+      T* base = Xw + (int64_t)pe * ldw + i;
+      for (int c0 = pe; c0 < k; c0 += CB, base += CB * ldw) {
+        T y[CB];
+#pragma unroll
+        for (int u = 0; u < CB; ++u) y[u] = c0 + u < k ? base[(int64_t)u * ldw] : T();
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          if (q < npl) {
+#pragma unroll
+            for (int u = 0; u < CB; ++u)
+              y[u] = st_s<T>(csub<C>(ld_c<C>(y[u]), cmul<C>(PR[(size_t)q * k + min(c0 + u, k - 1)], mult[q])));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < CB; ++u)
+          if (c0 + u < k) base[(int64_t)u * ldw] = y[u];
+      }
+    }
+  };
 
+  if (threadIdx.x == 0) s_npl = 0;
   {
     double v = -1.0;
     long long idx = -1;
     unsigned long long key = 0;
     local_scan(0, v, idx, key);
-    publish(0, 0, false, 0, v, idx, key);
+    publish(0, 0, false, 0, v, idx, key, k, 0);
   }
   arrive();
   wait();
@@ -265,6 +330,10 @@ __global__ void __launch_bounds__(HT)
   __shared__ int s_owner;
   for (int j = 0; j < k; ++j) {
     const int buf = j & 1;
+    // panel [p0, pe): its columns take every step at once; columns >= pe wait for the
+    // panel's end (pb <= 1: one panel, the whole block)
+    const int p0 = pb > 1 ? (j / pb) * pb : 0;
+    const int pe = pb > 1 ? min(k, p0 + pb) : k;
     double best;
     long long r;
     int owner;
@@ -313,10 +382,16 @@ __global__ void __launch_bounds__(HT)
       }
       if (r >= r0 && r < r1 && threadIdx.x == 0) ws.freerow[r] = 0;
       if (c == 0 && threadIdx.x == 0) { kept[j] = 1; pivots[nk] = r; }
+      if (pb > 1 && pe < k) {                                  // this step, owed by columns >= pe
+        const int q = s_npl;
+        for (int cc = pe + threadIdx.x; cc < k; cc += HT)
+          PR[(size_t)q * k + cc] = (CV)__ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
+      }
       __syncthreads();
+      if (pb > 1 && pe < k && threadIdx.x == 0) { s_pl[s_npl] = j; s_npl = s_npl + 1; }
       mark(1);
       const CV piv = pc[j];
-      const CV a1 = j + 1 < k ? pc[j + 1] : CV(0);
+      const CV a1 = j + 1 < pe ? pc[j + 1] : CV(0);
       // ofrr/basis.py:181-187: v = round_s(round_c(v / piv)); v[r] = 1; then (188-190,
       // precision.py:172-180) column j+1 at once -- the next pivot search needs it -- and
       // this thread's candidate for it
@@ -324,11 +399,11 @@ __global__ void __launch_bounds__(HT)
       long long cidx = -1;
       unsigned long long ckey = 0;
       for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
-        const T v = (i == r) ? st_s<T>(CV(1)) : st_s<T>(cdiv<C>(ld_c<C>(Xw[(int64_t)j * ldw + i]), piv));
-        Xw[(int64_t)j * ldw + i] = v;
+        const T v = (i == r) ? st_s<T>(CV(1)) : st_s<T>(cdiv<C>(ld_c<C>(col(j)[i]), piv));
+        col(j)[i] = v;
         Q[(int64_t)nk * ldq + i] = v;
-        if (j + 1 < k) {
-          T* yp = Xw + (int64_t)(j + 1) * ldw + i;
+        if (j + 1 < pe) {
+          T* yp = col(j + 1) + i;
           const T y = st_s<T>(csub<C>(ld_c<C>(*yp), cmul<C>(a1, ld_c<C>(v))));
           *yp = y;
           if (i != r && ws.freerow[i]) {
@@ -343,20 +418,21 @@ __global__ void __launch_bounds__(HT)
         }
       }
       mark(2);
-      if (j + 1 < k) {
-        publish(j + 1, buf ^ 1, true, j, cv, cidx, ckey);
+      if (j + 1 < pe) {
+        __syncthreads();                                       // s_pl / s_npl visible
+        publish(j + 1, buf ^ 1, true, j, cv, cidx, ckey, pe, pb > 1 ? s_npl : 0);
         arrive();
         mark(3);
         // ... columns j+2.. while the other CTAs catch up (hidden behind the barrier).
         // Two rows x two columns per iteration, all loads before the stores (ILP).
         for (int64_t i0 = r0 + trow; i0 < r1; i0 += 2 * rb) {
           const bool h1 = i0 + rb < r1;
-          const CV v0 = ld_c<C>(Xw[(int64_t)j * ldw + i0]);
-          const CV v1 = h1 ? ld_c<C>(Xw[(int64_t)j * ldw + i0 + rb]) : CV(0);
-          T* p = Xw + (int64_t)(j + 2 + tcol) * ldw + i0;
-          const int64_t st1 = (int64_t)tpr * ldw;
+          const CV v0 = ld_c<C>(col(j)[i0]);
+          const CV v1 = h1 ? ld_c<C>(col(j)[i0 + rb]) : CV(0);
+          T* p = col(j + 2 + tcol) + i0;
+          const int64_t st1 = (int64_t)tpr * (pwc ? nr : ldw);   // panel columns only
           int cc = j + 2 + tcol;
-          for (; cc + tpr < k; cc += 2 * tpr, p += 2 * st1) {
+          for (; cc + tpr < pe; cc += 2 * tpr, p += 2 * st1) {
             const CV a0 = pc[cc], a1 = pc[cc + tpr];
             const CV y00 = ld_c<C>(p[0]), y01 = ld_c<C>(p[st1]);
             const CV y10 = h1 ? ld_c<C>(p[rb]) : CV(0), y11 = h1 ? ld_c<C>(p[st1 + rb]) : CV(0);
@@ -367,7 +443,7 @@ __global__ void __launch_bounds__(HT)
               p[st1 + rb] = st_s<T>(csub<C>(y11, cmul<C>(a1, v1)));
             }
           }
-          if (cc < k) {
+          if (cc < pe) {
             const CV a0 = pc[cc];
             const CV y00 = ld_c<C>(p[0]);
             const CV y10 = h1 ? ld_c<C>(p[rb]) : CV(0);
@@ -379,16 +455,44 @@ __global__ void __launch_bounds__(HT)
         mark(4);
         wait();
         mark(5);
+      } else if (pe < k) {
+        // the panel's last column: columns >= pe take its kept steps, then column pe's search
+        __syncthreads();
+        blocked_update(pe, s_npl);
+        __syncthreads();
+        if (threadIdx.x == 0) s_npl = 0;                       // next panel (read after the barrier)
+        if (pwc) {
+          load_panel(pe);
+          __syncthreads();
+        }
+        double v = -1.0;
+        long long idx = -1;
+        unsigned long long key = 0;
+        local_scan(pe, v, idx, key);
+        publish(pe, buf ^ 1, false, 0, v, idx, key, k, 0);
+        arrive();
+        wait();
       }
       ++nk;
     } else {
       if (c == 0 && threadIdx.x == 0) kept[j] = 0;
       if (j + 1 < k) {
+        __syncthreads();
+        const bool pend = j + 1 == pe;                         // panel end: blocked update first
+        if (pend) {
+          blocked_update(pe, s_npl);
+          __syncthreads();
+          if (threadIdx.x == 0) s_npl = 0;
+          if (pwc) {
+            load_panel(pe);
+            __syncthreads();
+          }
+        }
         double v = -1.0;
         long long idx = -1;
         unsigned long long key = 0;
         local_scan(j + 1, v, idx, key);
-        publish(j + 1, buf ^ 1, false, 0, v, idx, key);
+        publish(j + 1, buf ^ 1, false, 0, v, idx, key, pend ? k : pe, pend ? 0 : (pb > 1 ? s_npl : 0));
         arrive();
         wait();
       }
@@ -418,6 +522,16 @@ static int hess_grid(int64_t n) {
   }
   int64_t g = (n + min_rows - 1) / min_rows;
   return (int)std::max<int64_t>(1, std::min<int64_t>(sms, g));
+}
+
+// test/tuning knobs (ofrr_debug_hess_mode): rows in global memory even when they fit in
+// shared memory; the panel width of the global-memory mode (-1: default)
+static int g_hess_force_global = 0;
+static int g_hess_pb = -2;
+int hess_mode(int force_global, int pb) {
+  g_hess_force_global = force_global;
+  g_hess_pb = pb;
+  return 0;
 }
 
 size_t hessenberg_ws(int64_t n, int k, int storage) {
@@ -453,8 +567,22 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   const size_t tile = (size_t)rows_per * k * sizeof(T);
   // up to the 227 KB opt-in per CTA (one CTA per SM): C3's fp32 rows (443 x 128) fit
   const size_t smem_max = 226 * 1024;
-  int in_smem = (size_t)2 * k * sizeof(double) + tile + 16 <= smem_max ? 1 : 0;
-  size_t shmem = (size_t)2 * k * sizeof(double) + (in_smem ? tile + 16 : 0);
+  // rows in shared memory: no panels (the per-step trailing update hides behind the grid
+  // barrier).  Rows in global memory: panels of pb (32) columns cached in shared memory, the
+  // columns beyond the panel updated once per panel (OFRR_HESS_PANEL overrides pb, <= 32)
+  if (g_hess_pb == -2) { const char* e = getenv("OFRR_HESS_PANEL"); g_hess_pb = e ? atoi(e) : -1; }
+  const int pb_env = g_hess_pb;
+  auto pr_bytes = [&](int b) { return b > 1 ? (((size_t)b * k * sizeof(typename CT<C>::type) + 7) / 8) * 8 : 0; };
+  const size_t base = (size_t)2 * k * sizeof(double);
+  int in_smem = (base + tile + 16 <= smem_max && !g_hess_force_global) ? 1 : 0;
+  int pb = 1;
+  size_t shmem = base + (in_smem ? tile + 16 : 0);
+  if (!in_smem) {
+    for (int b = pb_env >= 1 ? std::min(pb_env, 32) : 32; b > 1; b /= 2) {
+      const size_t need = base + pr_bytes(b) + (size_t)rows_per * b * sizeof(T) + 16;
+      if (need <= smem_max) { pb = b; shmem = need; break; }
+    }
+  }
   static bool attr = false;
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute((const void*)k_hessenberg<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -464,7 +592,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   (void)storage; (void)compute;
   void* args[] = {(void*)&Xp, (void*)&n, (void*)&k, (void*)&ldx, (void*)&Xw, (void*)&ldw, (void*)&tol,
                   (void*)&Qp, (void*)&ldq, (void*)&pivots, (void*)&kept, (void*)&n_kept, (void*)&h,
-                  (void*)&in_smem};
+                  (void*)&in_smem, (void*)&pb};
   OFRR_CUDA_TRY(cudaMemsetAsync(kept, 0, sizeof(int) * k, st));
   OFRR_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hessenberg<T, C>, dim3(G), dim3(HT), args, shmem, st));
   return OFRR_OK;

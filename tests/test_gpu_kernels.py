@@ -153,6 +153,36 @@ def test_hessenberg_bitwise(ofrr_gpu, oracle, pol, n, k):
     np.testing.assert_array_equal(_host(h.Q, nk), q)
 
 
+@pytest.mark.parametrize("pol", [(BF16, F32, F32), (F32, F32, F32), (F64, F64, F64), (FP8, BF16, F32)])
+@pytest.mark.parametrize("pb", [1, 8, 32])
+def test_hessenberg_global_panels_bitwise(ofrr_gpu, oracle, pol, pb):
+    """K3's global-memory mode (row blocks too large for shared memory, e.g. C3's fp64 rung)
+    with panel-deferred trailing updates: still the reference's Q, pivots and kept mask bit
+    for bit, including a dependent (dropped) column and a panel boundary inside the block."""
+    import ctypes
+    from paper_2505_00281_b200 import ops, _lib
+    p, o = ofrr_gpu, oracle
+    s, c, a_ = pol
+    n, k = 6000, 45
+    rng = np.random.default_rng(7)
+    x = o.round_to(rng.random((n, k)) - 0.5, s)
+    x[:, 9] = o.round_to(2.0 * x[:, 4], s)                 # dependent column -> skipped
+    L = _lib.load()
+    L.ofrr_debug_hess_mode.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.ofrr_debug_hess_mode(1, pb)
+    try:
+        h = ops.hessenberg(_blk(p, x, s), p.FpFormat(s), p.FpFormat(c), o.EPS[s])
+        nk = int(h.n_kept.item())
+        Q = _host(h.Q, nk)
+    finally:
+        L.ofrr_debug_hess_mode(0, -1)
+    q, piv, kept = o.hessenberg_basis(x, o.Pol(s, c, a_))
+    assert nk == q.shape[1]
+    np.testing.assert_array_equal(h.pivots[:nk].cpu().numpy(), piv)
+    np.testing.assert_array_equal(h.kept[:k].cpu().numpy().astype(bool), kept)
+    np.testing.assert_array_equal(Q, q)
+
+
 @pytest.mark.parametrize("case", ["f64_20x6", "f16_25x8", "mh_64x10", "f32_64x10", "tc16_300x12", "dep_6x3",
                                   "ties_8x3"])
 def test_hessenberg_golden(ofrr_gpu, golden, case):
