@@ -603,9 +603,10 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
       const uint64_t pol_v = policy_evict_last();
       int vs = 0;
       uint32_t vph = 0;
+      int vt = (int)(u0 / kbc), rem = (int)(u0 % kbc);     // (tile, k-block) of u, no divisions per step
       for (long long u = u0; u < u1; ++u) {
-        const int vt = (int)(u / kbc);
-        const int kb = (vt % nchunks) * kbc + (int)(u % kbc);
+        const int kb = (vt % nchunks) * kbc + rem;
+        if (++rem == kbc) { rem = 0; ++vt; }
         mbar_wait(&vempty[vs], vph ^ 1);
         mbar_expect_tx(&vfull[vs], C::V_SET);
         for (int q = 0; q < OZ_D; ++q)
@@ -699,9 +700,13 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
     float sc = 0.0f;
     bool fast = false, row_ok = false;
     uint4 nxt[2];
-    auto fetch = [&](long long u, uint4 (&raw)[2]) {
-      const int vt = (int)(u / kbc);
-      const int kb = (vt % nchunks) * kbc + (int)(u % kbc);
+    // (tile, k-block) of the next fetch, advanced without 64-bit divisions (they were a
+    // fifth of the converters' instructions)
+    int fvt = (int)(u0 / kbc), frem = (int)(u0 % kbc);
+    auto fetch = [&](long long /*u*/, uint4 (&raw)[2]) {
+      const int vt = fvt;
+      const int kb = (vt % nchunks) * kbc + frem;
+      if (++frem == kbc) { frem = 0; ++fvt; }
       const int64_t grow = (int64_t)(vt / nchunks) * OZ_TM + r;
       raw[0] = raw[1] = make_uint4(0, 0, 0, 0);
       if (grow >= rows) return;
@@ -718,12 +723,14 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
       }
     };
     if (u0 < u1) fetch(u0, nxt);
+    int lvt = (int)(u0 / kbc), lrem = (int)(u0 % kbc);
     for (long long u = u0; u < u1; ++u) {
       uint4 raw[4];
       raw[0] = nxt[0];
       raw[1] = nxt[1];
       if (u + 1 < u1) fetch(u + 1, nxt);                 // prefetch the next k-block's entries
-      const int vt = (int)(u / kbc);
+      const int vt = lvt;
+      if (++lrem == kbc) { lrem = 0; ++lvt; }
       if (vt != cur_vt) {
         cur_vt = vt;
         const int64_t grow = (int64_t)(vt / nchunks) * OZ_TM + r;
