@@ -281,9 +281,11 @@ def run_ours(args, cfg):
 
     from paper_2505_00281_b200 import _lib
     L = _lib.load()
-    # warm-up with the kernel timers on, so the CUDA graph of the outer iteration (captured
-    # during the warm-up) carries the K1 timing events the timed region harvests
-    L.ofrr_prof_gemm_enable(1)
+    # warm-up with the K1 in-kernel timers on (kernel arguments baked into the CUDA graphs
+    # captured during the warm-up: the outer iteration, the FP64 report and the device-side
+    # loop that replays them, csrc/loop.cu)
+    import ctypes
+    L.ofrr_prof_k1_stamp(1)
     for _ in range(args.warmup):
         solve()
     barrier()
@@ -294,7 +296,7 @@ def run_ours(args, cfg):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
-        L.ofrr_prof_gemm_enable(1)
+        L.ofrr_prof_k1_stamp(1)                          # zero the K1 accumulators
         e0.record()
         for _ in range(args.steps):
             rs = solve(stats)
@@ -304,24 +306,24 @@ def run_ours(args, cfg):
     ms_total = e0.elapsed_time(e1)
     log = ops.GEMM_LOG
     ops.GEMM_LOG = None
-    import ctypes
-    buf = (ctypes.c_float * 4096)()
-    nk = L.ofrr_prof_gemm_read(ctypes.addressof(buf), 4096)
-    L.ofrr_prof_gemm_enable(0)
-    durs = [float(buf[i]) for i in range(max(nk, 0))]
+    k1_ms, k1_n = ctypes.c_double(0.0), ctypes.c_longlong(0)
+    L.ofrr_prof_k1_read(ctypes.byref(k1_ms), ctypes.byref(k1_n))
+    k1_ms, k1_n = float(k1_ms.value), int(k1_n.value)
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    # dominant kernel (K1, k_gemm_av_tc): algorithmic bytes / kernel-only CUDA-event duration
-    nl = min(len(durs), len(log))
-    nbytes = float(np.mean([b for b, _ in log[:nl]])) if nl else float("nan")
-    flops = float(np.mean([f for _, f in log[:nl]])) if nl else float("nan")
-    avg_ms = float(np.mean(durs[:nl])) if nl else float("nan")
+    # dominant kernel (K1, k_gemm_av_tc): algorithmic bytes / its average launch duration,
+    # from the kernel's own first-entry / last-exit globaltimer stamps of every launch in the
+    # timed region (CUDA event nodes cannot live inside the device-side loop's graph)
+    nl = min(k1_n, len(log))
+    nbytes = float(np.mean([b for b, _ in log])) if log else float("nan")
+    flops = float(np.mean([f for _, f in log])) if log else float("nan")
+    avg_ms = k1_ms / k1_n if k1_n else float("nan")
     hbm, bf16_peak, peak_kind = _peaks()
     achieved = nbytes / (avg_ms * 1e-3) / 1e9
-    gemm_share = float(np.sum(durs)) / ms_total if ms_total > 0 else None
+    gemm_share = k1_ms / ms_total if ms_total > 0 else None
 
     # ---- e2e: public API with HOST buffers (A from pinned host memory, results back) --
     # Every step copies A host -> device into the caller's operator buffer (DenseMatrix.on_device,
@@ -378,11 +380,13 @@ def run_ours(args, cfg):
                    "max_residual_top": float(np.max(rs.residuals[:top])),
                    "parallelism": f"row-partitioned x{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (A = %d MiB per GPU)" % ((r1 - r0) * n * 2 >> 20)},
-        "roofline": {"kernel": "k_gemm_av_tc (K1, A.X block product; kernel-only CUDA events)", "bound": "hbm",
+        "roofline": {"kernel": "k_gemm_av_tc (K1, A.X block product; in-kernel globaltimer stamps per launch)",
+                     "bound": "hbm",
                      "achieved": _num(achieved), "peak": hbm, "unit": "GB/s", "frac": _num(achieved / hbm),
                      "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                      "bytes_per_launch": _num(nbytes),
-                     "avg_launch_ms": _num(avg_ms), "launches": len(durs), "share_of_step": gemm_share,
+                     "avg_launch_ms": _num(avg_ms), "launches": k1_n, "launches_logged": len(log),
+                     "share_of_step": gemm_share,
                      "tflops": _num(flops / (avg_ms * 1e-3) / 1e12), "tflops_peak_bf16": bf16_peak,
                      "launches_per_solve": nl / args.steps},
         "cpu_baseline": cpu,

@@ -106,6 +106,39 @@ int ofrr_prof_gemm_active(void);
 int ofrr_prof_gemm_collect(void);
 int ofrr_prof_gemm_claim(void);
 int ofrr_prof_gemm_collect_group(int group);
+/* The same measurement from inside the kernels (usable inside CUDA graphs with device-side
+ * loops, which cannot hold event nodes): while enabled (at launch/capture time), each
+ * k_gemm_av_tc launch stamps its first CTA entry and last CTA exit (globaltimer) and its
+ * k_finalize accumulates the interval; read returns the summed ms and the launch count. */
+int ofrr_prof_k1_stamp(int on);
+int ofrr_prof_k1_read(double* sum_ms, long long* count);
+
+/* ---------------------------------------------------------------------------------
+ * Device-side outer loop (ofrr/driver.py:101-111 with the tol extension) as one CUDA graph:
+ *   init -> first(iteration graph, e.g. with the start block's MatVec) -> decide
+ *        -> [copy first_out -> steady_in] -> WHILE(continue) { steady iteration -> decide
+ *        -> IF(report) { FP64 report graph -> confirm } }
+ * decide reads the iteration's status word (int32[8], driver layout) and the leading
+ * `top` residual estimates: non-finite / empty / narrowed basis or a pencil error stop the
+ * loop with a state for the host; otherwise it requests the FP64 report when the estimate
+ * passes tol, stalls (> 0.5x the previous, < 16 tol) or the iteration is the m-th; confirm
+ * stops the loop when the FP64 residuals pass.  ctl (device, ofrr_loop_ctl_bytes) holds the
+ * state, iteration count and per-iteration estimate / FP64 histories.  The graphs are
+ * cudaGraph_t handles (e.g. torch.cuda.CUDAGraph(keep_graph=True).raw_cuda_graph()); the
+ * result is an instantiated cudaGraphExec_t (launch / destroy below).
+ * ------------------------------------------------------------------------------- */
+#define OFRR_LOOP_RUNNING 0
+#define OFRR_LOOP_CONVERGED 1       /* FP64 residuals of the leading `top` pairs < tol */
+#define OFRR_LOOP_EXHAUSTED 2       /* m iterations, report made, not converged */
+#define OFRR_LOOP_HOST 3            /* a case the host loop handles (status error, narrowed
+                                       basis, report requested after the first iteration) */
+size_t ofrr_loop_ctl_bytes(void);
+int ofrr_loop_build(void* first_graph, void* steady_graph, void* report_graph, const int* st_first,
+                    const double* est_first, const int* st_steady, const double* est_steady,
+                    const double* res_report, const void* copy_src, void* copy_dst, size_t copy_bytes,
+                    void* ctl, int m, int top, int k, double tol, void** exec_out);
+int ofrr_loop_launch(void* exec, void* stream);
+int ofrr_loop_destroy(void* exec);
 
 /* K2: X[:,j] <- round_s(round_c(X[:,j] / colmax[j])) for colmax[j] != 0, in place.
  * Replaces ofrr/precision.py:159-169 scale_columns_inf. */

@@ -50,6 +50,13 @@ _SIGS = {
     "ofrr_prof_gemm_collect": ([], c_int),
     "ofrr_prof_gemm_claim": ([], c_int),
     "ofrr_prof_gemm_collect_group": ([c_int], c_int),
+    "ofrr_prof_k1_stamp": ([c_int], c_int),
+    "ofrr_prof_k1_read": ([c_vp, c_vp], c_int),
+    "ofrr_loop_ctl_bytes": ([], c_sz),
+    "ofrr_loop_build": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_int, c_int, c_int,
+                         c_dbl, c_vp], c_int),
+    "ofrr_loop_launch": ([c_vp, c_vp], c_int),
+    "ofrr_loop_destroy": ([c_vp], c_int),
     "ofrr_scale_columns": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_vp, c_vp], c_int),
     "ofrr_hessenberg_workspace": ([c_i64, c_int, c_int], c_sz),
     "ofrr_hessenberg": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp,

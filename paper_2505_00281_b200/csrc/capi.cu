@@ -395,3 +395,6 @@ extern "C" int ofrr_prof_gemm_active(void) { return ofrr::prof_active(); }
 extern "C" int ofrr_prof_gemm_collect(void) { return ofrr::prof_collect(); }
 extern "C" int ofrr_prof_gemm_claim(void) { return ofrr::prof_claim(); }
 extern "C" int ofrr_prof_gemm_collect_group(int group) { return ofrr::prof_collect_group(group); }
+namespace ofrr { int stamp_enable(int on); int stamp_read(double* sum_ms, long long* count); }
+extern "C" int ofrr_prof_k1_stamp(int on) { return ofrr::stamp_enable(on); }
+extern "C" int ofrr_prof_k1_read(double* sum_ms, long long* count) { return ofrr::stamp_read(sum_ms, count); }

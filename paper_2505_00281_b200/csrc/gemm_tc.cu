@@ -57,12 +57,24 @@ struct Segments {
   int kblocks;
 };
 
+// ---- in-kernel timing of k_gemm_av_tc for the bench roofline (works inside CUDA graphs
+// with device-side loops, where event nodes are not allowed): every CTA stamps its entry
+// (min) and exit (max) in globaltimer ns; the launch's k_finalize (stream-ordered after it)
+// adds the interval to a running sum and re-arms the stamps. ----
+__device__ unsigned long long g_k1_stamp[4] = {~0ull, 0ull, 0ull, 0ull};   // min start, max end, sum, count
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int BN, bool FP8K>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_av_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  float* __restrict__ ws, int kblocks, long long total_iters, int max_slots,
-                 uint32_t idesc) {
+                 uint32_t idesc, int stamp) {
   using C = TcCfg<BN>;
+  if (stamp && threadIdx.x == 0) atomicMin(&g_k1_stamp[0], gtimer_ns());
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
@@ -174,6 +186,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (stamp && threadIdx.x == 0) atomicMax(&g_k1_stamp[1], gtimer_ns());
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
@@ -190,7 +203,13 @@ __global__ void __launch_bounds__(256)
     k_finalize(const float* __restrict__ ws, int BN, int kblocks, long long total_iters, int G,
                int max_slots, int64_t rows, int k, void* __restrict__ W, int64_t ldw, int out_fmt,
                double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
-               int out_fmt2, int nsplit) {
+               int out_fmt2, int nsplit, int stamp) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
+    const unsigned long long t0 = g_k1_stamp[0], t1 = g_k1_stamp[1];
+    if (t1 > t0) { g_k1_stamp[2] += t1 - t0; g_k1_stamp[3] += 1; }
+    g_k1_stamp[0] = ~0ull;
+    g_k1_stamp[1] = 0ull;
+  }
   // nsplit > 1: the product was taken against [X_hi | X_mid | X_lo] (bf16 slices of an fp32
   // block, see k_split_bf16); output column j sums tile columns j + s*k, lowest slice first
   __shared__ float smax[8][FIN_COLS];
@@ -387,6 +406,23 @@ int prof_collect_group(int g) {
   return prof_harvest(g_prof_groups[g]);
 }
 
+static bool g_stamp_on = false;
+int stamp_enable(int on) {
+  g_stamp_on = on != 0;
+  if (on) {
+    const unsigned long long z[4] = {~0ull, 0ull, 0ull, 0ull};
+    if (cudaMemcpyToSymbol(g_k1_stamp, z, sizeof(z)) != cudaSuccess) return OFRR_ERR_CUDA;
+  }
+  return OFRR_OK;
+}
+int stamp_read(double* sum_ms, long long* count) {
+  unsigned long long v[4];
+  if (cudaMemcpyFromSymbol(v, g_k1_stamp, sizeof(v)) != cudaSuccess) return OFRR_ERR_CUDA;
+  *sum_ms = (double)v[2] * 1e-6;
+  *count = (long long)v[3];
+  return OFRR_OK;
+}
+
 int prof_read(float* ms, int max) {
   if (prof_collect() != 0) return -1;
   std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -436,7 +472,7 @@ static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPl
   }
   cudaEvent_t* ev = prof_slot();
   if (ev) prof_record(ev[0], st);
-  kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc);
+  kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc, g_stamp_on ? 1 : 0);
   if (ev) prof_record(ev[1], st);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
@@ -468,7 +504,7 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
   if (rc) return rc;
   k_finalize<<<dim3(p.m_tiles, (k / nsplit + FIN_COLS - 1) / FIN_COLS), 256, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
                                         rows, k / nsplit, W, ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
-                                        nsplit);
+                                        nsplit, g_stamp_on ? 1 : 0);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }

@@ -111,6 +111,7 @@ class RunStats:
     history: list = field(default_factory=list)   # (iteration, max residual over top)
     converged: bool = False
     a_passes: int = 0
+    device_loop: bool = False     # the outer loop ran as one graph with device-side control flow
 
 
 # status-vector slots (one int32[8] device vector, read once per sync point)
@@ -130,6 +131,26 @@ class _IterGraph:
     def __init__(self, graph, Xs, outs, rec, prof_group):
         self.graph, self.Xs, self.outs, self.rec, self.prof_group = graph, Xs, outs, rec, prof_group
         self.report = None      # _ReportGraph of the final Ritz vectors + FP64 residuals
+
+
+def _loop_debug(*msg) -> None:
+    import os
+    if os.environ.get("OFRR_LOOP_DEBUG"):
+        print("[device loop]", *msg, flush=True)
+
+
+class _LoopExec:
+    """An instantiated device-loop graph (cudaGraphExec_t), destroyed with its owner."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            from . import _lib
+            _lib.load().ofrr_loop_destroy(self.handle)
+        except Exception:
+            pass
 
 
 class _ReportGraph:
@@ -385,6 +406,10 @@ class EigEngine:
         self._block_oz(self.A_mv, X)                 # FP64 blocks: slice A once per run, eagerly
         if self.mv.storage != self.pol.storage:
             self._ozaki(self.A_pol) if self.pol.storage == FpFormat.F64 else None
+        if use_graph and check and stop_estimate is None and X.k == cfg.k and cfg.m >= 2:
+            rs = self._device_loop(X, top)
+            if rs is not None:
+                return rs
         for it in range(cfg.m):
             last = it == cfg.m - 1
             self._refresh_now = it == 0      # A's report scales: once per run (A may change between runs)
@@ -449,6 +474,109 @@ class EigEngine:
             rs = self._final_report(out, U, eig, U.k, r, vals, check, top)
         return rs
 
+    def _device_loop(self, X, top: int):
+        """The whole outer loop as one CUDA graph with device-side control flow (csrc/loop.cu):
+        the first iteration's graph, then the steady iteration graph inside a conditional
+        WHILE node, the FP64 report inside a conditional IF node -- the host launches once
+        and reads the control block once.  Needs the three graphs captured by earlier solves
+        of the same shapes; returns None when they are missing or the device stopped for a
+        case the host loop handles (errors, a narrowed basis), and the caller then runs the
+        host loop from the same start block (deterministic: same result)."""
+        import ctypes
+        import time
+        import torch
+        from . import _lib
+        t0 = time.perf_counter()
+        cfg = self.cfg
+        L = _lib.load()
+        self._refresh_now = True
+        kf = self._graph_key(True, top, True)
+        self._refresh_now = False
+        ks = self._graph_key(True, top, False)
+        gf, gs = _GRAPHS.get(kf), _GRAPHS.get(ks)
+        if gf is None or gs is None or gs.report is None or gf.outs.get("est") is None:
+            _loop_debug("graphs missing", gf is None, gs is None, gs is not None and gs.report is None)
+            return None
+        lk = (cfg.m, top, float(cfg.tol), id(gf))
+        loops = gs.__dict__.setdefault("loops", {})
+        lp = loops.get(lk)
+        if lp is None:
+            ctl = torch.zeros(int(L.ofrr_loop_ctl_bytes()), dtype=torch.uint8, device=self.device)
+            if gf is gs:
+                src = dst = None
+                nbytes = 0
+            else:
+                src_blk = gf.outs["Xnext"] if cfg.reuse_av else gf.Xs
+                src, dst = src_blk.t.data_ptr(), gs.Xs.t.data_ptr()
+                nbytes = gs.Xs.t.numel() * gs.Xs.t.element_size()
+                if src_blk.t.numel() != gs.Xs.t.numel():
+                    return None
+            ex = ctypes.c_void_p()
+            rc = L.ofrr_loop_build(gf.graph.raw_cuda_graph(), gs.graph.raw_cuda_graph(),
+                                   gs.report.graph.raw_cuda_graph(), gf.outs["st"].data_ptr(),
+                                   gf.outs["est"].data_ptr(), gs.outs["st"].data_ptr(), gs.outs["est"].data_ptr(),
+                                   gs.report.res.data_ptr(), src, dst, nbytes, ctl.data_ptr(), cfg.m, top, cfg.k,
+                                   float(cfg.tol), ctypes.byref(ex))
+            if rc != 0:
+                _loop_debug("build failed", _lib.last_error())   # the host loop takes over
+                loops[lk] = None
+                return None
+            lp = loops[lk] = (_LoopExec(ex.value), ctl)
+        elif lp is None:
+            return None
+        ex, ctl = lp
+        t1 = time.perf_counter()
+        if X.t.data_ptr() != gf.Xs.t.data_ptr():
+            gf.Xs.t.copy_(X.t)
+        t2 = time.perf_counter()
+        _lib.check(L.ofrr_loop_launch(ex.handle, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
+                   "loop_launch")
+        t3 = time.perf_counter()
+        # the solve's one synchronisation: control block, values and FP64 residuals in one
+        # pinned buffer
+        k = cfg.k
+        nb = ctl.numel()
+        stage = gs.__dict__.get("stage")
+        if stage is None:
+            stage = gs.stage = torch.empty(nb + 8 * (2 * k), dtype=torch.uint8, pin_memory=True)
+        stage[:nb].copy_(ctl, non_blocking=True)
+        stage[nb:nb + 8 * k].view(torch.float64).copy_(gs.outs["pack"][8:8 + k], non_blocking=True)
+        stage[nb + 8 * k:].view(torch.float64).copy_(gs.report.res[:k], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        host = stage
+        t4 = time.perf_counter()
+        head = host[:16].view(torch.int32).numpy()
+        state, its = int(head[0]), int(head[1])
+        if state not in (1, 2):
+            _loop_debug("device stopped for the host", state, its)
+            return None
+        hist = host[24:nb].view(torch.float64).numpy()
+        nh = (hist.size) // 2
+        est_h, fp64_h = hist[:nh], hist[nh:]
+        vals = host[nb:nb + 8 * k].view(torch.float64).numpy().copy()
+        res = host[nb + 8 * k:].view(torch.float64).numpy().copy()
+        rg = gs.report
+        self.stats.iterations = its
+        self.stats.a_passes += gf.a_passes + (its - 1) * gs.a_passes
+        for i in range(min(its, nh)):
+            self.stats.history.append((i + 1, float(fp64_h[i]) if fp64_h[i] >= 0 else float(est_h[i])))
+        self.stats.converged = state == 1
+        self.stats.device_loop = True
+        # launch / GEMM-log accounting of what ran on the device (bench.py gpu_launches, roofline)
+        nrep = int(np.sum(fp64_h[:min(its, nh)] >= 0))
+        gf.rec.replayed()
+        for _ in range(its - 1):
+            gs.rec.replayed()
+        for _ in range(nrep):
+            rg.rec.replayed()
+        self.ops._count(1 + its + nrep)                      # init, decide per iteration, confirm per report
+        U64c = self.ops.DevBlock(rg.U64.t.clone(), rg.U64.n, k, rg.U64.fmt)
+        out = RitzSet(np.array(vals), DenseMatrix.from_block(U64c), "eig", residuals=res)
+        t5 = time.perf_counter()
+        _loop_debug(f"host us: keys {1e6 * (t1 - t0):.0f} copy {1e6 * (t2 - t1):.0f} launch {1e6 * (t3 - t2):.0f} "
+                    f"sync {1e6 * (t4 - t3):.0f} post {1e6 * (t5 - t4):.0f}")
+        return out
+
     def _final_report(self, out, U, eig, kp, r, vals, check, top) -> RitzSet:
         """Ritz vectors in fp64 and the FP64 residual report -- replayed as a CUDA graph when
         the iteration came from one (full width), eager otherwise."""
@@ -471,7 +599,7 @@ class EigEngine:
     def _capture_report(self, g, U, eig, kp, r):
         import torch
         rec = self.ops.Recorder()
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=True)
         torch.cuda.synchronize(self.device)
         try:
             with rec:
@@ -562,7 +690,7 @@ class EigEngine:
         Xs = self.ops.new_block(self.n, self.cfg.k, self.mv.storage, self.device)
         Xs.t.copy_(X.t)
         rec = self.ops.Recorder()
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=True)     # the raw graph also feeds the device loop
         torch.cuda.synchronize(self.device)
         passes0 = self.stats.a_passes
         try:

@@ -294,3 +294,34 @@ def test_driver_reuse_av_ladder_to_tol(ofrr_gpu):
         res[reuse] = (rs, st)
     np.testing.assert_allclose(res[True][0].values[:top], res[False][0].values[:top], rtol=1e-12)
     assert res[True][1].a_passes < res[False][1].a_passes
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pname,reuse", [("full-f32", False), ("full-f32", True), ("full-f64", True)])
+def test_device_loop_matches_host_loop(ofrr_gpu, pname, reuse):
+    """The outer loop as one CUDA graph with device-side control flow (csrc/loop.cu:
+    conditional WHILE over the captured iteration, IF around the FP64 report): once the
+    graphs exist (two earlier solves), a solve launches it once and must reproduce the host
+    loop's iterations, values, vectors and residuals exactly."""
+    import os
+    p = ofrr_gpu
+    n, top, k = 4096, 16, 32
+    lam = p.geometric_spectrum(n, top, k)
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    tol = 1e-4 if pname == "full-f32" else 1e-9
+    cfg = p.IterConfig(k=k, m=40, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.POLICY_PRESETS[pname], seed=SEED, tol=tol, top=top, reuse_av=reuse)
+    runs = []
+    for _ in range(4):
+        st = p.RunStats()
+        rs = p.subspace_iter_eig(A, cfg, stats=st)
+        runs.append((rs, st))
+    host_rs, host_st = runs[0]
+    assert not host_st.device_loop and runs[-1][1].device_loop
+    for rs, st in runs[1:]:
+        assert st.converged and st.iterations == host_st.iterations and st.a_passes == host_st.a_passes
+        np.testing.assert_array_equal(rs.values, host_rs.values)
+        np.testing.assert_array_equal(rs.residuals, host_rs.residuals)
+        np.testing.assert_array_equal(rs.vectors.data, host_rs.vectors.data)
+        assert [i for i, _ in st.history] == [i for i, _ in host_st.history]
+    assert np.max(runs[-1][0].residuals[:top]) < tol
