@@ -107,4 +107,6 @@ if __name__ == "__main__":
     summarize_rep("oz_rowscale_c2", "K7z row scales of A (one pass over A), C2")
     summarize_rep("gram_c2", "K4 Gram partials (DMMA), n=16384 k=64 fp32 basis")
     summarize_rep("hess_c2", "K3 Hessenberg basis n=16384 k=64")
-    summarize_rep("pc_tri_k64", "K5c tridiagonal eigensolver k=64")
+    summarize_rep("pc_tri_k64", "K5c register-resident Householder tridiagonalisation, k=64")
+    summarize_rep("pc_eigvec_k64", "K5d eigenpairs of the tridiagonal + back-transformation (multi-CTA), k=64")
+    summarize_rep("pc_chol_k64", "K5a Cholesky + inverse of the Gram M, k=64")
