@@ -535,6 +535,138 @@ __global__ void __launch_bounds__(PT, 1)
 }
 
 // ---------------------------------------------------------------------------------
+// K5a for k <= 64: the same Cholesky + inverse + certificate with sym(M) in registers
+// (group-per-column layout of k_pc_tri_reg).  Step j: the group of column j forms
+// l = column j / sqrt(m_jj) from its registers and publishes it (shared memory, double
+// buffered); barrier; every later column takes the rank-1 update in registers.  Then L goes
+// to shared memory and each group solves L x = e_c for its own column (x_l broadcast by
+// shuffle from the lane holding row l, the update of the rows below in registers).
+// ---------------------------------------------------------------------------------
+template <int TPC, int RPT>
+__global__ void __launch_bounds__(PT, 1)
+    k_pc_chol_reg(const double* __restrict__ M, int k, double* __restrict__ Xg, int* __restrict__ gate) {
+  constexpr int RP = RPT + 2;
+  extern __shared__ double sm[];                                 // L, k x k column-major (ld k)
+  __shared__ __align__(16) double lv[2][TPC * RP];
+  __shared__ double red[PNW];
+  __shared__ double dinv[PK_MAX];
+  __shared__ int s_fail;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = threadIdx.x / TPC, sub = threadIdx.x % TPC;
+  const unsigned gmask = (TPC == 32 ? 0xffffffffu : (((1u << TPC) - 1u) << (lane & ~(TPC - 1))));
+  const int gl0 = lane & ~(TPC - 1);
+  const int r0 = sub * RPT;
+  const bool colok = c < k;
+  double a[RPT];
+  double ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    const int i = r0 + t;
+    a[t] = (colok && i < k) ? 0.5 * (M[(size_t)c * k + i] + M[(size_t)i * k + c]) : 0.0;
+    ss = fma(a[t], a[t], ss);
+  }
+  if (threadIdx.x == 0) s_fail = 0;
+  const double mnorm = sqrt(pc_block_sum(ss, red));             // includes barriers
+  pc_mark(0);
+  auto group_sum = [&](double v) {
+#pragma unroll
+    for (int o = TPC >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+    return v;
+  };
+  // group j: publish l = L[:, j] (rows >= j) to lv[buf], 1 / L_jj to dinv[j]
+  auto publish = [&](int j, int buf) {
+    double d = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPT; ++t)
+      if (r0 + t == j) d = a[t];
+    d = __shfl_sync(gmask, d, gl0 + j / RPT);
+    const bool bad = !(d > 0.0);
+    const double lj = bad ? 1.0 : sqrt(d);
+    const double il = pc_fast_div(1.0, lj);
+    double* lb = lv[buf] + sub * RP;
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = r0 + t;
+      const double l = i > j ? a[t] * il : (i == j ? lj : 0.0);
+      a[t] = l;                                                  // my column now holds L[:, j]
+      lb[t] = l;
+    }
+    if (sub == 0) {
+      dinv[j] = il;
+      if (bad) s_fail = 1;
+    }
+  };
+  if (c == 0) publish(0, 0);
+  __syncthreads();
+  for (int j = 0; j + 1 < k; ++j) {
+    const int buf = j & 1;
+    if (s_fail) break;                                           // uniform (read after a barrier)
+    const double* lb = lv[buf] + sub * RP;
+    if (colok && c > j) {
+      const double lc = lv[buf][c + 2 * (c / RPT)];
+#pragma unroll
+      for (int t = 0; t < RPT; t += 2) {
+        const double2 w = *reinterpret_cast<const double2*>(lb + t);
+        a[t] = fma(-w.x, lc, a[t]);
+        a[t + 1] = fma(-w.y, lc, a[t + 1]);
+      }
+    }
+    if (c == j + 1) publish(j + 1, buf ^ 1);
+    __syncthreads();
+  }
+  if (s_fail) {
+    if (threadIdx.x == 0) *gate = 1;
+    return;
+  }
+  pc_mark(1);
+  // L -> shared memory (column c, rows >= c; zeros above)
+  if (colok) {
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = r0 + t;
+      if (i < k) sm[(size_t)c * k + i] = i >= c ? a[t] : 0.0;
+    }
+  }
+  __syncthreads();
+  // X = L^-1, column c by the group of column c: x = e_c; for l = c..k-1: x_l *= 1/L_ll,
+  // then x_i -= L_il x_l for the rows below (right-looking, registers)
+  double xs = 0.0;
+  if (colok) {
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) a[t] = (r0 + t == c) ? 1.0 : 0.0;
+    for (int l = c; l < k; ++l) {
+      const int ol = l / RPT;                                    // lane holding row l
+      double xl = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+        if (r0 + t == l) { a[t] *= dinv[l]; xl = a[t]; }
+      xl = __shfl_sync(gmask, xl, gl0 + ol);
+      const double* Ll = sm + (size_t)l * k;
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        const int i = r0 + t;
+        if (i > l && i < k) a[t] = fma(-Ll[i], xl, a[t]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = r0 + t;
+      if (i < k) {
+        const double v = i >= c ? a[t] : 0.0;
+        Xg[(size_t)c * k + i] = v;
+        xs = fma(v, v, xs);
+      }
+    }
+  }
+  pc_mark(2);
+  const double xn2 = pc_block_sum(xs, red);
+  // mu_min(M) >= 1 / ||X||_F^2 must clear the reference's cutoff k eps mu_max (<= ||M||_F)
+  const bool cert = (1.0 / xn2) > 4.0 * (double)k * 2.220446049250313e-16 * mnorm;
+  if (threadIdx.x == 0) *gate = cert ? 0 : 1;
+  pc_mark(3);
+}
+
+// ---------------------------------------------------------------------------------
 // K5d: eigenpairs of the tridiagonal and their back-transformation, EPB eigenvalues per
 // CTA (ascending index m), spread over the GPU:
 //   multisection on division-free Sturm counts, one warp per eigenvalue (32 points per
@@ -832,7 +964,10 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
     attr = true;
   }
   const dim3 gg((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
-  k_pc_chol<<<1, PT, shm, st>>>(M, k, X, gate);
+  // register-resident for k <= 64 (k = 64: 61 -> 51 us); at k = 128 the 32-row register
+  // blocks make the in-smem kernel faster (100 + 116 us vs 131 + 257 us)
+  if (k <= 64) k_pc_chol_reg<8, 8><<<1, PT, (size_t)k * k * sizeof(double), st>>>(M, k, X, gate);
+  else k_pc_chol<<<1, PT, shm, st>>>(M, k, X, gate);
   OFRR_CHECK_LAUNCH();
   k_pc_gemm<false, false, true><<<gg, 256, 0, st>>>(X, B, T1, k, gate);
   k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);
