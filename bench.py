@@ -109,6 +109,8 @@ class ClockSampler:
             self._stop.wait(0.002)
 
     def __enter__(self):
+        if os.environ.get("OFRR_BENCH_NO_CLOCKS"):       # diagnostics only
+            return self
         try:
             import pynvml as nv
             nv.nvmlInit()
@@ -286,24 +288,38 @@ def run_ours(args, cfg):
     # loop that replays them, csrc/loop.cu)
     import ctypes
     L.ofrr_prof_k1_stamp(1)
+    rs = None
     for _ in range(args.warmup):
-        solve()
+        rs = solve()               # held like in the timed loop (same allocator pattern)
     barrier()
     # ---- timed region: K solves, CUDA events on the launching stream -------------
     ops.GEMM_LOG = []
     ops.LAUNCHES[0] = 0
     stats = p.RunStats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import gc
+    gc.collect()                                         # no collector pause inside the timed region
+    gc.disable()
     with ClockSampler(local) as clk:
         barrier()
         L.ofrr_prof_k1_stamp(1)                          # zero the K1 accumulators
         e0.record()
+        per = [] if os.environ.get("OFRR_BENCH_PER_STEP") else None
         for _ in range(args.steps):
+            if per is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                per.append(ev)
             rs = solve(stats)
         e1.record()
         barrier()
+    gc.enable()
     launches = ops.LAUNCHES[0]
     ms_total = e0.elapsed_time(e1)
+    if per is not None:
+        per.append(e1)
+        print("per-step ms:", [round(per[i].elapsed_time(per[i + 1]), 3) for i in range(len(per) - 1)],
+              file=sys.stderr)
     log = ops.GEMM_LOG
     ops.GEMM_LOG = None
     k1_ms, k1_n = ctypes.c_double(0.0), ctypes.c_longlong(0)

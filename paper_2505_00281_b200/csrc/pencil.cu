@@ -11,8 +11,7 @@
 //   k_pc_eigvec eigenvalues of Tri by multisection on division-free Sturm sequences,
 //               eigenvectors Z of Tri by twisted factorisation, W1 = Q Z by applying the
 //               reflectors -- a few eigenpairs per CTA, spread over the GPU
-//   k_pc_gemm   Y = X^T W1
-//   k_pc_finish descending order + the largest-|entry|-positive sign rule (smallsolve.py:52-61);
+//   k_pc_finish Y = X^T W1, descending order + the largest-|entry|-positive sign rule (smallsolve.py:52-61);
 //               numerically coincident eigenvalues raise the gate
 // Any failure (Cholesky breakdown, certificate not met, eigenvector breakdown) raises a gate
 // flag on the device and the general kernel (small_eig.cu: the reference's eig(M)
@@ -544,9 +543,11 @@ __global__ void __launch_bounds__(PT, 1)
 // ---------------------------------------------------------------------------------
 template <int TPC, int RPT>
 __global__ void __launch_bounds__(PT, 1)
-    k_pc_chol_reg(const double* __restrict__ M, int k, double* __restrict__ Xg, int* __restrict__ gate) {
+    k_pc_chol_reg(const double* __restrict__ M, int k, double* __restrict__ Xg, int* __restrict__ gate,
+                  const double* __restrict__ B, double* __restrict__ Tg) {
   constexpr int RP = RPT + 2;
-  extern __shared__ double sm[];                                 // L, k x k column-major (ld k)
+  extern __shared__ double sm[];                                 // L, k x k column-major (ld k); then X
+  double* sm2 = sm + (size_t)k * k;                              // sym(B), then G = sym(B) X^T
   __shared__ __align__(16) double lv[2][TPC * RP];
   __shared__ double red[PNW];
   __shared__ double dinv[PK_MAX];
@@ -659,11 +660,56 @@ __global__ void __launch_bounds__(PT, 1)
     }
   }
   pc_mark(2);
-  const double xn2 = pc_block_sum(xs, red);
+  const double xn2 = pc_block_sum(xs, red);                      // (barriers: L is dead after)
   // mu_min(M) >= 1 / ||X||_F^2 must clear the reference's cutoff k eps mu_max (<= ||M||_F)
   const bool cert = (1.0 / xn2) > 4.0 * (double)k * 2.220446049250313e-16 * mnorm;
   if (threadIdx.x == 0) *gate = cert ? 0 : 1;
   pc_mark(3);
+  if (!Tg || !cert) return;
+  // T = X sym(B) X^T here (no GEMM launches): X -> shared (column c from my registers),
+  // sym(B) -> shared; G[:, c] = sym(B) X[c, :]^T in registers, G -> shared, T[:, c] = X G[:, c]
+  if (colok) {
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = r0 + t;
+      if (i < k) sm[(size_t)c * k + i] = i >= c ? a[t] : 0.0;
+    }
+  }
+  for (int e = threadIdx.x; e < k * k; e += PT) {
+    const int i = e % k, j = e / k;
+    sm2[e] = 0.5 * (B[(size_t)j * k + i] + B[(size_t)i * k + j]);
+  }
+  __syncthreads();
+  double g[RPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) g[t] = 0.0;
+  if (colok) {
+    for (int l = 0; l <= c; ++l) {                               // X[c, l] = 0 for l > c
+      const double xcl = sm[(size_t)l * k + c];
+      const double* bl = sm2 + (size_t)l * k;                    // sym(B)[:, l] = sym(B)[l, :]
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+        if (r0 + t < k) g[t] = fma(bl[r0 + t], xcl, g[t]);
+    }
+  }
+  __syncthreads();
+  if (colok) {
+#pragma unroll
+    for (int t = 0; t < RPT; ++t)
+      if (r0 + t < k) sm2[(size_t)c * k + r0 + t] = g[t];
+  }
+  __syncthreads();
+  if (colok) {
+    const double* gc = sm2 + (size_t)c * k;
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = r0 + t;
+      if (i >= k) continue;
+      double acc = 0.0;
+      for (int l = 0; l <= i; ++l) acc = fma(sm[(size_t)l * k + i], gc[l], acc);   // X[i, l], l <= i
+      Tg[(size_t)c * k + i] = acc;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -879,17 +925,30 @@ __global__ void __launch_bounds__(EPT)
   pc_mark(9);
 }
 
-// values (descending) and the sign rule on Y's columns (smallsolve.py:52-61).
+// Y[:, c] = X^T W1[:, c] (X = L^-1 lower triangular: rows l >= i), values (descending) and
+// the sign rule on Y's columns (smallsolve.py:52-61), one column per CTA.
 __global__ void __launch_bounds__(256)
-    k_pc_finish(const double* __restrict__ lam, const double* __restrict__ Y, int k, double* __restrict__ values,
-                double* __restrict__ vectors, int* __restrict__ n_out, int* __restrict__ status,
-                const double* __restrict__ tnrm_g, int* __restrict__ gate) {
+    k_pc_finish(const double* __restrict__ lam, const double* __restrict__ X, const double* __restrict__ W1, int k,
+                double* __restrict__ values, double* __restrict__ vectors, int* __restrict__ n_out,
+                int* __restrict__ status, const double* __restrict__ tnrm_g, int* __restrict__ gate) {
   if (*gate) return;
   const int c = blockIdx.x;                  // one column per CTA
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ double sb[8];
   __shared__ int si[8];
   __shared__ int s_neg;
+  __shared__ double w1[PK_MAX], yc[PK_MAX];
+  for (int l = threadIdx.x; l < k; l += blockDim.x) w1[l] = W1[(size_t)c * k + l];
+  __syncthreads();
+  // warp per output row: y_i = sum_{l >= i} X[l, i] w1[l] (column i of X, coalesced)
+  for (int i = warp; i < k; i += blockDim.x / 32) {
+    double sacc = 0.0;
+    for (int l = i + lane; l < k; l += 32) sacc = fma(X[(size_t)i * k + l], w1[l], sacc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) yc[i] = sacc;
+  }
+  __syncthreads();
   // numerically coincident eigenvalues (gap <= 1e-9 of the Gershgorin bound): the twisted
   // vectors are not orthogonal there -- every CTA sees the same verdict and leaves the
   // pencil to the general kernel
@@ -905,7 +964,7 @@ __global__ void __launch_bounds__(256)
   double best = -1.0;
   int bi = 0x7fffffff;
   for (int r = threadIdx.x; r < k; r += blockDim.x) {
-    const double a = fabs(Y[(size_t)c * k + r]);
+    const double a = fabs(yc[r]);
     if (a > best) { best = a; bi = r; }
   }
 #pragma unroll
@@ -921,13 +980,13 @@ __global__ void __launch_bounds__(256)
     int ii = si[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
       if (sb[w] > b || (sb[w] == b && si[w] < ii)) { b = sb[w]; ii = si[w]; }
-    s_neg = Y[(size_t)c * k + ii] < 0.0;
+    s_neg = yc[ii] < 0.0;
     values[c] = lam[k - 1 - c];
     if (c == 0) { *n_out = k; *status = 0; }
   }
   __syncthreads();
   const double sg = s_neg ? -1.0 : 1.0;
-  for (int r = threadIdx.x; r < k; r += blockDim.x) vectors[(size_t)c * k + r] = sg * Y[(size_t)c * k + r];
+  for (int r = threadIdx.x; r < k; r += blockDim.x) vectors[(size_t)c * k + r] = sg * yc[r];
 }
 
 // ---------------------------------------------------------------------------------
@@ -947,7 +1006,6 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
   double* R = p + 3 * kk;   // reflectors of the tridiagonalisation
   double* tri = p + 4 * kk; // d | e | tau | tnrm (3k + 1 <= kk for k >= 4; else T1, dead by then)
   double* W1 = p + 5 * kk;  // Q Z
-  double* Y = p + 6 * kk;   // X^T W1
   double* lam = p + 7 * kk;
   if (3 * (size_t)k + 1 > kk) tri = T1;
   double* tnrm = tri + 3 * k;
@@ -959,6 +1017,8 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
                                        (int)((size_t)PK_MAX * (PK_MAX | 1) * sizeof(double))));
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_tri, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)((size_t)PK_MAX * (PK_MAX | 1) * sizeof(double))));
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_chol_reg<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)((size_t)2 * 64 * 64 * sizeof(double))));
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_eigvec, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(((size_t)PK_MAX * PK_MAX + 2 * pc_epb(PK_MAX) * PK_MAX) * sizeof(double))));
     attr = true;
@@ -966,21 +1026,24 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
   const dim3 gg((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
   // register-resident for k <= 64 (k = 64: 61 -> 51 us); at k = 128 the 32-row register
   // blocks make the in-smem kernel faster (100 + 116 us vs 131 + 257 us)
-  if (k <= 64) k_pc_chol_reg<8, 8><<<1, PT, (size_t)k * k * sizeof(double), st>>>(M, k, X, gate);
-  else k_pc_chol<<<1, PT, shm, st>>>(M, k, X, gate);
-  OFRR_CHECK_LAUNCH();
-  k_pc_gemm<false, false, true><<<gg, 256, 0, st>>>(X, B, T1, k, gate);
-  k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);
-  OFRR_CHECK_LAUNCH();
+  if (k <= 64) {
+    // Cholesky, inverse, certificate and T = X sym(B) X^T in one kernel
+    k_pc_chol_reg<8, 8><<<1, PT, (size_t)2 * k * k * sizeof(double), st>>>(M, k, X, gate, B, T);
+    OFRR_CHECK_LAUNCH();
+  } else {
+    k_pc_chol<<<1, PT, shm, st>>>(M, k, X, gate);
+    OFRR_CHECK_LAUNCH();
+    k_pc_gemm<false, false, true><<<gg, 256, 0, st>>>(X, B, T1, k, gate);
+    k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);
+    OFRR_CHECK_LAUNCH();
+  }
   if (k <= 64) k_pc_tri_reg<8, 8><<<1, PT, 0, st>>>(T, k, tri, R, gate);
   else if (k <= 128) k_pc_tri_reg<4, 32><<<1, PT, 0, st>>>(T, k, tri, R, gate);
   else k_pc_tri<<<1, PT, shm, st>>>(T, k, tri, R, gate);
   OFRR_CHECK_LAUNCH();
   k_pc_eigvec<<<(k + pc_epb(k) - 1) / pc_epb(k), EPT, shm_e, st>>>(tri, R, k, lam, W1, tnrm, gate);
   OFRR_CHECK_LAUNCH();
-  k_pc_gemm<true, false, false><<<gg, 256, 0, st>>>(X, W1, Y, k, gate);
-  OFRR_CHECK_LAUNCH();
-  k_pc_finish<<<k, 256, 0, st>>>(lam, Y, k, values, vectors, n_out, status, tnrm, gate);
+  k_pc_finish<<<k, 256, 0, st>>>(lam, X, W1, k, values, vectors, n_out, status, tnrm, gate);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
