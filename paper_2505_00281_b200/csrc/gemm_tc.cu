@@ -33,16 +33,22 @@ static constexpr int A_STAGE = TILE_M * KBYTES;  // 32 KB
 static constexpr int SMEM_BUDGET = 200 * 1024;
 static constexpr int THREADS = 192;
 
-template <int BN>
+// MH = M halves per tile: 2 (256 rows, the two M=128 UMMAs share each B tile, BN <= 256),
+// or 1 ("wide": 128 rows, BN up to 512 fp32 TMEM columns as two N chunks of <= 256 that share
+// each A tile -- one pass over A for N = 3k up to 510, e.g. the fp32 split at k = 128)
+template <int BN, int MH = 2>
 struct TcCfg {
+  static constexpr int TM = 128 * MH;               // rows per tile
+  static constexpr int A_ST = TM * KBYTES;
   static constexpr int B_STAGE = BN * KBYTES;
-  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGE = A_ST + B_STAGE;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  // two accumulators (M halves) of BN fp32 columns; allocation is a power of two >= 32
-  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
-                                   : (2 * BN) <= 256 ? 256 : 512;
+  // MH accumulators of BN fp32 columns; allocation is a power of two >= 32
+  static constexpr int TMEM_COLS = (MH * BN) <= 32 ? 32 : (MH * BN) <= 64 ? 64 : (MH * BN) <= 128 ? 128
+                                   : (MH * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE + 256;
+  static constexpr int XBOX = BN <= 256 ? BN : 128;    // rows per TMA box of the B operand
 };
 
 // Instruction descriptor (kind::f16 / kind::f8f6f4): c_format=F32 (bits 4-5), a/b formats
@@ -68,12 +74,13 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   return t;
 }
 
-template <int BN, bool FP8K>
+template <int BN, bool FP8K, int MH = 2>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_av_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  float* __restrict__ ws, int kblocks, long long total_iters, int max_slots,
-                 uint32_t idesc, int stamp) {
-  using C = TcCfg<BN>;
+                 uint32_t idesc, int stamp, uint32_t idesc2) {
+  using C = TcCfg<BN, MH>;
+  constexpr int TMR = C::TM;
   if (stamp && threadIdx.x == 0) atomicMin(&g_k1_stamp[0], gtimer_ns());
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -115,8 +122,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint8_t* sa = smem + stage * C::STAGE;
         mbar_expect_tx(&full[stage], C::STAGE);
         const int kcoord = FP8K ? kb * 128 : kb * 64;
-        tma_load_2d(sa, &tmA, kcoord, t * TILE_M, &full[stage], pol_a);
-        tma_load_2d(sa + A_STAGE, &tmX, kcoord, 0, &full[stage], pol_x);
+        tma_load_2d(sa, &tmA, kcoord, t * TMR, &full[stage], pol_a);
+#pragma unroll
+        for (int xb = 0; xb < BN; xb += C::XBOX)
+          tma_load_2d(sa + C::A_ST + xb * KBYTES, &tmX, kcoord, xb, &full[stage], pol_x);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -135,17 +144,30 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE);
-          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + A_STAGE);
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_ST);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+            if constexpr (MH == 2) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              // +32 B of K per step (>>4 = 2); second M half starts 128 rows (16 KB) later
-              const uint64_t a = da + (uint64_t)(k * 2 + h * (16384 >> 4));
-              const uint64_t b = db + (uint64_t)(k * 2);
-              if (FP8K) mma_f8(tmem + h * BN, a, b, idesc, acc);
-              else mma_f16(tmem + h * BN, a, b, idesc, acc);
+              for (int h = 0; h < 2; ++h) {
+                // +32 B of K per step (>>4 = 2); second M half starts 128 rows (16 KB) later
+                const uint64_t a = da + (uint64_t)(k * 2 + h * (16384 >> 4));
+                const uint64_t b = db + (uint64_t)(k * 2);
+                if (FP8K) mma_f8(tmem + h * BN, a, b, idesc, acc);
+                else mma_f16(tmem + h * BN, a, b, idesc, acc);
+              }
+            } else {
+              // one M=128 half, N in chunks of 256 columns sharing the A tile; the second
+              // chunk's B rows start 256 rows (32 KB) into the B stage
+              const uint64_t a = da + (uint64_t)(k * 2);
+              if (FP8K) mma_f8(tmem, a, db + (uint64_t)(k * 2), idesc, acc);
+              else mma_f16(tmem, a, db + (uint64_t)(k * 2), idesc, acc);
+              if constexpr (BN > 256) {
+                const uint64_t b2 = db + (uint64_t)(k * 2 + ((256 * KBYTES) >> 4));
+                if (FP8K) mma_f8(tmem + 256, a, b2, idesc2, acc);
+                else mma_f16(tmem + 256, a, b2, idesc2, acc);
+              }
             }
           }
           tc_commit(&empty[stage]);
@@ -168,15 +190,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       it += kb1 - kb0;
       mbar_wait(tfull, acc_phase);
       tc_fence_after();
-      float* dst = ws + ((size_t)blockIdx.x * max_slots + (t - t_first)) * (size_t)(TILE_M * BN);
+      float* dst = ws + ((size_t)blockIdx.x * max_slots + (t - t_first)) * (size_t)(TMR * BN);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < MH; ++h) {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + h * BN + c0, v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) dst[(size_t)(c0 + i) * TILE_M + h * 128 + row] = v[i];
+          for (int i = 0; i < 16; ++i) dst[(size_t)(c0 + i) * TMR + h * 128 + row] = v[i];
         }
       }
       tc_fence_before();
@@ -203,7 +225,7 @@ __global__ void __launch_bounds__(256)
     k_finalize(const float* __restrict__ ws, int BN, int kblocks, long long total_iters, int G,
                int max_slots, int64_t rows, int k, void* __restrict__ W, int64_t ldw, int out_fmt,
                double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
-               int out_fmt2, int nsplit, int stamp) {
+               int out_fmt2, int nsplit, int stamp, int TMR) {
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
     const unsigned long long t0 = g_k1_stamp[0], t1 = g_k1_stamp[1];
     if (t1 > t0) { g_k1_stamp[2] += t1 - t0; g_k1_stamp[3] += 1; }
@@ -224,7 +246,7 @@ __global__ void __launch_bounds__(256)
   while (c_lo > 0 && seg_begin(c_lo, total_iters, G) > x0) --c_lo;
   while (c_hi + 1 < G && seg_begin(c_hi + 1, total_iters, G) <= x1) ++c_hi;
   while (c_hi > 0 && seg_begin(c_hi, total_iters, G) > x1) --c_hi;
-  const int64_t grow = (int64_t)t * TILE_M + row;
+  const int64_t grow = (int64_t)t * TMR + row;
   const bool valid = grow < rows;
   float s[FIN_COLS];
 #pragma unroll
@@ -232,10 +254,10 @@ __global__ void __launch_bounds__(256)
   for (int sl = nsplit - 1; sl >= 0; --sl) {
     for (long long c = c_lo; c <= c_hi; ++c) {
       const int slot = t - (int)(seg_begin(c, total_iters, G) / kblocks);
-      const float* src = ws + ((size_t)c * max_slots + slot) * (size_t)(TILE_M * BN) + row + (size_t)sl * k * TILE_M;
+      const float* src = ws + ((size_t)c * max_slots + slot) * (size_t)(TMR * BN) + row + (size_t)sl * k * TMR;
 #pragma unroll
       for (int i = 0; i < FIN_COLS; ++i)
-        if (j0 + i < k) s[i] += src[(size_t)(j0 + i) * TILE_M];
+        if (j0 + i < k) s[i] += src[(size_t)(j0 + i) * TMR];
     }
   }
   int bad = 0;
@@ -257,7 +279,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (colmax && threadIdx.x < FIN_COLS && j0 + threadIdx.x < k) {
     float a = smax[0][threadIdx.x];
-    for (int w8 = 1; w8 < 8; ++w8) a = fmaxf(a, smax[w8][threadIdx.x]);
+    for (int w8 = 1; w8 < (int)(blockDim.x >> 5); ++w8) a = fmaxf(a, smax[w8][threadIdx.x]);
     atomic_max_nonneg(&colmax[j0 + threadIdx.x], (double)a);
   }
   if (bad && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
@@ -433,17 +455,22 @@ int prof_read(float* ms, int max) {
 
 static int pick_bn(int k) { return k <= 32 ? 32 : ((k + 31) / 32) * 32; }
 
+// N > 256 (up to 512): the wide one-M-half tile (TcCfg MH = 1), BN a multiple of 128
+static bool wide_n(int k) { return k > 256; }
+
 struct TcPlan {
-  int bn, m_tiles, kblocks, grid, max_slots;
+  int bn, m_tiles, kblocks, grid, max_slots, tm;
   long long total;
   size_t ws_bytes;
 };
 
 static TcPlan plan_tc(int64_t rows, int64_t cols, int k, int a_fmt) {
   TcPlan p;
-  p.bn = pick_bn(k);
+  const bool wide = wide_n(k);
+  p.bn = wide ? ((k + 127) / 128) * 128 : pick_bn(k);
+  p.tm = wide ? 128 : TILE_M;
   const int kel = (a_fmt == FP8) ? 128 : 64;
-  p.m_tiles = (int)((rows + TILE_M - 1) / TILE_M);
+  p.m_tiles = (int)((rows + p.tm - 1) / p.tm);
   p.kblocks = (int)((cols + kel - 1) / kel);
   p.total = (long long)p.m_tiles * p.kblocks;
   int sms = ofrr_device_sm_count(-1);
@@ -452,7 +479,7 @@ static TcPlan plan_tc(int64_t rows, int64_t cols, int k, int a_fmt) {
   if (p.grid < 1) p.grid = 1;
   const long long per = (p.total + p.grid - 1) / p.grid;
   p.max_slots = (int)((per + p.kblocks - 1) / p.kblocks) + 1;
-  p.ws_bytes = (size_t)p.grid * p.max_slots * TILE_M * p.bn * sizeof(float);
+  p.ws_bytes = (size_t)p.grid * p.max_slots * p.tm * p.bn * sizeof(float);
   return p;
 }
 
@@ -460,11 +487,11 @@ size_t tc_workspace(int64_t rows, int64_t cols, int k, int a_fmt) {
   return plan_tc(rows, cols, k, a_fmt).ws_bytes;
 }
 
-template <int BN, bool FP8K>
+template <int BN, bool FP8K, int MH>
 static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPlan& p, float* ws,
-                        uint32_t idesc, cudaStream_t st) {
-  using C = TcCfg<BN>;
-  auto kern = k_gemm_av_tc<BN, FP8K>;
+                        uint32_t idesc, uint32_t idesc2, cudaStream_t st) {
+  using C = TcCfg<BN, MH>;
+  auto kern = k_gemm_av_tc<BN, FP8K, MH>;
   static bool attr_done = false;
   if (!attr_done) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
@@ -472,7 +499,8 @@ static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPl
   }
   cudaEvent_t* ev = prof_slot();
   if (ev) prof_record(ev[0], st);
-  kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc, g_stamp_on ? 1 : 0);
+  kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc, g_stamp_on ? 1 : 0,
+                                               idesc2);
   if (ev) prof_record(ev[1], st);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
@@ -486,25 +514,39 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
     ofrr_set_error("gemm_av: workspace too small (%zu < %zu)", ws_bytes, p.ws_bytes);
     return OFRR_ERR_INVALID;
   }
+  if (k > 512) { ofrr_set_error("gemm_av: k=%d > 512 on the tensor-core path", k); return OFRR_ERR_INVALID; }
   const bool fp8 = a_fmt == FP8;
+  const bool wide = wide_n(k);
   const uint32_t kel = fp8 ? 128 : 64;
   CUtensorMap tA, tX;
-  int rc = make_tmap_2d(&tA, A, a_fmt, (uint64_t)cols, (uint64_t)rows, (uint64_t)lda, kel, TILE_M);
+  int rc = make_tmap_2d(&tA, A, a_fmt, (uint64_t)cols, (uint64_t)rows, (uint64_t)lda, kel, (uint32_t)p.tm);
   if (rc) return rc;
-  rc = make_tmap_2d(&tX, X, a_fmt, (uint64_t)cols, (uint64_t)k, (uint64_t)ldx, kel, (uint32_t)p.bn);
+  rc = make_tmap_2d(&tX, X, a_fmt, (uint64_t)cols, (uint64_t)k, (uint64_t)ldx, kel,
+                    (uint32_t)(wide ? 128 : p.bn));
   if (rc) return rc;
-  const uint32_t idesc = make_idesc(a_fmt, p.bn);
-#define TC_CASE(B) case B: rc = fp8 ? launch_tc_bn<B, true>(tA, tX, p, (float*)ws, idesc, st) \
-                                  : launch_tc_bn<B, false>(tA, tX, p, (float*)ws, idesc, st); break;
-  switch (p.bn) {
-    TC_CASE(32) TC_CASE(64) TC_CASE(96) TC_CASE(128) TC_CASE(160) TC_CASE(192) TC_CASE(224)
-    default: TC_CASE(256)
+  const uint32_t idesc = make_idesc(a_fmt, wide ? 256 : p.bn);
+  const uint32_t idesc2 = wide ? make_idesc(a_fmt, p.bn - 256) : 0u;
+#define TC_CASE(B) case B: rc = fp8 ? launch_tc_bn<B, true, 2>(tA, tX, p, (float*)ws, idesc, idesc2, st) \
+                                  : launch_tc_bn<B, false, 2>(tA, tX, p, (float*)ws, idesc, idesc2, st); break;
+#define TC_WIDE(B) case B: rc = fp8 ? launch_tc_bn<B, true, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st) \
+                                  : launch_tc_bn<B, false, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st); break;
+  if (wide) {
+    switch (p.bn) {
+      TC_WIDE(384)
+      default: TC_WIDE(512)
+    }
+  } else {
+    switch (p.bn) {
+      TC_CASE(32) TC_CASE(64) TC_CASE(96) TC_CASE(128) TC_CASE(160) TC_CASE(192) TC_CASE(224)
+      default: TC_CASE(256)
+    }
   }
 #undef TC_CASE
+#undef TC_WIDE
   if (rc) return rc;
-  k_finalize<<<dim3(p.m_tiles, (k / nsplit + FIN_COLS - 1) / FIN_COLS), 256, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
+  k_finalize<<<dim3(p.m_tiles, (k / nsplit + FIN_COLS - 1) / FIN_COLS), p.tm, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
                                         rows, k / nsplit, W, ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
-                                        nsplit, g_stamp_on ? 1 : 0);
+                                        nsplit, g_stamp_on ? 1 : 0, p.tm);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
@@ -530,7 +572,9 @@ __global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n
   }
 }
 
-static constexpr int SPLIT_KC = 85;   // 3 * 85 = 255 <= 256 columns per pass
+// columns per pass: 3 * 170 = 510 <= 512 (one pass over A up to k = 170; the wide tile
+// for 85 < k, the two-M-half tile up to 85)
+static constexpr int SPLIT_KC = 170;
 
 size_t split_workspace(int64_t rows, int64_t cols, int k) {
   const int kc = std::min(k, SPLIT_KC);
@@ -538,8 +582,8 @@ size_t split_workspace(int64_t rows, int64_t cols, int k) {
   return (size_t)3 * kc * lds * 2 + 1024 + tc_workspace(rows, cols, 3 * kc, BF16);
 }
 
-// k <= 85: one pass over A with N = 3k.  k > 85: column chunks of <= 85, one pass each
-// (full fp32 semantics at the price of ceil(k / 85) passes).
+// k <= 170: one pass over A with N = 3k.  k > 170: column chunks of <= 170, one pass each
+// (full fp32 semantics at the price of ceil(k / 170) passes).
 int tc_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, const float* X, int64_t ldx, int k,
                      void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes,
                      cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2) {

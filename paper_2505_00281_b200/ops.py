@@ -326,7 +326,7 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
     if split or (A.fmt.tensor_core and not transpose):
         # algorithmic bytes of the tensor-core kernel: A once + the B operand
         # once (3 bf16 slices in split mode); W is written by the finalize kernel
-        chunks = [min(85, k - j0) for j0 in range(0, k, 85)] if split else [k]   # one launch per chunk
+        chunks = [min(170, k - j0) for j0 in range(0, k, 170)] if split else [k]   # one launch per chunk
         for kc in chunks:
             kb = 3 * kc if split else kc
             nb = A.rows * A.cols * A.fmt.itemsize + A.cols * kb * (2 if split else X.fmt.itemsize)
