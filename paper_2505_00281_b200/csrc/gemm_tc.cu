@@ -21,6 +21,7 @@
 //     warps 2..5 = epilogue (TMEM -> registers -> fp32 partials, coalesced).
 #include "common.cuh"
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 #include <utility>
@@ -74,13 +75,19 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   return t;
 }
 
-template <int BN, bool FP8K, int MH = 2>
+// CL = 2 (wide tile only): a cluster of two CTAs works on a pair of 128-row tiles with the
+// same k-block sequence; each loads its own A tile and half of the B tile, multicast into
+// both CTAs' shared memory (X is read from L2 once per 256 rows, as in the MH = 2 tile),
+// and each MMA commit releases the stage in both CTAs.
+template <int BN, bool FP8K, int MH = 2, int CL = 1>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_av_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  float* __restrict__ ws, int kblocks, long long total_iters, int max_slots,
-                 uint32_t idesc, int stamp, uint32_t idesc2) {
+                 uint32_t idesc, int stamp, uint32_t idesc2, int m_tiles) {
   using C = TcCfg<BN, MH>;
   constexpr int TMR = C::TM;
+  static_assert(CL == 1 || MH == 1, "cluster pairs use the wide tile");
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
   if (stamp && threadIdx.x == 0) atomicMin(&g_k1_stamp[0], gtimer_ns());
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -91,13 +98,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long G = gridDim.x;
-  const long long it0 = (long long)blockIdx.x * total_iters / G;
-  const long long it1 = ((long long)blockIdx.x + 1) * total_iters / G;
+  const long long G = gridDim.x / CL;                          // work units are split per cluster
+  const long long cidx = blockIdx.x / CL;
+  const long long it0 = cidx * total_iters / G;
+  const long long it1 = (cidx + 1) * total_iters / G;
   const int t_first = (int)(it0 / kblocks);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL); }
     mbar_init(tfull, 1);
     mbar_init(tempty, 128);
     fence_barrier_init();
@@ -107,6 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();                   // peers' barriers initialised
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -122,11 +131,27 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint8_t* sa = smem + stage * C::STAGE;
         mbar_expect_tx(&full[stage], C::STAGE);
         const int kcoord = FP8K ? kb * 128 : kb * 64;
-        tma_load_2d(sa, &tmA, kcoord, t * TMR, &full[stage], pol_a);
+        tma_load_2d(sa, &tmA, kcoord, (t * CL + crank) * TMR, &full[stage], pol_a);
+        if constexpr (CL == 1) {
 #pragma unroll
-        for (int xb = 0; xb < BN; xb += C::XBOX)
-          tma_load_2d(sa + C::A_ST + xb * KBYTES, &tmX, kcoord, xb, &full[stage], pol_x);
+          for (int xb = 0; xb < BN; xb += C::XBOX)
+            tma_load_2d(sa + C::A_ST + xb * KBYTES, &tmX, kcoord, xb, &full[stage], pol_x);
+        } else {
+#pragma unroll
+          for (int xb = 0; xb < BN; xb += C::XBOX)
+            if ((xb / C::XBOX) % CL == crank)
+              tma_load_2d_mc(sa + C::A_ST + xb * KBYTES, &tmX, kcoord, xb, &full[stage], (uint16_t)((1u << CL) - 1u),
+                             pol_x);
+        }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      if constexpr (CL > 1) {
+        // drain: every stage's last release (this CTA's and the peer's commits) has landed
+        // before the cluster may exit
+        for (int i = 0; i < C::STAGES; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -170,7 +195,8 @@ __global__ void __launch_bounds__(THREADS, 1)
               }
             }
           }
-          tc_commit(&empty[stage]);
+          if constexpr (CL > 1) tc_commit_mc(&empty[stage], (uint16_t)((1u << CL) - 1u));
+          else tc_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit(tfull);
@@ -191,8 +217,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(tfull, acc_phase);
       tc_fence_after();
       float* dst = ws + ((size_t)blockIdx.x * max_slots + (t - t_first)) * (size_t)(TMR * BN);
+      const bool live = (long long)t * CL + crank < m_tiles;       // odd tile count: the pair's 2nd may not exist
 #pragma unroll
       for (int h = 0; h < MH; ++h) {
+        if (!live) break;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
@@ -208,6 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();
   if (stamp && threadIdx.x == 0) atomicMax(&g_k1_stamp[1], gtimer_ns());
   if (warp == 1) {
     tc_fence_after();
@@ -225,7 +254,7 @@ __global__ void __launch_bounds__(256)
     k_finalize(const float* __restrict__ ws, int BN, int kblocks, long long total_iters, int G,
                int max_slots, int64_t rows, int k, void* __restrict__ W, int64_t ldw, int out_fmt,
                double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
-               int out_fmt2, int nsplit, int stamp, int TMR) {
+               int out_fmt2, int nsplit, int stamp, int TMR, int CLN) {
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
     const unsigned long long t0 = g_k1_stamp[0], t1 = g_k1_stamp[1];
     if (t1 > t0) { g_k1_stamp[2] += t1 - t0; g_k1_stamp[3] += 1; }
@@ -239,7 +268,10 @@ __global__ void __launch_bounds__(256)
   const int j0 = blockIdx.y * FIN_COLS;
   const int row = threadIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long x0 = (long long)t * kblocks, x1 = x0 + kblocks - 1;
+  // cluster pairs (CLN = 2): tile t is rank t % 2 of pair t / 2, work split per cluster
+  const int tu = t / CLN, trank = t % CLN;
+  G /= CLN;
+  const long long x0 = (long long)tu * kblocks, x1 = x0 + kblocks - 1;
   // CTA owning iteration x: largest c with seg_begin(c) <= x
   long long c_lo = x0 * G / total_iters, c_hi = x1 * G / total_iters;
   while (c_lo + 1 < G && seg_begin(c_lo + 1, total_iters, G) <= x0) ++c_lo;
@@ -253,8 +285,9 @@ __global__ void __launch_bounds__(256)
   for (int i = 0; i < FIN_COLS; ++i) s[i] = 0.f;
   for (int sl = nsplit - 1; sl >= 0; --sl) {
     for (long long c = c_lo; c <= c_hi; ++c) {
-      const int slot = t - (int)(seg_begin(c, total_iters, G) / kblocks);
-      const float* src = ws + ((size_t)c * max_slots + slot) * (size_t)(TMR * BN) + row + (size_t)sl * k * TMR;
+      const int slot = tu - (int)(seg_begin(c, total_iters, G) / kblocks);
+      const float* src = ws + ((size_t)(c * CLN + trank) * max_slots + slot) * (size_t)(TMR * BN) + row +
+                         (size_t)sl * k * TMR;
 #pragma unroll
       for (int i = 0; i < FIN_COLS; ++i)
         if (j0 + i < k) s[i] += src[(size_t)(j0 + i) * TMR];
@@ -454,17 +487,19 @@ int prof_read(float* ms, int max) {
 }
 
 static int pick_bn(int k) { return k <= 32 ? 32 : ((k + 31) / 32) * 32; }
+static int g_no_cluster = -1;   // OFRR_K1_NO_CLUSTER=1: the wide tile without the cluster pairs
 
 // N > 256 (up to 512): the wide one-M-half tile (TcCfg MH = 1), BN a multiple of 128
 static bool wide_n(int k) { return k > 256; }
 
 struct TcPlan {
-  int bn, m_tiles, kblocks, grid, max_slots, tm;
+  int bn, m_tiles, kblocks, grid, max_slots, tm, cl;
   long long total;
   size_t ws_bytes;
 };
 
 static TcPlan plan_tc(int64_t rows, int64_t cols, int k, int a_fmt) {
+  if (g_no_cluster < 0) { const char* e = getenv("OFRR_K1_NO_CLUSTER"); g_no_cluster = (e && atoi(e) == 1) ? 1 : 0; }
   TcPlan p;
   const bool wide = wide_n(k);
   p.bn = wide ? ((k + 127) / 128) * 128 : pick_bn(k);
@@ -472,12 +507,14 @@ static TcPlan plan_tc(int64_t rows, int64_t cols, int k, int a_fmt) {
   const int kel = (a_fmt == FP8) ? 128 : 64;
   p.m_tiles = (int)((rows + p.tm - 1) / p.tm);
   p.kblocks = (int)((cols + kel - 1) / kel);
-  p.total = (long long)p.m_tiles * p.kblocks;
+  // the wide tile runs as cluster pairs (two 128-row tiles share each B tile by multicast)
+  p.cl = (wide && p.m_tiles >= 2 && !g_no_cluster) ? 2 : 1;
+  p.total = (long long)((p.m_tiles + p.cl - 1) / p.cl) * p.kblocks;   // work units per cluster
   int sms = ofrr_device_sm_count(-1);
   if (sms <= 0) sms = 148;
-  p.grid = (int)std::min<long long>(sms, p.total);
-  if (p.grid < 1) p.grid = 1;
-  const long long per = (p.total + p.grid - 1) / p.grid;
+  const long long nclus = std::min<long long>(sms / p.cl, p.total);
+  p.grid = (int)std::max<long long>(1, nclus) * p.cl;
+  const long long per = (p.total + p.grid / p.cl - 1) / (p.grid / p.cl);
   p.max_slots = (int)((per + p.kblocks - 1) / p.kblocks) + 1;
   p.ws_bytes = (size_t)p.grid * p.max_slots * p.tm * p.bn * sizeof(float);
   return p;
@@ -487,11 +524,11 @@ size_t tc_workspace(int64_t rows, int64_t cols, int k, int a_fmt) {
   return plan_tc(rows, cols, k, a_fmt).ws_bytes;
 }
 
-template <int BN, bool FP8K, int MH>
+template <int BN, bool FP8K, int MH, int CL>
 static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPlan& p, float* ws,
                         uint32_t idesc, uint32_t idesc2, cudaStream_t st) {
   using C = TcCfg<BN, MH>;
-  auto kern = k_gemm_av_tc<BN, FP8K, MH>;
+  auto kern = k_gemm_av_tc<BN, FP8K, MH, CL>;
   static bool attr_done = false;
   if (!attr_done) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
@@ -499,8 +536,26 @@ static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPl
   }
   cudaEvent_t* ev = prof_slot();
   if (ev) prof_record(ev[0], st);
-  kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc, g_stamp_on ? 1 : 0,
-                                               idesc2);
+  const int stamp = g_stamp_on ? 1 : 0;
+  if constexpr (CL == 1) {
+    kern<<<p.grid, THREADS, C::SMEM_BYTES, st>>>(tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc, stamp, idesc2,
+                                                 p.m_tiles);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    OFRR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tX, ws, p.kblocks, p.total, p.max_slots, idesc, stamp, idesc2,
+                                     p.m_tiles));
+  }
   if (ev) prof_record(ev[1], st);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
@@ -526,10 +581,12 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
   if (rc) return rc;
   const uint32_t idesc = make_idesc(a_fmt, wide ? 256 : p.bn);
   const uint32_t idesc2 = wide ? make_idesc(a_fmt, p.bn - 256) : 0u;
-#define TC_CASE(B) case B: rc = fp8 ? launch_tc_bn<B, true, 2>(tA, tX, p, (float*)ws, idesc, idesc2, st) \
-                                  : launch_tc_bn<B, false, 2>(tA, tX, p, (float*)ws, idesc, idesc2, st); break;
-#define TC_WIDE(B) case B: rc = fp8 ? launch_tc_bn<B, true, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st) \
-                                  : launch_tc_bn<B, false, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st); break;
+#define TC_CASE(B) case B: rc = fp8 ? launch_tc_bn<B, true, 2, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st) \
+                                  : launch_tc_bn<B, false, 2, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st); break;
+#define TC_WIDE(B) case B: if (p.cl == 2) { rc = fp8 ? launch_tc_bn<B, true, 1, 2>(tA, tX, p, (float*)ws, idesc, idesc2, st) \
+                                               : launch_tc_bn<B, false, 1, 2>(tA, tX, p, (float*)ws, idesc, idesc2, st); } \
+                           else { rc = fp8 ? launch_tc_bn<B, true, 1, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st) \
+                                           : launch_tc_bn<B, false, 1, 1>(tA, tX, p, (float*)ws, idesc, idesc2, st); } break;
   if (wide) {
     switch (p.bn) {
       TC_WIDE(384)
@@ -546,7 +603,7 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
   if (rc) return rc;
   k_finalize<<<dim3(p.m_tiles, (k / nsplit + FIN_COLS - 1) / FIN_COLS), p.tm, 0, st>>>((const float*)ws, p.bn, p.kblocks, p.total, p.grid, p.max_slots,
                                         rows, k / nsplit, W, ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
-                                        nsplit, g_stamp_on ? 1 : 0, p.tm);
+                                        nsplit, g_stamp_on ? 1 : 0, p.tm, p.cl);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }

@@ -341,7 +341,8 @@ def test_generator_bitwise(ofrr_gpu, oracle, n):
     np.testing.assert_allclose(ev[:50], lam[:50], atol=1e-13)
 
 
-@pytest.mark.parametrize("shape", [(2048, 2048, 64), (1000, 3000, 20), (4096, 1024, 85), (1024, 2048, 128), (700, 640, 200)])
+@pytest.mark.parametrize("shape", [(2048, 2048, 64), (1000, 3000, 20), (4096, 1024, 85), (1024, 2048, 128), (700, 640, 200),
+                                   (640, 512, 128), (100, 300, 90)])
 def test_gemm_split_fp32_block_vs_fp64(ofrr_gpu, oracle, shape):
     """K1 split mode: bf16 A times an fp32 block via three bf16 slices is fp32-accurate."""
     import torch
