@@ -363,7 +363,10 @@ def run_ours(args, cfg):
     op = ops.new_operator(r1 - r0, n, fmt, dev)
     times = []
     h2d = d2h = 0
-    for i in range(max(1, min(3, args.steps)) + 1):
+    # the first three solves of this operator warm its graphs (eager, capture, device-loop
+    # build -- the same warm-up the timed region had); the next ones are timed
+    n_warm_e2e = 3
+    for i in range(max(1, min(3, args.steps)) + n_warm_e2e):
         barrier()
         t0 = time.perf_counter()
         op.t[:, :n].copy_(a_host, non_blocking=True)           # H2D of this step's A rows
@@ -375,7 +378,7 @@ def run_ours(args, cfg):
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        if i > 0:
+        if i >= n_warm_e2e:
             times.append(float(dt.item()))
         h2d = a_host.numel() * a_host.element_size()
         d2h = vals.nbytes + vecs.nbytes + rsh.residuals.nbytes

@@ -113,10 +113,16 @@ class DevBlock:
         return self.t[:k, : self.n]
 
     def to_numpy_f64(self, k: Optional[int] = None):
-        """Host copy as an F-order float64 n x k array (the reference's layout)."""
+        """Host copy as an F-order float64 n x k array (the reference's layout).  The copy
+        lands in pinned memory from torch's caching host allocator (fast DMA, no page faults
+        on fresh pages; the block returns to the cache when the caller drops the array)."""
         import numpy as np
-        v = self.col_view(k).to(torch.float64).cpu().numpy()
-        return np.asfortranarray(v.T)
+        v = self.col_view(k)
+        if v.is_cuda:
+            h = torch.empty(v.shape, dtype=torch.float64, pin_memory=True)
+            h.copy_(v)                                    # (k, n) C-order == (n, k) F-order
+            return h.numpy().T
+        return np.asfortranarray(v.to(torch.float64).numpy().T)
 
     def narrow(self, k: int) -> "DevBlock":
         return DevBlock(self.t, self.n, int(k), self.fmt)
