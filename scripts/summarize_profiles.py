@@ -19,6 +19,9 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (SM cycles)"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("launch__cluster_dim_x", "cluster size"),
     ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
      "tensor pipe active % (elapsed)"),
     ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor memory (smem->TC) active %"),
@@ -103,6 +106,7 @@ def launches(name="launches_c2_bench.csv"):
 if __name__ == "__main__":
     launches()
     summarize_rep("k1_c2", "K1 bf16 block k=64 at C2 shape, third launch")
+    summarize_rep("k1_wide_c3", "K1 wide tile as cluster pairs, fp32 block k=128 split (N=384) at C3 shape 65536^2")
     summarize_rep("ozk_gemm_c2", "K7z int8 Ozaki product with in-kernel digit conversion, C2 residual r=64")
     summarize_rep("oz_rowscale_c2", "K7z row scales of A (one pass over A), C2")
     summarize_rep("gram_c2", "K4 Gram partials (DMMA), n=16384 k=64 fp32 basis")
