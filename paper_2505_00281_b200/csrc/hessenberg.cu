@@ -35,6 +35,7 @@ struct HessWs {
   long long* cand_idx;  // [2][G]
   double* cand_row;   // [2][G][k]
   unsigned char* freerow;  // [n]
+  ulonglong2* slot;   // [2][G] narrow storage: (packed key, (pivot value, next-column value) as f32 bits)
 };
 
 __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* sv, long long* si) {
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(HT)
   // F64 storage: (value, row) per CTA, reduced by every CTA after the barrier.
   constexpr bool KEYED = !std::is_same<T, double>::value;
   __shared__ unsigned long long sk[HT / 32];
+  __shared__ float s_v0, s_v1;                               // candidate / pivot: value, next column
   // this thread's candidate over its rows i (free rows only) of column jn
   auto local_scan = [&](int jn, double& v, long long& idx, unsigned long long& key) {
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
@@ -254,7 +256,6 @@ __global__ void __launch_bounds__(HT)
     if constexpr (KEYED) {
       key = block_max_key(key, sk);
       idx = key ? (long long)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull)) : -1;
-      if (threadIdx.x == 0 && key) atomicMax(&ws.key[jn], key);
     } else {
       block_argmax(v, idx, sv, si);
       if (threadIdx.x == 0) {
@@ -273,6 +274,22 @@ __global__ void __launch_bounds__(HT)
             y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(PR[(size_t)q * k + cc], ld_c<C>(col(s_pl[q])[idx]))));
         }
         ws.cand_row[((int64_t)buf * G + c) * k + cc] = el_d(y);
+        if constexpr (KEYED) {
+          if (cc == jn) s_v0 = (float)el_d(y);
+          if (cc == jn + 1) s_v1 = (float)el_d(y);
+        }
+      }
+    }
+    if constexpr (KEYED) {
+      // one 16-byte slot per CTA: the winner's pivot and next-column values travel with the
+      // key, so the critical path after the barrier needs no second read of the row
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const float v1 = jn + 1 < k ? s_v1 : 0.0f;
+        ulonglong2 sv;
+        sv.x = idx >= 0 ? key : 0ull;
+        sv.y = ((unsigned long long)__float_as_uint(s_v0) << 32) | (unsigned long long)__float_as_uint(v1);
+        __stcg(&ws.slot[buf * G + c], sv);
       }
     }
   };
@@ -338,11 +355,20 @@ __global__ void __launch_bounds__(HT)
     long long r;
     int owner;
     if constexpr (KEYED) {
-      // every thread reads the column's winning key (one L2 word)
-      const unsigned long long key = __ldcg(&ws.key[j]);
+      // the G slots (one 16-byte read per thread), max key -> pivot row, its value and the
+      // next column's value
+      ulonglong2 sv = make_ulonglong2(0ull, 0ull);
+      if (threadIdx.x < G) sv = __ldcg(&ws.slot[buf * G + threadIdx.x]);
+      const unsigned long long key = block_max_key(threadIdx.x < G ? sv.x : 0ull, sk);
+      if (key && sv.x == key && threadIdx.x < G) {
+        s_owner = threadIdx.x;
+        s_v0 = __uint_as_float((unsigned)(sv.y >> 32));
+        s_v1 = __uint_as_float((unsigned)(sv.y & 0xffffffffull));
+      }
+      __syncthreads();
       r = key ? (long long)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull)) : -1;
       best = (double)__uint_as_float((unsigned)(key >> 32));
-      owner = r >= 0 ? (int)(r / rows_per) : 0;
+      owner = r >= 0 ? s_owner : 0;
     } else {
       // warp 0 reduces the CTAs' candidates; max value, ties -> lowest row (CTA row
       // blocks ascend, so the lowest row is the reference's np.argmax choice)
@@ -375,10 +401,26 @@ __global__ void __launch_bounds__(HT)
     if (!skip) {
       // pivot row (values exact in the storage format); alpha_c = round_c(a[r, c]) is the
       // value itself (storage <= compute)
-      for (int cc = j + threadIdx.x; cc < k; cc += HT) {
-        const double a = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
-        prow[cc] = a;
-        pc[cc] = (CV)a;
+      // narrow storage: the row's loads are issued now and land in shared memory after the
+      // column work below (which needs only the pivot and next-column values of the slot)
+      double prr[2] = {0.0, 0.0};
+      if constexpr (KEYED) {
+#pragma unroll
+        for (int t2 = 0; t2 < 2; ++t2) {
+          const int cc = j + threadIdx.x + t2 * HT;
+          if (cc < k) prr[t2] = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
+        }
+        for (int cc = j + threadIdx.x + 2 * HT; cc < k; cc += HT) {   // k > 2 HT + j: rare
+          const double a = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
+          prow[cc] = a;
+          pc[cc] = (CV)a;
+        }
+      } else {
+        for (int cc = j + threadIdx.x; cc < k; cc += HT) {
+          const double a = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
+          prow[cc] = a;
+          pc[cc] = (CV)a;
+        }
       }
       if (r >= r0 && r < r1 && threadIdx.x == 0) ws.freerow[r] = 0;
       if (c == 0 && threadIdx.x == 0) { kept[j] = 1; pivots[nk] = r; }
@@ -390,8 +432,8 @@ __global__ void __launch_bounds__(HT)
       __syncthreads();
       if (pb > 1 && pe < k && threadIdx.x == 0) { s_pl[s_npl] = j; s_npl = s_npl + 1; }
       mark(1);
-      const CV piv = pc[j];
-      const CV a1 = j + 1 < pe ? pc[j + 1] : CV(0);
+      const CV piv = KEYED ? (CV)s_v0 : pc[j];
+      const CV a1 = j + 1 < pe ? (KEYED ? (CV)s_v1 : pc[j + 1]) : CV(0);
       // ofrr/basis.py:181-187: v = round_s(round_c(v / piv)); v[r] = 1; then (188-190,
       // precision.py:172-180) column j+1 at once -- the next pivot search needs it -- and
       // this thread's candidate for it
@@ -415,6 +457,13 @@ __global__ void __launch_bounds__(HT)
               if (cidx < 0 || a > cv) { cv = a; cidx = i; }
             }
           }
+        }
+      }
+      if constexpr (KEYED) {
+#pragma unroll
+        for (int t2 = 0; t2 < 2; ++t2) {
+          const int cc = j + threadIdx.x + t2 * HT;
+          if (cc < k) { prow[cc] = prr[t2]; pc[cc] = (CV)prr[t2]; }
         }
       }
       mark(2);
@@ -540,6 +589,7 @@ size_t hessenberg_ws(int64_t n, int k, int storage) {
   b += 2 * G * sizeof(double);
   b += 2 * G * sizeof(long long);
   b += (size_t)2 * G * k * sizeof(double);
+  b += (size_t)2 * G * 16 + 256;            // slots
   b += (size_t)n * fmt_bytes(storage) * k;  // working copy
   b += n;
   return b + 4096;
@@ -558,6 +608,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   h.cand_val = (double*)take(2 * G * sizeof(double));
   h.cand_idx = (long long*)take(2 * G * sizeof(long long));
   h.cand_row = (double*)take((size_t)2 * G * k * sizeof(double));
+  h.slot = (ulonglong2*)take((size_t)2 * G * 16);
   T* Xw = (T*)take((size_t)n * sizeof(T) * k);
   h.freerow = (unsigned char*)take(n);
   const T* Xp = (const T*)X;
