@@ -97,6 +97,20 @@ __device__ __forceinline__ void oz_planes4(const uint32_t (&lo)[4], const uint32
   w[4] = tl[1] ^ 0x80808080u;
   w[5] = tl[0] ^ 0x80808080u;
 }
+// plain two's-complement bytes of four fixed-point words (lo, hi) = t: byte 5 (signed: the
+// sign lives there since |t| < 2^46) first, bytes 4..0 unsigned -- the A digits of the
+// in-kernel product (no bias add, no byte flip; the MMA takes plane 0 as s8, 1..5 as u8)
+__device__ __forceinline__ void oz_planes4u(const uint32_t (&lo)[4], const uint32_t (&hi)[4], uint32_t (&w)[OZ_D]) {
+  uint32_t tl[4], th[4];
+  oz_t4(lo, tl);
+  oz_t4(hi, th);
+  w[0] = th[1];
+  w[1] = th[0];
+  w[2] = tl[3];
+  w[3] = tl[2];
+  w[4] = tl[1];
+  w[5] = tl[0];
+}
 __device__ __forceinline__ void oz_bias(uint32_t& lo, uint32_t& hi) {
   const uint32_t l = lo + 0x80808080u;
   hi = hi + 0x8080u + (l < lo ? 1u : 0u);
@@ -495,7 +509,9 @@ __global__ void __launch_bounds__(256)
 static constexpr int OZK_KB = 64;          // K elements (= int8 bytes) per k-block
 static constexpr int OZK_CONV_WARPS = 16;
 static constexpr int OZK_THREADS = 192 + 32 * OZK_CONV_WARPS;
-static constexpr int OZK_MAXCHUNK = 256;   // k-blocks per chunk (16384 terms)
+// k-blocks per chunk (8192 terms): with u8 A digits (<= 255) x s8 V digits a level sums up
+// to 6 products of |d| <= 255 * 128 per term -- 6 * 32640 * 8192 < 2^31
+static constexpr int OZK_MAXCHUNK = 128;
 
 template <int BN>
 struct OzkCfg {
@@ -641,7 +657,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
               for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
                 const int ng = std::min(256 / BN, nq - q0);
                 mma_i8(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
-                       dv + (uint64_t)((q0 * BN * OZK_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN, true, true),
+                       dv + (uint64_t)((q0 * BN * OZK_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN, p == 0, true),
                        acc);
               }
             }
@@ -746,13 +762,12 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
           uint32_t lo[4], hi[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const unsigned long long t =
-                (unsigned long long)__float2ll_rz(ozk_elem<FMT>(raw, 4 * g + e) * sc) + 0x808080808080ull;
+            const unsigned long long t = (unsigned long long)__float2ll_rz(ozk_elem<FMT>(raw, 4 * g + e) * sc);
             lo[e] = (uint32_t)t;
             hi[e] = (uint32_t)(t >> 32);
           }
           uint32_t pw[OZ_D];
-          oz_planes4(lo, hi, pw);
+          oz_planes4u(lo, hi, pw);
 #pragma unroll
           for (int p = 0; p < OZ_D; ++p) w[p][g] = pw[p];
         }
@@ -764,13 +779,17 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
           for (int e = 0; e < 4; ++e) {
             if (row_ok && E != OZ_BAD) {
               oz_fixed32(__float_as_uint(ozk_elem<FMT>(raw, 4 * g + e)), E, lo[e], hi[e]);
+              // back to the plain two's-complement word (oz_fixed32 returns it biased)
+              const unsigned long long t = (((unsigned long long)hi[e] << 32) | lo[e]) - 0x808080808080ull;
+              lo[e] = (uint32_t)t;
+              hi[e] = (uint32_t)(t >> 32);
             } else {
-              lo[e] = 0x80808080u;
-              hi[e] = 0x8080u;
+              lo[e] = 0u;
+              hi[e] = 0u;
             }
           }
           uint32_t pw[OZ_D];
-          oz_planes4(lo, hi, pw);
+          oz_planes4u(lo, hi, pw);
 #pragma unroll
           for (int p = 0; p < OZ_D; ++p) w[p][g] = pw[p];
         }
