@@ -719,15 +719,23 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
     // (tile, k-block) of the next fetch, advanced without 64-bit divisions (they were a
     // fifth of the converters' instructions)
     int fvt = (int)(u0 / kbc), frem = (int)(u0 % kbc);
+    // the fetch position's row, chunk start and row base address, refreshed only when the
+    // virtual tile changes (no divisions per k-block)
+    int fch = fvt % nchunks;
+    int64_t fgrow = (int64_t)(fvt / nchunks) * OZ_TM + r;
+    const uint8_t* frow = (const uint8_t*)A + (fgrow * lda + qt * 16) * EB;
     auto fetch = [&](long long /*u*/, uint4 (&raw)[2]) {
-      const int vt = fvt;
-      const int kb = (vt % nchunks) * kbc + frem;
-      if (++frem == kbc) { frem = 0; ++fvt; }
-      const int64_t grow = (int64_t)(vt / nchunks) * OZ_TM + r;
+      const int kb = fch * kbc + frem;
+      const int64_t grow = fgrow;
+      const uint8_t* src = frow + (int64_t)kb * OZK_KB * EB;
+      if (++frem == kbc) {
+        frem = 0;
+        ++fvt;
+        if (++fch == nchunks) { fch = 0; fgrow += OZ_TM; frow += (int64_t)OZ_TM * lda * EB; }
+      }
       raw[0] = raw[1] = make_uint4(0, 0, 0, 0);
       if (grow >= rows) return;
-      const int64_t o = grow * lda, l0 = (int64_t)kb * OZK_KB + qt * 16;
-      const uint8_t* src = (const uint8_t*)A + (o + l0) * EB;
+      const int64_t l0 = (int64_t)kb * OZK_KB + qt * 16;
       if (l0 + 16 <= cols && ((reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
         raw[0] = __ldcs(reinterpret_cast<const uint4*>(src));
         if (EB == 2) raw[1] = __ldcs(reinterpret_cast<const uint4*>(src) + 1);
