@@ -193,7 +193,7 @@ class EigEngine:
     """Device state of one subspace_iter_eig run (single GPU or row-partitioned)."""
 
     def __init__(self, a: DenseMatrix, cfg: IterConfig, comm: Optional[Comm] = None, n_global: Optional[int] = None,
-                 ops=None):
+                 ops=None, report_scales: bool = True):
         self.ops = ops or _ops
         self.comm = comm or Comm.world()
         self.cfg = cfg
@@ -215,8 +215,10 @@ class EigEngine:
         # the pencil solve occupies one SM (off the critical path), see _body
         self._res_oz = None
         self._refresh_now = True    # first iteration of a run: refresh the report's row scales
-        if (self.ops is _ops and not self.comm.distributed and FpFormat.F64 not in (self.mv.storage, self.pol.storage)
-                and hasattr(a, "residual_operator")):
+        # (a ladder rung that hands over to the next never reports: no early scale refresh;
+        # if it ends the run after all, the report prepares its operator then)
+        if (report_scales and self.ops is _ops and not self.comm.distributed
+                and FpFormat.F64 not in (self.mv.storage, self.pol.storage) and hasattr(a, "residual_operator")):
             A_res = a.residual_operator(self.A_mv.fmt)
             if A_res.fmt in _ops.OZAKI_FMTS:
                 self._res_oz = _ops.OzakiOperator(A_res, prepare=False)
@@ -786,7 +788,7 @@ def subspace_iter_eig(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats]
         # progress, then continue from its restart block in cfg.policy
         from dataclasses import replace as _replace
         low = _replace(cfg, policy=cfg.ladder, matvec_policy=None, ladder=None)
-        eng0 = EigEngine(a, low, comm=comm, n_global=n)
+        eng0 = EigEngine(a, low, comm=comm, n_global=n, report_scales=False)
         X0 = eng0.run(stop_estimate=cfg.ladder_switch)
         if isinstance(X0, RitzSet):                                # m exhausted in the low rung
             if stats is not None:
