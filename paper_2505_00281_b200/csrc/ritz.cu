@@ -6,71 +6,84 @@ namespace ofrr {
 
 // ---------------------------------------------------------------------------------
 // K6: Ut = scale * U[:, :kp] * Y[:kp, :r]  in fp64, fused with the storage rounding of
-// the restart block.  Replaces ofrr/projection.py:86 / :129-130 and ofrr/driver.py:109.
-// Block = 64 rows x 64 columns, 256 threads (4 x 4 outputs each), kp in slabs of 16.
+// the restart block (and, for A-pass reuse, the column inf-norms of the rounded block).
+// Replaces ofrr/projection.py:86 / :129-130 and ofrr/driver.py:109.  On the fp64 tensor
+// cores (DMMA m8n8k4): 64 x 64 output tile per CTA, each warp a 16 x 32 block (2 x 4 MMA
+// tiles), kp in slabs of 16 staged in shared memory as fp64 (storage values are exact).
 // ---------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884r(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
 template <typename T>
 __global__ void __launch_bounds__(256)
-    k_ritz(const T* __restrict__ U, int64_t ldu, int64_t n, int kp, const double* __restrict__ Y, int ldy,
-           const int* __restrict__ r_dev, int r_max, double scale, double* __restrict__ Ut64, int64_t ldo64,
-           void* __restrict__ Xout, int64_t ldx, int x_fmt, int* __restrict__ flags,
-           double* __restrict__ colmax) {
-  __shared__ double Us[16][65];
-  __shared__ double Ys[16][65];
+    k_ritz_dmma(const T* __restrict__ U, int64_t ldu, int64_t n, int kp, const double* __restrict__ Y, int ldy,
+                const int* __restrict__ r_dev, int r_max, double scale, double* __restrict__ Ut64, int64_t ldo64,
+                void* __restrict__ Xout, int64_t ldx, int x_fmt, int* __restrict__ flags,
+                double* __restrict__ colmax) {
+  constexpr int RS = 16 + 4;                 // Us row stride (doubles)
+  __shared__ double Us[64][RS];              // [row][l]
+  __shared__ double Ys[16][64 + 4];          // [l][col]
   __shared__ double cm[64];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
   const int64_t m0 = (int64_t)blockIdx.x * 64;
   const int n0 = blockIdx.y * 64;
   const int r = r_dev ? min(r_max, *r_dev) : r_max;
-  double acc[4][4] = {};
+  double acc[2][4][2] = {};
   for (int l0 = 0; l0 < kp; l0 += 16) {
     for (int e = tid; e < 16 * 64; e += 256) {
       const int rr = e & 63, ll = e >> 6;
       const int64_t gi = m0 + rr;
-      Us[ll][rr] = (gi < n && l0 + ll < kp) ? to_d(U[(int64_t)(l0 + ll) * ldu + gi]) : 0.0;
-      const int cc = e & 63;
-      const int gj = n0 + cc;
-      Ys[ll][cc] = (gj < r && l0 + ll < kp) ? Y[(int64_t)gj * ldy + l0 + ll] : 0.0;
+      Us[rr][ll] = (gi < n && l0 + ll < kp) ? to_d(U[(int64_t)(l0 + ll) * ldu + gi]) : 0.0;
+      const int gj = n0 + rr;
+      Ys[ll][rr] = (gj < r && l0 + ll < kp) ? Y[(int64_t)gj * ldy + l0 + ll] : 0.0;
     }
     __syncthreads();
 #pragma unroll
-    for (int ll = 0; ll < 16; ++ll) {
-      double a[4], b[4];
+    for (int kk = 0; kk < 16; kk += 4) {
+      double a[2], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = Us[ll][ty + 16 * i];
+      for (int i = 0; i < 2; ++i) a[i] = Us[wm + 8 * i + g][kk + t];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Ys[ll][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) b[j] = Ys[kk + t][wn + 8 * j + g];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma884r(acc[i][j], a[i], b[j]);
     }
     __syncthreads();
   }
-  int bad = 0;
   if (colmax && tid < 64) cm[tid] = 0.0;
   if (colmax) __syncthreads();
-  double cmax[4] = {0.0, 0.0, 0.0, 0.0};
+  int bad = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int j = 0; j < 4; ++j) {
+    double cmx[2] = {0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t gi = m0 + ty + 16 * i;
-      const int gj = n0 + tx + 16 * j;
-      if (gi >= n || gj >= r_max) continue;
-      const double v = gj < r ? scale * acc[i][j] : 0.0;
-      if (Ut64) Ut64[(int64_t)gj * ldo64 + gi] = v;
-      if (Xout) {
-        const double xv = rnd(v, x_fmt);
-        if (!isfinite(xv)) bad = 1;
-        st_fmt(Xout, (int64_t)gj * ldx + gi, x_fmt, xv);
-        cmax[j] = fmax(cmax[j], fabs(xv));
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gi = m0 + wm + 8 * i + g;
+        const int gj = n0 + wn + 8 * j + 2 * t + h;
+        if (gi >= n || gj >= r_max) continue;
+        const double v = gj < r ? scale * acc[i][j][h] : 0.0;
+        if (Ut64) Ut64[(int64_t)gj * ldo64 + gi] = v;
+        if (Xout) {
+          const double xv = rnd(v, x_fmt);
+          if (!isfinite(xv)) bad = 1;
+          st_fmt(Xout, (int64_t)gj * ldx + gi, x_fmt, xv);
+          cmx[h] = fmax(cmx[h], fabs(xv));
+        }
       }
-    }
-  if (bad && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
-  if (colmax) {                       // column inf-norms of the rounded block (K2's input)
+    if (colmax) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) atomic_max_nonneg(&cm[tx + 16 * j], cmax[j]);
+      for (int h = 0; h < 2; ++h) atomic_max_nonneg(&cm[wn + 8 * j + 2 * t + h], cmx[h]);
+    }
+  }
+  if (bad && flags) atomicOr(flags, OFRR_FLAG_NONFINITE);
+  if (colmax) {
     __syncthreads();
     if (tid < 64 && n0 + tid < r_max) atomic_max_nonneg(&colmax[n0 + tid], cm[tid]);
   }
@@ -82,11 +95,11 @@ int ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const
   if (n <= 0 || r_max <= 0) return OFRR_OK;
   dim3 grid((unsigned)((n + 63) / 64), (unsigned)((r_max + 63) / 64));
   switch (u_fmt) {
-    case F64: k_ritz<double><<<grid, 256, 0, st>>>((const double*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
-    case F32: k_ritz<float><<<grid, 256, 0, st>>>((const float*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
-    case F16: k_ritz<__half><<<grid, 256, 0, st>>>((const __half*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
-    case BF16: k_ritz<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
-    case FP8: k_ritz<__nv_fp8_e4m3><<<grid, 256, 0, st>>>((const __nv_fp8_e4m3*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case F64: k_ritz_dmma<double><<<grid, 256, 0, st>>>((const double*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case F32: k_ritz_dmma<float><<<grid, 256, 0, st>>>((const float*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case F16: k_ritz_dmma<__half><<<grid, 256, 0, st>>>((const __half*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case BF16: k_ritz_dmma<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
+    case FP8: k_ritz_dmma<__nv_fp8_e4m3><<<grid, 256, 0, st>>>((const __nv_fp8_e4m3*)U, ldu, n, kp, Y, ldy, r_dev, r_max, scale, Ut64, ldo64, Xout, ldx, x_fmt, flags, colmax); break;
     default: ofrr_set_error("ritz: basis format %d unsupported", u_fmt); return OFRR_ERR_UNSUPPORTED;
   }
   OFRR_CHECK_LAUNCH();
