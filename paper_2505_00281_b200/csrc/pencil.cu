@@ -367,6 +367,13 @@ __global__ void __launch_bounds__(PT, 1)
 // (S -= u (q_c - K u_c) + p u_c), the group of column j+1 accumulating the norm of its
 // new column on the way and forming the next reflector at once; barrier (B).
 // ---------------------------------------------------------------------------------
+__device__ __forceinline__ double pc_sum8(const double* r) {
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  double v[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) { const double2 x = r2[w]; v[w] = x.x + x.y; }
+  return (v[0] + v[1]) + (v[2] + v[3]);
+}
 __device__ __forceinline__ double pc_sum16(const double* r) {
   const double2* r2 = reinterpret_cast<const double2*>(r);
   double v[8];
@@ -375,14 +382,15 @@ __device__ __forceinline__ double pc_sum16(const double* r) {
   return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
 }
 
-template <int TPC, int RPT>
-__global__ void __launch_bounds__(PT, 1)
+template <int TPC, int RPT, int NT = PT>
+__global__ void __launch_bounds__(NT, 1)
     k_pc_tri_reg(const double* __restrict__ Tg, int k, double* __restrict__ tri, double* __restrict__ Rg,
                  int* __restrict__ gate) {
   if (*gate) return;
-  static_assert(PNW == 16, "pc_sum16 folds 16 warp partials");
+  constexpr int NW = NT / 32;
+  static_assert(NW == 16 || NW == 8, "16 or 8 warp partials");
   constexpr int RP = RPT + 2;                                     // padded chunk
-  __shared__ __align__(16) double red[2][PNW];
+  __shared__ __align__(16) double red[2][NW];
   __shared__ __align__(16) double uv[2][TPC * RP];               // reflector of the step, by parity
   __shared__ __align__(16) double pv[TPC * RP];
   __shared__ double dd[PK_MAX], ee[PK_MAX], tau[PK_MAX];
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(PT, 1)
     const int i = r0 + t;
     a[t] = (colok && i < k) ? 0.5 * (Tg[(size_t)c * k + i] + Tg[(size_t)i * k + c]) : 0.0;
   }
-  for (int i = threadIdx.x; i < TPC * RP; i += PT) {            // rows >= k stay zero
+  for (int i = threadIdx.x; i < TPC * RP; i += NT) {            // rows >= k stay zero
     pv[i] = 0.0;
     uv[0][i] = 0.0;
     uv[1][i] = 0.0;
@@ -484,7 +492,7 @@ __global__ void __launch_bounds__(PT, 1)
     __syncthreads();                                                     // (A)
     double s2 = 0.0;                                                     // column j+1's new norm
     if (!skip && own) {
-      const double K = 0.5 * tj * pc_sum16(red[buf]);
+      const double K = 0.5 * tj * (NW == 16 ? pc_sum16(red[buf]) : pc_sum8(red[buf]));
       const double qc = fma(-K, uc, pc) - K * uc;                        // q_c - K u_c
       const double* pb = pv + sub * RP;
 #pragma unroll
@@ -526,7 +534,7 @@ __global__ void __launch_bounds__(PT, 1)
   }
   __syncthreads();
   pc_mark(5);
-  for (int i = threadIdx.x; i < k; i += PT) {
+  for (int i = threadIdx.x; i < k; i += NT) {
     tri[i] = dd[i];
     tri[k + i] = ee[i];
     tri[2 * k + i] = tau[i];
@@ -1037,7 +1045,7 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
     k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);
     OFRR_CHECK_LAUNCH();
   }
-  if (k <= 64) k_pc_tri_reg<8, 8><<<1, PT, 0, st>>>(T, k, tri, R, gate);
+  if (k <= 64) k_pc_tri_reg<8, 8><<<1, PT, 0, st>>>(T, k, tri, R, gate);   // (<4, 16, 256>: same 2.4K cycles per step)
   else if (k <= 128) k_pc_tri_reg<4, 32><<<1, PT, 0, st>>>(T, k, tri, R, gate);
   else k_pc_tri<<<1, PT, shm, st>>>(T, k, tri, R, gate);
   OFRR_CHECK_LAUNCH();
