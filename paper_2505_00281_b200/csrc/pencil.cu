@@ -1035,8 +1035,12 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
   // register-resident for k <= 64 (k = 64: 61 -> 51 us); at k = 128 the 32-row register
   // blocks make the in-smem kernel faster (100 + 116 us vs 131 + 257 us)
   if (k <= 64) {
-    // Cholesky, inverse, certificate and T = X sym(B) X^T in one kernel
-    k_pc_chol_reg<8, 8><<<1, PT, (size_t)2 * k * k * sizeof(double), st>>>(M, k, X, gate, B, T);
+    // register Cholesky + inverse + certificate; T on the multi-CTA GEMMs (the in-kernel
+    // T = X sym(B) X^T measured 65 us against 28 us for the two launches)
+    k_pc_chol_reg<8, 8><<<1, PT, (size_t)2 * k * k * sizeof(double), st>>>(M, k, X, gate, nullptr, nullptr);
+    OFRR_CHECK_LAUNCH();
+    k_pc_gemm<false, false, true><<<gg, 256, 0, st>>>(X, B, T1, k, gate);
+    k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);
     OFRR_CHECK_LAUNCH();
   } else {
     k_pc_chol<<<1, PT, shm, st>>>(M, k, X, gate);
