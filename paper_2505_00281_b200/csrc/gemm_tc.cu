@@ -272,22 +272,35 @@ __global__ void __launch_bounds__(256)
   const int tu = t / CLN, trank = t % CLN;
   G /= CLN;
   const long long x0 = (long long)tu * kblocks, x1 = x0 + kblocks - 1;
-  // CTA owning iteration x: largest c with seg_begin(c) <= x
-  long long c_lo = x0 * G / total_iters, c_hi = x1 * G / total_iters;
-  while (c_lo + 1 < G && seg_begin(c_lo + 1, total_iters, G) <= x0) ++c_lo;
-  while (c_lo > 0 && seg_begin(c_lo, total_iters, G) > x0) --c_lo;
-  while (c_hi + 1 < G && seg_begin(c_hi + 1, total_iters, G) <= x1) ++c_hi;
-  while (c_hi > 0 && seg_begin(c_hi, total_iters, G) > x1) --c_hi;
+  // the CTAs owning the tile's iterations and their partial slots: thread 0 resolves them
+  // once per block (64-bit divisions), every thread reads the table
+  constexpr int MAXC = 160;
+  __shared__ long long s_base[MAXC];
+  __shared__ int s_nc;
+  if (threadIdx.x == 0) {
+    // CTA owning iteration x: largest c with seg_begin(c) <= x
+    long long c_lo = x0 * G / total_iters, c_hi = x1 * G / total_iters;
+    while (c_lo + 1 < G && seg_begin(c_lo + 1, total_iters, G) <= x0) ++c_lo;
+    while (c_lo > 0 && seg_begin(c_lo, total_iters, G) > x0) --c_lo;
+    while (c_hi + 1 < G && seg_begin(c_hi + 1, total_iters, G) <= x1) ++c_hi;
+    while (c_hi > 0 && seg_begin(c_hi, total_iters, G) > x1) --c_hi;
+    int nc = 0;
+    for (long long c = c_lo; c <= c_hi && nc < MAXC; ++c, ++nc) {
+      const int slot = tu - (int)(seg_begin(c, total_iters, G) / kblocks);
+      s_base[nc] = ((long long)(c * CLN + trank) * max_slots + slot) * (long long)(TMR * BN);
+    }
+    s_nc = nc;
+  }
+  __syncthreads();
+  const int nc = s_nc;
   const int64_t grow = (int64_t)t * TMR + row;
   const bool valid = grow < rows;
   float s[FIN_COLS];
 #pragma unroll
   for (int i = 0; i < FIN_COLS; ++i) s[i] = 0.f;
   for (int sl = nsplit - 1; sl >= 0; --sl) {
-    for (long long c = c_lo; c <= c_hi; ++c) {
-      const int slot = tu - (int)(seg_begin(c, total_iters, G) / kblocks);
-      const float* src = ws + ((size_t)(c * CLN + trank) * max_slots + slot) * (size_t)(TMR * BN) + row +
-                         (size_t)sl * k * TMR;
+    for (int q = 0; q < nc; ++q) {
+      const float* src = ws + s_base[q] + row + (size_t)sl * k * TMR;
 #pragma unroll
       for (int i = 0; i < FIN_COLS; ++i)
         if (j0 + i < k) s[i] += src[(size_t)(j0 + i) * TMR];

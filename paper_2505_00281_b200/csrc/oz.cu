@@ -843,31 +843,59 @@ __global__ void __launch_bounds__(OZ_TM)
   const bool valid = grow < rows;
   const int Ti = valid ? T[grow] : 0;
   const int nvalid = r_dev ? min(j0 + ncols, *r_dev) : j0 + ncols;
-  // segments covering the tile's units, per chunk, ascending (found on the fly per chunk)
-  auto seg_range = [&](int ch, long long& lo, long long& hi) {
-    const long long vt = (long long)t * nchunks + ch;
-    const long long x0 = vt * kbc, x1 = x0 + kbc - 1;
-    lo = x0 * G / total_units;
-    hi = x1 * G / total_units;
-    while (lo + 1 < G && oz_seg_begin(lo + 1, total_units, G) <= x0) ++lo;
-    while (lo > 0 && oz_seg_begin(lo, total_units, G) > x0) --lo;
-    while (hi + 1 < G && oz_seg_begin(hi + 1, total_units, G) <= x1) ++hi;
-    while (hi > 0 && oz_seg_begin(hi, total_units, G) > x1) --hi;
-  };
+  // the partial tiles of this row tile (per chunk, the CTA segments covering it, in
+  // ascending order): thread 0 resolves them once per block (64-bit divisions), every thread
+  // reads the table -- the summation order is unchanged
+  constexpr int MAXE = 512;
+  __shared__ long long s_base[MAXE];
+  __shared__ int s_ne;
+  if (threadIdx.x == 0) {
+    int ne = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const long long vt = (long long)t * nchunks + ch;
+      const long long x0 = vt * kbc, x1 = x0 + kbc - 1;
+      long long lo = x0 * G / total_units, hi = x1 * G / total_units;
+      while (lo + 1 < G && oz_seg_begin(lo + 1, total_units, G) <= x0) ++lo;
+      while (lo > 0 && oz_seg_begin(lo, total_units, G) > x0) --lo;
+      while (hi + 1 < G && oz_seg_begin(hi + 1, total_units, G) <= x1) ++hi;
+      while (hi > 0 && oz_seg_begin(hi, total_units, G) > x1) --hi;
+      for (long long c = lo; c <= hi; ++c) {
+        const int slot = (int)(vt - oz_seg_begin(c, total_units, G) / kbc);
+        if (ne < MAXE) s_base[ne] = ((long long)c * max_slots + slot) * (long long)(OZ_TM * BN);
+        ++ne;
+      }
+    }
+    s_ne = ne;
+  }
+  __syncthreads();
+  const int ne = s_ne;
   for (int jb = 16 * blockIdx.y; jb < ncols; jb += 16 * gridDim.y) {   // 16 columns per y-block
     double s[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) s[q] = 0.0;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const long long vt = (long long)t * nchunks + ch;
-      long long c_lo, c_hi;
-      seg_range(ch, c_lo, c_hi);
-      for (long long c = c_lo; c <= c_hi; ++c) {
-        const int slot = (int)(vt - oz_seg_begin(c, total_units, G) / kbc);
-        const double* src = ws + ((size_t)c * max_slots + slot) * (size_t)(OZ_TM * BN) + row;
+    if (ne <= MAXE) {
+      for (int e = 0; e < ne; ++e) {
+        const double* src = ws + s_base[e] + row;
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           if (jb + q < ncols) s[q] += src[(size_t)(jb + q) * OZ_TM];
+      }
+    } else {                                  // more segments than the table: resolve per thread
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const long long vt = (long long)t * nchunks + ch;
+        const long long x0 = vt * kbc, x1 = x0 + kbc - 1;
+        long long lo = x0 * G / total_units, hi = x1 * G / total_units;
+        while (lo + 1 < G && oz_seg_begin(lo + 1, total_units, G) <= x0) ++lo;
+        while (lo > 0 && oz_seg_begin(lo, total_units, G) > x0) --lo;
+        while (hi + 1 < G && oz_seg_begin(hi + 1, total_units, G) <= x1) ++hi;
+        while (hi > 0 && oz_seg_begin(hi, total_units, G) > x1) --hi;
+        for (long long c = lo; c <= hi; ++c) {
+          const int slot = (int)(vt - oz_seg_begin(c, total_units, G) / kbc);
+          const double* src = ws + ((size_t)c * max_slots + slot) * (size_t)(OZ_TM * BN) + row;
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (jb + q < ncols) s[q] += src[(size_t)(jb + q) * OZ_TM];
+        }
       }
     }
 #pragma unroll
