@@ -482,17 +482,22 @@ static int launch_resid64(const void* A, int64_t lda, int64_t m, int64_t K, cons
 }
 
 // res[j] = sqrt(sum_b part[b, j]) / |vals[j]|  (inf for vals[j] == 0), fixed order.
+// one warp per column: lane l sums blocks l, l + 32, ... (ascending), then a fixed
+// butterfly -- a fixed summation order (deterministic) with the latency of nblocks / 32 adds
 __global__ void k_residual_reduce(const double* __restrict__ part, int nblocks, int n,
                                   const double* __restrict__ vals, const int* __restrict__ r_dev,
                                   double* __restrict__ res, int accumulate_max) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (j >= n) return;
   // accumulate_max: 0 -> res = ||r|| / |lambda|; 1 -> res = max(res, ||r|| / |lambda|);
   //                 2 -> res = raw sum of squares (row-partitioned runs all-reduce it first)
   const int nvalid = r_dev ? min(n, *r_dev) : n;
-  if (j >= nvalid) { if (accumulate_max != 1) res[j] = 0.0; return; }
+  if (j >= nvalid) { if (accumulate_max != 1 && lane == 0) res[j] = 0.0; return; }
   double s = 0.0;
-  for (int b = 0; b < nblocks; ++b) s += part[(int64_t)b * n + j];
+  for (int b = lane; b < nblocks; b += 32) s += part[(int64_t)b * n + j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
   if (accumulate_max == 2) { res[j] = s; return; }
   const double lam = vals[j];
   const double r = lam == 0.0 ? INFINITY : sqrt(s) / fabs(lam);
@@ -527,7 +532,7 @@ int simt_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_f
 
 int residual_reduce(const double* part, int nblocks, int n, const double* vals, const int* r_dev, double* res,
                     int mode, cudaStream_t st) {
-  k_residual_reduce<<<(n + 127) / 128, 128, 0, st>>>(part, nblocks, n, vals, r_dev, res, mode);
+  k_residual_reduce<<<(n + 3) / 4, 128, 0, st>>>(part, nblocks, n, vals, r_dev, res, mode);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
@@ -571,7 +576,7 @@ int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
     const int rc = oz_product(A, rows, cols, lda, a_fmt, Xv, ldx, r_max, vals, r_dev, Yv, ldy, nullptr, 0, &part,
                               ws, ws_bytes, st);
     if (rc) return rc;
-    k_residual_reduce<<<(r_max + 127) / 128, 128, 0, st>>>(part, oz_nblocks(m), r_max, vals, r_dev, res,
+    k_residual_reduce<<<(r_max + 3) / 4, 128, 0, st>>>(part, oz_nblocks(m), r_max, vals, r_dev, res,
                                                            accumulate_max);
     OFRR_CHECK_LAUNCH();
     return OFRR_OK;
@@ -600,7 +605,7 @@ int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
     }
     if (rc) return rc;
     const int nb = (int)((m + RBM - 1) / RBM);
-    k_residual_reduce<<<(r_max + 127) / 128, 128, 0, st>>>(part, nb, r_max, vals, r_dev, res, accumulate_max);
+    k_residual_reduce<<<(r_max + 3) / 4, 128, 0, st>>>(part, nb, r_max, vals, r_dev, res, accumulate_max);
     OFRR_CHECK_LAUNCH();
     return OFRR_OK;
   }
@@ -613,7 +618,7 @@ int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
   }
   if (rc) return rc;
   const int nb = (int)((m + SBM - 1) / SBM);
-  k_residual_reduce<<<(r_max + 127) / 128, 128, 0, st>>>(part, nb, r_max, vals, r_dev, res, accumulate_max);
+  k_residual_reduce<<<(r_max + 3) / 4, 128, 0, st>>>(part, nb, r_max, vals, r_dev, res, accumulate_max);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
