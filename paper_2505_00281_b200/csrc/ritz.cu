@@ -113,80 +113,117 @@ int ritz_recover(const void* U, int64_t ldu, int u_fmt, int64_t n, int kp, const
 // the Ritz residual up to the accumulation error of W, without another pass over A.
 // Partial sums of squares per 64-row block -> part[block * r_max + j] (fixed order).
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-    k_resid_est(const void* __restrict__ U, int64_t ldu, int u_fmt, const void* __restrict__ W, int64_t ldw,
-                int w_fmt, int64_t n, int kp, const double* __restrict__ Y, int ldy, const int* __restrict__ r_dev,
+// On the fp64 tensor cores (DMMA m8n8k4): 32 rows x 32 Ritz columns per 128-thread CTA,
+// each warp a 16 x 16 block of both products (U y and W y, 2 x 2 MMA tiles each), kp in
+// slabs of 32 staged in shared memory as fp64 (storage values are exact).  At C2
+// (n = 16384, r = 32) that is 512 CTAs, all resident at once; no work past column r.
+// The per-column sums of squares reduce over the 8 row lanes of each MMA tile by a fixed
+// butterfly, then over the CTA's 4 row groups in fixed order.
+constexpr int RE_BM = 32, RE_BN = 32, RE_KC = 32, RE_RS = RE_KC + 4;
+
+template <typename TU, typename TW>
+__global__ void __launch_bounds__(128)
+    k_resid_est(const TU* __restrict__ U, int64_t ldu, const TW* __restrict__ W, int64_t ldw, int64_t n,
+                int kp, const double* __restrict__ Y, int ldy, const int* __restrict__ r_dev,
                 int r_max, const double* __restrict__ vals, double* __restrict__ part) {
-  __shared__ double Us[16][65];
-  __shared__ double Ws[16][65];
-  __shared__ double Ys[16][65];
-  __shared__ double csum[16][64];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t m0 = (int64_t)blockIdx.x * 64;
-  const int n0 = blockIdx.y * 64;
+  __shared__ double Us[RE_BM][RE_RS];        // [row][l]
+  __shared__ double Ws[RE_BM][RE_RS];
+  __shared__ double Ys[RE_KC][RE_BN + 4];    // [l][col]
+  __shared__ double csum[2][RE_BN];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
+  const int64_t m0 = (int64_t)blockIdx.x * RE_BM;
+  const int n0 = blockIdx.y * RE_BN;
   const int r = r_dev ? min(r_max, *r_dev) : r_max;
-  double au[4][4] = {}, aw[4][4] = {};
-  for (int l0 = 0; l0 < kp; l0 += 16) {
-    for (int e = tid; e < 16 * 64; e += 256) {
-      const int rr = e & 63, ll = e >> 6;
-      const int64_t gi = m0 + rr;
-      const bool ok = gi < n && l0 + ll < kp;
-      Us[ll][rr] = ok ? ld_fmt(U, (int64_t)(l0 + ll) * ldu + gi, u_fmt) : 0.0;
-      Ws[ll][rr] = ok ? ld_fmt(W, (int64_t)(l0 + ll) * ldw + gi, w_fmt) : 0.0;
-      const int gj = n0 + rr;
-      Ys[ll][rr] = (gj < r && l0 + ll < kp) ? Y[(int64_t)gj * ldy + l0 + ll] : 0.0;
+  double au[2][2][2] = {}, aw[2][2][2] = {};
+  if (n0 < r) {
+    for (int l0 = 0; l0 < kp; l0 += RE_KC) {
+#pragma unroll
+      for (int q = 0; q < RE_KC * RE_BM / 128; ++q) {
+        const int e = tid + 128 * q, rr = e & 31, ll = e >> 5;
+        const int64_t gi = m0 + rr;
+        const bool ok = gi < n && l0 + ll < kp;
+        Us[rr][ll] = ok ? to_d(U[(int64_t)(l0 + ll) * ldu + gi]) : 0.0;
+        Ws[rr][ll] = ok ? to_d(W[(int64_t)(l0 + ll) * ldw + gi]) : 0.0;
+        // Y is k x r column-major (ldy): the fast index runs down a column
+        const int gj = n0 + ll;
+        Ys[rr][ll] = (gj < r && l0 + rr < kp) ? Y[(int64_t)gj * ldy + l0 + rr] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < RE_KC; kk += 4) {
+        double a[2], w[2], b[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) { a[i] = Us[wm + 8 * i + g][kk + t]; w[i] = Ws[wm + 8 * i + g][kk + t]; }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) b[j] = Ys[kk + t][wn + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) { dmma884r(au[i][j], a[i], b[j]); dmma884r(aw[i][j], w[i], b[j]); }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-#pragma unroll
-    for (int ll = 0; ll < 16; ++ll) {
-      double a[4], w[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { a[i] = Us[ll][ty + 16 * i]; w[i] = Ws[ll][ty + 16 * i]; }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Ys[ll][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { au[i][j] = fma(a[i], b[j], au[i][j]); aw[i][j] = fma(w[i], b[j], aw[i][j]); }
-    }
-    __syncthreads();
   }
+  // thread holds rows wm + 8i + g, columns wn + 8j + 2t + h
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int gj = n0 + tx + 16 * j;
-    double s = 0.0;
-    if (gj < r) {
-      const double lam = vals[gj];
+  for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (m0 + ty + 16 * i < n) {
-          const double d = aw[i][j] - lam * au[i][j];
-          s += d * d;
-        }
+    for (int h = 0; h < 2; ++h) {
+      const int gj = n0 + wn + 8 * j + 2 * t + h;
+      double s = 0.0;
+      if (gj < r) {
+        const double lam = vals[gj];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          if (m0 + wm + 8 * i + g < n) {
+            const double d = aw[i][j][h] - lam * au[i][j][h];
+            s += d * d;
+          }
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      s += __shfl_xor_sync(0xffffffffu, s, 8);
+      s += __shfl_xor_sync(0xffffffffu, s, 16);
+      if (g == 0) csum[warp >> 1][wn + 8 * j + 2 * t + h] = s;
     }
-    csum[ty][tx + 16 * j] = s;
-  }
   __syncthreads();
-  if (tid < 64 && n0 + tid < r_max) {
-    double s = 0.0;
-    for (int y = 0; y < 16; ++y) s += csum[y][tid];
-    part[(int64_t)blockIdx.x * r_max + n0 + tid] = s;
-  }
+  if (tid < RE_BN && n0 + tid < r_max) part[(int64_t)blockIdx.x * r_max + n0 + tid] = csum[0][tid] + csum[1][tid];
 }
 
 int residual_reduce(const double* part, int nblocks, int n, const double* vals, const int* r_dev, double* res,
                     int mode, cudaStream_t st);
 
-size_t resid_est_ws(int64_t n, int r) { return (size_t)((n + 63) / 64) * (size_t)r * sizeof(double); }
+size_t resid_est_ws(int64_t n, int r) { return (size_t)((n + RE_BM - 1) / RE_BM) * (size_t)r * sizeof(double); }
 
 int resid_est(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt, int64_t n, int kp,
               const double* Y, int ldy, const double* vals, const int* r_dev, int r_max, double* res, int mode,
               void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n <= 0 || r_max <= 0) return OFRR_OK;
   if (ws_bytes < resid_est_ws(n, r_max)) { ofrr_set_error("residual estimate: workspace too small"); return OFRR_ERR_INVALID; }
-  const int nb = (int)((n + 63) / 64);
-  dim3 grid((unsigned)nb, (unsigned)((r_max + 63) / 64));
-  k_resid_est<<<grid, 256, 0, st>>>(U, ldu, u_fmt, W, ldw, w_fmt, n, kp, Y, ldy, r_dev, r_max, vals, (double*)ws);
+  const int nb = (int)((n + RE_BM - 1) / RE_BM);
+  dim3 grid((unsigned)nb, (unsigned)((r_max + RE_BN - 1) / RE_BN));
+  double* part = (double*)ws;
+  auto go = [&](auto tu, auto tw) {
+    using TU = decltype(tu);
+    using TW = decltype(tw);
+    k_resid_est<TU, TW><<<grid, 128, 0, st>>>((const TU*)U, ldu, (const TW*)W, ldw, n, kp, Y, ldy, r_dev, r_max,
+                                              vals, part);
+  };
+  auto with_u = [&](auto tw) {
+    switch (u_fmt) {
+      case F64: go(double(), tw); break;
+      case F32: go(float(), tw); break;
+      case F16: go(__half(), tw); break;
+      case BF16: go(__nv_bfloat16(), tw); break;
+      default: go(__nv_fp8_e4m3(), tw); break;
+    }
+  };
+  switch (w_fmt) {
+    case F64: with_u(double()); break;
+    case F32: with_u(float()); break;
+    default: ofrr_set_error("residual estimate: W format %d (want F32 or F64)", w_fmt); return OFRR_ERR_UNSUPPORTED;
+  }
   OFRR_CHECK_LAUNCH();
   return residual_reduce((double*)ws, nb, r_max, vals, r_dev, res, mode, st);
 }

@@ -278,6 +278,32 @@ def test_ritz_and_residual(ofrr_gpu, oracle):
     np.testing.assert_allclose(res, ref, rtol=1e-10)
 
 
+@pytest.mark.parametrize("n,k,r_max,rv,ufmt,wfmt", [(3001, 40, 30, 30, BF16, F32), (16384, 64, 32, 32, F32, F32),
+                                                    (1000, 70, 65, 41, F32, F64), (33, 5, 3, 2, F16, F32)])
+@pytest.mark.parametrize("mode", [0, 2])
+def test_residual_estimate_vs_numpy(ofrr_gpu, oracle, n, k, r_max, rv, ufmt, wfmt, mode):
+    """K7e: ||(W - lambda_j U) y_j|| / |lambda_j| (mode 0) / raw sums of squares (mode 2)
+    over the first r = min(r_max, *r_dev) Ritz columns, zeros past r."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(n + k)
+    u = o.round_to(rng.standard_normal((n, k)), ufmt)
+    w = rng.standard_normal((n, k))
+    w = w if wfmt == F64 else o.round_to(w, wfmt)
+    y = rng.standard_normal((k, k))
+    lam = rng.uniform(0.5, 2.0, k) * rng.choice([-1, 1], k)
+    U, W = _blk(p, u, ufmt), _blk(p, w, wfmt)
+    Y = torch.tensor(np.ascontiguousarray(y.T), device="cuda")
+    r_dev = torch.tensor([rv], dtype=torch.int32, device="cuda")
+    got = ops.residual_estimate(U, W, Y, k, torch.tensor(lam, device="cuda"), r_dev, r_max, mode=mode).cpu().numpy()
+    d = w @ y[:, :rv] - (u @ y[:, :rv]) * lam[None, :rv]
+    ss = np.sum(d * d, axis=0)
+    ref = ss if mode == 2 else np.sqrt(ss) / np.abs(lam[:rv])
+    np.testing.assert_allclose(got[:rv], ref, rtol=1e-11)
+    assert not got[rv:].any()
+
+
 @pytest.mark.parametrize("fmt,rows,cols,r,rv", [(BF16, 300, 20000, 64, 64), (BF16, 1000, 1000, 100, 90),
                                                 (F16, 257, 3001, 7, 7), (FP8, 640, 5000, 33, 20),
                                                 (BF16, 129, 16384, 32, 32)])
