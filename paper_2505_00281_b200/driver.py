@@ -239,9 +239,11 @@ class EigEngine:
         return self._ozaki(A) if X.fmt == FpFormat.F64 else None
 
     # ---- blocks ---------------------------------------------------------------------
-    def start_block(self):
+    def start_block(self, out=None):
         """X0 = PCG64(seed) U(0,1), rounded to the MatVec storage (ofrr/driver.py:97-99)."""
-        return self.ops.start_block(self.cfg.seed, self.n, self.cfg.k, self.mv.storage, self.device)
+        if out is None:
+            return self.ops.start_block(self.cfg.seed, self.n, self.cfg.k, self.mv.storage, self.device)
+        return self.ops.start_block(self.cfg.seed, self.n, self.cfg.k, self.mv.storage, self.device, out=out)
 
     def power(self, X, st, steps: Optional[int] = None):
         """cfg.iter MatVecs with inf-norm column scaling (ofrr/driver.py:102-105)."""
@@ -393,8 +395,9 @@ class EigEngine:
         cfg = self.cfg
         tol, top = cfg.tol, (cfg.top or cfg.k)
         check = tol is not None
-        if X0 is None:
-            X = self.start_block()
+        fresh = X0 is None
+        if fresh:
+            X = None                                  # made below (into the loop graph's input when it runs)
         elif X0.fmt != self.mv.storage:
             X = self.ops.new_block(X0.n, X0.k, self.mv.storage, self.device)
             self.ops.convert(X0, X)                               # exact widening (f32 -> f64)
@@ -405,13 +408,16 @@ class EigEngine:
         rs = vals = None
         use_graph = self._graph_capable()
         prev_est = None
-        self._block_oz(self.A_mv, X)                 # FP64 blocks: slice A once per run, eagerly
+        if (X.fmt if X is not None else self.mv.storage) == FpFormat.F64:
+            self._ozaki(self.A_mv)                   # FP64 blocks: slice A once per run, eagerly
         if self.mv.storage != self.pol.storage:
             self._ozaki(self.A_pol) if self.pol.storage == FpFormat.F64 else None
-        if use_graph and check and stop_estimate is None and X.k == cfg.k and cfg.m >= 2:
+        if use_graph and check and stop_estimate is None and (fresh or X.k == cfg.k) and cfg.m >= 2:
             rs = self._device_loop(X, top)
             if rs is not None:
                 return rs
+        if X is None:
+            X = self.start_block()
         for it in range(cfg.m):
             last = it == cfg.m - 1
             self._refresh_now = it == 0      # A's report scales: once per run (A may change between runs)
@@ -528,7 +534,11 @@ class EigEngine:
             return None
         ex, ctl = lp
         t1 = time.perf_counter()
-        if X.t.data_ptr() != gf.Xs.t.data_ptr():
+        if X is None and (gf.Xs.n, gf.Xs.k, FpFormat(gf.Xs.fmt)) == (self.n, cfg.k, FpFormat(self.mv.storage)):
+            self.start_block(out=gf.Xs)                # straight into the loop graph's input
+        elif X is None:
+            gf.Xs.t.copy_(self.start_block().t)
+        elif X.t.data_ptr() != gf.Xs.t.data_ptr():
             gf.Xs.t.copy_(X.t)
         t2 = time.perf_counter()
         _lib.check(L.ofrr_loop_launch(ex.handle, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
@@ -544,6 +554,8 @@ class EigEngine:
         stage[:nb].copy_(ctl, non_blocking=True)
         stage[nb:nb + 8 * k].view(torch.float64).copy_(gs.outs["pack"][8:8 + k], non_blocking=True)
         stage[nb + 8 * k:].view(torch.float64).copy_(gs.report.res[:k], non_blocking=True)
+        rg = gs.report
+        U64t = rg.U64.t.clone()                        # the returned vectors outlive the next replay
         torch.cuda.current_stream(self.device).synchronize()
         host = stage
         t4 = time.perf_counter()
@@ -557,7 +569,6 @@ class EigEngine:
         est_h, fp64_h = hist[:nh], hist[nh:]
         vals = host[nb:nb + 8 * k].view(torch.float64).numpy().copy()
         res = host[nb + 8 * k:].view(torch.float64).numpy().copy()
-        rg = gs.report
         self.stats.iterations = its
         self.stats.a_passes += gf.a_passes + (its - 1) * gs.a_passes
         for i in range(min(its, nh)):
@@ -572,7 +583,7 @@ class EigEngine:
         for _ in range(nrep):
             rg.rec.replayed()
         self.ops._count(1 + its + nrep)                      # init, decide per iteration, confirm per report
-        U64c = self.ops.DevBlock(rg.U64.t.clone(), rg.U64.n, k, rg.U64.fmt)
+        U64c = self.ops.DevBlock(U64t, rg.U64.n, k, rg.U64.fmt)
         out = RitzSet(np.array(vals), DenseMatrix.from_block(U64c), "eig", residuals=res)
         t5 = time.perf_counter()
         _loop_debug(f"host us: keys {1e6 * (t1 - t0):.0f} copy {1e6 * (t2 - t1):.0f} launch {1e6 * (t3 - t2):.0f} "

@@ -192,13 +192,19 @@ def _pcg64_state(seed: int):
     return st
 
 
-def start_block(seed: int, n: int, k: int, fmt: FpFormat, device) -> DevBlock:
+def start_block(seed: int, n: int, k: int, fmt: FpFormat, device, out: Optional[DevBlock] = None) -> DevBlock:
     """X0 = numpy default_rng(seed).random((n, k)) rounded to fmt, generated on the device
     bit for bit (ofrr/driver.py:97-99): numpy derives the PCG64 state from the seed, the
-    device walks the stream."""
+    device walks the stream.  ``out``: an n x k block of format fmt to write (its padding is
+    left as it is)."""
     s, inc = _pcg64_state(seed)
     m64 = (1 << 64) - 1
-    X = new_block(n, k, fmt, device, zero=True)
+    if out is not None:
+        if (out.n, out.k, FpFormat(out.fmt)) != (n, k, FpFormat(fmt)):
+            raise ValueError("start_block: output block shape/format mismatch")
+        X = out
+    else:
+        X = new_block(n, k, fmt, device, zero=True)
     L = _lib.load()
     _lib.check(L.ofrr_start_block_pcg64(s >> 64, s & m64, inc >> 64, inc & m64, n, k, X.ptr, X.ld, int(fmt),
                                         _stream()), "start_block")
