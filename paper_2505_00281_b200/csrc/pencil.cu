@@ -545,9 +545,10 @@ __global__ void __launch_bounds__(NT, 1)
 // K5a for k <= 64: the same Cholesky + inverse + certificate with sym(M) in registers
 // (group-per-column layout of k_pc_tri_reg).  Step j: the group of column j forms
 // l = column j / sqrt(m_jj) from its registers and publishes it (shared memory, double
-// buffered); barrier; every later column takes the rank-1 update in registers.  Then L goes
-// to shared memory and each group solves L x = e_c for its own column (x_l broadcast by
-// shuffle from the lane holding row l, the update of the rows below in registers).
+// buffered); barrier; every later column takes the rank-1 update in registers, and every
+// column c <= j takes step j of its forward substitution L x = e_c with the same published
+// column (x_j broadcast by shuffle from the lane holding row j) -- so X = L^-1 is done when
+// L is, in the operation order of the column-by-column solve.
 // ---------------------------------------------------------------------------------
 template <int TPC, int RPT>
 __global__ void __launch_bounds__(PT, 1)
@@ -605,6 +606,12 @@ __global__ void __launch_bounds__(PT, 1)
       if (bad) s_fail = 1;
     }
   };
+  // X = L^-1 alongside: column c of X in registers (x = e_c); step j applies row j of the
+  // column solve (x_j *= 1/L_jj, x_i -= L_ij x_j below) with the published column j -- the
+  // operation order of a column-by-column forward substitution, without its k serial steps
+  double x[RPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) x[t] = (r0 + t == c) ? 1.0 : 0.0;
   if (c == 0) publish(0, 0);
   __syncthreads();
   for (int j = 0; j + 1 < k; ++j) {
@@ -621,6 +628,17 @@ __global__ void __launch_bounds__(PT, 1)
       }
     }
     if (c == j + 1) publish(j + 1, buf ^ 1);
+    if (colok && c <= j) {                                       // x_j = 0 for columns past j
+      const double dj = dinv[j];
+      double xj = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+        if (r0 + t == j) { x[t] *= dj; xj = x[t]; }
+      xj = __shfl_sync(gmask, xj, gl0 + j / RPT);
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+        if (r0 + t > j) x[t] = fma(-lb[t], xj, x[t]);
+    }
     __syncthreads();
   }
   if (s_fail) {
@@ -628,40 +646,15 @@ __global__ void __launch_bounds__(PT, 1)
     return;
   }
   pc_mark(1);
-  // L -> shared memory (column c, rows >= c; zeros above)
-  if (colok) {
-#pragma unroll
-    for (int t = 0; t < RPT; ++t) {
-      const int i = r0 + t;
-      if (i < k) sm[(size_t)c * k + i] = i >= c ? a[t] : 0.0;
-    }
-  }
-  __syncthreads();
-  // X = L^-1, column c by the group of column c: x = e_c; for l = c..k-1: x_l *= 1/L_ll,
-  // then x_i -= L_il x_l for the rows below (right-looking, registers)
   double xs = 0.0;
   if (colok) {
 #pragma unroll
-    for (int t = 0; t < RPT; ++t) a[t] = (r0 + t == c) ? 1.0 : 0.0;
-    for (int l = c; l < k; ++l) {
-      const int ol = l / RPT;                                    // lane holding row l
-      double xl = 0.0;
-#pragma unroll
-      for (int t = 0; t < RPT; ++t)
-        if (r0 + t == l) { a[t] *= dinv[l]; xl = a[t]; }
-      xl = __shfl_sync(gmask, xl, gl0 + ol);
-      const double* Ll = sm + (size_t)l * k;
-#pragma unroll
-      for (int t = 0; t < RPT; ++t) {
-        const int i = r0 + t;
-        if (i > l && i < k) a[t] = fma(-Ll[i], xl, a[t]);
-      }
-    }
-#pragma unroll
     for (int t = 0; t < RPT; ++t) {
       const int i = r0 + t;
+      if (i == k - 1) x[t] *= dinv[k - 1];
+      a[t] = x[t];
       if (i < k) {
-        const double v = i >= c ? a[t] : 0.0;
+        const double v = i >= c ? x[t] : 0.0;
         Xg[(size_t)c * k + i] = v;
         xs = fma(v, v, xs);
       }
