@@ -567,6 +567,7 @@ class EigEngine:
         hist = host[24:nb].view(torch.float64).numpy()
         nh = (hist.size) // 2
         est_h, fp64_h = hist[:nh], hist[nh:]
+        _loop_debug("est", est_h[:its].tolist(), "fp64", fp64_h[:its].tolist())
         vals = host[nb:nb + 8 * k].view(torch.float64).numpy().copy()
         res = host[nb + 8 * k:].view(torch.float64).numpy().copy()
         self.stats.iterations = its
