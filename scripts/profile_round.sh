@@ -13,4 +13,5 @@ ncu --set full --clock-control none --import-source on -k regex:k_hessenberg -s 
 ncu --set full --clock-control none --import-source on -k regex:k_pc_tri_reg -s 2 -c 1 -o gpurun_out/pc_tri_k64 python scripts/pc_phases.py 64 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pc_eigvec -s 2 -c 1 -o gpurun_out/pc_eigvec_k64 python scripts/pc_phases.py 64 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pc_chol -s 2 -c 1 -o gpurun_out/pc_chol_k64 python scripts/pc_phases.py 64 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_resid_est -c 1 -o gpurun_out/resid_est_c2 python bench.py --config c2 --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
 ls -la gpurun_out

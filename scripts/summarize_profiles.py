@@ -114,3 +114,4 @@ if __name__ == "__main__":
     summarize_rep("pc_tri_k64", "K5c register-resident Householder tridiagonalisation, k=64")
     summarize_rep("pc_eigvec_k64", "K5d eigenpairs of the tridiagonal + back-transformation (multi-CTA), k=64")
     summarize_rep("pc_chol_k64", "K5a Cholesky + inverse of the Gram M, k=64")
+    summarize_rep("resid_est_c2", "K7e residual estimate (DMMA), C2: n=16384, kp=64, r=32")
