@@ -13,6 +13,7 @@ synchronising.  Nothing here computes on the host.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 from typing import Optional
 
@@ -190,6 +191,19 @@ def _pcg64_state(seed: int):
         if len(_PCG_STATE) < 64:
             _PCG_STATE[seed] = st
     return st
+
+
+def _zeros_pack(dev, *specs):
+    """Zeroed tensors of the given (shape, dtype) as views of ONE allocation (one fill kernel
+    instead of one per tensor -- inside a captured iteration each fill is a graph node)."""
+    sizes, off, total = [], [], 0
+    for shape, dt in specs:
+        nb = math.prod(shape) * torch.empty((), dtype=dt).element_size()
+        off.append(total)
+        sizes.append(nb)
+        total += (nb + 255) // 256 * 256
+    buf = torch.zeros(max(total, 256), dtype=torch.uint8, device=dev)
+    return [buf[o:o + nb].view(dt).view(shape) for o, nb, (shape, dt) in zip(off, sizes, specs)]
 
 
 def start_block(seed: int, n: int, k: int, fmt: FpFormat, device, out: Optional[DevBlock] = None) -> DevBlock:
@@ -372,9 +386,8 @@ def hessenberg(X: DevBlock, storage: FpFormat, compute: FpFormat, tol: float) ->
         convert(X, Xs)
         X = Xs
     Q = new_block(X.n, X.k, storage, dev)
-    piv = torch.zeros(max(X.k, 1), dtype=torch.int64, device=dev)
-    kept = torch.zeros(max(X.k, 1), dtype=torch.int32, device=dev)
-    nk = torch.zeros(1, dtype=torch.int32, device=dev)
+    piv, kept, nk = _zeros_pack(dev, ((max(X.k, 1),), torch.int64), ((max(X.k, 1),), torch.int32),
+                                ((1,), torch.int32))
     ws_b = L.ofrr_hessenberg_workspace(X.n, X.k, int(storage))
     ws = _ws(ws_b, dev)
     _lib.check(L.ofrr_hessenberg(X.ptr, X.n, X.k, X.ld, int(storage), int(compute), float(tol), Q.ptr, Q.ld,
@@ -422,10 +435,9 @@ def sym_def_gen_eig(B: torch.Tensor, M: torch.Tensor, k: int) -> EigOut:
     """B, M: fp64 column-major k x k (torch (k, k) with row j = column j)."""
     L = _lib.load()
     dev = B.device
-    vals = torch.zeros(max(k, 1), dtype=torch.float64, device=dev)
-    vecs = torch.zeros((max(k, 1), max(k, 1)), dtype=torch.float64, device=dev)
-    n_out = torch.zeros(1, dtype=torch.int32, device=dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    kk = max(k, 1)
+    vals, vecs, n_out, status = _zeros_pack(dev, ((kk,), torch.float64), ((kk, kk), torch.float64),
+                                            ((1,), torch.int32), ((1,), torch.int32))
     ws = _ws(L.ofrr_small_eig_workspace(k), dev)
     _lib.check(L.ofrr_sym_def_gen_eig(B.data_ptr(), M.data_ptr(), k, vals.data_ptr(), vecs.data_ptr(),
                                       n_out.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),
