@@ -813,15 +813,19 @@ __global__ void __launch_bounds__(EPT)
   }
   __syncthreads();
   pc_mark(7);
-  // ---- eigenvectors of the tridiagonal: twisted factorisation, two lanes per eigenvalue ----
-  if (threadIdx.x < 2 * epb) {
-    const int e = threadIdx.x >> 1, side = threadIdx.x & 1, m = m0 + e;
-    const bool act = m < k;
-    const double lm = act ? lam[e] : 0.0;
-    double* z = zb + (size_t)e * k;
-    double* dmn = dm + (size_t)e * k;
-    if (act) {
-      if (side == 0) {
+  // ---- eigenvectors of the tridiagonal: twisted factorisation, one warp per eigenvalue ----
+  // lanes 0 / 1 run the D+ / D- recurrences (serial); the twist index (first minimum of
+  // |gamma_i|, ties to the lowest i) is a warp argmin; the vector's entries, products of the
+  // ratios from the twist outwards, are a warp suffix / prefix product scan over chunks of
+  // TCH rows per lane, and the norm a warp sum.
+  {
+    constexpr int TCH = (PK_MAX + 31) / 32;
+    const int e = warp, m = m0 + e;
+    if (e < epb && m < k) {
+      const double lm = lam[e];
+      double* z = zb + (size_t)e * k;
+      double* dmn = dm + (size_t)e * k;
+      if (lane == 0) {
         double q = dd[0] - lm;
         if (fabs(q) < pivmin) q = -pivmin;
         z[0] = q;
@@ -830,7 +834,7 @@ __global__ void __launch_bounds__(EPT)
           if (fabs(q) < pivmin) q = -pivmin;
           z[i] = q;
         }
-      } else {
+      } else if (lane == 1) {
         double q = dd[k - 1] - lm;
         if (fabs(q) < pivmin) q = -pivmin;
         dmn[k - 1] = q;
@@ -840,48 +844,66 @@ __global__ void __launch_bounds__(EPT)
           dmn[i] = q;
         }
       }
-    }
-    const unsigned pm = (1u << (2 * epb)) - 1u;
-    __syncwarp(pm);
-    int r = 0;
-    if (act && side == 0) {
+      __syncwarp();
       double best = 1e300;
-      for (int i = 0; i < k; ++i) {
+      int r = 0;
+      for (int i = lane; i < k; i += 32) {
         const double g = fabs(z[i] + dmn[i] - (dd[i] - lm));
         if (g < best) { best = g; r = i; }
       }
-    }
-    r = __shfl_sync(pm, r, threadIdx.x & ~1);
-    __syncwarp(pm);
-    double nrm = 0.0;
-    if (act) {
-      double xv = 1.0;
-      if (side == 0) {
-        for (int i = r - 1; i >= 0; --i) {
-          xv = -pc_fast_div(ee[i], z[i]) * xv;
-          z[i] = xv;
-          nrm = fma(xv, xv, nrm);
-        }
-        z[r] = 1.0;
-        nrm += 1.0;
-      } else {
-        for (int i = r + 1; i < k; ++i) {
-          xv = -pc_fast_div(ee[i - 1], dmn[i]) * xv;
-          z[i] = xv;
-          nrm = fma(xv, xv, nrm);
-        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, r, o);
+        if (ob < best || (ob == best && orr < r)) { best = ob; r = orr; }
       }
-    }
-    nrm += __shfl_xor_sync(pm, nrm, 1);
-    __syncwarp(pm);
-    if (act) {
+      const int i0 = lane * TCH;
+      double lf[TCH], rf[TCH];
+      double pl = 1.0, pr = 1.0;
+#pragma unroll
+      for (int t = TCH - 1; t >= 0; --t) {                       // left: suffix products below r
+        const int i = i0 + t;
+        const double f = (i < r && i < k) ? -pc_fast_div(ee[i], z[i]) : 1.0;
+        pl *= f;
+        lf[t] = pl;
+      }
+#pragma unroll
+      for (int t = 0; t < TCH; ++t) {                            // right: prefix products above r
+        const int i = i0 + t;
+        const double f = (i > r && i < k) ? -pc_fast_div(ee[i - 1], dmn[i]) : 1.0;
+        pr *= f;
+        rf[t] = pr;
+      }
+      double sl = pl, sr = pr;                                   // inclusive scans over lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double vl = __shfl_down_sync(0xffffffffu, sl, o);
+        const double vr = __shfl_up_sync(0xffffffffu, sr, o);
+        if (lane + o < 32) sl *= vl;
+        if (lane >= o) sr *= vr;
+      }
+      double xl = __shfl_down_sync(0xffffffffu, sl, 1), xr = __shfl_up_sync(0xffffffffu, sr, 1);
+      if (lane == 31) xl = 1.0;
+      if (lane == 0) xr = 1.0;
+      double xv[TCH];
+      double nrm = 0.0;
+#pragma unroll
+      for (int t = 0; t < TCH; ++t) {
+        const int i = i0 + t;
+        xv[t] = i < r ? lf[t] * xl : (i == r ? 1.0 : rf[t] * xr);
+        if (i < k) nrm = fma(xv[t], xv[t], nrm);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
       nrm = sqrt(nrm);
+      __syncwarp();                                              // z / dmn reads done
       if (!(nrm > 0.0) || !isfinite(nrm)) {
-        *gate = 1;
+        if (lane == 0) *gate = 1;
       } else {
         const double inv = 1.0 / nrm;
-        if (side == 0) { for (int i = 0; i <= r; ++i) z[i] *= inv; }
-        else { for (int i = r + 1; i < k; ++i) z[i] *= inv; }
+#pragma unroll
+        for (int t = 0; t < TCH; ++t)
+          if (i0 + t < k) z[i0 + t] = xv[t] * inv;
       }
     }
   }
