@@ -112,6 +112,10 @@ int ofrr_prof_gemm_collect_group(int group);
  * k_finalize accumulates the interval; read returns the summed ms and the launch count. */
 int ofrr_prof_k1_stamp(int on);
 int ofrr_prof_k1_read(double* sum_ms, long long* count);
+/* The same in-kernel stamps for k_ozk_gemm (K7z, the FP64-accurate int8 Ozaki product),
+ * closed by the k_oz_resid launch that follows each product. */
+int ofrr_prof_oz_stamp(int on);
+int ofrr_prof_oz_read(double* sum_ms, long long* count);
 
 /* ---------------------------------------------------------------------------------
  * Device-side outer loop (ofrr/driver.py:101-111 with the tol extension) as one CUDA graph:

@@ -29,6 +29,32 @@
 
 namespace ofrr {
 
+// in-kernel timing of k_ozk_gemm for the bench roofline (the K1 scheme, gemm_tc.cu): every CTA
+// stamps its entry (min) and exit (max) in globaltimer ns; the k_oz_resid launch that follows
+// adds the interval to a running sum and re-arms the stamps
+__device__ unsigned long long g_oz_stamp[4] = {~0ull, 0ull, 0ull, 0ull};   // min start, max end, sum, count
+static bool g_oz_stamp_on = false;
+__device__ __forceinline__ unsigned long long oz_gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+int oz_stamp_enable(int on) {
+  g_oz_stamp_on = on != 0;
+  if (on) {
+    const unsigned long long z[4] = {~0ull, 0ull, 0ull, 0ull};
+    if (cudaMemcpyToSymbol(g_oz_stamp, z, sizeof(z)) != cudaSuccess) return OFRR_ERR_CUDA;
+  }
+  return OFRR_OK;
+}
+int oz_stamp_read(double* sum_ms, long long* count) {
+  unsigned long long v[4];
+  if (cudaMemcpyFromSymbol(v, g_oz_stamp, sizeof(v)) != cudaSuccess) return OFRR_ERR_CUDA;
+  *sum_ms = (double)v[2] * 1e-6;
+  *count = (long long)v[3];
+  return OFRR_OK;
+}
+
 static constexpr int OZ_D = 6;            // digits per operand
 static constexpr int OZ_TM = 128;         // rows per tile (UMMA M = 128)
 static constexpr int OZ_KB = 128;         // K per k-block (int8: one 128B swizzle row)
@@ -579,8 +605,9 @@ template <int FMT, int BN>
 __global__ void __launch_bounds__(OZK_THREADS, 1)
     k_ozk_gemm(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, const int* __restrict__ Tg,
                const __grid_constant__ CUtensorMap tmV, double* __restrict__ ws, int kbc, int nchunks,
-               long long total_units, int max_slots, int npad, int col0) {
+               long long total_units, int max_slots, int npad, int col0, int stamp) {
   using C = OzkCfg<BN>;
+  if (stamp && threadIdx.x == 0) atomicMin(&g_oz_stamp[0], oz_gtimer_ns());
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* abuf = smem;                                  // [A_STAGES][6][128 x 64 B]
@@ -816,6 +843,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (stamp && threadIdx.x == 0) atomicMax(&g_oz_stamp[1], oz_gtimer_ns());
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
@@ -834,8 +862,14 @@ __global__ void __launch_bounds__(OZ_TM)
                const double* __restrict__ vals, const int* __restrict__ r_dev, const double* __restrict__ Y,
                int64_t ldy, double* __restrict__ part, int ldp, void* __restrict__ W, int64_t ldw, int out_fmt,
                double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
-               int out_fmt2) {
+               int out_fmt2, int stamp) {
   __shared__ double red[4][16];
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
+    const unsigned long long t0 = g_oz_stamp[0], t1 = g_oz_stamp[1];
+    if (t1 > t0) { g_oz_stamp[2] += t1 - t0; g_oz_stamp[3] += 1; }
+    g_oz_stamp[0] = ~0ull;
+    g_oz_stamp[1] = 0ull;
+  }
   const int t = blockIdx.x;
   const int row = threadIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1072,7 +1106,7 @@ int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int
     if (rc) return rc;
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
-                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2);
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;
@@ -1134,7 +1168,7 @@ static int ozk_launch(const void* A, int64_t rows, int64_t cols, int64_t lda, co
     attr = true;
   }
   k_ozk_gemm<FMT, BN><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc, p.nchunks,
-                                                                 p.total, p.max_slots, p.npad, col0);
+                                                                 p.total, p.max_slots, p.npad, col0, g_oz_stamp_on ? 1 : 0);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
@@ -1194,7 +1228,7 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     if (rc) return rc;
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
-                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2);
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;

@@ -112,6 +112,7 @@ class RunStats:
     converged: bool = False
     a_passes: int = 0
     device_loop: bool = False     # the outer loop ran as one graph with device-side control flow
+    rungs: list = field(default_factory=list)   # (basis storage format, iterations, A passes) per ladder rung
 
 
 # status-vector slots (one int32[8] device vector, read once per sync point)
@@ -131,6 +132,26 @@ class _IterGraph:
     def __init__(self, graph, Xs, outs, rec, prof_group):
         self.graph, self.Xs, self.outs, self.rec, self.prof_group = graph, Xs, outs, rec, prof_group
         self.report = None      # _ReportGraph of the final Ritz vectors + FP64 residuals
+
+
+class _NoPhase:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+_NO_PHASE = _NoPhase()
+
+
+def _ph(name: str):
+    """A named host phase (torch.profiler record_function range, e.g. scripts/timeline.py);
+    free when no profiler is running."""
+    import torch
+    if torch._C._autograd._profiler_enabled():
+        return torch.autograd.profiler.record_function("ofrr." + name)
+    return _NO_PHASE
 
 
 def _loop_debug(*msg) -> None:
@@ -409,11 +430,13 @@ class EigEngine:
         use_graph = self._graph_capable()
         prev_est = None
         if (X.fmt if X is not None else self.mv.storage) == FpFormat.F64:
-            self._ozaki(self.A_mv)                   # FP64 blocks: slice A once per run, eagerly
+            with _ph("ozaki_prepare"):
+                self._ozaki(self.A_mv)               # FP64 blocks: slice A once per run, eagerly
         if self.mv.storage != self.pol.storage:
             self._ozaki(self.A_pol) if self.pol.storage == FpFormat.F64 else None
         if use_graph and check and stop_estimate is None and (fresh or X.k == cfg.k) and cfg.m >= 2:
-            rs = self._device_loop(X, top)
+            with _ph("device_loop"):
+                rs = self._device_loop(X, top)
             if rs is not None:
                 return rs
         if X is None:
@@ -425,14 +448,17 @@ class EigEngine:
             # (the basis keeps all k in the common case; dropped columns of Q are zero),
             # residual estimate -- replayed as one CUDA graph when possible.  One host sync.
             first = it == 0
-            out = self._graph_step(X, check, top, first) if use_graph and X.k == cfg.k else None
+            with _ph("graph_step"):
+                out = self._graph_step(X, check, top, first) if use_graph and X.k == cfg.k else None
             if out is None:
-                out = self._body(X, check, top, first)
+                with _ph("eager_body"):
+                    out = self._body(X, check, top, first)
                 if use_graph:
                     _WARM.add(self._graph_key(check, top, first))
             st, h, U, eig, Xn, est = out["st"], out["h"], out["U"], out["eig"], out["Xn"], out["est"]
             kp = U.k
-            s, vals_all, est_np = self._unpack(out, st, eig, est)      # the iteration's one sync
+            with _ph("iteration_sync"):
+                s, vals_all, est_np = self._unpack(out, st, eig, est)      # the iteration's one sync
             if s[S_MV_FLAGS] & 1:
                 raise OverflowDiagnostic("non-finite entries after MatVec")
             if s[S_NKEPT] == 0:
@@ -470,7 +496,8 @@ class EigEngine:
                     continue
                 prev_est = worst
                 if worst < tol or stalled or last:
-                    rs = self._final_report(out, U, eig, kp, r, vals, check, top)   # FP64 confirmation
+                    with _ph("final_report"):
+                        rs = self._final_report(out, U, eig, kp, r, vals, check, top)   # FP64 confirmation
                     worst = float(np.max(rs.residuals[: min(top, r)])) if r >= top else float("inf")
                     self.stats.history.append((it + 1, worst))
                     if worst < tol:
@@ -505,10 +532,18 @@ class EigEngine:
         if gf is None or gs is None or gs.report is None or gf.outs.get("est") is None:
             _loop_debug("graphs missing", gf is None, gs is None, gs is not None and gs.report is None)
             return None
-        lk = (cfg.m, top, float(cfg.tol), id(gf))
+        _GRAPHS.move_to_end(kf)
+        _GRAPHS.move_to_end(ks)
+        # the exec clones gf's and gs's nodes (raw pointers into their buffers): the cache entry
+        # holds gf itself, and an entry built from another gf (evicted and recaptured) is stale
+        lk = (cfg.m, top, float(cfg.tol))
         loops = gs.__dict__.setdefault("loops", {})
-        lp = loops.get(lk)
-        if lp is None:
+        ent = loops.get(lk)
+        if ent is not None and ent[0] is not gf:
+            loops.pop(lk)
+            ent = None
+        lp = ent[1] if ent is not None else None
+        if ent is None:
             ctl = torch.zeros(int(L.ofrr_loop_ctl_bytes()), dtype=torch.uint8, device=self.device)
             if gf is gs:
                 src = dst = None
@@ -527,9 +562,10 @@ class EigEngine:
                                    float(cfg.tol), ctypes.byref(ex))
             if rc != 0:
                 _loop_debug("build failed", _lib.last_error())   # the host loop takes over
-                loops[lk] = None
+                loops[lk] = (gf, None)
                 return None
-            lp = loops[lk] = (_LoopExec(ex.value), ctl)
+            lp = (_LoopExec(ex.value), ctl)
+            loops[lk] = (gf, lp)
         elif lp is None:
             return None
         ex, ctl = lp
@@ -541,8 +577,9 @@ class EigEngine:
         elif X.t.data_ptr() != gf.Xs.t.data_ptr():
             gf.Xs.t.copy_(X.t)
         t2 = time.perf_counter()
-        _lib.check(L.ofrr_loop_launch(ex.handle, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
-                   "loop_launch")
+        with _ph("loop_launch"):
+            _lib.check(L.ofrr_loop_launch(ex.handle, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
+                       "loop_launch")
         t3 = time.perf_counter()
         # the solve's one synchronisation: control block, values and FP64 residuals in one
         # pinned buffer
@@ -556,7 +593,8 @@ class EigEngine:
         stage[nb + 8 * k:].view(torch.float64).copy_(gs.report.res[:k], non_blocking=True)
         rg = gs.report
         U64t = rg.U64.t.clone()                        # the returned vectors outlive the next replay
-        torch.cuda.current_stream(self.device).synchronize()
+        with _ph("loop_sync"):
+            torch.cuda.current_stream(self.device).synchronize()
         host = stage
         t4 = time.perf_counter()
         head = host[:16].view(torch.int32).numpy()
@@ -800,22 +838,32 @@ def subspace_iter_eig(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats]
         # progress, then continue from its restart block in cfg.policy
         from dataclasses import replace as _replace
         low = _replace(cfg, policy=cfg.ladder, matvec_policy=None, ladder=None)
-        eng0 = EigEngine(a, low, comm=comm, n_global=n, report_scales=False)
-        X0 = eng0.run(stop_estimate=cfg.ladder_switch)
+        with _ph("rung_low"):
+            eng0 = EigEngine(a, low, comm=comm, n_global=n, report_scales=False)
+            X0 = eng0.run(stop_estimate=cfg.ladder_switch)
         if isinstance(X0, RitzSet):                                # m exhausted in the low rung
             if stats is not None:
                 stats.__dict__.update(eng0.stats.__dict__)
+                stats.rungs = [(cfg_rung_label(low), eng0.stats.iterations, eng0.stats.a_passes)]
             return X0
         hist, iters, passes = list(eng0.stats.history), eng0.stats.iterations, eng0.stats.a_passes
         cfg = _replace(cfg, ladder=None, m=max(1, cfg.m - iters))
-    eng = EigEngine(a, cfg, comm=comm, n_global=n)
-    rs = eng.run(X0=X0)
+    with _ph("rung_main"):
+        eng = EigEngine(a, cfg, comm=comm, n_global=n)
+        rs = eng.run(X0=X0)
     if stats is not None:
         stats.__dict__.update(eng.stats.__dict__)
+        stats.rungs = ([(cfg_rung_label(low), iters, passes)] if X0 is not None else []) + \
+            [(cfg_rung_label(cfg), eng.stats.iterations, eng.stats.a_passes)]
         stats.iterations += iters
         stats.a_passes += passes
         stats.history = hist + [(it + iters, w) for it, w in eng.stats.history]
     return rs
+
+
+def cfg_rung_label(cfg: IterConfig) -> str:
+    """Basis storage format of a rung (RunStats.rungs)."""
+    return FpFormat(cfg.policy.storage).name
 
 
 # -------------------------------------------------------------------------------------
