@@ -246,6 +246,11 @@ size_t ofrr_residual_workspace2(int64_t rows, int64_t cols, int r, int a_fmt, in
  *   residual  res[j] as ofrr_residual_pair (A not transposed) with the prepared operator.
  * Products agree with an FP64 GEMM to ~2^-46 relative to |A| |X| per term (random-sign
  * truncation), not bitwise. */
+/* Diagnostics of a prepared operator (synchronous): *full = 1 when its products use all six
+ * digit planes of A (some row's tails overflowed the per-row list or its scale left the f32
+ * range), 0 when they use the 3-digit heads plus the exact fp64 tails; *tails = number of
+ * tail entries listed over all rows. */
+int ofrr_ozaki_operator_info(const void* op_ws, int64_t rows, int* full, long long* tails);
 size_t ofrr_ozaki_operator_workspace(int64_t rows, int64_t cols);
 size_t ofrr_ozaki_workspace(int64_t rows, int64_t cols, int r);
 int ofrr_ozaki_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws,

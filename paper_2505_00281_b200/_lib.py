@@ -77,6 +77,7 @@ _SIGS = {
     "ofrr_residual_workspace2": ([c_i64, c_i64, c_int, c_int, c_int], c_sz),
     "ofrr_ozaki_operator_workspace": ([c_i64, c_i64], c_sz),
     "ofrr_ozaki_workspace": ([c_i64, c_i64, c_int], c_sz),
+    "ofrr_ozaki_operator_info": ([c_vp, c_i64, c_vp, c_vp], c_int),
     "ofrr_ozaki_prepare": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_sz, c_vp], c_int),
     "ofrr_ozaki_gemm": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_vp,
                          c_vp, c_i64, c_int, c_vp, c_sz, c_vp], c_int),

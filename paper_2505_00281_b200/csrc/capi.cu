@@ -27,6 +27,7 @@ size_t residual_ws(int64_t rows, int r);
 size_t residual_ws2(int64_t rows, int64_t cols, int r, int a_fmt, int transpose);
 size_t ozx_op_ws(int64_t rows, int64_t cols);
 size_t ozx_prod_ws(int64_t rows, int64_t cols, int r);
+int ozx_info(const void* op_ws, int64_t rows, int* full, long long* tails);
 int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws, size_t op_bytes,
                 cudaStream_t st);
 int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws, const double* V,
@@ -205,6 +206,9 @@ size_t ofrr_residual_workspace2(int64_t rows, int64_t cols, int r, int a_fmt, in
 
 size_t ofrr_ozaki_operator_workspace(int64_t rows, int64_t cols) { return ozx_op_ws(rows, cols); }
 size_t ofrr_ozaki_workspace(int64_t rows, int64_t cols, int r) { return ozx_prod_ws(rows, cols, r); }
+int ofrr_ozaki_operator_info(const void* op_ws, int64_t rows, int* full, long long* tails) {
+  return ozx_info(op_ws, rows, full, tails);
+}
 
 int ofrr_ozaki_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws,
                        size_t op_bytes, void* stream) {

@@ -23,6 +23,8 @@
 // accumulators for the six levels, stream-K over (row tile, K chunk) with fp64 partials),
 // k_oz_resid (deterministic partial sums -> (A v_j - lambda_j y_j) column sums of squares).
 #include "common.cuh"
+#include <vector>
+#include <mutex>
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -487,28 +489,93 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------------
-// Row scales of A only (the in-kernel slicing path below converts A on the fly).
+// Row scales of A and the sparse tails of its 3-digit heads (the in-kernel slicing path
+// below converts A on the fly).
+//
+// Head / tail split: with |a| < 2^T (T = row scale), the in-kernel product multiplies the
+// 24-bit head h = trunc(a 2^(22 - T)) (three int8 digits: byte 2 signed, bytes 1, 0
+// unsigned -- the top three of the six 46-bit digits, same weights) and the tail
+// a - h 2^(T - 22) (the bits of a below 2^(T - 22): |tail| < 2^(T - 22), same sign, at most
+// 8 significant bits, exact in f32) is applied exactly in fp64 from a per-row list.  For
+// 16/8-bit entries the tail is non-zero only for entries ~2^-15 below their row maximum (a
+// handful per row), so 15 digit products (p <= 2, p + q <= 5) replace 21 with no loss.
+// A row whose tails overflow OZ_TAIL_CAP, or whose scale leaves the f32 range of the
+// conversion, sets the operator's `full` flag: every product with it then uses all six
+// digits (the previous scheme).  Tails are listed in ascending column order (ordered
+// block compaction): deterministic sums.
 // ---------------------------------------------------------------------------------
+static constexpr int OZ_TAIL_CAP = 32;      // tail entries kept per row
+
+struct OzOpLayout {
+  int64_t rows_pad;
+  size_t off_T, off_full, off_cnt, off_col, off_val, bytes;
+};
+static OzOpLayout oz_op_layout(int64_t rows) {
+  OzOpLayout L;
+  L.rows_pad = (rows + OZ_TM - 1) / OZ_TM * OZ_TM;
+  size_t b = 0;
+  auto take = [&](size_t n) { size_t o = b; b += (n + 255) & ~size_t(255); return o; };
+  L.off_T = take((size_t)L.rows_pad * 4);
+  L.off_full = take(16);
+  L.off_cnt = take((size_t)L.rows_pad * 4);
+  L.off_col = take((size_t)L.rows_pad * OZ_TAIL_CAP * 4);
+  L.off_val = take((size_t)L.rows_pad * OZ_TAIL_CAP * 4);
+  L.bytes = b;
+  return L;
+}
+
+static constexpr int OZ_RS_THREADS = 512;    // k_oz_rowscale: one CTA per row, one 32-entry group per thread step
+
+// mantissa bits of the 16/8-bit formats: an entry with exponent e has no bit below 2^(e - MB)
+template <int FMT> __device__ __forceinline__ constexpr int oz_mant_bits() { return FMT == BF16 ? 7 : FMT == F16 ? 10 : 3; }
+
 template <int FMT>
-__global__ void __launch_bounds__(256)
-    k_oz_rowscale(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, int* __restrict__ T) {
+__global__ void __launch_bounds__(OZ_RS_THREADS)
+    k_oz_rowscale(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, int* __restrict__ T,
+                  int* __restrict__ full, int* __restrict__ tcnt, int* __restrict__ tcol, float* __restrict__ tval) {
+  constexpr int NW = OZ_RS_THREADS / 32;
+  extern __shared__ int8_t gmin[];          // per 32-entry group: min exponent of its non-zero entries
   const int64_t i = blockIdx.x;
-  __shared__ uint32_t red[8];
+  __shared__ uint32_t red[NW];
+  __shared__ int wsum[NW];
   if (i >= rows) {
-    if (threadIdx.x == 0) T[i] = 0;
+    if (threadIdx.x == 0) {
+      T[i] = 0;
+      if (tcnt) tcnt[i] = 0;
+    }
     return;
   }
   const int64_t base = i * lda;
   const int eb = FMT == FP8 ? 1 : 2;
   const bool vec = ((reinterpret_cast<uintptr_t>(A) + (uintptr_t)(base * eb)) & 15) == 0;
+  const int64_t step = 32 * (int64_t)OZ_RS_THREADS;
+  // pass 1: row maximum and, per group, the smallest exponent present (four 8-entry loads
+  // in flight per thread)
   uint32_t m = 0;
-  for (int64_t l0 = 8 * (int64_t)threadIdx.x; l0 < cols; l0 += 8 * (int64_t)blockDim.x) {
-    float x[8];
-    oz_ld8<FMT>(A, base, l0, cols, vec, x);
+  for (int64_t c0 = 0; c0 < cols; c0 += step) {
+    const int64_t l0 = c0 + 32 * (int64_t)threadIdx.x;
+    float x[4][8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t b = __float_as_uint(x[e]) & 0x7fffffffu;
-      m = b > m ? b : m;
+    for (int u = 0; u < 4; ++u) {
+      if (l0 + 8 * u < cols) oz_ld8<FMT>(A, base, l0 + 8 * u, cols, vec, x[u]);
+      else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[u][e] = 0.0f;
+      }
+    }
+    uint32_t emin = 255u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t bb = __float_as_uint(x[u][e]) & 0x7fffffffu;
+        m = bb > m ? bb : m;
+        const uint32_t ef = bb ? (bb >> 23) : 255u;       // biased f32 exponent (0: subnormal)
+        emin = ef < emin ? ef : emin;
+      }
+    if (tcnt && l0 < cols) {
+      const int eu = emin == 255u ? 127 : (emin == 0u ? -128 : (int)emin - 127);   // subnormal: conservative
+      gmin[l0 >> 5] = (int8_t)max(-128, min(127, eu));
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -517,10 +584,127 @@ __global__ void __launch_bounds__(256)
   }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
+  m = red[0];
+  for (int w = 1; w < NW; ++w) m = red[w] > m ? red[w] : m;
+  const int E = oz_scale((double)__uint_as_float(m));
+  if (threadIdx.x == 0) T[i] = E;
+  if (!tcnt) return;
+  // ---- pass 2: tails of the 3-digit heads, re-reading only the groups that can hold one
+  // (an entry with exponent e has bits below 2^(E - 22) only if e - MB < E - 22) ----
+  if (E == OZ_BAD) {                                   // non-finite row: its products are NaN anyway
+    if (threadIdx.x == 0) tcnt[i] = 0;
+    return;
+  }
+  if (22 - E > 127 || 22 - E < -126 || E - 22 < -126) {   // scale outside the f32 conversion range
+    if (threadIdx.x == 0) { tcnt[i] = 0; atomicOr(full, 1); }
+    return;
+  }
+  const float sc = __int_as_float((22 - E + 127) << 23);      // 2^(22 - E)
+  const float isc = __int_as_float((E - 22 + 127) << 23);     // 2^(E - 22)
+  const int ecut = E - 22 + oz_mant_bits<FMT>();              // candidate group: min exponent < ecut
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int total = 0;
+  for (int64_t c0 = 0; c0 < cols; c0 += step) {
+    const int64_t l0 = c0 + 32 * (int64_t)threadIdx.x;
+    uint32_t mask = 0;                                 // bit 8u + e: entry l0 + 8u + e has a tail
+    float x[4][8];
+    if (l0 < cols && (int)gmin[l0 >> 5] < ecut) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (l0 + 8 * u < cols) oz_ld8<FMT>(A, base, l0 + 8 * u, cols, vec, x[u]);
+        else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[u][e] = 0.0f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int h = __float2int_rz(x[u][e] * sc);
+          x[u][e] = x[u][e] - __int2float_rn(h) * isc;     // the tail (exact, see above)
+          mask |= (x[u][e] != 0.0f ? 1u : 0u) << (8 * u + e);
+        }
+    }
+    const int nt = __popc(mask);
+    int woff = 0, btot = 0, inc = nt;
+    if (__syncthreads_or(nt)) {                         // ordered block compaction (exclusive scan)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        woff += w < warp ? wsum[w] : 0;
+        btot += wsum[w];
+      }
+      int pos = total + woff + inc - nt;
+      while (mask) {
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        if (pos < OZ_TAIL_CAP) {
+          tcol[i * OZ_TAIL_CAP + pos] = (int)(l0 + b);
+          tval[i * OZ_TAIL_CAP + pos] = x[b >> 3][b & 7];
+        }
+        ++pos;
+      }
+      total += btot;
+      __syncthreads();                                 // wsum reused by the next chunk
+    }
+  }
   if (threadIdx.x == 0) {
-    m = red[0];
-    for (int w = 1; w < 8; ++w) m = red[w] > m ? red[w] : m;
-    T[i] = oz_scale((double)__uint_as_float(m));
+    tcnt[i] = total < OZ_TAIL_CAP ? total : OZ_TAIL_CAP;
+    if (total > OZ_TAIL_CAP) atomicOr(full, 1);
+  }
+}
+
+// The tails times one column pass of V: Wt[row * BN + j] = sum_e tail_e V[col_e, j0 + j]
+// (fp64, list order).  A warp per row, lanes over the pass's columns: each tail entry reads
+// one contiguous row of Vt.
+__global__ void __launch_bounds__(256)
+    k_oz_tailmul(int64_t rows, const int* __restrict__ full, const int* __restrict__ tcnt,
+                 const int* __restrict__ tcol, const float* __restrict__ tval, const double* __restrict__ Vt,
+                 int ldvt, int j0, int ncols, int BN, double* __restrict__ Wt) {
+  if (*full) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int cnt = tcnt[row];
+  const int mc = lane < cnt ? tcol[row * OZ_TAIL_CAP + lane] : 0;
+  const double mv = lane < cnt ? (double)tval[row * OZ_TAIL_CAP + lane] : 0.0;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int e = 0; e < cnt; ++e) {
+    const int c = __shfl_sync(0xffffffffu, mc, e);
+    const double v = __shfl_sync(0xffffffffu, mv, e);
+    const double* vr = Vt + (int64_t)c * ldvt + j0;
+    if (lane < ncols) acc0 = fma(v, vr[lane], acc0);
+    if (lane + 32 < ncols) acc1 = fma(v, vr[lane + 32], acc1);
+  }
+  if (lane < BN) Wt[row * BN + lane] = acc0;
+  if (lane + 32 < BN) Wt[row * BN + lane + 32] = acc1;
+}
+
+// V (fp64, column j contiguous with ld ldv, n rows x r columns) -> Vt row-major (row l holds
+// V[l, 0..r), leading dimension ldt): the tails read one contiguous row of V per entry
+__global__ void __launch_bounds__(256)
+    k_oz_vt(const double* __restrict__ V, int64_t ldv, int64_t n, int r, double* __restrict__ Vt, int ldt) {
+  __shared__ double tile[32][33];
+  const int64_t l0 = (int64_t)blockIdx.x * 32;
+  const int j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;      // 32 x 8
+  for (int jj = ty; jj < 32; jj += 8) {
+    const int j = j0 + jj;
+    const int64_t l = l0 + tx;
+    tile[jj][tx] = (j < r && l < n) ? V[(int64_t)j * ldv + l] : 0.0;
+  }
+  __syncthreads();
+  for (int ll = ty; ll < 32; ll += 8) {
+    const int64_t l = l0 + ll;
+    const int j = j0 + tx;
+    if (l < n && j < r) Vt[l * ldt + j] = tile[tx][ll];
   }
 }
 
@@ -601,12 +785,19 @@ __device__ __forceinline__ float ozk_elem(const uint4 (&raw)[4], int e) {
   }
 }
 
-template <int FMT, int BN>
+// NP = digit planes of A: 3 (the 24-bit heads; tails applied by k_oz_resid) or 6 (all of A).
+// Both variants are launched back to back; the one that does not match the operator's
+// `full` flag (set by its prepare pass) exits at once -- the choice stays on the device
+// (CUDA graphs) and the MMA issue loop stays fully unrolled.
+template <int FMT, int BN, int NP>
 __global__ void __launch_bounds__(OZK_THREADS, 1)
     k_ozk_gemm(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, const int* __restrict__ Tg,
                const __grid_constant__ CUtensorMap tmV, double* __restrict__ ws, int kbc, int nchunks,
-               long long total_units, int max_slots, int npad, int col0, int stamp) {
+               long long total_units, int max_slots, int npad, int col0, int stamp,
+               const int* __restrict__ full_flag) {
   using C = OzkCfg<BN>;
+  constexpr bool full = NP == OZ_D;
+  if (full_flag != nullptr && ((*full_flag != 0) != full)) return;
   if (stamp && threadIdx.x == 0) atomicMin(&g_oz_stamp[0], oz_gtimer_ns());
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -675,7 +866,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(abuf + as * C::A_SET);
           const uint64_t dv = umma_desc_sw64(smem_u32(vbuf + vs * C::V_SET));
-          for (int p = 0; p < OZ_D; ++p) {
+          for (int p = 0; p < NP; ++p) {
             const uint64_t da = umma_desc_sw64(sa + p * C::A_TILE);
             const int nq = OZ_D - p;
 #pragma unroll
@@ -789,9 +980,25 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
         E = row_ok ? Tg[grow] : 0;
         fast = row_ok && E != OZ_BAD && 46 - E <= 127 && 46 - E >= -126;
         sc = fast ? __int_as_float((46 - E + 127) << 23) : 0.0f;
+        if constexpr (!full) {                // heads: h = trunc(a 2^(22 - E)) (prepare checked the range)
+          fast = row_ok && E != OZ_BAD;
+          sc = fast ? __int_as_float((22 - E + 127) << 23) : 0.0f;
+        }
       }
       uint32_t w[OZ_D][4];
-      if (fast) {
+      if constexpr (!full) {
+        // 24-bit heads: byte 2 (signed) and bytes 1, 0 of the int32 h are the three digits
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t hw[4], tw[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hw[e] = (uint32_t)__float2int_rz(ozk_elem<FMT>(raw, 4 * g + e) * sc);
+          oz_t4(hw, tw);
+          w[0][g] = tw[2];
+          w[1][g] = tw[1];
+          w[2][g] = tw[0];
+        }
+      } else if (fast) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           uint32_t lo[4], hi[4];
@@ -834,7 +1041,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
       const int pos = (r >> 3) * 512 + (r & 7) * 64 + ((qt ^ ((r >> 1) & 3)) << 4);
 #pragma unroll
       for (int p = 0; p < OZ_D; ++p)
-        *reinterpret_cast<uint4*>(slot + p * C::A_TILE + pos) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+        if (p < NP) *reinterpret_cast<uint4*>(slot + p * C::A_TILE + pos) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[as]);
@@ -862,7 +1069,7 @@ __global__ void __launch_bounds__(OZ_TM)
                const double* __restrict__ vals, const int* __restrict__ r_dev, const double* __restrict__ Y,
                int64_t ldy, double* __restrict__ part, int ldp, void* __restrict__ W, int64_t ldw, int out_fmt,
                double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
-               int out_fmt2, int stamp) {
+               int out_fmt2, int stamp, const int* __restrict__ full, const double* __restrict__ Wt) {
   __shared__ double red[4][16];
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
     const unsigned long long t0 = g_oz_stamp[0], t1 = g_oz_stamp[1];
@@ -903,10 +1110,15 @@ __global__ void __launch_bounds__(OZ_TM)
   }
   __syncthreads();
   const int ne = s_ne;
+  // the exact fp64 tail products of this row (3-digit heads in the product kernel)
+  const double* wt = (Wt && valid && !*full) ? Wt + grow * BN : nullptr;
   for (int jb = 16 * blockIdx.y; jb < ncols; jb += 16 * gridDim.y) {   // 16 columns per y-block
-    double s[16];
+    double s[16], tl[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) s[q] = 0.0;
+    for (int q = 0; q < 16; ++q) {
+      s[q] = 0.0;
+      tl[q] = (wt && jb + q < ncols) ? wt[jb + q] : 0.0;
+    }
     if (ne <= MAXE) {
       for (int e = 0; e < ne; ++e) {
         const double* src = ws + s_base[e] + row;
@@ -939,7 +1151,7 @@ __global__ void __launch_bounds__(OZ_TM)
       if (valid && j < ncols && gj < nvalid) {
         const int Fj = F[j];
         const double av = (Ti == OZ_BAD || Fj == OZ_BAD) ? __longlong_as_double(0x7ff8000000000000ll)
-                                                          : ldexp(s[q], Ti + Fj);
+                                                          : ldexp(s[q], Ti + Fj) + tl[q];
         if (W) {
           // the product rounded to the output format; r2 carries |w| for the column max
           const double w = rnd(av, out_fmt);
@@ -1106,7 +1318,7 @@ int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int
     if (rc) return rc;
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
-                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0);
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0, nullptr, nullptr);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;
@@ -1124,10 +1336,10 @@ static bool oz_use_planes() {
 }
 
 struct OzkPlan {
-  int bn, npass, npad, m_tiles, kblocks, nchunks, kbc, grid, max_slots;
+  int bn, npass, npad, m_tiles, kblocks, nchunks, kbc, grid, max_slots, ldvt;
   int64_t rows_pad, cols_pad;
   long long total;
-  size_t off_F, off_dig, off_ws, off_part, bytes;
+  size_t off_F, off_dig, off_ws, off_part, off_vt, off_wt, bytes;
 };
 
 static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r) {
@@ -1154,30 +1366,62 @@ static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r) {
   p.off_dig = take((size_t)OZ_D * p.npad * p.cols_pad);
   p.off_ws = take((size_t)p.grid * p.max_slots * OZ_TM * p.bn * sizeof(double));
   p.off_part = take((size_t)p.m_tiles * r * sizeof(double));
+  p.ldvt = p.npad;
+  p.off_vt = take((size_t)cols * p.ldvt * sizeof(double));     // V row-major for the tails
+  p.off_wt = take((size_t)p.rows_pad * p.bn * sizeof(double));  // tails x V of one column pass
   p.bytes = b;
   return p;
 }
 
 template <int FMT, int BN>
 static int ozk_launch(const void* A, int64_t rows, int64_t cols, int64_t lda, const int* T, const CUtensorMap& tV,
-                      const OzkPlan& p, double* ws, int col0, cudaStream_t st) {
+                      const OzkPlan& p, double* ws, int col0, const int* full, cudaStream_t st) {
   using C = OzkCfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_ozk_gemm<FMT, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-    attr = true;
+  static std::once_flag attr;
+  cudaError_t ae = cudaSuccess;
+  std::call_once(attr, [&] {
+    ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (ae == cudaSuccess)
+      ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, OZ_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  });
+  OFRR_CUDA_TRY(ae);
+  const int stamp = g_oz_stamp_on ? 1 : 0;
+  if (full) {
+    k_ozk_gemm<FMT, BN, 3><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc, p.nchunks,
+                                                                      p.total, p.max_slots, p.npad, col0, stamp, full);
+    OFRR_CHECK_LAUNCH();
   }
-  k_ozk_gemm<FMT, BN><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc, p.nchunks,
-                                                                 p.total, p.max_slots, p.npad, col0, g_oz_stamp_on ? 1 : 0);
+  k_ozk_gemm<FMT, BN, OZ_D><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
+                                                                       p.nchunks, p.total, p.max_slots, p.npad, col0,
+                                                                       stamp, full);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
 
 size_t ozx_op_ws(int64_t rows, int64_t cols) {
-  return oz_use_planes() ? oz_plan(rows, cols, 1).op_bytes : (size_t)((rows + OZ_TM - 1) / OZ_TM * OZ_TM) * 4 + 1024;
+  return oz_use_planes() ? oz_plan(rows, cols, 1).op_bytes : oz_op_layout(rows).bytes + 1024;
+}
+static bool oz_no_tails() {     // OFRR_OZ_FULL=1: all six digits of A in every product (diagnostics)
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("OFRR_OZ_FULL"); v = (e && atoi(e) == 1) ? 1 : 0; }
+  return v == 1;
 }
 size_t ozx_prod_ws(int64_t rows, int64_t cols, int r) {
   return oz_use_planes() ? oz_plan(rows, cols, r).bytes : ozk_plan(rows, cols, r).bytes;
+}
+
+int ozx_info(const void* op_ws, int64_t rows, int* full, long long* tails) {
+  if (oz_use_planes()) { *full = 1; *tails = 0; return OFRR_OK; }
+  const OzOpLayout L = oz_op_layout(rows);
+  const uint8_t* b = (const uint8_t*)op_ws;
+  OFRR_CUDA_TRY(cudaDeviceSynchronize());
+  OFRR_CUDA_TRY(cudaMemcpy(full, b + L.off_full, sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<int> c((size_t)rows);
+  OFRR_CUDA_TRY(cudaMemcpy(c.data(), b + L.off_cnt, (size_t)rows * sizeof(int), cudaMemcpyDeviceToHost));
+  long long t = 0;
+  for (int v : c) t += v;
+  *tails = t;
+  return OFRR_OK;
 }
 
 int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws, size_t op_bytes,
@@ -1188,11 +1432,32 @@ int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fm
     return OFRR_ERR_UNSUPPORTED;
   }
   if (!op_ws || op_bytes < ozx_op_ws(rows, cols)) { ofrr_set_error("ozaki: operator workspace too small"); return OFRR_ERR_INVALID; }
-  const unsigned g = (unsigned)((rows + OZ_TM - 1) / OZ_TM * OZ_TM);
-  int* T = (int*)op_ws;
-  if (a_fmt == BF16) k_oz_rowscale<BF16><<<g, 256, 0, st>>>(A, rows, cols, lda, T);
-  else if (a_fmt == F16) k_oz_rowscale<F16><<<g, 256, 0, st>>>(A, rows, cols, lda, T);
-  else k_oz_rowscale<FP8><<<g, 256, 0, st>>>(A, rows, cols, lda, T);
+  const OzOpLayout L = oz_op_layout(rows);
+  const unsigned g = (unsigned)L.rows_pad;
+  uint8_t* b = (uint8_t*)op_ws;
+  int* T = (int*)(b + L.off_T);
+  int* full = (int*)(b + L.off_full);
+  int* tcnt = (int*)(b + L.off_cnt);
+  int* tcol = (int*)(b + L.off_col);
+  float* tval = (float*)(b + L.off_val);
+  const int one = oz_no_tails() ? 1 : 0;
+  const size_t gbytes = (size_t)((cols + 31) / 32);     // per-group minimum exponents (pass 1 -> pass 2)
+  if (gbytes > 48 * 1024) {
+    static std::once_flag big;
+    cudaError_t e = cudaSuccess;
+    std::call_once(big, [&] {
+      e = cudaFuncSetAttribute(k_oz_rowscale<BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_oz_rowscale<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_oz_rowscale<FP8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    OFRR_CUDA_TRY(e);
+    if (gbytes > 200 * 1024) { ofrr_set_error("ozaki: %lld columns exceed the row-scale pass", (long long)cols); return OFRR_ERR_UNSUPPORTED; }
+  }
+  OFRR_CUDA_TRY(cudaMemsetAsync(full, 0, sizeof(int), st));
+  if (one) OFRR_CUDA_TRY(cudaMemsetAsync(full, 0x01, 1, st));
+  if (a_fmt == BF16) k_oz_rowscale<BF16><<<g, OZ_RS_THREADS, gbytes, st>>>(A, rows, cols, lda, T, full, tcnt, tcol, tval);
+  else if (a_fmt == F16) k_oz_rowscale<F16><<<g, OZ_RS_THREADS, gbytes, st>>>(A, rows, cols, lda, T, full, tcnt, tcol, tval);
+  else k_oz_rowscale<FP8><<<g, OZ_RS_THREADS, gbytes, st>>>(A, rows, cols, lda, T, full, tcnt, tcol, tval);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
@@ -1206,13 +1471,23 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
                     out_fmt2, part_out, ws, ws_bytes, st);
   const OzkPlan p = ozk_plan(rows, cols, r);
   if (!ws || ws_bytes < p.bytes) { ofrr_set_error("ozaki: workspace too small (%zu < %zu)", ws_bytes, p.bytes); return OFRR_ERR_INVALID; }
-  const int* T = (const int*)op_ws;
+  const OzOpLayout OL = oz_op_layout(rows);
+  const uint8_t* ob = (const uint8_t*)op_ws;
+  const int* T = (const int*)(ob + OL.off_T);
+  const int* full = (const int*)(ob + OL.off_full);
+  const int* tcnt = (const int*)(ob + OL.off_cnt);
+  const int* tcol = (const int*)(ob + OL.off_col);
+  const float* tval = (const float*)(ob + OL.off_val);
   uint8_t* base = (uint8_t*)ws;
   int* F = (int*)(base + p.off_F);
   int8_t* dig = (int8_t*)(base + p.off_dig);
   double* pws = (double*)(base + p.off_ws);
   double* part = (double*)(base + p.off_part);
+  double* Vt = (double*)(base + p.off_vt);
+  double* Wt = (double*)(base + p.off_wt);
   k_oz_slices_v<<<(unsigned)p.npad, 256, 0, st>>>(V, ldv, cols, r, F, dig, p.npad, p.cols_pad);
+  OFRR_CHECK_LAUNCH();
+  k_oz_vt<<<dim3((unsigned)((cols + 31) / 32), (unsigned)((r + 31) / 32)), 256, 0, st>>>(V, ldv, cols, r, Vt, p.ldvt);
   OFRR_CHECK_LAUNCH();
   CUtensorMap tV;
   int rc = oz_make_tmap_u8_sw64(&tV, dig, (uint64_t)cols, (uint64_t)OZ_D * p.npad, (uint64_t)p.cols_pad, OZK_KB,
@@ -1221,14 +1496,17 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
   for (int ps = 0; ps < p.npass; ++ps) {
     const int j0 = ps * p.bn;
 #define OZK_CASE(F)                                                                              \
-    rc = p.bn == 32 ? ozk_launch<F, 32>(A, rows, cols, lda, T, tV, p, pws, j0, st)               \
-                    : ozk_launch<F, 64>(A, rows, cols, lda, T, tV, p, pws, j0, st);
+    rc = p.bn == 32 ? ozk_launch<F, 32>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)         \
+                    : ozk_launch<F, 64>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);
     if (a_fmt == BF16) { OZK_CASE(BF16) } else if (a_fmt == F16) { OZK_CASE(F16) } else { OZK_CASE(FP8) }
 #undef OZK_CASE
     if (rc) return rc;
+    k_oz_tailmul<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(rows, full, tcnt, tcol, tval, Vt, p.ldvt, j0,
+                                                             std::min(p.bn, r - j0), p.bn, Wt);
+    OFRR_CHECK_LAUNCH();
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
-                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0);
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0, full, Wt);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;

@@ -124,6 +124,7 @@ S_MV_FLAGS, S_NKEPT, S_EIG_STATUS, S_NOUT, S_GRAM_FLAGS, S_RESTART_FLAGS, S_NKEP
 # so a new operator at the same address replays correctly.
 _GRAPH_MAX = 8
 _GRAPHS = OrderedDict()
+DEVICE_LOOP = True      # the whole solve as one graph launch (csrc/loop.cu) once its graphs exist
 _WARM = set()
 _NO_GRAPH = set()
 
@@ -349,7 +350,8 @@ class EigEngine:
             est = ops.residual_estimate(Ul, W2, eig.vectors, kp, eig.values, eig.n_out, t,
                                         mode=2 if comm.distributed else 0)
             if comm.distributed:
-                comm.all_reduce_sum_(est)
+                comm.all_reduce_sum_(est)                      # sums of squares over the row blocks
+                est = _relative(est, eig.values, t)
         Xp = self.power_from(W2, eig, kp, st) if reuse else None
         self._join(side)
         if reuse:
@@ -393,16 +395,11 @@ class EigEngine:
             ops.ozaki_residual(oz, U64.narrow(r), Yl.narrow(r), vals, r_dev, r, res, 2)
         else:
             ops.residual_pair(A, False, U64.narrow(r), Yl.narrow(r), vals, r_dev, r, res, accumulate_max=2)
-        comm.all_reduce_sum_(res)
-        return res   # sum of squares; finished on the host (see _finish_residuals)
+        comm.all_reduce_sum_(res)                              # sums of squares over the row blocks
+        return _relative(res, vals, r)
 
     def finish_residuals(self, res, vals_np):
-        r = res.cpu().numpy()
-        if self.comm.distributed:
-            lam = vals_np[: len(r)]
-            with np.errstate(divide="ignore"):
-                return np.where(lam == 0.0, np.inf, np.sqrt(r) / np.abs(lam))
-        return r
+        return res.cpu().numpy()
 
     # ---- the outer loop -----------------------------------------------------------------
     def run(self, X0=None, stop_estimate: Optional[float] = None):
@@ -434,7 +431,7 @@ class EigEngine:
                 self._ozaki(self.A_mv)               # FP64 blocks: slice A once per run, eagerly
         if self.mv.storage != self.pol.storage:
             self._ozaki(self.A_pol) if self.pol.storage == FpFormat.F64 else None
-        if use_graph and check and stop_estimate is None and (fresh or X.k == cfg.k) and cfg.m >= 2:
+        if use_graph and DEVICE_LOOP and check and stop_estimate is None and (fresh or X.k == cfg.k) and cfg.m >= 2:
             with _ph("device_loop"):
                 rs = self._device_loop(X, top)
             if rs is not None:
@@ -680,11 +677,12 @@ class EigEngine:
         else:
             eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
         out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None, Xnext=Xnext)
-        if not self.comm.distributed:
-            parts = [st.to(torch.float64), eig.values.reshape(-1).to(torch.float64)]
-            if est is not None:
-                parts.append(est.reshape(-1).to(torch.float64))
-            out["pack"] = torch.cat(parts)
+        if self.comm.distributed:
+            self.comm.all_reduce_max_(st)        # every rank sees (and raises) the same status
+        parts = [st.to(torch.float64), eig.values.reshape(-1).to(torch.float64)]
+        if est is not None:
+            parts.append(est.reshape(-1).to(torch.float64))
+        out["pack"] = torch.cat(parts)
         return out
 
     def _unpack(self, out, st, eig, est):
@@ -697,8 +695,11 @@ class EigEngine:
         return host[:8].astype(np.int64), host[8:8 + k], (host[8 + k:] if est is not None else None)
 
     def _graph_capable(self) -> bool:
+        """CUDA graphs (and the device-side loop) need capturable collectives when the rows are
+        partitioned: NCCL; gloo (CPU tests, host-staged) runs eagerly."""
         import os
-        return (self.ops is _ops and self.device.type == "cuda" and not self.comm.distributed
+        return (self.ops is _ops and self.device.type == "cuda"
+                and (not self.comm.distributed or self.comm.graphable)
                 and os.environ.get("OFRR_CUDA_GRAPHS", "1") != "0")
 
     def _graph_key(self, check: bool, top: int, first: bool = True):
@@ -788,13 +789,8 @@ class EigEngine:
         return out
 
     def _finish(self, r, vals_np):
-        """Host finish of residuals read back: relative already (one GPU) or sums of
-        squares (row-partitioned, ||.||^2 all-reduced) -> sqrt / |lambda|."""
-        if self.comm.distributed:
-            lam = vals_np[: len(r)]
-            r = r[: len(lam)]
-            with np.errstate(divide="ignore"):
-                return np.where(lam == 0.0, np.inf, np.sqrt(r) / np.abs(lam))
+        """Residual estimates read back (already relative: the row-partitioned path finishes
+        its all-reduced sums of squares on the device, _relative)."""
         return r
 
     def report(self, U64, eig, r: int, vals=None) -> RitzSet:
@@ -808,6 +804,17 @@ class EigEngine:
         from dataclasses import replace
         res = self.residuals(U64, eig.values, eig.n_out, r)
         return replace(rs, residuals=self.finish_residuals(res, rs.values)[:r])
+
+
+def _relative(ss, vals, r: int):
+    """||.||^2 all-reduced over the row blocks -> sqrt(ss) / |lambda| (inf for lambda = 0), on
+    the device (capturable: the device-side loop compares it with tol)."""
+    import torch
+    lam = vals.reshape(-1)[:r].abs()
+    out = ss.clone()
+    head = torch.where(lam == 0, torch.full_like(lam, float("inf")), torch.sqrt(ss[:r]) / lam)
+    out[:r].copy_(head)
+    return out
 
 
 def _row_slice(B, r0: int, r1: int):

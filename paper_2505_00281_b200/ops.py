@@ -281,6 +281,17 @@ class OzakiOperator:
         if prepare:
             self.refresh()
 
+    def info(self):
+        """(full, tails): whether products use all six digit planes of A (else the 3-digit
+        heads plus the exact fp64 tails), and the number of listed tail entries (synchronous;
+        diagnostics and tests)."""
+        import ctypes
+        L = _lib.load()
+        full, tails = ctypes.c_int(0), ctypes.c_longlong(0)
+        _lib.check(L.ofrr_ozaki_operator_info(self.ws.data_ptr(), self.A.rows, ctypes.byref(full), ctypes.byref(tails)),
+                   "ozaki_operator_info")
+        return bool(full.value), int(tails.value)
+
     def refresh(self) -> None:
         L = _lib.load()
         A = self.A
@@ -301,7 +312,7 @@ def ozaki_gemm(oz: OzakiOperator, X: DevBlock, W: DevBlock, colmax=None, flags=N
                                  _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
                                  W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else int(W.fmt),
                                  ws.data_ptr(), ws.numel(), _stream()), "ozaki_gemm")
-    _count(2 + (X.k + 63) // 64 * 2)
+    _count(2 + (X.k + 63) // 64 * 4)     # digits of X, X row-major; per column pass: 2 product variants, tails, fixup
 
 
 def ozaki_residual(oz: OzakiOperator, Xv: DevBlock, Yv: DevBlock, vals: torch.Tensor,
@@ -313,7 +324,7 @@ def ozaki_residual(oz: OzakiOperator, Xv: DevBlock, Yv: DevBlock, vals: torch.Te
                                      Yv.ld, vals.data_ptr(),
                                      _p(r_dev), r_max, res.data_ptr(), int(accumulate_max), ws.data_ptr(), ws.numel(),
                                      _stream()), "ozaki_residual")
-    _count(3 + (r_max + 63) // 64 * 2)
+    _count(3 + (r_max + 63) // 64 * 4)
     return res
 
 

@@ -23,6 +23,9 @@ A, _ = p.synthetic_symmetric(lam, p.FpFormat[cfg["fmt"]], seed=bench.SEED, devic
 icfg = bench.make_iter_config(p, cfg)
 for _ in range(4):
     p.subspace_iter_eig(A, icfg)
+if os.environ.get("OFRR_TIMELINE_HOST_LOOP", "1") == "1":     # CUPTI misses kernels in conditional nodes
+    from paper_2505_00281_b200 import driver
+    driver.DEVICE_LOOP = False
 torch.cuda.synchronize()
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
@@ -30,7 +33,7 @@ with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         p.subspace_iter_eig(A, icfg)
     torch.cuda.synchronize()
 allev = list(prof.events())
-ev = [e for e in allev if e.device_type == torch.autograd.DeviceType.CUDA]
+ev = [e for e in allev if e.device_type == torch.autograd.DeviceType.CUDA and not e.name.startswith("ofrr.")]
 ranges = [e for e in allev if e.device_type != torch.autograd.DeviceType.CUDA and e.name.startswith("ofrr.")]
 ev.sort(key=lambda e: e.time_range.start)
 t0, t1 = ev[0].time_range.start, max(e.time_range.end for e in ev)

@@ -399,3 +399,54 @@ def test_start_block_matches_numpy(ofrr_gpu, oracle, n, k, fmt):
         X = ops.start_block(seed, n, k, ofrr_gpu.FpFormat(fmt), torch.device("cuda"))
         ref = oracle.round_to(np.random.default_rng(seed).random((n, k)), fmt)
         np.testing.assert_array_equal(_host(X), ref)
+
+
+def _exact_rows_dot(a, x):
+    """A X with every product and sum exact (A entries and X entries are floats; the sum of
+    exact products is formed in fp64 twice-compensated: a 2Sum/2Prod dot, error << 1 ulp)."""
+    import math
+    out = np.empty((a.shape[0], x.shape[1]))
+    for j in range(x.shape[1]):
+        for i in range(a.shape[0]):
+            out[i, j] = math.fsum(a[i] * x[:, j])      # exact rounding of the exact sum of exact products
+    return out
+
+
+@pytest.mark.parametrize("case", ["heads", "tails", "full"])
+def test_ozaki_heads_and_tails(ofrr_gpu, oracle, case):
+    """K7z's 3-digit heads of A + exact fp64 tails (oz.cu, k_oz_rowscale) against exact products.
+
+    heads: entries within 2^15 of their row maximum -> no tails (pure 15-digit-product path);
+    tails: a few entries per row far below the maximum -> listed tails, still the head path;
+    full:  rows with more tails than the per-row list holds -> all six digit planes.
+    Every case must be FP64-accurate: |W - AX| <= 2^-44 |A||X| + 4 ulp (the digit products with
+    p + q >= 6 are dropped: ~2^-46 per term, as in the six-digit scheme)."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng({"heads": 1, "tails": 2, "full": 3}[case])
+    rows, cols, k = 300, 3000, 40
+    a = rng.uniform(0.5, 1.0, (rows, cols)) * rng.choice([-1.0, 1.0], (rows, cols))
+    if case == "tails":
+        for i in range(rows):                        # 0..5 tiny entries per row
+            j = rng.choice(cols, size=i % 6, replace=False)
+            a[i, j] *= 2.0 ** rng.uniform(-40, -16, j.size)
+    elif case == "full":
+        a *= 2.0 ** rng.uniform(-30, 0, (rows, cols))   # wide range: most entries have tails
+    a = o.round_to(a * np.exp(rng.uniform(-2, 2, (rows, 1))), BF16)
+    x = rng.standard_normal((cols, k))
+    A = _op(p, a, BF16)
+    oz = ops.OzakiOperator(A)
+    full, tails = oz.info()
+    assert full == (case == "full"), (full, tails)
+    if case == "heads":
+        assert tails == 0
+    if case == "tails":
+        assert tails > 0
+    X = _blk(p, x, F64)
+    W = ops.new_block(rows, k, p.FpFormat.F64, torch.device("cuda"))
+    ops.gemm_av(A, X, W, oz=oz)
+    got = W.to_numpy_f64()
+    ref = _exact_rows_dot(a, x)
+    bound = 2.0 ** -44 * (np.abs(a) @ np.abs(x)) + 4 * np.spacing(np.abs(ref))
+    assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
