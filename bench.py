@@ -338,6 +338,12 @@ def _label(name: str) -> str:
     return "other (torch fills/copies, memcpy)"
 
 
+def _oz_products(name: str) -> int:
+    """Digit products per K7z launch: 15 with the 3-digit heads of A (k_ozk_gemm<F, BN, 3>),
+    21 with all six planes."""
+    return 15 if name.replace(" ", "").endswith(",3>") or ",3>(" in name.replace(" ", "") else 21
+
+
 def _kernel_work(name: str, cfg, rows: int):
     """(bytes, ops, ops_kind) per launch of a kernel of this config (algorithmic: SURVEY.md
     8(d)); None where the kernel is latency-bound (pencil, control) or bookkeeping."""
@@ -345,7 +351,7 @@ def _kernel_work(name: str, cfg, rows: int):
     s_blk = 8 if "double" in name else 4
     if "k_ozk_gemm" in name:
         bn = 64 if k > 32 else 32
-        return rows * n * 2 + 6 * n * bn, 21 * 2.0 * rows * n * bn, "int8"
+        return rows * n * 2 + 6 * n * bn, _oz_products(name) * 2.0 * rows * n * bn, "int8"
     if "k_hessenberg" in name:
         return 2 * n * k * s_blk, None, None
     if "k_gram_partial" in name:
@@ -629,11 +635,12 @@ def _roofline(table, stamps, log, cfg, rows, ms_step, hbm, bf16_peak, peak_kind,
     if "k_ozk_gemm" in dom:
         sm, cnt = stamps["oz"]
         avg_ms = sm / cnt if cnt else float("nan")
-        nb, ops_, _ = _kernel_work("k_ozk_gemm", cfg, rows)
+        nb, ops_, _ = _kernel_work(dom, cfg, rows)
         tops = ops_ / (avg_ms * 1e-3) / 1e12
         peak = 2.0 * bf16_peak
         gbs = nb / (avg_ms * 1e-3) / 1e9
-        out = {"kernel": "k_ozk_gemm (K7z: FP64-accurate A.X on the int8 tensor cores, 21 digit products)",
+        out = {"kernel": f"{dom[:40]} (K7z: FP64-accurate A.X on the int8 tensor cores, {_oz_products(dom)} "
+                         "digit products)",
                "bound": "tensor", "achieved": _num(tops), "peak": peak, "unit": "TOP/s (int8)",
                "frac": _num(tops / peak), "peak_kind": f"derived: 2 x {peak_kind} bf16 {bf16_peak} "
                                                      "(nominal dense int8:bf16 ratio, 4.5:2.25 P/s)",

@@ -325,6 +325,26 @@ int ofrr_host_gemm_mixed(const double* a, int64_t ars, int64_t acs, const double
 int ofrr_host_jacobi_eig(const double* a, int64_t n, int max_sweeps, double tol, double* vals,
                          double* vecs, int* sweeps, double* off);
 
+/* K8b: the reference's Gaussian-kernel test matrix (ofrr/matrix.py:97-113) evaluated on the
+ * device, FP64 in the reference's operation order, rounded once to out_fmt and written
+ * row-major (leading dimension ld >= m).  px: n x 2 points (row-major, device); py: m x 2
+ * column points (cross kernel, no diagonal term) or NULL (square kernel: py = px, + s on the
+ * diagonal).  Replaces the host generation in ofrr/cli.py:163-189 for the harness. */
+int ofrr_gaussian_kernel(const double* px, int64_t n, const double* py, int64_t m, double f, double l, double s,
+                         void* out, int64_t ld, int out_fmt, void* stream);
+
+/* Gram-Schmidt basis builders, the classical comparators that OFRR + Hessenberg replaces
+ * (SURVEY.md 8(f) rank 4).  Replaces ofrr/basis.py:65-148 (orthonormalize with
+ * method = 0 mgs-l, 1 mgs-r, 2 cgs, 3 cgs2; reorth as the reference's keyword).  Q receives
+ * the kept columns first (n_kept of them, zeros after), kept[k] marks the input columns
+ * kept.  Element arithmetic per the policy (storage / compute / accumulate), sums in
+ * parallel order: agrees with the reference to the accumulate format's rounding.
+ * k <= 512.  Returns OFRR_OK (an empty basis is *n_kept == 0; the caller raises). */
+size_t ofrr_orthonormalize_workspace(int64_t n, int k);
+int ofrr_orthonormalize(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute, int accumulate,
+                        double drop_tol, int method, int reorth, void* Q, int64_t ldq, int* kept, int* n_kept,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -192,6 +192,91 @@ def hessenberg_basis(x, pol: Pol):
     return np.asfortranarray(q[:, :nk]), piv[:nk].copy(), kept.astype(bool)
 
 
+def safe_norm2(x, pol: Pol) -> float:
+    """ofrr/precision.py:138-156 (overflow-safe 2-norm under the policy)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    m = float(np.max(np.abs(x)))
+    if m == 0.0:
+        return 0.0
+    u = round_to(x / m, pol.compute)
+    ss = mixed_dot(u, u, pol.compute, pol.accumulate)
+    r = float(round_to(np.sqrt(ss), pol.compute))
+    return float(round_to(m * r, pol.compute))
+
+
+def axpy(y, alpha, x, pol: Pol):
+    """ofrr/precision.py:172-180: y - c(alpha) * x with compute-format roundings, stored."""
+    c = pol.compute
+    t = round_to(float(round_to(alpha, c)) * np.asarray(x, dtype=np.float64), c)
+    return round_to(round_to(np.asarray(y, dtype=np.float64) - t, c), pol.storage)
+
+
+REORTH_THRESHOLD = np.sqrt(2.0) / 2.0   # ofrr/basis.py:20
+
+
+def orthonormalize(x, method: str, pol: Pol, reorth: bool = True):
+    """ofrr/basis.py:65-116 (+ _mgs_project :119-123, _cgs_project :126-130, _mgs_right
+    :133-148) -> (q n x k' F-order, kept bool[k]).  Products / differences are exact in fp64
+    before the compute-format rounding (storage <= compute), so the numpy formulation
+    rounds exactly like the reference's typed arrays."""
+    a = np.array(x, dtype=np.float64, order="F")
+    n, k = a.shape
+    if k == 0:
+        raise EmptyBasisError("no input columns")
+    kept = np.zeros(k, dtype=bool)
+    cols = []
+    if method == "mgs-r":
+        pre = np.array([safe_norm2(a[:, j], pol) for j in range(k)])
+        for j in range(k):
+            v = a[:, j]
+            nrm = safe_norm2(v, pol)
+            if nrm < pol.drop_tol * pre[j] or nrm == 0.0:
+                continue
+            q = round_to(round_to(v / nrm, pol.compute), pol.storage)
+            kept[j] = True
+            cols.append(q)
+            for i in range(j + 1, k):
+                h = mixed_dot(q, a[:, i], pol.compute, pol.accumulate)
+                a[:, i] = axpy(a[:, i], h, q, pol)
+    else:
+        def mgs(v):
+            for qi in cols:
+                v = axpy(v, mixed_dot(qi, v, pol.compute, pol.accumulate), qi, pol)
+            return v, safe_norm2(v, pol)
+
+        def cgs(v):
+            coeffs = [mixed_dot(qi, v, pol.compute, pol.accumulate) for qi in cols]
+            for h, qi in zip(coeffs, cols):
+                v = axpy(v, h, qi, pol)
+            return v
+
+        for j in range(k):
+            v = a[:, j].copy()
+            pre = safe_norm2(v, pol)
+            if method == "mgs-l":
+                v, nrm = mgs(v)
+                if reorth and nrm < REORTH_THRESHOLD * pre:
+                    v, nrm = mgs(v)
+            elif method in ("cgs", "cgs2"):
+                v = cgs(v)
+                nrm = safe_norm2(v, pol)
+                if method == "cgs2":
+                    n1 = nrm
+                    v = cgs(v)
+                    nrm = safe_norm2(v, pol)
+                    if nrm < REORTH_THRESHOLD * n1:
+                        continue
+            else:
+                raise ValueError(f"{method} is not a Gram-Schmidt method")
+            if nrm < pol.drop_tol * pre or nrm == 0.0:
+                continue
+            kept[j] = True
+            cols.append(round_to(round_to(v / nrm, pol.compute), pol.storage))
+    if not cols:
+        raise EmptyBasisError("all columns dropped during orthonormalization")
+    return np.asfortranarray(np.column_stack(cols)), kept
+
+
 # ----------------------------------------------------------------------------------
 # small solves (ofrr/smallsolve.py)
 # ----------------------------------------------------------------------------------
@@ -294,6 +379,15 @@ class Ritz:
     diagnostics: str = ""
 
 
+def rr_eig(a, q, pol: Pol) -> Ritz:
+    """ofrr/projection.py:64-72: eig of Q'AQ, vectors Q Y in FP64."""
+    w = apply_dense(a, q, pol)
+    b = _project(q, w, pol)
+    b = (b + b.T) / 2.0
+    vals, vecs = sym_eig(b)
+    return Ritz(vals, np.asarray(q) @ vecs, "eig")
+
+
 def ofrr_eig(a, u, pol: Pol) -> Ritz:
     """ofrr/projection.py:75-87."""
     w = apply_dense(a, u, pol)
@@ -374,7 +468,7 @@ def _check_finite(x, stage):
 
 
 def subspace_iter_eig(a, k, m=1, iters=1, pol=TC_BF16, mv_pol=None, seed=0,
-                      top=None, tol=None, history=None) -> Ritz:
+                      top=None, tol=None, history=None, method="hess-l", projection="ofrr") -> Ritz:
     """ofrr/driver.py:84-111 with hess-l/hess-r + ofrr.
 
     ``top``/``tol`` add the time-to-tolerance stop: after each
@@ -393,8 +487,8 @@ def subspace_iter_eig(a, k, m=1, iters=1, pol=TC_BF16, mv_pol=None, seed=0,
             x = apply_dense(a, x, mv)
             _check_finite(x, "MatVec")
             x = scale_columns_inf(x, mv)
-        q, _, _ = hessenberg_basis(x, pol)
-        rs = ofrr_eig(a, q, pol)
+        q = hessenberg_basis(x, pol)[0] if method in ("hess-l", "hess-r") else orthonormalize(x, method, pol)[0]
+        rs = rr_eig(a, q, pol) if projection == "rr" else ofrr_eig(a, q, pol)
         x = round_to(np.asfortranarray(rs.vectors), mv.storage)
         _check_finite(x, "projection")
         if tol is not None:

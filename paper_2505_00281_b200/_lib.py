@@ -78,6 +78,10 @@ _SIGS = {
     "ofrr_ozaki_operator_workspace": ([c_i64, c_i64], c_sz),
     "ofrr_ozaki_workspace": ([c_i64, c_i64, c_int], c_sz),
     "ofrr_ozaki_operator_info": ([c_vp, c_i64, c_vp, c_vp], c_int),
+    "ofrr_orthonormalize_workspace": ([c_i64, c_int], c_sz),
+    "ofrr_orthonormalize": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_int, c_dbl, c_int, c_int, c_vp, c_i64, c_vp,
+                             c_vp, c_vp, c_sz, c_vp], c_int),
+    "ofrr_gaussian_kernel": ([c_vp, c_i64, c_vp, c_i64, c_dbl, c_dbl, c_dbl, c_vp, c_i64, c_int, c_vp], c_int),
     "ofrr_ozaki_prepare": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_sz, c_vp], c_int),
     "ofrr_ozaki_gemm": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_vp,
                          c_vp, c_i64, c_int, c_vp, c_sz, c_vp], c_int),

@@ -1,8 +1,9 @@
-"""Basis builders on the B200 hot path: the Hessenberg process (hess-l / hess-r).
+"""Basis builders on the device: the Hessenberg process (hess-l / hess-r, the basis OFRR
+uses in place of QR) and the Gram-Schmidt family (mgs-l, mgs-r, cgs, cgs2 -- the QR
+comparators of SURVEY.md 8(f) rank 4, csrc/gs.cu).
 
-Same names as ofrr/basis.py:23-62.  Only the Hessenberg family runs here (it is the
-basis OFRR uses in place of QR); the Gram-Schmidt and Krylov builders are the
-reference's CPU baselines and are rejected with ValueError (there is no CPU fallback).
+Same names as ofrr/basis.py:23-148.  The Krylov builders (arnoldi-mgs, krylov-hess) belong
+to the reference's sparse Krylov solver and are rejected with ValueError (no CPU fallback).
 """
 
 from __future__ import annotations
@@ -45,12 +46,33 @@ class BasisFactorization:
 
 
 def build_basis(x: DenseMatrix, method: BasisMethod, policy: PrecisionPolicy) -> BasisFactorization:
-    """ofrr/basis.py:54-62 dispatch (Hessenberg family only on this path)."""
+    """ofrr/basis.py:54-62 dispatch."""
+    if method in GRAM_SCHMIDT_METHODS:
+        return orthonormalize(x, method, policy)
     if method in HESSENBERG_METHODS:
         return hessenberg_basis(x, "left" if method is BasisMethod.HESS_LEFT else "right", policy)
-    if method in GRAM_SCHMIDT_METHODS:
-        raise ValueError(f"{method} (Gram-Schmidt) is not on the B200 OFRR path; use hess-l / hess-r")
     raise ValueError(f"{method} is not a block basis method")
+
+
+def orthonormalize(x: DenseMatrix, method: BasisMethod, policy: PrecisionPolicy,
+                   reorth: bool = True) -> BasisFactorization:
+    """Gram-Schmidt family under an explicit precision policy (ofrr/basis.py:65-116), on the
+    device (K3g, csrc/gs.cu): drop rule nrm < drop_tol * pre, MGS-L's single
+    re-orthogonalization, CGS2's two sweeps, MGS-R's right-looking sweep."""
+    from . import ops
+    if method not in GRAM_SCHMIDT_METHODS:
+        raise ValueError(f"{method} is not a Gram-Schmidt method")
+    if x.cols == 0:
+        raise EmptyBasisError("no input columns")
+    X = x.device_block(policy.storage)
+    h = ops.orthonormalize(X, method.value, policy.storage, policy.compute, policy.accumulate, policy.drop_tol,
+                           reorth=reorth)
+    nk = int(h.n_kept.item())
+    if nk == 0:
+        raise EmptyBasisError("all columns dropped during orthonormalization")
+    q = DenseMatrix.from_block(h.Q.narrow(nk))
+    return BasisFactorization(q, np.zeros(0, dtype=np.int64), h.kept[: x.cols].cpu().numpy().astype(bool), method,
+                              policy)
 
 
 def hessenberg_basis(x: DenseMatrix, layout: str, policy: PrecisionPolicy) -> BasisFactorization:

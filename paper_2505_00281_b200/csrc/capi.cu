@@ -28,6 +28,12 @@ size_t residual_ws2(int64_t rows, int64_t cols, int r, int a_fmt, int transpose)
 size_t ozx_op_ws(int64_t rows, int64_t cols);
 size_t ozx_prod_ws(int64_t rows, int64_t cols, int r);
 int ozx_info(const void* op_ws, int64_t rows, int* full, long long* tails);
+int gaussian_kernel(const double* px, int64_t n, const double* py, int64_t m, double f, double l, double s,
+                    void* out, int64_t ld, int fmt, cudaStream_t st);
+size_t gram_schmidt_ws(int64_t n, int k);
+int gram_schmidt(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute, int accumulate,
+                 double drop_tol, int method, int reorth, void* Q, int64_t ldq, int* kept, int* n_kept, void* ws,
+                 size_t ws_bytes, cudaStream_t st);
 int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, void* op_ws, size_t op_bytes,
                 cudaStream_t st);
 int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws, const double* V,
@@ -206,6 +212,22 @@ size_t ofrr_residual_workspace2(int64_t rows, int64_t cols, int r, int a_fmt, in
 
 size_t ofrr_ozaki_operator_workspace(int64_t rows, int64_t cols) { return ozx_op_ws(rows, cols); }
 size_t ofrr_ozaki_workspace(int64_t rows, int64_t cols, int r) { return ozx_prod_ws(rows, cols, r); }
+size_t ofrr_orthonormalize_workspace(int64_t n, int k) { return gram_schmidt_ws(n, k); }
+int ofrr_orthonormalize(const void* X, int64_t n, int k, int64_t ldx, int storage, int compute, int accumulate,
+                        double drop_tol, int method, int reorth, void* Q, int64_t ldq, int* kept, int* n_kept,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  if (!valid_fmt(storage) || !valid_fmt(compute) || !valid_fmt(accumulate)) {
+    ofrr_set_error("orthonormalize: invalid format");
+    return OFRR_ERR_INVALID;
+  }
+  return gram_schmidt(X, n, k, ldx, storage, compute, accumulate, drop_tol, method, reorth, Q, ldq, kept, n_kept,
+                      workspace, workspace_bytes, S(stream));
+}
+int ofrr_gaussian_kernel(const double* px, int64_t n, const double* py, int64_t m, double f, double l, double s,
+                         void* out, int64_t ld, int out_fmt, void* stream) {
+  if (!valid_fmt(out_fmt)) { ofrr_set_error("gaussian_kernel: invalid format"); return OFRR_ERR_INVALID; }
+  return gaussian_kernel(px, n, py, m, f, l, s, out, ld, out_fmt, S(stream));
+}
 int ofrr_ozaki_operator_info(const void* op_ws, int64_t rows, int* full, long long* tails) {
   return ozx_info(op_ws, rows, full, tails);
 }

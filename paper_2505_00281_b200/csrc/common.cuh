@@ -7,6 +7,7 @@
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 #include <stdint.h>
+#include <atomic>
 #include "../../include/ofrr_b200.h"
 
 namespace ofrr {

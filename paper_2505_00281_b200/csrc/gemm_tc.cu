@@ -542,7 +542,7 @@ static int launch_tc_bn(const CUtensorMap& tA, const CUtensorMap& tX, const TcPl
                         uint32_t idesc, uint32_t idesc2, cudaStream_t st) {
   using C = TcCfg<BN, MH>;
   auto kern = k_gemm_av_tc<BN, FP8K, MH, CL>;
-  static bool attr_done = false;
+  static std::atomic<bool> attr_done{false};
   if (!attr_done) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_done = true;

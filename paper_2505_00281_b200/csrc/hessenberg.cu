@@ -634,7 +634,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
       if (need <= smem_max) { pb = b; shmem = need; break; }
     }
   }
-  static bool attr = false;
+  static std::atomic<bool> attr{false};   // set once; concurrent callers may both set it (idempotent)
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute((const void*)k_hessenberg<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_max));

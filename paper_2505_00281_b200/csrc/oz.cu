@@ -528,16 +528,34 @@ static constexpr int OZ_RS_THREADS = 512;    // k_oz_rowscale: one CTA per row, 
 
 // mantissa bits of the 16/8-bit formats: an entry with exponent e has no bit below 2^(e - MB)
 template <int FMT> __device__ __forceinline__ constexpr int oz_mant_bits() { return FMT == BF16 ? 7 : FMT == F16 ? 10 : 3; }
+// unbiased exponent of a non-negative 16-bit pattern (bf16 / f16); subnormals count as the
+// lowest normal exponent minus one (conservative for the candidate test)
+template <int FMT> __device__ __forceinline__ int oz_exp16(uint32_t p) {
+  if constexpr (FMT == BF16) return (int)(p >> 7) - 127;
+  else return (int)(p >> 10) - 15;
+}
+template <int FMT> __device__ __forceinline__ float oz_val16(uint32_t p) {
+  if constexpr (FMT == BF16) return __uint_as_float(p << 16);
+  else return __half2float(__ushort_as_half((unsigned short)p));
+}
 
+// Row scale T (|a| < 2^T), and the row's tails (see above).  Pass 1 reads the row once
+// (32 entries per thread step, four 16-byte loads in flight): the row maximum and, per
+// 32-entry group, the smallest non-zero magnitude -- as packed 16-bit SIMD max / min on the
+// bit patterns for bf16 / f16 (positive float patterns order like their values).  Pass 2
+// (warp 0 only) revisits just the groups whose smallest entry can hold bits below
+// 2^(T - 22): their indices are compacted in order from shared memory, then one lane per
+// candidate group re-reads its 32 entries and the tails are written in ascending column
+// order (warp scan of the per-group counts).
 template <int FMT>
 __global__ void __launch_bounds__(OZ_RS_THREADS)
     k_oz_rowscale(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, int* __restrict__ T,
                   int* __restrict__ full, int* __restrict__ tcnt, int* __restrict__ tcol, float* __restrict__ tval) {
   constexpr int NW = OZ_RS_THREADS / 32;
-  extern __shared__ int8_t gmin[];          // per 32-entry group: min exponent of its non-zero entries
+  constexpr bool P16 = FMT != FP8;
+  extern __shared__ int gsh[];               // per 32-entry group: smallest exponent (then: candidate list)
   const int64_t i = blockIdx.x;
   __shared__ uint32_t red[NW];
-  __shared__ int wsum[NW];
   if (i >= rows) {
     if (threadIdx.x == 0) {
       T[i] = 0;
@@ -549,34 +567,41 @@ __global__ void __launch_bounds__(OZ_RS_THREADS)
   const int eb = FMT == FP8 ? 1 : 2;
   const bool vec = ((reinterpret_cast<uintptr_t>(A) + (uintptr_t)(base * eb)) & 15) == 0;
   const int64_t step = 32 * (int64_t)OZ_RS_THREADS;
-  // pass 1: row maximum and, per group, the smallest exponent present (four 8-entry loads
-  // in flight per thread)
-  uint32_t m = 0;
+  const int64_t ngroups = (cols + 31) / 32;
+  uint32_t m = 0;                            // max |a| as f32 bits
   for (int64_t c0 = 0; c0 < cols; c0 += step) {
     const int64_t l0 = c0 + 32 * (int64_t)threadIdx.x;
-    float x[4][8];
+    if (l0 >= cols) continue;
+    int emin = 127;
+    if (P16 && vec && l0 + 32 <= cols) {
+      const uint4* src = reinterpret_cast<const uint4*>((const uint16_t*)A + base + l0);
+      uint4 w[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (l0 + 8 * u < cols) oz_ld8<FMT>(A, base, l0 + 8 * u, cols, vec, x[u]);
-      else {
+      for (int u = 0; u < 4; ++u) w[u] = __ldcs(src + u);
+      uint32_t vmax = 0u, vmin = 0xffffffffu;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[u][e] = 0.0f;
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t av = ww[q] & 0x7fff7fffu;
+          vmax = __vmaxu2(vmax, av);
+          vmin = __vminu2(vmin, av | __vcmpeq2(av, 0u));
+        }
       }
-    }
-    uint32_t emin = 255u;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const uint32_t bb = __float_as_uint(x[u][e]) & 0x7fffffffu;
+      const uint32_t pmax = max(vmax & 0xffffu, vmax >> 16);
+      const uint32_t pmin = min(vmin & 0xffffu, vmin >> 16);
+      const uint32_t fb = __float_as_uint(oz_val16<FMT>(pmax));
+      m = fb > m ? fb : m;
+      if (pmin != 0xffffu) emin = oz_exp16<FMT>(pmin);
+    } else {
+      for (int e = 0; e < 32 && l0 + e < cols; ++e) {
+        const uint32_t bb = __float_as_uint(oz_ld_f<FMT>(A, base + l0 + e)) & 0x7fffffffu;
         m = bb > m ? bb : m;
-        const uint32_t ef = bb ? (bb >> 23) : 255u;       // biased f32 exponent (0: subnormal)
-        emin = ef < emin ? ef : emin;
+        if (bb) emin = min(emin, bb >= 0x00800000u ? (int)(bb >> 23) - 127 : -127);
       }
-    if (tcnt && l0 < cols) {
-      const int eu = emin == 255u ? 127 : (emin == 0u ? -128 : (int)emin - 127);   // subnormal: conservative
-      gmin[l0 >> 5] = (int8_t)max(-128, min(127, eu));
     }
+    if (tcnt) gsh[l0 >> 5] = emin;
   }
   for (int o = 16; o > 0; o >>= 1) {
     const uint32_t om = __shfl_xor_sync(0xffffffffu, m, o);
@@ -584,78 +609,71 @@ __global__ void __launch_bounds__(OZ_RS_THREADS)
   }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
+  if (threadIdx.x >= 32) return;             // pass 2 is warp 0's
   m = red[0];
   for (int w = 1; w < NW; ++w) m = red[w] > m ? red[w] : m;
   const int E = oz_scale((double)__uint_as_float(m));
-  if (threadIdx.x == 0) T[i] = E;
+  const int lane = threadIdx.x;
+  if (lane == 0) T[i] = E;
   if (!tcnt) return;
-  // ---- pass 2: tails of the 3-digit heads, re-reading only the groups that can hold one
-  // (an entry with exponent e has bits below 2^(E - 22) only if e - MB < E - 22) ----
-  if (E == OZ_BAD) {                                   // non-finite row: its products are NaN anyway
-    if (threadIdx.x == 0) tcnt[i] = 0;
+  if (E == OZ_BAD) {                         // non-finite row: its products are NaN anyway
+    if (lane == 0) tcnt[i] = 0;
     return;
   }
   if (22 - E > 127 || 22 - E < -126 || E - 22 < -126) {   // scale outside the f32 conversion range
-    if (threadIdx.x == 0) { tcnt[i] = 0; atomicOr(full, 1); }
+    if (lane == 0) { tcnt[i] = 0; atomicOr(full, 1); }
     return;
   }
   const float sc = __int_as_float((22 - E + 127) << 23);      // 2^(22 - E)
   const float isc = __int_as_float((E - 22 + 127) << 23);     // 2^(E - 22)
-  const int ecut = E - 22 + oz_mant_bits<FMT>();              // candidate group: min exponent < ecut
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ecut = E - 22 + oz_mant_bits<FMT>();              // a group can hold a tail iff its min exponent < ecut
+  // ordered list of candidate groups, compacted in place (slot ncand <= g: no overlap)
+  int ncand = 0;
+  for (int64_t g0 = 0; g0 < ngroups; g0 += 32) {
+    const int64_t g = g0 + lane;
+    const bool c = g < ngroups && gsh[g] < ecut;
+    const uint32_t bal = __ballot_sync(0xffffffffu, c);
+    __syncwarp();
+    if (c) gsh[ncand + __popc(bal & ((1u << lane) - 1u))] = (int)g;
+    ncand += __popc(bal);
+    __syncwarp();
+  }
   int total = 0;
-  for (int64_t c0 = 0; c0 < cols; c0 += step) {
-    const int64_t l0 = c0 + 32 * (int64_t)threadIdx.x;
-    uint32_t mask = 0;                                 // bit 8u + e: entry l0 + 8u + e has a tail
-    float x[4][8];
-    if (l0 < cols && (int)gmin[l0 >> 5] < ecut) {
+  for (int c0 = 0; c0 < ncand; c0 += 32) {
+    uint32_t mask = 0;
+    int64_t l0 = 0;
+    float tl[32];
+    if (c0 + lane < ncand) {
+      l0 = (int64_t)gsh[c0 + lane] * 32;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (l0 + 8 * u < cols) oz_ld8<FMT>(A, base, l0 + 8 * u, cols, vec, x[u]);
-        else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[u][e] = 0.0f;
-        }
+      for (int e = 0; e < 32; ++e) {
+        const float x = l0 + e < cols ? oz_ld_f<FMT>(A, base + l0 + e) : 0.0f;
+        const int h = __float2int_rz(x * sc);
+        tl[e] = x - __int2float_rn(h) * isc;           // the tail (exact, see above)
+        mask |= (tl[e] != 0.0f ? 1u : 0u) << e;
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int h = __float2int_rz(x[u][e] * sc);
-          x[u][e] = x[u][e] - __int2float_rn(h) * isc;     // the tail (exact, see above)
-          mask |= (x[u][e] != 0.0f ? 1u : 0u) << (8 * u + e);
-        }
     }
     const int nt = __popc(mask);
-    int woff = 0, btot = 0, inc = nt;
-    if (__syncthreads_or(nt)) {                         // ordered block compaction (exclusive scan)
+    int inc = nt;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-      }
-      if (lane == 31) wsum[warp] = inc;
-      __syncthreads();
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    int pos = total + inc - nt;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        woff += w < warp ? wsum[w] : 0;
-        btot += wsum[w];
-      }
-      int pos = total + woff + inc - nt;
-      while (mask) {
-        const int b = __ffs(mask) - 1;
-        mask &= mask - 1;
+    for (int e = 0; e < 32; ++e) {
+      if ((mask >> e) & 1u) {
         if (pos < OZ_TAIL_CAP) {
-          tcol[i * OZ_TAIL_CAP + pos] = (int)(l0 + b);
-          tval[i * OZ_TAIL_CAP + pos] = x[b >> 3][b & 7];
+          tcol[i * OZ_TAIL_CAP + pos] = (int)(l0 + e);
+          tval[i * OZ_TAIL_CAP + pos] = tl[e];
         }
         ++pos;
       }
-      total += btot;
-      __syncthreads();                                 // wsum reused by the next chunk
     }
+    total += __shfl_sync(0xffffffffu, inc, 31);
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     tcnt[i] = total < OZ_TAIL_CAP ? total : OZ_TAIL_CAP;
     if (total > OZ_TAIL_CAP) atomicOr(full, 1);
   }
@@ -1254,7 +1272,7 @@ template <int BN>
 static int oz_launch(const CUtensorMap& tA, const CUtensorMap& tV, const OzPlan& p, double* ws, int col0,
                      cudaStream_t st) {
   using C = OzCfg<BN>;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};   // set once; concurrent callers may both set it (idempotent)
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_oz_gemm<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr = true;
@@ -1441,7 +1459,7 @@ int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fm
   int* tcol = (int*)(b + L.off_col);
   float* tval = (float*)(b + L.off_val);
   const int one = oz_no_tails() ? 1 : 0;
-  const size_t gbytes = (size_t)((cols + 31) / 32);     // per-group minimum exponents (pass 1 -> pass 2)
+  const size_t gbytes = (size_t)((cols + 31) / 32) * sizeof(int);   // per-group minimum exponents (pass 1 -> pass 2)
   if (gbytes > 48 * 1024) {
     static std::once_flag big;
     cudaError_t e = cudaSuccess;

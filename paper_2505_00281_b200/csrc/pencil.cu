@@ -1034,7 +1034,7 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
   double* tnrm = tri + 3 * k;
   const size_t shm = (size_t)k * (k | 1) * sizeof(double);
   const size_t shm_e = (kk + 2 * (size_t)pc_epb(k) * k) * sizeof(double);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};   // set once; concurrent callers may both set it (idempotent)
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)((size_t)PK_MAX * (PK_MAX | 1) * sizeof(double))));

@@ -454,7 +454,7 @@ static int launch_resid_dmma(const void* A, int64_t lda, int64_t m, int64_t K, c
                              const double* Y, int64_t ldy, const double* vals, const int* r_dev, double* part,
                              cudaStream_t st) {
   const size_t shm = (size_t)2 * (DBM + DBN) * DLK * sizeof(double);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};   // set once; concurrent callers may both set it (idempotent)
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_resid_dmma<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     attr = true;
@@ -470,7 +470,7 @@ static int launch_resid64(const void* A, int64_t lda, int64_t m, int64_t K, cons
                           const double* Y, int64_t ldy, const double* vals, const int* r_dev, double* part,
                           cudaStream_t st) {
   const size_t shm = (size_t)2 * RBK * ((RBM + 1) + (RBN + 1)) * sizeof(double);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};   // set once; concurrent callers may both set it (idempotent)
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_resid64<TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     attr = true;

@@ -722,7 +722,7 @@ int small_eig(int mode, const double* A, const double* M, int k, double raw_tol,
   const size_t budget = 160 * 1024;
   int nsm = one ? (int)std::min<size_t>(4, budget / one) : 0;
   const size_t shm = (size_t)nsm * one;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};   // set once; concurrent callers may both set it (idempotent)
   if (!attr) {
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_small_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;

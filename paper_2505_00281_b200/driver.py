@@ -20,6 +20,7 @@ results).  See DESIGN.md section "Multi-GPU".
 from __future__ import annotations
 
 import math
+import threading
 import time
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -28,7 +29,7 @@ from typing import Optional
 import numpy as np
 
 from . import ops as _ops
-from .basis import BasisMethod, HESSENBERG_METHODS, KRYLOV_METHODS
+from .basis import BasisMethod, GRAM_SCHMIDT_METHODS, HESSENBERG_METHODS, KRYLOV_METHODS
 from .comm import Comm
 from .errors import ConvergenceError, EmptyBasisError, EmptyPencilError, OverflowDiagnostic
 from .matrix import DenseMatrix
@@ -95,13 +96,12 @@ def operator_for(a: DenseMatrix, block_fmt: FpFormat):
 
 
 def _require_ofrr_path(cfg: IterConfig, what: str) -> None:
+    """Block basis methods only: Hessenberg (the OFRR path) or Gram-Schmidt (the classical
+    comparators), with projection 'ofrr' or 'rr' (ofrr/driver.py:52-58)."""
     if cfg.basis_method in KRYLOV_METHODS:
         raise ValueError(f"{what} needs a block basis method")
-    if cfg.basis_method not in HESSENBERG_METHODS or cfg.projection != "ofrr":
-        raise ValueError(
-            f"the B200 path runs basis_method in (hess-l, hess-r) with projection='ofrr'; got "
-            f"{cfg.basis_method.value!r} / {cfg.projection!r} (the Gram-Schmidt / classical RR "
-            "baselines are CPU-reference only)")
+    if cfg.basis_method not in HESSENBERG_METHODS and cfg.basis_method not in GRAM_SCHMIDT_METHODS:
+        raise ValueError(f"{cfg.basis_method.value!r} is not a block basis method")
 
 
 @dataclass
@@ -124,6 +124,11 @@ S_MV_FLAGS, S_NKEPT, S_EIG_STATUS, S_NOUT, S_GRAM_FLAGS, S_RESTART_FLAGS, S_NKEP
 # so a new operator at the same address replays correctly.
 _GRAPH_MAX = 8
 _GRAPHS = OrderedDict()
+# Concurrent callers (the reference CLI runs cells from a thread pool, ofrr/cli.py:399-401):
+# solves on the device are serialised by this lock, which also guards the graph caches, the
+# launch accounting and the Ozaki workspaces; a solve runs on the calling thread's current
+# stream.
+_SOLVE_LOCK = threading.RLock()
 DEVICE_LOOP = True      # the whole solve as one graph launch (csrc/loop.cu) once its graphs exist
 _WARM = set()
 _NO_GRAPH = set()
@@ -310,8 +315,13 @@ class EigEngine:
         return X
 
     def basis(self, X, st):
-        """Hessenberg basis (K3), redundant on every rank."""
-        h = self.ops.hessenberg(X, self.pol.storage, self.pol.compute, self.pol.drop_tol)
+        """Hessenberg basis (K3), or a Gram-Schmidt comparator (csrc/gs.cu); redundant on
+        every rank."""
+        if self.cfg.basis_method in GRAM_SCHMIDT_METHODS:
+            h = self.ops.orthonormalize(X, self.cfg.basis_method.value, self.pol.storage, self.pol.compute,
+                                        self.pol.accumulate, self.pol.drop_tol)
+        else:
+            h = self.ops.hessenberg(X, self.pol.storage, self.pol.compute, self.pol.drop_tol)
         st[S_NKEPT:S_NKEPT + 1].copy_(h.n_kept)
         return h
 
@@ -332,14 +342,15 @@ class EigEngine:
                     **({"oz": self._block_oz(self.A_pol, U)} if self.ops is _ops else {}))
         self.stats.a_passes += 1
         Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U
+        classical = self.cfg.projection == "rr"       # rr_eig (ofrr/projection.py:64-72): no mass matrix
         if comm.distributed:
             B, _ = ops.gram(Ul, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], want_m=False)
             comm.all_reduce_sum_(B)
-            _, M = ops.gram(U, None, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+            M = None if classical else ops.gram(U, None, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])[1]
         else:
-            B, M = ops.gram(U, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+            B, M = ops.gram(U, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], want_m=not classical)
         side = self._fork_res_scales()
-        eig = ops.sym_def_gen_eig(B, M, kp)
+        eig = ops.sym_eig(B, kp) if classical else ops.sym_def_gen_eig(B, M, kp)
         st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
         st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
         U64, Xn = ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=want64, x_fmt=self.mv.storage,
@@ -833,7 +844,13 @@ def subspace_iter_eig(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats]
     (ofrr/driver.py:84-111), on the device.
 
     ``a``: the operator (host DenseMatrix uploaded once; or device resident).  In a
-    row-partitioned run ``a`` holds this rank's rows and ``n_global`` the full n."""
+    row-partitioned run ``a`` holds this rank's rows and ``n_global`` the full n.
+    Thread-safe: concurrent calls are serialised on the device (_SOLVE_LOCK)."""
+    with _SOLVE_LOCK:
+        return _subspace_iter_eig(a, cfg, stats, comm, n_global)
+
+
+def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
     _require_ofrr_path(cfg, "subspace iteration")
     n = int(n_global if n_global is not None else a.rows)
     if cfg.k > n:
@@ -895,6 +912,14 @@ class SvdEngine:
     def single(cls, a, pol, mv):
         return cls(a, pol, mv)
 
+    def basis(self, X, cfg):
+        """Hessenberg basis (K3), or a Gram-Schmidt comparator (csrc/gs.cu)."""
+        pol = self.pol
+        if cfg.basis_method in GRAM_SCHMIDT_METHODS:
+            return self.ops.orthonormalize(X, cfg.basis_method.value, pol.storage, pol.compute, pol.accumulate,
+                                           pol.drop_tol)
+        return self.ops.hessenberg(X, pol.storage, pol.compute, pol.drop_tol)
+
     def matvec(self, op, X, st):
         import torch
         colmax = torch.zeros(X.k, dtype=torch.float64, device=self.device)
@@ -904,8 +929,9 @@ class SvdEngine:
         self.ops.scale_columns(W, colmax, self.mv.compute)
         return W
 
-    def project(self, U, V, want64: bool = True, x_fmt=None):
-        """ofrr_svd on device blocks U (n1 x k1), V (n2 x k2) in policy storage."""
+    def project(self, U, V, want64: bool = True, x_fmt=None, classical: bool = False):
+        """ofrr_svd on device blocks U (n1 x k1), V (n2 x k2) in policy storage; with
+        ``classical`` rr_svd (ofrr/projection.py:90-96): identity mass matrices."""
         import torch
         ops = self.ops
         k1, k2 = U.k, V.k
@@ -922,8 +948,11 @@ class SvdEngine:
         Gk = G[:k2, :k1]                 # column j (< k2) of G = U^T W -> row j
         Bm[k1:, :k1].copy_(Gk)           # columns k1.. of B hold G (rows 0..k1)
         Bm[:k1, k1:].copy_(Gk.t())       # columns 0..k1 of B hold G^T (rows k1..)
-        Mm[:k1, :k1].copy_((Mu + Mu.t()) / 2.0)
-        Mm[k1:, k1:].copy_((Mv + Mv.t()) / 2.0)
+        if classical:
+            Mm.fill_diagonal_(1.0)
+        else:
+            Mm[:k1, :k1].copy_((Mu + Mu.t()) / 2.0)
+            Mm[k1:, k1:].copy_((Mv + Mv.t()) / 2.0)
         eig = ops.sym_def_gen_eig(Bm, Mm, kk)
         st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
         st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
@@ -957,9 +986,21 @@ class SvdEngine:
 
 
 def subspace_iter_svd(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats] = None) -> RitzSet:
-    """Alternating subspace iteration for the SVD (ofrr/driver.py:141-173), on device."""
+    """Alternating subspace iteration for the SVD (ofrr/driver.py:141-173), on device
+    (thread-safe like subspace_iter_eig)."""
+    with _SOLVE_LOCK:
+        return _subspace_iter_svd(a, cfg, stats)
+
+
+def _subspace_iter_svd(a, cfg, stats) -> RitzSet:
+    """The SVD outer loop.  With cfg.tol the loop stops at the first outer iteration whose
+    leading ``top`` triplets have FP64 residuals max(||A v - s u||, ||A^T u - s v||) / s below
+    tol (``m`` is the cap); otherwise exactly m iterations (the reference).  ladder / reuse_av
+    are eigenvalue-path extensions and are rejected here."""
     from .projection import residual_report
     _require_ofrr_path(cfg, "SVD iteration")
+    if cfg.ladder is not None or cfg.reuse_av:
+        raise ValueError("subspace_iter_svd: ladder / reuse_av apply to subspace_iter_eig only")
     n1, n2 = a.rows, a.cols
     if cfg.k > min(n1, n2):
         raise ValueError("k exceeds min(n1, n2)")
@@ -968,15 +1009,19 @@ def subspace_iter_svd(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats]
     ops = eng.ops
     V = ops.start_block(cfg.seed, n2, cfg.k, mv.storage, eng.device)
     rs = None
+    checked = None
+    tol, top = cfg.tol, (cfg.top or cfg.k)
+    hist = []
+    converged = False
     import torch
-    for _ in range(cfg.m):
+    its = 0
+    for it in range(cfg.m):
         st = torch.zeros(8, dtype=torch.int32, device=eng.device)
         U = V
         for _ in range(cfg.iter):
             U = eng.matvec(eng.A_mv, V, st)
             V = eng.matvec(eng.At_mv, U, st)
-        hu = ops.hessenberg(U, pol.storage, pol.compute, pol.drop_tol)
-        hv = ops.hessenberg(V, pol.storage, pol.compute, pol.drop_tol)
+        hu, hv = eng.basis(U, cfg), eng.basis(V, cfg)
         st[S_NKEPT:S_NKEPT + 1].copy_(hu.n_kept)
         st[S_NKEPT2:S_NKEPT2 + 1].copy_(hv.n_kept)
         s = st.cpu().numpy()
@@ -984,14 +1029,36 @@ def subspace_iter_svd(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats]
             raise OverflowDiagnostic("non-finite entries after MatVec")
         k1, k2 = int(s[S_NKEPT]), int(s[S_NKEPT2])
         if k1 == 0 or k2 == 0:
-            raise EmptyBasisError("all columns skipped in Hessenberg process")
-        rs, Vx, st2 = eng.project(hu.Q.narrow(k1), hv.Q.narrow(k2), x_fmt=mv.storage)
+            raise EmptyBasisError("all columns skipped in basis construction")
+        rs, Vx, st2 = eng.project(hu.Q.narrow(k1), hv.Q.narrow(k2), x_fmt=mv.storage,
+                                  classical=cfg.projection == "rr")
         if Vx is None:
             raise EmptyPencilError("no positive eigenvalues in the SVD pencil")
         if int(st2[S_RESTART_FLAGS].item()) & 1:
             raise OverflowDiagnostic("non-finite entries after projection")
         V = Vx
+        its = it + 1
+        if tol is not None:
+            # FP64 confirmation on the leading triplets (two FP64-accurate products, K7z)
+            from dataclasses import replace as _rep
+            t = min(top, len(rs.values))
+            head = _rep(rs, values=rs.values[:t], vectors=_narrow_dm(rs.vectors, t),
+                        right_vectors=_narrow_dm(rs.right_vectors, t))
+            checked = residual_report(a, head)
+            worst = float(np.max(checked.residuals)) if t >= top else float("inf")
+            hist.append((its, worst))
+            if worst < tol:
+                converged = True
+                break
     if stats is not None:
-        stats.iterations = cfg.m
+        stats.iterations = its
         stats.a_passes = eng.a_passes
+        stats.history = hist
+        stats.converged = converged
     return residual_report(a, rs)
+
+
+def _narrow_dm(m: DenseMatrix, t: int) -> DenseMatrix:
+    """The first t columns of a device-resident block DenseMatrix."""
+    blk = m.device_block(FpFormat.F64)
+    return DenseMatrix.from_block(blk.narrow(t))

@@ -32,7 +32,14 @@ LAUNCHES = [0]
 GEMM_LOG = None
 
 
-_RECORDER = None   # a Recorder while a CUDA graph is being captured
+import threading
+
+_TLS = threading.local()          # .recorder: the Recorder of the graph this thread is capturing
+_ACCT = threading.Lock()          # LAUNCHES / GEMM_LOG updates from concurrent callers
+
+
+def _recorder():
+    return getattr(_TLS, "recorder", None)
 
 
 class Recorder:
@@ -43,33 +50,36 @@ class Recorder:
         self.gemm = []
 
     def __enter__(self):
-        global _RECORDER
-        self._prev = _RECORDER
-        _RECORDER = self
+        self._prev = _recorder()
+        _TLS.recorder = self
         return self
 
     def __exit__(self, *exc):
-        global _RECORDER
-        _RECORDER = self._prev
+        _TLS.recorder = self._prev
         return False
 
     def replayed(self) -> None:
-        LAUNCHES[0] += self.launches
-        if GEMM_LOG is not None:
-            GEMM_LOG.extend(self.gemm)
+        with _ACCT:
+            LAUNCHES[0] += self.launches
+            if GEMM_LOG is not None:
+                GEMM_LOG.extend(self.gemm)
 
 
 def _count(n: int) -> None:
-    LAUNCHES[0] += n
-    if _RECORDER is not None:
-        _RECORDER.launches += n
+    with _ACCT:
+        LAUNCHES[0] += n
+    rec = _recorder()
+    if rec is not None:
+        rec.launches += n
 
 
 def _log_gemm(entry) -> None:
-    if GEMM_LOG is not None:
-        GEMM_LOG.append(entry)
-    if _RECORDER is not None:
-        _RECORDER.gemm.append(entry)
+    with _ACCT:
+        if GEMM_LOG is not None:
+            GEMM_LOG.append(entry)
+    rec = _recorder()
+    if rec is not None:
+        rec.gemm.append(entry)
 
 
 def pad_ld(n: int) -> int:
@@ -408,6 +418,30 @@ def hessenberg(X: DevBlock, storage: FpFormat, compute: FpFormat, tol: float) ->
     return HessOut(Q, piv, kept, nk)
 
 
+# Gram-Schmidt comparators: ofrr/basis.py:65-148 on the device
+GS_METHODS = {"mgs-l": 0, "mgs-r": 1, "cgs": 2, "cgs2": 3}
+
+
+def orthonormalize(X: DevBlock, method: str, storage: FpFormat, compute: FpFormat, accumulate: FpFormat,
+                   drop_tol: float, reorth: bool = True) -> HessOut:
+    """Gram-Schmidt basis of X (kept columns first; pivots empty)."""
+    L = _lib.load()
+    dev = X.device
+    if FpFormat(storage) != X.fmt:
+        Xs = new_block(X.n, X.k, storage, dev)
+        convert(X, Xs)
+        X = Xs
+    Q = new_block(X.n, X.k, storage, dev)
+    piv, kept, nk = _zeros_pack(dev, ((1,), torch.int64), ((max(X.k, 1),), torch.int32), ((1,), torch.int32))
+    ws = _ws(L.ofrr_orthonormalize_workspace(X.n, X.k), dev)
+    _lib.check(L.ofrr_orthonormalize(X.ptr, X.n, X.k, X.ld, int(storage), int(compute), int(accumulate),
+                                     float(drop_tol), GS_METHODS[method], int(bool(reorth)), Q.ptr, Q.ld,
+                                     kept.data_ptr(), nk.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),
+               "orthonormalize")
+    _count(1)
+    return HessOut(Q, piv[:0], kept, nk)
+
+
 # ---------------------------------------------------------------------------------
 # K4
 # ---------------------------------------------------------------------------------
@@ -467,6 +501,7 @@ def sym_eig(S: torch.Tensor, k: int) -> EigOut:
     _lib.check(L.ofrr_sym_eig(S.data_ptr(), k, vals.data_ptr(), vecs.data_ptr(), status.data_ptr(), ws.data_ptr(),
                               ws.numel(), _stream()), "sym_eig")
     n_out = torch.full((1,), k, dtype=torch.int32, device=dev)
+    _count(1)
     return EigOut(vals, vecs, n_out, status)
 
 

@@ -1,9 +1,9 @@
 """Orthogonalization-free Rayleigh-Ritz projections on the device + FP64 residuals.
 
 Same names and contracts as ofrr/projection.py:21-158 (``ofrr_eig``, ``ofrr_svd``,
-``residual_report``, ``RitzSet``, ``projection_policy``, the error classes).  The
-classical ``rr_eig`` / ``rr_svd`` baselines need an orthonormal (QR) basis and are not
-part of this path.
+``residual_report``, ``RitzSet``, ``projection_policy``, the error classes), plus the
+classical ``rr_eig`` / ``rr_svd`` comparators (ofrr/projection.py:64-96) for bases from the
+Gram-Schmidt builders.
 
 Per ofrr_eig call: W = A U (K1, tensor cores for 16/8-bit storage), the projected
 matrices B = U^T W and M = U^T U (K4, fp64 sums), the symmetric-definite pencil solve
@@ -75,6 +75,40 @@ def ofrr_eig(a: DenseMatrix, u: DenseMatrix, policy: PrecisionPolicy) -> RitzSet
     return RitzSet(vals, DenseMatrix.from_block(U64.narrow(r)), "eig")
 
 
+def rr_eig(a: DenseMatrix, q: DenseMatrix, policy: PrecisionPolicy) -> RitzSet:
+    """ofrr/projection.py:64-72: classical Rayleigh-Ritz, eig of Q'AQ (Q intended-orthonormal,
+    deliberately unchecked) and the vectors Q Y in FP64."""
+    import torch
+    from . import ops
+    A = a.device_operator(policy.storage)
+    Q = q.device_block(policy.storage)
+    k = Q.k
+    _, out_fmt = projection_policy(policy)
+    st = torch.zeros(8, dtype=torch.int32, device=A.device)
+    W = ops.new_block(A.rows, k, policy.storage, A.device)
+    ops.gemm_av(A, Q, W, flags=st[0:1])
+    B, _ = ops.gram(Q, W, out_fmt, flags=st[1:2], want_m=False)
+    eig = ops.sym_eig(B, k)
+    st[2:3].copy_(eig.status)
+    U64, _ = ops.ritz(Q, eig.vectors, k, None, k, 1.0, want64=True)
+    s = st.cpu().numpy()
+    if s[0] & 1:
+        raise OverflowDiagnostic("non-finite entries in projected matrix")
+    _status(s, 2, 1, "projected matrix")
+    return RitzSet(eig.values[:k].cpu().numpy(), DenseMatrix.from_block(U64.narrow(k)), "eig")
+
+
+def rr_svd(a: DenseMatrix, u: DenseMatrix, v: DenseMatrix, policy: PrecisionPolicy) -> RitzSet:
+    """ofrr/projection.py:90-96: classical two-sided Rayleigh-Ritz, the SVD of U'AV -- taken
+    from the symmetric eigenproblem of [[0, U'AV], [(U'AV)', 0]] (the ofrr_svd block pencil
+    with identity mass matrices), singular vectors sqrt(2)-scaled."""
+    from . import driver
+    eng = driver.SvdEngine.single(a, policy, policy)
+    U = u.device_block(policy.storage)
+    V = v.device_block(policy.storage)
+    return eng.project(U, V, want64=True, classical=True)[0]
+
+
 def ofrr_svd(a: DenseMatrix, u: DenseMatrix, v: DenseMatrix, policy: PrecisionPolicy) -> RitzSet:
     """ofrr/projection.py:99-133: block pencil [[0, U'AV], [(U'AV)', 0]] vs
     diag(U'U, V'V); the eigenvalues above POSITIVE_EIG_TOL of the largest are the
@@ -109,5 +143,5 @@ def residual_report(a: DenseMatrix, rs: RitzSet) -> RitzSet:
     return replace(rs, residuals=res[:r].cpu().numpy())
 
 
-__all__ = ["RitzSet", "ofrr_eig", "ofrr_svd", "residual_report", "projection_policy", "POSITIVE_EIG_TOL",
+__all__ = ["RitzSet", "ofrr_eig", "ofrr_svd", "rr_eig", "rr_svd", "residual_report", "projection_policy", "POSITIVE_EIG_TOL",
            "OverflowDiagnostic", "EmptyPencilError", "to_dense_f64"]

@@ -10,14 +10,20 @@ pytestmark = pytest.mark.gpu
 SEED = 20240901
 
 
-def _criteria(vals, res, ref_vals, ref_res, exact, top):
+def _criteria(vals, res, ref_vals, ref_res, exact, top, per_pair=False):
     """North-star parity: Ritz values within max(10 x the reference's error vs exact,
-    1e-6 relative) and residuals within 2 x the reference's.  "The reference's error"
-    is its error level over the checked pairs (max over the top pairs): with 16-bit
-    storage a single pair's error is a rounding lottery between eps-sized outcomes, so a
-    per-pair 10x bound would test luck, not parity."""
+    1e-6 relative) and residuals within 2 x the reference's.
+
+    ``per_pair`` (fp32 / fp64 bases): every pair on its own.  Otherwise (16-bit storage) the
+    reference's error level over the checked pairs (max over the top pairs): a single pair's
+    error is a rounding lottery between eps-sized outcomes there, so a per-pair 10x bound
+    would test luck, not parity."""
     ref_err = np.abs(ref_vals[:top] - exact[:top]) / np.abs(exact[:top])
     err = np.abs(vals[:top] - exact[:top]) / np.abs(exact[:top])
+    if per_pair:
+        assert np.all(err <= np.maximum(10 * ref_err, 1e-6)), (err, ref_err)
+        assert np.all(res[:top] <= 2 * ref_res[:top] + 1e-13), (res[:top], ref_res[:top])
+        return
     assert np.max(err) <= max(10 * np.max(ref_err), 1e-6), (err, ref_err)
     assert np.max(res[:top]) <= 2 * np.max(ref_res[:top]) + 1e-13, (res[:top], ref_res[:top])
 
@@ -34,7 +40,8 @@ def test_driver_eig_vs_reference_golden(ofrr_gpu, golden, pname, method):
     rs = p.subspace_iter_eig(a, cfg)
     exact = golden["driver_eig/exact"] if pname == "full-f64" else \
         np.sort(np.linalg.eigvalsh(golden[key + "/a"]))[::-1]
-    _criteria(rs.values, rs.residuals, golden[key + "/vals"], golden[key + "/res"], exact, 6)
+    _criteria(rs.values, rs.residuals, golden[key + "/vals"], golden[key + "/res"], exact, 6,
+              per_pair=pname in ("full-f64", "full-f32"))
     assert rs.vectors.data.shape == golden[key + "/vecs"].shape
 
 
@@ -59,7 +66,7 @@ def test_driver_svd_vs_reference_golden(ofrr_gpu, golden, pname):
                        policy=p.POLICY_PRESETS[pname], seed=9)
     rs = p.subspace_iter_svd(a, cfg)
     exact = np.linalg.svd(golden[key + "/a"], compute_uv=False)
-    _criteria(rs.values, rs.residuals, golden[key + "/vals"], golden[key + "/res"], exact, 5)
+    _criteria(rs.values, rs.residuals, golden[key + "/vals"], golden[key + "/res"], exact, 5, per_pair=True)
 
 
 def test_ofrr_eig_known_answers(ofrr_gpu, golden):
@@ -114,7 +121,7 @@ def test_driver_eig_vs_oracle_geometric(ofrr_gpu, oracle, fmt):
     rs = p.subspace_iter_eig(A, cfg)
     ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=o.as_pol(pol), seed=SEED)
     exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
-    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top, per_pair=fmt == "full-f32")
 
 
 def test_driver_eig_c1_fp32(ofrr_gpu, oracle):
@@ -128,7 +135,7 @@ def test_driver_eig_c1_fp32(ofrr_gpu, oracle):
     rs = p.subspace_iter_eig(p.DenseMatrix(a_host, p.FpFormat.F32), cfg)
     ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=o.FULL_F32, seed=SEED)
     exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
-    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top, per_pair=True)
 
 
 def test_driver_eig_tolerance_stop(ofrr_gpu):
@@ -160,7 +167,7 @@ def test_driver_eig_fp32_basis_on_bf16_operator(ofrr_gpu, oracle):
     rs = p.subspace_iter_eig(A, cfg)
     ref = o.subspace_iter_eig(a_host, k=k, m=m, iters=1, pol=o.FULL_F32, seed=SEED)
     exact = np.sort(np.linalg.eigvalsh(a_host))[::-1]
-    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top)
+    _criteria(rs.values, rs.residuals, ref.values, ref.residuals, exact, top, per_pair=True)
     assert np.max(rs.residuals[:top]) < 1e-4
 
 

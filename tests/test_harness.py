@@ -86,15 +86,15 @@ def test_unsupported_experiment_raises():
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["harness_eig", "harness_svd"])
 def test_harness_rows_vs_reference_harness(ofrr_gpu, name):
-    """Every OFRR cell of the reference's own run: same rows (keys, order, status), the
-    north-star value / residual criteria per cell; the classical-RR cell is an ``error``
-    row (no CPU fallback)."""
+    """Every cell of the reference's own run -- the OFRR cells and the classical comparator
+    (Gram-Schmidt basis + classical RR, csrc/gs.cu): same rows (keys, order, status), the
+    north-star value / residual criteria per cell."""
     h = _h()
     spec = h.parse_spec_file(os.path.join(GOLD, name + ".cfg"))
     ours = h.run_experiment(spec)
     ref = _ref_rows(name)
-    ours_ok = [r for r in ours if r["projection"] == "ofrr"]
-    ref_ok = [r for r in ref if r["projection"] == "ofrr"]
+    ours_ok = list(ours)
+    ref_ok = list(ref)
     key = lambda r: (r["matrix"], r["policy"], r["basis_method"], r["projection"], str(r["index"]))  # noqa: E731
     assert [key(r) for r in ours_ok] == [key(r) for r in ref_ok]
     # per cell, the north-star criteria with the reading of tests/test_gpu_driver.py::
@@ -113,7 +113,33 @@ def test_harness_rows_vs_reference_harness(ofrr_gpu, name):
     for cell, (oe, re_, orr, rr) in cells.items():
         assert oe <= max(10 * re_, 1e-6), (cell, oe, re_)
         assert orr <= 2 * rr + 1e-13, (cell, orr, rr)
-    classical = [r for r in ours if r["projection"] == "rr"]
-    assert all(r["status"] == "error" for r in classical)
     text = h.format_results(ours, "csv")
     assert text.splitlines()[0].split(",") == h.CSV_COLUMNS
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["harness_eig", "harness_svd"])
+def test_device_kernel_generator_matches_host(ofrr_gpu, name):
+    """csrc/gen.cu evaluates the reference's kernel formula in the reference's operation order:
+    every entry within 1 ulp of the host FP64 matrix (CUDA's exp vs libm's), most bitwise."""
+    h = _h()
+    spec = h.parse_spec_file(os.path.join(GOLD, name + ".cfg"))
+    ks = h.kernel_spec(spec)
+    host = h.kernel_host(ks)
+    dev = h.kernel_operator(ks)
+    op = dev.device_operator()
+    got = op.t[:, :op.cols].cpu().numpy()
+    ulp = np.spacing(np.abs(host))
+    assert np.all(np.abs(got - host) <= ulp), np.max(np.abs(got - host) / ulp)
+    assert np.mean(got == host) > 0.99
+
+
+@pytest.mark.gpu
+def test_threaded_cells_equal_serial(ofrr_gpu):
+    """--threads: cells from a thread pool (ofrr/cli.py:399-401) give the serial rows."""
+    h = _h()
+    spec = h.parse_spec_file(os.path.join(GOLD, "harness_eig.cfg"))
+    serial = h.run_experiment(spec)
+    threaded = h.run_experiment(spec, threads=4)
+    strip = lambda rows: [{c: r[c] for c in h.CSV_COLUMNS if c != "wall_ms"} for r in rows]  # noqa: E731
+    assert strip(serial) == strip(threaded)

@@ -112,14 +112,17 @@ def test_driver_rejects_non_ofrr_paths_before_touching_the_gpu():
     a = p.DenseMatrix(np.eye(4), p.FpFormat.F64)
     with pytest.raises(ValueError):   # Krylov builders: ofrr/driver.py:92-93
         p.subspace_iter_eig(a, p.IterConfig(k=2, basis_method=p.BasisMethod.ARNOLDI_MGS, policy=p.FULL_F64))
-    with pytest.raises(ValueError):   # Gram-Schmidt + classical RR: CPU-reference baselines only
-        p.subspace_iter_eig(a, p.IterConfig(k=2, policy=p.FULL_F64))
+    with pytest.raises(ValueError):   # Krylov builders are not block builders for the SVD either
+        p.subspace_iter_svd(a, p.IterConfig(k=2, basis_method=p.BasisMethod.KRYLOV_HESS, policy=p.FULL_F64))
+    with pytest.raises(ValueError):   # the eig-path extensions are rejected by the SVD driver
+        p.subspace_iter_svd(a, p.IterConfig(k=2, basis_method=p.BasisMethod.HESS_LEFT, policy=p.FULL_F64,
+                                            tol=1e-6, ladder=p.FULL_F32))
     with pytest.raises(ValueError):   # k > n: ofrr/driver.py:94-96
         p.subspace_iter_eig(p.DenseMatrix(np.eye(3), p.FpFormat.F64),
                             p.IterConfig(k=5, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
                                          policy=p.FULL_F64))
     with pytest.raises(ValueError):
-        p.build_basis(a, p.BasisMethod.MGS_LEFT, p.FULL_F64)
+        p.build_basis(a, p.BasisMethod.ARNOLDI_MGS, p.FULL_F64)
 
 
 def test_projection_policy_rule():
