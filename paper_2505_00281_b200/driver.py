@@ -413,14 +413,18 @@ class EigEngine:
         return res.cpu().numpy()
 
     # ---- the outer loop -----------------------------------------------------------------
-    def run(self, X0=None, stop_estimate: Optional[float] = None):
+    def run(self, X0=None, stop_estimate: Optional[float] = None, stepped: bool = False):
         """The outer loop (ofrr/driver.py:101-111).  With cfg.tol the loop stops at the
         first iteration whose leading `top` residuals pass: the cheap estimate (K7e)
         nominates, the FP64 residual report (K7) confirms; the returned residuals are
         always the FP64 ones.
 
         Ladder rung (``stop_estimate``): return the restart block (no report) as soon as
-        the estimate falls below ``stop_estimate`` or stalls; ``X0`` starts from a block."""
+        the estimate falls below ``stop_estimate`` or stalls; ``X0`` starts from a block.
+        With A-pass reuse the rung hands over the NEXT iterate (its MatVec W Y, already made)
+        in ``self.handover`` and the next rung starts with ``stepped=True``: its first
+        iteration skips the power step (one FP64-accurate A pass fewer per ladder solve)."""
+        self.stepped = bool(stepped)
         cfg = self.cfg
         tol, top = cfg.tol, (cfg.top or cfg.k)
         check = tol is not None
@@ -455,7 +459,7 @@ class EigEngine:
             # one iteration: power step(s), Hessenberg basis, projection with every column
             # (the basis keeps all k in the common case; dropped columns of Q are zero),
             # residual estimate -- replayed as one CUDA graph when possible.  One host sync.
-            first = it == 0
+            first = it == 0 and not self.stepped
             with _ph("graph_step"):
                 out = self._graph_step(X, check, top, first) if use_graph and X.k == cfg.k else None
             if out is None:
@@ -500,6 +504,7 @@ class EigEngine:
                     prev_est = worst
                     self.stats.history.append((it + 1, worst))
                     if rung_done and not last:
+                        self.handover = X if cfg.reuse_av else None    # the next iterate, power step made
                         return Xrestart                            # next rung starts from here
                     continue
                 prev_est = worst
@@ -533,7 +538,7 @@ class EigEngine:
         cfg = self.cfg
         L = _lib.load()
         self._refresh_now = True
-        kf = self._graph_key(True, top, True)
+        kf = self._graph_key(True, top, not self.stepped)
         self._refresh_now = False
         ks = self._graph_key(True, top, False)
         gf, gs = _GRAPHS.get(kf), _GRAPHS.get(ks)
@@ -856,6 +861,7 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
     if cfg.k > n:
         raise ValueError("k exceeds the operator dimension")
     X0 = None
+    stepped = False
     hist, iters, passes = [], 0, 0
     if cfg.ladder is not None:
         # precision ladder: run the cheaper policy while it makes
@@ -865,6 +871,9 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
         with _ph("rung_low"):
             eng0 = EigEngine(a, low, comm=comm, n_global=n, report_scales=False)
             X0 = eng0.run(stop_estimate=cfg.ladder_switch)
+            stepped = getattr(eng0, "handover", None) is not None
+            if stepped:
+                X0 = eng0.handover
         if isinstance(X0, RitzSet):                                # m exhausted in the low rung
             if stats is not None:
                 stats.__dict__.update(eng0.stats.__dict__)
@@ -874,7 +883,7 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
         cfg = _replace(cfg, ladder=None, m=max(1, cfg.m - iters))
     with _ph("rung_main"):
         eng = EigEngine(a, cfg, comm=comm, n_global=n)
-        rs = eng.run(X0=X0)
+        rs = eng.run(X0=X0, stepped=X0 is not None and stepped)
     if stats is not None:
         stats.__dict__.update(eng.stats.__dict__)
         stats.rungs = ([(cfg_rung_label(low), iters, passes)] if X0 is not None else []) + \

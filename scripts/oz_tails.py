@@ -47,6 +47,8 @@ for _ in range(3):
 e1.record()
 torch.cuda.synchronize()
 print(f"prepare (row scales + tails): {e0.elapsed_time(e1) / 3:.3f} ms")
+if os.environ.get("OZT_NO_PROF"):
+    sys.exit(0)
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(3):
