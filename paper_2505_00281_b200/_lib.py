@@ -114,6 +114,8 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    # A/B experiments only: another build of the same library (scripts/)
+    path = os.environ.get("OFRR_LIB_OVERRIDE", path)
     with _lock:
         if _lib is not None:
             return _lib

@@ -26,7 +26,10 @@ namespace cg = cooperative_groups;
 
 namespace ofrr {
 
-static constexpr int HT = 256;
+#ifndef OFRR_HESS_THREADS
+#define OFRR_HESS_THREADS 256
+#endif
+static constexpr int HT = OFRR_HESS_THREADS;
 
 struct HessWs {
   unsigned* bar_count;  // grid barrier arrivals (monotonic)

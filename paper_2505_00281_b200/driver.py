@@ -130,6 +130,7 @@ _GRAPHS = OrderedDict()
 # stream.
 _SOLVE_LOCK = threading.RLock()
 DEVICE_LOOP = True      # the whole solve as one graph launch (csrc/loop.cu) once its graphs exist
+HANDOVER_STEPPED = False   # ladder: start the next rung from the previous rung's W Y (see _subspace_iter_eig)
 _WARM = set()
 _NO_GRAPH = set()
 
@@ -220,7 +221,7 @@ class EigEngine:
     """Device state of one subspace_iter_eig run (single GPU or row-partitioned)."""
 
     def __init__(self, a: DenseMatrix, cfg: IterConfig, comm: Optional[Comm] = None, n_global: Optional[int] = None,
-                 ops=None, report_scales: bool = True):
+                 ops=None, report_scales: bool = True, prepared=None):
         self.ops = ops or _ops
         self.comm = comm or Comm.world()
         self.cfg = cfg
@@ -238,6 +239,12 @@ class EigEngine:
         _, self.proj_out = projection_policy(self.pol)
         self.stats = RunStats()
         self._oz = {}           # prepared Ozaki digit planes per operator (this run)
+        if prepared is not None:
+            # an operator prepared on a side stream while the previous ladder rung ran
+            oz, ev = prepared
+            self._oz[id(oz.A)] = oz
+            import torch
+            torch.cuda.current_stream(oz.A.device).wait_event(ev)
         # the FP64 report's operator scales only depend on A: refreshed on a side stream while
         # the pencil solve occupies one SM (off the critical path), see _body
         self._res_oz = None
@@ -862,8 +869,10 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
         raise ValueError("k exceeds the operator dimension")
     X0 = None
     stepped = False
+    prepared = None
     hist, iters, passes = [], 0, 0
     if cfg.ladder is not None:
+        prepared = _prepare_ahead(a, cfg, comm)
         # precision ladder: run the cheaper policy while it makes
         # progress, then continue from its restart block in cfg.policy
         from dataclasses import replace as _replace
@@ -871,7 +880,10 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
         with _ph("rung_low"):
             eng0 = EigEngine(a, low, comm=comm, n_global=n, report_scales=False)
             X0 = eng0.run(stop_estimate=cfg.ladder_switch)
-            stepped = getattr(eng0, "handover", None) is not None
+            # hand the fp64 rung the fp32 rung's next iterate (W Y, power step made) instead of
+            # its Ritz vectors?  Measured at C3: one FP64 pass fewer but one iteration more
+            # (the rung then starts from an fp32-accurate A.U) -- slower, so off by default
+            stepped = HANDOVER_STEPPED and getattr(eng0, "handover", None) is not None
             if stepped:
                 X0 = eng0.handover
         if isinstance(X0, RitzSet):                                # m exhausted in the low rung
@@ -882,7 +894,7 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
         hist, iters, passes = list(eng0.stats.history), eng0.stats.iterations, eng0.stats.a_passes
         cfg = _replace(cfg, ladder=None, m=max(1, cfg.m - iters))
     with _ph("rung_main"):
-        eng = EigEngine(a, cfg, comm=comm, n_global=n)
+        eng = EigEngine(a, cfg, comm=comm, n_global=n, prepared=prepared)
         rs = eng.run(X0=X0, stepped=X0 is not None and stepped)
     if stats is not None:
         stats.__dict__.update(eng.stats.__dict__)
@@ -892,6 +904,32 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
         stats.a_passes += passes
         stats.history = hist + [(it + iters, w) for it, w in eng.stats.history]
     return rs
+
+
+_SIDE_STREAMS = {}
+
+
+def _prepare_ahead(a, cfg: IterConfig, comm):
+    """Ladder to an fp64 policy on a 16/8-bit operator: the FP64-accurate products need A's
+    row scales and head/tail split (K7z prepare, one read of A).  A does not change during
+    the solve, so the prepare runs on a side stream while the low rung computes; the main
+    rung's engine waits for its event.  None when the main rung needs no Ozaki operator."""
+    import torch
+    if FpFormat.F64 not in (cfg.policy.storage, cfg.mv_policy.storage) or not hasattr(a, "device_operator"):
+        return None
+    A = operator_for(a, FpFormat.F64)
+    if A.fmt not in _ops.OZAKI_FMTS:
+        return None
+    dev = A.device
+    side = _SIDE_STREAMS.get(dev.index)
+    if side is None:
+        side = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        oz = _ops.OzakiOperator(A)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    return oz, ev
 
 
 def cfg_rung_label(cfg: IterConfig) -> str:
