@@ -75,6 +75,13 @@ CONFIGS = {
                                  "products), A-pass reuse"),
     "c3-f64-reuse": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64", reuse=True,
                          name="as c3-f64 (fp64 basis throughout, to 1e-8), with A-pass reuse (IterConfig.reuse_av)"),
+    # sigma_i = 0.9^i puts sigma_100 = 2.7e-5 below the noise level (1e-4 sigma_1), so no basis
+    # precision reaches a per-triplet relative tolerance on all top-100: C4 runs the reference's
+    # fixed m outer iterations (ofrr/driver.py:141-173), m = 4
+    "c4": dict(kind="svd", n1=1048576, n=4096, rank=256, top=100, k=200, fmt="F16", tol=None, m=4, policy="tc-f16",
+               name="BASELINE configs[3]: partial SVD of a tall 1048576x4096 synthetic low-rank-plus-noise matrix "
+                    "(G1 diag(0.9^i) G2^T + 1e-4 N, rank 256, fp16), top-100 singular triplets, k=200, fp16 basis "
+                    "on the tensor cores (fp32 sums) / fp64 Grams, m=4 outer iterations (fixed, as the reference)"),
     "c3-f64": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
                    name="synthetic dense symmetric 65536x65536 (bf16 operator), geometric spectrum, top-64, "
                         "k=128, to 1e-8 (the north-star target): fp64 basis, FP64-accurate int8 tensor-core "
@@ -82,6 +89,7 @@ CONFIGS = {
 }
 MAX_OUTER = 60
 METRIC = "OFRR top-k eig time-to-tol"
+METRIC_SVD = "OFRR top-k SVD time-to-tol"
 
 # A passes per rung of one solve, as the GPU arm of the same config measured them on a B200
 # (bench.py --impl ours prints them as config.rungs; profiles/r02_passes.json holds the run
@@ -175,7 +183,7 @@ def _ref_kernels():
 _POL_CODES = {"F32": (1, 1, 1), "F64": (2, 2, 2), "BF16": (1, 1, 3), "F16": (1, 1, 0)}
 
 
-def ref_pass_seconds(gemm, oracle, n: int, k: int, rung: str, rows: int):
+def ref_pass_seconds(gemm, oracle, n: int, k: int, rung: str, rows: int, n_rows: int = None):
     """Seconds for ONE A pass (n x n operator times the n x k block) of the reference's
     gemm_mixed under the rung's policy, from `rows` rows timed (F-order A rows, exactly
     as apply_dense hands them to the kernel, ofrr/matrix.py:242-254), scaled to n rows."""
@@ -186,7 +194,7 @@ def ref_pass_seconds(gemm, oracle, n: int, k: int, rung: str, rows: int):
     t0 = time.perf_counter()
     gemm(a, x, c, acc, out)
     dt = time.perf_counter() - t0
-    return dt * n / rows, dt
+    return dt * (n if n_rows is None else n_rows) / rows, dt
 
 
 def ref_c1_full_solve(gemm, oracle):
@@ -221,8 +229,10 @@ def _rung_passes(cfg_name: str, cfg):
             rec = json.load(f)[cfg_name]
         return [(r, int(p)) for r, p in rec["rungs"]], rec.get("source", PASSES_FILE)
     except Exception:
-        rung = "F64" if cfg["policy"] == "full-f64" else "F32"
-        return [(rung, 4)], "no GPU record for this config: 4 passes assumed"
+        rung = {"full-f64": "F64", "tc-f16": "F16", "native-f16": "F16", "mixed-half": "F16",
+                "tc-bf16": "BF16"}.get(cfg["policy"], "F32")
+        passes = 3 * cfg["m"] if cfg.get("kind") == "svd" and cfg.get("m") else 4
+        return [(rung, passes)], f"no GPU record for this config: {passes} passes assumed"
 
 
 def reference_estimate(cfg_name: str, cfg, budget_s: float):
@@ -238,11 +248,11 @@ def reference_estimate(cfg_name: str, cfg, budget_s: float):
     per_pass_s = {}
     for rung, passes in rungs:
         rows = max(1, int(budget_s / len(rungs) / max(ref_pass_seconds(gemm, oracle, n, k, rung, 1)[1], 1e-6)))
-        per_pass, dt = ref_pass_seconds(gemm, oracle, n, k, rung, rows)
+        per_pass, dt = ref_pass_seconds(gemm, oracle, n, k, rung, rows, n_rows=_rows(cfg))
         per_pass_s[rung] = per_pass
         total += per_pass * passes
         parts.append(f"{rung} rung: {rows} rows x {n} cols x k={k} timed in {dt:.2f} s -> {per_pass:.0f} s per "
-                     f"A pass x {passes} passes")
+                     f"A pass ({_rows(cfg)} rows) x {passes} passes")
     wall = time.perf_counter() - t0
     return total, wall, kind, "; ".join(parts) + f" (pass counts: {src})", per_pass_s
 
@@ -267,7 +277,7 @@ def run_reference(args, cfg):
     sample = (f"per step: {detail}; A passes only (lower bound on the reference's solve); "
               f"1 core of {os.cpu_count()} (the reference's kernels are single-threaded)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC_SVD if cfg.get("kind") == "svd" else METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "value_kind": "extrapolated: one A pass per rung timed on a row sample, times the GPU run's pass count; "
                       "ms_per_step is the measured wall time of one such bounded sample",
@@ -284,10 +294,16 @@ def run_reference(args, cfg):
 # ------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------
+def _rows(cfg) -> int:
+    """Rows of A: n1 for the tall SVD configs, n for the square eigen configs."""
+    return int(cfg.get("n1", cfg["n"]))
+
+
 def make_iter_config(p, cfg):
     """The IterConfig of a bench config (also used by tests/ and scripts/)."""
-    return p.IterConfig(k=cfg["k"], m=MAX_OUTER, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
-                        policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=cfg["tol"], top=cfg["top"],
+    return p.IterConfig(k=cfg["k"], m=cfg.get("m", MAX_OUTER), iter=1, basis_method=p.BasisMethod.HESS_LEFT,
+                        projection="ofrr", policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=cfg["tol"],
+                        top=cfg["top"] if cfg["tol"] is not None else None,
                         ladder=p.POLICY_PRESETS[cfg["ladder"]] if cfg.get("ladder") else None,
                         ladder_switch=cfg.get("switch", 1e-4), reuse_av=bool(cfg.get("reuse", False)))
 
@@ -297,15 +313,20 @@ def _dtype(cfg) -> str:
         return "bf16 operator; basis f32 (bf16 tensor cores) -> f64 (int8 tensor cores, Ozaki)"
     return {"full-f32": "bf16 operator; f32 basis (bf16 tensor cores)",
             "full-f64": "bf16 operator; f64 basis (int8 tensor cores, Ozaki)",
-            "tc-bf16": "bf16"}.get(cfg["policy"], cfg["policy"])
+            "tc-bf16": "bf16", "tc-f16": "f16 operator and basis (f16 tensor cores, fp32 sums)"}.get(cfg["policy"],
+                                                                                                   cfg["policy"])
 
 
 def _config_block(name, cfg, world):
-    n = cfg["n"]
-    return {"workload": cfg["name"], "name": name, "n": n, "top": cfg["top"], "k": cfg["k"], "tol": cfg["tol"],
-            "policy": cfg["policy"], "ladder": cfg.get("ladder"), "reuse_av": bool(cfg.get("reuse", False)),
-            "parallelism": f"row-partitioned x{world}" if world > 1 else "single",
-            "l2": "inputs larger than L2 (A = %d MiB per GPU)" % (((n + world - 1) // world) * n * 2 >> 20)}
+    n, rows = cfg["n"], _rows(cfg)
+    out = {"workload": cfg["name"], "name": name, "kind": cfg.get("kind", "eig"), "n": n, "top": cfg["top"],
+           "k": cfg["k"], "tol": cfg["tol"], "policy": cfg["policy"], "ladder": cfg.get("ladder"),
+           "reuse_av": bool(cfg.get("reuse", False)),
+           "parallelism": f"row-partitioned x{world}" if world > 1 else "single",
+           "l2": "inputs larger than L2 (A = %d MiB per GPU)" % (((rows + world - 1) // world) * n * 2 >> 20)}
+    if rows != n:
+        out["n1"] = rows
+    return out
 
 
 # kernel name -> (label, what its algorithmic work is); bytes / flops per launch are
@@ -473,12 +494,12 @@ def _dry_run(args, cfg, p, torch, dist, world, rank):
     if world > 1:
         dist.init_process_group("gloo")
     comm = p.Comm.world()
-    r0, r1 = comm.row_range(cfg["n"])
+    r0, r1 = comm.row_range(_rows(cfg))
     rows = torch.tensor([r1 - r0], dtype=torch.int64)
     if world > 1:
         dist.all_reduce(rows)
     if rank == 0:
-        print(json.dumps({"dry_run": True, "n_gpus": world, "rows_total": int(rows.item()), "n": cfg["n"],
+        print(json.dumps({"dry_run": True, "n_gpus": world, "rows_total": int(rows.item()), "n": _rows(cfg),
                           "config": args.config}), flush=True)
     if world > 1:
         dist.barrier()
@@ -488,14 +509,21 @@ def _dry_run(args, cfg, p, torch, dist, world, rank):
 def _run_ours(args, cfg, p, _lib, ops, torch, dist, ctypes, world, rank, local, dev):
     comm = p.Comm.world()
     n, top, k, tol = cfg["n"], cfg["top"], cfg["k"], cfg["tol"]
+    rows_all = _rows(cfg)
     fmt = p.FpFormat[cfg["fmt"]]
-    lam = p.geometric_spectrum(n, top, k)
-    r0, r1 = comm.row_range(n)
-    A, _ = p.synthetic_symmetric(lam, fmt, seed=SEED, device=dev, row0=r0, rows=r1 - r0)
+    r0, r1 = comm.row_range(rows_all)
     icfg = make_iter_config(p, cfg)
+    svd = cfg.get("kind") == "svd"
+    if svd:
+        A, _ = p.synthetic_lowrank(rows_all, n, fmt, r=cfg["rank"], seed=SEED, device=dev, row0=r0, rows=r1 - r0)
+        driver = p.subspace_iter_svd
+    else:
+        lam = p.geometric_spectrum(n, top, k)
+        A, _ = p.synthetic_symmetric(lam, fmt, seed=SEED, device=dev, row0=r0, rows=r1 - r0)
+        driver = p.subspace_iter_eig
 
-    def solve(stats=None):
-        return p.subspace_iter_eig(A, icfg, stats=stats, comm=comm, n_global=n)
+    def solve(stats=None, a=None):
+        return driver(A if a is None else a, icfg, stats=stats, comm=comm, n_global=rows_all)
 
     def barrier():
         if world > 1:
@@ -569,7 +597,7 @@ def _run_ours(args, cfg, p, _lib, ops, torch, dist, ctypes, world, rank, local, 
         t0 = time.perf_counter()
         op.t[:, :n].copy_(a_host, non_blocking=True)
         Ah = p.DenseMatrix.on_device(op)
-        rsh = p.subspace_iter_eig(Ah, icfg, comm=comm, n_global=n)
+        rsh = solve(a=Ah)
         vals = np.asarray(rsh.values)
         vecs = rsh.vectors.data
         torch.cuda.synchronize()
@@ -606,7 +634,7 @@ def _run_ours(args, cfg, p, _lib, ops, torch, dist, ctypes, world, rank, local, 
                          f"(lower bound on the reference's solve); 1 core of {os.cpu_count()}",
                "c1_full_solve": c1}
     line = {
-        "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
+        "metric": METRIC_SVD if svd else METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": _dtype(cfg), "data": "synthetic",
         "config": dict(_config_block(args.config, cfg, world),

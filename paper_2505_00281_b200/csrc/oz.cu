@@ -741,15 +741,17 @@ static constexpr int OZK_THREADS = 192 + 32 * OZK_CONV_WARPS;
 // to 6 products of |d| <= 255 * 128 per term -- 6 * 32640 * 8192 < 2^31
 static constexpr int OZK_MAXCHUNK = 128;
 
-template <int BN>
+template <int BN, int NP = OZ_D>
 struct OzkCfg {
   static constexpr int A_TILE = OZ_TM * OZK_KB;         // 8 KB per digit plane
-  static constexpr int A_SET = OZ_D * A_TILE;           // 48 KB per k-block
+  static constexpr int A_SET = NP * A_TILE;             // NP digit planes per k-block (48 / 24 KB)
   static constexpr int V_SET = OZ_D * BN * OZK_KB;      // six V digit tiles per k-block
-  static constexpr int A_STAGES = 3;
-  static constexpr int V_STAGES = 2;
+  // the 3-digit heads free half of each A stage: deeper rings on both operands
+  static constexpr int A_STAGES = NP == OZ_D ? 3 : 5;
+  static constexpr int V_STAGES = NP == OZ_D ? 2 : (BN == 64 ? 3 : 4);
   static constexpr int TMEM_COLS = OZ_D * BN <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = 1024 + A_STAGES * A_SET + V_STAGES * V_SET + 256;
+  static_assert(SMEM_BYTES <= 227 * 1024, "ozk shared memory");
 };
 
 // UMMA shared-memory descriptor: K-major, 64B swizzle, 8-row groups 512 B apart
@@ -813,7 +815,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
                const __grid_constant__ CUtensorMap tmV, double* __restrict__ ws, int kbc, int nchunks,
                long long total_units, int max_slots, int npad, int col0, int stamp,
                const int* __restrict__ full_flag) {
-  using C = OzkCfg<BN>;
+  using C = OzkCfg<BN, NP>;
   constexpr bool full = NP == OZ_D;
   if (full_flag != nullptr && ((*full_flag != 0) != full)) return;
   if (stamp && threadIdx.x == 0) atomicMin(&g_oz_stamp[0], oz_gtimer_ns());
@@ -1394,19 +1396,21 @@ static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r) {
 template <int FMT, int BN>
 static int ozk_launch(const void* A, int64_t rows, int64_t cols, int64_t lda, const int* T, const CUtensorMap& tV,
                       const OzkPlan& p, double* ws, int col0, const int* full, cudaStream_t st) {
+  using C3 = OzkCfg<BN, 3>;
   using C = OzkCfg<BN>;
   static std::once_flag attr;
   cudaError_t ae = cudaSuccess;
   std::call_once(attr, [&] {
-    ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM_BYTES);
     if (ae == cudaSuccess)
       ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, OZ_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   });
   OFRR_CUDA_TRY(ae);
   const int stamp = g_oz_stamp_on ? 1 : 0;
   if (full) {
-    k_ozk_gemm<FMT, BN, 3><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc, p.nchunks,
-                                                                      p.total, p.max_slots, p.npad, col0, stamp, full);
+    k_ozk_gemm<FMT, BN, 3><<<p.grid, OZK_THREADS, C3::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
+                                                                       p.nchunks, p.total, p.max_slots, p.npad, col0,
+                                                                       stamp, full);
     OFRR_CHECK_LAUNCH();
   }
   k_ozk_gemm<FMT, BN, OZ_D><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,

@@ -945,8 +945,16 @@ class SvdEngine:
     ofrr/projection.py:99-133).  A V and A^T U both run K-major on the tensor cores:
     A^T is kept resident as a second row-major operator."""
 
-    def __init__(self, a: DenseMatrix, pol: PrecisionPolicy, mv: PrecisionPolicy, ops=None):
+    def __init__(self, a: DenseMatrix, pol: PrecisionPolicy, mv: PrecisionPolicy, ops=None,
+                 comm: Optional[Comm] = None, n1_global: Optional[int] = None):
+        """Row-partitioned: ``a`` holds this rank's rows of the tall A
+        (n1_global rows in all); V (n2 x k) is replicated.  Per power step A_p V is local,
+        A^T U = sum_p A_p^T U_p is an all-reduce(sum) of fp32 partial products (rounded to
+        storage after the sum); the U basis is built redundantly from the all-gathered U, its
+        Gram and the cross Gram U^T A V are all-reduced partials; the Ritz vectors U Y stay
+        row-partitioned (each rank returns its rows)."""
         self.ops = ops or _ops
+        self.comm = comm or Comm()
         self.a, self.pol, self.mv = a, pol, mv
         self.A_mv = a.device_operator(mv.storage)
         self.At_mv = a.device_operator_t(mv.storage)
@@ -954,6 +962,10 @@ class SvdEngine:
         self.device = self.A_mv.device
         _, self.proj_out = projection_policy(pol)
         self.a_passes = 0
+        self.n1 = int(n1_global if n1_global is not None else a.rows)
+        self.r0, self.r1 = self.comm.row_range(self.n1)
+        if self.comm.distributed and a.rows != self.r1 - self.r0:
+            raise ValueError(f"rank {self.comm.rank}: local A has {a.rows} rows, expected {self.r1 - self.r0}")
 
     @classmethod
     def single(cls, a, pol, mv):
@@ -968,13 +980,41 @@ class SvdEngine:
         return self.ops.hessenberg(X, pol.storage, pol.compute, pol.drop_tol)
 
     def matvec(self, op, X, st):
+        """A X (local rows when partitioned) with inf-norm column scaling over all ranks."""
         import torch
         colmax = torch.zeros(X.k, dtype=torch.float64, device=self.device)
         W = self.ops.new_block(op.rows, X.k, self.mv.storage, self.device)
         self.ops.gemm_av(op, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
         self.a_passes += 1
+        self.comm.all_reduce_max_(colmax)
         self.ops.scale_columns(W, colmax, self.mv.compute)
         return W
+
+    def matvec_t(self, U, st):
+        """A^T U with inf-norm column scaling.  Partitioned: the ranks' fp32 partial products
+        A_p^T U_p are all-reduced (sum), then rounded to storage and scaled."""
+        import torch
+        if not self.comm.distributed:
+            return self.matvec(self.At_mv, U, st)
+        ops, k, n2 = self.ops, U.k, self.At_mv.rows
+        acc = FpFormat.F64 if FpFormat.F64 in (self.At_mv.fmt, U.fmt) else FpFormat.F32
+        P = ops.new_block(n2, k, acc, self.device)
+        ops.gemm_av(self.At_mv, U, P, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+        self.a_passes += 1
+        self.comm.all_reduce_sum_(P.t)
+        W = ops.new_block(n2, k, self.mv.storage, self.device)
+        ops.convert(P, W, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+        colmax = W.t[:k, :n2].to(torch.float64).abs().amax(dim=1)
+        ops.scale_columns(W, colmax, self.mv.compute)
+        return W
+
+    def gather_rows(self, Xp):
+        """The full n1 x k block from every rank's rows (all-gather)."""
+        if not self.comm.distributed:
+            return Xp
+        X = self.ops.new_block(self.n1, Xp.k, Xp.fmt, self.device)
+        self.comm.all_gather_rows(Xp.t, X.t, self.n1, Xp.k)
+        return X
 
     def project(self, U, V, want64: bool = True, x_fmt=None, classical: bool = False):
         """ofrr_svd on device blocks U (n1 x k1), V (n2 x k2) in policy storage; with
@@ -987,7 +1027,12 @@ class SvdEngine:
         W = ops.new_block(self.A_pol.rows, k2, self.pol.storage, self.device)
         ops.gemm_av(self.A_pol, V, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
         self.a_passes += 1
-        G, Mu = ops.gram(U, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        dist = self.comm.distributed
+        Ul = _row_slice(U, self.r0, self.r1) if dist else U        # this rank's rows of the U basis
+        G, Mu = ops.gram(Ul, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
+        if dist:
+            self.comm.all_reduce_sum_(G)
+            self.comm.all_reduce_sum_(Mu)
         _, Mv = ops.gram(V, None, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1])
         # block pencil (tensors are column-major: row j = column j)
         Bm = torch.zeros((kk, kk), dtype=torch.float64, device=self.device)
@@ -1003,6 +1048,8 @@ class SvdEngine:
         eig = ops.sym_def_gen_eig(Bm, Mm, kk)
         st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
         st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
+        if dist:
+            self.comm.all_reduce_max_(st)
         s = st.cpu().numpy()
         if s[S_MV_FLAGS] & 1:
             raise OverflowDiagnostic("non-finite entries after MatVec")
@@ -1022,9 +1069,9 @@ class SvdEngine:
         if npos < min(k1, k2):
             diag = f"{npos} positive eigenvalues (pencil admits {min(k1, k2)})"
         if npos == 0:
-            return RitzSet(sig, DenseMatrix(np.zeros((U.n, 0)), FpFormat.F64), "svd",
+            return RitzSet(sig, DenseMatrix(np.zeros((Ul.n, 0)), FpFormat.F64), "svd",
                            right_vectors=DenseMatrix(np.zeros((V.n, 0)), FpFormat.F64), diagnostics=diag), None, None
-        U64, _ = ops.ritz(U, eig.vectors, kk, None, npos, math.sqrt(2.0), want64=True)
+        U64, _ = ops.ritz(Ul, eig.vectors, kk, None, npos, math.sqrt(2.0), want64=True)
         V64, Vx = ops.ritz(V, eig.vectors, kk, None, npos, math.sqrt(2.0), want64=True,
                            x_fmt=x_fmt, row_offset=k1, flags=st[S_RESTART_FLAGS:S_RESTART_FLAGS + 1])
         rs = RitzSet(sig, DenseMatrix.from_block(U64), "svd", right_vectors=DenseMatrix.from_block(V64),
@@ -1032,14 +1079,49 @@ class SvdEngine:
         return rs, Vx, st
 
 
-def subspace_iter_svd(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats] = None) -> RitzSet:
+    def residuals(self, rs: RitzSet, t: int) -> np.ndarray:
+        """FP64 max(||A v - s u||, ||A^T u - s v||) / s of the first t triplets
+        (ofrr/projection.py:136-158).  Partitioned: ||A_p v - s u_p||^2 summed over ranks;
+        A^T u = sum_p A_p^T u_p (FP64-accurate partial products, all-reduced)."""
+        import torch
+        from .projection import residual_report
+        if not self.comm.distributed and self.ops is _ops:
+            from dataclasses import replace as _rep
+            head = _rep(rs, values=rs.values[:t], vectors=_narrow_dm(rs.vectors, t),
+                        right_vectors=_narrow_dm(rs.right_vectors, t))
+            return residual_report(self.a, head).residuals
+        ops, dev = self.ops, self.device
+        A = self.a.residual_operator(self.A_mv.fmt)
+        At = self.a.residual_operator_t(self.A_mv.fmt)
+        if At.fmt not in _ops.OZAKI_FMTS and At.fmt != FpFormat.F64 and self.ops is _ops:
+            At = self.a.device_operator_t(FpFormat.F64)      # FP64 product of an f32 operator
+        Ub = rs.vectors.device_block(FpFormat.F64).narrow(t)
+        Vb = rs.right_vectors.device_block(FpFormat.F64).narrow(t)
+        sig = torch.as_tensor(np.asarray(rs.values[:t], dtype=np.float64), device=dev)
+        ss1 = torch.zeros(t, dtype=torch.float64, device=dev)
+        ops.residual_pair(A, False, Vb, Ub, sig, None, t, ss1, accumulate_max=2)
+        n2 = At.rows
+        P = ops.new_block(n2, t, FpFormat.F64, dev)
+        ops.gemm_av(At, Ub, P)
+        self.comm.all_reduce_sum_(ss1)
+        self.comm.all_reduce_sum_(P.t)
+        d = P.t[:t, :n2] - sig[:, None] * Vb.t[:t, :n2]
+        ss2 = (d * d).sum(dim=1)
+        r = torch.sqrt(torch.maximum(ss1, ss2)) / sig.abs()
+        return r.cpu().numpy()
+
+
+def subspace_iter_svd(a: DenseMatrix, cfg: IterConfig, stats: Optional[RunStats] = None,
+                      comm: Optional[Comm] = None, n_global: Optional[int] = None) -> RitzSet:
     """Alternating subspace iteration for the SVD (ofrr/driver.py:141-173), on device
-    (thread-safe like subspace_iter_eig)."""
+    (thread-safe like subspace_iter_eig).  Row-partitioned when ``comm`` spans several ranks:
+    ``a`` holds this rank's rows of A (``n_global`` rows in all) and the returned left
+    singular vectors hold this rank's rows."""
     with _SOLVE_LOCK:
-        return _subspace_iter_svd(a, cfg, stats)
+        return _subspace_iter_svd(a, cfg, stats, comm, n_global)
 
 
-def _subspace_iter_svd(a, cfg, stats) -> RitzSet:
+def _subspace_iter_svd(a, cfg, stats, comm=None, n_global=None, ops=None) -> RitzSet:
     """The SVD outer loop.  With cfg.tol the loop stops at the first outer iteration whose
     leading ``top`` triplets have FP64 residuals max(||A v - s u||, ||A^T u - s v||) / s below
     tol (``m`` is the cap); otherwise exactly m iterations (the reference).  ladder / reuse_av
@@ -1048,29 +1130,32 @@ def _subspace_iter_svd(a, cfg, stats) -> RitzSet:
     _require_ofrr_path(cfg, "SVD iteration")
     if cfg.ladder is not None or cfg.reuse_av:
         raise ValueError("subspace_iter_svd: ladder / reuse_av apply to subspace_iter_eig only")
-    n1, n2 = a.rows, a.cols
+    comm = comm or Comm.world()
+    n1, n2 = int(n_global if n_global is not None else a.rows), a.cols
     if cfg.k > min(n1, n2):
         raise ValueError("k exceeds min(n1, n2)")
     pol, mv = cfg.policy, cfg.mv_policy
-    eng = SvdEngine(a, pol, mv)
+    eng = SvdEngine(a, pol, mv, ops=ops, comm=comm, n1_global=n1)
     ops = eng.ops
     V = ops.start_block(cfg.seed, n2, cfg.k, mv.storage, eng.device)
     rs = None
-    checked = None
     tol, top = cfg.tol, (cfg.top or cfg.k)
     hist = []
     converged = False
     import torch
     its = 0
+    checked = None
     for it in range(cfg.m):
         st = torch.zeros(8, dtype=torch.int32, device=eng.device)
         U = V
         for _ in range(cfg.iter):
             U = eng.matvec(eng.A_mv, V, st)
-            V = eng.matvec(eng.At_mv, U, st)
-        hu, hv = eng.basis(U, cfg), eng.basis(V, cfg)
+            V = eng.matvec_t(U, st)
+        hu, hv = eng.basis(eng.gather_rows(U), cfg), eng.basis(V, cfg)
         st[S_NKEPT:S_NKEPT + 1].copy_(hu.n_kept)
         st[S_NKEPT2:S_NKEPT2 + 1].copy_(hv.n_kept)
+        if comm.distributed:
+            comm.all_reduce_max_(st)
         s = st.cpu().numpy()
         if s[S_MV_FLAGS] & 1:
             raise OverflowDiagnostic("non-finite entries after MatVec")
@@ -1081,18 +1166,17 @@ def _subspace_iter_svd(a, cfg, stats) -> RitzSet:
                                   classical=cfg.projection == "rr")
         if Vx is None:
             raise EmptyPencilError("no positive eigenvalues in the SVD pencil")
+        if comm.distributed:
+            comm.all_reduce_max_(st2)
         if int(st2[S_RESTART_FLAGS].item()) & 1:
             raise OverflowDiagnostic("non-finite entries after projection")
         V = Vx
         its = it + 1
         if tol is not None:
             # FP64 confirmation on the leading triplets (two FP64-accurate products, K7z)
-            from dataclasses import replace as _rep
             t = min(top, len(rs.values))
-            head = _rep(rs, values=rs.values[:t], vectors=_narrow_dm(rs.vectors, t),
-                        right_vectors=_narrow_dm(rs.right_vectors, t))
-            checked = residual_report(a, head)
-            worst = float(np.max(checked.residuals)) if t >= top else float("inf")
+            checked = eng.residuals(rs, t)
+            worst = float(np.max(checked)) if t >= top else float("inf")
             hist.append((its, worst))
             if worst < tol:
                 converged = True
@@ -1102,6 +1186,10 @@ def _subspace_iter_svd(a, cfg, stats) -> RitzSet:
         stats.a_passes = eng.a_passes
         stats.history = hist
         stats.converged = converged
+        stats.rungs = [(cfg_rung_label(cfg), its, eng.a_passes)]
+    if comm.distributed or eng.ops is not _ops:
+        from dataclasses import replace as _rep
+        return _rep(rs, residuals=eng.residuals(rs, len(rs.values)))
     return residual_report(a, rs)
 
 

@@ -65,6 +65,10 @@ def gemm_av(A, X, W, out_fmt=None, colmax=None, flags=None, transpose=False, W2=
         flags |= 1
 
 
+def convert(src, dst, flags=None):
+    _put(dst, o.round_to(_np(src), int(dst.fmt)))
+
+
 def scale_columns(X, colmax, compute):
     x = _np(X)
     m = colmax.numpy()
@@ -197,3 +201,13 @@ class RowBlock:
 
     def residual_operator(self, prefer):
         return self.op
+
+    def device_operator_t(self, fmt=None, device=None):
+        if not hasattr(self, "op_t"):
+            self.op_t = new_operator(self.cols, self.rows, self.fmt, CPU)
+            self.op_t.t.zero_()
+            self.op_t.t[:, : self.rows].copy_(self.op.t[:, : self.cols].t())
+        return self.op_t
+
+    def residual_operator_t(self, prefer):
+        return self.device_operator_t()

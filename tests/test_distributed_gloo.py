@@ -121,3 +121,76 @@ def test_comm_row_ranges():
             rows = [Comm(r, P).row_range(n) for r in range(P)]
             assert rows[0][0] == 0 and rows[-1][1] == n
             assert all(rows[i][1] == rows[i + 1][0] for i in range(P - 1))
+
+
+# ---- row-partitioned partial SVD (C4's layout): 2 gloo ranks vs 1 process ----------------
+N1, N2, KS, TS = 240, 60, 10, 4
+
+
+def _tall():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as o
+    rng = np.random.default_rng(SEED)
+    g1, _ = np.linalg.qr(rng.standard_normal((N1, 20)))
+    g2, _ = np.linalg.qr(rng.standard_normal((N2, 20)))
+    a = (g1 * 0.8 ** np.arange(20)) @ g2.T + 1e-4 * rng.standard_normal((N1, N2))
+    return o.round_to(a, o.F32)
+
+
+def _svd(a_rows, comm, tol=None):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cpu_ops
+    import paper_2505_00281_b200 as p
+    from paper_2505_00281_b200.driver import _subspace_iter_svd
+    cfg = p.IterConfig(k=KS, m=5, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.FULL_F32, seed=SEED, tol=tol, top=TS if tol else None)
+    st = p.RunStats()
+    rs = _subspace_iter_svd(cpu_ops.RowBlock(a_rows, p.FpFormat.F32), cfg, st, comm=comm, n_global=N1, ops=cpu_ops)
+    return rs.values, rs.residuals, rs.vectors.data, rs.right_vectors.data, st.iterations
+
+
+def _svd_worker(rank, world, port, q, tol):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, ROOT)
+        from paper_2505_00281_b200.comm import Comm
+        comm = Comm.world()
+        r0, r1 = comm.row_range(N1)
+        q.put((rank, _svd(_tall()[r0:r1], comm, tol)))
+    except Exception as e:
+        import traceback
+        q.put((rank, repr(e) + traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("tol", [None, 1e-4])
+def test_row_partitioned_svd_two_ranks_equals_one(tol):
+    sys.path.insert(0, ROOT)
+    from paper_2505_00281_b200.comm import Comm
+    single = _svd(_tall(), Comm(), tol)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_svd_worker, args=(r, 2, port, q, tol)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank in range(2):
+        assert not isinstance(out[rank], str), out[rank]
+        vals, res, U, V, its = out[rank]
+        # A^T U is summed from the ranks' fp32 partial products (rounded once more than the
+        # single run's product): agreement to fp32 rounding
+        assert its == single[4]
+        np.testing.assert_allclose(vals, single[0], rtol=1e-6)
+        assert np.all(res <= 2 * single[1] + 1e-7) and np.all(single[1] <= 2 * res + 1e-7)
+        np.testing.assert_allclose(V, single[3], atol=1e-5)
+        np.testing.assert_array_equal(out[0][3], out[1][3])        # V replicated bit for bit
+    U = np.vstack([out[0][2], out[1][2]])                # row-partitioned left vectors
+    np.testing.assert_allclose(U, single[2], atol=1e-5)
