@@ -889,11 +889,12 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
           for (int p = 0; p < NP; ++p) {
             const uint64_t da = umma_desc_sw64(sa + p * C::A_TILE);
             const int nq = OZ_D - p;
+            // both K halves of a k-block back to back on the same accumulator columns
+            for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
+              const int ng = std::min(256 / BN, nq - q0);
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const uint32_t acc = (u > seg_start || p > 0 || k > 0) ? 1u : 0u;
-              for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
-                const int ng = std::min(256 / BN, nq - q0);
+              for (int k = 0; k < 2; ++k) {
+                const uint32_t acc = (u > seg_start || p > 0 || k > 0) ? 1u : 0u;
                 mma_i8(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
                        dv + (uint64_t)((q0 * BN * OZK_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN, p == 0, true),
                        acc);

@@ -234,7 +234,7 @@ def test_gen_eig_golden(ofrr_gpu, golden, n):
     np.testing.assert_allclose(r.vectors, golden[f"geneig/{n}/vecs"], rtol=1e-8, atol=1e-9)
 
 
-@pytest.mark.parametrize("k", [64, 100, 128, 200])
+@pytest.mark.parametrize("k", [64, 100, 128, 200, 400])
 def test_gen_eig_large_vs_lapack(ofrr_gpu, k):
     """K5 at the basis widths of the BASELINE configs (k = 64 / 128; 200 / 400 for SVD)."""
     import scipy.linalg
@@ -249,6 +249,29 @@ def test_gen_eig_large_vs_lapack(ofrr_gpu, k):
     np.testing.assert_allclose(res.values, ref, atol=1e-9 * np.abs(ref).max())
     g = res.vectors.T @ m @ res.vectors
     np.testing.assert_allclose(g, np.eye(k), atol=1e-8)
+
+
+def test_svd_block_pencil_k400_vs_lapack(ofrr_gpu):
+    """The C4 SVD pencil (k1 = k2 = 200 -> 400 x 400): [[0, G], [G', 0]] against
+    diag(Mu, Mv), as ofrr_svd assembles it (ofrr/projection.py:99-133): the positive
+    eigenvalues are the singular values of Lu^-1 G Lv^-T (Mu = Lu Lu', Mv = Lv Lv')."""
+    import scipy.linalg
+    p = ofrr_gpu
+    rng = np.random.default_rng(400)
+    k1 = k2 = 200
+    g = rng.standard_normal((k1, k2)) * (0.9 ** np.arange(k2))[None, :]
+    ru, rv = rng.standard_normal((k1, k1)), rng.standard_normal((k2, k2))
+    mu, mv = ru.T @ ru / k1 + np.eye(k1), rv.T @ rv / k2 + np.eye(k2)
+    b = np.zeros((k1 + k2, k1 + k2))
+    b[:k1, k1:], b[k1:, :k1] = g, g.T
+    m = scipy.linalg.block_diag(mu, mv)
+    res = p.sym_def_gen_eig(b, m)
+    lu, lv = np.linalg.cholesky(mu), np.linalg.cholesky(mv)
+    sv = np.linalg.svd(np.linalg.solve(lu, np.linalg.solve(lv, g.T).T), compute_uv=False)
+    np.testing.assert_allclose(res.values[:k2], sv, rtol=1e-9, atol=1e-12 * sv[0])
+    np.testing.assert_allclose(res.values[k2:], -sv[::-1], rtol=1e-9, atol=1e-12 * sv[0])
+    y = res.vectors
+    np.testing.assert_allclose(y.T @ m @ y, np.eye(k1 + k2), atol=1e-8)
 
 
 def test_ritz_and_residual(ofrr_gpu, oracle):
