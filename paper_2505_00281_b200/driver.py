@@ -238,6 +238,7 @@ class EigEngine:
                              f"{self.r1 - self.r0} (rows {self.r0}..{self.r1} of {self.n})")
         _, self.proj_out = projection_policy(self.pol)
         self.stats = RunStats()
+        self._last_w2 = None    # the latest projection's W = A U in its accumulation format
         self._oz = {}           # prepared Ozaki digit planes per operator (this run)
         if prepared is not None:
             # an operator prepared on a side stream while the previous ladder rung ran
@@ -348,6 +349,7 @@ class EigEngine:
         ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2,
                     **({"oz": self._block_oz(self.A_pol, U)} if self.ops is _ops else {}))
         self.stats.a_passes += 1
+        self._last_w2 = W2
         Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U
         classical = self.cfg.projection == "rr"       # rr_eig (ofrr/projection.py:64-72): no mass matrix
         if comm.distributed:
@@ -488,7 +490,7 @@ class EigEngine:
                 st[S_EIG_STATUS:].zero_()                     # gram/pencil/restart slots
                 res = self.project(U, st, want64=False, top_check=(top if check else None), reuse=cfg.reuse_av)
                 eig, _, Xn, est = res[:4]
-                out = dict(out, Xnext=res[4] if cfg.reuse_av else None)
+                out = dict(out, Xnext=res[4] if cfg.reuse_av else None, W2=self._last_w2, graph=None)
                 s, vals_all, est_np = self._fetch(st, eig.values, est)
             _raise_for(s, "projection")
             r = int(s[S_NOUT])
@@ -666,7 +668,31 @@ class EigEngine:
                 U64c = self.ops.DevBlock(U64.t.clone(), U64.n, r, U64.fmt)   # outlive the next replay
                 return RitzSet(np.array(vals[:r]), DenseMatrix.from_block(U64c), "eig", residuals=res)
         U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
+        W2 = out.get("W2")
+        if self._w2_is_fp64(W2, U):
+            rs = RitzSet(np.array(vals[:r]), DenseMatrix.from_block(U64.narrow(r)), "eig")
+            res = self.residuals_from_w(U, W2, eig, r)
+            return RitzSet(rs.values, rs.vectors, "eig", residuals=res.cpu().numpy()[:r])
         return self.report(U64, eig, r, vals)
+
+    @staticmethod
+    def _w2_is_fp64(W2, U) -> bool:
+        return W2 is not None and W2.fmt == FpFormat.F64 and W2.k >= U.k
+
+    def residuals_from_w(self, U, W2, eig, r: int):
+        """FP64 residuals ||A u_j - lambda_j u_j|| / |lambda_j| of the Ritz vectors u_j = U y_j
+        when the projection's W2 = A U is itself an FP64-accurate product (fp64 blocks: K7z on
+        a 16/8-bit operator, fp64 FMA otherwise): A u_j = W2 y_j, so the report is
+        ||(W2 - lambda_j U) y_j|| / |lambda_j| in fp64 (K7e with fp64 operands) -- no further
+        pass over A.  Row-partitioned: sums of squares all-reduced, finished on the device."""
+        ops, comm = self.ops, self.comm
+        Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U
+        res = ops.residual_estimate(Ul, W2, eig.vectors, U.k, eig.values, eig.n_out, r,
+                                    mode=2 if comm.distributed else 0)
+        if comm.distributed:
+            comm.all_reduce_sum_(res)
+            res = _relative(res, eig.values, r)
+        return res
 
     def _capture_report(self, g, U, eig, kp, r):
         import torch
@@ -677,7 +703,11 @@ class EigEngine:
             with rec:
                 with torch.cuda.graph(graph):
                     U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
-                    res = self.residuals(U64, eig.values, eig.n_out, r)
+                    W2 = g.outs.get("W2")
+                    if self._w2_is_fp64(W2, U):
+                        res = self.residuals_from_w(U, W2, eig, r)
+                    else:
+                        res = self.residuals(U64, eig.values, eig.n_out, r)
         except Exception:
             g.report = None
             return None
@@ -699,7 +729,7 @@ class EigEngine:
             eig, _, Xn, est, Xnext = self.project(U, st, want64=False, top_check=(top if check else None), reuse=True)
         else:
             eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
-        out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None, Xnext=Xnext)
+        out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None, Xnext=Xnext, W2=self._last_w2)
         if self.comm.distributed:
             self.comm.all_reduce_max_(st)        # every rank sees (and raises) the same status
         parts = [st.to(torch.float64), eig.values.reshape(-1).to(torch.float64)]
