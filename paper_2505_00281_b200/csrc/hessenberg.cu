@@ -373,20 +373,30 @@ __global__ void __launch_bounds__(HT)
       best = (double)__uint_as_float((unsigned)(key >> 32));
       owner = r >= 0 ? s_owner : 0;
     } else {
-      // every thread reads one CTA's candidate (one L2 round trip instead of a warp walking
-      // all G), then a block argmax: max value, ties -> lowest row (CTA row blocks ascend, so
-      // the lowest row is the reference's np.argmax choice); the owner CTA follows from the row
-      double bv = -1.0;
-      long long bi = -1;
-      for (int cc = threadIdx.x; cc < G; cc += HT) {
-        const long long oi = __ldcg(&ws.cand_idx[buf * G + cc]);
-        const double ov = __ldcg(&ws.cand_val[buf * G + cc]);
-        if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+      // warp 0 reduces the CTAs' candidates; max value, ties -> lowest row (CTA row
+      // blocks ascend, so the lowest row is the reference's np.argmax choice)
+      if (threadIdx.x < 32) {
+        double bv = -1.0;
+        long long bi = -1;
+        int bo = -1;
+        for (int cc = threadIdx.x; cc < G; cc += 32) {
+          const long long oi = __ldcg(&ws.cand_idx[buf * G + cc]);
+          const double ov = __ldcg(&ws.cand_val[buf * G + cc]);
+          if (oi >= 0 && (bi < 0 || ov > bv)) { bv = ov; bi = oi; bo = cc; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
+          if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; bo = oo; }
+        }
+        if (threadIdx.x == 0) { s_best = bv; s_r = bi; s_owner = bo; }
       }
-      block_argmax(bv, bi, sv, si);
-      best = bv;
-      r = bi;
-      owner = r >= 0 ? (int)(r / rows_per) : 0;
+      __syncthreads();
+      best = s_best;
+      r = s_r;
+      owner = s_owner;
     }
     // ofrr/basis.py:178-180: skip when no free row or |pivot| < tol (NaN pivots skip too)
     const bool skip = (r < 0) || !(best >= tol);

@@ -270,8 +270,10 @@ def test_svd_block_pencil_k400_vs_lapack(ofrr_gpu):
     sv = np.linalg.svd(np.linalg.solve(lu, np.linalg.solve(lv, g.T).T), compute_uv=False)
     np.testing.assert_allclose(res.values[:k2], sv, rtol=1e-9, atol=1e-12 * sv[0])
     np.testing.assert_allclose(res.values[k2:], -sv[::-1], rtol=1e-9, atol=1e-12 * sv[0])
+    # +-sigma pairs of the smallest singular values (0.9^200 ~ 7e-10) are nearly degenerate
+    # around 0: M-orthonormality there is ~eps ||B|| / gap
     y = res.vectors
-    np.testing.assert_allclose(y.T @ m @ y, np.eye(k1 + k2), atol=1e-8)
+    np.testing.assert_allclose(y.T @ m @ y, np.eye(k1 + k2), atol=1e-6)
 
 
 def test_ritz_and_residual(ofrr_gpu, oracle):
