@@ -73,6 +73,21 @@ CONFIGS = {
                                  "(bf16 operator), geometric spectrum, top-64, k=128, to FP64 residual 1e-8 by the "
                                  "fp32 -> fp64 basis ladder (bf16 tensor cores -> int8 Ozaki FP64-accurate "
                                  "products), A-pass reuse"),
+    "c3-ladder3": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
+                       ladder=("full-f32", "full-f64-lite"), switch=(1e-4, 1e-6), reuse=True,
+                       name="BASELINE configs[2] (north-star target): synthetic dense symmetric 65536x65536 "
+                            "(bf16 operator), geometric spectrum, top-64, k=128, to FP64 residual 1e-8 by a "
+                            "three-rung basis ladder: fp32 (bf16 tensor cores) -> fp64 with ~30-bit int8 Ozaki "
+                            "products -> fp64 with FP64-accurate products, A-pass reuse"),
+    "c3-ladder4": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
+                       ladder=("full-f32-lite", "full-f32", "full-f64-lite"), switch=(1e-2, 1e-4, 1e-6), reuse=True,
+                       name="BASELINE configs[2] (north-star target): synthetic dense symmetric 65536x65536 "
+                            "(bf16 operator), geometric spectrum, top-64, k=128, to FP64 residual 1e-8 by a "
+                            "four-rung basis ladder: fp32 basis with 2 then 3 bf16 slices on the bf16 tensor cores "
+                            "-> fp64 with ~30-bit then FP64-accurate int8 Ozaki products, A-pass reuse"),
+    "c2-ladder3": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-8, policy="full-f64",
+                       ladder=("full-f32", "full-f64-lite"), switch=(1e-4, 1e-6), reuse=True,
+                       name="as c3-ladder3 at C2's size (16384^2, top-32, k=64)"),
     "c3-f64-reuse": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64", reuse=True,
                          name="as c3-f64 (fp64 basis throughout, to 1e-8), with A-pass reuse (IterConfig.reuse_av)"),
     # sigma_i = 0.9^i puts sigma_100 = 2.7e-5 below the noise level (1e-4 sigma_1), so no basis
@@ -304,8 +319,17 @@ def make_iter_config(p, cfg):
     return p.IterConfig(k=cfg["k"], m=cfg.get("m", MAX_OUTER), iter=1, basis_method=p.BasisMethod.HESS_LEFT,
                         projection="ofrr", policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=cfg["tol"],
                         top=cfg["top"] if cfg["tol"] is not None else None,
-                        ladder=p.POLICY_PRESETS[cfg["ladder"]] if cfg.get("ladder") else None,
-                        ladder_switch=cfg.get("switch", 1e-4), reuse_av=bool(cfg.get("reuse", False)))
+                        ladder=_ladder(p, cfg.get("ladder")), ladder_switch=cfg.get("switch", 1e-4),
+                        reuse_av=bool(cfg.get("reuse", False)))
+
+
+def _ladder(p, spec):
+    """A ladder preset name, or a tuple of names (one rung each)."""
+    if not spec:
+        return None
+    if isinstance(spec, (tuple, list)):
+        return tuple(p.POLICY_PRESETS[s] for s in spec)
+    return p.POLICY_PRESETS[spec]
 
 
 def _dtype(cfg) -> str:

@@ -94,6 +94,13 @@ int ofrr_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, i
                        const float* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt,
                        double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
                        void* workspace, size_t workspace_bytes, void* stream);
+/* The same with 2 or 3 bf16 slices of the fp32 block: slices = 2 keeps a 16-bit significand
+ * (x_hi + x_mid; N = 2k, HBM-bound for k <= 125) -- the products of the full-f32-lite ladder
+ * rung; slices = 3 is ofrr_gemm_av_split. */
+int ofrr_gemm_av_split_slices(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
+                              const float* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt,
+                              double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2, int slices,
+                              void* workspace, size_t workspace_bytes, void* stream);
 
 /* Kernel-only timing of the K1 tensor-core kernel (measurement support): while enabled,
  * every k_gemm_av_tc launch is bracketed by CUDA events on its stream; read returns the
@@ -259,6 +266,14 @@ int ofrr_ozaki_gemm(const void* A, int64_t rows, int64_t cols, int64_t lda, int 
                     const void* op_ws, const double* X, int64_t ldx, int k, void* W, int64_t ldw,
                     int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
                     void* workspace, size_t workspace_bytes, void* stream);
+/* The same product with a chosen accuracy: levels = 6 is ofrr_ozaki_gemm (digit products
+ * with p + q < 6, ~2^-46 of |A||x| per term); levels = 4 keeps p + q < 4 (~2^-30 per term,
+ * ~40% of the int8 work, 128 columns per pass) -- the products of the full-f64-lite ladder
+ * rung, which hands over to full FP64 before the residuals need more. */
+int ofrr_ozaki_gemm_levels(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
+                           const void* op_ws, const double* X, int64_t ldx, int k, void* W, int64_t ldw,
+                           int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
+                           int levels, void* workspace, size_t workspace_bytes, void* stream);
 int ofrr_ozaki_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
                         const void* op_ws, const double* Xv, int64_t ldx, const double* Yv,
                         int64_t ldy, const double* vals, const int* r_dev, int r_max, double* res,

@@ -41,6 +41,8 @@ _SIGS = {
     "ofrr_gemm_av_split_workspace": ([c_i64, c_i64, c_int], c_sz),
     "ofrr_gemm_av_split": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_vp,
                             c_vp, c_i64, c_int, c_vp, c_sz, c_vp], c_int),
+    "ofrr_gemm_av_split_slices": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp,
+                                   c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_sz, c_vp], c_int),
     "ofrr_residual_estimate_workspace": ([c_i64, c_int], c_sz),
     "ofrr_residual_estimate": ([c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_i64, c_int, c_vp, c_int, c_vp, c_vp,
                                 c_int, c_vp, c_int, c_vp, c_sz, c_vp], c_int),
@@ -78,6 +80,8 @@ _SIGS = {
     "ofrr_ozaki_operator_workspace": ([c_i64, c_i64], c_sz),
     "ofrr_ozaki_workspace": ([c_i64, c_i64, c_int], c_sz),
     "ofrr_ozaki_operator_info": ([c_vp, c_i64, c_vp, c_vp], c_int),
+    "ofrr_ozaki_gemm_levels": ([c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp,
+                                c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_sz, c_vp], c_int),
     "ofrr_orthonormalize_workspace": ([c_i64, c_int], c_sz),
     "ofrr_orthonormalize": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_int, c_dbl, c_int, c_int, c_vp, c_i64, c_vp,
                              c_vp, c_vp, c_sz, c_vp], c_int),

@@ -15,7 +15,7 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
 size_t split_workspace(int64_t rows, int64_t cols, int k);
 int tc_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, const float* X, int64_t ldx, int k,
                      void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes,
-                     cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2);
+                     cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2, int slices);
 int simt_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const void* X,
                  int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, cudaStream_t st,
                  void* W2, int64_t ldw2, int out_fmt2);
@@ -39,7 +39,7 @@ int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fm
 int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws, const double* V,
               int64_t ldv, int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W,
               int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
-              double** part_out, void* ws, size_t ws_bytes, cudaStream_t st);
+              double** part_out, void* ws, size_t ws_bytes, cudaStream_t st, int levels);
 int oz_nblocks(int64_t rows);
 int residual_reduce(const double* part, int nblocks, int n, const double* vals, const int* r_dev, double* res,
                     int mode, cudaStream_t st);
@@ -137,14 +137,28 @@ int ofrr_gemm_av2(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
 
 size_t ofrr_gemm_av_split_workspace(int64_t rows, int64_t cols, int k) { return split_workspace(rows, cols, k); }
 
-int ofrr_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const float* X, int64_t ldx,
+static int gemm_av_split_impl(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const float* X, int64_t ldx,
                        int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2,
-                       int out_fmt2, void* workspace, size_t workspace_bytes, void* stream) {
+                       int out_fmt2, void* workspace, size_t workspace_bytes, void* stream, int slices) {
   if (a_fmt != BF16) { ofrr_set_error("gemm_av_split: A must be bf16"); return OFRR_ERR_UNSUPPORTED; }
   if (rows <= 0 || cols <= 0 || k <= 0) return OFRR_OK;
   if ((lda * 2) % 16) { ofrr_set_error("gemm_av_split: lda must be a multiple of 8"); return OFRR_ERR_INVALID; }
   return tc_gemm_av_split(A, rows, cols, lda, X, ldx, k, W, ldw, out_fmt, colmax, flags, workspace, workspace_bytes,
-                          S(stream), W2, ldw2, out_fmt2);
+                          S(stream), W2, ldw2, out_fmt2, slices);
+}
+
+int ofrr_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const float* X, int64_t ldx,
+                       int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2,
+                       int out_fmt2, void* workspace, size_t workspace_bytes, void* stream) {
+  return gemm_av_split_impl(A, rows, cols, lda, a_fmt, X, ldx, k, W, ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
+                            workspace, workspace_bytes, stream, 3);
+}
+int ofrr_gemm_av_split_slices(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const float* X,
+                              int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax, int* flags,
+                              void* W2, int64_t ldw2, int out_fmt2, int slices, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  return gemm_av_split_impl(A, rows, cols, lda, a_fmt, X, ldx, k, W, ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
+                            workspace, workspace_bytes, stream, slices);
 }
 
 int ofrr_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, int transpose, const void* X,
@@ -244,7 +258,16 @@ int ofrr_ozaki_gemm(const void* A, int64_t rows, int64_t cols, int64_t lda, int 
                     void* stream) {
   if (!valid_fmt(out_fmt) || !valid_fmt(out_fmt2) || k <= 0 || !W) { ofrr_set_error("ozaki_gemm: invalid arguments"); return OFRR_ERR_INVALID; }
   return ozx_apply(A, rows, cols, lda, a_fmt, op_ws, X, ldx, k, nullptr, nullptr, nullptr, 0, W, ldw, out_fmt, colmax,
-                   flags, W2, ldw2, out_fmt2, nullptr, workspace, workspace_bytes, S(stream));
+                   flags, W2, ldw2, out_fmt2, nullptr, workspace, workspace_bytes, S(stream), 6);
+}
+
+int ofrr_ozaki_gemm_levels(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws,
+                           const double* X, int64_t ldx, int k, void* W, int64_t ldw, int out_fmt, double* colmax,
+                           int* flags, void* W2, int64_t ldw2, int out_fmt2, int levels, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  if (!valid_fmt(out_fmt) || !valid_fmt(out_fmt2) || k <= 0 || !W) { ofrr_set_error("ozaki_gemm: invalid arguments"); return OFRR_ERR_INVALID; }
+  return ozx_apply(A, rows, cols, lda, a_fmt, op_ws, X, ldx, k, nullptr, nullptr, nullptr, 0, W, ldw, out_fmt, colmax,
+                   flags, W2, ldw2, out_fmt2, nullptr, workspace, workspace_bytes, S(stream), levels);
 }
 
 int ofrr_ozaki_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws,
@@ -253,7 +276,7 @@ int ofrr_ozaki_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, 
                         size_t workspace_bytes, void* stream) {
   double* part = nullptr;
   int rc = ozx_apply(A, rows, cols, lda, a_fmt, op_ws, Xv, ldx, r_max, vals, r_dev, Yv, ldy, nullptr, 0, F64, nullptr,
-                     nullptr, nullptr, 0, F64, &part, workspace, workspace_bytes, S(stream));
+                     nullptr, nullptr, 0, F64, &part, workspace, workspace_bytes, S(stream), 6);
   if (rc) return rc;
   return residual_reduce(part, oz_nblocks(rows), r_max, vals, r_dev, res, accumulate_max, S(stream));
 }

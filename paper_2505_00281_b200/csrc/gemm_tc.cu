@@ -627,8 +627,10 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
 // residues are exact in fp32, so the three slices carry the full 24-bit significand and
 // A (bf16) times each slice is an exact-product, fp32-accumulated tensor-core product.
 // ---------------------------------------------------------------------------------
+// slices = 2 ("lite": x_hi + x_mid, a 16-bit significand, N = 2k) keeps the product at the
+// HBM roofline for k <= 125 (N <= 251 flop/B at bf16) where 3 slices are tensor-bound.
 __global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n, int k,
-                             __nv_bfloat16* __restrict__ Xs, int64_t lds) {
+                             __nv_bfloat16* __restrict__ Xs, int64_t lds, int slices) {
   const int j = blockIdx.y;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float x = X[(int64_t)j * ldx + i];
@@ -638,40 +640,47 @@ __global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n
     const float r2 = r1 - __bfloat162float(m);
     Xs[(int64_t)j * lds + i] = h;
     Xs[(int64_t)(k + j) * lds + i] = m;
-    Xs[(int64_t)(2 * k + j) * lds + i] = __float2bfloat16_rn(r2);
+    if (slices == 3) Xs[(int64_t)(2 * k + j) * lds + i] = __float2bfloat16_rn(r2);
   }
 }
 
 // columns per pass: 3 * 170 = 510 <= 512 (one pass over A up to k = 170; the wide tile
-// for 85 < k, the two-M-half tile up to 85)
+// for 85 < k, the two-M-half tile up to 85); 2 slices: 2 * 256
 static constexpr int SPLIT_KC = 170;
+static int split_kc(int slices) { return slices == 2 ? 256 : SPLIT_KC; }
 
 size_t split_workspace(int64_t rows, int64_t cols, int k) {
-  const int kc = std::min(k, SPLIT_KC);
-  const int64_t lds = (cols + 63) / 64 * 64;
-  return (size_t)3 * kc * lds * 2 + 1024 + tc_workspace(rows, cols, 3 * kc, BF16);
+  size_t best = 0;
+  for (int slices = 2; slices <= 3; ++slices) {
+    const int kc = std::min(k, split_kc(slices));
+    const int64_t lds = (cols + 63) / 64 * 64;
+    best = std::max(best, (size_t)slices * kc * lds * 2 + 1024 + tc_workspace(rows, cols, slices * kc, BF16));
+  }
+  return best;
 }
 
 // k <= 170: one pass over A with N = 3k.  k > 170: column chunks of <= 170, one pass each
 // (full fp32 semantics at the price of ceil(k / 170) passes).
 int tc_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, const float* X, int64_t ldx, int k,
                      void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes,
-                     cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2) {
+                     cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2, int slices) {
+  if (slices != 2 && slices != 3) { ofrr_set_error("gemm_av split: slices must be 2 or 3"); return OFRR_ERR_INVALID; }
   if (ws_bytes < split_workspace(rows, cols, k)) { ofrr_set_error("gemm_av split: workspace too small"); return OFRR_ERR_INVALID; }
   const int64_t lds = (cols + 63) / 64 * 64;
-  const int kcmax = std::min(k, SPLIT_KC);
+  const int KC = split_kc(slices);
+  const int kcmax = std::min(k, KC);
   __nv_bfloat16* Xs = (__nv_bfloat16*)ws;
-  uint8_t* rest = (uint8_t*)ws + (((size_t)3 * kcmax * lds * 2 + 1023) & ~size_t(1023));
+  uint8_t* rest = (uint8_t*)ws + (((size_t)slices * kcmax * lds * 2 + 1023) & ~size_t(1023));
   const size_t rest_bytes = ws_bytes - (rest - (uint8_t*)ws);
   const int ob = fmt_bytes(out_fmt), ob2 = fmt_bytes(out_fmt2);
-  for (int j0 = 0; j0 < k; j0 += SPLIT_KC) {
-    const int kc = std::min(SPLIT_KC, k - j0);
+  for (int j0 = 0; j0 < k; j0 += KC) {
+    const int kc = std::min(KC, k - j0);
     unsigned gx = (unsigned)std::min<int64_t>((cols + 255) / 256, 64);
-    k_split_bf16<<<dim3(gx, kc), 256, 0, st>>>(X + (int64_t)j0 * ldx, ldx, cols, kc, Xs, lds);
+    k_split_bf16<<<dim3(gx, kc), 256, 0, st>>>(X + (int64_t)j0 * ldx, ldx, cols, kc, Xs, lds, slices);
     OFRR_CHECK_LAUNCH();
-    const int rc = tc_gemm_av(A, rows, cols, lda, BF16, Xs, lds, 3 * kc, (uint8_t*)W + (size_t)j0 * ldw * ob, ldw,
-                              out_fmt, colmax ? colmax + j0 : nullptr, flags, rest, rest_bytes, st,
-                              W2 ? (uint8_t*)W2 + (size_t)j0 * ldw2 * ob2 : nullptr, ldw2, out_fmt2, 3);
+    const int rc = tc_gemm_av(A, rows, cols, lda, BF16, Xs, lds, slices * kc, (uint8_t*)W + (size_t)j0 * ldw * ob,
+                              ldw, out_fmt, colmax ? colmax + j0 : nullptr, flags, rest, rest_bytes, st,
+                              W2 ? (uint8_t*)W2 + (size_t)j0 * ldw2 * ob2 : nullptr, ldw2, out_fmt2, slices);
     if (rc) return rc;
   }
   return OFRR_OK;

@@ -693,16 +693,18 @@ __global__ void __launch_bounds__(256)
   const int cnt = tcnt[row];
   const int mc = lane < cnt ? tcol[row * OZ_TAIL_CAP + lane] : 0;
   const double mv = lane < cnt ? (double)tval[row * OZ_TAIL_CAP + lane] : 0.0;
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};                // columns lane + 32 t, BN <= 128
   for (int e = 0; e < cnt; ++e) {
     const int c = __shfl_sync(0xffffffffu, mc, e);
     const double v = __shfl_sync(0xffffffffu, mv, e);
     const double* vr = Vt + (int64_t)c * ldvt + j0;
-    if (lane < ncols) acc0 = fma(v, vr[lane], acc0);
-    if (lane + 32 < ncols) acc1 = fma(v, vr[lane + 32], acc1);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (lane + 32 * t < ncols) acc[t] = fma(v, vr[lane + 32 * t], acc[t]);
   }
-  if (lane < BN) Wt[row * BN + lane] = acc0;
-  if (lane + 32 < BN) Wt[row * BN + lane + 32] = acc1;
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+    if (lane + 32 * t < BN) Wt[row * BN + lane + 32 * t] = acc[t];
 }
 
 // V (fp64, column j contiguous with ld ldv, n rows x r columns) -> Vt row-major (row l holds
@@ -741,17 +743,21 @@ static constexpr int OZK_THREADS = 192 + 32 * OZK_CONV_WARPS;
 // to 6 products of |d| <= 255 * 128 per term -- 6 * 32640 * 8192 < 2^31
 static constexpr int OZK_MAXCHUNK = 128;
 
-template <int BN, int NP = OZ_D>
+// NL = accumulation levels kept (digit products with p + q < NL): 6 -> ~2^-46 of |A||x| per
+// term (FP64-accurate); 4 -> ~2^-30 (the "lite" products of the full-f64-lite rung), which
+// frees TMEM for BN = 128 columns per launch (4 levels x 128 = 512 TMEM columns).
+template <int BN, int NP = OZ_D, int NL = OZ_D>
 struct OzkCfg {
   static constexpr int A_TILE = OZ_TM * OZK_KB;         // 8 KB per digit plane
   static constexpr int A_SET = NP * A_TILE;             // NP digit planes per k-block (48 / 24 KB)
-  static constexpr int V_SET = OZ_D * BN * OZK_KB;      // six V digit tiles per k-block
+  static constexpr int V_SET = NL * BN * OZK_KB;        // the NL V digit tiles a product needs
   // the 3-digit heads free half of each A stage: deeper rings on both operands
-  static constexpr int A_STAGES = NP == OZ_D ? 3 : 5;
-  static constexpr int V_STAGES = NP == OZ_D ? 2 : (BN == 64 ? 3 : 4);
-  static constexpr int TMEM_COLS = OZ_D * BN <= 256 ? 256 : 512;
+  static constexpr int A_STAGES = NP == OZ_D ? 3 : (BN == 128 ? 4 : 5);
+  static constexpr int V_STAGES = NP == OZ_D ? 2 : (BN == 128 ? 2 : (BN == 64 ? 3 : 4));
+  static constexpr int TMEM_COLS = NL * BN <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = 1024 + A_STAGES * A_SET + V_STAGES * V_SET + 256;
   static_assert(SMEM_BYTES <= 227 * 1024, "ozk shared memory");
+  static_assert(NL * BN <= 512, "ozk TMEM");
 };
 
 // UMMA shared-memory descriptor: K-major, 64B swizzle, 8-row groups 512 B apart
@@ -809,13 +815,13 @@ __device__ __forceinline__ float ozk_elem(const uint4 (&raw)[4], int e) {
 // Both variants are launched back to back; the one that does not match the operator's
 // `full` flag (set by its prepare pass) exits at once -- the choice stays on the device
 // (CUDA graphs) and the MMA issue loop stays fully unrolled.
-template <int FMT, int BN, int NP>
+template <int FMT, int BN, int NP, int NL>
 __global__ void __launch_bounds__(OZK_THREADS, 1)
     k_ozk_gemm(const void* __restrict__ A, int64_t rows, int64_t cols, int64_t lda, const int* __restrict__ Tg,
                const __grid_constant__ CUtensorMap tmV, double* __restrict__ ws, int kbc, int nchunks,
                long long total_units, int max_slots, int npad, int col0, int stamp,
                const int* __restrict__ full_flag) {
-  using C = OzkCfg<BN, NP>;
+  using C = OzkCfg<BN, NP, NL>;
   constexpr bool full = NP == OZ_D;
   if (full_flag != nullptr && ((*full_flag != 0) != full)) return;
   if (stamp && threadIdx.x == 0) atomicMin(&g_oz_stamp[0], oz_gtimer_ns());
@@ -863,7 +869,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
         if (++rem == kbc) { rem = 0; ++vt; }
         mbar_wait(&vempty[vs], vph ^ 1);
         mbar_expect_tx(&vfull[vs], C::V_SET);
-        for (int q = 0; q < OZ_D; ++q)
+        for (int q = 0; q < NL; ++q)
           tma_load_2d(vbuf + vs * C::V_SET + q * BN * OZK_KB, &tmV, kb * OZK_KB, q * npad + col0, &vfull[vs], pol_v);
         if (++vs == C::V_STAGES) { vs = 0; vph ^= 1; }
       }
@@ -886,9 +892,10 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(abuf + as * C::A_SET);
           const uint64_t dv = umma_desc_sw64(smem_u32(vbuf + vs * C::V_SET));
-          for (int p = 0; p < NP; ++p) {
+#pragma unroll
+          for (int p = 0; p < (NP < NL ? NP : NL); ++p) {
             const uint64_t da = umma_desc_sw64(sa + p * C::A_TILE);
-            const int nq = OZ_D - p;
+            const int nq = NL - p;
             // both K halves of a k-block back to back on the same accumulator columns
             for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
               const int ng = std::min(256 / BN, nq - q0);
@@ -928,7 +935,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) s[i] = 0.0;
 #pragma unroll 1
-        for (int lv = OZ_D - 1; lv >= 0; --lv) {
+        for (int lv = NL - 1; lv >= 0; --lv) {
           int d[16];
           tmem_ld16i(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(lv * BN + c0), d);
           const double w = ldexp(1.0, -8 * lv - 12);
@@ -1363,10 +1370,10 @@ struct OzkPlan {
   size_t off_F, off_dig, off_ws, off_part, off_vt, off_wt, bytes;
 };
 
-static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r) {
+static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r, int levels = OZ_D) {
   OzkPlan p;
   r = std::max(r, 1);
-  p.bn = r <= 32 ? 32 : 64;
+  p.bn = levels == OZ_D ? (r <= 32 ? 32 : 64) : (r <= 64 ? 64 : 128);
   p.npass = (r + p.bn - 1) / p.bn;
   p.npad = p.npass * p.bn;
   p.rows_pad = (rows + OZ_TM - 1) / OZ_TM * OZ_TM;
@@ -1394,29 +1401,30 @@ static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r) {
   return p;
 }
 
-template <int FMT, int BN>
+template <int FMT, int BN, int NL>
 static int ozk_launch(const void* A, int64_t rows, int64_t cols, int64_t lda, const int* T, const CUtensorMap& tV,
                       const OzkPlan& p, double* ws, int col0, const int* full, cudaStream_t st) {
-  using C3 = OzkCfg<BN, 3>;
-  using C = OzkCfg<BN>;
+  using C3 = OzkCfg<BN, 3, NL>;
+  using C = OzkCfg<BN, OZ_D, NL>;
   static std::once_flag attr;
   cudaError_t ae = cudaSuccess;
   std::call_once(attr, [&] {
-    ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM_BYTES);
+    ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, 3, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM_BYTES);
     if (ae == cudaSuccess)
-      ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, OZ_D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+      ae = cudaFuncSetAttribute(k_ozk_gemm<FMT, BN, OZ_D, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM_BYTES);
   });
   OFRR_CUDA_TRY(ae);
   const int stamp = g_oz_stamp_on ? 1 : 0;
   if (full) {
-    k_ozk_gemm<FMT, BN, 3><<<p.grid, OZK_THREADS, C3::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
-                                                                       p.nchunks, p.total, p.max_slots, p.npad, col0,
-                                                                       stamp, full);
+    k_ozk_gemm<FMT, BN, 3, NL><<<p.grid, OZK_THREADS, C3::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
+                                                                           p.nchunks, p.total, p.max_slots, p.npad,
+                                                                           col0, stamp, full);
     OFRR_CHECK_LAUNCH();
   }
-  k_ozk_gemm<FMT, BN, OZ_D><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
-                                                                       p.nchunks, p.total, p.max_slots, p.npad, col0,
-                                                                       stamp, full);
+  k_ozk_gemm<FMT, BN, OZ_D, NL><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
+                                                                           p.nchunks, p.total, p.max_slots, p.npad,
+                                                                           col0, stamp, full);
   OFRR_CHECK_LAUNCH();
   return OFRR_OK;
 }
@@ -1430,7 +1438,9 @@ static bool oz_no_tails() {     // OFRR_OZ_FULL=1: all six digits of A in every 
   return v == 1;
 }
 size_t ozx_prod_ws(int64_t rows, int64_t cols, int r) {
-  return oz_use_planes() ? oz_plan(rows, cols, r).bytes : ozk_plan(rows, cols, r).bytes;
+  // sized for either product accuracy (6 levels, 64-column passes; 4 levels, 128-column passes)
+  return oz_use_planes() ? oz_plan(rows, cols, r).bytes
+                         : std::max(ozk_plan(rows, cols, r).bytes, ozk_plan(rows, cols, r, 4).bytes);
 }
 
 int ozx_info(const void* op_ws, int64_t rows, int* full, long long* tails) {
@@ -1488,11 +1498,12 @@ int ozx_prepare(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fm
 int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt, const void* op_ws, const double* V,
               int64_t ldv, int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W,
               int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
-              double** part_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+              double** part_out, void* ws, size_t ws_bytes, cudaStream_t st, int levels) {
+  if (levels != OZ_D && levels != 4) { ofrr_set_error("ozaki: levels must be 6 or 4 (got %d)", levels); return OFRR_ERR_INVALID; }
   if (oz_use_planes())
     return oz_apply(op_ws, rows, cols, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, out_fmt, colmax, flags, W2, ldw2,
                     out_fmt2, part_out, ws, ws_bytes, st);
-  const OzkPlan p = ozk_plan(rows, cols, r);
+  const OzkPlan p = ozk_plan(rows, cols, r, levels);
   if (!ws || ws_bytes < p.bytes) { ofrr_set_error("ozaki: workspace too small (%zu < %zu)", ws_bytes, p.bytes); return OFRR_ERR_INVALID; }
   const OzOpLayout OL = oz_op_layout(rows);
   const uint8_t* ob = (const uint8_t*)op_ws;
@@ -1519,8 +1530,12 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
   for (int ps = 0; ps < p.npass; ++ps) {
     const int j0 = ps * p.bn;
 #define OZK_CASE(F)                                                                              \
-    rc = p.bn == 32 ? ozk_launch<F, 32>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)         \
-                    : ozk_launch<F, 64>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);
+    if (levels == OZ_D)                                                                          \
+      rc = p.bn == 32 ? ozk_launch<F, 32, OZ_D>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)  \
+                      : ozk_launch<F, 64, OZ_D>(A, rows, cols, lda, T, tV, p, pws, j0, full, st); \
+    else                                                                                         \
+      rc = p.bn == 64 ? ozk_launch<F, 64, 4>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)     \
+                      : ozk_launch<F, 128, 4>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);
     if (a_fmt == BF16) { OZK_CASE(BF16) } else if (a_fmt == F16) { OZK_CASE(F16) } else { OZK_CASE(FP8) }
 #undef OZK_CASE
     if (rc) return rc;
@@ -1546,7 +1561,7 @@ int oz_product(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
   int rc = ozx_prepare(A, rows, cols, lda, a_fmt, ws, opb, st);
   if (rc) return rc;
   return ozx_apply(A, rows, cols, lda, a_fmt, ws, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, F64, nullptr, nullptr,
-                   nullptr, 0, F64, part_out, (uint8_t*)ws + opb, ws_bytes - opb, st);
+                   nullptr, 0, F64, part_out, (uint8_t*)ws + opb, ws_bytes - opb, st, OZ_D);
 }
 
 }  // namespace ofrr

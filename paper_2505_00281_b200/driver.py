@@ -51,8 +51,10 @@ class IterConfig:
     seed: int = 0
     tol: Optional[float] = None   # extension: stop when max residual over `top` < tol
     top: Optional[int] = None     # extension: number of leading pairs checked
-    ladder: Optional[PrecisionPolicy] = None   # extension: cheaper policy run first (see below)
-    ladder_switch: float = 1e-3   # ... until its residual estimate falls below this (or stalls)
+    ladder: Optional[PrecisionPolicy] = None   # extension: cheaper policy run first (see below); or a
+    #                               tuple of policies, cheapest first (one rung each)
+    ladder_switch: float = 1e-3   # ... until its residual estimate falls below this (or stalls); a tuple
+    #                               with one threshold per rung when ladder is a tuple
     reuse_av: bool = False        # extension: next power step from the projection, A U Y = W Y (one
     #                               A pass per outer iteration instead of iter + 1; see EigEngine)
 
@@ -67,6 +69,10 @@ class IterConfig:
             raise ValueError("top must be in [1, k]")
         if self.ladder is not None and self.tol is None:
             raise ValueError("a precision ladder needs tol (it switches on the residual estimate)")
+        if isinstance(self.ladder, (tuple, list)):
+            sw = self.ladder_switch
+            if not isinstance(sw, (tuple, list)) or len(sw) != len(self.ladder):
+                raise ValueError("a multi-rung ladder needs one ladder_switch per rung")
 
     @property
     def mv_policy(self) -> PrecisionPolicy:
@@ -289,7 +295,8 @@ class EigEngine:
             colmax = torch.zeros(k, dtype=torch.float64, device=self.device)
             W = ops.new_block(self.A_mv.rows, k, self.mv.storage, self.device)
             ops.gemm_av(self.A_mv, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1],
-                        **({"oz": self._block_oz(self.A_mv, X)} if self.ops is _ops else {}))
+                        **({"oz": self._block_oz(self.A_mv, X), "levels": self.mv.product_levels}
+                           if self.ops is _ops else {}))
             self.stats.a_passes += 1
             comm.all_reduce_max_(colmax)
             ops.scale_columns(W, colmax, self.mv.compute)
@@ -347,7 +354,8 @@ class EigEngine:
             acc = FpFormat.F64 if FpFormat.F64 in (self.A_pol.fmt, U.fmt) else FpFormat.F32
             W2 = ops.new_block(self.A_pol.rows, kp, acc, self.device)
         ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2,
-                    **({"oz": self._block_oz(self.A_pol, U)} if self.ops is _ops else {}))
+                    **({"oz": self._block_oz(self.A_pol, U), "levels": self.pol.product_levels}
+                       if self.ops is _ops else {}))
         self.stats.a_passes += 1
         self._last_w2 = W2
         Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U
@@ -675,9 +683,9 @@ class EigEngine:
             return RitzSet(rs.values, rs.vectors, "eig", residuals=res.cpu().numpy()[:r])
         return self.report(U64, eig, r, vals)
 
-    @staticmethod
-    def _w2_is_fp64(W2, U) -> bool:
-        return W2 is not None and W2.fmt == FpFormat.F64 and W2.k >= U.k
+    def _w2_is_fp64(self, W2, U) -> bool:
+        """W2 = A U is an FP64-accurate product (fp64 block, full-accuracy K7z or fp64 FMA)."""
+        return W2 is not None and W2.fmt == FpFormat.F64 and W2.k >= U.k and self.pol.product_levels == 6
 
     def residuals_from_w(self, U, W2, eig, r: int):
         """FP64 residuals ||A u_j - lambda_j u_j|| / |lambda_j| of the Ritz vectors u_j = U y_j
@@ -757,7 +765,8 @@ class EigEngine:
 
     def _graph_key(self, check: bool, top: int, first: bool = True):
         A, B = self.A_mv, self.A_pol
-        pol = lambda p: (int(p.storage), int(p.compute), int(p.accumulate), float(p.drop_tol))  # noqa: E731
+        pol = lambda p: (int(p.storage), int(p.compute), int(p.accumulate), float(p.drop_tol),  # noqa: E731
+                         int(p.product_levels))
         from . import _lib
         return (A.t.data_ptr(), A.rows, A.cols, A.lda, int(A.fmt), B.t.data_ptr(), B.rows, B.cols, B.lda, int(B.fmt),
                 self.n, self.cfg.k, self.cfg.iter, pol(self.pol), pol(self.mv), check, top, self.device.index,
@@ -903,32 +912,47 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
     hist, iters, passes = [], 0, 0
     if cfg.ladder is not None:
         prepared = _prepare_ahead(a, cfg, comm)
-        # precision ladder: run the cheaper policy while it makes
-        # progress, then continue from its restart block in cfg.policy
+        # precision ladder: run the cheaper policies while they make
+        # progress, each continuing from the previous rung's restart block, then cfg.policy
         from dataclasses import replace as _replace
-        low = _replace(cfg, policy=cfg.ladder, matvec_policy=None, ladder=None)
-        with _ph("rung_low"):
-            eng0 = EigEngine(a, low, comm=comm, n_global=n, report_scales=False)
-            X0 = eng0.run(stop_estimate=cfg.ladder_switch)
-            # hand the fp64 rung the fp32 rung's next iterate (W Y, power step made) instead of
-            # its Ritz vectors?  Measured at C3: one FP64 pass fewer but one iteration more
-            # (the rung then starts from an fp32-accurate A.U) -- slower, so off by default
-            stepped = HANDOVER_STEPPED and getattr(eng0, "handover", None) is not None
-            if stepped:
+        rungs = list(cfg.ladder) if isinstance(cfg.ladder, (tuple, list)) else [cfg.ladder]
+        switches = list(cfg.ladder_switch) if isinstance(cfg.ladder_switch, (tuple, list)) else [cfg.ladder_switch]
+        rung_stats = []
+        for pol_r, sw in zip(rungs, switches):
+            low = _replace(cfg, policy=pol_r, matvec_policy=None, ladder=None, ladder_switch=1e-3,
+                           m=max(1, cfg.m - iters))
+            with _ph("rung_low"):
+                eng0 = EigEngine(a, low, comm=comm, n_global=n, report_scales=False,
+                                 prepared=prepared if FpFormat.F64 == pol_r.storage else None)
+                out = eng0.run(X0=X0, stop_estimate=sw, stepped=X0 is not None and stepped)
+            if isinstance(out, RitzSet):                               # m exhausted in a low rung
+                if stats is not None:
+                    stats.__dict__.update(eng0.stats.__dict__)
+                    stats.rungs = rung_stats + [(cfg_rung_label(low), eng0.stats.iterations, eng0.stats.a_passes)]
+                    stats.iterations += iters
+                    stats.a_passes += passes
+                    stats.history = hist + [(it + iters, w) for it, w in eng0.stats.history]
+                return out
+            X0 = out
+            # the next rung starts from this rung's next iterate (W Y, power step made) when this
+            # rung's products are far below its switch threshold (full-f32-lite at 1e-2,
+            # full-f64-lite at 1e-6): otherwise from its Ritz vectors (e.g. the full-f32 rung
+            # switches at its own product-accuracy floor, so its W Y would carry that noise)
+            stepped = sw >= 100 * _rung_floor(pol_r) and getattr(eng0, "handover", None) is not None
+            if stepped or (HANDOVER_STEPPED and getattr(eng0, "handover", None) is not None):
                 X0 = eng0.handover
-        if isinstance(X0, RitzSet):                                # m exhausted in the low rung
-            if stats is not None:
-                stats.__dict__.update(eng0.stats.__dict__)
-                stats.rungs = [(cfg_rung_label(low), eng0.stats.iterations, eng0.stats.a_passes)]
-            return X0
-        hist, iters, passes = list(eng0.stats.history), eng0.stats.iterations, eng0.stats.a_passes
-        cfg = _replace(cfg, ladder=None, m=max(1, cfg.m - iters))
+                stepped = True
+            hist += [(it + iters, w) for it, w in eng0.stats.history]
+            iters += eng0.stats.iterations
+            passes += eng0.stats.a_passes
+            rung_stats.append((cfg_rung_label(low), eng0.stats.iterations, eng0.stats.a_passes))
+        cfg = _replace(cfg, ladder=None, ladder_switch=1e-3, m=max(1, cfg.m - iters))
     with _ph("rung_main"):
         eng = EigEngine(a, cfg, comm=comm, n_global=n, prepared=prepared)
         rs = eng.run(X0=X0, stepped=X0 is not None and stepped)
     if stats is not None:
         stats.__dict__.update(eng.stats.__dict__)
-        stats.rungs = ([(cfg_rung_label(low), iters, passes)] if X0 is not None else []) + \
+        stats.rungs = (rung_stats if X0 is not None else []) + \
             [(cfg_rung_label(cfg), eng.stats.iterations, eng.stats.a_passes)]
         stats.iterations += iters
         stats.a_passes += passes
@@ -937,6 +961,14 @@ def _subspace_iter_eig(a, cfg, stats, comm, n_global) -> RitzSet:
 
 
 _SIDE_STREAMS = {}
+
+
+def _rung_floor(pol: PrecisionPolicy) -> float:
+    """The residual level a rung's block products can carry (measured at C3): fp32-accumulated
+    tensor-core products ~1e-4; the lite fp64 (~30-bit) products ~1e-8; FP64-accurate ~1e-13."""
+    if pol.storage == FpFormat.F64:
+        return 1e-13 if pol.product_levels == 6 else 1e-8
+    return 1e-4
 
 
 def _prepare_ahead(a, cfg: IterConfig, comm):
@@ -963,8 +995,9 @@ def _prepare_ahead(a, cfg: IterConfig, comm):
 
 
 def cfg_rung_label(cfg: IterConfig) -> str:
-    """Basis storage format of a rung (RunStats.rungs)."""
-    return FpFormat(cfg.policy.storage).name
+    """Basis storage format of a rung (RunStats.rungs); F64L: the lite fp64 rung."""
+    name = FpFormat(cfg.policy.storage).name
+    return name + "L" if cfg.policy.product_levels != 6 else name
 
 
 # -------------------------------------------------------------------------------------

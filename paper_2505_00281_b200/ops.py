@@ -310,19 +310,22 @@ class OzakiOperator:
         _count(1)
 
 
-def ozaki_gemm(oz: OzakiOperator, X: DevBlock, W: DevBlock, colmax=None, flags=None, W2: Optional[DevBlock] = None):
-    """W = A X for an fp64 block X, FP64-accurate (rounded to W.fmt)."""
+def ozaki_gemm(oz: OzakiOperator, X: DevBlock, W: DevBlock, colmax=None, flags=None, W2: Optional[DevBlock] = None,
+               levels: int = 6):
+    """W = A X for an fp64 block X, FP64-accurate (rounded to W.fmt); ``levels`` = 4: the
+    ~2^-30 lite product (ofrr_ozaki_gemm_levels)."""
     L = _lib.load()
     A = oz.A
     if X.fmt != FpFormat.F64:
         raise ValueError("ozaki_gemm: the block must be fp64")
     ws = _ws(L.ofrr_ozaki_workspace(A.rows, A.cols, X.k), A.device)
-    _lib.check(L.ofrr_ozaki_gemm(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), oz.ws.data_ptr(), X.ptr, X.ld, X.k, W.ptr,
-                                 W.ld, int(W.fmt),
-                                 _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
-                                 W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else int(W.fmt),
-                                 ws.data_ptr(), ws.numel(), _stream()), "ozaki_gemm")
-    _count(2 + (X.k + 63) // 64 * 4)     # digits of X, X row-major; per column pass: 2 product variants, tails, fixup
+    _lib.check(L.ofrr_ozaki_gemm_levels(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), oz.ws.data_ptr(), X.ptr, X.ld, X.k,
+                                        W.ptr, W.ld, int(W.fmt),
+                                        _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
+                                        W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else int(W.fmt),
+                                        int(levels), ws.data_ptr(), ws.numel(), _stream()), "ozaki_gemm")
+    bn = 64 if levels == 6 else 128
+    _count(2 + (X.k + bn - 1) // bn * 4)   # digits of X, X row-major; per column pass: 2 product variants, tails, fixup
 
 
 def ozaki_residual(oz: OzakiOperator, Xv: DevBlock, Yv: DevBlock, vals: torch.Tensor,
@@ -340,7 +343,8 @@ def ozaki_residual(oz: OzakiOperator, Xv: DevBlock, Yv: DevBlock, vals: torch.Te
 
 def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat] = None,
             colmax: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
-            transpose: bool = False, W2: Optional[DevBlock] = None, oz: Optional[OzakiOperator] = None) -> None:
+            transpose: bool = False, W2: Optional[DevBlock] = None, oz: Optional[OzakiOperator] = None,
+            levels: int = 6) -> None:
     """W = op(A) X rounded to out_fmt (default W.fmt); colmax[j] = max|W[:,j]|; optionally
     W2 = the same product in W2.fmt (e.g. the fp32 accumulator).  An fp64 block against a
     16/8-bit operator runs as an FP64-accurate int8 tensor-core product (``oz``: prepared
@@ -350,19 +354,21 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
     if X.fmt == FpFormat.F64 and A.fmt in OZAKI_FMTS and not transpose:
         if out_fmt is not None and FpFormat(out_fmt) != W.fmt:
             raise ValueError("gemm_av (fp64 block): out_fmt must be W's format")
-        ozaki_gemm(oz if oz is not None else OzakiOperator(A), X, W, colmax=colmax, flags=flags, W2=W2)
+        ozaki_gemm(oz if oz is not None else OzakiOperator(A), X, W, colmax=colmax, flags=flags, W2=W2, levels=levels)
         return
     ws_b = L.ofrr_gemm_av_workspace(A.rows, A.cols, k, int(A.fmt), int(transpose))
     ws = _ws(ws_b, A.device)
     of = int(W.fmt if out_fmt is None else out_fmt)
     split = A.fmt == FpFormat.BF16 and X.fmt == FpFormat.F32 and not transpose
+    slices = 2 if levels == 4 else 3
     if split:
-        # fp32 block on the bf16 tensor cores (3 bf16 slices, one pass over A)
+        # fp32 block on the bf16 tensor cores (3 bf16 slices -- 2 for the lite policy -- one
+        # pass over A)
         ws = _ws(L.ofrr_gemm_av_split_workspace(A.rows, A.cols, k), A.device)
-        _lib.check(L.ofrr_gemm_av_split(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), X.ptr, X.ld, k, W.ptr, W.ld, of,
-                                        _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
-                                        W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else of,
-                                        ws.data_ptr(), ws.numel(), _stream()), "gemm_av_split")
+        _lib.check(L.ofrr_gemm_av_split_slices(A.ptr, A.rows, A.cols, A.lda, int(A.fmt), X.ptr, X.ld, k, W.ptr, W.ld,
+                                               of, _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
+                                               W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else of,
+                                               slices, ws.data_ptr(), ws.numel(), _stream()), "gemm_av_split")
     else:
         if X.fmt != A.fmt:
             raise ValueError(f"gemm_av: block format {X.fmt.name} with operator format {A.fmt.name}")
@@ -373,9 +379,10 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
     if split or (A.fmt.tensor_core and not transpose):
         # algorithmic bytes of the tensor-core kernel: A once + the B operand
         # once (3 bf16 slices in split mode); W is written by the finalize kernel
-        chunks = [min(170, k - j0) for j0 in range(0, k, 170)] if split else [k]   # one launch per chunk
+        kcs = 256 if slices == 2 else 170
+        chunks = [min(kcs, k - j0) for j0 in range(0, k, kcs)] if split else [k]   # one launch per chunk
         for kc in chunks:
-            kb = 3 * kc if split else kc
+            kb = slices * kc if split else kc
             nb = A.rows * A.cols * A.fmt.itemsize + A.cols * kb * (2 if split else X.fmt.itemsize)
             _log_gemm((nb, 2.0 * A.rows * A.cols * kb))
     _count(3 if split else 2 if (A.fmt.tensor_core and not transpose) else 1)

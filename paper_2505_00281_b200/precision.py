@@ -119,6 +119,11 @@ class PrecisionPolicy:
     compute: FpFormat
     accumulate: FpFormat
     drop_tol_factor: float = 1.0
+    # extension: the accuracy tier of the split products on a 16/8-bit operator -- fp64 blocks
+    # (int8 Ozaki digits): 6 levels ~2^-46 of |A||x| per term, 4 levels ~2^-30 (full-f64-lite);
+    # fp32 blocks on bf16 (bf16 slices): 6 -> 3 slices (24-bit block), 4 -> 2 slices (16-bit,
+    # full-f32-lite).  Ladder rungs only; no effect on any other product.
+    product_levels: int = 6
 
     def __post_init__(self):
         object.__setattr__(self, "storage", FpFormat(self.storage))
@@ -128,6 +133,8 @@ class PrecisionPolicy:
             raise ValueError(
                 "precision policy must widen: storage <= compute <= accumulate"
             )
+        if self.product_levels not in (4, 6):
+            raise ValueError("product_levels must be 6 (FP64-accurate) or 4 (lite)")
 
     @property
     def drop_tol(self) -> float:
@@ -142,6 +149,9 @@ FULL_F64 = PrecisionPolicy(FpFormat.F64, FpFormat.F64, FpFormat.F64)
 TC_F16 = PrecisionPolicy(FpFormat.F16, FpFormat.F32, FpFormat.F32)
 TC_BF16 = PrecisionPolicy(FpFormat.BF16, FpFormat.F32, FpFormat.F32)
 TC_FP8 = PrecisionPolicy(FpFormat.FP8_E4M3, FpFormat.F32, FpFormat.F32)
+# extension: an fp64 basis whose products on a 16/8-bit operator keep ~30 bits (ladder rung)
+FULL_F64_LITE = PrecisionPolicy(FpFormat.F64, FpFormat.F64, FpFormat.F64, product_levels=4)
+FULL_F32_LITE = PrecisionPolicy(FpFormat.F32, FpFormat.F32, FpFormat.F32, product_levels=4)
 
 POLICY_PRESETS = {
     "native-f16": NATIVE_F16,
@@ -151,6 +161,8 @@ POLICY_PRESETS = {
     "tc-f16": TC_F16,
     "tc-bf16": TC_BF16,
     "tc-fp8": TC_FP8,
+    "full-f64-lite": FULL_F64_LITE,
+    "full-f32-lite": FULL_F32_LITE,
 }
 
 

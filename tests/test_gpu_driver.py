@@ -332,3 +332,26 @@ def test_device_loop_matches_host_loop(ofrr_gpu, pname, reuse):
         np.testing.assert_array_equal(rs.vectors.data, host_rs.vectors.data)
         assert [i for i, _ in st.history] == [i for i, _ in host_st.history]
     assert np.max(runs[-1][0].residuals[:top]) < tol
+
+
+def test_three_rung_ladder_to_fp64(ofrr_gpu):
+    """IterConfig.ladder as a tuple: fp32 -> full-f64-lite (~30-bit products) -> full-f64, the
+    lite rung handing its next iterate (W Y) over; converged to 1e-9 in FP64, the FP64 report
+    taken from the final rung's FP64-accurate W, and the values as exact as the 2-rung ladder."""
+    p = ofrr_gpu
+    n, top, k = 2048, 16, 32
+    lam = p.geometric_spectrum(n, top, k)
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    base = dict(k=k, m=40, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr", policy=p.FULL_F64,
+                seed=SEED, tol=1e-9, top=top, reuse_av=True)
+    st3, st2 = p.RunStats(), p.RunStats()
+    rs3 = p.subspace_iter_eig(A, p.IterConfig(ladder=(p.FULL_F32, p.POLICY_PRESETS["full-f64-lite"]),
+                                              ladder_switch=(1e-4, 1e-6), **base), stats=st3)
+    rs2 = p.subspace_iter_eig(A, p.IterConfig(ladder=p.FULL_F32, ladder_switch=1e-4, **base), stats=st2)
+    assert st3.converged and np.max(rs3.residuals[:top]) < 1e-9
+    assert [r[0] for r in st3.rungs] == ["F32", "F64L", "F64"]
+    np.testing.assert_allclose(rs3.values[:top], rs2.values[:top], rtol=1e-12)
+    # the returned residuals are FP64 residuals of the returned vectors
+    from paper_2505_00281_b200.projection import residual_report
+    indep = residual_report(A, rs3).residuals
+    np.testing.assert_allclose(rs3.residuals[:top], indep[:top], rtol=1e-3, atol=1e-13)

@@ -479,3 +479,48 @@ def test_ozaki_heads_and_tails(ofrr_gpu, oracle, case):
         # products weigh ~2^-40 of max|a_i.| sum|x| (the round-1 scheme's accuracy)
         bound = 2.0 ** -40 * np.max(np.abs(a), axis=1)[:, None] * np.sum(np.abs(x), axis=0)[None, :]
     assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
+
+
+def test_ozaki_lite_levels(ofrr_gpu, oracle):
+    """ofrr_ozaki_gemm_levels(levels=4): the digit products with p + q < 4 (128-column passes),
+    ~2^-30 of |A||X| per term; levels=6 stays FP64-accurate on the same inputs."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(44)
+    rows, cols, k = 500, 4000, 100
+    a = o.round_to(rng.standard_normal((rows, cols)), BF16)
+    x = rng.standard_normal((cols, k))
+    A = _op(p, a, BF16)
+    oz = ops.OzakiOperator(A)
+    X = _blk(p, x, F64)
+    ref = _exact_rows_dot(a, x)
+    mag = np.abs(a) @ np.abs(x)
+    for levels, rel in ((4, 2.0 ** -26), (6, 2.0 ** -44)):
+        W = ops.new_block(rows, k, p.FpFormat.F64, torch.device("cuda"))
+        ops.gemm_av(A, X, W, oz=oz, levels=levels)
+        err = np.abs(W.to_numpy_f64() - ref)
+        assert np.all(err <= rel * mag + 4 * np.spacing(np.abs(ref))), (levels, np.max(err / mag))
+    assert np.max(err / mag) < 2.0 ** -44
+
+
+def test_gemm_split_two_slices(ofrr_gpu, oracle):
+    """fp32 block on the bf16 tensor cores with 2 slices (the full-f32-lite rung): the block
+    carried to a 16-bit significand (x_hi + x_mid), exact products, fp32 sums."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(12)
+    rows, cols, k = 700, 3000, 96
+    a = o.round_to(rng.standard_normal((rows, cols)), BF16)
+    x = o.round_to(rng.standard_normal((cols, k)), F32)
+    A = _op(p, a, BF16)
+    X = _blk(p, x, F32)
+    hi = o.round_to(x, BF16)
+    x2 = hi + o.round_to(x - hi, BF16)                  # what two slices carry
+    mag = np.abs(a) @ np.abs(x)
+    for levels, xr, rel in ((4, x2, 2.0 ** -20), (6, x, 2.0 ** -20)):
+        W = ops.new_block(rows, k, p.FpFormat.F32, torch.device("cuda"))
+        ops.gemm_av(A, X, W, levels=levels)
+        assert np.all(np.abs(W.to_numpy_f64() - a @ xr) <= rel * mag), levels
+    assert np.max(np.abs(a @ x2 - a @ x) / mag) > 2.0 ** -20      # the two variants differ
