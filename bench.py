@@ -6,10 +6,11 @@ Default workload (every N): BASELINE configs[2] / SURVEY.md 8 "C3", the north-st
 synthetic dense symmetric 65536 x 65536 (bf16 operator, 8 GiB, HBM resident), geometric
 spectrum (rho = 0.1^(1/(k-top+1))), top-64 eigenpairs, k = 128, hess-l + ofrr, stopped when
 the FP64 relative residuals of the leading 64 pairs are below 1e-8.  The basis runs a
-precision ladder: fp32-accurate products on the bf16 tensor cores (K1, 3 bf16 slices of the
-block) until the residual estimate reaches 1e-3, then an fp64 basis whose block products are
-FP64-accurate int8 tensor-core products (K7z, Ozaki digits); A-pass reuse (IterConfig.reuse_av)
-makes every outer iteration after the first one A pass.  One step = one complete solve from
+three-rung precision ladder: fp32-accurate products on the bf16 tensor cores (K1, 3 bf16
+slices of the block) until the residual estimate reaches 1e-4, then an fp64 basis with
+~30-bit int8 Ozaki products (K7z, 4 levels) until 1e-6, then FP64-accurate K7z products (6
+levels), whose W = A U also yields the FP64 residual report; A-pass reuse
+(IterConfig.reuse_av) makes every outer iteration after the first one A pass.  One step = one complete solve from
 X0 until convergence is confirmed in FP64.  A (8 GiB) is larger than L2 (126 MB): no flush.
 
 N > 1: one process per GPU (NCCL).  `python bench.py --gpus N` without WORLD_SIZE re-launches
@@ -38,7 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SEED = 20240901
-DEFAULT_CONFIG = "c3-ladder-reuse"
+DEFAULT_CONFIG = "c3-ladder3"
 CONFIGS = {
     "c2": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-2, policy="full-f32",
                name="synthetic dense symmetric 16384x16384 (bf16 operator), geometric spectrum, top-32, k=64, "
@@ -195,7 +196,10 @@ def _ref_kernels():
         return oracle.mixed_gemm, "port", oracle
 
 
-_POL_CODES = {"F32": (1, 1, 1), "F64": (2, 2, 2), "BF16": (1, 1, 3), "F16": (1, 1, 0)}
+# the reference's gemm_mixed policy per rung label (lite rungs have no reference counterpart:
+# the reference computes them at the full format)
+_POL_CODES = {"F32": (1, 1, 1), "F32L": (1, 1, 1), "F64": (2, 2, 2), "F64L": (2, 2, 2), "BF16": (1, 1, 3),
+              "F16": (1, 1, 0)}
 
 
 def ref_pass_seconds(gemm, oracle, n: int, k: int, rung: str, rows: int, n_rows: int = None):

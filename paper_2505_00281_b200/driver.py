@@ -291,15 +291,20 @@ class EigEngine:
         import torch
         ops, comm = self.ops, self.comm
         k = X.k
+        fp8 = self.mv.storage == FpFormat.FP8_E4M3
         for _ in range(self.cfg.iter if steps is None else steps):
             colmax = torch.zeros(k, dtype=torch.float64, device=self.device)
-            W = ops.new_block(self.A_mv.rows, k, self.mv.storage, self.device)
+            # e4m3 storage (max 448): the product stays in fp32 until the column scaling, then
+            # is rounded once into e4m3 (per-column scaling; see _to_fp8)
+            W = ops.new_block(self.A_mv.rows, k, FpFormat.F32 if fp8 else self.mv.storage, self.device)
             ops.gemm_av(self.A_mv, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1],
                         **({"oz": self._block_oz(self.A_mv, X), "levels": self.mv.product_levels}
                            if self.ops is _ops else {}))
             self.stats.a_passes += 1
             comm.all_reduce_max_(colmax)
             ops.scale_columns(W, colmax, self.mv.compute)
+            if fp8:
+                W = self._to_fp8(W, st)
             if comm.distributed:
                 Xn = ops.new_block(self.n, k, self.mv.storage, self.device)
                 comm.all_gather_rows(W.t, Xn.t, self.n, k)
@@ -307,6 +312,12 @@ class EigEngine:
             else:
                 X = W
         return X
+
+    def _to_fp8(self, W, st):
+        """An inf-norm-scaled fp32 block rounded once into e4m3 (the FP8 rung's storage)."""
+        X8 = self.ops.new_block(W.n, W.k, FpFormat.FP8_E4M3, self.device)
+        self.ops.convert(W, X8, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+        return X8
 
     def power_from(self, W, eig, kp: int, st):
         """A-pass reuse (cfg.reuse_av): the restart block is Ut = U Y, so its MatVec is
@@ -317,10 +328,13 @@ class EigEngine:
         import torch
         ops, comm = self.ops, self.comm
         colmax = torch.zeros(kp, dtype=torch.float64, device=self.device)
-        X = ops.reuse_power(W, eig.vectors, kp, eig.n_out, kp, self.mv.storage, colmax,
+        fp8 = self.mv.storage == FpFormat.FP8_E4M3
+        X = ops.reuse_power(W, eig.vectors, kp, eig.n_out, kp, FpFormat.F32 if fp8 else self.mv.storage, colmax,
                             flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
         comm.all_reduce_max_(colmax)
         ops.scale_columns(X, colmax, self.mv.compute)
+        if fp8:
+            X = self._to_fp8(X, st)
         if comm.distributed:
             Xn = ops.new_block(self.n, kp, self.mv.storage, self.device)
             comm.all_gather_rows(X.t, Xn.t, self.n, kp)
@@ -348,14 +362,27 @@ class EigEngine:
         pairs is formed from it (K7e) -- no extra pass over A."""
         ops, comm = self.ops, self.comm
         kp = U.k
-        W = ops.new_block(self.A_pol.rows, kp, self.pol.storage, self.device)
+        fp8 = self.pol.storage == FpFormat.FP8_E4M3
         W2 = None
-        if top_check is not None or reuse:
-            acc = FpFormat.F64 if FpFormat.F64 in (self.A_pol.fmt, U.fmt) else FpFormat.F32
-            W2 = ops.new_block(self.A_pol.rows, kp, acc, self.device)
-        ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2,
-                    **({"oz": self._block_oz(self.A_pol, U), "levels": self.pol.product_levels}
-                       if self.ops is _ops else {}))
+        if fp8:
+            # e4m3 storage: W = A U stays in its fp32 accumulation format (A U exceeds e4m3's
+            # 448 long before the basis does), the Grams are formed from U widened to fp32
+            # (exact) and that W
+            W = ops.new_block(self.A_pol.rows, kp, FpFormat.F32, self.device)
+            ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1],
+                        **({"levels": self.pol.product_levels} if self.ops is _ops else {}))
+            W2 = W if (top_check is not None or reuse) else None
+            U8 = U
+            U = ops.new_block(U8.n, kp, FpFormat.F32, self.device)
+            ops.convert(U8, U)
+        else:
+            W = ops.new_block(self.A_pol.rows, kp, self.pol.storage, self.device)
+            if top_check is not None or reuse:
+                acc = FpFormat.F64 if FpFormat.F64 in (self.A_pol.fmt, U.fmt) else FpFormat.F32
+                W2 = ops.new_block(self.A_pol.rows, kp, acc, self.device)
+            ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2,
+                        **({"oz": self._block_oz(self.A_pol, U), "levels": self.pol.product_levels}
+                           if self.ops is _ops else {}))
         self.stats.a_passes += 1
         self._last_w2 = W2
         Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U

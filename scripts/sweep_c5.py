@@ -100,7 +100,9 @@ for r in rows:
     print(f"| {r['rung']} | {r['A']} | {r['tol']:.0e} | {r['time_to_tol_s'] * 1e3:.1f} ms | {r['converged']} | "
           f"{r['outer_iterations']} / {r['a_passes']} | {r['max_residual_top']:.2e} | "
           f"{r['max_rel_value_error']:.2e} | {r['floor_30_iterations']:.2e} | {r['time_30_iterations_s'] * 1e3:.1f} ms |")
-print("\nFP8 e4m3 cannot hold this pipeline at n = 32768: the entries of A must stay above the "
-      "2^-6 normal range while the block products A U (Hessenberg basis entries up to 1) must stay "
-      "below 448, i.e. roughly n < 448 * 64; the MatVec / projection overflow diagnostic fires "
-      "(the reference raises the same OverflowDiagnostic for out-of-range fp16).")
+print("The FP8 rung keeps A and the basis blocks in e4m3 on the f8f6f4 tensor cores; the block "
+      "products stay in fp32 until the column scaling (power steps) or the Grams (projection), so "
+      "A U never has to fit e4m3's 448 (per-column scaling; the spectrum is scaled by a power of two "
+      "so that A's entries sit in e4m3's normal range).  With 3 mantissa bits the basis settles at "
+      "residuals ~0.3 on this clustered spectrum: FP8 is a time point of the sweep, not a rung that "
+      "reaches a tolerance of its own.")

@@ -355,3 +355,27 @@ def test_three_rung_ladder_to_fp64(ofrr_gpu):
     from paper_2505_00281_b200.projection import residual_report
     indep = residual_report(A, rs3).residuals
     np.testing.assert_allclose(rs3.residuals[:top], indep[:top], rtol=1e-3, atol=1e-13)
+
+
+def test_fp8_rung_with_column_scaling(ofrr_gpu):
+    """The FP8 (e4m3) basis: A and the basis blocks in e4m3 on the f8f6f4 tensor cores; the
+    products stay in fp32 until the column scaling (power steps) or the Grams (projection),
+    so A U never has to fit e4m3's 448 (C5: it used to overflow).  A clustered spectrum scaled
+    to e4m3's range, top-16: no overflow, and the FP8 basis settles at its format's floor
+    (e4m3 keeps 3 mantissa bits: residuals ~0.15-0.3, values to a few percent)."""
+    p = ofrr_gpu
+    n, top, k = 4096, 16, 32
+    lam = p.clustered_spectrum(n, clusters=2, per=8)
+    probe, _ = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=SEED)
+    amax = float(probe.device_operator(p.FpFormat.BF16).t[:, :n].abs().max())
+    lam = lam * 2.0 ** np.round(np.log2(2.0 / amax))
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.FP8_E4M3, seed=SEED)
+    cfg = p.IterConfig(k=k, m=30, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr", policy=p.TC_FP8,
+                       seed=SEED, tol=1e-1, top=top)
+    st = p.RunStats()
+    rs = p.subspace_iter_eig(A, cfg, stats=st)
+    assert np.all(np.isfinite(rs.values[:top])) and np.all(np.isfinite(rs.residuals[:top]))
+    assert np.max(rs.residuals[:top]) < 0.5
+    assert min(w for _, w in st.history) < 0.3                   # it converged to the e4m3 floor
+    err = np.abs(rs.values[:top] - lam[:top]) / lam[:top]
+    assert np.max(err) < 0.1, err
