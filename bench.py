@@ -361,6 +361,7 @@ def _config_block(name, cfg, world):
 # computed in _kernel_work from the config (SURVEY.md 8(d) per-unit figures)
 _KNOWN = [
     ("k_gemm_av_tc", "K1 A.X block product (bf16 tensor cores)"),
+    ("k_ozk_ts", "K7z FP64-accurate A.X (int8 tensor cores, Ozaki digit heads in TMEM)"),
     ("k_ozk_gemm", "K7z FP64-accurate A.X (int8 tensor cores, Ozaki digits)"),
     ("k_oz_gemm", "K7z (digit-plane variant)"),
     ("k_hessenberg", "K3 Hessenberg basis"),
@@ -387,10 +388,25 @@ def _label(name: str) -> str:
     return "other (torch fills/copies, memcpy)"
 
 
+def _ozk_args(name: str):
+    """(BN, NP, NL) of a k_ozk_gemm<FMT, BN, NP, NL> / k_ozk_ts<FMT, BN, NL> (heads: NP = 3)
+    instance from its kernel name."""
+    import re
+    m = re.search(r"k_ozk_ts<\s*(\d+),\s*(\d+),\s*(\d+)>", name)
+    if m:
+        return int(m.group(2)), 3, int(m.group(3))
+    m = re.search(r"k_ozk_gemm<\s*(\d+),\s*(\d+),\s*(\d+)(?:,\s*(\d+))?>", name)
+    if not m:
+        return 64, 3, 6
+    return int(m.group(2)), int(m.group(3)), int(m.group(4) or 6)
+
+
 def _oz_products(name: str) -> int:
-    """Digit products per K7z launch: 15 with the 3-digit heads of A (k_ozk_gemm<F, BN, 3>),
-    21 with all six planes."""
-    return 15 if name.replace(" ", "").endswith(",3>") or ",3>(" in name.replace(" ", "") else 21
+    """Digit products per column block of a K7z launch: plane p of A (p < NP) meets the NL - p
+    digits of the block that keep its level below NL -- 15 for the FP64 heads (NP=3, NL=6),
+    21 with all six planes, 9 for the ~30-bit lite tier (NP=3, NL=4)."""
+    _, np_, nl = _ozk_args(name)
+    return sum(nl - p for p in range(min(np_, nl)))
 
 
 def _kernel_work(name: str, cfg, rows: int):
@@ -398,9 +414,10 @@ def _kernel_work(name: str, cfg, rows: int):
     8(d)); None where the kernel is latency-bound (pencil, control) or bookkeeping."""
     n, k = cfg["n"], cfg["k"]
     s_blk = 8 if "double" in name else 4
-    if "k_ozk_gemm" in name:
-        bn = 64 if k > 32 else 32
-        return rows * n * 2 + 6 * n * bn, _oz_products(name) * 2.0 * rows * n * bn, "int8"
+    if "k_ozk_gemm" in name or "k_ozk_ts" in name:
+        bn, _, nl = _ozk_args(name)
+        bn = min(bn, k)
+        return rows * n * 2 + nl * n * bn, _oz_products(name) * 2.0 * rows * n * bn, "int8"
     if "k_hessenberg" in name:
         return 2 * n * k * s_blk, None, None
     if "k_gram_partial" in name:
@@ -688,7 +705,7 @@ def _roofline(table, stamps, log, cfg, rows, ms_step, hbm, bf16_peak, peak_kind,
     region (K1 / K7z), else from the CUPTI table."""
     n, k = cfg["n"], cfg["k"]
     dom = table[0]["kernel"] if table else ("k_ozk_gemm" if cfg["policy"] == "full-f64" else "k_gemm_av_tc")
-    if "k_ozk_gemm" in dom:
+    if "k_ozk_gemm" in dom or "k_ozk_ts" in dom:
         sm, cnt = stamps["oz"]
         avg_ms = sm / cnt if cnt else float("nan")
         nb, ops_, _ = _kernel_work(dom, cfg, rows)
@@ -731,7 +748,7 @@ def _profiled_traffic(cfg_name: str, kernel: str):
     try:
         with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             rec = json.load(f)
-        key = "k_ozk_gemm" if "k_ozk_gemm" in kernel else "k_gemm_av_tc"
+        key = "k_ozk_ts" if "k_ozk_ts" in kernel else "k_ozk_gemm" if "k_ozk_gemm" in kernel else "k_gemm_av_tc"
         e = rec[cfg_name][key]
         return float(e["bytes_per_launch"]), e["source"]
     except Exception:

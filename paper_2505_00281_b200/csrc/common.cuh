@@ -221,6 +221,56 @@ __device__ __forceinline__ void mma_f8(uint32_t d_tmem, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld_shared_v2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+// Warp-wide issue: the whole warp runs the issue loop and one elected lane issues.  With the
+// warp index made visibly warp-uniform (warp_index() below) ptxas keeps the descriptors in
+// uniform registers and emits back-to-back UTC*MMA; issuing from `if (lane == 0)` instead wraps
+// every MMA in a per-lane waterfall (ELECT + five R2UR + branch) -- the issuing thread, not the
+// tensor pipe, then paces a kernel whose MMAs are short.
+__device__ __forceinline__ int warp_index() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+#define OFRR_MMA_WS(NAME, KIND)                                                                  \
+  __device__ __forceinline__ void NAME(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, \
+                                       uint32_t accumulate) {                                       \
+    asm volatile(                                                                                   \
+        "{\n\t.reg .pred p, e;\n\t"                                                               \
+        "elect.sync _|e, 0xffffffff;\n\t"                                                          \
+        "setp.ne.b32 p, %4, 0;\n\t"                                                                \
+        "@e tcgen05.mma.cta_group::1.kind::" KIND " [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),      \
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));                                        \
+  }
+OFRR_MMA_WS(mma_f16_ws, "f16")
+OFRR_MMA_WS(mma_f8_ws, "f8f6f4")
+OFRR_MMA_WS(mma_i8_ws, "i8")
+#undef OFRR_MMA_WS
+__device__ __forceinline__ void tc_commit_ws(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc_ws(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(

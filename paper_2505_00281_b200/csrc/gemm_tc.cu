@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_index(), lane = threadIdx.x & 31;
   const long long G = gridDim.x / CL;                          // work units are split per cluster
   const long long cidx = blockIdx.x / CL;
   const long long it0 = cidx * total_iters / G;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   if constexpr (CL > 1) cluster_sync_all();                   // peers' barriers initialised
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer (single thread) =====
+    {
+      // ===== MMA issuer (warp-wide, elected lane issues) =====
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
       long long it = it0;
@@ -179,27 +179,27 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // +32 B of K per step (>>4 = 2); second M half starts 128 rows (16 KB) later
                 const uint64_t a = da + (uint64_t)(k * 2 + h * (16384 >> 4));
                 const uint64_t b = db + (uint64_t)(k * 2);
-                if (FP8K) mma_f8(tmem + h * BN, a, b, idesc, acc);
-                else mma_f16(tmem + h * BN, a, b, idesc, acc);
+                if (FP8K) mma_f8_ws(tmem + h * BN, a, b, idesc, acc);
+                else mma_f16_ws(tmem + h * BN, a, b, idesc, acc);
               }
             } else {
               // one M=128 half, N in chunks of 256 columns sharing the A tile; the second
               // chunk's B rows start 256 rows (32 KB) into the B stage
               const uint64_t a = da + (uint64_t)(k * 2);
-              if (FP8K) mma_f8(tmem, a, db + (uint64_t)(k * 2), idesc, acc);
-              else mma_f16(tmem, a, db + (uint64_t)(k * 2), idesc, acc);
+              if (FP8K) mma_f8_ws(tmem, a, db + (uint64_t)(k * 2), idesc, acc);
+              else mma_f16_ws(tmem, a, db + (uint64_t)(k * 2), idesc, acc);
               if constexpr (BN > 256) {
                 const uint64_t b2 = db + (uint64_t)(k * 2 + ((256 * KBYTES) >> 4));
-                if (FP8K) mma_f8(tmem + 256, a, b2, idesc2, acc);
-                else mma_f16(tmem + 256, a, b2, idesc2, acc);
+                if (FP8K) mma_f8_ws(tmem + 256, a, b2, idesc2, acc);
+                else mma_f16_ws(tmem + 256, a, b2, idesc2, acc);
               }
             }
           }
-          if constexpr (CL > 1) tc_commit_mc(&empty[stage], (uint16_t)((1u << CL) - 1u));
-          else tc_commit(&empty[stage]);
+          if constexpr (CL > 1) tc_commit_mc_ws(&empty[stage], (uint16_t)((1u << CL) - 1u));
+          else tc_commit_ws(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(tfull);
+        tc_commit_ws(tfull);
         acc_phase ^= 1;
       }
     }
@@ -380,6 +380,13 @@ static int make_tmap_2d(CUtensorMap* tm, const void* base, int a_fmt, uint64_t i
 int oz_make_tmap_u8(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
                     uint32_t box_inner, uint32_t box_outer) {
   return make_tmap_2d(tm, base, FP8, inner, outer, ld_bytes, box_inner, box_outer);
+}
+
+// raw operator rows for the K7z converters: 64 entries x 128 rows, 128B swizzle (64B for fp8)
+int oz_make_tmap_a(CUtensorMap* tm, const void* base, int a_fmt, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                   uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_2d(tm, base, a_fmt, inner, outer, ld_elems, box_inner, box_outer,
+                      a_fmt == FP8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 int oz_make_tmap_u8_sw64(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,

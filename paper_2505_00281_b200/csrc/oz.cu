@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_index(), lane = threadIdx.x & 31;
   const long long G = gridDim.x;
   const long long u0 = (long long)blockIdx.x * total_units / G;
   const long long u1 = ((long long)blockIdx.x + 1) * total_units / G;
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -406,8 +406,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
+    {
+      // ===== MMA issuer (warp-wide loop, elected lane issues) =====
       int as = 0, vs = 0;
       uint32_t aph = 0, vph = 0, acc_phase = 0;
       long long u = u0;
@@ -432,18 +432,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               const uint32_t acc = (u > seg_start || p > 0 || k > 0) ? 1u : 0u;
               for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
                 const int ng = std::min(256 / BN, nq - q0);
-                mma_i8(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
+                mma_i8_ws(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
                        dv + (uint64_t)((q0 * BN * OZ_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN, true, true),
                        acc);
               }
             }
-            tc_commit(&aempty[as]);
+            tc_commit_ws(&aempty[as]);
             if (++as == C::A_STAGES) { as = 0; aph ^= 1; }
           }
-          tc_commit(&vempty[vs]);
+          tc_commit_ws(&vempty[vs]);
           if (++vs == 2) { vs = 0; vph ^= 1; }
         }
-        tc_commit(tfull);
+        tc_commit_ws(tfull);
         acc_phase ^= 1;
       }
     }
@@ -798,7 +798,7 @@ __device__ __forceinline__ void ozk_load32(const void* A, int64_t off, bool ok_v
   }
 }
 template <int FMT>
-__device__ __forceinline__ float ozk_elem(const uint4 (&raw)[4], int e) {
+__device__ __forceinline__ float ozk_elem(const uint4 (&raw)[2], int e) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(raw);
   if constexpr (FMT == BF16) {
     return __uint_as_float(((w[e >> 1] >> (16 * (e & 1))) & 0xffffu) << 16);
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_index(), lane = threadIdx.x & 31;
   const long long G = gridDim.x;
   const long long u0 = (long long)blockIdx.x * total_units / G;
   const long long u1 = ((long long)blockIdx.x + 1) * total_units / G;
@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -875,8 +875,8 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
+    {
+      // ===== MMA issuer (warp-wide loop, elected lane issues) =====
       int as = 0, vs = 0;
       uint32_t aph = 0, vph = 0, acc_phase = 0;
       long long u = u0;
@@ -902,18 +902,18 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
 #pragma unroll
               for (int k = 0; k < 2; ++k) {
                 const uint32_t acc = (u > seg_start || p > 0 || k > 0) ? 1u : 0u;
-                mma_i8(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
+                mma_i8_ws(tmem + (uint32_t)((p + q0) * BN), da + (uint64_t)(k * 2),
                        dv + (uint64_t)((q0 * BN * OZK_KB) >> 4) + (uint64_t)(k * 2), oz_idesc(ng * BN, p == 0, true),
                        acc);
               }
             }
           }
-          tc_commit(&aempty[as]);
-          tc_commit(&vempty[vs]);
+          tc_commit_ws(&aempty[as]);
+          tc_commit_ws(&vempty[vs]);
           if (++as == C::A_STAGES) { as = 0; aph ^= 1; }
           if (++vs == C::V_STAGES) { vs = 0; vph ^= 1; }
         }
-        tc_commit(tfull);
+        tc_commit_ws(tfull);
         acc_phase ^= 1;
       }
     }
@@ -961,7 +961,6 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
     int E = 0;
     float sc = 0.0f;
     bool fast = false, row_ok = false;
-    uint4 nxt[2];
     // (tile, k-block) of the next fetch, advanced without 64-bit divisions (they were a
     // fifth of the converters' instructions)
     int fvt = (int)(u0 / kbc), frem = (int)(u0 % kbc);
@@ -992,13 +991,11 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
             for (int bb = 0; bb < EB; ++bb) dst[EB * e + bb] = src[EB * e + bb];
       }
     };
-    if (u0 < u1) fetch(u0, nxt);
     int lvt = (int)(u0 / kbc), lrem = (int)(u0 % kbc);
-    for (long long u = u0; u < u1; ++u) {
-      uint4 raw[4];
-      raw[0] = nxt[0];
-      raw[1] = nxt[1];
-      if (u + 1 < u1) fetch(u + 1, nxt);                 // prefetch the next k-block's entries
+    const uint32_t abase = smem_u32(abuf);
+    // one k-block: convert `raw`, refill it with the entries two k-blocks ahead (`refill`),
+    // then wait for the stage and store the digit planes
+    auto step = [&](uint4 (&raw)[2], bool refill) {
       const int vt = lvt;
       if (++lrem == kbc) { lrem = 0; ++lvt; }
       if (vt != cur_vt) {
@@ -1064,16 +1061,26 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
           for (int p = 0; p < OZ_D; ++p) w[p][g] = pw[p];
         }
       }
+      // the global loads two k-blocks ahead go out now: a one-deep prefetch left the
+      // converters waiting on HBM latency every k-block
+      if (refill) fetch(0, raw);
       mbar_wait(&aempty[as], aph ^ 1);
-      uint8_t* slot = abuf + as * C::A_SET;
+      const uint32_t slot = abase + as * C::A_SET;
       const int pos = (r >> 3) * 512 + (r & 7) * 64 + ((qt ^ ((r >> 1) & 3)) << 4);
 #pragma unroll
       for (int p = 0; p < OZ_D; ++p)
-        if (p < NP) *reinterpret_cast<uint4*>(slot + p * C::A_TILE + pos) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+        if (p < NP) st_shared_v4(slot + p * C::A_TILE + pos, w[p][0], w[p][1], w[p][2], w[p][3]);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[as]);
       if (++as == C::A_STAGES) { as = 0; aph ^= 1; }
+    };
+    uint4 pa[2], pb[2];
+    if (u0 < u1) fetch(u0, pa);
+    if (u0 + 1 < u1) fetch(u0 + 1, pb);
+    for (long long u = u0; u < u1; u += 2) {
+      step(pa, u + 2 < u1);
+      if (u + 1 < u1) step(pb, u + 3 < u1);
     }
   }
   tc_fence_before();
@@ -1082,6 +1089,314 @@ __global__ void __launch_bounds__(OZK_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ---- K7z heads with the digit planes of A in tensor memory ------------------------------
+// The shared-memory kernel above moves ~148 KB through shared memory per k-block (A digit
+// planes written by the converters and read once per MMA group, V digit tiles written by TMA
+// and read by every group): at ~75% of the SM's shared-memory bandwidth that, not the tensor
+// pipe, set its pace.  Here the converters store the three head planes straight into TMEM
+// (tcgen05.st) and the MMAs take A from there (tcgen05.mma ... [a-tmem]), so shared memory only
+// carries the V tiles: 84 KB per k-block, below the MMA floor.  Stages are half k-blocks (the
+// 32 entries of one MMA: 8 TMEM columns per plane) in the columns the level accumulators leave
+// free.  Heads only (NP = 3); the six-plane variant stays on the shared-memory kernel.
+template <int BN, int NL, int EB>
+struct OzkTsCfg {
+  static constexpr int HALF_COLS = 3 * 8;                  // 3 planes x 32 int8 entries per row
+  static constexpr int ACC_COLS = NL * BN;
+  static constexpr int A_TSTAGES = (512 - ACC_COLS) / HALF_COLS < 8 ? (512 - ACC_COLS) / HALF_COLS : 8;
+  static constexpr int R_SET = OZ_TM * OZK_KB * EB;        // one raw A tile (TMA, 128 / 64 B swizzle)
+  static constexpr int R_STAGES = 6;
+  static constexpr int V_SET = NL * BN * OZK_KB;
+  static constexpr int V_STAGES = (216 * 1024 - R_STAGES * R_SET) / V_SET < 8 ? (216 * 1024 - R_STAGES * R_SET) / V_SET : 8;
+  static constexpr int SMEM_BYTES = 1024 + R_STAGES * R_SET + V_STAGES * V_SET + 512;
+  static_assert(A_TSTAGES >= 3, "ozk-ts: TMEM stages");
+  static_assert(SMEM_BYTES <= 227 * 1024, "ozk-ts shared memory");
+};
+
+__device__ __forceinline__ void mma_i8_ts_ws(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+// 16 lanes x 256 bits: thread t -> lanes t/4 (v[0], v[1]) and t/4 + 8 (v[2], v[3]), columns
+// 2 (t % 4) and 2 (t % 4) + 1
+__device__ __forceinline__ void tmem_st_16x256(uint32_t taddr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+static constexpr int OZK_TS_THREADS = OZK_THREADS + 32;   // + warp 22: the raw A producer
+
+template <int FMT, int BN, int NL>
+__global__ void __launch_bounds__(OZK_TS_THREADS, 1)
+    k_ozk_ts(const __grid_constant__ CUtensorMap tmA, int64_t rows, const int* __restrict__ Tg,
+             const __grid_constant__ CUtensorMap tmV, double* __restrict__ ws, int kbc, int nchunks,
+             long long total_units, int max_slots, int npad, int col0, int stamp, const int* __restrict__ full_flag) {
+  constexpr int EB = FMT == FP8 ? 1 : 2;
+  using C = OzkTsCfg<BN, NL, EB>;
+  if (full_flag != nullptr && *full_flag != 0) return;     // the operator needs all six planes
+  if (stamp && threadIdx.x == 0) atomicMin(&g_oz_stamp[0], oz_gtimer_ns());
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* rbuf = smem;                                  // [R_STAGES][128 rows x 64 entries] raw A
+  uint8_t* vbuf = smem + C::R_STAGES * C::R_SET;         // [V_STAGES][NL][BN x 64 B]
+  uint64_t* afull = reinterpret_cast<uint64_t*>(vbuf + C::V_STAGES * C::V_SET);
+  uint64_t* aempty = afull + C::A_TSTAGES;
+  uint64_t* vfull = aempty + C::A_TSTAGES;
+  uint64_t* vempty = vfull + C::V_STAGES;
+  uint64_t* rfull = vempty + C::V_STAGES;
+  uint64_t* rempty = rfull + C::R_STAGES;
+  uint64_t* tfull = rempty + C::R_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = warp_index(), lane = threadIdx.x & 31;
+  const long long G = gridDim.x;
+  const long long u0 = (long long)blockIdx.x * total_units / G;
+  const long long u1 = ((long long)blockIdx.x + 1) * total_units / G;
+  const int vt_first = (int)(u0 / kbc);
+
+  if (threadIdx.x == 0) {
+    // a half-stage is written by the 8 converter warps holding its two 16-entry quarters
+    for (int s = 0; s < C::A_TSTAGES; ++s) { mbar_init(&afull[s], OZK_CONV_WARPS / 2); mbar_init(&aempty[s], 1); }
+    for (int s = 0; s < C::V_STAGES; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
+    for (int s = 0; s < C::R_STAGES; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], OZK_CONV_WARPS); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_barrier_init();
+    prefetch_tmap(&tmV);
+    prefetch_tmap(&tmA);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer: V digit tiles (the raw A tiles have their own warp: one thread
+      // serving both rings held the raw tiles back behind a full V ring) =====
+      const uint64_t pol_v = policy_evict_last();
+      int vs = 0;
+      uint32_t vph = 0;
+      int vt = (int)(u0 / kbc), rem = (int)(u0 % kbc);
+      for (long long u = u0; u < u1; ++u) {
+        const int kb = (vt % nchunks) * kbc + rem;
+        if (++rem == kbc) { rem = 0; ++vt; }
+        mbar_wait(&vempty[vs], vph ^ 1);
+        mbar_expect_tx(&vfull[vs], C::V_SET);
+        for (int q = 0; q < NL; ++q)
+          tma_load_2d(vbuf + vs * C::V_SET + q * BN * OZK_KB, &tmV, kb * OZK_KB, q * npad + col0, &vfull[vs], pol_v);
+        if (++vs == C::V_STAGES) { vs = 0; vph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (warp-wide loop, elected lane issues) =====
+    int hs = 0, vs = 0;
+    uint32_t hph = 0, vph = 0, acc_phase = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int vt = (int)(u / kbc);
+      const long long seg_end = std::min<long long>(u1, (long long)(vt + 1) * kbc);
+      const long long seg_start = u;
+      mbar_wait(tempty, acc_phase ^ 1);
+      tc_fence_after();
+      for (; u < seg_end; ++u) {
+        mbar_wait(&vfull[vs], vph);
+        const uint64_t dv = umma_desc_sw64(smem_u32(vbuf + vs * C::V_SET));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&afull[hs], hph);
+          tc_fence_after();
+          const uint32_t ta = tmem + (uint32_t)(C::ACC_COLS + hs * C::HALF_COLS);
+#pragma unroll
+          for (int p = 0; p < (NL < 3 ? NL : 3); ++p) {
+            const int nq = NL - p;
+#pragma unroll
+            for (int q0 = 0; q0 < nq; q0 += 256 / BN) {
+              const int ng = (256 / BN < nq - q0) ? 256 / BN : nq - q0;
+              const uint32_t acc = (u > seg_start || p > 0 || h > 0) ? 1u : 0u;
+              mma_i8_ts_ws(tmem + (uint32_t)((p + q0) * BN), ta + (uint32_t)(p * 8),
+                           dv + (uint64_t)((q0 * BN * OZK_KB) >> 4) + (uint64_t)(h * 2), oz_idesc(ng * BN, p == 0, true),
+                           acc);
+            }
+          }
+          tc_commit_ws(&aempty[hs]);
+          if (++hs == C::A_TSTAGES) { hs = 0; hph ^= 1; }
+        }
+        tc_commit_ws(&vempty[vs]);
+        if (++vs == C::V_STAGES) { vs = 0; vph ^= 1; }
+      }
+      tc_commit_ws(tfull);
+      acc_phase ^= 1;
+    }
+  } else if (warp == 22) {
+    if (lane == 0) {
+      // ===== TMA producer: raw A tiles =====
+      const uint64_t pol_a = policy_evict_first();
+      int rs = 0;
+      uint32_t rph = 0;
+      int vt = (int)(u0 / kbc), rem = (int)(u0 % kbc);
+      for (long long u = u0; u < u1; ++u) {
+        const int kb = (vt % nchunks) * kbc + rem;
+        const int mt = vt / nchunks;
+        if (++rem == kbc) { rem = 0; ++vt; }
+        mbar_wait(&rempty[rs], rph ^ 1);
+        mbar_expect_tx(&rfull[rs], C::R_SET);
+        tma_load_2d(rbuf + rs * C::R_SET, &tmA, kb * OZK_KB, mt * OZ_TM, &rfull[rs], pol_a);
+        if (++rs == C::R_STAGES) { rs = 0; rph ^= 1; }
+      }
+    }
+  } else if (warp < 6) {
+    // ===== epilogue warps 2..5: TMEM int32 levels -> fp64 partial tile (column-major) =====
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    uint32_t acc_phase = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int vt = (int)(u / kbc);
+      u = std::min<long long>(u1, (long long)(vt + 1) * kbc);
+      mbar_wait(tfull, acc_phase);
+      tc_fence_after();
+      double* dst = ws + ((size_t)blockIdx.x * max_slots + (vt - vt_first)) * (size_t)(OZ_TM * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        double s[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s[i] = 0.0;
+#pragma unroll 1
+        for (int lv = NL - 1; lv >= 0; --lv) {
+          int d[16];
+          tmem_ld16i(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(lv * BN + c0), d);
+          const double w = ldexp(1.0, -8 * lv - 12);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) s[i] = fma((double)d[i], w, s[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dst[(size_t)(c0 + i) * OZ_TM + row] = s[i];
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+      acc_phase ^= 1;
+    }
+  } else {
+    // ===== converter warps: raw A tile (smem) -> three head digit planes in TMEM ==========
+    // warp -> TMEM lane quarter Q = warp % 4, half k-block h and 16-lane half of the quarter;
+    // one tcgen05.st 16x256b per plane covers its 16 rows x 8 columns (32 entries): thread t
+    // holds rows t/4 and t/4 + 8 of them, entries 8(t%4) .. +8 (two TMEM columns).  The raw
+    // tile arrives by TMA (a four-deep ring: register prefetch left HBM latency exposed).
+    const int cw = warp - 6;                   // 0..15
+    const int quarter = warp & 3;
+    const int sub = (cw >> 2) & 1;             // 16-lane half of the quarter
+    const int h = cw >> 3;                     // half k-block = TMEM stage parity
+    const int t0 = lane & 3, t1 = lane >> 2;
+    const int r = quarter * 32 + sub * 16 + t1;           // first row; the second is r + 8
+    const uint32_t tbase = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16) + (uint32_t)C::ACC_COLS;
+    // byte offsets of this thread's 8 entries in the two rows of a swizzled raw tile
+    constexpr int P = OZK_KB * EB;             // row pitch: 128 B (bf16/f16, 128B swizzle), 64 B (fp8)
+    auto roff = [&](int row) {
+      const int b = (h * 32 + t0 * 8) * EB;
+      return row * P + ((((b >> 4) ^ ((row * P >> 7) & (P / 16 - 1)))) << 4) + (b & 15);
+    };
+    const uint32_t offa = (uint32_t)roff(r), offb = (uint32_t)roff(r + 8);
+    const uint32_t rbase = smem_u32(rbuf);
+    int hs = h, hph = 0;                       // this warp's half-stage: global half index 2j + h
+    int rs = 0;
+    uint32_t rph = 0;
+    int cur_vt = -1;
+    float sca = 0.0f, scb = 0.0f;
+    auto elem = [&](const uint4& v, int e) -> float {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
+      if constexpr (FMT == BF16) {
+        return __uint_as_float(((w[e >> 1] >> (16 * (e & 1))) & 0xffffu) << 16);
+      } else if constexpr (FMT == F16) {
+        return __half2float(__ushort_as_half((uint16_t)(w[e >> 1] >> (16 * (e & 1)))));
+      } else {
+        __nv_fp8_e4m3 q;
+        q.__x = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
+        return float(q);
+      }
+    };
+    int lvt = (int)(u0 / kbc), lrem = (int)(u0 % kbc);
+    for (long long u = u0; u < u1; ++u) {
+      const int vt = lvt;
+      if (++lrem == kbc) { lrem = 0; ++lvt; }
+      if (vt != cur_vt) {
+        cur_vt = vt;
+        // heads: h = trunc(a 2^(22 - E)) (the prepare pass checked the range)
+        const int64_t ga = (int64_t)(vt / nchunks) * OZ_TM + r;
+        const int Ea = ga < rows ? Tg[ga] : OZ_BAD;
+        const int Eb = ga + 8 < rows ? Tg[ga + 8] : OZ_BAD;
+        sca = Ea != OZ_BAD ? __int_as_float((22 - Ea + 127) << 23) : 0.0f;
+        scb = Eb != OZ_BAD ? __int_as_float((22 - Eb + 127) << 23) : 0.0f;
+      }
+      uint4 raw[2];
+      mbar_wait(&rfull[rs], rph);
+      const uint32_t rb = rbase + rs * C::R_SET;
+      if constexpr (EB == 2) {
+        raw[0] = ld_shared_v4(rb + offa);
+        raw[1] = ld_shared_v4(rb + offb);
+      } else {
+        const uint2 qa = ld_shared_v2(rb + offa), qb = ld_shared_v2(rb + offb);
+        raw[0] = make_uint4(qa.x, qa.y, 0, 0);
+        raw[1] = make_uint4(qb.x, qb.y, 0, 0);
+      }
+      // w[p] = {row a: columns 2 t0, 2 t0 + 1; row b: the same columns}
+      uint32_t w[3][4];
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const float sc = rr == 0 ? sca : scb;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          uint32_t hw[4], tw[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hw[e] = (uint32_t)__float2int_rz(elem(raw[rr], 4 * g + e) * sc);
+          oz_t4(hw, tw);
+          w[0][2 * rr + g] = tw[2];
+          w[1][2 * rr + g] = tw[1];
+          w[2][2 * rr + g] = tw[0];
+        }
+      }
+      mbar_wait(&aempty[hs], hph ^ 1);
+      tc_fence_after();
+      const uint32_t ta = tbase + (uint32_t)(hs * C::HALF_COLS);
+      tmem_st_16x256(ta, w[0]);
+      tmem_st_16x256(ta + 8, w[1]);
+      tmem_st_16x256(ta + 16, w[2]);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      // both stages are released only after the TMEM stores completed: their source registers
+      // (hence the shared loads of the raw stage) are then consumed for certain
+      if (lane == 0) {
+        mbar_arrive(&afull[hs]);
+        mbar_arrive(&rempty[rs]);
+      }
+      if (++rs == C::R_STAGES) { rs = 0; rph ^= 1; }
+      hs += 2;
+      if (hs >= C::A_TSTAGES) { hs -= C::A_TSTAGES; hph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (stamp && threadIdx.x == 0) atomicMax(&g_oz_stamp[1], oz_gtimer_ns());
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -1354,6 +1669,8 @@ int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int
 }
 
 // ---- in-kernel slicing path (default): operator workspace = row scales only ----------
+int oz_make_tmap_a(CUtensorMap* tm, const void* base, int a_fmt, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                   uint32_t box_inner, uint32_t box_outer);
 int oz_make_tmap_u8_sw64(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
                          uint32_t box_inner, uint32_t box_outer);   // gemm_tc.cu
 
@@ -1370,9 +1687,17 @@ struct OzkPlan {
   size_t off_F, off_dig, off_ws, off_part, off_vt, off_wt, bytes;
 };
 
+// OFRR_OZK_TMEM_A=0: the heads on the shared-memory kernel (comparison runs)
+static bool ozk_use_tmem_a() {       // read per launch: the tests compare both kernels in one process
+  const char* e = getenv("OFRR_OZK_TMEM_A");
+  return !(e && e[0] == '0');
+}
+
 static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r, int levels = OZ_D) {
   OzkPlan p;
   r = std::max(r, 1);
+  // lite tier: 128-column passes on the shared-memory kernel (64-column passes with the digit
+  // planes in TMEM read A twice: 5.2 vs 4.4 ms per A pass at C3)
   p.bn = levels == OZ_D ? (r <= 32 ? 32 : 64) : (r <= 64 ? 64 : 128);
   p.npass = (r + p.bn - 1) / p.bn;
   p.npad = p.npass * p.bn;
@@ -1417,10 +1742,32 @@ static int ozk_launch(const void* A, int64_t rows, int64_t cols, int64_t lda, co
   OFRR_CUDA_TRY(ae);
   const int stamp = g_oz_stamp_on ? 1 : 0;
   if (full) {
-    k_ozk_gemm<FMT, BN, 3, NL><<<p.grid, OZK_THREADS, C3::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
-                                                                           p.nchunks, p.total, p.max_slots, p.npad,
-                                                                           col0, stamp, full);
-    OFRR_CHECK_LAUNCH();
+    bool ts = false;
+    if constexpr (NL * BN <= 384) {
+      CUtensorMap tA;
+      // TMA needs a 16-byte aligned base and row pitch; otherwise the shared-memory kernel
+      const int eb = FMT == FP8 ? 1 : 2;
+      if (ozk_use_tmem_a() && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && ((uint64_t)lda * eb) % 16 == 0 &&
+          oz_make_tmap_a(&tA, A, FMT, (uint64_t)cols, (uint64_t)rows, (uint64_t)lda, OZK_KB, OZ_TM) == OFRR_OK) {
+        using CT = OzkTsCfg<BN, NL, FMT == FP8 ? 1 : 2>;
+        static std::once_flag attr_ts;
+        std::call_once(attr_ts, [&] {
+          ae = cudaFuncSetAttribute(k_ozk_ts<FMT, BN, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT::SMEM_BYTES);
+        });
+        OFRR_CUDA_TRY(ae);
+        k_ozk_ts<FMT, BN, NL><<<p.grid, OZK_TS_THREADS, CT::SMEM_BYTES, st>>>(tA, rows, T, tV, ws, p.kbc, p.nchunks,
+                                                                         p.total, p.max_slots, p.npad, col0, stamp,
+                                                                         full);
+        OFRR_CHECK_LAUNCH();
+        ts = true;
+      }
+    }
+    if (!ts) {
+      k_ozk_gemm<FMT, BN, 3, NL><<<p.grid, OZK_THREADS, C3::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
+                                                                             p.nchunks, p.total, p.max_slots, p.npad,
+                                                                             col0, stamp, full);
+      OFRR_CHECK_LAUNCH();
+    }
   }
   k_ozk_gemm<FMT, BN, OZ_D, NL><<<p.grid, OZK_THREADS, C::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
                                                                            p.nchunks, p.total, p.max_slots, p.npad,

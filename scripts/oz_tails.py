@@ -41,6 +41,14 @@ for _ in range(5):
 e1.record()
 torch.cuda.synchronize()
 print(f"product n={n} k={k}: {e0.elapsed_time(e1) / 5:.3f} ms per A pass (both column passes)")
+for _ in range(2):
+    ops.gemm_av(op, X, W, oz=oz, levels=4)
+e0.record()
+for _ in range(5):
+    ops.gemm_av(op, X, W, oz=oz, levels=4)
+e1.record()
+torch.cuda.synchronize()
+print(f"lite product (4 levels) n={n} k={k}: {e0.elapsed_time(e1) / 5:.3f} ms per A pass")
 e0.record()
 for _ in range(3):
     oz.refresh()

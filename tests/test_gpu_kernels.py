@@ -481,6 +481,46 @@ def test_ozaki_heads_and_tails(ofrr_gpu, oracle, case):
     assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
 
 
+@pytest.mark.parametrize("fmt", [BF16, F16])
+def test_ozaki_tmem_kernel_large(ofrr_gpu, oracle, monkeypatch, fmt):
+    """The heads kernel with the digit planes in TMEM (k_ozk_ts) at a size where every CTA runs
+    ~50 k-blocks (all rings wrap many times): bitwise equal to the shared-memory kernel
+    (k_ozk_gemm, same integer digit products and the same fp64 level sums), bitwise repeatable,
+    and within 2^-44 |A||X| of an FP64 product."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(5)
+    rows, cols, k = 4000, 16000, 64
+    a = o.round_to(rng.standard_normal((rows, cols)) * np.exp(rng.uniform(-3, 3, (rows, 1))), fmt)
+    x = rng.standard_normal((cols, k))
+    A = _op(p, a, fmt)
+    oz = ops.OzakiOperator(A)
+    assert oz.info()[0] == 0
+    X = _blk(p, x, F64)
+    outs = []
+    for flag in ("1", "1", "1", "0"):
+        monkeypatch.setenv("OFRR_OZK_TMEM_A", flag)
+        W = ops.new_block(rows, k, p.FpFormat.F64, torch.device("cuda"))
+        ops.gemm_av(A, X, W, oz=oz)
+        torch.cuda.synchronize()
+        outs.append(W.to_numpy_f64())
+    for w in outs[1:]:
+        np.testing.assert_array_equal(outs[0], w)
+    ref = (torch.as_tensor(a, device="cuda") @ torch.as_tensor(x, device="cuda")).cpu().numpy()
+    mag = np.abs(a) @ np.abs(x)
+    assert np.all(np.abs(outs[0] - ref) <= (2.0 ** -44 + cols * 2.0 ** -53) * mag)
+    # the lite tier (shared-memory kernel, 128-column passes): repeatable, ~2^-30
+    lite = []
+    for _ in range(2):
+        W = ops.new_block(rows, k, p.FpFormat.F64, torch.device("cuda"))
+        ops.gemm_av(A, X, W, oz=oz, levels=4)
+        torch.cuda.synchronize()
+        lite.append(W.to_numpy_f64())
+    np.testing.assert_array_equal(lite[0], lite[1])
+    assert np.all(np.abs(lite[0] - ref) <= 2.0 ** -26 * mag)
+
+
 def test_ozaki_lite_levels(ofrr_gpu, oracle):
     """ofrr_ozaki_gemm_levels(levels=4): the digit products with p + q < 4 (128-column passes),
     ~2^-30 of |A||X| per term; levels=6 stays FP64-accurate on the same inputs."""
