@@ -323,6 +323,15 @@ int ofrr_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int ds
 int ofrr_transpose_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int dst_fmt,
                            int64_t ld_dst, int64_t rows, int64_t cols, int* flags, void* stream);
 
+/* utility: symmetric operator upload from a HOST row-major n x n array already in the
+ * storage format `fmt`.  Only one triangle is read (uplo 0: entries (i, j >= i); uplo 1:
+ * (i, j <= i) -- the dsyev(uplo) convention; the eigen path ofrr/driver.py:84-111 is defined
+ * for symmetric A): it crosses PCIe as 2-D copies of `block_rows`-row blocks (0: 2048) on
+ * `stream`, and a side stream mirrors each block into the other triangle as it lands.
+ * *bytes = host bytes copied.  `host` should be pinned for the copies to be asynchronous. */
+int ofrr_upload_sym(const void* host, int64_t ld_host, void* A, int64_t lda, int64_t n, int fmt, int uplo,
+                    int64_t block_rows, long long* bytes, void* stream);
+
 /* ---------------------------------------------------------------------------------
  * Host-buffer plugin entry points: the exact signatures of the reference's kernel
  * module (ofrr/_kernels.pyx) so `ofrr.backend.kernels` can bind them.

@@ -49,6 +49,8 @@ int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
 int scale_columns(void* X, int64_t n, int k, int64_t ldx, int storage, int compute, const double* colmax, cudaStream_t st);
 int convert(const void* src, int sf, int64_t lds, void* dst, int df, int64_t ldd, int64_t n, int64_t k, int* flags,
             cudaStream_t st);
+int upload_sym(const void* host, int64_t ld_host, void* A, int64_t lda, int64_t n, int fmt, int uplo,
+               int64_t block_rows, long long* bytes, cudaStream_t st);
 int transpose_convert(const void* src, int sf, int64_t lds, void* dst, int df, int64_t ldd, int64_t rows, int64_t cols,
                       int* flags, cudaStream_t st);
 size_t hessenberg_ws(int64_t n, int k, int storage);
@@ -324,6 +326,11 @@ int ofrr_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int ds
 int ofrr_transpose_convert(const void* src, int src_fmt, int64_t ld_src, void* dst, int dst_fmt, int64_t ld_dst,
                            int64_t rows, int64_t cols, int* flags, void* stream) {
   return transpose_convert(src, src_fmt, ld_src, dst, dst_fmt, ld_dst, rows, cols, flags, S(stream));
+}
+
+int ofrr_upload_sym(const void* host, int64_t ld_host, void* A, int64_t lda, int64_t n, int fmt, int uplo,
+                    int64_t block_rows, long long* bytes, void* stream) {
+  return upload_sym(host, ld_host, A, lda, n, fmt, uplo, block_rows, bytes, S(stream));
 }
 
 // ---------------------------------------------------------------------------------

@@ -28,7 +28,13 @@ from .precision import FpFormat, round_to
 class DenseMatrix:
     """2-D matrix with a storage-format tag (ofrr/matrix.py:25-47) plus a device copy."""
 
-    def __init__(self, data, fmt: FpFormat):
+    def __init__(self, data, fmt: FpFormat, uplo: Optional[str] = None):
+        """``uplo`` ("U"/"L", extension): A is symmetric and only that triangle of a host
+        torch tensor in the storage dtype is read -- it is the only part copied to the device
+        (ops.upload_symmetric; the dsyev(uplo) convention).  None: the whole array is read."""
+        if uplo not in (None, "U", "L"):
+            raise ValueError("uplo must be None, 'U' or 'L'")
+        self.uplo = uplo
         self.fmt = FpFormat(fmt)
         self._host = None
         self._dev = {}          # FpFormat -> ops.DevOperator (row-major operator copies)
@@ -63,7 +69,9 @@ class DenseMatrix:
         """Column-major float64 host array (materialised from the device if needed)."""
         if self._host is None:
             import torch
-            if self._src_tensor is not None:
+            if self.uplo is not None and self._src_tensor is not None and not self._dev:
+                self.device_operator()          # the declared triangle, mirrored on the device
+            if self._src_tensor is not None and self.uplo is None:
                 self._host = np.asfortranarray(self._src_tensor.to(torch.float64).cpu().numpy())
             elif self._blocks:
                 blk = max(self._blocks.values(), key=lambda b: b.fmt.itemsize)
@@ -95,6 +103,7 @@ class DenseMatrix:
     def on_device(cls, op) -> "DenseMatrix":
         """Wrap an existing ops.DevOperator (row-major, HBM resident)."""
         m = cls.__new__(cls)
+        m.uplo = None
         m.fmt = FpFormat(op.fmt)
         m._host = None
         m._src_tensor = None
@@ -132,6 +141,11 @@ class DenseMatrix:
             _lib.check(L.ofrr_convert(src.ptr, int(src.fmt), src.lda, op.ptr, int(fmt), op.lda, self.cols,
                                       self.rows, flags.data_ptr(), st), "convert operator")
             exact = self._exact.get(src.fmt, False) and fmt >= src.fmt
+        elif self.uplo is not None and self._src_tensor is not None and self._src_tensor.device.type == "cpu" \
+                and self._src_tensor.dtype == fmt.torch_dtype and self._src_tensor.stride(1) == 1 \
+                and self.rows == self.cols:
+            ops.upload_symmetric(op, self._src_tensor, self.uplo)   # one triangle over PCIe
+            exact = True
         elif self._src_tensor is not None and self._src_tensor.dtype == fmt.torch_dtype \
                 and self._src_tensor.stride(1) == 1:
             op.t[:, : self.cols].copy_(self._src_tensor, non_blocking=True)   # plain H2D / D2D copy
@@ -208,6 +222,7 @@ class DenseMatrix:
     def from_block(cls, blk) -> "DenseMatrix":
         """Wrap an ops.DevBlock (column-major n x k on the device)."""
         m = cls.__new__(cls)
+        m.uplo = None
         m.fmt = FpFormat(blk.fmt)
         m._host = None
         m._src_tensor = None

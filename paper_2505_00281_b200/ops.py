@@ -13,6 +13,7 @@ synchronising.  Nothing here computes on the host.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 from typing import Optional
@@ -171,6 +172,26 @@ def new_operator(rows: int, cols: int, fmt: FpFormat, device) -> DevOperator:
     fmt = FpFormat(fmt)
     t = torch.empty((int(rows), pad_ld(cols)), dtype=fmt.torch_dtype, device=device)
     return DevOperator(t, int(rows), int(cols), fmt)
+
+
+def upload_symmetric(op: DevOperator, a_host: torch.Tensor, uplo: str = "U", block_rows: int = 2048) -> int:
+    """Fill the square device operator ``op`` from a host row-major tensor already in
+    ``op.fmt``'s dtype, reading only the ``uplo`` triangle of ``a_host`` (dsyev convention;
+    the eigen path, ofrr/driver.py:84-111, is defined for symmetric A): about half of A
+    crosses PCIe, the other triangle is mirrored on the device as the blocks land
+    (csrc/upload.cu).  Returns the host bytes copied; queued on the current stream."""
+    if uplo not in ("U", "L"):
+        raise ValueError("uplo must be 'U' or 'L'")
+    if op.rows != op.cols or tuple(a_host.shape) != (op.rows, op.cols):
+        raise ValueError("upload_symmetric needs a square host array of the operator's shape")
+    if a_host.device.type != "cpu" or a_host.dtype != op.fmt.torch_dtype or a_host.stride(1) != 1:
+        raise ValueError("upload_symmetric needs a row-major host tensor in the operator's storage dtype")
+    L = _lib.load()
+    nbytes = ctypes.c_longlong(0)
+    _lib.check(L.ofrr_upload_sym(a_host.data_ptr(), a_host.stride(0), op.ptr, op.lda, op.rows, int(op.fmt),
+                                 0 if uplo == "U" else 1, int(block_rows), ctypes.addressof(nbytes),
+                                 torch.cuda.current_stream(op.device).cuda_stream), "upload symmetric operator")
+    return int(nbytes.value)
 
 
 def block_from_host(x, fmt: FpFormat, device) -> DevBlock:
