@@ -34,11 +34,10 @@ static constexpr int HT = OFRR_HESS_THREADS;
 struct HessWs {
   unsigned* bar_count;  // grid barrier arrivals (monotonic)
   unsigned long long* key;  // [k] packed (|pivot| f32 bits, ~row) maxima, non-f64 storage
-  double* cand_val;   // [2][G]
-  long long* cand_idx;  // [2][G]
   double* cand_row;   // [2][G][k]
   unsigned char* freerow;  // [n]
   ulonglong2* slot;   // [2][G] narrow storage: (packed key, (pivot value, next-column value) as f32 bits)
+  double2* slot64;    // [2][G][2] F64 storage: (|candidate|, row as bits), (pivot value, next-column value)
 };
 
 __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* sv, long long* si) {
@@ -139,12 +138,21 @@ template <typename T, typename V> __device__ __forceinline__ T st_s(V v) {
     }
   }
 }
+// L2 load (bypasses L1: written by other CTAs during the launch) of any storage element
+template <typename T> __device__ __forceinline__ T ldcg_el(const T* p) {
+  T r;
+  if constexpr (sizeof(T) == 1) { const unsigned char b = __ldcg(reinterpret_cast<const unsigned char*>(p)); memcpy(&r, &b, 1); }
+  else if constexpr (sizeof(T) == 2) { const unsigned short b = __ldcg(reinterpret_cast<const unsigned short*>(p)); memcpy(&r, &b, 2); }
+  else if constexpr (sizeof(T) == 4) { const unsigned b = __ldcg(reinterpret_cast<const unsigned*>(p)); memcpy(&r, &b, 4); }
+  else { const unsigned long long b = __ldcg(reinterpret_cast<const unsigned long long*>(p)); memcpy(&r, &b, 8); }
+  return r;
+}
 template <typename T> __device__ __forceinline__ double el_d(T y) {
   if constexpr (std::is_same<T, f8>::value) { __nv_fp8_e4m3 v; v.__x = y.x; return (double)float(v); }
   else return to_d(y);
 }
 
-__device__ unsigned long long g_hessprof[8];   // debug: CTA 0 per-phase time (ns), last launch
+__device__ unsigned long long g_hessprof[10];   // debug: CTA 0 per-phase time (ns), last launch
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(HT)
   using CV = typename CT<C>::type;
   __shared__ double sv[HT / 32];
   __shared__ long long si[HT / 32];
-  extern __shared__ double dyn[];
+  extern __shared__ __align__(16) double dyn[];
   double* prow = dyn;                                        // pivot row values, k entries
   CV* pc = reinterpret_cast<CV*>(dyn + k);                   // alpha_c (compute format), k entries
   // panel mode (pb > 1): the pivot rows of the panel's kept steps (compute format, k each)
@@ -168,6 +176,8 @@ __global__ void __launch_bounds__(HT)
   CV* PR = reinterpret_cast<CV*>(dyn + 2 * k);
   __shared__ int s_pl[32];                                   // kept steps of the panel
   __shared__ int s_npl;
+  __shared__ long long s_prow[32];                           // their pivot rows
+  __shared__ int s_pnk[32];                                  // and Q columns
 
   const int G = gridDim.x, c = blockIdx.x;
   const int64_t rows_per = (n + G - 1) / G;
@@ -176,8 +186,8 @@ __global__ void __launch_bounds__(HT)
   const int64_t nr = r1 - r0;
   // my working rows: in shared memory when they fit (column-major, ld rows_per), else in
   // the global workspace.  Xw is indexed with global row numbers.
-  const int64_t ldw = in_smem ? rows_per : ldg;
-  const size_t pr_dbl = pb > 1 ? ((size_t)pb * k * sizeof(CV) + 7) / 8 : 0;   // PR, in doubles
+  const int64_t ldw = in_smem ? ((rows_per + 3) & ~(int64_t)3) : ldg;   // 16-byte columns for 4-byte storage
+  const size_t pr_dbl = pb > 1 ? ((size_t)(pb * k + pb * pb) * sizeof(CV) + 7) / 8 : 0;   // PR + M, in doubles
   T* Xw = in_smem ? reinterpret_cast<T*>(dyn + 2 * k + pr_dbl) - r0 : Xg;
   // rows in global memory + panels: the current panel's columns are cached in shared
   // memory (col(cc) is a row-indexed pointer to column cc wherever it lives)
@@ -189,8 +199,16 @@ __global__ void __launch_bounds__(HT)
   };
   auto load_panel = [&](int q0) {   // global -> shared memory (caller syncs before and after)
     const int qe = min(k, q0 + pb);
-    for (int cc = q0; cc < qe; ++cc)
-      for (int64_t i = threadIdx.x; i < nr; i += HT) Pw[(int64_t)(cc - q0) * nr + i] = Xw[(int64_t)cc * ldw + r0 + i];
+    constexpr int PU = 8;             // columns in flight per thread (latency-bound otherwise)
+    for (int c0 = q0; c0 < qe; c0 += PU)
+      for (int64_t i = threadIdx.x; i < nr; i += HT) {
+        T v[PU];
+#pragma unroll
+        for (int u = 0; u < PU; ++u) v[u] = c0 + u < qe ? Xw[(int64_t)(c0 + u) * ldw + r0 + i] : T();
+#pragma unroll
+        for (int u = 0; u < PU; ++u)
+          if (c0 + u < qe) Pw[(int64_t)(c0 + u - q0) * nr + i] = v[u];
+      }
     cp0 = q0;
   };
   // thread -> (row, column phase) for the trailing updates: two threads per row when the
@@ -200,9 +218,33 @@ __global__ void __launch_bounds__(HT)
   const int trow = threadIdx.x % rb, tcol = threadIdx.x / rb;
 
   // prologue: private copy of my rows, free flags
-  for (int j = 0; j < k; ++j)
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Xw[(int64_t)j * ldw + i] = X[(int64_t)j * ldx + i];
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) ws.freerow[i] = 1;
+  {
+    constexpr int PU = 16;            // columns in flight per thread: the copy is latency-bound otherwise
+    for (int j0 = 0; j0 < k; j0 += PU)
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+        T v[PU];
+#pragma unroll
+        for (int u = 0; u < PU; ++u) v[u] = j0 + u < k ? X[(int64_t)(j0 + u) * ldx + i] : T();
+#pragma unroll
+        for (int u = 0; u < PU; ++u)
+          if (j0 + u < k) Xw[(int64_t)(j0 + u) * ldw + i] = v[u];
+      }
+  }
+  if (in_smem)   // pad rows of the shared-memory tile (computed on by the 16-byte updates, never read)
+    for (int j = 0; j < k; ++j)
+      for (int64_t i = r1 + threadIdx.x; i < r0 + ldw; i += HT) Xw[(int64_t)j * ldw + i] = T();
+  // free rows: this thread's rows are r0 + threadIdx.x + m * HT in every row loop below, so
+  // their flags live in a register bit mask (bit m) -- no memory access on the per-column
+  // critical path; a global byte array only when a thread owns more than 64 rows
+  const bool fmask = rows_per <= (int64_t)64 * HT;
+  unsigned long long fm = 0;
+  if (fmask) {
+    const int64_t mine = nr > threadIdx.x ? (nr - threadIdx.x + HT - 1) / HT : 0;
+    fm = mine >= 64 ? ~0ull : ((1ull << mine) - 1ull);
+  } else {
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) ws.freerow[i] = 1;
+  }
+  auto is_free = [&](int64_t i, int m) -> bool { return fmask ? ((fm >> m) & 1ull) : ws.freerow[i]; };
   __syncthreads();
   if (pwc) {
     load_panel(0);
@@ -236,10 +278,12 @@ __global__ void __launch_bounds__(HT)
   constexpr bool KEYED = !std::is_same<T, double>::value;
   __shared__ unsigned long long sk[HT / 32];
   __shared__ float s_v0, s_v1;                               // candidate / pivot: value, next column
+  __shared__ double s_d0, s_d1;                              // the same, F64 storage
   // this thread's candidate over its rows i (free rows only) of column jn
   auto local_scan = [&](int jn, double& v, long long& idx, unsigned long long& key) {
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
-      if (!ws.freerow[i]) continue;
+    int m = 0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT, ++m) {
+      if (!is_free(i, m)) continue;
       const double a = fabs(el_d(col(jn)[i]));
       if constexpr (KEYED) {
         const unsigned long long kk = cand_key((float)a, i);
@@ -254,33 +298,38 @@ __global__ void __launch_bounds__(HT)
   // in Xw: their values for the candidate row are formed here with exactly the arithmetic
   // of the deferred update.
   // pending beyond the panel: columns >= pe still owe the panel's kept steps s_pl[0..npl)
+  // Panels (pb > 1): only the panel's columns [jn, lim) are published -- the columns beyond
+  // the panel take the panel's pivot rows at its end (compute_pr), straight from memory.
   auto publish = [&](int jn, int buf, bool pending, int jp, double v, long long idx, unsigned long long key,
-                     int pe, int npl) {
+                     int pe, int npl, int lim) {
     if constexpr (KEYED) {
       key = block_max_key(key, sk);
       idx = key ? (long long)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull)) : -1;
     } else {
       block_argmax(v, idx, sv, si);
-      if (threadIdx.x == 0) {
-        ws.cand_val[buf * G + c] = v;
-        ws.cand_idx[buf * G + c] = idx;
-      }
     }
     if (idx >= 0) {
       const CV vr = pending ? ld_c<C>(col(jp)[idx]) : CV(0);
-      for (int cc = jn + threadIdx.x; cc < k; cc += HT) {
-        T y = col(cc)[idx];
-        if (cc < pe) {
-          if (pending && cc > jn) y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(pc[cc], vr)));
-        } else {
-          for (int q = 0; q < npl; ++q)    // the panel's kept steps, in order (bitwise the blocked update)
-            y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(PR[(size_t)q * k + cc], ld_c<C>(col(s_pl[q])[idx]))));
-        }
+      for (int cc = jn + threadIdx.x; cc < lim; cc += HT) {
+        T y = col(cc)[idx];            // cc < lim <= pe: a panel column (or no panels)
+        if (pending && cc > jn) y = st_s<T>(csub<C>(ld_c<C>(y), cmul<C>(pc[cc], vr)));
         ws.cand_row[((int64_t)buf * G + c) * k + cc] = el_d(y);
         if constexpr (KEYED) {
           if (cc == jn) s_v0 = (float)el_d(y);
           if (cc == jn + 1) s_v1 = (float)el_d(y);
+        } else {
+          if (cc == jn) s_d0 = el_d(y);
+          if (cc == jn + 1) s_d1 = el_d(y);
         }
+      }
+    }
+    if constexpr (!KEYED) {
+      // one 32-byte slot per CTA: (|candidate|, row) and the row's pivot and next-column
+      // values -- the critical path after the barrier needs no second read of the row
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __stcg(&ws.slot64[((int64_t)buf * G + c) * 2], make_double2(v, __longlong_as_double(idx)));
+        __stcg(&ws.slot64[((int64_t)buf * G + c) * 2 + 1], make_double2(s_d0, jn + 1 < lim ? s_d1 : 0.0));
       }
     }
     if constexpr (KEYED) {
@@ -296,36 +345,86 @@ __global__ void __launch_bounds__(HT)
       }
     }
   };
-  // panel end: columns >= pe take the panel's kept steps, element by element in step order
+  // panel end, step 1: the panel's pivot rows in the columns beyond it, PR[q][cc] = row
+  // s_prow[q] of column cc after the panel's kept steps 0..q-1 -- formed here from memory
+  // (columns >= pe are untouched during the panel; the multipliers are the pivot rows'
+  // entries of the panel's Q columns), with exactly the arithmetic of the blocked update.
+  // Wavefront order: PR[q'] is final once steps 0..q'-1 are in, then step q' goes into every
+  // later row at once (independent chains per column).
+  auto compute_pr = [&](int pe, int npl) {
+    if (npl == 0 || pe >= k) return;
+    constexpr int QMAX = 32;
+    CV* Mq = reinterpret_cast<CV*>(PR + (size_t)pb * k);     // [npl][npl]: M[q][q'] (q' < q)
+    for (int e = threadIdx.x; e < npl * npl; e += HT) {
+      const int q = e / npl, q2 = e - q * npl;
+      Mq[e] = q2 < q ? ld_c<C>(ldcg_el(&Q[(int64_t)s_pnk[q2] * ldq + s_prow[q]])) : CV(0);
+    }
+    __syncthreads();
+    for (int cc = pe + threadIdx.x; cc < k; cc += HT) {
+      T y[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) y[q] = q < npl ? ldcg_el(&Xw[(int64_t)cc * ldw + s_prow[q]]) : T();
+#pragma unroll
+      for (int q2 = 0; q2 < QMAX; ++q2) {
+        if (q2 < npl) {
+          const CV a = ld_c<C>(y[q2]);
+          PR[(size_t)q2 * k + cc] = a;
+#pragma unroll
+          for (int q = q2 + 1; q < QMAX; ++q)
+            if (q < npl) y[q] = st_s<T>(csub<C>(ld_c<C>(y[q]), cmul<C>(a, Mq[q * npl + q2])));
+        }
+      }
+    }
+    __syncthreads();
+  };
+  // panel end, step 2: columns >= pe take the panel's kept steps, element by element in step
+  // order.  Work units (row, 8-column segment), rows fastest (coalesced): each unit holds its
+  // row's npl multipliers and 8 trailing elements in registers, the pivot rows broadcast
+  // from shared memory; every trailing element is read and written once per panel.
   auto blocked_update = [&](int pe, int npl) {
     if (npl == 0 || pe >= k) return;
-    // thread per row: the row's npl multipliers in registers, the pivot rows broadcast
-    // from shared memory, each trailing element read and written once (coalesced)
-    constexpr int QMAX = 32;
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+    constexpr int QMAX = 32, CB = 8;
+    const unsigned nseg = (unsigned)((k - pe + CB - 1) / CB);
+    const unsigned nru = (unsigned)nr, units = nru * nseg;
+    // the next unit's elements are loaded while this unit computes (software pipeline)
+    T yn[CB];
+    auto unit_at = [&](unsigned u, int64_t& i, int& c0) {
+      const unsigned seg = u / nru;
+      i = r0 + (int64_t)(u - seg * nru);
+      c0 = pe + (int)seg * CB;
+    };
+    auto load_unit = [&](unsigned u) {
+      int64_t i;
+      int c0;
+      unit_at(u, i, c0);
+      const T* b = Xw + (int64_t)c0 * ldw + i;
+#pragma unroll
+      for (int v = 0; v < CB; ++v) yn[v] = c0 + v < k ? b[(int64_t)v * ldw] : T();
+    };
+    if (threadIdx.x < units) load_unit(threadIdx.x);
+    for (unsigned u = threadIdx.x; u < units; u += HT) {
+      int64_t i;
+      int c0;
+      unit_at(u, i, c0);
+      T y[CB];
+#pragma unroll
+      for (int v = 0; v < CB; ++v) y[v] = yn[v];
+      if (u + HT < units) load_unit(u + HT);
       CV mult[QMAX];
 #pragma unroll
       for (int q = 0; q < QMAX; ++q) mult[q] = q < npl ? ld_c<C>(col(s_pl[q])[i]) : CV(0);
-      // columns >= pe live in global memory; eight at a time, every load issued before the
-      // stores (the stores could alias the next loads otherwise, serialising the latency)
-      constexpr int CB = 8;
-      T* base = Xw + (int64_t)pe * ldw + i;
-      for (int c0 = pe; c0 < k; c0 += CB, base += CB * ldw) {
-        T y[CB];
+      T* base = Xw + (int64_t)c0 * ldw + i;
 #pragma unroll
-        for (int u = 0; u < CB; ++u) y[u] = c0 + u < k ? base[(int64_t)u * ldw] : T();
+      for (int q = 0; q < QMAX; ++q) {
+        if (q < npl) {
+          const CV* pr = PR + (size_t)q * k + c0;               // may run past row q: unused lanes
 #pragma unroll
-        for (int q = 0; q < QMAX; ++q) {
-          if (q < npl) {
-#pragma unroll
-            for (int u = 0; u < CB; ++u)
-              y[u] = st_s<T>(csub<C>(ld_c<C>(y[u]), cmul<C>(PR[(size_t)q * k + min(c0 + u, k - 1)], mult[q])));
-          }
+          for (int v = 0; v < CB; ++v) y[v] = st_s<T>(csub<C>(ld_c<C>(y[v]), cmul<C>(pr[v], mult[q])));
         }
-#pragma unroll
-        for (int u = 0; u < CB; ++u)
-          if (c0 + u < k) base[(int64_t)u * ldw] = y[u];
       }
+#pragma unroll
+      for (int v = 0; v < CB; ++v)
+        if (c0 + v < k) base[(int64_t)v * ldw] = y[v];
     }
   };
 
@@ -335,18 +434,16 @@ __global__ void __launch_bounds__(HT)
     long long idx = -1;
     unsigned long long key = 0;
     local_scan(0, v, idx, key);
-    publish(0, 0, false, 0, v, idx, key, k, 0);
+    publish(0, 0, false, 0, v, idx, key, k, 0, pb > 1 ? min(k, pb) : k);
   }
   arrive();
   wait();
 
   int nk = 0;
-  unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0}, tp = gtime();
+  unsigned long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tp = gtime();
   auto mark = [&](int ph) {
     if (c == 0 && threadIdx.x == 0) { const unsigned long long t = gtime(); pacc[ph] += t - tp; tp = t; }
   };
-  __shared__ double s_best;
-  __shared__ long long s_r;
   __shared__ int s_owner;
   for (int j = 0; j < k; ++j) {
     const int buf = j & 1;
@@ -373,30 +470,30 @@ __global__ void __launch_bounds__(HT)
       best = (double)__uint_as_float((unsigned)(key >> 32));
       owner = r >= 0 ? s_owner : 0;
     } else {
-      // warp 0 reduces the CTAs' candidates; max value, ties -> lowest row (CTA row
-      // blocks ascend, so the lowest row is the reference's np.argmax choice)
-      if (threadIdx.x < 32) {
-        double bv = -1.0;
-        long long bi = -1;
-        int bo = -1;
-        for (int cc = threadIdx.x; cc < G; cc += 32) {
-          const long long oi = __ldcg(&ws.cand_idx[buf * G + cc]);
-          const double ov = __ldcg(&ws.cand_val[buf * G + cc]);
-          if (oi >= 0 && (bi < 0 || ov > bv)) { bv = ov; bi = oi; bo = cc; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
-          if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; bo = oo; }
-        }
-        if (threadIdx.x == 0) { s_best = bv; s_r = bi; s_owner = bo; }
+      // every thread reads one CTA's 32-byte slot (one round trip), block argmax: max value,
+      // ties -> lowest row (the reference's np.argmax choice); the winner's pivot and
+      // next-column values travel in its slot
+      double bv = -1.0, d0 = 0.0, d1 = 0.0;
+      long long bi = -1;
+      if (threadIdx.x < G) {
+        const double2 a = __ldcg(&ws.slot64[((int64_t)buf * G + threadIdx.x) * 2]);
+        const double2 b = __ldcg(&ws.slot64[((int64_t)buf * G + threadIdx.x) * 2 + 1]);
+        bv = a.x;
+        bi = __double_as_longlong(a.y);
+        d0 = b.x;
+        d1 = b.y;
+      }
+      const long long mine = bi;
+      block_argmax(bv, bi, sv, si);
+      if (threadIdx.x < G && bi >= 0 && mine == bi) {
+        s_owner = threadIdx.x;
+        s_d0 = d0;
+        s_d1 = d1;
       }
       __syncthreads();
-      best = s_best;
-      r = s_r;
-      owner = s_owner;
+      best = bv;
+      r = bi;
+      owner = r >= 0 ? s_owner : 0;
     }
     // ofrr/basis.py:178-180: skip when no free row or |pivot| < tol (NaN pivots skip too)
     const bool skip = (r < 0) || !(best >= tol);
@@ -406,44 +503,45 @@ __global__ void __launch_bounds__(HT)
       // value itself (storage <= compute)
       // narrow storage: the row's loads are issued now and land in shared memory after the
       // column work below (which needs only the pivot and next-column values of the slot)
+      // the row's loads (the panel's columns) are issued now and land in shared memory after
+      // the column work below, which needs only the pivot and next-column values of the slot
       double prr[2] = {0.0, 0.0};
-      if constexpr (KEYED) {
 #pragma unroll
-        for (int t2 = 0; t2 < 2; ++t2) {
-          const int cc = j + threadIdx.x + t2 * HT;
-          if (cc < k) prr[t2] = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
-        }
-        for (int cc = j + threadIdx.x + 2 * HT; cc < k; cc += HT) {   // k > 2 HT + j: rare
-          const double a = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
-          prow[cc] = a;
-          pc[cc] = (CV)a;
-        }
-      } else {
-        for (int cc = j + threadIdx.x; cc < k; cc += HT) {
-          const double a = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
-          prow[cc] = a;
-          pc[cc] = (CV)a;
+      for (int t2 = 0; t2 < 2; ++t2) {
+        const int cc = j + threadIdx.x + t2 * HT;
+        if (cc < pe) prr[t2] = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
+      }
+      for (int cc = j + threadIdx.x + 2 * HT; cc < pe; cc += HT) {   // pe > 2 HT + j: rare
+        const double a = __ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
+        prow[cc] = a;
+        pc[cc] = (CV)a;
+      }
+      if (r >= r0 && r < r1) {
+        if (!fmask) {
+          if (threadIdx.x == 0) ws.freerow[r] = 0;
+        } else if ((r - r0) % HT == threadIdx.x) {
+          fm &= ~(1ull << (int)((r - r0) / HT));
         }
       }
-      if (r >= r0 && r < r1 && threadIdx.x == 0) ws.freerow[r] = 0;
       if (c == 0 && threadIdx.x == 0) { kept[j] = 1; pivots[nk] = r; }
-      if (pb > 1 && pe < k) {                                  // this step, owed by columns >= pe
-        const int q = s_npl;
-        for (int cc = pe + threadIdx.x; cc < k; cc += HT)
-          PR[(size_t)q * k + cc] = (CV)__ldcg(&ws.cand_row[((int64_t)buf * G + owner) * k + cc]);
-      }
       __syncthreads();
-      if (pb > 1 && pe < k && threadIdx.x == 0) { s_pl[s_npl] = j; s_npl = s_npl + 1; }
+      if (pb > 1 && pe < k && threadIdx.x == 0) {            // this step, owed by columns >= pe
+        s_pl[s_npl] = j;
+        s_prow[s_npl] = r;
+        s_pnk[s_npl] = nk;
+        s_npl = s_npl + 1;
+      }
       mark(1);
-      const CV piv = KEYED ? (CV)s_v0 : pc[j];
-      const CV a1 = j + 1 < pe ? (KEYED ? (CV)s_v1 : pc[j + 1]) : CV(0);
+      const CV piv = KEYED ? (CV)s_v0 : (CV)s_d0;
+      const CV a1 = j + 1 < pe ? (KEYED ? (CV)s_v1 : (CV)s_d1) : CV(0);
       // ofrr/basis.py:181-187: v = round_s(round_c(v / piv)); v[r] = 1; then (188-190,
       // precision.py:172-180) column j+1 at once -- the next pivot search needs it -- and
       // this thread's candidate for it
       double cv = -1.0;
       long long cidx = -1;
       unsigned long long ckey = 0;
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) {
+      int m = 0;
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += HT, ++m) {
         const T v = (i == r) ? st_s<T>(CV(1)) : st_s<T>(cdiv<C>(ld_c<C>(col(j)[i]), piv));
         col(j)[i] = v;
         Q[(int64_t)nk * ldq + i] = v;
@@ -451,7 +549,7 @@ __global__ void __launch_bounds__(HT)
           T* yp = col(j + 1) + i;
           const T y = st_s<T>(csub<C>(ld_c<C>(*yp), cmul<C>(a1, ld_c<C>(v))));
           *yp = y;
-          if (i != r && ws.freerow[i]) {
+          if (i != r && is_free(i, m)) {
             const double a = fabs(el_d(y));
             if constexpr (KEYED) {
               const unsigned long long kk = cand_key((float)a, i);
@@ -462,22 +560,67 @@ __global__ void __launch_bounds__(HT)
           }
         }
       }
-      if constexpr (KEYED) {
 #pragma unroll
-        for (int t2 = 0; t2 < 2; ++t2) {
-          const int cc = j + threadIdx.x + t2 * HT;
-          if (cc < k) { prow[cc] = prr[t2]; pc[cc] = (CV)prr[t2]; }
-        }
+      for (int t2 = 0; t2 < 2; ++t2) {
+        const int cc = j + threadIdx.x + t2 * HT;
+        if (cc < pe) { prow[cc] = prr[t2]; pc[cc] = (CV)prr[t2]; }
       }
       mark(2);
       if (j + 1 < pe) {
         __syncthreads();                                       // s_pl / s_npl visible
-        publish(j + 1, buf ^ 1, true, j, cv, cidx, ckey, pe, pb > 1 ? s_npl : 0);
+        publish(j + 1, buf ^ 1, true, j, cv, cidx, ckey, pe, pb > 1 ? s_npl : 0, pe);
         arrive();
         mark(3);
         // ... columns j+2.. while the other CTAs catch up (hidden behind the barrier).
+        bool vec_done = false;
+        if constexpr (sizeof(T) == 4) {
+          if (in_smem) {
+            // 4-byte storage in shared memory: four consecutive rows per 16-byte access (the
+            // columns are 16-byte aligned, ldw % 4 == 0; the pad rows past r1 compute garbage
+            // nobody reads), threads spread over (row quad, column phase), two columns in flight
+            const int ngr = (int)((nr + 3) >> 2);
+            const bool wide = ngr >= HT;
+            const int P = wide ? 1 : HT / max(ngr, 1);
+            const int ph = wide ? 0 : threadIdx.x / max(ngr, 1);
+            if (ngr > 0 && ph < P) {
+              for (int g = wide ? threadIdx.x : threadIdx.x % ngr; g < ngr; g += wide ? HT : ngr) {
+                float* base = reinterpret_cast<float*>(Xw + r0) + 4 * g;
+                const float4 vq = *reinterpret_cast<const float4*>(base + (int64_t)j * ldw);
+                const CV v0 = ld_c<C>(vq.x), v1 = ld_c<C>(vq.y), v2 = ld_c<C>(vq.z), v3 = ld_c<C>(vq.w);
+                auto upd = [&](float4 y, CV a) {
+                  y.x = st_s<T>(csub<C>(ld_c<C>(y.x), cmul<C>(a, v0)));
+                  y.y = st_s<T>(csub<C>(ld_c<C>(y.y), cmul<C>(a, v1)));
+                  y.z = st_s<T>(csub<C>(ld_c<C>(y.z), cmul<C>(a, v2)));
+                  y.w = st_s<T>(csub<C>(ld_c<C>(y.w), cmul<C>(a, v3)));
+                  return y;
+                };
+                // U columns in flight per thread (all loads before the stores)
+                constexpr int U = 4;
+                int cc = j + 2 + ph;
+                for (; cc + (U - 1) * P < pe; cc += U * P) {
+                  float4* pp[U];
+                  float4 y[U];
+                  CV a[U];
+#pragma unroll
+                  for (int u = 0; u < U; ++u) {
+                    pp[u] = reinterpret_cast<float4*>(base + (int64_t)(cc + u * P) * ldw);
+                    y[u] = *pp[u];
+                    a[u] = pc[cc + u * P];
+                  }
+#pragma unroll
+                  for (int u = 0; u < U; ++u) *pp[u] = upd(y[u], a[u]);
+                }
+                for (; cc < pe; cc += P) {
+                  float4* p0 = reinterpret_cast<float4*>(base + (int64_t)cc * ldw);
+                  *p0 = upd(*p0, pc[cc]);
+                }
+              }
+            }
+            vec_done = true;
+          }
+        }
         // Two rows x two columns per iteration, all loads before the stores (ILP).
-        for (int64_t i0 = r0 + trow; i0 < r1; i0 += 2 * rb) {
+        for (int64_t i0 = r0 + trow; !vec_done && i0 < r1; i0 += 2 * rb) {
           const bool h1 = i0 + rb < r1;
           const CV v0 = ld_c<C>(col(j)[i0]);
           const CV v1 = h1 ? ld_c<C>(col(j)[i0 + rb]) : CV(0);
@@ -510,20 +653,25 @@ __global__ void __launch_bounds__(HT)
       } else if (pe < k) {
         // the panel's last column: columns >= pe take its kept steps, then column pe's search
         __syncthreads();
+        compute_pr(pe, s_npl);
+        mark(6);
         blocked_update(pe, s_npl);
         __syncthreads();
         if (threadIdx.x == 0) s_npl = 0;                       // next panel (read after the barrier)
+        mark(7);
         if (pwc) {
           load_panel(pe);
           __syncthreads();
         }
+        mark(8);
         double v = -1.0;
         long long idx = -1;
         unsigned long long key = 0;
         local_scan(pe, v, idx, key);
-        publish(pe, buf ^ 1, false, 0, v, idx, key, k, 0);
+        publish(pe, buf ^ 1, false, 0, v, idx, key, k, 0, min(k, pe + pb));
         arrive();
         wait();
+        mark(9);
       }
       ++nk;
     } else {
@@ -532,6 +680,7 @@ __global__ void __launch_bounds__(HT)
         __syncthreads();
         const bool pend = j + 1 == pe;                         // panel end: blocked update first
         if (pend) {
+          compute_pr(pe, s_npl);
           blocked_update(pe, s_npl);
           __syncthreads();
           if (threadIdx.x == 0) s_npl = 0;
@@ -544,7 +693,8 @@ __global__ void __launch_bounds__(HT)
         long long idx = -1;
         unsigned long long key = 0;
         local_scan(j + 1, v, idx, key);
-        publish(j + 1, buf ^ 1, false, 0, v, idx, key, pend ? k : pe, pend ? 0 : (pb > 1 ? s_npl : 0));
+        publish(j + 1, buf ^ 1, false, 0, v, idx, key, pend ? k : pe, pend ? 0 : (pb > 1 ? s_npl : 0),
+                pb > 1 ? (pend ? min(k, pe + pb) : pe) : k);
         arrive();
         wait();
       }
@@ -555,7 +705,7 @@ __global__ void __launch_bounds__(HT)
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Q[(int64_t)j * ldq + i] = st_s<T>(CV(0));
   if (c == 0 && threadIdx.x == 0) {
     *n_kept = nk;
-    for (int i = 0; i < 6; ++i) g_hessprof[i] = pacc[i];
+    for (int i = 0; i < 10; ++i) g_hessprof[i] = pacc[i];
   }
 }
 
@@ -589,8 +739,7 @@ int hess_mode(int force_global, int pb) {
 size_t hessenberg_ws(int64_t n, int k, int storage) {
   const int G = hess_grid(n);
   size_t b = 256 + (size_t)k * 8 + 256;
-  b += 2 * G * sizeof(double);
-  b += 2 * G * sizeof(long long);
+  b += (size_t)2 * G * 32 + 256;           // F64 slots
   b += (size_t)2 * G * k * sizeof(double);
   b += (size_t)2 * G * 16 + 256;            // slots
   b += (size_t)n * fmt_bytes(storage) * k;  // working copy
@@ -608,8 +757,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   h.bar_count = (unsigned*)take(256);
   h.key = (unsigned long long*)take((size_t)k * 8);
   OFRR_CUDA_TRY(cudaMemsetAsync(h.bar_count, 0, 256 + ((size_t)k * 8 + 255) / 256 * 256, st));
-  h.cand_val = (double*)take(2 * G * sizeof(double));
-  h.cand_idx = (long long*)take(2 * G * sizeof(long long));
+  h.slot64 = (double2*)take((size_t)2 * G * 32);
   h.cand_row = (double*)take((size_t)2 * G * k * sizeof(double));
   h.slot = (ulonglong2*)take((size_t)2 * G * 16);
   T* Xw = (T*)take((size_t)n * sizeof(T) * k);
@@ -618,7 +766,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   T* Qp = (T*)Q;
   int64_t ldw = n;
   const int64_t rows_per = (n + G - 1) / G;
-  const size_t tile = (size_t)rows_per * k * sizeof(T);
+  const size_t tile = (size_t)((rows_per + 3) & ~(int64_t)3) * k * sizeof(T);   // kernel: ldw % 4 == 0
   // up to the 227 KB opt-in per CTA (one CTA per SM): C3's fp32 rows (443 x 128) fit
   const size_t smem_max = 226 * 1024;
   // rows in shared memory: no panels (the per-step trailing update hides behind the grid
@@ -626,7 +774,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   // columns beyond the panel updated once per panel (OFRR_HESS_PANEL overrides pb, <= 32)
   if (g_hess_pb == -2) { const char* e = getenv("OFRR_HESS_PANEL"); g_hess_pb = e ? atoi(e) : -1; }
   const int pb_env = g_hess_pb;
-  auto pr_bytes = [&](int b) { return b > 1 ? (((size_t)b * k * sizeof(typename CT<C>::type) + 7) / 8) * 8 : 0; };
+  auto pr_bytes = [&](int b) { return b > 1 ? (((size_t)(b * k + b * b) * sizeof(typename CT<C>::type) + 7) / 8) * 8 : 0; };
   const size_t base = (size_t)2 * k * sizeof(double);
   int in_smem = (base + tile + 16 <= smem_max && !g_hess_force_global) ? 1 : 0;
   int pb = 1;

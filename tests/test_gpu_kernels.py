@@ -153,6 +153,27 @@ def test_hessenberg_bitwise(ofrr_gpu, oracle, pol, n, k):
     np.testing.assert_array_equal(_host(h.Q, nk), q)
 
 
+@pytest.mark.parametrize("pol", [(F32, F32, F32), (F64, F64, F64), (BF16, F32, F32), (F32, F64, F64)])
+def test_hessenberg_c3_shape_bitwise(ofrr_gpu, oracle, pol):
+    """K3 at the headline shape (65536 x 128: 443 rows per CTA, the fp32 rows in shared
+    memory with 16-byte trailing updates, the fp64 rows in global memory with panels), a
+    dependent column included: Q, pivots and kept bit for bit."""
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    s, c, a_ = pol
+    n, k = 65536, 128
+    rng = np.random.default_rng(65)
+    x = o.round_to(rng.random((n, k)) - 0.25, s)
+    x[:, 77] = o.round_to(0.5 * x[:, 3], s)
+    h = ops.hessenberg(_blk(p, x, s), p.FpFormat(s), p.FpFormat(c), o.EPS[s])
+    nk = int(h.n_kept.item())
+    q, piv, kept = o.hessenberg_basis(x, o.Pol(s, c, a_))
+    assert nk == q.shape[1] and nk < k
+    np.testing.assert_array_equal(h.pivots[:nk].cpu().numpy(), piv)
+    np.testing.assert_array_equal(h.kept[:k].cpu().numpy().astype(bool), kept)
+    np.testing.assert_array_equal(_host(h.Q, nk), q)
+
+
 @pytest.mark.parametrize("pol", [(BF16, F32, F32), (F32, F32, F32), (F64, F64, F64), (FP8, BF16, F32)])
 @pytest.mark.parametrize("pb", [1, 8, 32])
 def test_hessenberg_global_panels_bitwise(ofrr_gpu, oracle, pol, pb):
