@@ -320,7 +320,7 @@ def _rows(cfg) -> int:
 
 def make_iter_config(p, cfg):
     """The IterConfig of a bench config (also used by tests/ and scripts/)."""
-    return p.IterConfig(k=cfg["k"], m=cfg.get("m", MAX_OUTER), iter=1, basis_method=p.BasisMethod.HESS_LEFT,
+    return p.IterConfig(k=cfg["k"], m=cfg.get("m", MAX_OUTER), iter=cfg.get("iter", 1), basis_method=p.BasisMethod.HESS_LEFT,
                         projection="ofrr", policy=p.POLICY_PRESETS[cfg["policy"]], seed=SEED, tol=cfg["tol"],
                         top=cfg["top"] if cfg["tol"] is not None else None,
                         ladder=_ladder(p, cfg.get("ladder")), ladder_switch=cfg.get("switch", 1e-4),
@@ -349,7 +349,7 @@ def _config_block(name, cfg, world):
     n, rows = cfg["n"], _rows(cfg)
     out = {"workload": cfg["name"], "name": name, "kind": cfg.get("kind", "eig"), "n": n, "top": cfg["top"],
            "k": cfg["k"], "tol": cfg["tol"], "policy": cfg["policy"], "ladder": cfg.get("ladder"),
-           "reuse_av": bool(cfg.get("reuse", False)),
+           "reuse_av": bool(cfg.get("reuse", False)), "iter": int(cfg.get("iter", 1)),
            "parallelism": f"row-partitioned x{world}" if world > 1 else "single",
            "l2": "inputs larger than L2 (A = %d MiB per GPU)" % (((rows + world - 1) // world) * n * 2 >> 20)}
     if rows != n:

@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(HT)
   auto blocked_update = [&](int pe, int npl) {
     if (npl == 0 || pe >= k) return;
     constexpr int QMAX = 32, CB = 8;
+    const bool kvec = (k % 4 == 0) && (pb % 4 == 0);   // PR rows and segments 16-byte aligned
     const unsigned nseg = (unsigned)((k - pe + CB - 1) / CB);
     const unsigned nru = (unsigned)nr, units = nru * nseg;
     // the next unit's elements are loaded while this unit computes (software pipeline)
@@ -418,8 +419,17 @@ __global__ void __launch_bounds__(HT)
       for (int q = 0; q < QMAX; ++q) {
         if (q < npl) {
           const CV* pr = PR + (size_t)q * k + c0;               // may run past row q: unused lanes
+          CV pv[CB];
+          if (kvec) {                                           // 16-byte broadcasts
 #pragma unroll
-          for (int v = 0; v < CB; ++v) y[v] = st_s<T>(csub<C>(ld_c<C>(y[v]), cmul<C>(pr[v], mult[q])));
+            for (int v = 0; v < CB; v += 16 / (int)sizeof(CV))
+              *reinterpret_cast<uint4*>(&pv[v]) = *reinterpret_cast<const uint4*>(pr + v);
+          } else {
+#pragma unroll
+            for (int v = 0; v < CB; ++v) pv[v] = pr[v];
+          }
+#pragma unroll
+          for (int v = 0; v < CB; ++v) y[v] = st_s<T>(csub<C>(ld_c<C>(y[v]), cmul<C>(pv[v], mult[q])));
         }
       }
 #pragma unroll
