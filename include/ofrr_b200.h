@@ -227,6 +227,23 @@ int ofrr_reuse_power(const void* W, int64_t ldw, int w_fmt, int64_t n, int kp, c
                      double* colmax, int* flags, void* stream);
 
 /* ---------------------------------------------------------------------------------
+ * K6f: the restart step of one outer iteration in one pass over (U, W) -- ofrr_ritz_recover
+ * (Xu = round(U Y), U64 = U Y), ofrr_reuse_power (Xw = round(W Y), colmax) and
+ * ofrr_residual_estimate (columns < t, mode as there) fused: both products of a row tile
+ * on the fp64 tensor cores from one Y slab.  Every output is optional (NULL); Xu / U64 / Xw
+ * are bitwise those of the separate entries.  Replaces ofrr/projection.py:86 and
+ * ofrr/driver.py:102-109 of the next iteration (A-pass reuse) plus the convergence estimate.
+ * W (w_fmt F32 or F64) may be NULL when only Xu / U64 are asked for.  The workspace
+ * (ofrr_restart_workspace(n, t) bytes) holds the per-row-block residual sums.
+ * ------------------------------------------------------------------------------- */
+size_t ofrr_restart_workspace(int64_t n, int t);
+int ofrr_restart(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt, int64_t n,
+                 int kp, const double* Y, int ldy, const int* r_dev, int r_max, void* Xu, int64_t ldxu,
+                 int xu_fmt, int* flags_u, double* U64, int64_t ld64, void* Xw, int64_t ldxw, int xw_fmt,
+                 int* flags_w, double* colmax, const double* vals, int t, double* res, int mode,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
  * K7: FP64 residuals  res[j] = || A v_j - lambda_j v_j ||_2 / |lambda_j|  (inf when
  * lambda_j == 0).  Replaces ofrr/projection.py:136-147 residual_report (eig branch).
  * A (rows x cols row-major, a_fmt) is promoted to fp64 exactly.  For the SVD branch

@@ -101,6 +101,10 @@ _SIGS = {
                                 c_vp, c_i64, c_int, c_vp], c_int),
     "ofrr_convert": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_i64, c_i64, c_vp, c_vp], c_int),
     "ofrr_transpose_convert": ([c_vp, c_int, c_i64, c_vp, c_int, c_i64, c_i64, c_i64, c_vp, c_vp], c_int),
+    "ofrr_restart_workspace": ([c_i64, c_int], c_sz),
+    "ofrr_restart": ([c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_i64, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_i64,
+                      c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_sz,
+                      c_vp], c_int),
     "ofrr_upload_sym": ([c_vp, c_i64, c_vp, c_i64, c_i64, c_int, c_int, c_i64, c_vp, c_vp], c_int),
     "ofrr_host_gemm_mixed": ([c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int,
                               c_int, c_vp], c_int),

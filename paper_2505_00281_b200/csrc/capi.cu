@@ -49,6 +49,11 @@ int simt_residual(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_
 int scale_columns(void* X, int64_t n, int k, int64_t ldx, int storage, int compute, const double* colmax, cudaStream_t st);
 int convert(const void* src, int sf, int64_t lds, void* dst, int df, int64_t ldd, int64_t n, int64_t k, int* flags,
             cudaStream_t st);
+size_t restart_ws(int64_t n, int t);
+int restart(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt, int64_t n, int kp,
+            const double* Y, int ldy, const int* r_dev, int r_max, void* Xu, int64_t ldxu, int xu_fmt, int* flags_u,
+            double* U64, int64_t ld64, void* Xw, int64_t ldxw, int xw_fmt, int* flags_w, double* colmax,
+            const double* vals, int t, double* res, int mode, void* ws, size_t ws_bytes, cudaStream_t st);
 int upload_sym(const void* host, int64_t ld_host, void* A, int64_t lda, int64_t n, int fmt, int uplo,
                int64_t block_rows, long long* bytes, cudaStream_t st);
 int transpose_convert(const void* src, int sf, int64_t lds, void* dst, int df, int64_t ldd, int64_t rows, int64_t cols,
@@ -219,6 +224,21 @@ int ofrr_reuse_power(const void* W, int64_t ldw, int w_fmt, int64_t n, int kp, c
   if (!Xout || !colmax || !valid_fmt(x_fmt)) { ofrr_set_error("reuse_power: invalid arguments"); return OFRR_ERR_INVALID; }
   return ritz_recover(W, ldw, w_fmt, n, kp, Y, ldy, r_dev, r_max, 1.0, nullptr, 0, Xout, ldx, x_fmt, flags, S(stream),
                       colmax);
+}
+
+size_t ofrr_restart_workspace(int64_t n, int t) { return restart_ws(n, t); }
+int ofrr_restart(const void* U, int64_t ldu, int u_fmt, const void* W, int64_t ldw, int w_fmt, int64_t n, int kp,
+                 const double* Y, int ldy, const int* r_dev, int r_max, void* Xu, int64_t ldxu, int xu_fmt,
+                 int* flags_u, double* U64, int64_t ld64, void* Xw, int64_t ldxw, int xw_fmt, int* flags_w,
+                 double* colmax, const double* vals, int t, double* res, int mode, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  if (!valid_fmt(u_fmt) || (W && !valid_fmt(w_fmt)) || (Xu && !valid_fmt(xu_fmt)) || (Xw && !valid_fmt(xw_fmt)) ||
+      n < 0 || kp < 0 || r_max < 0 || t < 0) {
+    ofrr_set_error("restart: invalid arguments");
+    return OFRR_ERR_INVALID;
+  }
+  return restart(U, ldu, u_fmt, W, ldw, w_fmt, n, kp, Y, ldy, r_dev, r_max, Xu, ldxu, xu_fmt, flags_u, U64, ld64, Xw,
+                 ldxw, xw_fmt, flags_w, colmax, vals, t, res, mode, workspace, workspace_bytes, S(stream));
 }
 
 size_t ofrr_residual_workspace(int64_t rows, int r) { return residual_ws(rows, r); }

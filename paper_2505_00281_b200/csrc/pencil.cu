@@ -27,7 +27,7 @@ static constexpr int PK_MAX = 160;        // one k x (k|1) fp64 matrix in shared
 
 __device__ __forceinline__ int pc_ld(int k) { return k | 1; }
 
-__device__ unsigned long long g_pcprof[16];   // debug: phase end times (globaltimer ns | SM clock)
+__device__ unsigned long long g_pcprof[24];   // debug: phase end times (globaltimer ns | SM clock)
 __device__ __forceinline__ void pc_mark(int i) {
   if (threadIdx.x == 0) {
     unsigned long long t;
@@ -117,6 +117,225 @@ __global__ void __launch_bounds__(PT, 1)
       xs = fma(v, v, xs);
     }
   const double xn2 = pc_block_sum(xs, red);
+  // mu_min(M) >= 1 / ||X||_F^2 must clear the reference's cutoff k eps mu_max (<= ||M||_F)
+  const bool cert = (1.0 / xn2) > 4.0 * (double)k * 2.220446049250313e-16 * mnorm;
+  if (threadIdx.x == 0) *gate = cert ? 0 : 1;
+  pc_mark(3);
+}
+
+// ---------------------------------------------------------------------------------
+// K5a, blocked (64 < k <= 128): the same Cholesky + inverse + certificate on 32 x 32
+// blocks, so that the k-step serial chain becomes kb = ceil(k/32) short ones.
+//   diagonal block b: one warp, lane r holding row r in registers -- Cholesky with the
+//     column broadcast by shuffles, then its triangular inverse Xd_bb (rows finalised in
+//     order, each broadcast to the later lanes);
+//   panel and trailing update: L_ib = A_ib Xd_bb^T, A_ij -= L_ib L_jb^T, a warp per block;
+//   X = L^-1 by block rows: X_ib = -Xd_ii (sum_{b <= m < i} L_im X_mb), all b at once.
+// L and X live as lower block triangles in shared memory (10 + 10 blocks, ld 33); the
+// matrix is padded with the identity to 32 kb.  Not bitwise the column-by-column kernel
+// (different summation order); the certificate and the gate are the same.
+// ---------------------------------------------------------------------------------
+constexpr int CB_N = 32, CB_LD = 33, CB_SZ = CB_N * CB_LD, CB_KB = 4;
+constexpr size_t CB_SMEM = (size_t)2 * (CB_KB * (CB_KB + 1) / 2) * CB_SZ * sizeof(double);
+__device__ __forceinline__ int cb_idx(int i, int j) { return (i * (i + 1) / 2 + j) * CB_SZ; }
+
+__device__ __forceinline__ double pc_fast_div(double a, double b);   // below (MUFU seed + Newton)
+constexpr int CB_T = 256, CB_NW = CB_T / 32;   // 255 registers per thread: the diagonal warp's rows
+__device__ double cb_block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < CB_NW; ++w) s += red[w];   // fixed order, every thread
+  return s;
+}
+
+__global__ void __launch_bounds__(CB_T, 1)
+    k_pc_chol_blk(const double* __restrict__ M, int k, double* __restrict__ Xg, int* __restrict__ gate) {
+  extern __shared__ __align__(16) double sm[];
+  double* Lr = sm;                                   // lower block triangle: A, then L
+  double* Xr = sm + (size_t)(CB_KB * (CB_KB + 1) / 2) * CB_SZ;   // X = L^-1 (diagonal blocks: Xd)
+  __shared__ double red[CB_NW];
+  __shared__ double sdg[CB_N], srd[CB_N];
+  __shared__ int s_fail;
+  // this thread's entries (i, c), c <= i < 32, of a diagonal block: e = i (i + 1) / 2 + c
+  int pi[3], pc_[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int e = threadIdx.x + CB_T * q;
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    pi[q] = e < CB_N * (CB_N + 1) / 2 ? i : CB_N;            // CB_N: no entry
+    pc_[q] = e < CB_N * (CB_N + 1) / 2 ? e - i * (i + 1) / 2 : CB_N;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kb = (k + CB_N - 1) / CB_N;
+  // ---- load sym(M) (lower blocks, identity padding) and ||sym(M)||_F --------------------
+  double ss = 0.0;
+  for (int e = threadIdx.x; e < k * k; e += CB_T) {
+    const int i = e % k, j = e / k;
+    const double v = 0.5 * (M[(size_t)j * k + i] + M[(size_t)i * k + j]);
+    ss = fma(v, v, ss);
+  }
+  for (int bi = 0; bi < kb; ++bi)
+    for (int bj = 0; bj <= bi; ++bj)
+      for (int e = threadIdx.x; e < CB_N * CB_N; e += CB_T) {
+        const int r = e & 31, c = e >> 5;
+        const int gi = bi * CB_N + r, gj = bj * CB_N + c;
+        const double v = (gi < k && gj < k) ? 0.5 * (M[(size_t)gj * k + gi] + M[(size_t)gi * k + gj])
+                                            : (gi == gj ? 1.0 : 0.0);
+        Lr[cb_idx(bi, bj) + c * CB_LD + r] = v;
+      }
+  if (threadIdx.x == 0) s_fail = 0;
+  const double mnorm = sqrt(cb_block_sum(ss, red));   // includes the barrier after the loads
+  pc_mark(0);
+
+  // warp-level block product on lane rows: out[c] (row `lane`) += sum_m A(lane, m) B'(m, c)
+  // where B'(m, c) = B(c, m) (BT) or B(m, c); A, B blocks in shared memory (ld 33)
+  auto row_gemm = [&](double (&out)[CB_N], const double* A, const double* B, bool bt) {
+    if (bt) {
+#pragma unroll 2
+      for (int m = 0; m < CB_N; ++m) {
+        const double am = A[m * CB_LD + lane];
+#pragma unroll
+        for (int c = 0; c < CB_N; ++c) out[c] = fma(am, B[m * CB_LD + c], out[c]);
+      }
+    } else {
+#pragma unroll 2
+      for (int m = 0; m < CB_N; ++m) {
+        const double am = A[m * CB_LD + lane];
+#pragma unroll
+        for (int c = 0; c < CB_N; ++c) out[c] = fma(am, B[c * CB_LD + m], out[c]);
+      }
+    }
+  };
+  for (int b = 0; b < kb; ++b) {
+    // ---- diagonal block: Cholesky + triangular inverse by the whole CTA, thread per
+    // lower-triangle entry (up to 3 of the 528); one barrier per step -------------------
+    {
+      double* Ab = Lr + cb_idx(b, b);
+      double* Xb = Xr + cb_idx(b, b);
+      // right-looking, columns scaled at the end: A[i][c] -= A[i][j] A[c][j] / A[j][j]
+      for (int j = 0; j < CB_N; ++j) {
+        const double d = Ab[j * CB_LD + j];
+        if (!(d > 0.0)) { if (threadIdx.x == 0) s_fail = 1; break; }   // uniform: same d everywhere
+        const double inv = pc_fast_div(1.0, d);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int i = pi[q], c = pc_[q];
+          if (c > j) Ab[c * CB_LD + i] -= Ab[j * CB_LD + i] * (Ab[j * CB_LD + c] * inv);
+        }
+        __syncthreads();
+      }
+      if (!s_fail) {
+        // L[i][j] = A[i][j] / sqrt(A[j][j]); X = L^-1 right-looking: row p final at step p
+        // (X[p][c] = (delta_pc - acc[p][c]) / L[p][p]), then acc[i][c] += L[i][p] X[p][c]
+        if (threadIdx.x < CB_N) {
+          const double dg = sqrt(Ab[threadIdx.x * CB_LD + threadIdx.x]);
+          sdg[threadIdx.x] = dg;
+          srd[threadIdx.x] = 1.0 / dg;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int i = pi[q], c = pc_[q];
+          if (i < CB_N) {
+            Ab[c * CB_LD + i] = i == c ? sdg[i] : Ab[c * CB_LD + i] * srd[c];
+            Xb[c * CB_LD + i] = 0.0;
+          }
+        }
+        __syncthreads();
+        for (int pp = 0; pp < CB_N; ++pp) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (pi[q] == pp) Xb[pc_[q] * CB_LD + pp] = ((pc_[q] == pp ? 1.0 : 0.0) - Xb[pc_[q] * CB_LD + pp]) * srd[pp];
+          __syncthreads();
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const int i = pi[q], c = pc_[q];
+            if (i > pp && c <= pp && i < CB_N) Xb[c * CB_LD + i] += Ab[pp * CB_LD + i] * Xb[c * CB_LD + pp];
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {                          // zeros above the diagonal
+          const int i = pi[q], c = pc_[q];
+          if (i < CB_N && i != c) { Ab[i * CB_LD + c] = 0.0; Xb[i * CB_LD + c] = 0.0; }
+        }
+      }
+    }
+    __syncthreads();
+    if (b == 0) pc_mark(20);
+    if (s_fail) break;                                         // uniform
+    // ---- panel: L_ib = A_ib Xd_bb^T (each lane rewrites only its own row) --------------
+    for (int i = b + 1 + warp; i < kb; i += CB_NW) {
+      double out[CB_N];
+#pragma unroll
+      for (int c = 0; c < CB_N; ++c) out[c] = 0.0;
+      double* Ai = Lr + cb_idx(i, b);
+      row_gemm(out, Ai, Xr + cb_idx(b, b), true);              // Xd^T(m, c) = Xd(c, m)
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < CB_N; ++c) Ai[c * CB_LD + lane] = out[c];
+    }
+    __syncthreads();
+    if (b == 0) pc_mark(21);
+    // ---- trailing: A_ij -= L_ib L_jb^T, b < j <= i ------------------------------------
+    {
+      int pidx = 0;
+      for (int i = b + 1; i < kb; ++i)
+        for (int j = b + 1; j <= i; ++j, ++pidx) {
+          if (pidx % CB_NW != warp) continue;
+          double out[CB_N];
+          double* Aij = Lr + cb_idx(i, j);
+#pragma unroll
+          for (int c = 0; c < CB_N; ++c) out[c] = 0.0;
+          row_gemm(out, Lr + cb_idx(i, b), Lr + cb_idx(j, b), true);    // L_jb^T(m, c) = L_jb(c, m)
+#pragma unroll
+          for (int c = 0; c < CB_N; ++c) Aij[c * CB_LD + lane] -= out[c];
+        }
+    }
+    __syncthreads();
+  }
+  if (s_fail) {
+    if (threadIdx.x == 0) *gate = 1;
+    return;
+  }
+  pc_mark(1);
+  // ---- X = L^-1 below the diagonal blocks: block row i after block rows < i -------------
+  for (int i = 1; i < kb; ++i) {
+    for (int b = warp; b < i; b += CB_NW) {
+      double t[CB_N];
+#pragma unroll
+      for (int c = 0; c < CB_N; ++c) t[c] = 0.0;
+      for (int m = b; m < i; ++m) row_gemm(t, Lr + cb_idx(i, m), Xr + cb_idx(m, b), false);  // X_mb(m', c)
+      double* Xib = Xr + cb_idx(i, b);
+#pragma unroll
+      for (int c = 0; c < CB_N; ++c) Xib[c * CB_LD + lane] = t[c];          // scratch: T
+      __syncwarp();
+      double o[CB_N];
+#pragma unroll
+      for (int c = 0; c < CB_N; ++c) o[c] = 0.0;
+      row_gemm(o, Xr + cb_idx(i, i), Xib, false);                            // Xd_ii T
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < CB_N; ++c) Xib[c * CB_LD + lane] = -o[c];
+    }
+    __syncthreads();
+  }
+  pc_mark(2);
+  double xs = 0.0;
+  for (int e = threadIdx.x; e < k * k; e += CB_T) {
+    const int i = e % k, j = e / k;
+    const int bi = i >> 5, bj = j >> 5;
+    const double v = i >= j ? Xr[cb_idx(bi, bj) + (j & 31) * CB_LD + (i & 31)] : 0.0;
+    Xg[(size_t)j * k + i] = v;
+    xs = fma(v, v, xs);
+  }
+  const double xn2 = cb_block_sum(xs, red);
   // mu_min(M) >= 1 / ||X||_F^2 must clear the reference's cutoff k eps mu_max (<= ||M||_F)
   const bool cert = (1.0 / xn2) > 4.0 * (double)k * 2.220446049250313e-16 * mnorm;
   if (threadIdx.x == 0) *gate = cert ? 0 : 1;
@@ -1040,6 +1259,7 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
                                        (int)((size_t)PK_MAX * (PK_MAX | 1) * sizeof(double))));
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_tri, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)((size_t)PK_MAX * (PK_MAX | 1) * sizeof(double))));
+    OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CB_SMEM));
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_chol_reg<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)((size_t)2 * 64 * 64 * sizeof(double))));
     OFRR_CUDA_TRY(cudaFuncSetAttribute(k_pc_eigvec, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1053,6 +1273,12 @@ int pencil_eig(const double* B, const double* M, int k, double* values, double* 
     // register Cholesky + inverse + certificate; T on the multi-CTA GEMMs (the in-kernel
     // T = X sym(B) X^T measured 65 us against 28 us for the two launches)
     k_pc_chol_reg<8, 8><<<1, PT, (size_t)2 * k * k * sizeof(double), st>>>(M, k, X, gate, nullptr, nullptr);
+    OFRR_CHECK_LAUNCH();
+    k_pc_gemm<false, false, true><<<gg, 256, 0, st>>>(X, B, T1, k, gate);
+    k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);
+    OFRR_CHECK_LAUNCH();
+  } else if (k <= CB_KB * CB_N) {
+    k_pc_chol_blk<<<1, CB_T, CB_SMEM, st>>>(M, k, X, gate);
     OFRR_CHECK_LAUNCH();
     k_pc_gemm<false, false, true><<<gg, 256, 0, st>>>(X, B, T1, k, gate);
     k_pc_gemm<false, true, false><<<gg, 256, 0, st>>>(T1, X, T, k, gate);

@@ -319,7 +319,7 @@ class EigEngine:
         self.ops.convert(W, X8, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
         return X8
 
-    def power_from(self, W, eig, kp: int, st):
+    def power_from(self, W, eig, kp: int, st, made=None):
         """A-pass reuse (cfg.reuse_av): the restart block is Ut = U Y, so its MatVec is
         A Ut = (A U) Y = W Y with W the projection's block product (kept in its accumulation
         format): X = round(W Y) to the MatVec storage, inf-norm scaled (ofrr/driver.py:
@@ -327,10 +327,13 @@ class EigEngine:
         reference's A round(Ut) up to the rounding of Ut and the accumulation error of W."""
         import torch
         ops, comm = self.ops, self.comm
-        colmax = torch.zeros(kp, dtype=torch.float64, device=self.device)
         fp8 = self.mv.storage == FpFormat.FP8_E4M3
-        X = ops.reuse_power(W, eig.vectors, kp, eig.n_out, kp, FpFormat.F32 if fp8 else self.mv.storage, colmax,
-                            flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
+        if made is not None:                      # W Y and its column norms from K6f (project)
+            X, colmax = made
+        else:
+            colmax = torch.zeros(kp, dtype=torch.float64, device=self.device)
+            X = ops.reuse_power(W, eig.vectors, kp, eig.n_out, kp, FpFormat.F32 if fp8 else self.mv.storage, colmax,
+                                flags=st[S_MV_FLAGS:S_MV_FLAGS + 1])
         comm.all_reduce_max_(colmax)
         ops.scale_columns(X, colmax, self.mv.compute)
         if fp8:
@@ -397,6 +400,23 @@ class EigEngine:
         eig = ops.sym_eig(B, kp) if classical else ops.sym_def_gen_eig(B, M, kp)
         st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
         st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
+        if (not comm.distributed and hasattr(ops, "restart") and W2 is not None and W2.n == U.n
+                and (reuse or top_check is not None)):
+            # K6f: Ritz block, next power step and residual estimate in one pass over (U, W2)
+            import torch
+            mv8 = self.mv.storage == FpFormat.FP8_E4M3
+            colmax = torch.zeros(kp, dtype=torch.float64, device=self.device) if reuse else None
+            U64, Xn, Xw, est = ops.restart(
+                U, W2 if (reuse or top_check is not None) else None, eig.vectors, kp, eig.n_out, kp, want64=want64,
+                xu_fmt=self.mv.storage, flags_u=st[S_RESTART_FLAGS:S_RESTART_FLAGS + 1],
+                xw_fmt=(FpFormat.F32 if mv8 else self.mv.storage) if reuse else None, colmax=colmax,
+                flags_w=st[S_MV_FLAGS:S_MV_FLAGS + 1], vals=eig.values if top_check is not None else None,
+                t=min(top_check, kp) if top_check is not None else 0, mode=0)
+            Xp = self.power_from(W2, eig, kp, st, made=(Xw, colmax)) if reuse else None
+            self._join(side)
+            if reuse:
+                return eig, U64, Xn, est, Xp
+            return eig, U64, Xn, est
         U64, Xn = ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=want64, x_fmt=self.mv.storage,
                            flags=st[S_RESTART_FLAGS:S_RESTART_FLAGS + 1])
         est = None

@@ -565,6 +565,34 @@ def reuse_power(W: DevBlock, Y: torch.Tensor, ldy: int, r_dev: Optional[torch.Te
     return X
 
 
+def restart(U: DevBlock, W: Optional[DevBlock], Y: torch.Tensor, ldy: int, r_dev: Optional[torch.Tensor], r_max: int,
+            want64: bool = False, xu_fmt: Optional[FpFormat] = None, flags_u: Optional[torch.Tensor] = None,
+            xw_fmt: Optional[FpFormat] = None, colmax: Optional[torch.Tensor] = None,
+            flags_w: Optional[torch.Tensor] = None, vals: Optional[torch.Tensor] = None, t: int = 0, mode: int = 0):
+    """K6f: the restart step in one pass over (U, W) -- ritz (U64 = U Y, Xu = round(U Y)),
+    reuse_power (Xw = round(W Y) + colmax, zeroed by the caller) and residual_estimate
+    (columns < t) fused.  Returns (U64, Xu, Xw, est); absent outputs are None."""
+    L = _lib.load()
+    dev = U.device
+    t = min(int(t), r_max) if (W is not None and vals is not None) else 0
+    U64 = new_block(U.n, r_max, FpFormat.F64, dev) if want64 else None
+    Xu = new_block(U.n, r_max, xu_fmt, dev) if xu_fmt is not None else None
+    Xw = new_block(U.n, r_max, xw_fmt, dev) if (xw_fmt is not None and W is not None) else None
+    est = torch.zeros(max(t, 1), dtype=torch.float64, device=dev) if t > 0 else None
+    ws = _ws(L.ofrr_restart_workspace(U.n, t), dev) if t > 0 else None
+    _lib.check(L.ofrr_restart(U.ptr, U.ld, int(U.fmt), W.ptr if W is not None else None, W.ld if W is not None else 0,
+                              int(W.fmt) if W is not None else 0, U.n, U.k, Y.data_ptr(), ldy, _p(r_dev), r_max,
+                              _p(Xu.t) if Xu else None, Xu.ld if Xu else 0, int(xu_fmt) if Xu else 0, _p(flags_u),
+                              _p(U64.t) if U64 else None, U64.ld if U64 else 0,
+                              _p(Xw.t) if Xw else None, Xw.ld if Xw else 0, int(xw_fmt) if Xw else 0, _p(flags_w),
+                              _p(colmax) if Xw is not None else None,
+                              vals.data_ptr() if t > 0 else None, t, est.data_ptr() if t > 0 else None, int(mode),
+                              ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
+                              _stream()), "restart")
+    _count(2 if t > 0 else 1)
+    return U64, Xu, Xw, est
+
+
 def residual_estimate(U: DevBlock, W: DevBlock, Y: torch.Tensor, ldy: int, vals: torch.Tensor,
                       r_dev: Optional[torch.Tensor], r_max: int, mode: int = 0) -> torch.Tensor:
     """K7e: ||(W - lambda_j U) y_j|| / |lambda_j| (mode 0) or raw sums of squares (mode 2)."""

@@ -13,7 +13,7 @@ for _ in range(2):
     ops.sym_def_gen_eig(B, M, k)
 torch.cuda.synchronize()
 L = _lib.load()
-out = (ctypes.c_longlong * 16)()
+out = (ctypes.c_longlong * 24)()
 L.ofrr_debug_k5_profile.argtypes = [ctypes.c_void_p]
 L.ofrr_debug_k5_profile(ctypes.addressof(out))
 t = list(out)

@@ -31,7 +31,7 @@ import ctypes  # noqa: E402
 from paper_2505_00281_b200 import _lib  # noqa: E402
 if os.environ.get("OFRR_K5_LEGACY") != "1":
     L = _lib.load()
-    out = (ctypes.c_ulonglong * 16)()
+    out = (ctypes.c_ulonglong * 24)()
     L.ofrr_debug_pencil_profile.argtypes = [ctypes.c_void_p]
     for k in (64, 128):
         rng = np.random.default_rng(k)

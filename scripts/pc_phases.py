@@ -26,7 +26,7 @@ for k in [int(a) for a in sys.argv[1:]] or [64, 128]:
         ops.sym_def_gen_eig(B, M, k)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / 20
-    out = (ctypes.c_ulonglong * 16)()
+    out = (ctypes.c_ulonglong * 24)()
     L.ofrr_debug_pencil_profile(ctypes.addressof(out))
     t = list(out)
     print(f"k={k}: pencil solve wall {wall * 1e6:.1f} us")

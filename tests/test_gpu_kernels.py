@@ -350,6 +350,53 @@ def test_residual_estimate_vs_numpy(ofrr_gpu, oracle, n, k, r_max, rv, ufmt, wfm
     assert not got[rv:].any()
 
 
+@pytest.mark.parametrize("n,k,r_max,rv,t,ufmt,wfmt,xfmt", [(3001, 40, 40, 30, 24, BF16, F32, BF16),
+                                                            (65536, 128, 128, 128, 64, F32, F32, F32),
+                                                            (1000, 70, 65, 41, 65, F64, F64, F64),
+                                                            (33, 5, 3, 2, 1, F16, F32, F16),
+                                                            (777, 96, 96, 80, 0, F32, F32, F32)])
+def test_restart_fused_vs_separate(ofrr_gpu, oracle, n, k, r_max, rv, t, ufmt, wfmt, xfmt):
+    """K6f: Ritz block (fp64 and rounded), next power step W Y (rounded, column maxima,
+    non-finite flags) bit for bit those of K6 (ritz / reuse_power); the residual estimate
+    of the first t columns vs K7e and numpy."""
+    import torch
+    from paper_2505_00281_b200 import ops
+    p, o = ofrr_gpu, oracle
+    rng = np.random.default_rng(n + k + t)
+    u = o.round_to(rng.standard_normal((n, k)), ufmt)
+    w = rng.standard_normal((n, k)) * 3.0
+    w = w if wfmt == F64 else o.round_to(w, wfmt)
+    y = rng.standard_normal((k, k))
+    lam = rng.uniform(0.5, 2.0, k) * rng.choice([-1, 1], k)
+    U, W = _blk(p, u, ufmt), _blk(p, w, wfmt)
+    Y = torch.tensor(np.ascontiguousarray(y.T), device="cuda")
+    r_dev = torch.tensor([rv], dtype=torch.int32, device="cuda")
+    vals = torch.tensor(lam, device="cuda")
+    fl = torch.zeros(2, dtype=torch.int32, device="cuda")
+    cm = torch.zeros(r_max, dtype=torch.float64, device="cuda")
+    U64, Xu, Xw, est = ops.restart(U, W, Y, k, r_dev, r_max, want64=True, xu_fmt=p.FpFormat(xfmt), flags_u=fl[0:1],
+                                   xw_fmt=p.FpFormat(xfmt), colmax=cm, flags_w=fl[1:2], vals=vals, t=t)
+    R64, RX = ops.ritz(U, Y, k, r_dev, r_max, 1.0, want64=True, x_fmt=p.FpFormat(xfmt))
+    cm2 = torch.zeros(r_max, dtype=torch.float64, device="cuda")
+    RW = ops.reuse_power(W, Y, k, r_dev, r_max, p.FpFormat(xfmt), cm2)
+    assert torch.equal(U64.t[:r_max, :n], R64.t[:r_max, :n])
+    assert torch.equal(Xu.t[:r_max, :n], RX.t[:r_max, :n])
+    assert torch.equal(Xw.t[:r_max, :n], RW.t[:r_max, :n])
+    assert torch.equal(cm, cm2)
+    assert not fl.any()
+    if t == 0:
+        assert est is None
+        return
+    ref_dev = ops.residual_estimate(U, W, Y, k, vals, r_dev, min(t, r_max)).cpu().numpy()
+    got = est.cpu().numpy()
+    tv = min(t, rv)
+    d = w @ y[:, :tv] - (u @ y[:, :tv]) * lam[None, :tv]
+    ref = np.sqrt(np.sum(d * d, axis=0)) / np.abs(lam[:tv])
+    np.testing.assert_allclose(got[:tv], ref, rtol=1e-11)
+    np.testing.assert_allclose(got[:tv], ref_dev[:tv], rtol=1e-13)
+    assert not got[tv:].any()
+
+
 @pytest.mark.parametrize("fmt,rows,cols,r,rv", [(BF16, 300, 20000, 64, 64), (BF16, 1000, 1000, 100, 90),
                                                 (F16, 257, 3001, 7, 7), (FP8, 640, 5000, 33, 20),
                                                 (BF16, 129, 16384, 32, 32)])
