@@ -6,8 +6,10 @@ Default workload (every N): BASELINE configs[2] / SURVEY.md 8 "C3", the north-st
 synthetic dense symmetric 65536 x 65536 (bf16 operator, 8 GiB, HBM resident), geometric
 spectrum (rho = 0.1^(1/(k-top+1))), top-64 eigenpairs, k = 128, hess-l + ofrr, stopped when
 the FP64 relative residuals of the leading 64 pairs are below 1e-8.  The basis runs a
-three-rung precision ladder: fp32-accurate products on the bf16 tensor cores (K1, 3 bf16
-slices of the block) until the residual estimate reaches 1e-4, then an fp64 basis with
+three-rung precision ladder: an fp32 basis whose products take 2 bf16 slices of the block on
+the bf16 tensor cores (K1: 16-bit block digits, fp32 sums -- at K = 65536 the fp32 sums'
+own noise is of the same order, so the third slice buys no earlier switch) until the
+residual estimate reaches 1e-4, then an fp64 basis with
 ~30-bit int8 Ozaki products (K7z, 4 levels) until 1e-6, then FP64-accurate K7z products (6
 levels), whose W = A U also yields the FP64 residual report; A-pass reuse
 (IterConfig.reuse_av) makes every outer iteration after the first one A pass.  One step = one complete solve from
@@ -39,7 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SEED = 20240901
-DEFAULT_CONFIG = "c3-ladder3"
+DEFAULT_CONFIG = "c3-ladder3l"
 CONFIGS = {
     "c2": dict(n=16384, top=32, k=64, fmt="BF16", tol=1e-2, policy="full-f32",
                name="synthetic dense symmetric 16384x16384 (bf16 operator), geometric spectrum, top-32, k=64, "
@@ -80,6 +82,13 @@ CONFIGS = {
                             "(bf16 operator), geometric spectrum, top-64, k=128, to FP64 residual 1e-8 by a "
                             "three-rung basis ladder: fp32 (bf16 tensor cores) -> fp64 with ~30-bit int8 Ozaki "
                             "products -> fp64 with FP64-accurate products, A-pass reuse"),
+    "c3-ladder3l": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
+                        ladder=("full-f32-lite", "full-f64-lite"), switch=(1e-4, 1e-6), reuse=True,
+                        name="BASELINE configs[2] (north-star target): synthetic dense symmetric 65536x65536 "
+                             "(bf16 operator), geometric spectrum, top-64, k=128, to FP64 residual 1e-8 by a "
+                             "three-rung basis ladder: fp32 basis with 2-slice bf16 products (bf16 tensor cores) "
+                             "-> fp64 with ~30-bit int8 Ozaki products -> fp64 with FP64-accurate products, "
+                             "A-pass reuse"),
     "c3-ladder4": dict(n=65536, top=64, k=128, fmt="BF16", tol=1e-8, policy="full-f64",
                        ladder=("full-f32-lite", "full-f32", "full-f64-lite"), switch=(1e-2, 1e-4, 1e-6), reuse=True,
                        name="BASELINE configs[2] (north-star target): synthetic dense symmetric 65536x65536 "
@@ -208,7 +217,7 @@ def ref_pass_seconds(gemm, oracle, n: int, k: int, rung: str, rows: int, n_rows:
     as apply_dense hands them to the kernel, ofrr/matrix.py:242-254), scaled to n rows."""
     c, acc, out = _POL_CODES.get(rung, (1, 1, 1))
     rng = np.random.default_rng(SEED)
-    x = oracle.round_to(rng.random((n, k)), oracle.F64 if rung == "F64" else oracle.F32)
+    x = oracle.round_to(rng.random((n, k)), oracle.F64 if rung in ("F64", "F64L") else oracle.F32)
     a = np.asfortranarray(oracle.round_to(rng.standard_normal((rows, n)) * 1e-3, oracle.BF16))
     t0 = time.perf_counter()
     gemm(a, x, c, acc, out)
@@ -370,7 +379,9 @@ _KNOWN = [
     ("k_oz_rowscale", "K7z row scales of A"),
     ("k_oz_slices_v", "K7z digits of the block"),
     ("k_gram", "K4 Grams"),
+    ("k_restart_dmma", "K6f restart step: Ritz block + next power step + residual estimate (DMMA)"),
     ("k_ritz", "K6 Ritz recovery / reuse power step"),
+    ("k_oz_tailmul", "K7z exact fp64 tails of A"),
     ("k_pc_", "K5 pencil pipeline"),
     ("k_small_eig", "K5 general pencil kernel"),
     ("k_resid_est", "K7e residual estimate"),
@@ -422,6 +433,8 @@ def _kernel_work(name: str, cfg, rows: int):
         return 2 * n * k * s_blk, None, None
     if "k_gram_partial" in name:
         return n * k * 2 * s_blk, 4.0 * n * k * k, "fp64"
+    if "k_restart_dmma" in name:                 # U Y and W Y: read U, W; write both rounded blocks
+        return n * k * 4 * s_blk, 4.0 * n * k * k, "fp64"
     if "k_ritz" in name:
         return n * k * (s_blk + 8), 2.0 * n * k * k, "fp64"
     if "k_resid_est" in name:

@@ -107,7 +107,8 @@ def test_c2_bench_answer_independent_fp64(ofrr_gpu):
 @pytest.mark.gpu
 def test_c3_headline_answer_independent_fp64(ofrr_gpu):
     p = ofrr_gpu
-    cfg, A, f, lam, rs, st = _solve(p, "c3-ladder-reuse")
+    import bench
+    cfg, A, f, lam, rs, st = _solve(p, bench.DEFAULT_CONFIG)          # the headline as benched
     top, tol, n = cfg["top"], cfg["tol"], cfg["n"]
     assert st.converged
     op = A.device_operator(p.FpFormat.BF16)
