@@ -400,7 +400,7 @@ class EigEngine:
         eig = ops.sym_eig(B, kp) if classical else ops.sym_def_gen_eig(B, M, kp)
         st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
         st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
-        if (not comm.distributed and hasattr(ops, "restart") and W2 is not None and W2.n == U.n
+        if (not comm.distributed and hasattr(ops, "restart") and W2 is not None and W2.n == U.n and kp <= 256
                 and (reuse or top_check is not None)):
             # K6f: Ritz block, next power step and residual estimate in one pass over (U, W2)
             import torch
