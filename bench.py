@@ -631,7 +631,9 @@ def _run_ours(args, cfg, p, _lib, ops, torch, dist, ctypes, world, rank, local, 
     log = ops.GEMM_LOG
     ops.GEMM_LOG = None
     stamps = {}
-    for nm, fn in (("k1", L.ofrr_prof_k1_read), ("oz", L.ofrr_prof_oz_read)):
+    for nm, fn in (("k1", L.ofrr_prof_k1_read), ("oz", L.ofrr_prof_oz_read),
+                   ("oz_fp64", lambda a, b: L.ofrr_prof_oz_read_tier(1, a, b)),
+                   ("oz_lite", lambda a, b: L.ofrr_prof_oz_read_tier(2, a, b))):
         sm, cnt = ctypes.c_double(0.0), ctypes.c_longlong(0)
         fn(ctypes.byref(sm), ctypes.byref(cnt))
         stamps[nm] = (float(sm.value), int(cnt.value))
@@ -726,15 +728,19 @@ def _roofline(table, stamps, log, cfg, rows, ms_step, hbm, bf16_peak, peak_kind,
     and its average launch duration from its own in-kernel globaltimer stamps over the timed
     region (K1 / K7z), else from the CUPTI table."""
     n, k = cfg["n"], cfg["k"]
-    dom = table[0]["kernel"] if table else ("k_ozk_gemm" if cfg["policy"] == "full-f64" else "k_gemm_av_tc")
+    dom = table[0]["kernel"] if table else ("k_ozk_ts<3, 64, 6>" if cfg["policy"] == "full-f64" else "k_gemm_av_tc")
     if "k_ozk_gemm" in dom or "k_ozk_ts" in dom:
-        sm, cnt = stamps["oz"]
+        # the in-kernel stamps of this kernel's accuracy tier only (the lite and FP64-accurate
+        # products are different instances with different work per launch)
+        _, _, nl = _ozk_args(dom)
+        sm, cnt = stamps["oz_lite" if nl == 4 else "oz_fp64"]
         avg_ms = sm / cnt if cnt else float("nan")
         nb, ops_, _ = _kernel_work(dom, cfg, rows)
         tops = ops_ / (avg_ms * 1e-3) / 1e12
         peak = 2.0 * bf16_peak
         gbs = nb / (avg_ms * 1e-3) / 1e9
-        out = {"kernel": f"{dom[:40]} (K7z: FP64-accurate A.X on the int8 tensor cores, {_oz_products(dom)} "
+        tier = "~30-bit lite" if nl == 4 else "FP64-accurate"
+        out = {"kernel": f"{dom[:40]} (K7z: {tier} A.X on the int8 tensor cores, {_oz_products(dom)} "
                          "digit products)",
                "bound": "tensor", "achieved": _num(tops), "peak": peak, "unit": "TOP/s (int8)",
                "frac": _num(tops / peak), "peak_kind": f"derived: 2 x {peak_kind} bf16 {bf16_peak} "

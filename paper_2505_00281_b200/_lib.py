@@ -56,6 +56,7 @@ _SIGS = {
     "ofrr_prof_k1_read": ([c_vp, c_vp], c_int),
     "ofrr_prof_oz_stamp": ([c_int], c_int),
     "ofrr_prof_oz_read": ([c_vp, c_vp], c_int),
+    "ofrr_prof_oz_read_tier": ([c_int, c_vp, c_vp], c_int),
     "ofrr_loop_ctl_bytes": ([], c_sz),
     "ofrr_loop_build": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_int, c_int, c_int,
                          c_dbl, c_vp], c_int),

@@ -474,6 +474,9 @@ extern "C" int ofrr_prof_gemm_collect_group(int group) { return ofrr::prof_colle
 namespace ofrr { int stamp_enable(int on); int stamp_read(double* sum_ms, long long* count); }
 extern "C" int ofrr_prof_k1_stamp(int on) { return ofrr::stamp_enable(on); }
 extern "C" int ofrr_prof_k1_read(double* sum_ms, long long* count) { return ofrr::stamp_read(sum_ms, count); }
-namespace ofrr { int oz_stamp_enable(int on); int oz_stamp_read(double* sum_ms, long long* count); }
+namespace ofrr { int oz_stamp_enable(int on); int oz_stamp_read(double* sum_ms, long long* count, int tier); }
 extern "C" int ofrr_prof_oz_stamp(int on) { return ofrr::oz_stamp_enable(on); }
-extern "C" int ofrr_prof_oz_read(double* sum_ms, long long* count) { return ofrr::oz_stamp_read(sum_ms, count); }
+extern "C" int ofrr_prof_oz_read(double* sum_ms, long long* count) { return ofrr::oz_stamp_read(sum_ms, count, 0); }
+extern "C" int ofrr_prof_oz_read_tier(int tier, double* sum_ms, long long* count) {
+  return ofrr::oz_stamp_read(sum_ms, count, tier);
+}

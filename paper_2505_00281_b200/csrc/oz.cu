@@ -34,7 +34,9 @@ namespace ofrr {
 // in-kernel timing of k_ozk_gemm for the bench roofline (the K1 scheme, gemm_tc.cu): every CTA
 // stamps its entry (min) and exit (max) in globaltimer ns; the k_oz_resid launch that follows
 // adds the interval to a running sum and re-arms the stamps
-__device__ unsigned long long g_oz_stamp[4] = {~0ull, 0ull, 0ull, 0ull};   // min start, max end, sum, count
+// min start, max end, then (sum, count) per tier: [2..3] every product, [4..5] FP64-accurate
+// (6 levels), [6..7] lite (4 levels) -- the k_oz_resid launch passes stamp = 1 + (lite ? 1 : 0)
+__device__ unsigned long long g_oz_stamp[8] = {~0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
 static bool g_oz_stamp_on = false;
 __device__ __forceinline__ unsigned long long oz_gtimer_ns() {
   unsigned long long t;
@@ -44,16 +46,17 @@ __device__ __forceinline__ unsigned long long oz_gtimer_ns() {
 int oz_stamp_enable(int on) {
   g_oz_stamp_on = on != 0;
   if (on) {
-    const unsigned long long z[4] = {~0ull, 0ull, 0ull, 0ull};
+    const unsigned long long z[8] = {~0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
     if (cudaMemcpyToSymbol(g_oz_stamp, z, sizeof(z)) != cudaSuccess) return OFRR_ERR_CUDA;
   }
   return OFRR_OK;
 }
-int oz_stamp_read(double* sum_ms, long long* count) {
-  unsigned long long v[4];
+int oz_stamp_read(double* sum_ms, long long* count, int tier) {   // tier 0 all, 1 FP64-accurate, 2 lite
+  unsigned long long v[8];
+  if (tier < 0 || tier > 2) return OFRR_ERR_INVALID;
   if (cudaMemcpyFromSymbol(v, g_oz_stamp, sizeof(v)) != cudaSuccess) return OFRR_ERR_CUDA;
-  *sum_ms = (double)v[2] * 1e-6;
-  *count = (long long)v[3];
+  *sum_ms = (double)v[2 + 2 * tier] * 1e-6;
+  *count = (long long)v[3 + 2 * tier];
   return OFRR_OK;
 }
 
@@ -1416,7 +1419,12 @@ __global__ void __launch_bounds__(OZ_TM)
   __shared__ double red[4][16];
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
     const unsigned long long t0 = g_oz_stamp[0], t1 = g_oz_stamp[1];
-    if (t1 > t0) { g_oz_stamp[2] += t1 - t0; g_oz_stamp[3] += 1; }
+    if (t1 > t0) {
+      g_oz_stamp[2] += t1 - t0;
+      g_oz_stamp[3] += 1;
+      g_oz_stamp[2 + 2 * stamp] += t1 - t0;
+      g_oz_stamp[3 + 2 * stamp] += 1;
+    }
     g_oz_stamp[0] = ~0ull;
     g_oz_stamp[1] = 0ull;
   }
@@ -1891,7 +1899,8 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     OFRR_CHECK_LAUNCH();
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
-                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0, full, Wt);
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
+                                           g_oz_stamp_on ? (levels == OZ_D ? 1 : 2) : 0, full, Wt);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;
