@@ -61,6 +61,35 @@ __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* 
   }
 }
 
+// The same argmax on integer keys with warp reductions (redux.sync): |v| >= 0 orders like its
+// bit pattern, so the maximum is taken on the high then the low word and the lowest row among
+// the maxima on the row.  idx < 0 / v < 0: no candidate.  Every thread gets the result.
+__device__ __forceinline__ void block_argmax_redux(double& v, long long& idx, unsigned long long* sk2,
+                                                   unsigned* sr2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool has = idx >= 0 && v >= 0.0;
+  const unsigned long long key = has ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned row = has ? (unsigned)idx : 0xFFFFFFFFu;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const unsigned mrow = __reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? row : 0xFFFFFFFFu);
+  if (lane == 0) {
+    sk2[warp] = ((unsigned long long)mhi << 32) | mlo;
+    sr2[warp] = mrow;
+  }
+  __syncthreads();
+  unsigned long long bk = sk2[0];
+  unsigned br = sr2[0];
+  for (int w = 1; w < HT / 32; ++w) {
+    const unsigned long long k2 = sk2[w];
+    const unsigned r2 = sr2[w];
+    if (k2 > bk || (k2 == bk && r2 < br)) { bk = k2; br = r2; }
+  }
+  idx = br == 0xFFFFFFFFu ? -1 : (long long)br;
+  v = idx >= 0 ? __longlong_as_double((long long)bk) : -1.0;
+}
+
 // Packed candidate key for storage formats narrower than f64: |x| is exact in f32 and its
 // bit pattern orders like the value (NaN above inf, as np.argmax picks NaN); the low word
 // ~row makes ties resolve to the lowest row.  0 = no candidate.
@@ -69,10 +98,11 @@ __device__ __forceinline__ unsigned long long cand_key(float absval, long long r
 }
 __device__ __forceinline__ unsigned long long block_max_key(unsigned long long key, unsigned long long* sk) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
-    key = ok > key ? ok : key;
+  {   // warp max of a 64-bit key: high word, then the low word among the high maxima (redux.sync)
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    key = ((unsigned long long)mhi << 32) | mlo;
   }
   if (lane == 0) sk[warp] = key;
   __syncthreads();
@@ -277,6 +307,7 @@ __global__ void __launch_bounds__(HT)
   // F64 storage: (value, row) per CTA, reduced by every CTA after the barrier.
   constexpr bool KEYED = !std::is_same<T, double>::value;
   __shared__ unsigned long long sk[HT / 32];
+  __shared__ unsigned sr2[HT / 32];
   __shared__ float s_v0, s_v1;                               // candidate / pivot: value, next column
   __shared__ double s_d0, s_d1;                              // the same, F64 storage
   // this thread's candidate over its rows i (free rows only) of column jn
@@ -306,7 +337,7 @@ __global__ void __launch_bounds__(HT)
       key = block_max_key(key, sk);
       idx = key ? (long long)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull)) : -1;
     } else {
-      block_argmax(v, idx, sv, si);
+      block_argmax_redux(v, idx, sk, sr2);
     }
     if (idx >= 0) {
       const CV vr = pending ? ld_c<C>(col(jp)[idx]) : CV(0);
@@ -403,6 +434,10 @@ __global__ void __launch_bounds__(HT)
       for (int v = 0; v < CB; ++v) yn[v] = c0 + v < k ? b[(int64_t)v * ldw] : T();
     };
     if (threadIdx.x < units) load_unit(threadIdx.x);
+    // the panel columns' offsets in the panel cache, once per panel end (not per unit)
+    int moff[QMAX];
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) moff[q] = (pwc && q < npl) ? (s_pl[q] - cp0) * (int)nr : 0;
     for (unsigned u = threadIdx.x; u < units; u += HT) {
       int64_t i;
       int c0;
@@ -412,8 +447,10 @@ __global__ void __launch_bounds__(HT)
       for (int v = 0; v < CB; ++v) y[v] = yn[v];
       if (u + HT < units) load_unit(u + HT);
       CV mult[QMAX];
+      const int li = (int)(i - r0);
 #pragma unroll
-      for (int q = 0; q < QMAX; ++q) mult[q] = q < npl ? ld_c<C>(col(s_pl[q])[i]) : CV(0);
+      for (int q = 0; q < QMAX; ++q)
+        mult[q] = q < npl ? ld_c<C>(pwc ? Pw[moff[q] + li] : col(s_pl[q])[i]) : CV(0);
       T* base = Xw + (int64_t)c0 * ldw + i;
 #pragma unroll
       for (int q = 0; q < QMAX; ++q) {
@@ -494,7 +531,7 @@ __global__ void __launch_bounds__(HT)
         d1 = b.y;
       }
       const long long mine = bi;
-      block_argmax(bv, bi, sv, si);
+      block_argmax_redux(bv, bi, sk, sr2);
       if (threadIdx.x < G && bi >= 0 && mine == bi) {
         s_owner = threadIdx.x;
         s_d0 = d0;
