@@ -384,25 +384,36 @@ __global__ void __launch_bounds__(HT)
   // later row at once (independent chains per column).
   auto compute_pr = [&](int pe, int npl) {
     if (npl == 0 || pe >= k) return;
-    constexpr int QMAX = 32;
     CV* Mq = reinterpret_cast<CV*>(PR + (size_t)pb * k);     // [npl][npl]: M[q][q'] (q' < q)
     for (int e = threadIdx.x; e < npl * npl; e += HT) {
       const int q = e / npl, q2 = e - q * npl;
       Mq[e] = q2 < q ? ld_c<C>(ldcg_el(&Q[(int64_t)s_pnk[q2] * ldq + s_prow[q]])) : CV(0);
     }
     __syncthreads();
+    // rolled loops (a fully unrolled 32 x 32 wavefront runs once per panel end and is
+    // instruction-fetch bound); each thread owns columns cc and keeps them in PR itself
     for (int cc = pe + threadIdx.x; cc < k; cc += HT) {
-      T y[QMAX];
+      {                                                        // all the loads in flight at once
+        T t32[32];
 #pragma unroll
-      for (int q = 0; q < QMAX; ++q) y[q] = q < npl ? ldcg_el(&Xw[(int64_t)cc * ldw + s_prow[q]]) : T();
+        for (int u = 0; u < 32; ++u) t32[u] = u < npl ? ldcg_el(&Xw[(int64_t)cc * ldw + s_prow[u]]) : T();
 #pragma unroll
-      for (int q2 = 0; q2 < QMAX; ++q2) {
-        if (q2 < npl) {
-          const CV a = ld_c<C>(y[q2]);
-          PR[(size_t)q2 * k + cc] = a;
+        for (int u = 0; u < 32; ++u)
+          if (u < npl) PR[(size_t)u * k + cc] = ld_c<C>(t32[u]);
+      }
+      for (int q2 = 0; q2 + 1 < npl; ++q2) {
+        const CV a = PR[(size_t)q2 * k + cc];
+        for (int q0 = q2 + 1; q0 < npl; q0 += 4) {            // 4 independent rows: loads first
+          CV y4[4], m4[4];
 #pragma unroll
-          for (int q = q2 + 1; q < QMAX; ++q)
-            if (q < npl) y[q] = st_s<T>(csub<C>(ld_c<C>(y[q]), cmul<C>(a, Mq[q * npl + q2])));
+          for (int u = 0; u < 4; ++u) {
+            const int q = min(q0 + u, npl - 1);
+            y4[u] = PR[(size_t)q * k + cc];
+            m4[u] = Mq[q * npl + q2];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (q0 + u < npl) PR[(size_t)(q0 + u) * k + cc] = ld_c<C>(st_s<T>(csub<C>(y4[u], cmul<C>(a, m4[u]))));
         }
       }
     }
