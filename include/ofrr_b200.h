@@ -150,6 +150,15 @@ int ofrr_loop_build(void* first_graph, void* steady_graph, void* report_graph, c
                     const double* est_first, const int* st_steady, const double* est_steady,
                     const double* res_report, const void* copy_src, void* copy_dst, size_t copy_bytes,
                     void* ctl, int m, int top, int k, double tol, void** exec_out);
+/* A precision-ladder rung's loop (driver.py EigEngine.run with stop_estimate): the first and
+ * steady iteration graphs, no report; the rung stops when its worst leading estimate falls
+ * below `sw` or stops halving -> state OFRR_LOOP_RUNG_DONE, the restart block and the next
+ * iterate are the last iteration's outputs. */
+#define OFRR_LOOP_RUNG_DONE 4
+int ofrr_loop_build_rung(void* first_graph, void* steady_graph, const int* st_first,
+                         const double* est_first, const int* st_steady, const double* est_steady,
+                         const void* copy_src, void* copy_dst, size_t copy_bytes, void* ctl, int m,
+                         int top, int k, double sw, void** exec_out);
 int ofrr_loop_launch(void* exec, void* stream);
 int ofrr_loop_destroy(void* exec);
 

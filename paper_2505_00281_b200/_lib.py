@@ -60,6 +60,8 @@ _SIGS = {
     "ofrr_loop_ctl_bytes": ([], c_sz),
     "ofrr_loop_build": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_int, c_int, c_int,
                          c_dbl, c_vp], c_int),
+    "ofrr_loop_build_rung": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_int, c_int, c_int,
+                              c_dbl, c_vp], c_int),
     "ofrr_loop_launch": ([c_vp, c_vp], c_int),
     "ofrr_loop_destroy": ([c_vp], c_int),
     "ofrr_scale_columns": ([c_vp, c_i64, c_int, c_i64, c_int, c_int, c_vp, c_vp], c_int),

@@ -515,6 +515,12 @@ class EigEngine:
                 rs = self._device_loop(X, top)
             if rs is not None:
                 return rs
+        if (use_graph and DEVICE_LOOP and check and stop_estimate is not None and (fresh or X.k == cfg.k)
+                and cfg.m >= 2 and not self.comm.distributed):
+            with _ph("device_rung"):
+                Xr = self._device_rung(X, top, stop_estimate)
+            if Xr is not None:
+                return Xr
         if X is None:
             X = self.start_block()
         for it in range(cfg.m):
@@ -705,6 +711,95 @@ class EigEngine:
         _loop_debug(f"host us: keys {1e6 * (t1 - t0):.0f} copy {1e6 * (t2 - t1):.0f} launch {1e6 * (t3 - t2):.0f} "
                     f"sync {1e6 * (t4 - t3):.0f} post {1e6 * (t5 - t4):.0f}")
         return out
+
+    def _device_rung(self, X, top: int, sw: float):
+        """A ladder rung's outer loop as one CUDA graph (csrc/loop.cu loop_build_rung): the
+        first and steady iteration graphs, the rung's stop test on the device (the host loop's
+        `rung_done`, same thresholds), one launch and one read.  Returns the restart block
+        (and sets self.handover) when the rung finished; None when the graphs are missing or
+        the device stopped for a case the host loop handles -- the caller then runs the host
+        loop from the same start block (the graphs' input copies leave X untouched)."""
+        import ctypes
+        import torch
+        from . import _lib
+        cfg = self.cfg
+        L = _lib.load()
+        self._refresh_now = True
+        kf = self._graph_key(True, top, not self.stepped)
+        self._refresh_now = False
+        ks = self._graph_key(True, top, False)
+        gf, gs = _GRAPHS.get(kf), _GRAPHS.get(ks)
+        if gf is None or gs is None or gf.outs.get("est") is None or gs.outs.get("est") is None:
+            return None
+        _GRAPHS.move_to_end(kf)
+        _GRAPHS.move_to_end(ks)
+        lk = ("rung", cfg.m, top, float(sw))
+        loops = gs.__dict__.setdefault("loops", {})
+        ent = loops.get(lk)
+        if ent is not None and ent[0] is not gf:
+            loops.pop(lk)
+            ent = None
+        lp = ent[1] if ent is not None else None
+        if ent is None:
+            ctl = torch.zeros(int(L.ofrr_loop_ctl_bytes()), dtype=torch.uint8, device=self.device)
+            if gf is gs:
+                src = dst = None
+                nbytes = 0
+            else:
+                src_blk = gf.outs["Xnext"] if cfg.reuse_av else gf.Xs
+                src, dst = src_blk.t.data_ptr(), gs.Xs.t.data_ptr()
+                nbytes = gs.Xs.t.numel() * gs.Xs.t.element_size()
+                if src_blk.t.numel() != gs.Xs.t.numel():
+                    return None
+            ex = ctypes.c_void_p()
+            rc = L.ofrr_loop_build_rung(gf.graph.raw_cuda_graph(), gs.graph.raw_cuda_graph(), gf.outs["st"].data_ptr(),
+                                        gf.outs["est"].data_ptr(), gs.outs["st"].data_ptr(), gs.outs["est"].data_ptr(),
+                                        src, dst, nbytes, ctl.data_ptr(), cfg.m, top, cfg.k, float(sw),
+                                        ctypes.byref(ex))
+            if rc != 0:
+                _loop_debug("rung build failed", _lib.last_error())
+                loops[lk] = (gf, None)
+                return None
+            lp = (_LoopExec(ex.value), ctl)
+            loops[lk] = (gf, lp)
+        elif lp is None:
+            return None
+        ex, ctl = lp
+        if X is None and (gf.Xs.n, gf.Xs.k, FpFormat(gf.Xs.fmt)) == (self.n, cfg.k, FpFormat(self.mv.storage)):
+            self.start_block(out=gf.Xs)
+        elif X is None:
+            gf.Xs.t.copy_(self.start_block().t)
+        elif X.t.data_ptr() != gf.Xs.t.data_ptr():
+            gf.Xs.t.copy_(X.t)
+        _lib.check(L.ofrr_loop_launch(ex.handle, ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)),
+                   "loop_launch")
+        nb = ctl.numel()
+        stage = gs.__dict__.get("stage_rung")
+        if stage is None:
+            stage = gs.stage_rung = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        stage.copy_(ctl, non_blocking=True)
+        with _ph("rung_sync"):
+            torch.cuda.current_stream(self.device).synchronize()
+        head = stage[:16].view(torch.int32).numpy()
+        state, its = int(head[0]), int(head[1])
+        if state != 4:
+            _loop_debug("rung: device stopped for the host", state, its)
+            return None
+        hist = stage[24:nb].view(torch.float64).numpy()
+        est_h = hist[:hist.size // 2]
+        self.stats.iterations = its
+        self.stats.a_passes += gf.a_passes + (its - 1) * gs.a_passes
+        for i in range(min(its, est_h.size)):
+            self.stats.history.append((i + 1, float(est_h[i])))
+        gf.rec.replayed()
+        for _ in range(its - 1):
+            gs.rec.replayed()
+        self.ops._count(1 + its)                                 # init, decide per iteration
+        self.stats.device_loop = True
+        out = gf.outs if its == 1 else gs.outs
+        r = cfg.k                                                # the device stops for the host otherwise
+        self.handover = out["Xnext"].narrow(r) if cfg.reuse_av else None
+        return out["Xn"].narrow(r)
 
     def _final_report(self, out, U, eig, kp, r, vals, check, top) -> RitzSet:
         """Ritz vectors in fp64 and the FP64 residual report -- replayed as a CUDA graph when
