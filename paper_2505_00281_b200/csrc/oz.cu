@@ -1706,7 +1706,9 @@ static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r, int levels = OZ_D) {
   r = std::max(r, 1);
   // lite tier: 128-column passes on the shared-memory kernel (64-column passes with the digit
   // planes in TMEM read A twice: 5.2 vs 4.4 ms per A pass at C3)
-  p.bn = levels == OZ_D ? (r <= 32 ? 32 : 64) : (r <= 64 ? 64 : 128);
+  static int lite_bn = -1;                 // OFRR_OZK_LITE_BN=64: lite passes of 64 columns (comparison runs)
+  if (lite_bn < 0) { const char* e = getenv("OFRR_OZK_LITE_BN"); lite_bn = e ? atoi(e) : 128; }
+  p.bn = levels == OZ_D ? (r <= 32 ? 32 : 64) : (r <= 64 || lite_bn == 64 ? 64 : 128);
   p.npass = (r + p.bn - 1) / p.bn;
   p.npad = p.npass * p.bn;
   p.rows_pad = (rows + OZ_TM - 1) / OZ_TM * OZ_TM;

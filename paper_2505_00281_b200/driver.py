@@ -817,13 +817,23 @@ class EigEngine:
                 U64 = rg.U64
                 U64c = self.ops.DevBlock(U64.t.clone(), U64.n, r, U64.fmt)   # outlive the next replay
                 return RitzSet(np.array(vals[:r]), DenseMatrix.from_block(U64c), "eig", residuals=res)
-        U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
         W2 = out.get("W2")
         if self._w2_is_fp64(W2, U):
+            U64, res = self._report_from_w(U, W2, eig, kp, r)
             rs = RitzSet(np.array(vals[:r]), DenseMatrix.from_block(U64.narrow(r)), "eig")
-            res = self.residuals_from_w(U, W2, eig, r)
             return RitzSet(rs.values, rs.vectors, "eig", residuals=res.cpu().numpy()[:r])
+        U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
         return self.report(U64, eig, r, vals)
+
+    def _report_from_w(self, U, W2, eig, kp: int, r: int):
+        """fp64 Ritz vectors U Y and their FP64 residuals from an FP64-accurate W2 = A U: one
+        K6f pass (U64 + the residual sums) on one process, K6 + K7e otherwise."""
+        if not self.comm.distributed and hasattr(self.ops, "restart") and kp <= 256 and W2.n == U.n:
+            U64, _, _, res = self.ops.restart(U, W2, eig.vectors, kp, eig.n_out, kp, want64=True,
+                                             vals=eig.values, t=r, mode=0)
+            return U64, res
+        U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
+        return U64, self.residuals_from_w(U, W2, eig, r)
 
     def _w2_is_fp64(self, W2, U) -> bool:
         """W2 = A U is an FP64-accurate product (fp64 block, full-accuracy K7z or fp64 FMA)."""
@@ -852,11 +862,11 @@ class EigEngine:
         try:
             with rec:
                 with torch.cuda.graph(graph):
-                    U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
                     W2 = g.outs.get("W2")
                     if self._w2_is_fp64(W2, U):
-                        res = self.residuals_from_w(U, W2, eig, r)
+                        U64, res = self._report_from_w(U, W2, eig, kp, r)
                     else:
+                        U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
                         res = self.residuals(U64, eig.values, eig.n_out, r)
         except Exception:
             g.report = None
