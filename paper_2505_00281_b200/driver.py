@@ -136,7 +136,7 @@ _GRAPHS = OrderedDict()
 # stream.
 _SOLVE_LOCK = threading.RLock()
 DEVICE_LOOP = True      # the whole solve as one graph launch (csrc/loop.cu) once its graphs exist
-HANDOVER_STEPPED = False   # ladder: start the next rung from the previous rung's W Y (see _subspace_iter_eig)
+HANDOVER_STEPPED = __import__("os").environ.get("OFRR_HANDOVER_STEPPED") == "1"   # ladder: start every rung from the previous rung's W Y (experiments; see _subspace_iter_eig)
 _WARM = set()
 _NO_GRAPH = set()
 
