@@ -66,6 +66,7 @@ static constexpr int OZ_KB = 128;         // K per k-block (int8: one 128B swizz
 static constexpr int OZ_THREADS = 192;    // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
 static constexpr int OZ_MAXCHUNK = 128;   // k-blocks per accumulation chunk (16384 terms)
 static constexpr int OZ_BAD = INT_MIN;    // scale marker: the row / column has inf or NaN
+static constexpr int OZR_CG = 8;          // k_oz_resid: columns per CTA (8: ~60 registers, 2x the resident warps of 16)
 
 template <int BN>
 struct OzCfg {
@@ -1416,7 +1417,7 @@ __global__ void __launch_bounds__(OZ_TM)
                int64_t ldy, double* __restrict__ part, int ldp, void* __restrict__ W, int64_t ldw, int out_fmt,
                double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
                int out_fmt2, int stamp, const int* __restrict__ full, const double* __restrict__ Wt) {
-  __shared__ double red[4][16];
+  __shared__ double red[4][OZR_CG];
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
     const unsigned long long t0 = g_oz_stamp[0], t1 = g_oz_stamp[1];
     if (t1 > t0) {
@@ -1463,10 +1464,10 @@ __global__ void __launch_bounds__(OZ_TM)
   const int ne = s_ne;
   // the exact fp64 tail products of this row (3-digit heads in the product kernel)
   const double* wt = (Wt && valid && !*full) ? Wt + grow * BN : nullptr;
-  for (int jb = 16 * blockIdx.y; jb < ncols; jb += 16 * gridDim.y) {   // 16 columns per y-block
-    double s[16], tl[16];
+  for (int jb = OZR_CG * blockIdx.y; jb < ncols; jb += OZR_CG * gridDim.y) {   // OZR_CG columns per y-block
+    double s[OZR_CG], tl[OZR_CG];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
+    for (int q = 0; q < OZR_CG; ++q) {
       s[q] = 0.0;
       tl[q] = (wt && jb + q < ncols) ? wt[jb + q] : 0.0;
     }
@@ -1474,7 +1475,7 @@ __global__ void __launch_bounds__(OZ_TM)
       for (int e = 0; e < ne; ++e) {
         const double* src = ws + s_base[e] + row;
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
+        for (int q = 0; q < OZR_CG; ++q)
           if (jb + q < ncols) s[q] += src[(size_t)(jb + q) * OZ_TM];
       }
     } else {                                  // more segments than the table: resolve per thread
@@ -1490,13 +1491,13 @@ __global__ void __launch_bounds__(OZ_TM)
           const int slot = (int)(vt - oz_seg_begin(c, total_units, G) / kbc);
           const double* src = ws + ((size_t)c * max_slots + slot) * (size_t)(OZ_TM * BN) + row;
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
+          for (int q = 0; q < OZR_CG; ++q)
             if (jb + q < ncols) s[q] += src[(size_t)(jb + q) * OZ_TM];
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
+    for (int q = 0; q < OZR_CG; ++q) {
       const int j = jb + q, gj = j0 + j;
       double r2 = 0.0;
       if (valid && j < ncols && gj < nvalid) {
@@ -1525,10 +1526,11 @@ __global__ void __launch_bounds__(OZ_TM)
       if (lane == 0) red[warp][q] = r2;
     }
     __syncthreads();
-    if (threadIdx.x < 16 && jb + threadIdx.x < ncols) {
+    if (threadIdx.x < OZR_CG && jb + threadIdx.x < ncols) {
       const double* rr = &red[0][0];
       if (W) {
-        const double m = fmax(fmax(rr[threadIdx.x], rr[16 + threadIdx.x]), fmax(rr[32 + threadIdx.x], rr[48 + threadIdx.x]));
+        const double m = fmax(fmax(rr[threadIdx.x], rr[OZR_CG + threadIdx.x]),
+                              fmax(rr[2 * OZR_CG + threadIdx.x], rr[3 * OZR_CG + threadIdx.x]));
         if (colmax) atomic_max_nonneg(&colmax[j0 + jb + threadIdx.x], m);
       } else {
         part[(int64_t)t * ldp + j0 + jb + threadIdx.x] =
@@ -1667,7 +1669,7 @@ int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int
     const int j0 = ps * p.bn;
     rc = p.bn == 32 ? oz_launch<32>(tA, tV, p, pws, j0, st) : oz_launch<64>(tA, tV, p, pws, j0, st);
     if (rc) return rc;
-    k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
+    k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + OZR_CG - 1) / OZR_CG)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
                                            ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0, nullptr, nullptr);
     OFRR_CHECK_LAUNCH();
@@ -1899,7 +1901,7 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     k_oz_tailmul<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(rows, full, tcnt, tcol, tval, Vt, p.ldvt, j0,
                                                              std::min(p.bn, r - j0), p.bn, Wt);
     OFRR_CHECK_LAUNCH();
-    k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + 15) / 16)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
+    k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + OZR_CG - 1) / OZR_CG)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
                                            ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
                                            g_oz_stamp_on ? (levels == OZ_D ? 1 : 2) : 0, full, Wt);
