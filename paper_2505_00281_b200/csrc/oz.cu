@@ -340,6 +340,54 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The same split over (column, segment) CTAs: the column maxima first (bit patterns of
+// non-negative doubles order like the values, NaN above inf -> OZ_BAD as above), then the
+// digits of each segment -- one CTA per column left most SMs idle on this streaming pass.
+__global__ void __launch_bounds__(256)
+    k_oz_vmax(const double* __restrict__ V, int64_t ldv, int64_t cols, int n, unsigned long long* __restrict__ vmax,
+              int64_t seg) {
+  const int j = blockIdx.x;
+  if (j >= n) return;
+  const double* v = V + (size_t)j * ldv;
+  const int64_t l1 = std::min<int64_t>(cols, ((int64_t)blockIdx.y + 1) * seg);
+  unsigned long long m = 0ull;
+  for (int64_t l = (int64_t)blockIdx.y * seg + threadIdx.x; l < l1; l += blockDim.x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[l]));
+    m = b > m ? b : m;
+  }
+  const unsigned hi = (unsigned)(m >> 32), lo = (unsigned)m;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  if ((threadIdx.x & 31) == 0) atomicMax(&vmax[j], ((unsigned long long)mhi << 32) | mlo);
+}
+
+__global__ void __launch_bounds__(256)
+    k_oz_slices_vs(const double* __restrict__ V, int64_t ldv, int64_t cols, int n,
+                   const unsigned long long* __restrict__ vmax, int* __restrict__ F, int8_t* __restrict__ dig, int npad,
+                   int64_t cols_pad, int64_t seg) {
+  const int j = blockIdx.x;
+  const size_t plane = (size_t)npad * cols_pad;
+  int8_t* row0 = dig + (size_t)j * cols_pad;
+  const int64_t s0 = (int64_t)blockIdx.y * seg, s1 = std::min<int64_t>(cols_pad, s0 + seg);
+  if (j >= n) {
+    for (int64_t l = s0 + threadIdx.x; l < s1; l += blockDim.x)
+      for (int p = 0; p < OZ_D; ++p) row0[p * plane + l] = 0;
+    if (blockIdx.y == 0 && threadIdx.x == 0) F[j] = 0;
+    return;
+  }
+  const double* v = V + (size_t)j * ldv;
+  const int E = oz_scale(__longlong_as_double((long long)vmax[j]));
+  if (blockIdx.y == 0 && threadIdx.x == 0) F[j] = E;
+  for (int64_t l0 = s0 + 4 * (int64_t)threadIdx.x; l0 < s1; l0 += 4 * (int64_t)blockDim.x) {
+    uint32_t w[OZ_D], lo[4], hi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) oz_fixed64(l0 + e < cols ? v[l0 + e] : 0.0, E, lo[e], hi[e]);
+    oz_planes4(lo, hi, w);
+#pragma unroll
+    for (int p = 0; p < OZ_D; ++p) *reinterpret_cast<uint32_t*>(row0 + p * plane + l0) = w[p];
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // The int8 tensor-core product.  Work unit = one k-block of a virtual tile vt = (row tile,
 // K chunk); stream-K splits the units evenly over the grid.  Per unit the V digit tiles
@@ -1694,7 +1742,7 @@ struct OzkPlan {
   int bn, npass, npad, m_tiles, kblocks, nchunks, kbc, grid, max_slots, ldvt;
   int64_t rows_pad, cols_pad;
   long long total;
-  size_t off_F, off_dig, off_ws, off_part, off_vt, off_wt, bytes;
+  size_t off_F, off_dig, off_ws, off_part, off_vt, off_wt, off_vmax, bytes;
 };
 
 // OFRR_OZK_TMEM_A=0: the heads on the shared-memory kernel (comparison runs)
@@ -1734,6 +1782,7 @@ static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r, int levels = OZ_D) {
   p.ldvt = p.npad;
   p.off_vt = take((size_t)cols * p.ldvt * sizeof(double));     // V row-major for the tails
   p.off_wt = take((size_t)p.rows_pad * p.bn * sizeof(double));  // tails x V of one column pass
+  p.off_vmax = take((size_t)p.npad * sizeof(unsigned long long));   // column maxima of |V| (bits)
   p.bytes = b;
   return p;
 }
@@ -1878,8 +1927,17 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
   double* part = (double*)(base + p.off_part);
   double* Vt = (double*)(base + p.off_vt);
   double* Wt = (double*)(base + p.off_wt);
-  k_oz_slices_v<<<(unsigned)p.npad, 256, 0, st>>>(V, ldv, cols, r, F, dig, p.npad, p.cols_pad);
-  OFRR_CHECK_LAUNCH();
+  {
+    unsigned long long* vmax = (unsigned long long*)(base + p.off_vmax);
+    const int64_t seg = 4096;                                   // multiple of 4 (digit groups)
+    const unsigned nseg = (unsigned)((p.cols_pad + seg - 1) / seg);
+    OFRR_CUDA_TRY(cudaMemsetAsync(vmax, 0, (size_t)p.npad * sizeof(unsigned long long), st));
+    k_oz_vmax<<<dim3((unsigned)p.npad, nseg), 256, 0, st>>>(V, ldv, cols, r, vmax, seg);
+    OFRR_CHECK_LAUNCH();
+    k_oz_slices_vs<<<dim3((unsigned)p.npad, nseg), 256, 0, st>>>(V, ldv, cols, r, vmax, F, dig, p.npad, p.cols_pad,
+                                                                 seg);
+    OFRR_CHECK_LAUNCH();
+  }
   k_oz_vt<<<dim3((unsigned)((cols + 31) / 32), (unsigned)((r + 31) / 32)), 256, 0, st>>>(V, ldv, cols, r, Vt, p.ldvt);
   OFRR_CHECK_LAUNCH();
   CUtensorMap tV;
