@@ -353,6 +353,9 @@ class EigEngine:
             h = self.ops.orthonormalize(X, self.cfg.basis_method.value, self.pol.storage, self.pol.compute,
                                         self.pol.accumulate, self.pol.drop_tol)
         else:
+            if self.ops is _ops:                 # the kept count straight into the status word
+                return self.ops.hessenberg(X, self.pol.storage, self.pol.compute, self.pol.drop_tol,
+                                           n_kept_out=st[S_NKEPT:S_NKEPT + 1])
             h = self.ops.hessenberg(X, self.pol.storage, self.pol.compute, self.pol.drop_tol)
         st[S_NKEPT:S_NKEPT + 1].copy_(h.n_kept)
         return h
@@ -397,9 +400,13 @@ class EigEngine:
         else:
             B, M = ops.gram(U, W, self.proj_out, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], want_m=not classical)
         side = self._fork_res_scales()
-        eig = ops.sym_eig(B, kp) if classical else ops.sym_def_gen_eig(B, M, kp)
-        st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
-        st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
+        if classical or ops is not _ops:
+            eig = ops.sym_eig(B, kp) if classical else ops.sym_def_gen_eig(B, M, kp)
+            st[S_EIG_STATUS:S_EIG_STATUS + 1].copy_(eig.status)
+            st[S_NOUT:S_NOUT + 1].copy_(eig.n_out)
+        else:                                    # status and count straight into the status word
+            eig = ops.sym_def_gen_eig(B, M, kp, n_out_out=st[S_NOUT:S_NOUT + 1],
+                                      status_out=st[S_EIG_STATUS:S_EIG_STATUS + 1])
         if (not comm.distributed and hasattr(ops, "restart") and W2 is not None and W2.n == U.n and kp <= 256
                 and (reuse or top_check is not None)):
             # K6f: Ritz block, next power step and residual estimate in one pass over (U, W2)
@@ -924,6 +931,9 @@ class EigEngine:
                 self.n, self.cfg.k, self.cfg.iter, pol(self.pol), pol(self.mv), check, top, self.device.index,
                 bool(_lib.load().ofrr_prof_gemm_active()), self._refresh_now and self._res_oz is not None,
                 self.cfg.reuse_av, first or not self.cfg.reuse_av,
+                # what else shapes the captured body: basis builder, projection, row partition
+                str(self.cfg.basis_method.value), str(self.cfg.projection), bool(self.comm.distributed),
+                int(getattr(self, "r0", 0)), int(getattr(self, "r1", 0)), id(self.ops),
                 # Ozaki workspaces the captured kernels read (made outside the capture)
                 tuple(sorted(oz.ws.data_ptr() for oz in self._oz.values())))
 

@@ -427,7 +427,10 @@ class HessOut:
     n_kept: torch.Tensor  # int32[1]
 
 
-def hessenberg(X: DevBlock, storage: FpFormat, compute: FpFormat, tol: float) -> HessOut:
+def hessenberg(X: DevBlock, storage: FpFormat, compute: FpFormat, tol: float,
+               n_kept_out: Optional[torch.Tensor] = None) -> HessOut:
+    """K3.  ``n_kept_out`` (int32[1], e.g. a slot of the driver's status word): the kernel
+    writes the kept count there directly (no copy node in a captured iteration)."""
     L = _lib.load()
     dev = X.device
     if FpFormat(storage) != X.fmt:
@@ -437,6 +440,8 @@ def hessenberg(X: DevBlock, storage: FpFormat, compute: FpFormat, tol: float) ->
     Q = new_block(X.n, X.k, storage, dev)
     piv, kept, nk = _zeros_pack(dev, ((max(X.k, 1),), torch.int64), ((max(X.k, 1),), torch.int32),
                                 ((1,), torch.int32))
+    if n_kept_out is not None:
+        nk = n_kept_out
     ws_b = L.ofrr_hessenberg_workspace(X.n, X.k, int(storage))
     ws = _ws(ws_b, dev)
     _lib.check(L.ofrr_hessenberg(X.ptr, X.n, X.k, X.ld, int(storage), int(compute), float(tol), Q.ptr, Q.ld,
@@ -504,13 +509,19 @@ class EigOut:
     status: torch.Tensor   # int32[1]
 
 
-def sym_def_gen_eig(B: torch.Tensor, M: torch.Tensor, k: int) -> EigOut:
-    """B, M: fp64 column-major k x k (torch (k, k) with row j = column j)."""
+def sym_def_gen_eig(B: torch.Tensor, M: torch.Tensor, k: int, n_out_out: Optional[torch.Tensor] = None,
+                    status_out: Optional[torch.Tensor] = None) -> EigOut:
+    """B, M: fp64 column-major k x k (torch (k, k) with row j = column j).  ``n_out_out`` /
+    ``status_out`` (int32[1], zeroed): written by the kernels directly (status-word slots)."""
     L = _lib.load()
     dev = B.device
     kk = max(k, 1)
     vals, vecs, n_out, status = _zeros_pack(dev, ((kk,), torch.float64), ((kk, kk), torch.float64),
                                             ((1,), torch.int32), ((1,), torch.int32))
+    if n_out_out is not None:
+        n_out = n_out_out
+    if status_out is not None:
+        status = status_out
     ws = _ws(L.ofrr_small_eig_workspace(k), dev)
     _lib.check(L.ofrr_sym_def_gen_eig(B.data_ptr(), M.data_ptr(), k, vals.data_ptr(), vecs.data_ptr(),
                                       n_out.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),

@@ -81,8 +81,12 @@ def test_driver_classical_vs_reference(ofrr_gpu, gold, pname, meth, proj):
     ref_err = np.abs(gold[key + "/vals"][:top] - exact[:top]) / np.abs(exact[:top])
     err = np.abs(rs.values[:top] - exact[:top]) / np.abs(exact[:top])
     assert np.all(err <= np.maximum(10 * ref_err, 1e-6)), (err, ref_err)
-    assert np.all(rs.residuals[:top] <= 2 * gold[key + "/res"][:top] + 1e-13), (rs.residuals[:top],
-                                                                                gold[key + "/res"][:top])
+    # per pair: within 2x of the reference's residual, plus (fp32 policy) the fp32 rounding floor
+    # of the pair -- u |lambda_1| / |lambda_i| times a small constant: at that floor both runs'
+    # residuals are rounding noise of their own (different) summation orders
+    floor = 0.0 if pname == "full-f64" else 8 * 2.0 ** -24 * np.abs(exact[0]) / np.abs(exact[:top])
+    assert np.all(rs.residuals[:top] <= 2 * gold[key + "/res"][:top] + floor + 1e-13), (
+        rs.residuals[:top], gold[key + "/res"][:top], floor)
 
 
 def test_driver_svd_classical_vs_reference(ofrr_gpu, gold):

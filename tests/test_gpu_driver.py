@@ -379,3 +379,29 @@ def test_fp8_rung_with_column_scaling(ofrr_gpu):
     assert min(w for _, w in st.history) < 0.3                   # it converged to the e4m3 floor
     err = np.abs(rs.values[:top] - lam[:top]) / lam[:top]
     assert np.max(err) < 0.1, err
+
+
+@pytest.mark.gpu
+def test_graph_cache_keyed_by_basis_and_projection(ofrr_gpu, monkeypatch):
+    """Captured iteration graphs are reused only by solves whose body they captured: a solve
+    with another basis builder / projection on the same operator and shapes must not replay a
+    graph captured for the first one (results equal the graph-free run, bit for bit)."""
+    p = ofrr_gpu
+    n, k, top = 600, 16, 6
+    lam = p.geometric_spectrum(n, top, k)
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.F32, seed=5)
+    pol = p.POLICY_PRESETS["full-f32"]
+
+    def run(meth, proj):
+        cfg = p.IterConfig(k=k, m=3, iter=1, basis_method=p.BasisMethod(meth), projection=proj, policy=pol, seed=3)
+        return p.subspace_iter_eig(A, cfg)
+
+    monkeypatch.setenv("OFRR_CUDA_GRAPHS", "0")
+    ref = run("cgs", "rr")
+    monkeypatch.setenv("OFRR_CUDA_GRAPHS", "1")
+    for _ in range(3):
+        run("hess-l", "ofrr")                    # warms and captures graphs for these shapes
+    for _ in range(3):
+        got = run("cgs", "rr")
+        np.testing.assert_array_equal(np.asarray(got.values), np.asarray(ref.values))
+        np.testing.assert_array_equal(np.asarray(got.residuals), np.asarray(ref.residuals))
