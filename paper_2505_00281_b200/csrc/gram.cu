@@ -41,6 +41,9 @@ __global__ void __launch_bounds__(256)
   const int i0 = blockIdx.y * GT;      // rows of the Gram (columns of U)
   const int j0 = blockIdx.z * GT;      // columns of the Gram ([W U])
   const int ncols = kw + k;
+  // U^T U is symmetric: with tile-aligned blocks (kw % GT == 0) the tiles below its diagonal
+  // are not computed; k_gram_reduce mirrors them (the pencil symmetrises M anyway)
+  if (kw % GT == 0 && j0 >= kw && (j0 - kw) / GT < i0 / GT) return;
   const int64_t rb = (int64_t)blockIdx.x * rows_per_chunk;
   const int64_t re = std::min<int64_t>(n, rb + rows_per_chunk);
   double acc[2][4][2] = {};
@@ -115,10 +118,15 @@ __global__ void __launch_bounds__(256) k_gram_reduce(const double* __restrict__ 
   const int64_t total = (int64_t)ncols * k;
   const int lx = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lx;
+  int64_t es = e;                                   // the partials' element (mirrored tiles of U^T U)
+  if (e < total && kw % GT == 0) {
+    const int gj = (int)(e / k), gi = (int)(e % k);
+    if (gj >= kw && (gj - kw) / GT < gi / GT) es = (int64_t)(kw + gi) * k + (gj - kw);
+  }
   double s = 0.0;
   if (e < total) {
 #pragma unroll 4
-    for (int c = g; c < nchunks; c += 8) s += part[(int64_t)c * total + e];
+    for (int c = g; c < nchunks; c += 8) s += part[(int64_t)c * total + es];
   }
   red[g][lx] = s;
   __syncthreads();
@@ -137,7 +145,9 @@ struct GramPlan { int nchunks; int64_t rows_per; };
 static GramPlan gram_plan(int64_t n, int k, int kw) {
   int sms = ofrr_device_sm_count(-1);
   if (sms <= 0) sms = 148;
-  const int tiles = ((k + GT - 1) / GT) * ((kw + k + GT - 1) / GT);
+  const int kt = (k + GT - 1) / GT;
+  // computed tiles: U^T U below its diagonal is mirrored (k_gram_partial) when tile-aligned
+  const int tiles = kt * ((kw + k + GT - 1) / GT) - (kw % GT == 0 ? kt * (kt - 1) / 2 : 0);
   // ~4 CTAs per SM (each has one slab of loads in flight; more CTAs hide the latency),
   // at least 4 slabs per chunk (the partials are re-read by the reduce)
   int64_t chunks = std::max<int64_t>(1, (4 * sms + tiles - 1) / tiles);

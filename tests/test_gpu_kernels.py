@@ -222,12 +222,14 @@ def test_hessenberg_golden(ofrr_gpu, golden, case):
 
 
 @pytest.mark.parametrize("fmt,out", [(BF16, F64), (F16, F32), (F32, F64), (F64, F64)])
-def test_gram_vs_fp64(ofrr_gpu, oracle, fmt, out):
-    """K4: U^T W and U^T U (fp64 sums of exact products), rounded to the projection format."""
+@pytest.mark.parametrize("k", [70, 128])
+def test_gram_vs_fp64(ofrr_gpu, oracle, fmt, out, k):
+    """K4: U^T W and U^T U (fp64 sums of exact products), rounded to the projection format
+    (k = 128: tile-aligned, the U^T U tiles below the diagonal mirrored)."""
     from paper_2505_00281_b200 import ops
     p, o = ofrr_gpu, oracle
     rng = np.random.default_rng(fmt * 10 + out)
-    n, k = 9000, 70
+    n = 9000
     u = o.round_to(rng.standard_normal((n, k)), fmt)
     w = o.round_to(rng.standard_normal((n, k)), fmt)
     G1, G2 = ops.gram(_blk(p, u, fmt), _blk(p, w, fmt), p.FpFormat(out))
