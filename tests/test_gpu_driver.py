@@ -405,3 +405,34 @@ def test_graph_cache_keyed_by_basis_and_projection(ofrr_gpu, monkeypatch):
         got = run("cgs", "rr")
         np.testing.assert_array_equal(np.asarray(got.values), np.asarray(ref.values))
         np.testing.assert_array_equal(np.asarray(got.residuals), np.asarray(ref.residuals))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("switch,m", [((1e-3, 1e-6), 40), ((1e-30, 1e-30), 3)])
+def test_ladder_device_rungs_equal_host_loop(ofrr_gpu, monkeypatch, switch, m):
+    """Ladder rungs on the device-side loop (k_loop_decide_rung) give bit for bit the host
+    loop's answer: a rung that finishes on the device, and a rung that exhausts m (the device
+    stops for the host, which re-runs the rung from the same start block)."""
+    from paper_2505_00281_b200 import driver
+    p = ofrr_gpu
+    n, k, top = 4096, 32, 8
+    lam = p.geometric_spectrum(n, top, k)
+    A, _ = p.synthetic_symmetric(lam, p.FpFormat.BF16, seed=21)
+    cfg = p.IterConfig(k=k, m=m, iter=1, basis_method=p.BasisMethod.HESS_LEFT, projection="ofrr",
+                       policy=p.POLICY_PRESETS["full-f64"], seed=4, tol=1e-9, top=top,
+                       ladder=(p.POLICY_PRESETS["full-f32-lite"], p.POLICY_PRESETS["full-f64-lite"]),
+                       ladder_switch=switch, reuse_av=True)
+
+    def solve():
+        st = p.RunStats()
+        return p.subspace_iter_eig(A, cfg, stats=st), st
+
+    monkeypatch.setattr(driver, "DEVICE_LOOP", False)
+    ref, st_ref = solve()
+    monkeypatch.setattr(driver, "DEVICE_LOOP", True)
+    for _ in range(3):                          # capture, then the device loops
+        got, st = solve()
+    np.testing.assert_array_equal(np.asarray(got.values), np.asarray(ref.values))
+    np.testing.assert_array_equal(np.asarray(got.residuals), np.asarray(ref.residuals))
+    assert st.iterations == st_ref.iterations and st.a_passes == st_ref.a_passes
+    assert st.rungs == st_ref.rungs
