@@ -182,7 +182,7 @@ template <typename T> __device__ __forceinline__ double el_d(T y) {
   else return to_d(y);
 }
 
-__device__ unsigned long long g_hessprof[10];   // debug: CTA 0 per-phase time (ns), last launch
+__device__ unsigned long long g_hessprof[11];   // debug: CTA 0 per-phase time (ns), last launch
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(HT)
   wait();
 
   int nk = 0;
-  unsigned long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tp = gtime();
+  unsigned long long pacc[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tp = gtime();
   auto mark = [&](int ph) {
     if (c == 0 && threadIdx.x == 0) { const unsigned long long t = gtime(); pacc[ph] += t - tp; tp = t; }
   };
@@ -618,6 +618,7 @@ __global__ void __launch_bounds__(HT)
           }
         }
       }
+      mark(10);
 #pragma unroll
       for (int t2 = 0; t2 < 2; ++t2) {
         const int cc = j + threadIdx.x + t2 * HT;
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(HT)
     for (int64_t i = r0 + threadIdx.x; i < r1; i += HT) Q[(int64_t)j * ldq + i] = st_s<T>(CV(0));
   if (c == 0 && threadIdx.x == 0) {
     *n_kept = nk;
-    for (int i = 0; i < 10; ++i) g_hessprof[i] = pacc[i];
+    for (int i = 0; i < 11; ++i) g_hessprof[i] = pacc[i];
   }
 }
 

@@ -17,12 +17,12 @@ dev = torch.device("cuda")
 rng = np.random.default_rng(0)
 L = _lib.load()
 L.ofrr_debug_hess_profile.argtypes = [ctypes.c_void_p]
-names = ["wait->reduce", "prow", "scale+col j+1", "publish+arrive", "deferred update", "wait", "panel-end PR", "panel-end blocked update", "panel load", "panel-end scan+barrier"]
+names = ["wait->reduce", "prow", "scale+col j+1", "publish+arrive", "deferred update", "wait", "panel-end PR", "panel-end blocked update", "panel load", "panel-end scan+barrier", "scale loop (before the pivot-row stores)"]
 for (n, k, fmt, comp) in ((65536, 128, p.FpFormat.F32, p.FpFormat.F32), (65536, 128, p.FpFormat.F64, p.FpFormat.F64),
                           (16384, 64, p.FpFormat.F32, p.FpFormat.F32)):
     X = ops.block_from_host(p.round_to(rng.random((n, k)), fmt), fmt, dev)
     t = timeit(lambda: ops.hessenberg(X, fmt, comp, 2.0 ** -20))
-    out = (ctypes.c_ulonglong * 10)()
+    out = (ctypes.c_ulonglong * 11)()
     L.ofrr_debug_hess_profile(ctypes.addressof(out))
     print(f"n={n} k={k} {fmt.name}: {t * 1e3:.1f} us ({t * 1e3 / k:.2f} us/column); CTA0 per column: " +
           ", ".join(f"{nm} {out[i] / 1e3 / k:.2f}" for i, nm in enumerate(names)) + " (us)", flush=True)
