@@ -123,7 +123,7 @@ int ofrr_prof_k1_read(double* sum_ms, long long* count);
  * closed by the k_oz_resid launch that follows each product. */
 int ofrr_prof_oz_stamp(int on);
 int ofrr_prof_oz_read(double* sum_ms, long long* count);
-/* the same split by product tier: 1 = FP64-accurate (6 levels), 2 = lite (4 levels), 0 = all */
+/* the same split by product tier: 1 = FP64-accurate (6 levels), 2 = lite (4 levels), 3 = 5 levels, 0 = all */
 int ofrr_prof_oz_read_tier(int tier, double* sum_ms, long long* count);
 
 /* ---------------------------------------------------------------------------------

@@ -35,8 +35,8 @@ namespace ofrr {
 // stamps its entry (min) and exit (max) in globaltimer ns; the k_oz_resid launch that follows
 // adds the interval to a running sum and re-arms the stamps
 // min start, max end, then (sum, count) per tier: [2..3] every product, [4..5] FP64-accurate
-// (6 levels), [6..7] lite (4 levels) -- the k_oz_resid launch passes stamp = 1 + (lite ? 1 : 0)
-__device__ unsigned long long g_oz_stamp[8] = {~0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+// (6 levels), [6..7] lite (4 levels), [8..9] 5 levels -- the k_oz_resid launch passes the tier
+__device__ unsigned long long g_oz_stamp[10] = {~0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
 static bool g_oz_stamp_on = false;
 __device__ __forceinline__ unsigned long long oz_gtimer_ns() {
   unsigned long long t;
@@ -46,14 +46,14 @@ __device__ __forceinline__ unsigned long long oz_gtimer_ns() {
 int oz_stamp_enable(int on) {
   g_oz_stamp_on = on != 0;
   if (on) {
-    const unsigned long long z[8] = {~0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+    const unsigned long long z[10] = {~0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
     if (cudaMemcpyToSymbol(g_oz_stamp, z, sizeof(z)) != cudaSuccess) return OFRR_ERR_CUDA;
   }
   return OFRR_OK;
 }
-int oz_stamp_read(double* sum_ms, long long* count, int tier) {   // tier 0 all, 1 FP64-accurate, 2 lite
-  unsigned long long v[8];
-  if (tier < 0 || tier > 2) return OFRR_ERR_INVALID;
+int oz_stamp_read(double* sum_ms, long long* count, int tier) {   // tier 0 all, 1 FP64-accurate, 2 lite, 3 5-level
+  unsigned long long v[10];
+  if (tier < 0 || tier > 3) return OFRR_ERR_INVALID;
   if (cudaMemcpyFromSymbol(v, g_oz_stamp, sizeof(v)) != cudaSuccess) return OFRR_ERR_CUDA;
   *sum_ms = (double)v[2 + 2 * tier] * 1e-6;
   *count = (long long)v[3 + 2 * tier];
@@ -1758,7 +1758,7 @@ static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r, int levels = OZ_D) {
   // planes in TMEM read A twice: 5.2 vs 4.4 ms per A pass at C3)
   static int lite_bn = -1;                 // OFRR_OZK_LITE_BN=64: lite passes of 64 columns (comparison runs)
   if (lite_bn < 0) { const char* e = getenv("OFRR_OZK_LITE_BN"); lite_bn = e ? atoi(e) : 128; }
-  p.bn = levels == OZ_D ? (r <= 32 ? 32 : 64) : (r <= 64 || lite_bn == 64 ? 64 : 128);
+  p.bn = levels >= 5 ? (r <= 32 ? 32 : 64) : (r <= 64 || lite_bn == 64 ? 64 : 128);
   p.npass = (r + p.bn - 1) / p.bn;
   p.npad = p.npass * p.bn;
   p.rows_pad = (rows + OZ_TM - 1) / OZ_TM * OZ_TM;
@@ -1907,7 +1907,10 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
               int64_t ldv, int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W,
               int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
               double** part_out, void* ws, size_t ws_bytes, cudaStream_t st, int levels) {
-  if (levels != OZ_D && levels != 4) { ofrr_set_error("ozaki: levels must be 6 or 4 (got %d)", levels); return OFRR_ERR_INVALID; }
+  if (levels != OZ_D && levels != 5 && levels != 4) {
+    ofrr_set_error("ozaki: levels must be 6, 5 or 4 (got %d)", levels);
+    return OFRR_ERR_INVALID;
+  }
   if (oz_use_planes())
     return oz_apply(op_ws, rows, cols, V, ldv, r, vals, r_dev, Y, ldy, W, ldw, out_fmt, colmax, flags, W2, ldw2,
                     out_fmt2, part_out, ws, ws_bytes, st);
@@ -1950,6 +1953,9 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     if (levels == OZ_D)                                                                          \
       rc = p.bn == 32 ? ozk_launch<F, 32, OZ_D>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)  \
                       : ozk_launch<F, 64, OZ_D>(A, rows, cols, lda, T, tV, p, pws, j0, full, st); \
+    else if (levels == 5)                                                                        \
+      rc = p.bn == 32 ? ozk_launch<F, 32, 5>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)     \
+                      : ozk_launch<F, 64, 5>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);    \
     else                                                                                         \
       rc = p.bn == 64 ? ozk_launch<F, 64, 4>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)     \
                       : ozk_launch<F, 128, 4>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);
@@ -1962,7 +1968,7 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + OZR_CG - 1) / OZR_CG)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
                                            ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
-                                           g_oz_stamp_on ? (levels == OZ_D ? 1 : 2) : 0, full, Wt);
+                                           g_oz_stamp_on ? (levels == OZ_D ? 1 : levels == 5 ? 3 : 2) : 0, full, Wt);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;

@@ -136,6 +136,11 @@ _GRAPHS = OrderedDict()
 # stream.
 _SOLVE_LOCK = threading.RLock()
 DEVICE_LOOP = True      # the whole solve as one graph launch (csrc/loop.cu) once its graphs exist
+# the first iteration of a rung that starts from the previous rung's next iterate (stepped) takes
+# its block product with 5 Ozaki levels (~2^-38 of |A||x|) instead of 6 when the rung's products
+# are FP64-accurate: that iteration never produces the FP64 report (a convergence there goes to
+# the host loop, which then takes the report from a separate FP64 product)
+LEAD_LEVELS = int(__import__("os").environ.get("OFRR_LEAD_LEVELS", "5"))
 HANDOVER_STEPPED = __import__("os").environ.get("OFRR_HANDOVER_STEPPED") == "1"   # ladder: start every rung from the previous rung's W Y (experiments; see _subspace_iter_eig)
 _WARM = set()
 _NO_GRAPH = set()
@@ -245,6 +250,7 @@ class EigEngine:
         _, self.proj_out = projection_policy(self.pol)
         self.stats = RunStats()
         self._last_w2 = None    # the latest projection's W = A U in its accumulation format
+        self._last_w2_levels = 6
         self._oz = {}           # prepared Ozaki digit planes per operator (this run)
         if prepared is not None:
             # an operator prepared on a side stream while the previous ladder rung ran
@@ -360,6 +366,15 @@ class EigEngine:
         st[S_NKEPT:S_NKEPT + 1].copy_(h.n_kept)
         return h
 
+    def _proj_levels_for(self, lead: bool) -> int:
+        lv = self.pol.product_levels
+        return LEAD_LEVELS if (lead and lv == 6 and LEAD_LEVELS in (5, 6)) else lv
+
+    def _proj_levels(self) -> int:
+        """Ozaki levels of this iteration's projection product (see LEAD_LEVELS)."""
+        lv = self.pol.product_levels
+        return LEAD_LEVELS if (getattr(self, "_lead", False) and lv == 6 and LEAD_LEVELS in (5, 6)) else lv
+
     def project(self, U, st, want64: bool, top_check: Optional[int] = None, reuse: bool = False):
         """ofrr_eig (ofrr/projection.py:75-87) + restart block (ofrr/driver.py:109).
 
@@ -387,10 +402,11 @@ class EigEngine:
                 acc = FpFormat.F64 if FpFormat.F64 in (self.A_pol.fmt, U.fmt) else FpFormat.F32
                 W2 = ops.new_block(self.A_pol.rows, kp, acc, self.device)
             ops.gemm_av(self.A_pol, U, W, flags=st[S_GRAM_FLAGS:S_GRAM_FLAGS + 1], W2=W2,
-                        **({"oz": self._block_oz(self.A_pol, U), "levels": self.pol.product_levels}
+                        **({"oz": self._block_oz(self.A_pol, U), "levels": self._proj_levels()}
                            if self.ops is _ops else {}))
         self.stats.a_passes += 1
         self._last_w2 = W2
+        self._last_w2_levels = self._proj_levels() if W2 is not None and W2.fmt == FpFormat.F64 else 6
         Ul = _row_slice(U, self.r0, self.r1) if comm.distributed else U
         classical = self.cfg.projection == "rr"       # rr_eig (ofrr/projection.py:64-72): no mass matrix
         if comm.distributed:
@@ -537,13 +553,14 @@ class EigEngine:
             # (the basis keeps all k in the common case; dropped columns of Q are zero),
             # residual estimate -- replayed as one CUDA graph when possible.  One host sync.
             first = it == 0 and not self.stepped
+            lead = it == 0 and self.stepped
             with _ph("graph_step"):
-                out = self._graph_step(X, check, top, first) if use_graph and X.k == cfg.k else None
+                out = self._graph_step(X, check, top, first, lead) if use_graph and X.k == cfg.k else None
             if out is None:
                 with _ph("eager_body"):
-                    out = self._body(X, check, top, first)
+                    out = self._body(X, check, top, first, lead)
                 if use_graph:
-                    _WARM.add(self._graph_key(check, top, first))
+                    _WARM.add(self._graph_key(check, top, first, lead))
             st, h, U, eig, Xn, est = out["st"], out["h"], out["U"], out["eig"], out["Xn"], out["est"]
             kp = U.k
             with _ph("iteration_sync"):
@@ -558,7 +575,8 @@ class EigEngine:
                 st[S_EIG_STATUS:].zero_()                     # gram/pencil/restart slots
                 res = self.project(U, st, want64=False, top_check=(top if check else None), reuse=cfg.reuse_av)
                 eig, _, Xn, est = res[:4]
-                out = dict(out, Xnext=res[4] if cfg.reuse_av else None, W2=self._last_w2, graph=None)
+                out = dict(out, Xnext=res[4] if cfg.reuse_av else None, W2=self._last_w2, graph=None,
+                           w2_levels=self._last_w2_levels)
                 s, vals_all, est_np = self._fetch(st, eig.values, est)
             _raise_for(s, "projection")
             r = int(s[S_NOUT])
@@ -615,7 +633,7 @@ class EigEngine:
         cfg = self.cfg
         L = _lib.load()
         self._refresh_now = True
-        kf = self._graph_key(True, top, not self.stepped)
+        kf = self._graph_key(True, top, not self.stepped, self.stepped)
         self._refresh_now = False
         ks = self._graph_key(True, top, False)
         gf, gs = _GRAPHS.get(kf), _GRAPHS.get(ks)
@@ -732,7 +750,7 @@ class EigEngine:
         cfg = self.cfg
         L = _lib.load()
         self._refresh_now = True
-        kf = self._graph_key(True, top, not self.stepped)
+        kf = self._graph_key(True, top, not self.stepped, self.stepped)
         self._refresh_now = False
         ks = self._graph_key(True, top, False)
         gf, gs = _GRAPHS.get(kf), _GRAPHS.get(ks)
@@ -825,7 +843,7 @@ class EigEngine:
                 U64c = self.ops.DevBlock(U64.t.clone(), U64.n, r, U64.fmt)   # outlive the next replay
                 return RitzSet(np.array(vals[:r]), DenseMatrix.from_block(U64c), "eig", residuals=res)
         W2 = out.get("W2")
-        if self._w2_is_fp64(W2, U):
+        if self._w2_is_fp64(W2, U, out.get("w2_levels", 6)):
             U64, res = self._report_from_w(U, W2, eig, kp, r)
             rs = RitzSet(np.array(vals[:r]), DenseMatrix.from_block(U64.narrow(r)), "eig")
             return RitzSet(rs.values, rs.vectors, "eig", residuals=res.cpu().numpy()[:r])
@@ -842,9 +860,10 @@ class EigEngine:
         U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
         return U64, self.residuals_from_w(U, W2, eig, r)
 
-    def _w2_is_fp64(self, W2, U) -> bool:
+    def _w2_is_fp64(self, W2, U, levels: int = 6) -> bool:
         """W2 = A U is an FP64-accurate product (fp64 block, full-accuracy K7z or fp64 FMA)."""
-        return W2 is not None and W2.fmt == FpFormat.F64 and W2.k >= U.k and self.pol.product_levels == 6
+        return (W2 is not None and W2.fmt == FpFormat.F64 and W2.k >= U.k and self.pol.product_levels == 6
+                and levels == 6)
 
     def residuals_from_w(self, U, W2, eig, r: int):
         """FP64 residuals ||A u_j - lambda_j u_j|| / |lambda_j| of the Ritz vectors u_j = U y_j
@@ -870,7 +889,7 @@ class EigEngine:
             with rec:
                 with torch.cuda.graph(graph):
                     W2 = g.outs.get("W2")
-                    if self._w2_is_fp64(W2, U):
+                    if self._w2_is_fp64(W2, U, g.outs.get("w2_levels", 6)):
                         U64, res = self._report_from_w(U, W2, eig, kp, r)
                     else:
                         U64, _ = self.ops.ritz(U, eig.vectors, kp, eig.n_out, kp, 1.0, want64=True)
@@ -882,7 +901,7 @@ class EigEngine:
         return g.report
 
     # ---- one outer iteration: eager body, or a replayed CUDA graph of it -----------------
-    def _body(self, X, check: bool, top: int, first: bool = True) -> dict:
+    def _body(self, X, check: bool, top: int, first: bool = True, lead: bool = False) -> dict:
         """One outer iteration.  With cfg.reuse_av the input of every iteration but the
         first is already the power-stepped block (the previous projection made it)."""
         import torch
@@ -892,11 +911,17 @@ class EigEngine:
         h = self.basis(Xp, st)
         U = h.Q.narrow(Xp.k)
         Xnext = None
-        if reuse:
-            eig, _, Xn, est, Xnext = self.project(U, st, want64=False, top_check=(top if check else None), reuse=True)
-        else:
-            eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
-        out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None, Xnext=Xnext, W2=self._last_w2)
+        self._lead = lead
+        try:
+            if reuse:
+                eig, _, Xn, est, Xnext = self.project(U, st, want64=False, top_check=(top if check else None),
+                                                      reuse=True)
+            else:
+                eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
+        finally:
+            self._lead = False
+        out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None, Xnext=Xnext, W2=self._last_w2,
+                   w2_levels=self._last_w2_levels)
         if self.comm.distributed:
             self.comm.all_reduce_max_(st)        # every rank sees (and raises) the same status
         parts = [st.to(torch.float64), eig.values.reshape(-1).to(torch.float64)]
@@ -922,7 +947,7 @@ class EigEngine:
                 and (not self.comm.distributed or self.comm.graphable)
                 and os.environ.get("OFRR_CUDA_GRAPHS", "1") != "0")
 
-    def _graph_key(self, check: bool, top: int, first: bool = True):
+    def _graph_key(self, check: bool, top: int, first: bool = True, lead: bool = False):
         A, B = self.A_mv, self.A_pol
         pol = lambda p: (int(p.storage), int(p.compute), int(p.accumulate), float(p.drop_tol),  # noqa: E731
                          int(p.product_levels))
@@ -930,22 +955,22 @@ class EigEngine:
         return (A.t.data_ptr(), A.rows, A.cols, A.lda, int(A.fmt), B.t.data_ptr(), B.rows, B.cols, B.lda, int(B.fmt),
                 self.n, self.cfg.k, self.cfg.iter, pol(self.pol), pol(self.mv), check, top, self.device.index,
                 bool(_lib.load().ofrr_prof_gemm_active()), self._refresh_now and self._res_oz is not None,
-                self.cfg.reuse_av, first or not self.cfg.reuse_av,
+                self.cfg.reuse_av, first or not self.cfg.reuse_av, bool(lead) and self._proj_levels_for(lead) != 6,
                 # what else shapes the captured body: basis builder, projection, row partition
                 str(self.cfg.basis_method.value), str(self.cfg.projection), bool(self.comm.distributed),
                 int(getattr(self, "r0", 0)), int(getattr(self, "r1", 0)), id(self.ops),
                 # Ozaki workspaces the captured kernels read (made outside the capture)
                 tuple(sorted(oz.ws.data_ptr() for oz in self._oz.values())))
 
-    def _graph_step(self, X, check: bool, top: int, first: bool = True):
+    def _graph_step(self, X, check: bool, top: int, first: bool = True, lead: bool = False):
         """Replay the captured iteration (capturing it first once the shapes have run
         eagerly in this process); None -> run it eagerly."""
-        key = self._graph_key(check, top, first)
+        key = self._graph_key(check, top, first, lead)
         g = _GRAPHS.get(key)
         if g is None:
             if key not in _WARM or key in _NO_GRAPH:
                 return None
-            g = self._capture(X, check, top, key, first)
+            g = self._capture(X, check, top, key, first, lead)
             if g is None:
                 return None
         else:
@@ -960,7 +985,7 @@ class EigEngine:
         out["graph"] = g
         return out
 
-    def _capture(self, X, check: bool, top: int, key, first: bool = True):
+    def _capture(self, X, check: bool, top: int, key, first: bool = True, lead: bool = False):
         import torch
         from . import _lib
         L = _lib.load()
@@ -973,7 +998,7 @@ class EigEngine:
         try:
             with rec:
                 with torch.cuda.graph(graph):
-                    outs = self._body(Xs, check, top, first)
+                    outs = self._body(Xs, check, top, first, lead)
                     nxt = outs["Xnext"] if self.cfg.reuse_av else outs["Xn"]
                     if first and self.cfg.reuse_av:
                         pass                                       # input: the start block

@@ -345,7 +345,7 @@ def ozaki_gemm(oz: OzakiOperator, X: DevBlock, W: DevBlock, colmax=None, flags=N
                                         _p(colmax), _p(flags), W2.ptr if W2 is not None else None,
                                         W2.ld if W2 is not None else 0, int(W2.fmt) if W2 is not None else int(W.fmt),
                                         int(levels), ws.data_ptr(), ws.numel(), _stream()), "ozaki_gemm")
-    bn = 64 if levels == 6 else 128
+    bn = 64 if levels >= 5 else 128
     _count(2 + (X.k + bn - 1) // bn * 4)   # digits of X, X row-major; per column pass: 2 product variants, tails, fixup
 
 
