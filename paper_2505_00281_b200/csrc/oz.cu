@@ -1907,8 +1907,8 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
               int64_t ldv, int r, const double* vals, const int* r_dev, const double* Y, int64_t ldy, void* W,
               int64_t ldw, int out_fmt, double* colmax, int* flags, void* W2, int64_t ldw2, int out_fmt2,
               double** part_out, void* ws, size_t ws_bytes, cudaStream_t st, int levels) {
-  if (levels != OZ_D && levels != 5 && levels != 4) {
-    ofrr_set_error("ozaki: levels must be 6, 5 or 4 (got %d)", levels);
+  if (levels < 3 || levels > OZ_D) {
+    ofrr_set_error("ozaki: levels must be 3..6 (got %d)", levels);
     return OFRR_ERR_INVALID;
   }
   if (oz_use_planes())
@@ -1956,6 +1956,9 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     else if (levels == 5)                                                                        \
       rc = p.bn == 32 ? ozk_launch<F, 32, 5>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)     \
                       : ozk_launch<F, 64, 5>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);    \
+    else if (levels == 3)                                                                        \
+      rc = p.bn == 64 ? ozk_launch<F, 64, 3>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)     \
+                      : ozk_launch<F, 128, 3>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);   \
     else                                                                                         \
       rc = p.bn == 64 ? ozk_launch<F, 64, 4>(A, rows, cols, lda, T, tV, p, pws, j0, full, st)     \
                       : ozk_launch<F, 128, 4>(A, rows, cols, lda, T, tV, p, pws, j0, full, st);

@@ -141,6 +141,9 @@ DEVICE_LOOP = True      # the whole solve as one graph launch (csrc/loop.cu) onc
 # are FP64-accurate: that iteration never produces the FP64 report (a convergence there goes to
 # the host loop, which then takes the report from a separate FP64 product)
 LEAD_LEVELS = int(__import__("os").environ.get("OFRR_LEAD_LEVELS", "5"))
+# a lite fp64 rung (4 levels, ~2^-30) entered from an fp32 rung's Ritz block (not stepped):
+# that block is only fp32-accurate, so its first power step takes 3 levels (6 products, ~2^-22)
+FIRST_POWER_LEVELS = int(__import__("os").environ.get("OFRR_FIRST_POWER_LEVELS", "3"))
 HANDOVER_STEPPED = __import__("os").environ.get("OFRR_HANDOVER_STEPPED") == "1"   # ladder: start every rung from the previous rung's W Y (experiments; see _subspace_iter_eig)
 _WARM = set()
 _NO_GRAPH = set()
@@ -292,11 +295,12 @@ class EigEngine:
             return self.ops.start_block(self.cfg.seed, self.n, self.cfg.k, self.mv.storage, self.device)
         return self.ops.start_block(self.cfg.seed, self.n, self.cfg.k, self.mv.storage, self.device, out=out)
 
-    def power(self, X, st, steps: Optional[int] = None):
+    def power(self, X, st, steps: Optional[int] = None, levels: Optional[int] = None):
         """cfg.iter MatVecs with inf-norm column scaling (ofrr/driver.py:102-105)."""
         import torch
         ops, comm = self.ops, self.comm
         k = X.k
+        levels = self.mv.product_levels if levels is None else levels
         fp8 = self.mv.storage == FpFormat.FP8_E4M3
         for _ in range(self.cfg.iter if steps is None else steps):
             colmax = torch.zeros(k, dtype=torch.float64, device=self.device)
@@ -304,7 +308,7 @@ class EigEngine:
             # is rounded once into e4m3 (per-column scaling; see _to_fp8)
             W = ops.new_block(self.A_mv.rows, k, FpFormat.F32 if fp8 else self.mv.storage, self.device)
             ops.gemm_av(self.A_mv, X, W, colmax=colmax, flags=st[S_MV_FLAGS:S_MV_FLAGS + 1],
-                        **({"oz": self._block_oz(self.A_mv, X), "levels": self.mv.product_levels}
+                        **({"oz": self._block_oz(self.A_mv, X), "levels": levels}
                            if self.ops is _ops else {}))
             self.stats.a_passes += 1
             comm.all_reduce_max_(colmax)
@@ -512,6 +516,7 @@ class EigEngine:
         in ``self.handover`` and the next rung starts with ``stepped=True``: its first
         iteration skips the power step (one FP64-accurate A pass fewer per ladder solve)."""
         self.stepped = bool(stepped)
+        self._entered_from_block = X0 is not None and not self.stepped   # (FIRST_POWER_LEVELS)
         cfg = self.cfg
         tol, top = cfg.tol, (cfg.top or cfg.k)
         check = tol is not None
@@ -907,7 +912,12 @@ class EigEngine:
         import torch
         st = torch.zeros(8, dtype=torch.int32, device=self.device)
         reuse = self.cfg.reuse_av
-        Xp = self.power(X, st) if (first or not reuse) else X
+        lv = None
+        if (first and self.mv.storage == FpFormat.F64 and self.mv.product_levels == 4 and X.fmt == FpFormat.F64
+                and FIRST_POWER_LEVELS in (3, 4) and self.ops is _ops and X.k == self.cfg.k
+                and getattr(self, "_entered_from_block", False)):
+            lv = FIRST_POWER_LEVELS
+        Xp = self.power(X, st, levels=lv) if (first or not reuse) else X
         h = self.basis(Xp, st)
         U = h.Q.narrow(Xp.k)
         Xnext = None
@@ -956,6 +966,7 @@ class EigEngine:
                 self.n, self.cfg.k, self.cfg.iter, pol(self.pol), pol(self.mv), check, top, self.device.index,
                 bool(_lib.load().ofrr_prof_gemm_active()), self._refresh_now and self._res_oz is not None,
                 self.cfg.reuse_av, first or not self.cfg.reuse_av, bool(lead) and self._proj_levels_for(lead) != 6,
+                bool(first and getattr(self, "_entered_from_block", False)),
                 # what else shapes the captured body: basis builder, projection, row partition
                 str(self.cfg.basis_method.value), str(self.cfg.projection), bool(self.comm.distributed),
                 int(getattr(self, "r0", 0)), int(getattr(self, "r1", 0)), id(self.ops),
