@@ -144,6 +144,9 @@ LEAD_LEVELS = int(__import__("os").environ.get("OFRR_LEAD_LEVELS", "5"))
 # a lite fp64 rung (4 levels, ~2^-30) entered from an fp32 rung's Ritz block (not stepped):
 # that block is only fp32-accurate, so its first power step takes 3 levels (6 products, ~2^-22)
 FIRST_POWER_LEVELS = int(__import__("os").environ.get("OFRR_FIRST_POWER_LEVELS", "3"))
+# ... and so does that iteration's projection product (its W feeds a Rayleigh-Ritz step whose
+# subspace carries the ~2^-22 power step anyway, and the next power step W Y): 3 levels
+FIRST_PROJ_LEVELS = int(__import__("os").environ.get("OFRR_FIRST_PROJ_LEVELS", "3"))
 HANDOVER_STEPPED = __import__("os").environ.get("OFRR_HANDOVER_STEPPED") == "1"   # ladder: start every rung from the previous rung's W Y (experiments; see _subspace_iter_eig)
 _WARM = set()
 _NO_GRAPH = set()
@@ -377,6 +380,8 @@ class EigEngine:
     def _proj_levels(self) -> int:
         """Ozaki levels of this iteration's projection product (see LEAD_LEVELS)."""
         lv = self.pol.product_levels
+        if getattr(self, "_entry_iter", False) and lv == 4 and self.pol.storage == FpFormat.F64:
+            return FIRST_PROJ_LEVELS if FIRST_PROJ_LEVELS in (3, 4) else lv
         return LEAD_LEVELS if (getattr(self, "_lead", False) and lv == 6 and LEAD_LEVELS in (5, 6)) else lv
 
     def project(self, U, st, want64: bool, top_check: Optional[int] = None, reuse: bool = False):
@@ -918,6 +923,7 @@ class EigEngine:
                 and getattr(self, "_entered_from_block", False)):
             lv = FIRST_POWER_LEVELS
         Xp = self.power(X, st, levels=lv) if (first or not reuse) else X
+        self._entry_iter = lv is not None
         h = self.basis(Xp, st)
         U = h.Q.narrow(Xp.k)
         Xnext = None
@@ -930,6 +936,7 @@ class EigEngine:
                 eig, _, Xn, est = self.project(U, st, want64=False, top_check=(top if check else None))
         finally:
             self._lead = False
+            self._entry_iter = False
         out = dict(st=st, h=h, U=U, eig=eig, Xn=Xn, est=est, pack=None, Xnext=Xnext, W2=self._last_w2,
                    w2_levels=self._last_w2_levels)
         if self.comm.distributed:
