@@ -635,7 +635,8 @@ int tc_gemm_av(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt
 // A (bf16) times each slice is an exact-product, fp32-accumulated tensor-core product.
 // ---------------------------------------------------------------------------------
 // slices = 2 ("lite": x_hi + x_mid, a 16-bit significand, N = 2k) keeps the product at the
-// HBM roofline for k <= 125 (N <= 251 flop/B at bf16) where 3 slices are tensor-bound.
+// HBM roofline for k <= 125 (N <= 251 flop/B at bf16) where 3 slices are tensor-bound; slices
+// = 1 (x_hi only) for a product whose block needs no more (the random start block).
 __global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n, int k,
                              __nv_bfloat16* __restrict__ Xs, int64_t lds, int slices) {
   const int j = blockIdx.y;
@@ -646,7 +647,7 @@ __global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n
     const __nv_bfloat16 m = __float2bfloat16_rn(r1);
     const float r2 = r1 - __bfloat162float(m);
     Xs[(int64_t)j * lds + i] = h;
-    Xs[(int64_t)(k + j) * lds + i] = m;
+    if (slices >= 2) Xs[(int64_t)(k + j) * lds + i] = m;
     if (slices == 3) Xs[(int64_t)(2 * k + j) * lds + i] = __float2bfloat16_rn(r2);
   }
 }
@@ -654,11 +655,11 @@ __global__ void k_split_bf16(const float* __restrict__ X, int64_t ldx, int64_t n
 // columns per pass: 3 * 170 = 510 <= 512 (one pass over A up to k = 170; the wide tile
 // for 85 < k, the two-M-half tile up to 85); 2 slices: 2 * 256
 static constexpr int SPLIT_KC = 170;
-static int split_kc(int slices) { return slices == 2 ? 256 : SPLIT_KC; }
+static int split_kc(int slices) { return slices == 1 ? 384 : slices == 2 ? 256 : SPLIT_KC; }
 
 size_t split_workspace(int64_t rows, int64_t cols, int k) {
   size_t best = 0;
-  for (int slices = 2; slices <= 3; ++slices) {
+  for (int slices = 1; slices <= 3; ++slices) {
     const int kc = std::min(k, split_kc(slices));
     const int64_t lds = (cols + 63) / 64 * 64;
     best = std::max(best, (size_t)slices * kc * lds * 2 + 1024 + tc_workspace(rows, cols, slices * kc, BF16));
@@ -671,7 +672,7 @@ size_t split_workspace(int64_t rows, int64_t cols, int k) {
 int tc_gemm_av_split(const void* A, int64_t rows, int64_t cols, int64_t lda, const float* X, int64_t ldx, int k,
                      void* W, int64_t ldw, int out_fmt, double* colmax, int* flags, void* ws, size_t ws_bytes,
                      cudaStream_t st, void* W2, int64_t ldw2, int out_fmt2, int slices) {
-  if (slices != 2 && slices != 3) { ofrr_set_error("gemm_av split: slices must be 2 or 3"); return OFRR_ERR_INVALID; }
+  if (slices < 1 || slices > 3) { ofrr_set_error("gemm_av split: slices must be 1, 2 or 3"); return OFRR_ERR_INVALID; }
   if (ws_bytes < split_workspace(rows, cols, k)) { ofrr_set_error("gemm_av split: workspace too small"); return OFRR_ERR_INVALID; }
   const int64_t lds = (cols + 63) / 64 * 64;
   const int KC = split_kc(slices);

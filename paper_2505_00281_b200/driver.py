@@ -147,6 +147,9 @@ FIRST_POWER_LEVELS = int(__import__("os").environ.get("OFRR_FIRST_POWER_LEVELS",
 # ... and so does that iteration's projection product (its W feeds a Rayleigh-Ritz step whose
 # subspace carries the ~2^-22 power step anyway, and the next power step W Y): 3 levels
 FIRST_PROJ_LEVELS = int(__import__("os").environ.get("OFRR_FIRST_PROJ_LEVELS", "3"))
+# a fresh solve's first power step multiplies the random start block: one bf16 slice of it is
+# as good a start as three (the fp32 rung's later products keep their slices)
+START_SLICES_LEVELS = int(__import__("os").environ.get("OFRR_START_LEVELS", "2"))
 HANDOVER_STEPPED = __import__("os").environ.get("OFRR_HANDOVER_STEPPED") == "1"   # ladder: start every rung from the previous rung's W Y (experiments; see _subspace_iter_eig)
 _WARM = set()
 _NO_GRAPH = set()
@@ -922,8 +925,13 @@ class EigEngine:
                 and FIRST_POWER_LEVELS in (3, 4) and self.ops is _ops and X.k == self.cfg.k
                 and getattr(self, "_entered_from_block", False)):
             lv = FIRST_POWER_LEVELS
+        elif (first and self.mv.storage == FpFormat.F32 and self.mv.product_levels == 4   # the lite fp32 rung
+              and self.A_mv.fmt == FpFormat.BF16 and self.ops is _ops
+              and not self.stepped and not getattr(self, "_entered_from_block", False)
+              and START_SLICES_LEVELS in (2, 4, 6)):
+            lv = START_SLICES_LEVELS
         Xp = self.power(X, st, levels=lv) if (first or not reuse) else X
-        self._entry_iter = lv is not None
+        self._entry_iter = lv is not None and self.mv.storage == FpFormat.F64
         h = self.basis(Xp, st)
         U = h.Q.narrow(Xp.k)
         Xnext = None

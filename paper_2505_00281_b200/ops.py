@@ -381,7 +381,7 @@ def gemm_av(A: DevOperator, X: DevBlock, W: DevBlock, out_fmt: Optional[FpFormat
     ws = _ws(ws_b, A.device)
     of = int(W.fmt if out_fmt is None else out_fmt)
     split = A.fmt == FpFormat.BF16 and X.fmt == FpFormat.F32 and not transpose
-    slices = 2 if levels == 4 else 3
+    slices = {2: 1, 4: 2}.get(int(levels), 3)     # fp32 blocks: "levels" 2 / 4 / 6 = 1 / 2 / 3 bf16 slices
     if split:
         # fp32 block on the bf16 tensor cores (3 bf16 slices -- 2 for the lite policy -- one
         # pass over A)
