@@ -150,6 +150,8 @@ FIRST_PROJ_LEVELS = int(__import__("os").environ.get("OFRR_FIRST_PROJ_LEVELS", "
 # a fresh solve's first power step multiplies the random start block: one bf16 slice of it is
 # as good a start as three (the fp32 rung's later products keep their slices)
 START_SLICES_LEVELS = int(__import__("os").environ.get("OFRR_START_LEVELS", "2"))
+# ... and that first iteration's projection (residuals there are ~1e-1: a 2^-8 product is plenty)
+START_PROJ_LEVELS = int(__import__("os").environ.get("OFRR_START_PROJ_LEVELS", "2"))
 HANDOVER_STEPPED = __import__("os").environ.get("OFRR_HANDOVER_STEPPED") == "1"   # ladder: start every rung from the previous rung's W Y (experiments; see _subspace_iter_eig)
 _WARM = set()
 _NO_GRAPH = set()
@@ -385,6 +387,8 @@ class EigEngine:
         lv = self.pol.product_levels
         if getattr(self, "_entry_iter", False) and lv == 4 and self.pol.storage == FpFormat.F64:
             return FIRST_PROJ_LEVELS if FIRST_PROJ_LEVELS in (3, 4) else lv
+        if getattr(self, "_entry_iter", False) and lv == 4 and self.pol.storage == FpFormat.F32:
+            return START_PROJ_LEVELS if START_PROJ_LEVELS in (2, 4) else lv
         return LEAD_LEVELS if (getattr(self, "_lead", False) and lv == 6 and LEAD_LEVELS in (5, 6)) else lv
 
     def project(self, U, st, want64: bool, top_check: Optional[int] = None, reuse: bool = False):
@@ -931,7 +935,7 @@ class EigEngine:
               and START_SLICES_LEVELS in (2, 4, 6)):
             lv = START_SLICES_LEVELS
         Xp = self.power(X, st, levels=lv) if (first or not reuse) else X
-        self._entry_iter = lv is not None and self.mv.storage == FpFormat.F64
+        self._entry_iter = lv is not None
         h = self.basis(Xp, st)
         U = h.Q.narrow(Xp.k)
         Xnext = None
