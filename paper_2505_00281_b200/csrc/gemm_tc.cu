@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // output format, write W (column-major) and the per-column inf-norm.
 __device__ __forceinline__ long long seg_begin(long long c, long long T, long long G) { return c * T / G; }
 
-static constexpr int FIN_COLS = 8;   // columns per finalize block
+static constexpr int FIN_COLS = 16;   // columns per finalize block
 
 __global__ void __launch_bounds__(256)
     k_finalize(const float* __restrict__ ws, int BN, int kblocks, long long total_iters, int G,
