@@ -794,6 +794,9 @@ static constexpr int OZK_THREADS = 192 + 32 * OZK_CONV_WARPS;
 // k-blocks per chunk (8192 terms): with u8 A digits (<= 255) x s8 V digits a level sums up
 // to 6 products of |d| <= 255 * 128 per term -- 6 * 32640 * 8192 < 2^31
 static constexpr int OZK_MAXCHUNK = 128;
+// the 3-plane (heads) variants sum at most 3 digit products per level: 3 * 128^2 * 32768 < 2^31,
+// so their chunks are twice as long (half the fp64 partial tiles for k_oz_resid)
+static constexpr int OZK_MAXCHUNK_H = 256;
 
 // NL = accumulation levels kept (digit products with p + q < NL): 6 -> ~2^-46 of |A||x| per
 // term (FP64-accurate); 4 -> ~2^-30 (the "lite" products of the full-f64-lite rung), which
@@ -1464,8 +1467,16 @@ __global__ void __launch_bounds__(OZ_TM)
                const double* __restrict__ vals, const int* __restrict__ r_dev, const double* __restrict__ Y,
                int64_t ldy, double* __restrict__ part, int ldp, void* __restrict__ W, int64_t ldw, int out_fmt,
                double* __restrict__ colmax, int* __restrict__ flags, void* __restrict__ W2, int64_t ldw2,
-               int out_fmt2, int stamp, const int* __restrict__ full, const double* __restrict__ Wt) {
+               int out_fmt2, int stamp, const int* __restrict__ full, const double* __restrict__ Wt,
+               int kbc_h, int nchunks_h, long long total_h, int slots_h) {
   __shared__ double red[4][OZR_CG];
+  // the heads variant ran (full == 0): its own, longer chunks
+  if (full && !*full) {
+    kbc = kbc_h;
+    nchunks = nchunks_h;
+    total_units = total_h;
+    max_slots = slots_h;
+  }
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // the product kernel is done
     const unsigned long long t0 = g_oz_stamp[0], t1 = g_oz_stamp[1];
     if (t1 > t0) {
@@ -1719,7 +1730,8 @@ int oz_apply(const void* op_ws, int64_t rows, int64_t cols, const double* V, int
     if (rc) return rc;
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + OZR_CG - 1) / OZR_CG)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
-                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0, nullptr, nullptr);
+                                           ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2, g_oz_stamp_on ? 1 : 0, nullptr, nullptr,
+                                           p.kbc, p.nchunks, p.total, p.max_slots);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;
@@ -1740,8 +1752,9 @@ static bool oz_use_planes() {
 
 struct OzkPlan {
   int bn, npass, npad, m_tiles, kblocks, nchunks, kbc, grid, max_slots, ldvt;
+  int nchunks_h, kbc_h, slots_h;      // the heads variants' chunking (OZK_MAXCHUNK_H)
   int64_t rows_pad, cols_pad;
-  long long total;
+  long long total, total_h;
   size_t off_F, off_dig, off_ws, off_part, off_vt, off_wt, off_vmax, bytes;
 };
 
@@ -1768,16 +1781,21 @@ static OzkPlan ozk_plan(int64_t rows, int64_t cols, int r, int levels = OZ_D) {
   p.nchunks = (p.kblocks + OZK_MAXCHUNK - 1) / OZK_MAXCHUNK;
   p.kbc = (p.kblocks + p.nchunks - 1) / p.nchunks;
   p.total = (long long)p.m_tiles * p.nchunks * p.kbc;
+  p.nchunks_h = (p.kblocks + OZK_MAXCHUNK_H - 1) / OZK_MAXCHUNK_H;
+  p.kbc_h = (p.kblocks + p.nchunks_h - 1) / p.nchunks_h;
+  p.total_h = (long long)p.m_tiles * p.nchunks_h * p.kbc_h;
   int sms = ofrr_device_sm_count(-1);
   if (sms <= 0) sms = 148;
-  p.grid = (int)std::max<long long>(1, std::min<long long>(sms, p.total));
+  p.grid = (int)std::max<long long>(1, std::min<long long>(sms, std::min(p.total, p.total_h)));
   const long long per = (p.total + p.grid - 1) / p.grid;
   p.max_slots = (int)((per + p.kbc - 1) / p.kbc) + 1;
+  const long long per_h = (p.total_h + p.grid - 1) / p.grid;
+  p.slots_h = (int)((per_h + p.kbc_h - 1) / p.kbc_h) + 1;
   size_t b = 0;
   auto take = [&](size_t n) { size_t o = b; b += (n + 1023) & ~size_t(1023); return o; };
   p.off_F = take((size_t)p.npad * 4);
   p.off_dig = take((size_t)OZ_D * p.npad * p.cols_pad);
-  p.off_ws = take((size_t)p.grid * p.max_slots * OZ_TM * p.bn * sizeof(double));
+  p.off_ws = take((size_t)p.grid * std::max(p.max_slots, p.slots_h) * OZ_TM * p.bn * sizeof(double));
   p.off_part = take((size_t)p.m_tiles * r * sizeof(double));
   p.ldvt = p.npad;
   p.off_vt = take((size_t)cols * p.ldvt * sizeof(double));     // V row-major for the tails
@@ -1816,16 +1834,17 @@ static int ozk_launch(const void* A, int64_t rows, int64_t cols, int64_t lda, co
           ae = cudaFuncSetAttribute(k_ozk_ts<FMT, BN, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT::SMEM_BYTES);
         });
         OFRR_CUDA_TRY(ae);
-        k_ozk_ts<FMT, BN, NL><<<p.grid, OZK_TS_THREADS, CT::SMEM_BYTES, st>>>(tA, rows, T, tV, ws, p.kbc, p.nchunks,
-                                                                         p.total, p.max_slots, p.npad, col0, stamp,
+        k_ozk_ts<FMT, BN, NL><<<p.grid, OZK_TS_THREADS, CT::SMEM_BYTES, st>>>(tA, rows, T, tV, ws, p.kbc_h,
+                                                                         p.nchunks_h, p.total_h, p.slots_h, p.npad,
+                                                                         col0, stamp,
                                                                          full);
         OFRR_CHECK_LAUNCH();
         ts = true;
       }
     }
     if (!ts) {
-      k_ozk_gemm<FMT, BN, 3, NL><<<p.grid, OZK_THREADS, C3::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc,
-                                                                             p.nchunks, p.total, p.max_slots, p.npad,
+      k_ozk_gemm<FMT, BN, 3, NL><<<p.grid, OZK_THREADS, C3::SMEM_BYTES, st>>>(A, rows, cols, lda, T, tV, ws, p.kbc_h,
+                                                                             p.nchunks_h, p.total_h, p.slots_h, p.npad,
                                                                              col0, stamp, full);
       OFRR_CHECK_LAUNCH();
     }
@@ -1971,7 +1990,8 @@ int ozx_apply(const void* A, int64_t rows, int64_t cols, int64_t lda, int a_fmt,
     k_oz_resid<<<dim3(p.m_tiles, (unsigned)((std::min(p.bn, r - j0) + OZR_CG - 1) / OZR_CG)), OZ_TM, 0, st>>>(pws, p.bn, p.kbc, p.nchunks, p.total, p.grid, p.max_slots, rows,
                                            std::min(p.bn, r - j0), j0, T, F + j0, vals, r_dev, Y, ldy, part, r, W,
                                            ldw, out_fmt, colmax, flags, W2, ldw2, out_fmt2,
-                                           g_oz_stamp_on ? (levels == OZ_D ? 1 : levels == 5 ? 3 : 2) : 0, full, Wt);
+                                           g_oz_stamp_on ? (levels == OZ_D ? 1 : levels == 5 ? 3 : 2) : 0, full, Wt,
+                                           p.kbc_h, p.nchunks_h, p.total_h, p.slots_h);
     OFRR_CHECK_LAUNCH();
   }
   if (part_out) *part_out = part;
