@@ -854,7 +854,7 @@ static int launch_hess(const void* X, int64_t n, int k, int64_t ldx, int storage
   void* args[] = {(void*)&Xp, (void*)&n, (void*)&k, (void*)&ldx, (void*)&Xw, (void*)&ldw, (void*)&tol,
                   (void*)&Qp, (void*)&ldq, (void*)&pivots, (void*)&kept, (void*)&n_kept, (void*)&h,
                   (void*)&in_smem, (void*)&pb};
-  OFRR_CUDA_TRY(cudaMemsetAsync(kept, 0, sizeof(int) * k, st));
+  // kept[j] is written for every column by the kernel (kept or skipped): no clearing node
   OFRR_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_hessenberg<T, C>, dim3(G), dim3(HT), args, shmem, st));
   return OFRR_OK;
 }
