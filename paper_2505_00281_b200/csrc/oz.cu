@@ -576,7 +576,7 @@ static OzOpLayout oz_op_layout(int64_t rows) {
   return L;
 }
 
-static constexpr int OZ_RS_THREADS = 512;    // k_oz_rowscale: one CTA per row, one 32-entry group per thread step
+static constexpr int OZ_RS_THREADS = 128;    // k_oz_rowscale: one CTA per row, one 32-entry group per thread step
 
 // mantissa bits of the 16/8-bit formats: an entry with exponent e has no bit below 2^(e - MB)
 template <int FMT> __device__ __forceinline__ constexpr int oz_mant_bits() { return FMT == BF16 ? 7 : FMT == F16 ? 10 : 3; }
