@@ -683,6 +683,11 @@ __global__ void __launch_bounds__(NT, 1)
     make_reflector(0, 0, s2);
   }
   __syncthreads();
+#ifdef OFRR_PC_TRI_PROF
+  __shared__ unsigned long long s_prof[4];
+  if (threadIdx.x < 4) s_prof[threadIdx.x] = 0;
+  unsigned long long tp_b = clock64(), tp_a = 0;
+#endif
   for (int j = 0; j + 2 < k; ++j) {
     const int buf = j & 1, j1 = j + 1;
     const double tj = s_tau[buf];
@@ -709,6 +714,10 @@ __global__ void __launch_bounds__(NT, 1)
       if (lane == 0) red[buf][warp] = kp;
     }
     __syncthreads();                                                     // (A)
+#ifdef OFRR_PC_TRI_PROF
+    tp_a = clock64();
+    if (threadIdx.x == 0) s_prof[0] += tp_a - tp_b;
+#endif
     double s2 = 0.0;                                                     // column j+1's new norm
     if (!skip && own) {
       const double K = 0.5 * tj * (NW == 16 ? pc_sum16(red[buf]) : pc_sum8(red[buf]));
@@ -729,15 +738,28 @@ __global__ void __launch_bounds__(NT, 1)
       for (int t = 0; t < RPT; ++t)
         if (r0 + t > j1 + 1) s2 = fma(a[t], a[t], s2);
     }
+#ifdef OFRR_PC_TRI_PROF
+    const unsigned long long tp_m = clock64();
+#endif
     if (c == j1) {
       if (j1 + 2 < k) {
         make_reflector(j1, buf ^ 1, s2);
+#ifdef OFRR_PC_TRI_PROF
+        if (sub == 0) { s_prof[2] += tp_m - tp_a; s_prof[3] += clock64() - tp_m; }
+#endif
       } else if (sub == 0) {                                             // last two: no reflector
         s_tau[buf ^ 1] = 0.0;
       }
     }
     __syncthreads();                                                     // (B)
+#ifdef OFRR_PC_TRI_PROF
+    tp_b = clock64();
+    if (threadIdx.x == 0) s_prof[1] += tp_b - tp_a;
+#endif
   }
+#ifdef OFRR_PC_TRI_PROF
+  if (threadIdx.x < 4) g_pcprof[16 + threadIdx.x] = s_prof[threadIdx.x];
+#endif
   // d_{k-2}, e_{k-2}, d_{k-1} from the owners' registers
 #pragma unroll
   for (int t = 0; t < RPT; ++t) {
